@@ -1,0 +1,240 @@
+"""ctypes wrapper over the unmodified reference library (oracle/_ref/librgg_ref.so).
+
+ORACLE / TEST INFRASTRUCTURE ONLY.  See oracle/ref_shim.cpp for the C entry
+points and the reference file:line each one wraps.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "librgg_ref.so")
+
+_lib = None
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_up = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_lp = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_qp = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"reference oracle library missing: {LIB_PATH} (run `make -C oracle`)")
+        L = C.CDLL(LIB_PATH)
+        L.rr_last_error.restype = C.c_char_p
+        L.rr_world_from_scn.restype = C.c_void_p
+        L.rr_world_from_scn.argtypes = [C.c_char_p]
+        L.rr_world_from_roadmap.restype = C.c_void_p
+        L.rr_world_from_roadmap.argtypes = [_dp, _dp, C.c_int, _dp, C.c_int, _ip, C.c_double, C.c_int]
+        L.rr_world_add_obstacle.argtypes = [C.c_void_p, _dp, C.c_int]
+        L.rr_world_free.argtypes = [C.c_void_p]
+        L.rr_world_counts.argtypes = [C.c_void_p, _lp]
+        L.rr_world_moves.argtypes = [C.c_void_p, _ip, _dp]
+        L.rr_world_layout.argtypes = [C.c_void_p] + [C.c_void_p] * 11
+        L.rr_world_obbs.argtypes = [C.c_void_p, _dp]
+        L.rr_obstacle_operands.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.rr_engine_new.restype = C.c_void_p
+        L.rr_engine_new.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.rr_engine_free.argtypes = [C.c_void_p]
+        L.rr_engine_update.argtypes = [C.c_void_p, C.c_int32, _dp, C.c_int, _lp]
+        L.rr_engine_run.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.POINTER(C.c_double)]
+        L.rr_engine_states.argtypes = [C.c_void_p, _up]
+        L.rr_engine_bits.argtypes = [C.c_void_p, _qp]
+        L.rr_engine_groups.argtypes = [C.c_void_p]
+        L.rr_engine_mask.argtypes = [C.c_void_p, C.c_int, _ip, C.c_int, C.c_int32, _up]
+        L.rr_kat_sat.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip, _up]
+        L.rr_kat_seg.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, _dp, _ip, _up]
+        L.rr_kat_sat_pairs.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _dp, _dp, _up, _dp]
+        L.rr_sat_prep.argtypes = [C.c_int, _dp, _dp]
+        L.rr_tf_euler.argtypes = [C.c_double, C.c_double, C.c_double, _dp]
+        L.rr_tf_axis_angle.argtypes = [_dp, C.c_double, _dp]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().rr_last_error().decode()
+        if msg.startswith("invalid_argument"):
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+
+@dataclass
+class Layout:
+    """The serialized layout view (CSR over real segments), numpy arrays."""
+
+    n_nodes: int
+    n_edges: int
+    N: int
+    B: int
+    S: int
+    K: int
+    M: int
+    C: int
+    edge_sat: np.ndarray  # N*B x 21
+    e_plus: np.ndarray  # N*B x 24
+    comp_aabb: np.ndarray  # N x 6
+    row_off: np.ndarray  # N*B*S + 1
+    segs: np.ndarray  # T x 7
+    seg_pts: np.ndarray  # T x 6
+    spline_r: np.ndarray  # B*S
+    obst_he: np.ndarray  # M x 3
+    obst_sph_local: np.ndarray  # M x C x 3
+    obst_sph_r: np.ndarray  # M
+    obst_sph_n: np.ndarray  # M
+
+
+class World:
+    """Reference roadmap + components + canonical obstacles."""
+
+    def __init__(self, handle):
+        if not handle:
+            raise RuntimeError(lib().rr_last_error().decode())
+        self.h = handle
+
+    @classmethod
+    def from_scn(cls, text: str) -> "World":
+        return cls(lib().rr_world_from_scn(text.encode()))
+
+    @classmethod
+    def from_roadmap(cls, robot_he, env, nodes, edges, eps=0.25, max_segments=16) -> "World":
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        edges = np.ascontiguousarray(edges, dtype=np.int32)
+        h = lib().rr_world_from_roadmap(np.asarray(robot_he, np.float64), np.asarray(env, np.float64),
+                                        nodes.shape[0], nodes.reshape(-1), edges.shape[0], edges.reshape(-1),
+                                        float(eps), int(max_segments))
+        return cls(h)
+
+    def add_obstacle(self, he, spheres=0):
+        _check(lib().rr_world_add_obstacle(self.h, np.asarray(he, np.float64), int(spheres)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.rr_world_free(self.h)
+            self.h = None
+
+    def counts(self):
+        out = np.zeros(12, np.int64)
+        _check(lib().rr_world_counts(self.h, out))
+        keys = ["n_nodes", "n_edges", "N", "B", "S", "K", "M", "C", "segs", "n_moves", "iterations", "lazy"]
+        return dict(zip(keys, out.tolist()))
+
+    def moves(self):
+        n = self.counts()["n_moves"]
+        ids = np.zeros(n, np.int32)
+        rt = np.zeros((n, 12), np.float64)
+        _check(lib().rr_world_moves(self.h, ids, rt.reshape(-1)))
+        return ids, rt
+
+    def layout(self) -> Layout:
+        k = self.counts()
+        N, B, S, M, Cs, T = k["N"], k["B"], k["S"], k["M"], k["C"], k["segs"]
+        a = dict(
+            edge_sat=np.zeros((N * B, 21)), e_plus=np.zeros((N * B, 24)), comp_aabb=np.zeros((N, 6)),
+            row_off=np.zeros(N * B * S + 1, np.int32), segs=np.zeros((T, 7)), seg_pts=np.zeros((T, 6)),
+            spline_r=np.zeros(B * S), obst_he=np.zeros((M, 3)), obst_sph_local=np.zeros((M, Cs, 3)),
+            obst_sph_r=np.zeros(M), obst_sph_n=np.zeros(M, np.int32))
+        order = ["edge_sat", "e_plus", "comp_aabb", "row_off", "segs", "seg_pts", "spline_r", "obst_he",
+                 "obst_sph_local", "obst_sph_r", "obst_sph_n"]
+        _check(lib().rr_world_layout(self.h, *[a[n].ctypes.data_as(C.c_void_p) for n in order]))
+        return Layout(n_nodes=k["n_nodes"], n_edges=k["n_edges"], N=N, B=B, S=S, K=k["K"], M=M, C=Cs, **a)
+
+    def obbs(self):
+        k = self.counts()
+        out = np.zeros((k["N"] * k["B"], 15))
+        _check(lib().rr_world_obbs(self.h, out.reshape(-1)))
+        return out
+
+    def obstacle_operands(self, o: int, rt12):
+        k = self.counts()
+        sat, aabb, cen, saabb = np.zeros(21), np.zeros(6), np.zeros(k["C"] * 3), np.zeros(6)
+        _check(lib().rr_obstacle_operands(self.h, int(o), np.asarray(rt12, np.float64), sat, aabb, cen, saabb))
+        return sat, aabb, cen.reshape(-1, 3), saabb
+
+
+class Engine:
+    """Reference BatchEngine (kind=0) or SequentialEngine (kind=1), grouped for M > 64."""
+
+    def __init__(self, world: World, kind=0, threads=1, use_under=True, cell_capacity=1024, group_size=64):
+        self.world = world
+        self.h = lib().rr_engine_new(world.h, kind, threads, int(use_under), cell_capacity, group_size)
+        if not self.h:
+            raise RuntimeError(lib().rr_last_error().decode())
+        self.N = world.counts()["N"]
+        self.groups = lib().rr_engine_groups(self.h)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.rr_engine_free(self.h)
+            self.h = None
+
+    def update(self, o, rt12, lazy=True):
+        rep = np.zeros(11, np.int64)
+        _check(lib().rr_engine_update(self.h, int(o), np.ascontiguousarray(rt12, np.float64), int(lazy), rep))
+        return rep
+
+    def run(self, ids, rts, lazy=True) -> float:
+        ids = np.ascontiguousarray(ids, np.int32)
+        rts = np.ascontiguousarray(rts, np.float64).reshape(-1)
+        us = C.c_double(0)
+        _check(lib().rr_engine_run(self.h, len(ids), ids, rts, int(lazy), C.byref(us)))
+        return us.value
+
+    def states(self):
+        out = np.zeros(self.N, np.uint8)
+        _check(lib().rr_engine_states(self.h, out))
+        return out
+
+    def bits(self):
+        out = np.zeros(self.N * self.groups, np.uint64)
+        _check(lib().rr_engine_bits(self.h, out))
+        return out.reshape(self.N, self.groups)
+
+    def mask(self, kind, cands, o):
+        cands = np.ascontiguousarray(cands, np.int32)
+        out = np.zeros(len(cands), np.uint8)
+        _check(lib().rr_engine_mask(self.h, kind, cands, len(cands), int(o), out))
+        return out
+
+
+def kat_sat(seed=2025, n_boxes=5000, n_idx=10000):
+    boxes, obst, idx, out = np.zeros((n_boxes, 21)), np.zeros(21), np.zeros(n_idx, np.int32), np.zeros(n_idx, np.uint8)
+    _check(lib().rr_kat_sat(seed, n_boxes, n_idx, boxes.reshape(-1), obst, idx, out))
+    return boxes, obst, idx, out
+
+
+def kat_seg(seed=777, n_rand=4000, n_point=50, n_idx=9001):
+    segs, idx, out = np.zeros((n_rand + n_point, 7)), np.zeros(n_idx, np.int32), np.zeros(n_idx, np.uint8)
+    _check(lib().rr_kat_seg(seed, n_rand, n_point, n_idx, segs.reshape(-1), idx, out))
+    return segs, idx, out
+
+
+def kat_sat_pairs(seed, n, span=4.0, extent=2.0):
+    a, b, out, margin = np.zeros((n, 21)), np.zeros((n, 21)), np.zeros(n, np.uint8), np.zeros(n)
+    _check(lib().rr_kat_sat_pairs(seed, n, span, extent, a.reshape(-1), b.reshape(-1), out, margin))
+    return a, b, out, margin
+
+
+def tf_euler(rx, ry, rz):
+    out = np.zeros(12)
+    _check(lib().rr_tf_euler(rx, ry, rz, out))
+    return out
+
+
+def tf_axis_angle(axis, angle):
+    out = np.zeros(12)
+    _check(lib().rr_tf_axis_angle(np.asarray(axis, np.float64), angle, out))
+    return out
