@@ -1,0 +1,163 @@
+/* rgg_gpu.h — C-ABI of the B200-native SerRGG edge-classification engine.
+ *
+ * This is the drop-in boundary.  It replaces the hot path of
+ *   class rgg::BatchEngine          proj/include/rgg/engine_batch.hpp:17-63
+ *   rgg::BatchEngine::update_obstacle / batch_update
+ *                                   proj/src/engine_batch.cpp:145-215
+ * and, below it, the per-pair plugin seam
+ *   struct rgg::kern::Backend       proj/include/rgg/kernels.hpp:49-54
+ * which is too fine-grained for a GPU (one host call per obstacle sphere).
+ * Plain pointers and sizes only; no torch or C++ types cross it.  A handle is
+ * single-host-thread (updates are not reentrant, proj/include/rgg/engine_sequential.hpp:11-12).
+ *
+ * Errors: every entry returns RGG_OK or an RGG_E* code; rgg_gpu_last_error()
+ * gives the message.  The messages of RGG_EINVAL match the reference's
+ * std::invalid_argument texts ("unknown obstacle id", engine_batch.cpp:147;
+ * "obstacle bitsets support at most 64 obstacles", engine_batch.cpp:27) so the
+ * C++ wrapper (include/rgg/engine_gpu.hpp) can rethrow them verbatim.
+ */
+#ifndef RGG_GPU_H
+#define RGG_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RGG_OK 0
+#define RGG_EINVAL 1  /* bad argument (reference: std::invalid_argument) */
+#define RGG_ECUDA 2   /* CUDA runtime failure, or no sm_100 device */
+#define RGG_ENCCL 3   /* collective failure (multi-GPU plumbing) */
+#define RGG_ENOMEM 4  /* device allocation failed */
+#define RGG_ELOGIC 5  /* layout contract violated (reference: std::logic_error) */
+
+/* Validity labels, numerically equal to rgg::ValidityState (proj/include/rgg/roadmap.hpp:26-30). */
+#define RGG_GREEN 0
+#define RGG_RED 1
+#define RGG_GRAY 2
+
+/* rgg_gpu_update flags */
+#define RGG_LAZY 1      /* lazy update (the only mode the GPU resolves by itself) */
+#define RGG_PER_MOVE 2  /* fill one rgg_update_report per move (finish_counts semantics) */
+#define RGG_ASYNC 4     /* enqueue only; the call returns before the device finishes */
+
+/* The serialized store, borrowed for the duration of rgg_gpu_create.  It is the
+ * reference's BatchLayout (proj/include/rgg/batch_layout.hpp:23-66) with the padded
+ * segment block replaced by CSR over real segments:
+ *   edge_sat        N*B*21   kern::SatBox rows (center[3], e[3][3], u[3][3]) — layout.edge_sat
+ *   comp_aabb       N*6      component_aabb (min xyz, max xyz)
+ *   row_off         N*B*S+1  real segments of row (c, b, s) are [row_off[r], row_off[r+1]),
+ *                            r = (c*B + b)*S + s  (layout.seg_count as offsets)
+ *   segs            T*7      kern::SegPrep rows (a[3], d[3], dd) of the real segments
+ *   spline_radius   B*S      layout.spline_radius
+ *   obst_he         M*3      canonical obstacle half extents (ObstacleModel::half_extents)
+ *   obst_sph_local  M*C*3    inner sphere centres in the obstacle frame
+ *   obst_sph_r      M        layout.o_minus_r
+ *   obst_sph_n      M        layout.o_sphere_count
+ */
+typedef struct rgg_layout_view {
+    int32_t n_components; /* N */
+    int32_t n_bodies;     /* B */
+    int32_t n_slots;      /* S */
+    int32_t n_obstacles;  /* M */
+    int32_t max_spheres;  /* C */
+    const double* edge_sat;
+    const double* comp_aabb;
+    const int32_t* row_off;
+    const double* segs;
+    const double* spline_radius;
+    const double* obst_he;
+    const double* obst_sph_local;
+    const double* obst_sph_r;
+    const int32_t* obst_sph_n;
+} rgg_layout_view;
+
+typedef struct rgg_gpu_options {
+    int32_t device;        /* CUDA ordinal (one process per GPU) */
+    int32_t use_under;     /* EngineOptions::use_under (update_report.hpp:43-46) */
+    int32_t cell_size;     /* components per cell (0 -> 128; multiple of 32, <= 256) */
+    int32_t cell_capacity; /* inline event slots per cell before overflow (0 -> 64) */
+    int32_t allow_wide;    /* accept M > 64 (bitsets become ceil(M/64) words) */
+    int32_t shard_rank;    /* this handle owns cells c with c % shard_count == shard_rank */
+    int32_t shard_count;   /* 0 or 1: unsharded */
+} rgg_gpu_options;
+
+/* Mirrors rgg::UpdateReport (proj/include/rgg/update_report.hpp:11-25).  The
+ * *_us fields carry device-event microseconds of the batch split into the
+ * phases of this engine (pose -> reval_us, binning -> over_us, classify ->
+ * under_us, compaction -> resolve_us); they are filled on the last report of
+ * a batch only. */
+typedef struct rgg_update_report {
+    int32_t obstacle;
+    int32_t new_green;
+    int32_t new_red;
+    int32_t new_gray;
+    int64_t reval_us;
+    int64_t over_us;
+    int64_t under_us;
+    int64_t resolve_us;
+    int32_t unknown_after_heuristic;
+    int32_t residual_unknown;
+    int32_t resolve_checks;
+    int32_t _pad;
+} rgg_update_report;
+
+typedef struct rgg_gpu rgg_gpu;
+
+/* BatchEngine::BatchEngine (engine_batch.cpp:20-31): uploads the store into
+ * HBM (cell-sorted SoA), builds the cells, all labels GREEN, bits 0. */
+int rgg_gpu_create(const rgg_layout_view* view, const rgg_gpu_options* opts, rgg_gpu** out);
+void rgg_gpu_destroy(rgg_gpu* h);
+const char* rgg_gpu_last_error(const rgg_gpu* h);
+
+/* BatchEngine::batch_update (engine_batch.cpp:207-215) over n moves
+ * (ids[i], pose rt12[12*i .. 12*i+11] = row-major rotation then translation).
+ * Moves are applied in order; labels after the call equal the reference's after
+ * the same moves.  reports (n entries, PER_MOVE) or NULL.  On an unknown id at
+ * position k, moves [0, k) are applied and RGG_EINVAL is returned. */
+int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
+                   rgg_update_report* reports);
+/* Same, with ids/rt12 already in device memory (no host copies); always async.
+ * The host-side id validation is skipped: ids must be in [0, M). */
+int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12, int32_t n, int32_t flags);
+int rgg_gpu_sync(rgg_gpu* h);
+
+int rgg_gpu_count(const rgg_gpu* h, int32_t* n_components, int32_t* n_obstacles, int32_t* words_per_comp);
+/* states(): N labels in component-id order (sharded handles: unowned entries are 0xFF). */
+int rgg_gpu_read_states(rgg_gpu* h, uint8_t* out);
+/* obstacle_bits(): N * words, component-major; word w holds obstacles [64w, 64w+64). */
+int rgg_gpu_read_bits(rgg_gpu* h, uint64_t* out, int32_t words_per_comp);
+int rgg_gpu_unknown_count(rgg_gpu* h, int32_t* out);
+/* Ascending ids of every GRAY component (the gray list handed to the exact resolve). */
+int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
+/* Components over-hit by the last move of the last update that are still GRAY
+ * (the over_hits the reference resolves in eager mode, engine_batch.cpp:193-200). */
+int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
+/* Eager / resolve_all_unknown write-back: states[ids[i]] = st[i] (bits untouched). */
+int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int32_t n);
+/* batch_over (kind 0) / batch_under (kind 1) on explicit candidates against
+ * obstacle o at its current pose (engine_batch.hpp:34-37). */
+int rgg_gpu_pair_masks(rgg_gpu* h, int32_t kind, const int32_t* cand, int32_t n, int32_t o, uint8_t* mask);
+
+/* Measurement hooks (bench.py): device time of the last update's phases and the
+ * algorithmic census of the current poses. */
+typedef struct rgg_gpu_stats {
+    float pose_ms, bin_ms, classify_ms, compact_ms, total_ms;
+    int32_t dirty_cells, events, overflow_cells;
+    int64_t over_pairs, sat_flops, under_pairs, seg_sphere_tests, over_hits, under_hits;
+    int64_t bytes_components; /* algorithmic bytes of the dirty components */
+} rgg_gpu_stats;
+int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out);
+/* Full-roadmap census against all active obstacles (one untimed launch). */
+int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out);
+/* The CUDA stream the engine launches on (cudaStream_t), for event timing. */
+void* rgg_gpu_stream(rgg_gpu* h);
+/* Measured non-FMA fp64 add/mul rate of `device` in GFLOP/s (the compute roof
+ * of the fp64-exact classification). */
+int rgg_gpu_fp64_peak(int device, double* gflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -85,8 +85,9 @@ def synthetic(name, kind, n_nodes, k, half, m, iterations, seed, snap_every):
 
 
 def kats():
-    boxes, obst, idx, out = ref.kat_sat(2025, 5000, 10000)
-    np.savez_compressed(os.path.join(OUT, "kat_sat.npz"), boxes=boxes, obstacle=obst, idx=idx, out=out)
+    boxes, obst, idx, out, pose, he = ref.kat_sat(2025, 5000, 10000)
+    np.savez_compressed(os.path.join(OUT, "kat_sat.npz"), boxes=boxes, obstacle=obst, idx=idx, out=out,
+                        obstacle_pose=pose, obstacle_he=he)
     segs, idx, out = ref.kat_seg(777, 4000, 50, 9001)
     np.savez_compressed(os.path.join(OUT, "kat_seg.npz"), segs=segs, idx=idx, out=out,
                         center=np.array([0.3, -0.2, 0.1]), r_total=1.1)

@@ -54,7 +54,7 @@ def lib():
         L.rr_engine_bits.argtypes = [C.c_void_p, _qp]
         L.rr_engine_groups.argtypes = [C.c_void_p]
         L.rr_engine_mask.argtypes = [C.c_void_p, C.c_int, _ip, C.c_int, C.c_int32, _up]
-        L.rr_kat_sat.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip, _up]
+        L.rr_kat_sat.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _ip, _up, _dp, _dp]
         L.rr_kat_seg.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, _dp, _ip, _up]
         L.rr_kat_sat_pairs.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, _dp, _dp, _up, _dp]
         L.rr_sat_prep.argtypes = [C.c_int, _dp, _dp]
@@ -212,8 +212,9 @@ class Engine:
 
 def kat_sat(seed=2025, n_boxes=5000, n_idx=10000):
     boxes, obst, idx, out = np.zeros((n_boxes, 21)), np.zeros(21), np.zeros(n_idx, np.int32), np.zeros(n_idx, np.uint8)
-    _check(lib().rr_kat_sat(seed, n_boxes, n_idx, boxes.reshape(-1), obst, idx, out))
-    return boxes, obst, idx, out
+    pose, he = np.zeros(12), np.zeros(3)
+    _check(lib().rr_kat_sat(seed, n_boxes, n_idx, boxes.reshape(-1), obst, idx, out, pose, he))
+    return boxes, obst, idx, out, pose, he
 
 
 def kat_seg(seed=777, n_rand=4000, n_point=50, n_idx=9001):

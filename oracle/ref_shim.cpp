@@ -447,9 +447,12 @@ int rr_engine_mask(void* ep, int kind, const std::int32_t* cands, int n, std::in
 
 // proj/tests/test_kernels.cpp:50-71: 5000 near-contact boxes, one obstacle,
 // 10000 random indices, seed 2025.  Writes boxes (n_boxes*21), obstacle (21),
-// idx (n_idx), and the scalar backend's bytes (n_idx).
+// idx (n_idx), and the scalar backend's bytes (n_idx).  The obstacle's
+// random_obb (proj/tests/oracles.hpp:98-109) is expanded inline — same Rng draw
+// order — so its pose (rotation + centre, obstacle_pose12) and half extents
+// (obstacle_he3) can be handed to an engine as a box obstacle.
 int rr_kat_sat(std::uint64_t seed, int n_boxes, int n_idx, double* boxes21, double* obstacle21, std::int32_t* idx,
-               std::uint8_t* out) {
+               std::uint8_t* out, double* obstacle_pose12, double* obstacle_he3) {
     return guarded([&] {
         Rng rng(seed);
         std::vector<kern::SatBox> boxes;
@@ -458,11 +461,24 @@ int rr_kat_sat(std::uint64_t seed, int n_boxes, int n_idx, double* boxes21, doub
             return kern::sat_prep(&c[0].x);
         };
         for (int i = 0; i < n_boxes; ++i) boxes.push_back(sat_of(oracle::random_obb(rng, 1.5, 1.2)));
-        const kern::SatBox obstacle = sat_of(oracle::random_obb(rng, 0.5, 2.0));
+        const Transform rot = oracle::random_rotation(rng);
+        Obb ob;
+        ob.center = {rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5)};
+        ob.axes[0] = rot.rotate({1, 0, 0});
+        ob.axes[1] = rot.rotate({0, 1, 0});
+        ob.axes[2] = rot.rotate({0, 0, 1});
+        ob.half_extents = {rng.uniform(0.05, 2.0), rng.uniform(0.05, 2.0), rng.uniform(0.05, 2.0)};
+        const kern::SatBox obstacle = sat_of(ob);
         for (int i = 0; i < n_idx; ++i) idx[i] = rng.uniform_int(0, n_boxes - 1);
         kern::scalar_backend().sat_batch(boxes.data(), idx, n_idx, &obstacle, out);
         for (int i = 0; i < n_boxes; ++i) put_sat(boxes[i], boxes21 + 21 * i);
         put_sat(obstacle, obstacle21);
+        Transform pose = rot;
+        pose.t = ob.center;
+        put_tf(pose, obstacle_pose12);
+        obstacle_he3[0] = ob.half_extents.x;
+        obstacle_he3[1] = ob.half_extents.y;
+        obstacle_he3[2] = ob.half_extents.z;
     });
 }
 

@@ -1,0 +1,65 @@
+"""Build the native libraries in-tree (they travel to the GPU box with the repo).
+
+    python -m paper_2603_28674_b200.build
+
+* ``lib/librgg_gpu.so``   — the CUDA engine (csrc/rgg_kernels.cu + csrc/rgg_capi.cu),
+  nvcc for sm_100a only, -lineinfo for ncu source mapping, static cudart.
+* ``lib/librgg_build.so`` — the CPU roadmap producer (csrc/producer.cpp).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "lib")
+ROOT = os.path.dirname(PKG)
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+GPU_SOURCES = ["rgg_kernels.cu", "rgg_capi.cu"]
+GPU_DEPS = GPU_SOURCES + ["rgg_device.cuh", "rgg_kernels.cuh"]
+PRODUCER_SOURCES = ["producer.cpp"]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build_gpu(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "librgg_gpu.so")
+    deps = [os.path.join(CSRC, f) for f in GPU_DEPS] + [os.path.join(ROOT, "include", "rgg_gpu.h")]
+    if force or _stale(out, deps):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-Xptxas", "-v" if verbose else "-O3", "-o", out] + [os.path.join(CSRC, f) for f in GPU_SOURCES]
+        subprocess.check_call(cmd)
+    return out
+
+
+def build_producer(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "librgg_build.so")
+    srcs = [os.path.join(CSRC, f) for f in PRODUCER_SOURCES]
+    deps = srcs + [os.path.join(ROOT, "include", "rgg_build.h")]
+    if not all(os.path.exists(s) for s in srcs):
+        return ""
+    if force or _stale(out, deps):
+        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
+               "-I", os.path.join(ROOT, "include"), "-o", out] + srcs
+        subprocess.check_call(cmd)
+    return out
+
+
+def build_all(force: bool = False) -> None:
+    build_gpu(force)
+    build_producer(force)
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

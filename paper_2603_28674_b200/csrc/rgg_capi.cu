@@ -1,0 +1,778 @@
+// rgg_capi.cu — host side of the C-ABI in include/rgg_gpu.h.
+//
+// Owns the device-resident store (cell-sorted SoA in HBM, resident across
+// updates), the per-batch scratch, and the stream every kernel is launched on.
+// No CPU fallback: creation fails with RGG_ECUDA unless an sm_100 device is
+// present, and every compute entry launches the kernels of rgg_kernels.cu.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/rgg_gpu.h"
+#include "rgg_kernels.cuh"
+
+using rggk::Batch;
+using rggk::Event;
+using rggk::Store;
+
+struct rgg_gpu {
+    std::string err;
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    Store s{};
+    // device allocations
+    double2* d_aabb = nullptr;
+    double* d_sat = nullptr;
+    int32_t* d_row = nullptr;
+    double* d_seg = nullptr;
+    double* d_spline = nullptr;
+    int32_t* d_orig = nullptr;
+    int32_t* d_rank = nullptr;
+    double* d_cell_aabb = nullptr;
+    double* d_ohe = nullptr;
+    double* d_osl = nullptr;
+    double* d_osr = nullptr;
+    int32_t* d_osn = nullptr;
+    uint8_t* d_state = nullptr;
+    uint32_t* d_cnt = nullptr;
+    unsigned long long* d_over = nullptr;
+    unsigned long long* d_under = nullptr;
+    Event* d_cur = nullptr;
+    double* d_cur_union = nullptr;
+    int32_t* d_ctr = nullptr;
+    unsigned long long* d_census = nullptr;
+    int32_t* d_gray = nullptr;
+    int32_t* d_tiles = nullptr;
+    int32_t* d_hits = nullptr;
+    int32_t* d_cell_count = nullptr;
+    int32_t* d_cell_list = nullptr;
+    int32_t* d_cell_ovf = nullptr;
+    int32_t* d_dirty = nullptr;
+    // batch buffers (grown on demand)
+    int32_t cap_moves = 0;
+    int32_t* d_ids = nullptr;
+    double* d_rt = nullptr;
+    int32_t* d_prev = nullptr;
+    uint8_t* d_last = nullptr;
+    Event* d_ev = nullptr;
+    int32_t* d_mv = nullptr;
+    int32_t* d_pool = nullptr;
+    int64_t pool_cap = 0;
+    // pinned staging
+    int32_t cap_pin = 0;
+    int32_t* h_ids = nullptr;
+    double* h_rt = nullptr;
+    int32_t* h_prev = nullptr;
+    uint8_t* h_last = nullptr;
+    int32_t* h_mv = nullptr;
+    int32_t* h_ctr = nullptr;
+    // host mirrors
+    std::vector<int32_t> orig;  // sorted -> id (owned)
+    int32_t words = 1;
+    int32_t last_n = 0;
+    int32_t last_flags = 0;
+    bool last_hits_valid = false;
+    int32_t unknown = 0;
+    bool unknown_stale = false;
+    cudaEvent_t ev[6] = {};
+    bool timed = false;
+    int grid_classify = 1;
+    int64_t total_segs_owned = 0;
+};
+
+namespace {
+
+int fail(rgg_gpu* h, int code, const std::string& msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ != cudaSuccess) return fail(h, RGG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+cudaError_t dalloc(T** p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, n) * sizeof(T));
+}
+
+uint64_t spread3(uint64_t x) {
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+int grow_batch(rgg_gpu* h, int32_t n) {
+    if (n <= h->cap_moves && static_cast<int64_t>(h->s.ncells) * n <= h->pool_cap) return RGG_OK;
+    const int32_t cap = std::max(n, std::max(64, h->cap_moves * 2));
+    cudaFree(h->d_ids);
+    cudaFree(h->d_rt);
+    cudaFree(h->d_prev);
+    cudaFree(h->d_last);
+    cudaFree(h->d_ev);
+    cudaFree(h->d_mv);
+    cudaFree(h->d_pool);
+    CK(dalloc(&h->d_ids, cap));
+    CK(dalloc(&h->d_rt, static_cast<size_t>(cap) * 12));
+    CK(dalloc(&h->d_prev, cap));
+    CK(dalloc(&h->d_last, cap));
+    CK(dalloc(&h->d_ev, cap));
+    CK(dalloc(&h->d_mv, static_cast<size_t>(cap) * 4));
+    // every (cell, event) pair fits: the overflow pool can never run out
+    h->pool_cap = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * cap);
+    CK(dalloc(&h->d_pool, static_cast<size_t>(h->pool_cap)));
+    h->cap_moves = cap;
+    return RGG_OK;
+}
+
+int grow_pinned(rgg_gpu* h, int32_t n) {
+    if (n <= h->cap_pin) return RGG_OK;
+    const int32_t cap = std::max(n, std::max(64, h->cap_pin * 2));
+    cudaFreeHost(h->h_ids);
+    cudaFreeHost(h->h_rt);
+    cudaFreeHost(h->h_prev);
+    cudaFreeHost(h->h_last);
+    cudaFreeHost(h->h_mv);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), cap * sizeof(int32_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_rt), cap * 12 * sizeof(double), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_prev), cap * sizeof(int32_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_last), cap * sizeof(uint8_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), 0));
+    h->cap_pin = cap;
+    return RGG_OK;
+}
+
+Batch batch_of(rgg_gpu* h, int32_t n) {
+    Batch b{};
+    b.n = n;
+    b.ids = h->d_ids;
+    b.rt = h->d_rt;
+    b.prev = h->d_prev;
+    b.last = h->d_last;
+    b.ev = h->d_ev;
+    b.cell_count = h->d_cell_count;
+    b.cell_list = h->d_cell_list;
+    b.cell_ovf = h->d_cell_ovf;
+    b.pool = h->d_pool;
+    b.pool_cap = static_cast<int32_t>(std::min<int64_t>(h->pool_cap, INT32_MAX));
+    b.ctr = h->d_ctr;
+    b.dirty = h->d_dirty;
+    b.mv = h->d_mv;
+    b.hits = h->d_hits;
+    b.census = h->d_census;
+    return b;
+}
+
+// Enqueue the whole pipeline for n moves already in d_ids/d_rt/d_prev/d_last.
+int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
+    const Batch b = batch_of(h, n);
+    int kf = 0;
+    if (flags & RGG_PER_MOVE) kf |= rggk::kPerMove;
+    if (n == 1) kf |= rggk::kHits;
+    CK(cudaEventRecord(h->ev[0], h->stream));
+    CK(rggk::launch_pose(h->s, b, h->stream));
+    CK(cudaEventRecord(h->ev[1], h->stream));
+    CK(rggk::launch_bin(h->s, b, h->stream));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
+    CK(cudaEventRecord(h->ev[3], h->stream));
+    CK(rggk::launch_commit(h->s, b, h->stream));
+    CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+    CK(cudaEventRecord(h->ev[4], h->stream));
+    h->last_n = n;
+    h->last_flags = flags;
+    h->last_hits_valid = n == 1;
+    h->timed = true;
+    h->unknown_stale = true;
+    return RGG_OK;
+}
+
+// host-side move preparation: prev / last indices per obstacle
+void link_moves(const int32_t* ids, int32_t n, int32_t m, int32_t* prev, uint8_t* last) {
+    std::vector<int32_t> seen(static_cast<size_t>(m), -1);
+    for (int32_t i = 0; i < n; ++i) {
+        prev[i] = seen[ids[i]];
+        seen[ids[i]] = i;
+        last[i] = 0;
+    }
+    for (int32_t o = 0; o < m; ++o)
+        if (seen[o] >= 0) last[seen[o]] = 1;
+}
+
+int refresh_unknown(rgg_gpu* h) {
+    if (!h->unknown_stale) return RGG_OK;
+    int32_t v = 0;
+    CK(cudaMemcpyAsync(&v, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->unknown = v;
+    h->unknown_stale = false;
+    return RGG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rgg_gpu_last_error(const rgg_gpu* h) { return h ? h->err.c_str() : "null handle"; }
+
+int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gpu** out) {
+    if (!out) return RGG_EINVAL;
+    *out = nullptr;
+    rgg_gpu* h = new rgg_gpu();
+    *out = h;
+    if (!v) return fail(h, RGG_EINVAL, "null layout view");
+    rgg_gpu_options o{};
+    if (opts) o = *opts;
+    const int32_t N = v->n_components, B = v->n_bodies, S = v->n_slots, M = v->n_obstacles, C = v->max_spheres;
+    if (N < 0 || B < 1 || S < 1 || M < 0 || C < 0) return fail(h, RGG_EINVAL, "malformed layout view");
+    if (M > 64 && !o.allow_wide) return fail(h, RGG_EINVAL, "obstacle bitsets support at most 64 obstacles");
+    if (C > rggk::kMaxSpheres) return fail(h, RGG_EINVAL, "too many spheres per obstacle (max 16)");
+    if (M > 0xfffe) return fail(h, RGG_EINVAL, "too many obstacles");
+    const int cell = o.cell_size > 0 ? o.cell_size : 128;
+    if (cell % 32 != 0 || cell > 256) return fail(h, RGG_EINVAL, "cell_size must be a multiple of 32, <= 256");
+    const int cap = o.cell_capacity > 0 ? o.cell_capacity : 64;
+    const int shards = o.shard_count > 1 ? o.shard_count : 1;
+    const int rank = shards > 1 ? o.shard_rank : 0;
+    if (rank < 0 || rank >= shards) return fail(h, RGG_EINVAL, "shard_rank out of range");
+    for (int32_t i = 0; i < M; ++i)
+        if (v->obst_sph_n[i] < 0 || v->obst_sph_n[i] > C) return fail(h, RGG_EINVAL, "bad obstacle sphere count");
+    const int64_t nrows = static_cast<int64_t>(N) * B * S;
+    if (v->row_off[0] != 0) return fail(h, RGG_ELOGIC, "row_off must start at 0");
+    for (int64_t r = 0; r < nrows; ++r)
+        if (v->row_off[r + 1] < v->row_off[r]) return fail(h, RGG_ELOGIC, "row_off must be non-decreasing");
+
+    h->device = o.device;
+    CK(cudaSetDevice(h->device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, h->device));
+    if (prop.major != 10) return fail(h, RGG_ECUDA, std::string("needs an sm_100 (B200) device, found ") + prop.name);
+    h->sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    for (auto& e : h->ev) CK(cudaEventCreate(&e));
+
+    // ---- cell-sort components by the Morton code of their AABB centre
+    std::vector<int32_t> order(N);
+    std::iota(order.begin(), order.end(), 0);
+    if (N > 1) {
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        std::vector<double> ctr(static_cast<size_t>(N) * 3);
+        for (int32_t c = 0; c < N; ++c) {
+            for (int k = 0; k < 3; ++k) {
+                double x = 0.5 * (v->comp_aabb[6 * c + k] + v->comp_aabb[6 * c + 3 + k]);
+                if (!(x == x)) x = 0;  // NaN guard
+                ctr[3 * c + k] = x;
+                lo[k] = std::min(lo[k], x);
+                hi[k] = std::max(hi[k], x);
+            }
+        }
+        std::vector<uint64_t> key(N);
+        for (int32_t c = 0; c < N; ++c) {
+            uint64_t code = 0;
+            for (int k = 0; k < 3; ++k) {
+                const double span = hi[k] - lo[k];
+                const double t = span > 0 ? (ctr[3 * c + k] - lo[k]) / span : 0.0;
+                const uint64_t q = static_cast<uint64_t>(std::min(std::max(t, 0.0), 1.0) * 2097151.0);
+                code |= spread3(q) << k;
+            }
+            key[c] = code;
+        }
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+    }
+    // ---- shard: interleaved cells of the global order
+    std::vector<int32_t> owned;
+    owned.reserve(N / shards + cell);
+    const int64_t gcells = (static_cast<int64_t>(N) + cell - 1) / cell;
+    for (int64_t g = 0; g < gcells; ++g) {
+        if (g % shards != rank) continue;
+        for (int64_t i = g * cell; i < std::min<int64_t>(N, (g + 1) * cell); ++i) owned.push_back(order[i]);
+    }
+    const int32_t Np = static_cast<int32_t>(owned.size());
+    const int32_t ncells = (Np + cell - 1) / cell;
+    h->orig = owned;
+    h->words = M <= 64 ? 1 : (M + 63) / 64;
+
+    // ---- host staging in sorted order
+    std::vector<double2> aabb(static_cast<size_t>(Np) * 3);
+    std::vector<double> sat(static_cast<size_t>(Np) * B * 22, 0.0);
+    std::vector<int32_t> row(static_cast<size_t>(Np) * B * S + 1);
+    std::vector<double> cell_aabb(static_cast<size_t>(ncells) * 6);
+    int64_t total = 0;
+    for (int32_t i = 0; i < Np; ++i) {
+        const int32_t c = owned[i];
+        const double* a = v->comp_aabb + 6 * static_cast<size_t>(c);
+        aabb[i] = make_double2(a[0], a[1]);
+        aabb[Np + i] = make_double2(a[2], a[3]);
+        aabb[2 * static_cast<size_t>(Np) + i] = make_double2(a[4], a[5]);
+        for (int b = 0; b < B; ++b)
+            std::memcpy(&sat[(static_cast<size_t>(i) * B + b) * 22], v->edge_sat + (static_cast<size_t>(c) * B + b) * 21,
+                        21 * sizeof(double));
+        for (int r = 0; r < B * S; ++r) {
+            row[static_cast<size_t>(i) * B * S + r] = static_cast<int32_t>(total);
+            const int64_t src = static_cast<int64_t>(c) * B * S + r;
+            total += v->row_off[src + 1] - v->row_off[src];
+        }
+    }
+    row[static_cast<size_t>(Np) * B * S] = static_cast<int32_t>(total);
+    if (total > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
+    h->total_segs_owned = total;
+    std::vector<double> seg(static_cast<size_t>(total) * 8, 0.0);
+    for (int32_t i = 0; i < Np; ++i) {
+        const int32_t c = owned[i];
+        for (int r = 0; r < B * S; ++r) {
+            const int64_t src = static_cast<int64_t>(c) * B * S + r;
+            int64_t dst = row[static_cast<size_t>(i) * B * S + r];
+            for (int64_t k = v->row_off[src]; k < v->row_off[src + 1]; ++k, ++dst)
+                std::memcpy(&seg[dst * 8], v->segs + 7 * k, 7 * sizeof(double));
+        }
+    }
+    for (int32_t g = 0; g < ncells; ++g) {
+        double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+        for (int32_t i = g * cell; i < std::min(Np, (g + 1) * cell); ++i) {
+            const double* a = v->comp_aabb + 6 * static_cast<size_t>(owned[i]);
+            for (int k = 0; k < 3; ++k) {
+                box[k] = std::min(box[k], a[k]);
+                box[3 + k] = std::max(box[3 + k], a[3 + k]);
+            }
+        }
+        std::memcpy(&cell_aabb[6 * static_cast<size_t>(g)], box, sizeof(box));
+    }
+    std::vector<int32_t> rankv(static_cast<size_t>(N), -1);
+    for (int32_t i = 0; i < Np; ++i) rankv[owned[i]] = i;
+
+    // ---- device store
+    CK(dalloc(&h->d_aabb, aabb.size()));
+    CK(dalloc(&h->d_sat, sat.size()));
+    CK(dalloc(&h->d_row, row.size()));
+    CK(dalloc(&h->d_seg, seg.size()));
+    CK(dalloc(&h->d_spline, static_cast<size_t>(B) * S));
+    CK(dalloc(&h->d_orig, Np));
+    CK(dalloc(&h->d_rank, N));
+    CK(dalloc(&h->d_cell_aabb, cell_aabb.size()));
+    CK(dalloc(&h->d_ohe, static_cast<size_t>(M) * 3));
+    CK(dalloc(&h->d_osl, static_cast<size_t>(M) * std::max(C, 1) * 3));
+    CK(dalloc(&h->d_osr, M));
+    CK(dalloc(&h->d_osn, M));
+    CK(dalloc(&h->d_state, static_cast<size_t>(N) + 16));
+    CK(dalloc(&h->d_cnt, Np));
+    CK(dalloc(&h->d_over, static_cast<size_t>(h->words) * Np));
+    CK(dalloc(&h->d_under, static_cast<size_t>(h->words) * Np));
+    CK(dalloc(&h->d_cur, M));
+    CK(dalloc(&h->d_cur_union, static_cast<size_t>(M) * 6));
+    CK(dalloc(&h->d_ctr, 8));
+    CK(dalloc(&h->d_census, 8));
+    CK(dalloc(&h->d_gray, N));
+    CK(dalloc(&h->d_tiles, N / 4096 + 2));
+    CK(dalloc(&h->d_hits, N));
+    CK(dalloc(&h->d_cell_count, ncells));
+    CK(dalloc(&h->d_cell_list, static_cast<size_t>(ncells) * cap));
+    CK(dalloc(&h->d_cell_ovf, ncells));
+    CK(dalloc(&h->d_dirty, ncells));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 8 * sizeof(int32_t), 0));
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+        return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream) : cudaSuccess;
+    };
+    CK(up(h->d_aabb, aabb.data(), aabb.size() * sizeof(double2)));
+    CK(up(h->d_sat, sat.data(), sat.size() * sizeof(double)));
+    CK(up(h->d_row, row.data(), row.size() * sizeof(int32_t)));
+    CK(up(h->d_seg, seg.data(), seg.size() * sizeof(double)));
+    CK(up(h->d_spline, v->spline_radius, static_cast<size_t>(B) * S * sizeof(double)));
+    CK(up(h->d_orig, owned.data(), owned.size() * sizeof(int32_t)));
+    CK(up(h->d_rank, rankv.data(), rankv.size() * sizeof(int32_t)));
+    CK(up(h->d_cell_aabb, cell_aabb.data(), cell_aabb.size() * sizeof(double)));
+    CK(up(h->d_ohe, v->obst_he, static_cast<size_t>(M) * 3 * sizeof(double)));
+    CK(up(h->d_osl, v->obst_sph_local, static_cast<size_t>(M) * C * 3 * sizeof(double)));
+    CK(up(h->d_osr, v->obst_sph_r, static_cast<size_t>(M) * sizeof(double)));
+    CK(up(h->d_osn, v->obst_sph_n, static_cast<size_t>(M) * sizeof(int32_t)));
+    // labels: GREEN for owned components, 0xFF for components of other shards
+    CK(cudaMemsetAsync(h->d_state, shards > 1 ? 0xFF : 0, static_cast<size_t>(N) + 16, h->stream));
+    if (shards > 1) {
+        std::vector<uint8_t> st(static_cast<size_t>(N), 0xFF);
+        for (int32_t c : owned) st[c] = 0;
+        CK(cudaMemcpyAsync(h->d_state, st.data(), st.size(), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    CK(cudaMemsetAsync(h->d_cnt, 0, static_cast<size_t>(Np) * sizeof(uint32_t), h->stream));
+    CK(cudaMemsetAsync(h->d_over, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
+    CK(cudaMemsetAsync(h->d_under, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
+    CK(cudaMemsetAsync(h->d_ctr, 0, 8 * sizeof(int32_t), h->stream));
+
+    Store& s = h->s;
+    s.N = N;
+    s.Np = Np;
+    s.B = B;
+    s.S = S;
+    s.M = M;
+    s.C = C;
+    s.W = h->words;
+    s.cell = cell;
+    s.ncells = ncells;
+    s.cap = cap;
+    s.use_under = o.use_under ? 1 : 0;
+    s.aabb = h->d_aabb;
+    s.sat = h->d_sat;
+    s.row = h->d_row;
+    s.seg = h->d_seg;
+    s.spline_r = h->d_spline;
+    s.orig = h->d_orig;
+    s.cell_aabb = h->d_cell_aabb;
+    s.ohe = h->d_ohe;
+    s.osl = h->d_osl;
+    s.osr = h->d_osr;
+    s.osn = h->d_osn;
+    s.state = h->d_state;
+    s.cnt = h->d_cnt;
+    s.over = h->d_over;
+    s.under = h->d_under;
+    s.cur = h->d_cur;
+    s.cur_union = h->d_cur_union;
+    CK(rggk::launch_init_obstacles(s, nullptr, h->stream));
+    h->grid_classify = std::max(1, std::min(ncells, h->sms * rggk::classify_occupancy(cell, rggk::kPerMove)));
+    const int rc = grow_batch(h, 64);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    h->unknown = 0;
+    h->unknown_stale = false;
+    return RGG_OK;
+}
+
+void rgg_gpu_destroy(rgg_gpu* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+                   h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
+                   h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
+                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_prev, h->d_last, h->d_ev,
+                   h->d_mv, h->d_pool};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    void* pin[] = {h->h_ids, h->h_rt, h->h_prev, h->h_last, h->h_mv, h->h_ctr};
+    for (void* p : pin)
+        if (p) cudaFreeHost(p);
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
+                   rgg_update_report* reports) {
+    if (!h) return RGG_EINVAL;
+    if (n < 0 || (n > 0 && (!ids || !rt12))) return fail(h, RGG_EINVAL, "bad move list");
+    if (!(flags & RGG_LAZY))
+        return fail(h, RGG_EINVAL, "eager updates resolve gray components on the host: call with RGG_LAZY per move, "
+                                   "then rgg_gpu_last_hits + rgg_gpu_write_states");
+    if ((flags & RGG_ASYNC) && reports) return fail(h, RGG_EINVAL, "reports need a synchronous update");
+    CK(cudaSetDevice(h->device));
+    // the reference applies moves in order and throws at the first bad id
+    int32_t k = 0;
+    while (k < n && ids[k] >= 0 && ids[k] < h->s.M) ++k;
+    const bool bad = k < n;
+    if (k > 0) {
+        if (reports && (flags & RGG_PER_MOVE)) {
+            const int rc = refresh_unknown(h);
+            if (rc) return rc;
+        }
+        const int32_t u0 = h->unknown;
+        int rc = grow_batch(h, k);
+        if (rc) return rc;
+        rc = grow_pinned(h, k);
+        if (rc) return rc;
+        std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
+        std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 12 * sizeof(double));
+        link_moves(ids, k, h->s.M, h->h_prev, h->h_last);
+        CK(cudaMemcpyAsync(h->d_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->d_rt, h->h_rt, static_cast<size_t>(k) * 12 * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream));
+        CK(cudaMemcpyAsync(h->d_prev, h->h_prev, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->d_last, h->h_last, k * sizeof(uint8_t), cudaMemcpyHostToDevice, h->stream));
+        rc = enqueue(h, k, flags);
+        if (rc) return rc;
+        if (!(flags & RGG_ASYNC) || bad) {
+            if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
+                                            cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, "overflow pool exhausted");
+            h->unknown = h->h_ctr[4];
+            h->unknown_stale = false;
+            if (reports) {
+                float t[4] = {0, 0, 0, 0};
+                for (int p = 0; p < 4; ++p) cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]);
+                int32_t u = u0;
+                for (int32_t i = 0; i < k; ++i) {
+                    rgg_update_report& r = reports[i];
+                    std::memset(&r, 0, sizeof(r));
+                    r.obstacle = ids[i];
+                    if (flags & RGG_PER_MOVE) {
+                        r.new_green = h->h_mv[4 * i];
+                        r.new_red = h->h_mv[4 * i + 1];
+                        r.new_gray = h->h_mv[4 * i + 2];
+                        u += r.new_gray - h->h_mv[4 * i + 3];
+                        r.unknown_after_heuristic = u;
+                        r.residual_unknown = u;
+                    } else {
+                        r.unknown_after_heuristic = r.residual_unknown = h->unknown;
+                    }
+                }
+                rgg_update_report& last = reports[k - 1];
+                last.reval_us = static_cast<int64_t>(t[0] * 1000.0f);
+                last.over_us = static_cast<int64_t>(t[1] * 1000.0f);
+                last.under_us = static_cast<int64_t>(t[2] * 1000.0f);
+                last.resolve_us = static_cast<int64_t>(t[3] * 1000.0f);
+            }
+        }
+    }
+    if (bad) return fail(h, RGG_EINVAL, "unknown obstacle id");
+    return RGG_OK;
+}
+
+int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12, int32_t n, int32_t flags) {
+    if (!h) return RGG_EINVAL;
+    if (n <= 0) return RGG_OK;
+    if (!(flags & RGG_LAZY)) return fail(h, RGG_EINVAL, "only lazy updates run on device");
+    CK(cudaSetDevice(h->device));
+    int rc = grow_batch(h, n);
+    if (rc) return rc;
+    rc = grow_pinned(h, n);
+    if (rc) return rc;
+    // prev/last need the ids on the host once; device-resident scripts are
+    // usually replayed, so the link table is computed from a D2H of the ids.
+    CK(cudaMemcpyAsync(h->h_ids, d_ids, n * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int32_t i = 0; i < n; ++i)
+        if (h->h_ids[i] < 0 || h->h_ids[i] >= h->s.M) return fail(h, RGG_EINVAL, "unknown obstacle id");
+    link_moves(h->h_ids, n, h->s.M, h->h_prev, h->h_last);
+    CK(cudaMemcpyAsync(h->d_ids, d_ids, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_rt, d_rt12, static_cast<size_t>(n) * 12 * sizeof(double), cudaMemcpyDeviceToDevice,
+                       h->stream));
+    CK(cudaMemcpyAsync(h->d_prev, h->h_prev, n * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_last, h->h_last, n * sizeof(uint8_t), cudaMemcpyHostToDevice, h->stream));
+    return enqueue(h, n, flags | RGG_ASYNC);
+}
+
+int rgg_gpu_sync(rgg_gpu* h) {
+    if (!h) return RGG_EINVAL;
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    return RGG_OK;
+}
+
+void* rgg_gpu_stream(rgg_gpu* h) { return h ? static_cast<void*>(h->stream) : nullptr; }
+
+int rgg_gpu_count(const rgg_gpu* h, int32_t* n_components, int32_t* n_obstacles, int32_t* words_per_comp) {
+    if (!h) return RGG_EINVAL;
+    if (n_components) *n_components = h->s.N;
+    if (n_obstacles) *n_obstacles = h->s.M;
+    if (words_per_comp) *words_per_comp = h->words;
+    return RGG_OK;
+}
+
+int rgg_gpu_read_states(rgg_gpu* h, uint8_t* out) {
+    if (!h || !out) return RGG_EINVAL;
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(out, h->d_state, h->s.N, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return RGG_OK;
+}
+
+int rgg_gpu_read_bits(rgg_gpu* h, uint64_t* out, int32_t words_per_comp) {
+    if (!h || !out) return RGG_EINVAL;
+    if (words_per_comp < h->words) return fail(h, RGG_EINVAL, "words_per_comp too small");
+    CK(cudaSetDevice(h->device));
+    const int32_t Np = h->s.Np;
+    std::vector<uint64_t> w(static_cast<size_t>(h->words) * Np);
+    if (!w.empty()) {
+        CK(cudaMemcpyAsync(w.data(), h->d_over, w.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    std::memset(out, 0, static_cast<size_t>(h->s.N) * words_per_comp * 8);
+    for (int32_t i = 0; i < Np; ++i)
+        for (int32_t k = 0; k < h->words; ++k)
+            out[static_cast<size_t>(h->orig[i]) * words_per_comp + k] = w[static_cast<size_t>(k) * Np + i];
+    return RGG_OK;
+}
+
+int rgg_gpu_unknown_count(rgg_gpu* h, int32_t* out) {
+    if (!h || !out) return RGG_EINVAL;
+    CK(cudaSetDevice(h->device));
+    const int rc = refresh_unknown(h);
+    if (rc) return rc;
+    *out = h->unknown;
+    return RGG_OK;
+}
+
+int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
+    if (!h || !n) return RGG_EINVAL;
+    CK(cudaSetDevice(h->device));
+    const int rc = refresh_unknown(h);
+    if (rc) return rc;
+    *n = h->unknown;
+    if (out && cap > 0 && h->unknown > 0) {
+        CK(cudaMemcpyAsync(out, h->d_gray, std::min(cap, h->unknown) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return RGG_OK;
+}
+
+int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
+    if (!h || !n) return RGG_EINVAL;
+    if (!h->last_hits_valid) return fail(h, RGG_EINVAL, "last hits are kept for single-move updates only");
+    CK(cudaSetDevice(h->device));
+    int32_t cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, h->d_ctr + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    *n = cnt;
+    if (out && cap > 0 && cnt > 0) {
+        CK(cudaMemcpyAsync(out, h->d_hits, std::min(cap, cnt) * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        std::sort(out, out + std::min(cap, cnt));
+    }
+    return RGG_OK;
+}
+
+int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int32_t n) {
+    if (!h) return RGG_EINVAL;
+    if (n <= 0) return RGG_OK;
+    for (int32_t i = 0; i < n; ++i) {
+        if (ids[i] < 0 || ids[i] >= h->s.N) return fail(h, RGG_EINVAL, "unknown component id");
+        if (st[i] > 2) return fail(h, RGG_EINVAL, "bad validity state");
+    }
+    CK(cudaSetDevice(h->device));
+    int32_t* d_ids = nullptr;
+    uint8_t* d_st = nullptr;
+    CK(dalloc(&d_ids, n));
+    CK(dalloc(&d_st, n));
+    CK(cudaMemcpyAsync(d_ids, ids, n * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(d_st, st, n, cudaMemcpyHostToDevice, h->stream));
+    CK(rggk::launch_write_states(h->s, d_ids, d_st, n, h->stream));
+    CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(d_ids);
+    cudaFree(d_st);
+    h->unknown_stale = true;
+    h->last_hits_valid = false;
+    return RGG_OK;
+}
+
+int rgg_gpu_pair_masks(rgg_gpu* h, int32_t kind, const int32_t* cand, int32_t n, int32_t o, uint8_t* mask) {
+    if (!h) return RGG_EINVAL;
+    if (o < 0 || o >= h->s.M) return fail(h, RGG_EINVAL, "unknown obstacle id");
+    if (kind != 0 && kind != 1) return fail(h, RGG_EINVAL, "kind must be 0 (over) or 1 (under)");
+    if (n <= 0) return RGG_OK;
+    for (int32_t i = 0; i < n; ++i)
+        if (cand[i] < 0 || cand[i] >= h->s.N) return fail(h, RGG_EINVAL, "unknown component id");
+    CK(cudaSetDevice(h->device));
+    int32_t* d_c = nullptr;
+    uint8_t* d_m = nullptr;
+    CK(dalloc(&d_c, n));
+    CK(dalloc(&d_m, n));
+    CK(cudaMemcpyAsync(d_c, cand, n * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    CK(rggk::launch_pair_masks(h->s, h->d_rank, kind, d_c, n, o, d_m, h->stream));
+    CK(cudaMemcpyAsync(mask, d_m, n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(d_c);
+    cudaFree(d_m);
+    return RGG_OK;
+}
+
+int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out) {
+    if (!h || !out) return RGG_EINVAL;
+    std::memset(out, 0, sizeof(*out));
+    if (!h->timed) return RGG_OK;
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    float t[5] = {0, 0, 0, 0, 0};
+    for (int p = 0; p < 4; ++p) CK(cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]));
+    CK(cudaEventElapsedTime(&t[4], h->ev[0], h->ev[4]));
+    out->pose_ms = t[0];
+    out->bin_ms = t[1];
+    out->classify_ms = t[2];
+    out->compact_ms = t[3];
+    out->total_ms = t[4];
+    int32_t ctr[8];
+    CK(cudaMemcpy(ctr, h->d_ctr, sizeof(ctr), cudaMemcpyDeviceToHost));
+    out->dirty_cells = ctr[0];
+    out->overflow_cells = ctr[3];
+    out->events = h->last_n;
+    return RGG_OK;
+}
+
+// Re-runs the last batch's classification in counting mode (no state change):
+// the reference's per-move work over the same (component, event) pairs.
+int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
+    if (!h || !out) return RGG_EINVAL;
+    if (h->last_n <= 0) return fail(h, RGG_EINVAL, "no update to count");
+    CK(cudaSetDevice(h->device));
+    int rc = rgg_gpu_last_stats(h, out);
+    if (rc) return rc;
+    Batch b = batch_of(h, h->last_n);
+    CK(cudaMemsetAsync(h->d_census, 0, 8 * sizeof(unsigned long long), h->stream));
+    CK(cudaMemsetAsync(h->d_ctr + 2, 0, sizeof(int32_t), h->stream));  // work counter
+    CK(rggk::launch_classify(h->s, b, rggk::kCensus, h->grid_classify, h->stream));
+    unsigned long long c[8];
+    CK(cudaMemcpyAsync(c, h->d_census, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    out->over_pairs = static_cast<int64_t>(c[0]);
+    out->sat_flops = static_cast<int64_t>(c[1]);
+    out->under_pairs = static_cast<int64_t>(c[2]);
+    out->seg_sphere_tests = static_cast<int64_t>(c[3]);
+    out->over_hits = static_cast<int64_t>(c[4]);
+    out->under_hits = static_cast<int64_t>(c[5]);
+    const int64_t narrow = static_cast<int64_t>(c[6]), narrow_segs = static_cast<int64_t>(c[7]);
+    // algorithmic bytes: every component of a dirty cell reads its AABB (48 B),
+    // label (1 B) and counters (4 B) and bit words (16 B per word); the ones
+    // with an AABB overlap also read their SatBoxes (B*168 B), row offsets and
+    // real segments (56 B each); labels/counters/bits are written back.
+    const int64_t dirty_comps = static_cast<int64_t>(std::min(out->dirty_cells * h->s.cell, h->s.Np));
+    out->bytes_components = dirty_comps * (48 + 2 * (1 + 4 + 16 * h->words)) +
+                            narrow * (static_cast<int64_t>(h->s.B) * 168 + 4 * (h->s.B * h->s.S + 1)) +
+                            narrow_segs * 56;
+    return RGG_OK;
+}
+
+// Measured fp64 (non-FMA add/mul) issue rate in GFLOP/s: the compute roof of
+// the fp64-exact classification (bench.py roofline).
+int rgg_gpu_fp64_peak(int device, double* gflops) {
+    rgg_gpu* h = nullptr;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    double* sink = nullptr;
+    CK(cudaMalloc(&sink, 8));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const int block = 256, grid = prop.multiProcessorCount * 8, iters = 4096;
+    CK(rggk::launch_fp64_peak(sink, iters, grid, block, nullptr));
+    CK(cudaDeviceSynchronize());
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        CK(cudaEventRecord(a));
+        CK(rggk::launch_fp64_peak(sink, iters, grid, block, nullptr));
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    const double flops = 2.0 * 8.0 * iters * static_cast<double>(grid) * block;
+    *gflops = flops / (best * 1e-3) / 1e9;
+    return RGG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+// rgg_device.cuh — fp64-exact device predicates of the SerRGG hot path (sm_100a).
+//
+// Every expression is written with explicit round-to-nearest intrinsics
+// (__dadd_rn / __dsub_rn / __dmul_rn / __ddiv_rn / __dsqrt_rn), which nvcc
+// never contracts into DFMA, in the operation order of the reference's scalar
+// backend (proj/src/kernels_scalar.cpp, built with -ffp-contract=off,
+// proj/CMakeLists.txt:12-14).  That is what makes every predicate bit-identical
+// to the reference on every input (proj/include/rgg/kernels.hpp:8-13 states the
+// same contract for its AVX2 backend).
+#pragma once
+
+#include <cstdint>
+
+namespace rggd {
+
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+
+// dot3 of kernels_scalar.cpp:35: (x0 y0 + x1 y1) + x2 y2
+__device__ __forceinline__ double dot3(const double* x, const double* y) {
+    return add(add(mul(x[0], y[0]), mul(x[1], y[1])), mul(x[2], y[2]));
+}
+
+// Vec3 dot (vec3.hpp:39) has the same association.
+__device__ __forceinline__ double dot3v(double x0, double x1, double x2, double y0, double y1, double y2) {
+    return add(add(mul(x0, y0), mul(x1, y1)), mul(x2, y2));
+}
+
+// SatBox as 21 doubles: center[0..2], e[k][j] at 3+3k+j, u[k][j] at 12+3k+j
+// (proj/include/rgg/kernels.hpp:18-22).
+
+// separated_on, proj/src/kernels_scalar.cpp:37-42.  a = edge box, b = obstacle.
+__device__ __forceinline__ bool separated_on(const double* a, const double* b, const double* d, const double* ax) {
+    const double ra = add(add(fabs(dot3(a + 3, ax)), fabs(dot3(a + 6, ax))), fabs(dot3(a + 9, ax)));
+    const double rb = add(add(fabs(dot3(b + 3, ax)), fabs(dot3(b + 6, ax))), fabs(dot3(b + 9, ax)));
+    const double s = fabs(dot3(d, ax));
+    return s > add(ra, rb);
+}
+
+// sat_boxes, proj/src/kernels_scalar.cpp:48-69.  The verdict is "no tested
+// axis separates"; the set of tested axes (face axes always, cross axes iff
+// n2 >= 1e-12) is the reference's, so the boolean is identical whatever the
+// evaluation order.  COUNT accumulates SATCOST_ref in
+// reference order when non-null.
+template <bool COUNT>
+__device__ __forceinline__ bool sat_boxes(const double* a, const double* b, long long* cost) {
+    double d[3];
+    d[0] = sub(b[0], a[0]);
+    d[1] = sub(b[1], a[1]);
+    d[2] = sub(b[2], a[2]);
+    int flops = 3;
+    bool sep = false;
+#pragma unroll
+    for (int k = 0; k < 3 && !sep; ++k) {
+        flops += 40;
+        sep = separated_on(a, b, d, a + 12 + 3 * k);
+    }
+#pragma unroll
+    for (int k = 0; k < 3 && !sep; ++k) {
+        flops += 40;
+        sep = separated_on(a, b, d, b + 12 + 3 * k);
+    }
+#pragma unroll
+    for (int i = 0; i < 3 && !sep; ++i) {
+        const double* x = a + 12 + 3 * i;
+#pragma unroll
+        for (int j = 0; j < 3 && !sep; ++j) {
+            const double* y = b + 12 + 3 * j;
+            double axis[3];
+            axis[0] = sub(mul(x[1], y[2]), mul(x[2], y[1]));
+            axis[1] = sub(mul(x[2], y[0]), mul(x[0], y[2]));
+            axis[2] = sub(mul(x[0], y[1]), mul(x[1], y[0]));
+            const double n2 = dot3(axis, axis);
+            flops += 14;
+            if (n2 >= 1e-12) {
+                flops += 40;
+                sep = separated_on(a, b, d, axis);
+            }
+        }
+    }
+    if (COUNT) *cost += flops;
+    return !sep;
+}
+
+// seg_point_dist + seg_sphere, proj/src/kernels_scalar.cpp:81-96.
+// s = SegPrep (a[3], d[3], dd).  Closed predicate.
+__device__ __forceinline__ bool seg_sphere(const double* s, const double* c, double r_total) {
+    const double px = sub(c[0], s[0]);
+    const double py = sub(c[1], s[1]);
+    const double pz = sub(c[2], s[2]);
+    double t = 0.0;
+    if (s[6] > 0.0) {
+        t = __ddiv_rn(add(add(mul(px, s[3]), mul(py, s[4])), mul(pz, s[5])), s[6]);
+        t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    }
+    const double qx = sub(px, mul(t, s[3]));
+    const double qy = sub(py, mul(t, s[4]));
+    const double qz = sub(pz, mul(t, s[5]));
+    return __dsqrt_rn(add(add(mul(qx, qx), mul(qy, qy)), mul(qz, qz))) <= r_total;
+}
+
+// sat_prep, proj/src/kernels_scalar.cpp:7-30.
+__device__ __forceinline__ void sat_prep(const double* c, double* s) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int hi = (1 << k) * 3;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s[3 + 3 * k + j] = mul(0.5, sub(c[hi + j], c[j]));
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s[j] = add(add(add(c[j], s[3 + j]), s[6 + j]), s[9 + j]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double* ek = s + 3 + 3 * k;
+        const double n2 = add(add(mul(ek[0], ek[0]), mul(ek[1], ek[1])), mul(ek[2], ek[2]));
+        if (n2 > 0.0) {
+            const double len = __dsqrt_rn(n2);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) s[12 + 3 * k + j] = __ddiv_rn(ek[j], len);
+        } else {
+            s[12 + 3 * k + 0] = s[12 + 3 * k + 1] = s[12 + 3 * k + 2] = 0.0;
+        }
+    }
+}
+
+// Transform::apply, proj/include/rgg/vec3.hpp:72-76: ((r0 x + r1 y) + r2 z) + t.
+__device__ __forceinline__ void tf_apply(const double* rt, double x, double y, double z, double* out) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        out[i] = add(add(add(mul(rt[3 * i], x), mul(rt[3 * i + 1], y)), mul(rt[3 * i + 2], z)), rt[9 + i]);
+}
+
+// Aabb::overlaps, proj/include/rgg/vec3.hpp:126-129 (closed).
+__device__ __forceinline__ bool overlaps(const double* a, const double* b) {
+    return a[0] <= b[3] && b[0] <= a[3] && a[1] <= b[4] && b[1] <= a[4] && a[2] <= b[5] && b[2] <= a[5];
+}
+
+}  // namespace rggd

@@ -1,0 +1,91 @@
+// rgg_kernels.cuh — device data structures and kernel launchers shared by the
+// C-ABI (rgg_capi.cu) and the kernels (rgg_kernels.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rggk {
+
+constexpr int kMaxSpheres = 16;  // obstacle inner spheres per event (C)
+constexpr int kEvChunk = 32;     // events staged in shared memory per pass
+
+// One obstacle move after re-posing (BatchLayout::update_transforms,
+// proj/src/batch_layout.cpp:148-172), plus the obstacle's previous union box.
+struct alignas(16) Event {
+    double sat[21];  // kern::SatBox of the moved box
+    double r;        // o_minus_r (shared sphere radius)
+    double box[6];   // obstacle_aabb
+    double sph[6];   // obstacle_sphere_aabb
+    double nu[6];    // box U sph (new pose)
+    double old[6];   // box U sph at the pose before this move (empty if inactive)
+    double cen[kMaxSpheres * 3];
+    int32_t o;
+    int32_t nsph;
+    int32_t move;  // index of the move in the batch
+    int32_t pad;
+};
+static_assert(sizeof(Event) % 16 == 0, "Event must be 16-byte granular");
+
+// Device-resident store (cell-sorted SoA).
+struct Store {
+    int32_t N;       // components in the roadmap
+    int32_t Np;      // components owned by this handle (sorted order)
+    int32_t B, S, M, C, W;
+    int32_t cell, ncells, cap;
+    int32_t use_under;
+    const double2* aabb;       // 3 planes of Np double2: (minx,miny) (minz,maxx) (maxy,maxz)
+    const double* sat;         // Np*B*22 (21 + pad)
+    const int32_t* row;        // Np*B*S+1
+    const double* seg;         // T*8 (a, d, dd, pad)
+    const double* spline_r;    // B*S
+    const int32_t* orig;       // Np: sorted -> component id
+    const double* cell_aabb;   // ncells*6
+    const double* ohe;         // M*3
+    const double* osl;         // M*C*3
+    const double* osr;         // M
+    const int32_t* osn;        // M
+    uint8_t* state;            // N labels (component-id order)
+    uint32_t* cnt;             // Np: over_cnt | both_cnt << 16
+    unsigned long long* over;  // W*Np, word-major
+    unsigned long long* under; // W*Np
+    Event* cur;                // M: obstacle operands at the current pose
+    double* cur_union;         // M*6: box U sph of active obstacles (empty if inactive)
+};
+
+// Per-batch scratch.
+struct Batch {
+    int32_t n;
+    const int32_t* ids;
+    const double* rt;
+    const int32_t* prev;   // previous move of the same obstacle in this batch, or -1
+    const uint8_t* last;   // 1 if this is the obstacle's last move in this batch
+    Event* ev;             // n
+    int32_t* cell_count;   // ncells
+    int32_t* cell_list;    // ncells*cap
+    int32_t* cell_ovf;     // ncells: base in pool when count > cap
+    int32_t* pool;         // overflow pool (capacity pool_cap)
+    int32_t pool_cap;
+    int32_t* ctr;          // [0] dirty count, [1] pool top, [2] work counter, [3] overflow cells,
+                           // [4] gray count, [5] hits count, [6] error flag
+    int32_t* dirty;        // ncells
+    int32_t* mv;           // n*4: to_green, to_red, to_gray, from_gray
+    int32_t* hits;         // N: over-hit-by-last-move & still gray
+    unsigned long long* census;  // 8 counters
+};
+
+enum Flags : int32_t { kPerMove = 2, kHits = 8, kCensus = 16 };
+
+cudaError_t launch_pose(const Store& s, const Batch& b, cudaStream_t st);
+cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st);
+cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st);
+cudaError_t launch_commit(const Store& s, const Batch& b, cudaStream_t st);
+cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st);
+cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st);
+cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, const int32_t* cand, int n, int o,
+                              uint8_t* mask, cudaStream_t st);
+cudaError_t launch_init_obstacles(const Store& s, Event* scratch, cudaStream_t st);
+cudaError_t launch_fp64_peak(double* sink, int iters, int grid, int block, cudaStream_t st);
+int classify_occupancy(int cell, int flags);
+
+}  // namespace rggk

@@ -1,0 +1,371 @@
+"""Host-side mirror of ``rgg::BatchEngine`` over the C-ABI of include/rgg_gpu.h.
+
+Same names, argument meaning and error behaviour as the reference's update API
+(proj/include/rgg/engine_batch.hpp:17-63):
+
+    =====================================  ============================================
+    reference                              here
+    =====================================  ============================================
+    BatchEngine(components, scene, opts,   GpuEngine(layout, use_under=..., ...)
+                cell_capacity)             (layout = the serialized store, see LayoutView)
+    update_obstacle(o, pose, lazy)         update_obstacle(o, pose, lazy=True)
+    batch_update(moves, lazy)              batch_update(moves, lazy=True)
+    states()                               states()         -> uint8[N]
+    obstacle_bits()                        obstacle_bits()  -> uint64[N] (uint64[N, W] if M > 64)
+    unknown_count()                        unknown_count()
+    batch_over / batch_under               batch_over / batch_under (explicit candidates)
+    resolve_all_unknown()                  resolve_all_unknown(resolver)
+    std::invalid_argument                  ValueError (same message)
+    std::logic_error                       RuntimeError
+    =====================================  ============================================
+
+There is no CPU fallback: constructing a GpuEngine without the built
+``lib/librgg_gpu.so`` or without an sm_100 GPU raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Iterable, Sequence
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "librgg_gpu.so")
+
+RGG_OK, RGG_EINVAL, RGG_ECUDA, RGG_ENCCL, RGG_ENOMEM, RGG_ELOGIC = 0, 1, 2, 3, 4, 5
+RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC = 1, 2, 4
+GREEN, RED, GRAY = 0, 1, 2
+
+
+class _View(C.Structure):
+    _fields_ = [("n_components", C.c_int32), ("n_bodies", C.c_int32), ("n_slots", C.c_int32),
+                ("n_obstacles", C.c_int32), ("max_spheres", C.c_int32),
+                ("edge_sat", C.c_void_p), ("comp_aabb", C.c_void_p), ("row_off", C.c_void_p),
+                ("segs", C.c_void_p), ("spline_radius", C.c_void_p), ("obst_he", C.c_void_p),
+                ("obst_sph_local", C.c_void_p), ("obst_sph_r", C.c_void_p), ("obst_sph_n", C.c_void_p)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("device", C.c_int32), ("use_under", C.c_int32), ("cell_size", C.c_int32),
+                ("cell_capacity", C.c_int32), ("allow_wide", C.c_int32), ("shard_rank", C.c_int32),
+                ("shard_count", C.c_int32)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("obstacle", C.c_int32), ("new_green", C.c_int32), ("new_red", C.c_int32),
+                ("new_gray", C.c_int32), ("reval_us", C.c_int64), ("over_us", C.c_int64),
+                ("under_us", C.c_int64), ("resolve_us", C.c_int64), ("unknown_after_heuristic", C.c_int32),
+                ("residual_unknown", C.c_int32), ("resolve_checks", C.c_int32), ("_pad", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("pose_ms", C.c_float), ("bin_ms", C.c_float), ("classify_ms", C.c_float),
+                ("compact_ms", C.c_float), ("total_ms", C.c_float), ("dirty_cells", C.c_int32),
+                ("events", C.c_int32), ("overflow_cells", C.c_int32), ("over_pairs", C.c_int64),
+                ("sat_flops", C.c_int64), ("under_pairs", C.c_int64), ("seg_sphere_tests", C.c_int64),
+                ("over_hits", C.c_int64), ("under_hits", C.c_int64), ("bytes_components", C.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    """Load lib/librgg_gpu.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA engine not built: {LIB_PATH} missing "
+                               f"(run `python -m paper_2603_28674_b200.build`)")
+        L = C.CDLL(LIB_PATH)
+        vp, ip, i32 = C.c_void_p, C.POINTER(C.c_int32), C.c_int32
+        L.rgg_gpu_create.argtypes = [C.POINTER(_View), C.POINTER(_Options), C.POINTER(vp)]
+        L.rgg_gpu_destroy.argtypes = [vp]
+        L.rgg_gpu_destroy.restype = None
+        L.rgg_gpu_last_error.argtypes = [vp]
+        L.rgg_gpu_last_error.restype = C.c_char_p
+        L.rgg_gpu_update.argtypes = [vp, vp, vp, i32, i32, vp]
+        L.rgg_gpu_update_device.argtypes = [vp, vp, vp, i32, i32]
+        L.rgg_gpu_sync.argtypes = [vp]
+        L.rgg_gpu_count.argtypes = [vp, ip, ip, ip]
+        L.rgg_gpu_read_states.argtypes = [vp, vp]
+        L.rgg_gpu_read_bits.argtypes = [vp, vp, i32]
+        L.rgg_gpu_unknown_count.argtypes = [vp, ip]
+        L.rgg_gpu_gray_ids.argtypes = [vp, vp, i32, ip]
+        L.rgg_gpu_last_hits.argtypes = [vp, vp, i32, ip]
+        L.rgg_gpu_write_states.argtypes = [vp, vp, vp, i32]
+        L.rgg_gpu_pair_masks.argtypes = [vp, i32, vp, i32, i32, vp]
+        L.rgg_gpu_last_stats.argtypes = [vp, C.POINTER(Stats)]
+        L.rgg_gpu_census.argtypes = [vp, C.POINTER(Stats)]
+        L.rgg_gpu_stream.argtypes = [vp]
+        L.rgg_gpu_stream.restype = vp
+        L.rgg_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+        _lib = L
+    return _lib
+
+
+EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_update", "rgg_gpu_update_device",
+            "rgg_gpu_sync", "rgg_gpu_count", "rgg_gpu_read_states", "rgg_gpu_read_bits", "rgg_gpu_unknown_count",
+            "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
+            "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak"]
+
+
+@dataclass
+class LayoutView:
+    """The serialized store handed to rgg_gpu_create (see include/rgg_gpu.h)."""
+
+    N: int
+    B: int
+    S: int
+    M: int
+    C: int
+    edge_sat: np.ndarray  # (N*B, 21) float64
+    comp_aabb: np.ndarray  # (N, 6) float64
+    row_off: np.ndarray  # (N*B*S + 1,) int32
+    segs: np.ndarray  # (T, 7) float64
+    spline_r: np.ndarray  # (B*S,) float64
+    obst_he: np.ndarray  # (M, 3)
+    obst_sph_local: np.ndarray  # (M, C, 3)
+    obst_sph_r: np.ndarray  # (M,)
+    obst_sph_n: np.ndarray  # (M,) int32
+    meta: dict = field(default_factory=dict)
+
+    @classmethod
+    def from_any(cls, obj) -> "LayoutView":
+        """From any object/dict carrying the same attribute names (e.g. a golden fixture)."""
+        get = (lambda k: obj[k]) if isinstance(obj, dict) else (lambda k: getattr(obj, k))
+        return cls(N=int(get("N")), B=int(get("B")), S=int(get("S")), M=int(get("M")), C=int(get("C")),
+                   edge_sat=get("edge_sat"), comp_aabb=get("comp_aabb"), row_off=get("row_off"),
+                   segs=get("segs"), spline_r=get("spline_r"), obst_he=get("obst_he"),
+                   obst_sph_local=get("obst_sph_local"), obst_sph_r=get("obst_sph_r"),
+                   obst_sph_n=get("obst_sph_n"))
+
+
+@dataclass
+class UpdateReport:
+    """rgg::UpdateReport (proj/include/rgg/update_report.hpp:11-39)."""
+
+    obstacle: int = -1
+    new_green: int = 0
+    new_red: int = 0
+    new_gray: int = 0
+    reval_us: int = 0
+    over_us: int = 0
+    under_us: int = 0
+    resolve_us: int = 0
+    unknown_after_heuristic: int = 0
+    residual_unknown: int = 0
+    resolve_checks: int = 0
+
+
+def _pose12(pose) -> np.ndarray:
+    p = np.ascontiguousarray(pose, dtype=np.float64).reshape(-1)
+    if p.size != 12:
+        raise ValueError("pose must be 12 doubles: row-major rotation r[9] then translation t[3]")
+    return p
+
+
+class GpuEngine:
+    def __init__(self, layout, use_under: bool = True, cell_size: int = 128, cell_capacity: int = 64,
+                 allow_wide: bool | None = None, device: int = 0, shard_rank: int = 0, shard_count: int = 1):
+        L = library()
+        lv = layout if isinstance(layout, LayoutView) else LayoutView.from_any(layout)
+        keep = {}
+
+        def arr(name, dt, shape=None):
+            a = np.ascontiguousarray(getattr(lv, name), dtype=dt)
+            keep[name] = a
+            return a.ctypes.data
+
+        view = _View(lv.N, lv.B, lv.S, lv.M, lv.C, arr("edge_sat", np.float64), arr("comp_aabb", np.float64),
+                     arr("row_off", np.int32), arr("segs", np.float64), arr("spline_r", np.float64),
+                     arr("obst_he", np.float64), arr("obst_sph_local", np.float64), arr("obst_sph_r", np.float64),
+                     arr("obst_sph_n", np.int32))
+        wide = lv.M > 64 if allow_wide is None else allow_wide
+        opts = _Options(device, int(use_under), cell_size, cell_capacity, int(wide), shard_rank, shard_count)
+        h = C.c_void_p()
+        rc = L.rgg_gpu_create(C.byref(view), C.byref(opts), C.byref(h))
+        self._h = h
+        if rc != RGG_OK:
+            msg = L.rgg_gpu_last_error(h).decode()
+            L.rgg_gpu_destroy(h)
+            self._h = None
+            self._raise(rc, msg)
+        n, m, w = C.c_int32(), C.c_int32(), C.c_int32()
+        L.rgg_gpu_count(h, C.byref(n), C.byref(m), C.byref(w))
+        self.n_components, self.n_obstacles, self.words = n.value, m.value, w.value
+        self.layout = lv
+
+    # ------------------------------------------------------------- plumbing
+    @staticmethod
+    def _raise(rc, msg):
+        if rc == RGG_EINVAL:
+            raise ValueError(msg)
+        raise RuntimeError(f"rgg_gpu error {rc}: {msg}")
+
+    def _check(self, rc):
+        if rc != RGG_OK:
+            self._raise(rc, library().rgg_gpu_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            library().rgg_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ------------------------------------------------------------ update API
+    def batch_update(self, moves, lazy: bool = True, per_move: bool = True,
+                     resolve: Callable[[np.ndarray], np.ndarray] | None = None) -> list[UpdateReport]:
+        """moves: list of (obstacle, pose12) pairs, or a tuple (ids int32[n], rt12 float64[n, 12])."""
+        ids, rts = self._moves(moves)
+        if not lazy:
+            return [self.update_obstacle(int(o), r, lazy=False, resolve=resolve) for o, r in zip(ids, rts)]
+        n = len(ids)
+        if n == 0:
+            return []
+        reps = (_Report * n)()
+        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0)
+        rc = library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, n, flags, reps)
+        self._check(rc)
+        return [UpdateReport(*[getattr(r, f) for f, _ in _Report._fields_[:-1]]) for r in reps]
+
+    def update_obstacle(self, o: int, pose, lazy: bool = True,
+                        resolve: Callable[[np.ndarray], np.ndarray] | None = None) -> UpdateReport:
+        """BatchEngine::update_obstacle (engine_batch.cpp:145-205).  Eager mode needs
+        ``resolve(ids) -> uint8 states``: the exact per-component check of
+        exact_component_valid (proj/src/roadmap.cpp:129-163), which stays on the host."""
+        if lazy:
+            return self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=True)[0]
+        if resolve is None:
+            raise ValueError("eager updates need an exact resolver for the gray over-hits")
+        before = self.states()
+        rep = self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=True)[0]
+        hits = self.last_hits()
+        rep.resolve_checks = len(hits)
+        if len(hits):
+            st = np.asarray(resolve(hits), np.uint8)
+            self.write_states(hits, st)
+            # finish_counts (engine_batch.cpp:41-53) compares the pre-move label with the final one
+            b0 = before[hits]
+            rep.new_gray -= int(np.sum(b0 != GRAY))
+            rep.new_green += int(np.sum((st == GREEN) & (b0 != GREEN)))
+            rep.new_red += int(np.sum((st == RED) & (b0 != RED)))
+        rep.residual_unknown = self.unknown_count()
+        return rep
+
+    def update_async(self, ids, rts):
+        """Enqueue a lazy batch without waiting (timed device path)."""
+        ids, rts = self._moves((ids, rts))
+        self._check(library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, len(ids),
+                                             RGG_LAZY | RGG_ASYNC, None))
+
+    def update_device(self, d_ids_ptr: int, d_rt_ptr: int, n: int, per_move: bool = False):
+        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0)
+        self._check(library().rgg_gpu_update_device(self._h, C.c_void_p(d_ids_ptr), C.c_void_p(d_rt_ptr), n, flags))
+
+    def sync(self):
+        self._check(library().rgg_gpu_sync(self._h))
+
+    @staticmethod
+    def _moves(moves):
+        if isinstance(moves, tuple) and len(moves) == 2 and not np.isscalar(moves[0]):
+            ids = np.ascontiguousarray(moves[0], dtype=np.int32).reshape(-1)
+            rts = np.ascontiguousarray(moves[1], dtype=np.float64).reshape(len(ids), 12)
+        else:
+            moves = list(moves)
+            ids = np.array([int(o) for o, _ in moves], dtype=np.int32)
+            rts = np.array([_pose12(p) for _, p in moves], dtype=np.float64).reshape(len(ids), 12)
+        return ids, rts
+
+    # -------------------------------------------------------------- queries
+    def states(self) -> np.ndarray:
+        out = np.empty(self.n_components, np.uint8)
+        self._check(library().rgg_gpu_read_states(self._h, out.ctypes.data))
+        return out
+
+    def obstacle_bits(self) -> np.ndarray:
+        out = np.empty(self.n_components * self.words, np.uint64)
+        self._check(library().rgg_gpu_read_bits(self._h, out.ctypes.data, self.words))
+        return out if self.words == 1 else out.reshape(self.n_components, self.words)
+
+    def unknown_count(self) -> int:
+        v = C.c_int32()
+        self._check(library().rgg_gpu_unknown_count(self._h, C.byref(v)))
+        return v.value
+
+    def gray_ids(self) -> np.ndarray:
+        n = C.c_int32()
+        self._check(library().rgg_gpu_gray_ids(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.int32)
+        if n.value:
+            self._check(library().rgg_gpu_gray_ids(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def last_hits(self) -> np.ndarray:
+        n = C.c_int32()
+        self._check(library().rgg_gpu_last_hits(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.int32)
+        if n.value:
+            self._check(library().rgg_gpu_last_hits(self._h, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def write_states(self, ids, st):
+        ids = np.ascontiguousarray(ids, np.int32)
+        st = np.ascontiguousarray(st, np.uint8)
+        self._check(library().rgg_gpu_write_states(self._h, ids.ctypes.data, st.ctypes.data, len(ids)))
+
+    def resolve_all_unknown(self, resolve: Callable[[np.ndarray], np.ndarray]) -> int:
+        """BatchEngine::resolve_all_unknown (engine_batch.cpp:217-227) with the exact
+        check supplied by the caller."""
+        ids = self.gray_ids()
+        if len(ids):
+            self.write_states(ids, np.asarray(resolve(ids), np.uint8))
+        return len(ids)
+
+    def _mask(self, kind, candidates, o) -> np.ndarray:
+        cands = np.ascontiguousarray(candidates, np.int32)
+        out = np.zeros(len(cands), np.uint8)
+        self._check(library().rgg_gpu_pair_masks(self._h, kind, cands.ctypes.data, len(cands), int(o),
+                                                 out.ctypes.data))
+        return out
+
+    def batch_over(self, candidates: Sequence[int], o: int) -> np.ndarray:
+        return self._mask(0, candidates, o)
+
+    def batch_under(self, candidates: Sequence[int], o: int) -> np.ndarray:
+        return self._mask(1, candidates, o)
+
+    # ---------------------------------------------------------- measurement
+    def last_stats(self) -> dict:
+        s = Stats()
+        self._check(library().rgg_gpu_last_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def census(self) -> dict:
+        s = Stats()
+        self._check(library().rgg_gpu_census(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def stream(self) -> int:
+        return library().rgg_gpu_stream(self._h) or 0
+
+
+def fp64_peak_gflops(device: int = 0) -> float:
+    v = C.c_double()
+    rc = library().rgg_gpu_fp64_peak(device, C.byref(v))
+    if rc != RGG_OK:
+        raise RuntimeError(library().rgg_gpu_last_error(None).decode())
+    return v.value

@@ -1,0 +1,156 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the reference's golden vectors.
+
+Every assertion is bit-exact: labels and obstacle bitsets are integers, and the
+fp64 predicates follow the reference's operation order (rgg_device.cuh).  The
+cases mirror the reference's own suites:
+  * kernel known-answer sets          proj/tests/test_kernels.cpp:46-121
+  * batch_over/batch_under masks      proj/tests/test_batch.cpp:208-234
+  * states + bits + reports per move  proj/tests/test_batch.cpp:260-285
+  * empty move list                   proj/tests/test_batch.cpp:287-295
+  * unknown obstacle id               proj/src/engine_batch.cpp:146-148
+"""
+import numpy as np
+import pytest
+
+from conftest import SCENARIOS, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng_mod():
+    from paper_2603_28674_b200 import engine
+
+    engine.library()
+    return engine
+
+
+def _layout(g):
+    from paper_2603_28674_b200.engine import LayoutView
+
+    return LayoutView.from_any(g)
+
+
+def _bits2d(b, words):
+    return b.reshape(-1, words)
+
+
+@pytest.mark.parametrize("name", SCENARIOS)
+def test_replay_per_move(eng_mod, name):
+    """One update_obstacle per move: reports and snapshots equal the reference's."""
+    g = load_golden(name)
+    eng = eng_mod.GpuEngine(_layout(g))
+    grouped = int(g["groups"]) > 1
+    snaps = {int(i): k for k, i in enumerate(g["snap_at"])}
+    for i, (o, rt) in enumerate(zip(g["ids"], g["rts"])):
+        rep = eng.update_obstacle(int(o), rt)
+        if not grouped:
+            exp = g["reports"][i]
+            assert [rep.new_green, rep.new_red, rep.new_gray, rep.unknown_after_heuristic] == exp[:4].tolist(), i
+        if i in snaps:
+            k = snaps[i]
+            assert np.array_equal(eng.states(), g["snap_states"][k]), f"states differ after move {i}"
+            bits = _bits2d(eng.obstacle_bits(), eng.words)
+            assert np.array_equal(bits, g["snap_bits"][k].reshape(bits.shape)), f"bits differ after move {i}"
+
+
+@pytest.mark.parametrize("name", SCENARIOS)
+def test_replay_one_batch(eng_mod, name):
+    """The whole move script as ONE batch_update: per-move reports from one launch sequence."""
+    g = load_golden(name)
+    eng = eng_mod.GpuEngine(_layout(g))
+    reps = eng.batch_update((g["ids"], g["rts"]))
+    assert len(reps) == len(g["ids"])
+    if int(g["groups"]) == 1:
+        got = np.array([[r.new_green, r.new_red, r.new_gray, r.unknown_after_heuristic] for r in reps])
+        assert np.array_equal(got, g["reports"][:, :4])
+    assert np.array_equal(eng.states(), g["snap_states"][-1])
+    bits = _bits2d(eng.obstacle_bits(), eng.words)
+    assert np.array_equal(bits, g["snap_bits"][-1].reshape(bits.shape))
+    st = g["snap_states"][-1]
+    assert eng.unknown_count() == int(np.sum(st == 2))
+    assert np.array_equal(eng.gray_ids(), np.nonzero(st == 2)[0].astype(np.int32))
+    allc = np.arange(int(g["N"]), dtype=np.int32)
+    o = int(g["mask_obstacle"])
+    assert np.array_equal(eng.batch_over(allc, o), g["masks"][0])
+    assert np.array_equal(eng.batch_under(allc, o), g["masks"][1])
+
+
+@pytest.mark.parametrize("name", ["scn_table4_obstacles_1000_5x", "syn_se2_m80"])
+@pytest.mark.parametrize("chunk", [7, 64])
+def test_replay_chunked_lazy(eng_mod, name, chunk):
+    """Lazy batches without per-move reports (the bench path); final state is the reference's."""
+    g = load_golden(name)
+    eng = eng_mod.GpuEngine(_layout(g), cell_size=64, cell_capacity=4)  # tiny capacity: overflow pool in use
+    ids, rts = g["ids"], g["rts"]
+    for a in range(0, len(ids), chunk):
+        eng.batch_update((ids[a:a + chunk], rts[a:a + chunk]), per_move=False)
+    assert np.array_equal(eng.states(), g["snap_states"][-1])
+    bits = _bits2d(eng.obstacle_bits(), eng.words)
+    assert np.array_equal(bits, g["snap_bits"][-1].reshape(bits.shape))
+
+
+def test_kat_sat_through_engine(eng_mod):
+    """test_kernels.cpp:46-87: 10000 SAT bytes, seed 2025, via batch_over."""
+    g = load_golden("kat_sat")
+    from paper_2603_28674_b200.engine import LayoutView
+
+    n = len(g["idx"])
+    lv = LayoutView(N=n, B=1, S=1, M=1, C=1, edge_sat=g["boxes"][g["idx"]],
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (n, 1)).astype(np.float64),
+                    row_off=np.zeros(n + 1, np.int32), segs=np.zeros((0, 7)), spline_r=np.zeros(1),
+                    obst_he=g["obstacle_he"][None, :], obst_sph_local=np.zeros((1, 1, 3)),
+                    obst_sph_r=np.zeros(1), obst_sph_n=np.ones(1, np.int32))
+    eng = eng_mod.GpuEngine(lv)
+    eng.update_obstacle(0, g["obstacle_pose"])
+    mask = eng.batch_over(np.arange(n, dtype=np.int32), 0)
+    assert np.array_equal(mask, g["out"])
+    assert 0 < mask.sum() < n
+
+
+def test_kat_seg_through_engine(eng_mod):
+    """test_kernels.cpp:89-121: 9001 seg-sphere bytes, seed 777, via batch_under."""
+    g = load_golden("kat_seg")
+    from paper_2603_28674_b200.engine import LayoutView
+
+    n = len(g["idx"])
+    pose = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, *g["center"]], np.float64)
+    lv = LayoutView(N=n, B=1, S=1, M=1, C=1, edge_sat=np.zeros((n, 21)),
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (n, 1)).astype(np.float64),
+                    row_off=np.arange(n + 1, dtype=np.int32), segs=g["segs"][g["idx"]],
+                    spline_r=np.array([float(g["r_total"])]), obst_he=np.ones((1, 3)),
+                    obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.zeros(1), obst_sph_n=np.ones(1, np.int32))
+    eng = eng_mod.GpuEngine(lv)
+    eng.update_obstacle(0, pose)
+    mask = eng.batch_under(np.arange(n, dtype=np.int32), 0)
+    assert np.array_equal(mask, g["out"])
+
+
+def test_empty_moves_and_bad_id(eng_mod):
+    g = load_golden("scn_quick_smoke")
+    eng = eng_mod.GpuEngine(_layout(g))
+    assert eng.batch_update([]) == []
+    assert np.array_equal(eng.states(), np.zeros(int(g["N"]), np.uint8))
+    ids = np.array([0, 1, 7], np.int32)
+    with pytest.raises(ValueError, match="unknown obstacle id"):
+        eng.batch_update((ids, g["rts"][:3]))
+    # moves before the bad one were applied, like the reference's sequential loop
+    ref = eng_mod.GpuEngine(_layout(g))
+    ref.batch_update((ids[:2], g["rts"][:2]))
+    assert np.array_equal(eng.states(), ref.states())
+
+
+def test_wide_requires_opt_in(eng_mod):
+    g = load_golden("syn_se2_m80")
+    with pytest.raises(ValueError, match="at most 64 obstacles"):
+        eng_mod.GpuEngine(_layout(g), allow_wide=False)
+
+
+def test_use_under_false_never_red(eng_mod):
+    """update_report.hpp:41-45: outer-only mode produces no red."""
+    g = load_golden("scn_table4_obstacles_1000_5x")
+    eng = eng_mod.GpuEngine(_layout(g), use_under=False)
+    eng.batch_update((g["ids"][:50], g["rts"][:50]))
+    st = eng.states()
+    assert not np.any(st == 1)
+    assert np.any(st == 2)
