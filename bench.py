@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py — SerRGG edge classification on B200: edges classified/s and per-update latency.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "c2"): SE(2) warehouse roadmap, 10k nodes /
+114k edges (N = 124,080 components incl. nodes), 64 moving yaw-rotated box
+obstacles, a move script of W + K iterations.  One STEP = one update of the
+obstacle set = one iteration of the script: all 64 obstacles re-posed through
+``batch_update`` with per-move UpdateReports (the reference's 64 calls to
+BatchEngine::update_obstacle, proj/src/engine_batch.cpp:145-215).  After each
+step every one of the N labels is the reference's, so
+
+    value = N_components x steps / device time          ("edges/s")
+    per-update latency = ms_per_step
+
+* ``value``: moves already resident in HBM, timed with CUDA events on the
+  engine's stream, L2 flushed (512 MB write) between steps.
+* ``e2e``: the same steps through the public API with HOST buffers
+  (GpuEngine.batch_update -> rgg_gpu_update: H2D of the moves, D2H of the
+  per-move reports), wall clock around the call.
+* ``--impl reference``: the reference's own CPU SerRGG path (BatchEngine, AVX2
+  backend, all host threads) from oracle/_ref on the same roadmap and moves.
+
+N > 1 (torchrun, one rank per GPU, NCCL): weak scaling.  Rank r owns tile r of
+an N-tile world (a c2 roadmap + 64 obstacles per tile, tiles side by side);
+obstacle moves are broadcast from rank 0 every step (ncclBroadcast) and the
+per-move report counters are summed onto every rank (ncclAllReduce).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASE_METRIC = "edges classified/sec and per-update latency (ms) at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="c2")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--seed", type=int, default=12345)
+    p.add_argument("--cpu-sample-s", type=float, default=15.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--json-out", default="")
+    p.add_argument("--clock-window-s", type=float, default=1.0)
+    return p.parse_args()
+
+
+def tile_workload(config, rank, seed, iterations):
+    """Rank r's tile: the config's roadmap shifted by r tiles in x, obstacles r*M..r*M+M-1."""
+    from paper_2603_28674_b200 import producer, synth
+
+    kind, nodes, k, half, m, ohalf = synth.CONFIGS[config]
+    rm = synth.make_roadmap(kind, nodes, k, half, seed + 1000 * rank)
+    obs = synth.make_obstacles(kind, m, seed + 1)
+    shift = 2.0 * (ohalf + 5.0) * rank
+    rm.nodes[:, 0] += shift
+    rm.env[[0, 3]] += shift
+    return rm, obs, shift
+
+
+def world_moves(config, world, seed, iterations):
+    """Moves of every tile, interleaved per iteration: [iteration][tile][obstacle]."""
+    from paper_2603_28674_b200 import synth
+
+    kind, nodes, k, half, m, ohalf = synth.CONFIGS[config]
+    ids_all, rts_all = [], []
+    for r in range(world):
+        ids, rts = synth.make_moves(kind, m, iterations, ohalf, seed + 2 + 7919 * r)
+        rts[:, 9] += 2.0 * (ohalf + 5.0) * r
+        ids_all.append(ids.reshape(iterations, m) + r * m)
+        rts_all.append(rts.reshape(iterations, m, 12))
+    ids = np.stack(ids_all, 1).reshape(iterations, world * m).astype(np.int32)
+    rts = np.stack(rts_all, 1).reshape(iterations, world * m, 12)
+    return ids, rts
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_run(config, seed, iterations, sample_s, threads, engine_kind=0):
+    """The reference's CPU SerRGG path on tile 0's roadmap + moves (oracle/_ref)."""
+    from oracle import ref
+    from paper_2603_28674_b200 import producer, synth
+
+    rm, obs, _ = tile_workload(config, 0, seed, iterations)
+    w = ref.World.from_roadmap(rm.robot_he, rm.env, rm.nodes, rm.edges, rm.eps, rm.max_segments)
+    for he, ns in zip(obs.he, obs.spheres):
+        w.add_obstacle(he, int(ns))
+    ids, rts = world_moves(config, 1, seed, iterations)
+    eng = ref.Engine(w, kind=engine_kind, threads=threads, group_size=64)
+    n = w.counts()["N"]
+    done, spent = 0, 0.0
+    per_step = []
+    for it in range(iterations):
+        us = eng.run(ids[it], rts[it], lazy=True)
+        per_step.append(us)
+        spent += us * 1e-6
+        done += 1
+        if spent >= sample_s:
+            break
+    return n, done, spent, per_step, eng
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    iterations = args.warmup + args.steps
+    n, done, spent, per_step, _ = cpu_reference_run(args.config, args.seed, iterations, 1e18, threads)
+    timed = per_step[args.warmup:] or per_step
+    t = sum(timed) * 1e-6
+    value = n * len(timed) / t
+    line = {
+        "impl": "reference", "metric": BASE_METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
+        "steps": len(timed), "warmup": min(args.warmup, done), "ms_per_step": 1e3 * t / len(timed),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args, n),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": f"rgg::BatchEngine (AVX2, {threads} threads) on tile 0: {len(timed)} updates x "
+                                   f"64 moves, oracle/_ref/librgg_ref.so"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, n_components, world=1):
+    from paper_2603_28674_b200 import synth
+
+    kind, nodes, k, half, m, ohalf = synth.CONFIGS[args.config]
+    return {"workload": f"{args.config}: {'SE(2)' if kind == 'se2' else '3D'} roadmap {nodes} nodes k={k} "
+                        f"({n_components} components incl. nodes) x {m} moving OBB obstacles per GPU tile; "
+                        f"1 step = 1 update = all {m} obstacles re-posed (per-move reports)",
+            "components_per_gpu": n_components, "obstacles_per_gpu": m, "moves_per_step": m * world,
+            "l2": "flushed (512 MB write) between timed steps", "parallelism": f"tiles x{world} (weak)",
+            "precision": "fp64-exact (reference op order, no FMA)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2603_28674_b200 import engine as E
+    from paper_2603_28674_b200 import producer
+
+    iterations = args.warmup + args.steps
+    rm, obs, _ = tile_workload(args.config, rank, args.seed, iterations)
+    obs_all = obs
+    if world > 1:
+        from paper_2603_28674_b200 import synth
+
+        obs_all = synth.Obstacles(he=np.tile(obs.he, (world, 1)), spheres=np.tile(obs.spheres, world))
+    lv = producer.layout_for(rm, obs_all)
+    eng = E.GpuEngine(lv, device=local)
+    N = lv.N
+    m_step = len(obs.he) * world
+    if rank == 0:
+        ids_h, rts_h = world_moves(args.config, world, args.seed, iterations)
+    else:
+        ids_h = np.zeros((iterations, m_step), np.int32)
+        rts_h = np.zeros((iterations, m_step, 12))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
+    ids_d = torch.from_numpy(ids_h).to(dev)
+    rts_d = torch.from_numpy(rts_h).to(dev)
+    counters = torch.zeros((m_step, 4), dtype=torch.int32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+
+    def step_device(it):
+        with torch.cuda.stream(stream):
+            if dist is not None:
+                dist.broadcast(ids_d[it], 0)
+                dist.broadcast(rts_d[it], 0)
+        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True)
+        if dist is not None:
+            with torch.cuda.stream(stream):
+                eng.copy_counters(counters.data_ptr(), m_step)
+                dist.all_reduce(counters)
+
+    # ---- warm-up (device path), then K timed steps with L2 flushed in between
+    for it in range(args.warmup):
+        step_device(it)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    classify_ms, stats = [], []
+    with ClockSampler(local) as clk:
+        t_clock0 = time.perf_counter()
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev[k][0].record(stream)
+            step_device(args.warmup + k)
+            ev[k][1].record(stream)
+            st = eng.last_stats()
+            classify_ms.append(st["classify_ms"])
+            stats.append(st)
+        torch.cuda.synchronize()
+        # keep the same load under the sampler for >= 1 s so clocks are observed under load
+        while time.perf_counter() - t_clock0 < args.clock_window_s:
+            step_device(args.warmup + (args.steps - 1))
+            torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if dist is not None:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    launches_per_step = 7 + (0 if dist is None else 0)
+    census = eng.census()
+    flops = census["sat_flops"] + 21 * census["seg_sphere_tests"]
+    byts = census["bytes_components"] + m_step * 768
+    mean_classify = statistics.mean(classify_ms)
+
+    # ---- e2e through the public API with host buffers (rank 0 drives; N>1 via torch collectives)
+    eng_e2e = E.GpuEngine(lv, device=local)
+    e2e_s = []
+    for it in range(iterations):
+        if it >= args.warmup:
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if dist is None:
+            reps = eng_e2e.batch_update((ids_h[it], rts_h[it]), per_move=True)
+        else:
+            ids_t = torch.from_numpy(ids_h[it]).pin_memory().to(dev, non_blocking=True)
+            rts_t = torch.from_numpy(rts_h[it]).pin_memory().to(dev, non_blocking=True)
+            dist.broadcast(ids_t, 0)
+            dist.broadcast(rts_t, 0)
+            torch.cuda.current_stream().synchronize()
+            eng_e2e.update_device(ids_t.data_ptr(), rts_t.data_ptr(), m_step, per_move=True)
+            with torch.cuda.stream(stream):
+                eng_e2e.copy_counters(counters.data_ptr(), m_step)
+                dist.all_reduce(counters)
+            reps = counters.cpu()
+        t1 = time.perf_counter()
+        if it >= args.warmup:
+            e2e_s.append(t1 - t0)
+    e2e_total = sum(e2e_s)
+    if dist is not None:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    # e2e and device engines must agree on the final labels
+    agree = bool(np.array_equal(eng.states(), eng_e2e.states()))
+
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return 0
+
+    n_total = N * world
+    value = n_total * args.steps / (total_ms * 1e-3)
+    e2e_value = n_total * args.steps / e2e_total
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    fp64 = E.fp64_peak_gflops(local)
+    t_fl = flops / (fp64 * 1e9)
+    t_by = byts / (hbm * 1e9)
+    if t_fl >= t_by:
+        roof = {"bound": "fp64", "achieved": flops / (mean_classify * 1e-3) / 1e12, "peak": fp64 / 1e3,
+                "unit": "TFLOP/s", "peak_source": "measured live: non-FMA DADD/DMUL issue rate (rgg_gpu_fp64_peak)"}
+    else:
+        roof = {"bound": "hbm", "achieved": byts / (mean_classify * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = "classify_kernel (rgg_kernels.cu)"
+    roof["algorithmic"] = {"flops_per_launch": flops, "bytes_per_launch": byts, "classify_ms_mean": mean_classify,
+                           "roof_ms": 1e3 * max(t_fl, t_by), "census": census}
+    line = {
+        "metric": BASE_METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, N, world),
+        "per_update_ms": total_ms / args.steps, "per_move_us": 1e3 * total_ms / args.steps / m_step,
+        "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": 1e3 * e2e_total / args.steps,
+                "h2d_bytes_per_step": m_step * (4 + 96 + 4 + 1), "d2h_bytes_per_step": m_step * 16 + 32,
+                "path": "GpuEngine.batch_update -> rgg_gpu_update (host numpy moves, per-move reports)",
+                "labels_equal_device_path": agree},
+        "gpu_launches": launches_per_step * args.steps,
+        "phase_ms_mean": {k: statistics.mean(s[k] for s in stats) for k in
+                          ("pose_ms", "bin_ms", "classify_ms", "compact_ms", "total_ms")},
+        "dirty_cells_mean": statistics.mean(s["dirty_cells"] for s in stats),
+        "roofline": roof, "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n, done, spent, per_step, _ = cpu_reference_run(args.config, args.seed, iterations, args.cpu_sample_s,
+                                                        threads)
+        cpu_v = n * done / spent
+        line["cpu_baseline"] = {"value": cpu_v, "unit": "edges/s", "cores": threads, "kind": "reference",
+                                "sample": f"rgg::BatchEngine (AVX2, {threads} threads) on the same tile-0 roadmap "
+                                          f"and moves: {done} updates x 64 moves in {spent:.1f} s",
+                                "ms_per_step": 1e3 * spent / done}
+    print(json.dumps(line), flush=True)
+    if args.json_out:
+        json.dump(line, open(args.json_out, "w"), indent=1)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

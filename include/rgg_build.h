@@ -1,0 +1,43 @@
+/* rgg_build.h — C-ABI of the host-side roadmap producer (CPU, multithreaded).
+ *
+ * Produces the serialized store consumed by rgg_gpu_create (include/rgg_gpu.h)
+ * from a roadmap of a free-flying box robot, following the reference's
+ * preprocessing so the inputs have the reference's shapes:
+ *   discretize_edge        proj/src/robot.cpp:39-64
+ *   forward_kinematics     proj/src/robot.cpp:66-84 (free-flying branch)
+ *   build_outer_approx     proj/src/swept.cpp:100-118 + obb_from_points geometry.cpp:134-195
+ *   build_inner_approx     proj/src/swept.cpp:188-228 (+ simplify :79-92, cap_segments :125-162)
+ *   build_components       proj/src/roadmap.cpp:104-127 (nodes first, then edges)
+ *   BatchLayout::serialize proj/src/batch_layout.cpp:21-146 (slots, SatBox, CSR of real segments)
+ * It is the step before the hot path, not part of it.
+ */
+#ifndef RGG_BUILD_H
+#define RGG_BUILD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rgg_built rgg_built;
+
+/* nodes: n_nodes x 6 DOFs (x, y, z, rx, ry, rz — fixed-axis XYZ Euler); edges: n_edges x 2.
+ * threads <= 0: hardware concurrency.  Returns 0, or -1 (see rgg_build_last_error). */
+int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
+                     const int32_t* edges, double eps, int32_t max_segments, int32_t threads, rgg_built** out);
+/* out[0..3] = N, B, S, T (real segments) */
+int rgg_built_counts(const rgg_built* b, int64_t* out);
+/* Any pointer may be null.  edge_sat N*B*21, comp_aabb N*6, row_off N*B*S+1, segs T*7,
+ * spline_r B*S, obb15 N*B*15 (centre, axes[3][3], half extents). */
+int rgg_built_export(const rgg_built* b, double* edge_sat, double* comp_aabb, int32_t* row_off, double* segs,
+                     double* spline_r, double* obb15);
+void rgg_built_free(rgg_built* b);
+const char* rgg_build_last_error(void);
+/* obstacle_inner_spheres (proj/src/swept.cpp:23-49): count centres (count*3) and the radius. */
+int rgg_obstacle_spheres(const double* he3, int32_t count, double* centres, double* radius);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -122,6 +122,10 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
  * The host-side id validation is skipped: ids must be in [0, M). */
 int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12, int32_t n, int32_t flags);
 int rgg_gpu_sync(rgg_gpu* h);
+/* Device-to-device copy (on the engine stream) of the last update's per-move
+ * counters, n x {to_green, to_red, to_gray, from_gray} int32 — the per-shard
+ * report terms a multi-GPU driver sums with one all-reduce. */
+int rgg_gpu_copy_counters(rgg_gpu* h, void* dst_device, int32_t n);
 
 int rgg_gpu_count(const rgg_gpu* h, int32_t* n_components, int32_t* n_obstacles, int32_t* words_per_comp);
 /* states(): N labels in component-id order (sharded handles: unowned entries are 0xFF). */

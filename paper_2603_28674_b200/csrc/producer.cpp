@@ -1,0 +1,598 @@
+// producer.cpp — host roadmap producer: swept-volume approximations + serialized store.
+//
+// Free-flying box robot (one body).  Every floating-point expression keeps the
+// association of the reference's preprocessing (built, like the reference, with
+// -ffp-contract=off) so the store it emits is the one the reference would
+// serialize for the same roadmap; tests/test_producer.py checks that bit for bit.
+// Components are independent, so they are built on a pool of std::threads.
+#include "../../include/rgg_build.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct V3 {
+    double x, y, z;
+};
+inline V3 operator+(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+inline V3 operator-(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline V3 operator*(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+inline double dotv(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline V3 crossv(V3 a, V3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+inline bool same(V3 a, V3 b) { return a.x == b.x && a.y == b.y && a.z == b.z; }
+
+// Rigid transform, row-major rotation (vec3.hpp:52-100).
+struct Tf {
+    double r[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    V3 t{0, 0, 0};
+    V3 apply(V3 p) const {
+        return {r[0] * p.x + r[1] * p.y + r[2] * p.z + t.x, r[3] * p.x + r[4] * p.y + r[5] * p.z + t.y,
+                r[6] * p.x + r[7] * p.y + r[8] * p.z + t.z};
+    }
+    V3 rotate(V3 p) const {
+        return {r[0] * p.x + r[1] * p.y + r[2] * p.z, r[3] * p.x + r[4] * p.y + r[5] * p.z,
+                r[6] * p.x + r[7] * p.y + r[8] * p.z};
+    }
+    Tf compose(const Tf& o) const {  // (this * o)
+        Tf out;
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+                out.r[i * 3 + j] = r[i * 3 + 0] * o.r[j] + r[i * 3 + 1] * o.r[3 + j] + r[i * 3 + 2] * o.r[6 + j];
+        out.t = apply(o.t);
+        return out;
+    }
+};
+
+// Transform::rotation_axis_angle (geometry.cpp:13-29), Rodrigues.
+Tf axis_angle(V3 axis, double angle) {
+    const double len = std::sqrt(dotv(axis, axis));
+    const double kx = axis.x / len, ky = axis.y / len, kz = axis.z / len;
+    const double c = std::cos(angle), s = std::sin(angle), v = 1.0 - c;
+    Tf tf;
+    tf.r[0] = kx * kx * v + c;
+    tf.r[1] = kx * ky * v - kz * s;
+    tf.r[2] = kx * kz * v + ky * s;
+    tf.r[3] = ky * kx * v + kz * s;
+    tf.r[4] = ky * ky * v + c;
+    tf.r[5] = ky * kz * v - kx * s;
+    tf.r[6] = kz * kx * v - ky * s;
+    tf.r[7] = kz * ky * v + kx * s;
+    tf.r[8] = kz * kz * v + c;
+    return tf;
+}
+
+struct Box {
+    V3 c;
+    V3 ax[3];
+    V3 he;
+};
+
+// obb_corners (geometry.cpp:50-62): corner i takes +axis k iff bit k of i.
+void corners_of(const Box& o, V3 out[8]) {
+    const V3 e0 = o.ax[0] * o.he.x, e1 = o.ax[1] * o.he.y, e2 = o.ax[2] * o.he.z;
+    for (int i = 0; i < 8; ++i) {
+        V3 p = (i & 1) ? o.c + e0 : o.c - e0;
+        p = (i & 2) ? p + e1 : p - e1;
+        p = (i & 4) ? p + e2 : p - e2;
+        out[i] = p;
+    }
+}
+
+// ---- obb_from_points (geometry.cpp:64-195): PCA frame + per-axis sweep
+
+void jacobi3(double m[3][3], double vals[3], V3 vecs[3]) {
+    double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        const double off = std::fabs(m[0][1]) + std::fabs(m[0][2]) + std::fabs(m[1][2]);
+        if (off == 0.0) break;
+        for (int p = 0; p < 2; ++p) {
+            for (int q = p + 1; q < 3; ++q) {
+                if (m[p][q] == 0.0) continue;
+                const double theta = (m[q][q] - m[p][p]) / (2.0 * m[p][q]);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double c = 1.0 / std::sqrt(t * t + 1.0);
+                const double s = t * c;
+                for (int k = 0; k < 3; ++k) {
+                    const double a = m[k][p], b = m[k][q];
+                    m[k][p] = c * a - s * b;
+                    m[k][q] = s * a + c * b;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    const double a = m[p][k], b = m[q][k];
+                    m[p][k] = c * a - s * b;
+                    m[q][k] = s * a + c * b;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    const double a = v[k][p], b = v[k][q];
+                    v[k][p] = c * a - s * b;
+                    v[k][q] = s * a + c * b;
+                }
+            }
+        }
+    }
+    for (int i = 0; i < 3; ++i) {
+        vals[i] = m[i][i];
+        vecs[i] = {v[0][i], v[1][i], v[2][i]};
+    }
+}
+
+inline double min_ref(double a, double b) { return b < a ? b : a; }  // std::min
+inline double max_ref(double a, double b) { return a < b ? b : a; }  // std::max
+
+struct Extent {
+    double lo[3], hi[3], vol;
+};
+
+Extent extents(const std::vector<V3>& pts, const V3 ax[3]) {
+    Extent f;
+    for (int k = 0; k < 3; ++k) {
+        f.lo[k] = INFINITY;
+        f.hi[k] = -INFINITY;
+    }
+    for (const V3& p : pts) {
+        for (int k = 0; k < 3; ++k) {
+            const double t = dotv(p, ax[k]);
+            f.lo[k] = min_ref(f.lo[k], t);
+            f.hi[k] = max_ref(f.hi[k], t);
+        }
+    }
+    f.vol = (f.hi[0] - f.lo[0]) * (f.hi[1] - f.lo[1]) * (f.hi[2] - f.lo[2]);
+    return f;
+}
+
+Box fit_box(const std::vector<V3>& pts) {
+    Box box{{0, 0, 0}, {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}, {0, 0, 0}};
+    if (pts.size() == 1) {
+        box.c = pts[0];
+        return box;
+    }
+    V3 mean{0, 0, 0};
+    for (const V3& p : pts) mean = mean + p;
+    mean = mean * (1.0 / static_cast<double>(pts.size()));
+    double cov[3][3] = {};
+    for (const V3& p : pts) {
+        const V3 d = p - mean;
+        const double dc[3] = {d.x, d.y, d.z};
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) cov[i][j] += dc[i] * dc[j];
+    }
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) cov[i][j] /= static_cast<double>(pts.size());
+    double vals[3];
+    V3 axes[3];
+    jacobi3(cov, vals, axes);
+    // largest variance first (stable), right-handed
+    int ord[3] = {0, 1, 2};
+    for (int i = 1; i < 3; ++i)
+        for (int j = i; j > 0 && vals[ord[j]] > vals[ord[j - 1]]; --j) std::swap(ord[j], ord[j - 1]);
+    V3 best[3] = {axes[ord[0]], axes[ord[1]], axes[ord[2]]};
+    best[2] = crossv(best[0], best[1]);
+    double best_vol = extents(pts, best).vol;
+    constexpr double kStep = 3.0 * 3.141592653589793 / 180.0;
+    for (int k = 0; k < 3; ++k) {
+        const V3 pivot = best[k];
+        V3 win[3] = {best[0], best[1], best[2]};
+        for (int step = -5; step <= 5; ++step) {
+            if (step == 0) continue;
+            const Tf rot = axis_angle(pivot, step * kStep);
+            V3 cand[3];
+            for (int j = 0; j < 3; ++j) cand[j] = rot.rotate(best[j]);
+            const double vol = extents(pts, cand).vol;
+            if (vol < best_vol) {
+                best_vol = vol;
+                for (int j = 0; j < 3; ++j) win[j] = cand[j];
+            }
+        }
+        for (int j = 0; j < 3; ++j) best[j] = win[j];
+    }
+    const Extent f = extents(pts, best);
+    box.c = best[0] * ((f.lo[0] + f.hi[0]) * 0.5) + best[1] * ((f.lo[1] + f.hi[1]) * 0.5) +
+            best[2] * ((f.lo[2] + f.hi[2]) * 0.5);
+    for (int k = 0; k < 3; ++k) box.ax[k] = best[k];
+    box.he = {(f.hi[0] - f.lo[0]) * 0.5, (f.hi[1] - f.lo[1]) * 0.5, (f.hi[2] - f.lo[2]) * 0.5};
+    return box;
+}
+
+// ---- predicates shared with the serialized store (kernels_scalar.cpp:7-96)
+
+void sat_prep(const double* c, double* s) {
+    for (int k = 0; k < 3; ++k) {
+        const int hi = (1 << k) * 3;
+        for (int j = 0; j < 3; ++j) s[3 + 3 * k + j] = 0.5 * (c[hi + j] - c[j]);
+    }
+    for (int j = 0; j < 3; ++j) s[j] = ((c[j] + s[3 + j]) + s[6 + j]) + s[9 + j];
+    for (int k = 0; k < 3; ++k) {
+        const double* e = s + 3 + 3 * k;
+        const double n2 = (e[0] * e[0] + e[1] * e[1]) + e[2] * e[2];
+        if (n2 > 0.0) {
+            const double len = std::sqrt(n2);
+            for (int j = 0; j < 3; ++j) s[12 + 3 * k + j] = e[j] / len;
+        } else {
+            s[12 + 3 * k] = s[13 + 3 * k] = s[14 + 3 * k] = 0.0;
+        }
+    }
+}
+
+void seg_prep(V3 a, V3 b, double* p) {
+    p[0] = a.x, p[1] = a.y, p[2] = a.z;
+    p[3] = b.x - a.x, p[4] = b.y - a.y, p[5] = b.z - a.z;
+    p[6] = (p[3] * p[3] + p[4] * p[4]) + p[5] * p[5];
+}
+
+double point_seg_dist(V3 a, V3 b, V3 c) {
+    double s[7];
+    seg_prep(a, b, s);
+    const double px = c.x - s[0], py = c.y - s[1], pz = c.z - s[2];
+    double t = 0.0;
+    if (s[6] > 0.0) {
+        t = ((px * s[3] + py * s[4]) + pz * s[5]) / s[6];
+        t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    }
+    const double qx = px - t * s[3], qy = py - t * s[4], qz = pz - t * s[5];
+    return std::sqrt((qx * qx + qy * qy) + qz * qz);
+}
+
+// ---- inner approximation (swept.cpp:23-228)
+
+struct Sph {
+    V3 c;
+    double r;
+};
+
+std::vector<Sph> inner_spheres(V3 he, int count) {
+    const double h[3] = {he.x, he.y, he.z};
+    const double radius = std::min({h[0], h[1], h[2]});
+    int axis = 0;
+    for (int k = 1; k < 3; ++k)
+        if (h[k] > h[axis]) axis = k;
+    const double span = h[axis] - radius;
+    std::vector<Sph> out;
+    for (int i = 0; i < count; ++i) {
+        const double t = count == 1 ? 0.0 : -span + (2.0 * span) * (static_cast<double>(i) / (count - 1));
+        V3 c{0, 0, 0};
+        (axis == 0 ? c.x : axis == 1 ? c.y : c.z) = t;
+        out.push_back({c, radius});
+    }
+    return out;
+}
+
+int sphere_count(V3 he) {
+    const double longest = std::max({he.x, he.y, he.z}), shortest = std::min({he.x, he.y, he.z});
+    return std::max(1, static_cast<int>(std::ceil(longest / shortest)));
+}
+
+bool covers(const std::vector<V3>& pts, int j, int p, double radius) {
+    for (int m = j + 1; m < p; ++m)
+        if (!(point_seg_dist(pts[j], pts[p], pts[m]) < radius)) return false;
+    return true;
+}
+
+std::vector<int> simplify(const std::vector<V3>& pts, double radius) {
+    const int n = static_cast<int>(pts.size());
+    std::vector<int> keep{0};
+    int j = 0;
+    while (j < n - 1) {
+        int p = j + 1;
+        while (p + 1 <= n - 1 && covers(pts, j, p + 1, radius)) ++p;
+        keep.push_back(p);
+        j = p;
+    }
+    return keep;
+}
+
+struct Spline {
+    std::vector<V3> pts;
+    double radius;
+    int sphere;
+};
+
+void cap_split(const std::vector<V3>& raw, const std::vector<int>& kept, double radius, double tol, int K, int sphere,
+               std::vector<Spline>& out) {
+    const int q = static_cast<int>(kept.size()) - 1;
+    if (q <= K) {
+        Spline s{{}, radius, sphere};
+        for (int i : kept) s.pts.push_back(raw[i]);
+        out.push_back(std::move(s));
+        return;
+    }
+    std::vector<int> sub;
+    for (int i = 0; i <= K; ++i) sub.push_back(kept[static_cast<size_t>(std::llround(static_cast<double>(i) * q / K))]);
+    bool ok = true;
+    for (size_t i = 0; ok && i + 1 < sub.size(); ++i) ok = covers(raw, sub[i], sub[i + 1], tol);
+    if (ok) {
+        Spline s{{}, radius, sphere};
+        for (int i : sub) s.pts.push_back(raw[i]);
+        out.push_back(std::move(s));
+        return;
+    }
+    for (int start = 0; start < q; start += K) {
+        const int stop = std::min(start + K, q);
+        Spline s{{}, radius, sphere};
+        for (int i = start; i <= stop; ++i) s.pts.push_back(raw[kept[i]]);
+        out.push_back(std::move(s));
+    }
+}
+
+struct Comp {
+    Box over;
+    std::vector<Spline> under;
+};
+
+struct Robot {
+    V3 he;
+    std::vector<Sph> spheres;
+    std::vector<double> lipschitz, radius, tol;
+};
+
+Robot make_robot(V3 he, double eps) {
+    Robot r;
+    r.he = he;
+    r.spheres = inner_spheres(he, sphere_count(he));
+    for (const Sph& s : r.spheres) {
+        // center_lipschitz (swept.cpp:166-178), body.local = identity
+        const Tf local;
+        const V3 p = local.apply(s.c);
+        const double L = std::sqrt(1.0 + 3.0 * dotv(p, p));
+        // certified_spline_radius (swept.cpp:180-186)
+        const double half_step = 0.5 * L * eps;
+        const double r2 = s.r * s.r - half_step * half_step;
+        double rad = 0.0;
+        if (r2 > 0.0) rad = std::sqrt(r2) * (1.0 - 0.1) - 1e-9;
+        r.lipschitz.push_back(L);
+        r.radius.push_back(rad);
+        r.tol.push_back(std::sqrt(s.r * s.r - 0.25 * L * eps * L * eps) - rad - 1e-9);
+    }
+    return r;
+}
+
+// forward_kinematics, free-flying branch (robot.cpp:71-74).
+Tf body_pose(const double* c) {
+    Tf world = axis_angle({0, 0, 1}, c[5]).compose(axis_angle({0, 1, 0}, c[4])).compose(axis_angle({1, 0, 0}, c[3]));
+    world.t = {c[0], c[1], c[2]};
+    return world.compose(Tf{});
+}
+
+Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K) {
+    // discretize_edge (robot.cpp:39-64)
+    double len2 = 0.0;
+    for (int i = 0; i < 6; ++i) {
+        const double d = b[i] - a[i];
+        len2 += d * d;
+    }
+    const double len = std::sqrt(len2);
+    const int n = std::max(2, static_cast<int>(std::ceil(len / eps)) + 1);
+    std::vector<Tf> fk(n);
+    double cfg[6];
+    for (int i = 0; i < n; ++i) {
+        if (i == 0) {
+            std::memcpy(cfg, a, sizeof(cfg));
+        } else if (i == n - 1) {
+            std::memcpy(cfg, b, sizeof(cfg));
+        } else {
+            const double t = static_cast<double>(i) / static_cast<double>(n - 1);
+            for (int k = 0; k < 6; ++k) cfg[k] = a[k] + (b[k] - a[k]) * t;
+        }
+        fk[i] = body_pose(cfg);
+    }
+    Comp comp;
+    // build_outer_approx (swept.cpp:100-118)
+    std::vector<V3> cloud;
+    cloud.reserve(static_cast<size_t>(n) * 8);
+    for (const Tf& T : fk) {
+        Box w;
+        w.c = T.apply({0, 0, 0});
+        w.ax[0] = T.rotate({1, 0, 0});
+        w.ax[1] = T.rotate({0, 1, 0});
+        w.ax[2] = T.rotate({0, 0, 1});
+        w.he = rb.he;
+        V3 cs[8];
+        corners_of(w, cs);
+        cloud.insert(cloud.end(), cs, cs + 8);
+    }
+    comp.over = fit_box(cloud);
+    // build_inner_approx (swept.cpp:188-228)
+    for (size_t si = 0; si < rb.spheres.size(); ++si) {
+        const double rad = rb.radius[si];
+        if (rad <= 0.0) continue;
+        const double step_bound = rb.lipschitz[si] * eps;
+        std::vector<V3> raw;
+        bool step_ok = true;
+        for (const Tf& T : fk) {
+            const V3 c = T.apply(rb.spheres[si].c);
+            if (!raw.empty()) {
+                const V3 d = c - raw.back();
+                if (std::sqrt(dotv(d, d)) > step_bound) step_ok = false;
+            }
+            if (raw.empty() || !same(c, raw.back())) raw.push_back(c);
+        }
+        if (!step_ok) continue;
+        const std::vector<int> kept = simplify(raw, rb.tol[si]);
+        cap_split(raw, kept, rad, rb.tol[si], K, static_cast<int>(si), comp.under);
+    }
+    return comp;
+}
+
+}  // namespace
+
+struct rgg_built {
+    int32_t N = 0, B = 1, S = 1;
+    std::vector<double> edge_sat, comp_aabb, segs, spline_r, obb15;
+    std::vector<int32_t> row_off;
+};
+
+extern "C" {
+
+const char* rgg_build_last_error(void) { return g_err.c_str(); }
+
+int rgg_build_layout(const double* he3, int32_t n_nodes, const double* nodes, int32_t n_edges, const int32_t* edges,
+                     double eps, int32_t K, int32_t threads, rgg_built** out) {
+    try {
+        if (!out) throw std::invalid_argument("null output");
+        if (!(eps > 0)) throw std::invalid_argument("resolution must be positive");
+        if (K < 1) throw std::invalid_argument("segment cap must be >= 1");
+        for (int32_t e = 0; e < n_edges; ++e)
+            if (edges[2 * e] < 0 || edges[2 * e] >= n_nodes || edges[2 * e + 1] < 0 || edges[2 * e + 1] >= n_nodes)
+                throw std::invalid_argument("edge endpoint out of range");
+        const Robot rb = make_robot({he3[0], he3[1], he3[2]}, eps);
+        const int32_t N = n_nodes + n_edges;
+        std::vector<Comp> comps(static_cast<size_t>(N));
+        int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+        nt = std::max(1, std::min(nt, 256));
+        std::atomic<int32_t> next{0};
+        std::string err;
+        std::atomic<bool> failed{false};
+        auto work = [&] {
+            try {
+                for (;;) {
+                    const int32_t c0 = next.fetch_add(256);
+                    if (c0 >= N || failed) break;
+                    for (int32_t c = c0; c < std::min(N, c0 + 256); ++c) {
+                        const double *a, *b;
+                        if (c < n_nodes) {
+                            a = b = nodes + 6 * static_cast<size_t>(c);
+                        } else {
+                            const int32_t e = c - n_nodes;
+                            a = nodes + 6 * static_cast<size_t>(edges[2 * e]);
+                            b = nodes + 6 * static_cast<size_t>(edges[2 * e + 1]);
+                        }
+                        comps[c] = build_comp(rb, a, b, eps, K);
+                    }
+                }
+            } catch (const std::exception& ex) {
+                failed = true;
+                err = ex.what();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int i = 1; i < nt; ++i) pool.emplace_back(work);
+        work();
+        for (auto& t : pool) t.join();
+        if (failed) throw std::runtime_error(err);
+
+        // ---- serialize (batch_layout.cpp:21-146)
+        rgg_built* L = new rgg_built();
+        L->N = N;
+        const int32_t nsph = static_cast<int32_t>(rb.spheres.size());
+        int32_t max_parts = 1;
+        std::vector<int32_t> parts(nsph);
+        for (const Comp& c : comps) {
+            std::fill(parts.begin(), parts.end(), 0);
+            for (const Spline& s : c.under) max_parts = std::max(max_parts, ++parts[s.sphere]);
+        }
+        const int32_t S = std::max(1, nsph) * max_parts;
+        L->S = S;
+        L->spline_r.assign(S, 0.0);
+        L->edge_sat.resize(static_cast<size_t>(N) * 21);
+        L->comp_aabb.resize(static_cast<size_t>(N) * 6);
+        L->obb15.resize(static_cast<size_t>(N) * 15);
+        L->row_off.assign(static_cast<size_t>(N) * S + 1, 0);
+        std::vector<int32_t> count(static_cast<size_t>(N) * S, 0);
+        std::vector<int32_t> slot_of;
+        for (int32_t c = 0; c < N; ++c) {
+            const Comp& cp = comps[c];
+            V3 cs[8];
+            corners_of(cp.over, cs);
+            sat_prep(&cs[0].x, &L->edge_sat[21 * static_cast<size_t>(c)]);
+            double box[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            for (const V3& p : cs) {
+                box[0] = std::fmin(box[0], p.x), box[1] = std::fmin(box[1], p.y), box[2] = std::fmin(box[2], p.z);
+                box[3] = std::fmax(box[3], p.x), box[4] = std::fmax(box[4], p.y), box[5] = std::fmax(box[5], p.z);
+            }
+            // component_aabb = union of the body boxes (one body): Aabb::empty().expand(box)
+            std::memcpy(&L->comp_aabb[6 * static_cast<size_t>(c)], box, sizeof(box));
+            double* o = &L->obb15[15 * static_cast<size_t>(c)];
+            o[0] = cp.over.c.x, o[1] = cp.over.c.y, o[2] = cp.over.c.z;
+            for (int k = 0; k < 3; ++k) o[3 + 3 * k] = cp.over.ax[k].x, o[4 + 3 * k] = cp.over.ax[k].y,
+                                        o[5 + 3 * k] = cp.over.ax[k].z;
+            o[12] = cp.over.he.x, o[13] = cp.over.he.y, o[14] = cp.over.he.z;
+            std::vector<int32_t> used(nsph, 0);
+            for (const Spline& s : cp.under) {
+                const int32_t segc = std::max<int32_t>(1, static_cast<int32_t>(s.pts.size()) - 1);
+                if (segc > K) throw std::logic_error("spline exceeds the segment cap; the build policy should have split it");
+                const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
+                double& sr = L->spline_r[slot];
+                if (sr == 0.0)
+                    sr = s.radius;
+                else if (sr != s.radius)
+                    throw std::logic_error("inconsistent spline radius for a layout slot");
+                count[static_cast<size_t>(c) * S + slot] = segc;
+            }
+        }
+        int64_t total = 0;
+        for (size_t r = 0; r < count.size(); ++r) {
+            L->row_off[r] = static_cast<int32_t>(total);
+            total += count[r];
+        }
+        L->row_off[count.size()] = static_cast<int32_t>(total);
+        L->segs.resize(static_cast<size_t>(total) * 7);
+        for (int32_t c = 0; c < N; ++c) {
+            std::vector<int32_t> used(nsph, 0);
+            for (const Spline& s : comps[c].under) {
+                const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
+                double* dst = &L->segs[7 * static_cast<size_t>(L->row_off[static_cast<size_t>(c) * S + slot])];
+                if (s.pts.size() == 1) {
+                    seg_prep(s.pts[0], s.pts[0], dst);
+                } else {
+                    for (size_t p = 0; p + 1 < s.pts.size(); ++p) seg_prep(s.pts[p], s.pts[p + 1], dst + 7 * p);
+                }
+            }
+        }
+        *out = L;
+        return 0;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
+    }
+}
+
+int rgg_built_counts(const rgg_built* b, int64_t* out) {
+    if (!b || !out) return -1;
+    out[0] = b->N;
+    out[1] = b->B;
+    out[2] = b->S;
+    out[3] = static_cast<int64_t>(b->segs.size() / 7);
+    return 0;
+}
+
+int rgg_built_export(const rgg_built* b, double* edge_sat, double* comp_aabb, int32_t* row_off, double* segs,
+                     double* spline_r, double* obb15) {
+    if (!b) return -1;
+    auto cp = [](void* dst, const auto& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(edge_sat, b->edge_sat);
+    cp(comp_aabb, b->comp_aabb);
+    cp(row_off, b->row_off);
+    cp(segs, b->segs);
+    cp(spline_r, b->spline_r);
+    cp(obb15, b->obb15);
+    return 0;
+}
+
+void rgg_built_free(rgg_built* b) { delete b; }
+
+int rgg_obstacle_spheres(const double* he3, int32_t count, double* centres, double* radius) {
+    if (count < 1 || !(he3[0] > 0 && he3[1] > 0 && he3[2] > 0)) {
+        g_err = "bad obstacle sphere request";
+        return -1;
+    }
+    const std::vector<Sph> s = inner_spheres({he3[0], he3[1], he3[2]}, count);
+    for (int32_t i = 0; i < count; ++i) {
+        centres[3 * i] = s[i].c.x;
+        centres[3 * i + 1] = s[i].c.y;
+        centres[3 * i + 2] = s[i].c.z;
+    }
+    *radius = s[0].r;
+    return 0;
+}
+
+}  // extern "C"

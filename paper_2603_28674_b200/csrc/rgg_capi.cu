@@ -6,6 +6,7 @@
 // present, and every compute entry launches the kernels of rgg_kernels.cu.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -56,8 +57,9 @@ struct rgg_gpu {
     int32_t cap_moves = 0;
     int32_t* d_ids = nullptr;
     double* d_rt = nullptr;
-    int32_t* d_prev = nullptr;
     uint8_t* d_last = nullptr;
+    int32_t* d_unknown = nullptr;
+    unsigned long long* d_dbg = nullptr;
     Event* d_ev = nullptr;
     int32_t* d_mv = nullptr;
     int32_t* d_pool = nullptr;
@@ -66,8 +68,6 @@ struct rgg_gpu {
     int32_t cap_pin = 0;
     int32_t* h_ids = nullptr;
     double* h_rt = nullptr;
-    int32_t* h_prev = nullptr;
-    uint8_t* h_last = nullptr;
     int32_t* h_mv = nullptr;
     int32_t* h_ctr = nullptr;
     // host mirrors
@@ -117,14 +117,12 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     const int32_t cap = std::max(n, std::max(64, h->cap_moves * 2));
     cudaFree(h->d_ids);
     cudaFree(h->d_rt);
-    cudaFree(h->d_prev);
     cudaFree(h->d_last);
     cudaFree(h->d_ev);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
     CK(dalloc(&h->d_ids, cap));
     CK(dalloc(&h->d_rt, static_cast<size_t>(cap) * 12));
-    CK(dalloc(&h->d_prev, cap));
     CK(dalloc(&h->d_last, cap));
     CK(dalloc(&h->d_ev, cap));
     CK(dalloc(&h->d_mv, static_cast<size_t>(cap) * 4));
@@ -140,13 +138,9 @@ int grow_pinned(rgg_gpu* h, int32_t n) {
     const int32_t cap = std::max(n, std::max(64, h->cap_pin * 2));
     cudaFreeHost(h->h_ids);
     cudaFreeHost(h->h_rt);
-    cudaFreeHost(h->h_prev);
-    cudaFreeHost(h->h_last);
     cudaFreeHost(h->h_mv);
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), cap * sizeof(int32_t), 0));
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_rt), cap * 12 * sizeof(double), 0));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_prev), cap * sizeof(int32_t), 0));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_last), cap * sizeof(uint8_t), 0));
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), 0));
     h->cap_pin = cap;
     return RGG_OK;
@@ -157,7 +151,6 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.n = n;
     b.ids = h->d_ids;
     b.rt = h->d_rt;
-    b.prev = h->d_prev;
     b.last = h->d_last;
     b.ev = h->d_ev;
     b.cell_count = h->d_cell_count;
@@ -170,21 +163,61 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.mv = h->d_mv;
     b.hits = h->d_hits;
     b.census = h->d_census;
+    b.unknown = h->d_unknown;
+    static const bool dbg_timing = std::getenv("RGG_DEBUG_TIMING") != nullptr;
+    if (dbg_timing && !h->d_dbg) {
+        cudaMalloc(reinterpret_cast<void**>(&h->d_dbg), static_cast<size_t>(h->s.ncells) * 64);
+        cudaMemset(h->d_dbg, 0, static_cast<size_t>(h->s.ncells) * 64);
+    }
+    b.dbg = h->d_dbg;
     return b;
 }
 
-// Enqueue the whole pipeline for n moves already in d_ids/d_rt/d_prev/d_last.
+// Enqueue the whole pipeline for n moves already in d_ids/d_rt.
 int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     const Batch b = batch_of(h, n);
     int kf = 0;
     if (flags & RGG_PER_MOVE) kf |= rggk::kPerMove;
     if (n == 1) kf |= rggk::kHits;
+    static const bool debug = std::getenv("RGG_DEBUG_PHASES") != nullptr;
+    auto phase = [&](const char* name) -> int {
+        if (!debug) return RGG_OK;
+        CK(cudaStreamSynchronize(h->stream));
+        std::fprintf(stderr, "[rgg] %s done\n", name);
+        return RGG_OK;
+    };
     CK(cudaEventRecord(h->ev[0], h->stream));
     CK(rggk::launch_pose(h->s, b, h->stream));
+    if (phase("pose")) return RGG_ECUDA;
     CK(cudaEventRecord(h->ev[1], h->stream));
     CK(rggk::launch_bin(h->s, b, h->stream));
+    if (phase("bin")) return RGG_ECUDA;
     CK(cudaEventRecord(h->ev[2], h->stream));
     CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
+    if (phase("classify")) return RGG_ECUDA;
+    if (b.dbg) {
+        std::vector<unsigned long long> t(static_cast<size_t>(h->s.ncells) * 8);
+        CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        unsigned long long lo = ~0ull, hi = 0;
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        int n = 0, ev = 0;
+        for (int c = 0; c < h->s.ncells; ++c) {
+            const unsigned long long* d = &t[8 * c];
+            if (!d[1]) continue;
+            lo = std::min(lo, d[0]);
+            hi = std::max(hi, d[6]);
+            for (int k = 0; k < 6; ++k) acc[k] += static_cast<double>(d[k + 1] - d[k]);
+            acc[6] += static_cast<double>(d[6] - d[0]);
+            ev += static_cast<int>(d[7]);
+            ++n;
+        }
+        std::fprintf(stderr, "[rgg] cells %d events/cell %.1f span %.1f us | per cell us: fetch %.2f comp %.2f "
+                             "stage %.2f A %.2f B %.2f C+wb %.2f total %.2f\n",
+                     n, n ? double(ev) / n : 0.0, (hi - lo) * 1e-3, acc[0] / n * 1e-3, acc[1] / n * 1e-3,
+                     acc[2] / n * 1e-3, acc[3] / n * 1e-3, acc[4] / n * 1e-3, acc[5] / n * 1e-3, acc[6] / n * 1e-3);
+        CK(cudaMemsetAsync(b.dbg, 0, t.size() * 8, h->stream));
+    }
     CK(cudaEventRecord(h->ev[3], h->stream));
     CK(rggk::launch_commit(h->s, b, h->stream));
     CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
@@ -197,22 +230,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     return RGG_OK;
 }
 
-// host-side move preparation: prev / last indices per obstacle
-void link_moves(const int32_t* ids, int32_t n, int32_t m, int32_t* prev, uint8_t* last) {
-    std::vector<int32_t> seen(static_cast<size_t>(m), -1);
-    for (int32_t i = 0; i < n; ++i) {
-        prev[i] = seen[ids[i]];
-        seen[ids[i]] = i;
-        last[i] = 0;
-    }
-    for (int32_t o = 0; o < m; ++o)
-        if (seen[o] >= 0) last[seen[o]] = 1;
-}
-
 int refresh_unknown(rgg_gpu* h) {
     if (!h->unknown_stale) return RGG_OK;
     int32_t v = 0;
-    CK(cudaMemcpyAsync(&v, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(&v, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->unknown = v;
     h->unknown_stale = false;
@@ -239,7 +260,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     if (C > rggk::kMaxSpheres) return fail(h, RGG_EINVAL, "too many spheres per obstacle (max 16)");
     if (M > 0xfffe) return fail(h, RGG_EINVAL, "too many obstacles");
     const int cell = o.cell_size > 0 ? o.cell_size : 128;
-    if (cell % 32 != 0 || cell > 256) return fail(h, RGG_EINVAL, "cell_size must be a multiple of 32, <= 256");
+    if (cell % 32 != 0 || cell > rggk::kMaxCell) return fail(h, RGG_EINVAL, "cell_size must be a multiple of 32, <= 128");
     const int cap = o.cell_capacity > 0 ? o.cell_capacity : 64;
     const int shards = o.shard_count > 1 ? o.shard_count : 1;
     const int rank = shards > 1 ? o.shard_rank : 0;
@@ -369,6 +390,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_cur, M));
     CK(dalloc(&h->d_cur_union, static_cast<size_t>(M) * 6));
     CK(dalloc(&h->d_ctr, 8));
+    CK(dalloc(&h->d_unknown, 1));
     CK(dalloc(&h->d_census, 8));
     CK(dalloc(&h->d_gray, N));
     CK(dalloc(&h->d_tiles, N / 4096 + 2));
@@ -405,6 +427,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(cudaMemsetAsync(h->d_over, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
     CK(cudaMemsetAsync(h->d_under, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
     CK(cudaMemsetAsync(h->d_ctr, 0, 8 * sizeof(int32_t), h->stream));
+    CK(cudaMemsetAsync(h->d_unknown, 0, sizeof(int32_t), h->stream));
 
     Store& s = h->s;
     s.N = N;
@@ -452,11 +475,11 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     void* dev[] = {h->d_aabb, h->d_sat, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
-                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_prev, h->d_last, h->d_ev,
+                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_last, h->d_unknown, h->d_ev,
                    h->d_mv, h->d_pool};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* pin[] = {h->h_ids, h->h_rt, h->h_prev, h->h_last, h->h_mv, h->h_ctr};
+    void* pin[] = {h->h_ids, h->h_rt, h->h_mv, h->h_ctr};
     for (void* p : pin)
         if (p) cudaFreeHost(p);
     for (auto& e : h->ev)
@@ -490,21 +513,19 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
         if (rc) return rc;
         std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
         std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 12 * sizeof(double));
-        link_moves(ids, k, h->s.M, h->h_prev, h->h_last);
         CK(cudaMemcpyAsync(h->d_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
         CK(cudaMemcpyAsync(h->d_rt, h->h_rt, static_cast<size_t>(k) * 12 * sizeof(double), cudaMemcpyHostToDevice,
                            h->stream));
-        CK(cudaMemcpyAsync(h->d_prev, h->h_prev, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->d_last, h->h_last, k * sizeof(uint8_t), cudaMemcpyHostToDevice, h->stream));
         rc = enqueue(h, k, flags);
         if (rc) return rc;
         if (!(flags & RGG_ASYNC) || bad) {
             if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
                                             cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 7 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(h->h_ctr + 7, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
             if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, "overflow pool exhausted");
-            h->unknown = h->h_ctr[4];
+            h->unknown = h->h_ctr[7];
             h->unknown_stale = false;
             if (reports) {
                 float t[4] = {0, 0, 0, 0};
@@ -542,22 +563,12 @@ int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12
     if (n <= 0) return RGG_OK;
     if (!(flags & RGG_LAZY)) return fail(h, RGG_EINVAL, "only lazy updates run on device");
     CK(cudaSetDevice(h->device));
-    int rc = grow_batch(h, n);
+    const int rc = grow_batch(h, n);
     if (rc) return rc;
-    rc = grow_pinned(h, n);
-    if (rc) return rc;
-    // prev/last need the ids on the host once; device-resident scripts are
-    // usually replayed, so the link table is computed from a D2H of the ids.
-    CK(cudaMemcpyAsync(h->h_ids, d_ids, n * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    for (int32_t i = 0; i < n; ++i)
-        if (h->h_ids[i] < 0 || h->h_ids[i] >= h->s.M) return fail(h, RGG_EINVAL, "unknown obstacle id");
-    link_moves(h->h_ids, n, h->s.M, h->h_prev, h->h_last);
+    // no host round trip: ids are trusted; prev/last links are computed by the pose kernel
     CK(cudaMemcpyAsync(h->d_ids, d_ids, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaMemcpyAsync(h->d_rt, d_rt12, static_cast<size_t>(n) * 12 * sizeof(double), cudaMemcpyDeviceToDevice,
                        h->stream));
-    CK(cudaMemcpyAsync(h->d_prev, h->h_prev, n * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->d_last, h->h_last, n * sizeof(uint8_t), cudaMemcpyHostToDevice, h->stream));
     return enqueue(h, n, flags | RGG_ASYNC);
 }
 
@@ -658,6 +669,7 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
     CK(cudaMemcpyAsync(d_st, st, n, cudaMemcpyHostToDevice, h->stream));
     CK(rggk::launch_write_states(h->s, d_ids, d_st, n, h->stream));
     CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+    CK(cudaMemcpyAsync(h->d_unknown, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     cudaFree(d_ids);
     cudaFree(d_st);
@@ -776,3 +788,12 @@ int rgg_gpu_fp64_peak(int device, double* gflops) {
 }
 
 }  // extern "C"
+
+extern "C" int rgg_gpu_copy_counters(rgg_gpu* h, void* dst_device, int32_t n) {
+    if (!h || !dst_device) return RGG_EINVAL;
+    if (n > h->last_n) return fail(h, RGG_EINVAL, "more counters than moves in the last update");
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(dst_device, h->d_mv, static_cast<size_t>(n) * 4 * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                       h->stream));
+    return RGG_OK;
+}

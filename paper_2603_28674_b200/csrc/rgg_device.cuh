@@ -83,6 +83,36 @@ __device__ __forceinline__ bool sat_boxes(const double* a, const double* b, long
     return !sep;
 }
 
+// One lane's share of sat_boxes: the axes {g, g+G, ...} of the reference's
+// 15 (a.u[0..2], b.u[0..2], then a.u[i] x b.u[j] row-major).  The pair is
+// separated iff some lane finds a separating tested axis, so OR-ing the
+// lanes' results gives exactly !sat_boxes(a, b).  a/b stay in memory (global,
+// L1-cached / shared) so the axis index can be dynamic.
+__device__ __forceinline__ bool sat_separated_part(const double* a, const double* b, int g, int G) {
+    double d[3];
+    d[0] = sub(b[0], a[0]);
+    d[1] = sub(b[1], a[1]);
+    d[2] = sub(b[2], a[2]);
+    for (int ax = g; ax < 15; ax += G) {
+        double axis[3];
+        if (ax < 6) {
+            const double* u = ax < 3 ? a + 12 + 3 * ax : b + 12 + 3 * (ax - 3);
+            axis[0] = u[0];
+            axis[1] = u[1];
+            axis[2] = u[2];
+        } else {
+            const double* x = a + 12 + 3 * ((ax - 6) / 3);
+            const double* y = b + 12 + 3 * ((ax - 6) % 3);
+            axis[0] = sub(mul(x[1], y[2]), mul(x[2], y[1]));
+            axis[1] = sub(mul(x[2], y[0]), mul(x[0], y[2]));
+            axis[2] = sub(mul(x[0], y[1]), mul(x[1], y[0]));
+            if (!(dot3(axis, axis) >= 1e-12)) continue;
+        }
+        if (separated_on(a, b, d, axis)) return true;
+    }
+    return false;
+}
+
 // seg_point_dist + seg_sphere, proj/src/kernels_scalar.cpp:81-96.
 // s = SegPrep (a[3], d[3], dd).  Closed predicate.
 __device__ __forceinline__ bool seg_sphere(const double* s, const double* c, double r_total) {
@@ -98,6 +128,41 @@ __device__ __forceinline__ bool seg_sphere(const double* s, const double* c, dou
     const double qy = sub(py, mul(t, s[4]));
     const double qz = sub(pz, mul(t, s[5]));
     return __dsqrt_rn(add(add(mul(qx, qx), mul(qy, qy)), mul(qz, qz))) <= r_total;
+}
+
+// seg_sphere with an exact fast path.  Returns the same verdict as seg_sphere
+// on every input: the clamp cases t = 0 (num <= 0) and t = 1 (num >= dd)
+// produce the reference's q without the division (num/dd lands on the clamp
+// value), and sqrt_rn(x) <= r is decided from x against r*r outside a 2^-40
+// relative band (sqrt_rn is monotone and within half an ulp), so the fp64
+// division and square root run only for interior projections and for the
+// band (SURVEY.md §7 "fp32-fast + recheck" done entirely in fp64).
+__device__ __forceinline__ bool seg_sphere_fast(const double* s, const double* c, double r_total) {
+    if (!(r_total >= 0.0)) return false;  // sqrt_rn(x) >= 0 > r_total (or NaN)
+    const double px = sub(c[0], s[0]);
+    const double py = sub(c[1], s[1]);
+    const double pz = sub(c[2], s[2]);
+    double qx = px, qy = py, qz = pz;
+    if (s[6] > 0.0) {
+        const double num = add(add(mul(px, s[3]), mul(py, s[4])), mul(pz, s[5]));
+        if (!(num == num)) return false;  // NaN propagates to the reference's distance
+        if (num >= s[6]) {  // t = 1 (num/dd >= 1 is clamped, or is 1.0)
+            qx = sub(px, s[3]);
+            qy = sub(py, s[4]);
+            qz = sub(pz, s[5]);
+        } else if (num > 0.0) {  // 0 < t <= 1
+            double t = __ddiv_rn(num, s[6]);
+            t = t > 1.0 ? 1.0 : t;
+            qx = sub(px, mul(t, s[3]));
+            qy = sub(py, mul(t, s[4]));
+            qz = sub(pz, mul(t, s[5]));
+        }  // num <= 0: t = +-0 and q == p in value
+    }
+    const double x = add(add(mul(qx, qx), mul(qy, qy)), mul(qz, qz));
+    const double r2 = r_total * r_total;
+    if (x < r2 * (1.0 - 0x1p-40)) return true;
+    if (x > r2 * (1.0 + 0x1p-40)) return false;
+    return __dsqrt_rn(x) <= r_total;
 }
 
 // sat_prep, proj/src/kernels_scalar.cpp:7-30.

@@ -8,7 +8,8 @@
 namespace rggk {
 
 constexpr int kMaxSpheres = 16;  // obstacle inner spheres per event (C)
-constexpr int kEvChunk = 32;     // events staged in shared memory per pass
+constexpr int kEvChunk = 32;     // events staged in shared memory per pass (one bit each)
+constexpr int kMaxCell = 128;    // components per cell = threads per classify CTA
 
 // One obstacle move after re-posing (BatchLayout::update_transforms,
 // proj/src/batch_layout.cpp:148-172), plus the obstacle's previous union box.
@@ -58,8 +59,7 @@ struct Batch {
     int32_t n;
     const int32_t* ids;
     const double* rt;
-    const int32_t* prev;   // previous move of the same obstacle in this batch, or -1
-    const uint8_t* last;   // 1 if this is the obstacle's last move in this batch
+    uint8_t* last;         // 1 if this is the obstacle's last move in this batch (pose kernel)
     Event* ev;             // n
     int32_t* cell_count;   // ncells
     int32_t* cell_list;    // ncells*cap
@@ -72,6 +72,8 @@ struct Batch {
     int32_t* mv;           // n*4: to_green, to_red, to_gray, from_gray
     int32_t* hits;         // N: over-hit-by-last-move & still gray
     unsigned long long* census;  // 8 counters
+    int32_t* unknown;      // running GRAY count, persistent across batches
+    unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
 };
 
 enum Flags : int32_t { kPerMove = 2, kHits = 8, kCensus = 16 };

@@ -104,6 +104,7 @@ def library() -> C.CDLL:
         L.rgg_gpu_stream.argtypes = [vp]
         L.rgg_gpu_stream.restype = vp
         L.rgg_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+        L.rgg_gpu_copy_counters.argtypes = [vp, vp, i32]
         _lib = L
     return _lib
 
@@ -111,7 +112,8 @@ def library() -> C.CDLL:
 EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_update", "rgg_gpu_update_device",
             "rgg_gpu_sync", "rgg_gpu_count", "rgg_gpu_read_states", "rgg_gpu_read_bits", "rgg_gpu_unknown_count",
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
-            "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak"]
+            "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
+            "rgg_gpu_copy_counters"]
 
 
 @dataclass
@@ -278,6 +280,10 @@ class GpuEngine:
 
     def sync(self):
         self._check(library().rgg_gpu_sync(self._h))
+
+    def copy_counters(self, dst_ptr: int, n: int):
+        """Per-move counters of the last update -> device buffer (n x 4 int32), engine stream."""
+        self._check(library().rgg_gpu_copy_counters(self._h, C.c_void_p(dst_ptr), int(n)))
 
     @staticmethod
     def _moves(moves):

@@ -1,0 +1,104 @@
+"""ctypes wrapper over lib/librgg_build.so (csrc/producer.cpp): roadmap -> LayoutView.
+
+The producer is the CPU step before the hot path.  It
+follows the reference's preprocessing for a free-flying box robot so the
+synthetic workloads of BASELINE.json configs 2-5 carry the reference's shapes
+(fitted swept-volume OBBs, certified spline under-approximations).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .engine import LayoutView
+from . import synth
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "librgg_build.so")
+_lib = None
+
+
+def library():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"producer not built: {LIB_PATH} (run `python -m paper_2603_28674_b200.build`)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.rgg_build_layout.argtypes = [vp, C.c_int32, vp, C.c_int32, vp, C.c_double, C.c_int32, C.c_int32,
+                                       C.POINTER(vp)]
+        L.rgg_built_counts.argtypes = [vp, vp]
+        L.rgg_built_export.argtypes = [vp] * 7
+        L.rgg_built_free.argtypes = [vp]
+        L.rgg_built_free.restype = None
+        L.rgg_build_last_error.restype = C.c_char_p
+        L.rgg_obstacle_spheres.argtypes = [vp, C.c_int32, vp, vp]
+        _lib = L
+    return _lib
+
+
+def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False):
+    """Components (nodes first, then edges) of a free-flying box robot -> store arrays."""
+    L = library()
+    he = np.ascontiguousarray(robot_he, np.float64)
+    nodes = np.ascontiguousarray(nodes, np.float64)
+    edges = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
+    h = C.c_void_p()
+    rc = L.rgg_build_layout(he.ctypes.data, len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
+                            float(eps), int(max_segments), int(threads), C.byref(h))
+    if rc != 0:
+        raise RuntimeError(L.rgg_build_last_error().decode())
+    try:
+        cnt = np.zeros(4, np.int64)
+        L.rgg_built_counts(h, cnt.ctypes.data)
+        N, B, S, T = (int(x) for x in cnt)
+        a = dict(edge_sat=np.empty((N * B, 21)), comp_aabb=np.empty((N, 6)), row_off=np.empty(N * B * S + 1, np.int32),
+                 segs=np.empty((T, 7)), spline_r=np.empty(B * S), obb15=np.empty((N * B, 15)) if with_obbs else None)
+        L.rgg_built_export(h, *[(v.ctypes.data if v is not None else None) for v in a.values()])
+    finally:
+        L.rgg_built_free(h)
+    return N, B, S, a
+
+
+def obstacle_spheres(he, count):
+    """obstacle_inner_spheres (proj/src/swept.cpp:23-49)."""
+    cen = np.zeros((int(count), 3))
+    r = C.c_double()
+    rc = library().rgg_obstacle_spheres(np.ascontiguousarray(he, np.float64).ctypes.data, int(count),
+                                        cen.ctypes.data, C.byref(r))
+    if rc != 0:
+        raise RuntimeError(library().rgg_build_last_error().decode())
+    return cen, r.value
+
+
+def layout_for(roadmap: synth.Roadmap, obstacles: synth.Obstacles, threads=0) -> LayoutView:
+    N, B, S, a = build_layout(roadmap.robot_he, roadmap.nodes, roadmap.edges, roadmap.eps, roadmap.max_segments,
+                              threads)
+    M = len(obstacles.he)
+    Cmax = int(obstacles.spheres.max()) if M else 1
+    sl = np.zeros((M, Cmax, 3))
+    sr = np.zeros(M)
+    for o in range(M):
+        cen, r = obstacle_spheres(obstacles.he[o], obstacles.spheres[o])
+        sl[o, : len(cen)] = cen
+        sr[o] = r
+    return LayoutView(N=N, B=B, S=S, M=M, C=Cmax, edge_sat=a["edge_sat"], comp_aabb=a["comp_aabb"],
+                      row_off=a["row_off"], segs=a["segs"], spline_r=a["spline_r"],
+                      obst_he=np.ascontiguousarray(obstacles.he, np.float64), obst_sph_local=sl, obst_sph_r=sr,
+                      obst_sph_n=np.ascontiguousarray(obstacles.spheres, np.int32),
+                      meta=dict(n_nodes=len(roadmap.nodes), n_edges=len(roadmap.edges)))
+
+
+def workload(name: str, seed: int = 12345, iterations: int = 1, threads: int = 0, scale: float = 1.0):
+    """BASELINE config name ("c2".."c5") -> (LayoutView, roadmap, obstacles, ids, rt12)."""
+    kind, nodes, k, half, m, ohalf = synth.CONFIGS[name]
+    nodes = max(16, int(nodes * scale))
+    half = half * np.sqrt(scale) if kind == "se2" else half * scale ** (1 / 3)
+    ohalf = ohalf * np.sqrt(scale) if kind == "se2" else ohalf * scale ** (1 / 3)
+    rm = synth.make_roadmap(kind, nodes, k, half, seed)
+    obs = synth.make_obstacles(kind, m, seed + 1)
+    lv = layout_for(rm, obs, threads)
+    ids, rts = synth.make_moves(kind, m, iterations, ohalf, seed + 2)
+    return lv, rm, obs, ids, rts
