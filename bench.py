@@ -281,7 +281,10 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    launches_per_step = 7 + (0 if dist is None else 0)
+    launches_per_step = 7
+    # one more (untimed) update of the last step's moves with the byte census on, then the flop census
+    eng.update_device(ids_d[args.warmup + args.steps - 1].data_ptr(), rts_d[args.warmup + args.steps - 1].data_ptr(),
+                      m_step, per_move=True, census=True)
     census = eng.census()
     flops = census["sat_flops"] + 21 * census["seg_sphere_tests"]
     byts = census["bytes_components"] + m_step * 768
@@ -342,7 +345,7 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
-    roof["kernel"] = "classify_kernel (rgg_kernels.cu)"
+    roof["kernel"] = "classify_warp_kernel (paper_2603_28674_b200/csrc/rgg_kernels.cu)"
     roof["algorithmic"] = {"flops_per_launch": flops, "bytes_per_launch": byts, "classify_ms_mean": mean_classify,
                            "roof_ms": 1e3 * max(t_fl, t_by), "census": census}
     line = {

@@ -53,6 +53,8 @@ struct rgg_gpu {
     int32_t* d_cell_list = nullptr;
     int32_t* d_cell_ovf = nullptr;
     int32_t* d_dirty = nullptr;
+    int4* d_crec = nullptr;
+    long long* d_mtop = nullptr;
     // batch buffers (grown on demand)
     int32_t cap_moves = 0;
     int32_t* d_ids = nullptr;
@@ -64,6 +66,11 @@ struct rgg_gpu {
     int32_t* d_mv = nullptr;
     int32_t* d_pool = nullptr;
     int64_t pool_cap = 0;
+    uint32_t* d_mpool = nullptr;
+    int64_t mpool_cap = 0;
+    int4* d_items_over = nullptr;
+    int4* d_items_under = nullptr;
+    int32_t items_cap = 0;
     // pinned staging
     int32_t cap_pin = 0;
     int32_t* h_ids = nullptr;
@@ -79,6 +86,13 @@ struct rgg_gpu {
     int32_t unknown = 0;
     bool unknown_stale = false;
     cudaEvent_t ev[6] = {};
+    // CUDA graphs of the update pipeline, keyed by (moves, kernel flags, buffer generation)
+    struct GraphEntry {
+        int32_t n, kf, gen;
+        cudaGraphExec_t exec;
+    };
+    std::vector<GraphEntry> graphs;
+    int32_t gen = 0;
     bool timed = false;
     int grid_classify = 1;
     int64_t total_segs_owned = 0;
@@ -90,6 +104,10 @@ int fail(rgg_gpu* h, int code, const std::string& msg) {
     if (h) h->err = msg;
     return code;
 }
+
+// Entry points first drop any stale non-sticky error left by an earlier runtime
+// call, so a launcher's cudaGetLastError() reports its own launch only.
+inline void clear_stale_error() { (void)cudaGetLastError(); }
 
 #define CK(expr)                                                                                 \
     do {                                                                                         \
@@ -121,6 +139,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     cudaFree(h->d_ev);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
+    cudaFree(h->d_mpool);
     CK(dalloc(&h->d_ids, cap));
     CK(dalloc(&h->d_rt, static_cast<size_t>(cap) * 12));
     CK(dalloc(&h->d_last, cap));
@@ -129,7 +148,12 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     // every (cell, event) pair fits: the overflow pool can never run out
     h->pool_cap = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * cap);
     CK(dalloc(&h->d_pool, static_cast<size_t>(h->pool_cap)));
+    // mask words of the touch / narrow / apply kernels: 3 * ceil(L/32) per component of a listed cell
+    h->mpool_cap = std::max<int64_t>(1, 3ll * h->s.ncells * h->s.cell * ((cap + 31) / 32));
+    if (h->mpool_cap > INT32_MAX) return fail(h, RGG_ENOMEM, "batch too large for the mask pool; split it");
+    CK(dalloc(&h->d_mpool, static_cast<size_t>(h->mpool_cap)));
     h->cap_moves = cap;
+    ++h->gen;  // buffers moved: captured graphs are stale
     return RGG_OK;
 }
 
@@ -164,10 +188,18 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.hits = h->d_hits;
     b.census = h->d_census;
     b.unknown = h->d_unknown;
+    b.mpool = h->d_mpool;
+    b.mtop = h->d_mtop;
+    b.mpool_cap = h->mpool_cap;
+    b.crec = h->d_crec;
+    b.items_over = h->d_items_over;
+    b.items_under = h->d_items_under;
+    b.items_cap = h->items_cap;
     static const bool dbg_timing = std::getenv("RGG_DEBUG_TIMING") != nullptr;
+    const size_t dbg_n = static_cast<size_t>((h->s.Np + 31) / 32) * 16;
     if (dbg_timing && !h->d_dbg) {
-        cudaMalloc(reinterpret_cast<void**>(&h->d_dbg), static_cast<size_t>(h->s.ncells) * 64);
-        cudaMemset(h->d_dbg, 0, static_cast<size_t>(h->s.ncells) * 64);
+        cudaMalloc(reinterpret_cast<void**>(&h->d_dbg), dbg_n * 8);
+        cudaMemset(h->d_dbg, 0, dbg_n * 8);
     }
     b.dbg = h->d_dbg;
     return b;
@@ -175,7 +207,8 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
 
 // Enqueue the whole pipeline for n moves already in d_ids/d_rt.
 int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
-    const Batch b = batch_of(h, n);
+    Batch b = batch_of(h, n);
+    b.census_on = (flags & RGG_CENSUS) ? 1 : 0;
     int kf = 0;
     if (flags & RGG_PER_MOVE) kf |= rggk::kPerMove;
     if (n == 1) kf |= rggk::kHits;
@@ -186,6 +219,43 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         std::fprintf(stderr, "[rgg] %s done\n", name);
         return RGG_OK;
     };
+    static const bool no_graph = std::getenv("RGG_NO_GRAPH") != nullptr;
+    const bool use_graph = !debug && !b.dbg && !no_graph;
+    const int32_t key = kf | (b.census_on ? 64 : 0);
+    if (use_graph) {
+        cudaGraphExec_t exec = nullptr;
+        for (const auto& g : h->graphs)
+            if (g.n == n && g.kf == key && g.gen == h->gen) exec = g.exec;
+        if (!exec) {
+            // capture the launch sequence once (pose, bin, classify, compaction + phase events)
+            // phase events become event-record nodes (cudaEventRecordExternal), so they time the replay
+            const auto rec = [&](cudaEvent_t ev) { return cudaEventRecordWithFlags(ev, h->stream, cudaEventRecordExternal); };
+            CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = rec(h->ev[0]);
+            if (e == cudaSuccess) e = rggk::launch_pose(h->s, b, h->stream);
+            if (e == cudaSuccess) e = rec(h->ev[1]);
+            if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);
+            if (e == cudaSuccess) e = rec(h->ev[2]);
+            if (e == cudaSuccess) e = rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
+            if (e == cudaSuccess) e = rec(h->ev[3]);
+            if (e == cudaSuccess) e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
+            if (e == cudaSuccess) e = rec(h->ev[4]);
+            cudaGraph_t graph = nullptr;
+            const cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
+            CK(e);
+            CK(e2);
+            CK(cudaGraphInstantiate(&exec, graph, 0));
+            cudaGraphDestroy(graph);
+            h->graphs.push_back({n, key, h->gen, exec});
+        }
+        CK(cudaGraphLaunch(exec, h->stream));
+        h->last_n = n;
+        h->last_flags = flags;
+        h->last_hits_valid = n == 1;
+        h->timed = true;
+        h->unknown_stale = true;
+        return RGG_OK;
+    }
     CK(cudaEventRecord(h->ev[0], h->stream));
     CK(rggk::launch_pose(h->s, b, h->stream));
     if (phase("pose")) return RGG_ECUDA;
@@ -196,30 +266,31 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
     if (phase("classify")) return RGG_ECUDA;
     if (b.dbg) {
-        std::vector<unsigned long long> t(static_cast<size_t>(h->s.ncells) * 8);
+        const size_t ns = static_cast<size_t>((h->s.Np + 31) / 32);
+        std::vector<unsigned long long> t(ns * 16);
         CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        unsigned long long lo = ~0ull, hi = 0;
-        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        int n = 0, ev = 0;
-        for (int c = 0; c < h->s.ncells; ++c) {
-            const unsigned long long* d = &t[8 * c];
-            if (!d[1]) continue;
-            lo = std::min(lo, d[0]);
-            hi = std::max(hi, d[6]);
-            for (int k = 0; k < 6; ++k) acc[k] += static_cast<double>(d[k + 1] - d[k]);
-            acc[6] += static_cast<double>(d[6] - d[0]);
-            ev += static_cast<int>(d[7]);
-            ++n;
+        // sections: comp loads, staging, masks, worklist, narrow, transitions+, writes
+        double acc[2][7] = {}, cnt[2] = {0, 0}, lo = 1e300, hi = 0;
+        for (size_t q = 0; q < ns; ++q) {
+            const unsigned long long* d = &t[16 * q];
+            if (!d[0] || !d[7]) continue;
+            const int heavy = (d[9] + d[10]) > 0 ? 1 : 0;
+            for (int k = 0; k < 7; ++k) acc[heavy][k] += double(d[k + 1]) - double(d[k]);
+            cnt[heavy] += 1;
+            lo = std::min(lo, double(d[0]));
+            hi = std::max(hi, double(d[7]));
         }
-        std::fprintf(stderr, "[rgg] cells %d events/cell %.1f span %.1f us | per cell us: fetch %.2f comp %.2f "
-                             "stage %.2f A %.2f B %.2f C+wb %.2f total %.2f\n",
-                     n, n ? double(ev) / n : 0.0, (hi - lo) * 1e-3, acc[0] / n * 1e-3, acc[1] / n * 1e-3,
-                     acc[2] / n * 1e-3, acc[3] / n * 1e-3, acc[4] / n * 1e-3, acc[5] / n * 1e-3, acc[6] / n * 1e-3);
+        for (int hv = 0; hv < 2; ++hv)
+            if (cnt[hv])
+                std::fprintf(stderr, "[rgg] %s slices %5.0f us: comp %.2f stage %.2f masks %.2f list %.2f narrow %.2f "
+                                     "trans %.2f write %.2f | span %.1f\n", hv ? "narrow" : "plain ", cnt[hv],
+                             acc[hv][0] / cnt[hv] * 1e-3, acc[hv][1] / cnt[hv] * 1e-3, acc[hv][2] / cnt[hv] * 1e-3,
+                             acc[hv][3] / cnt[hv] * 1e-3, acc[hv][4] / cnt[hv] * 1e-3, acc[hv][5] / cnt[hv] * 1e-3,
+                             acc[hv][6] / cnt[hv] * 1e-3, (hi - lo) * 1e-3);
         CK(cudaMemsetAsync(b.dbg, 0, t.size() * 8, h->stream));
     }
     CK(cudaEventRecord(h->ev[3], h->stream));
-    CK(rggk::launch_commit(h->s, b, h->stream));
     CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
     CK(cudaEventRecord(h->ev[4], h->stream));
     h->last_n = n;
@@ -273,6 +344,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         if (v->row_off[r + 1] < v->row_off[r]) return fail(h, RGG_ELOGIC, "row_off must be non-decreasing");
 
     h->device = o.device;
+    clear_stale_error();
     CK(cudaSetDevice(h->device));
     cudaDeviceProp prop{};
     CK(cudaGetDeviceProperties(&prop, h->device));
@@ -389,9 +461,14 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_under, static_cast<size_t>(h->words) * Np));
     CK(dalloc(&h->d_cur, M));
     CK(dalloc(&h->d_cur_union, static_cast<size_t>(M) * 6));
-    CK(dalloc(&h->d_ctr, 8));
+    CK(dalloc(&h->d_ctr, 16));
+    CK(dalloc(&h->d_mtop, 1));
     CK(dalloc(&h->d_unknown, 1));
-    CK(dalloc(&h->d_census, 8));
+    CK(dalloc(&h->d_census, 16));
+    CK(dalloc(&h->d_crec, ncells));
+    h->items_cap = static_cast<int32_t>(std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(1 << 16, 4ll * Np)));
+    CK(dalloc(&h->d_items_over, h->items_cap));
+    CK(dalloc(&h->d_items_under, h->items_cap));
     CK(dalloc(&h->d_gray, N));
     CK(dalloc(&h->d_tiles, N / 4096 + 2));
     CK(dalloc(&h->d_hits, N));
@@ -426,7 +503,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(cudaMemsetAsync(h->d_cnt, 0, static_cast<size_t>(Np) * sizeof(uint32_t), h->stream));
     CK(cudaMemsetAsync(h->d_over, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
     CK(cudaMemsetAsync(h->d_under, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
-    CK(cudaMemsetAsync(h->d_ctr, 0, 8 * sizeof(int32_t), h->stream));
+    CK(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(int32_t), h->stream));
     CK(cudaMemsetAsync(h->d_unknown, 0, sizeof(int32_t), h->stream));
 
     Store& s = h->s;
@@ -475,13 +552,14 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     void* dev[] = {h->d_aabb, h->d_sat, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
-                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_last, h->d_unknown, h->d_ev,
+                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_last, h->d_unknown, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
                    h->d_mv, h->d_pool};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* pin[] = {h->h_ids, h->h_rt, h->h_mv, h->h_ctr};
     for (void* p : pin)
         if (p) cudaFreeHost(p);
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -491,6 +569,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
 int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
                    rgg_update_report* reports) {
     if (!h) return RGG_EINVAL;
+    clear_stale_error();
     if (n < 0 || (n > 0 && (!ids || !rt12))) return fail(h, RGG_EINVAL, "bad move list");
     if (!(flags & RGG_LAZY))
         return fail(h, RGG_EINVAL, "eager updates resolve gray components on the host: call with RGG_LAZY per move, "
@@ -524,7 +603,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
             CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 7 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaMemcpyAsync(h->h_ctr + 7, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
-            if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, "overflow pool exhausted");
+            if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, h->h_ctr[6] == 1 ? "overflow pool exhausted" : "mask pool exhausted");
             h->unknown = h->h_ctr[7];
             h->unknown_stale = false;
             if (reports) {
@@ -560,6 +639,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
 
 int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12, int32_t n, int32_t flags) {
     if (!h) return RGG_EINVAL;
+    clear_stale_error();
     if (n <= 0) return RGG_OK;
     if (!(flags & RGG_LAZY)) return fail(h, RGG_EINVAL, "only lazy updates run on device");
     CK(cudaSetDevice(h->device));
@@ -730,10 +810,9 @@ int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
     int rc = rgg_gpu_last_stats(h, out);
     if (rc) return rc;
     Batch b = batch_of(h, h->last_n);
-    CK(cudaMemsetAsync(h->d_census, 0, 8 * sizeof(unsigned long long), h->stream));
-    CK(cudaMemsetAsync(h->d_ctr + 2, 0, sizeof(int32_t), h->stream));  // work counter
+    CK(cudaMemsetAsync(h->d_census, 0, 16 * sizeof(unsigned long long), h->stream));
     CK(rggk::launch_classify(h->s, b, rggk::kCensus, h->grid_classify, h->stream));
-    unsigned long long c[8];
+    unsigned long long c[16];
     CK(cudaMemcpyAsync(c, h->d_census, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     out->over_pairs = static_cast<int64_t>(c[0]);
@@ -742,15 +821,14 @@ int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
     out->seg_sphere_tests = static_cast<int64_t>(c[3]);
     out->over_hits = static_cast<int64_t>(c[4]);
     out->under_hits = static_cast<int64_t>(c[5]);
-    const int64_t narrow = static_cast<int64_t>(c[6]), narrow_segs = static_cast<int64_t>(c[7]);
     // algorithmic bytes: every component of a dirty cell reads its AABB (48 B),
-    // label (1 B) and counters (4 B) and bit words (16 B per word); the ones
-    // with an AABB overlap also read their SatBoxes (B*168 B), row offsets and
-    // real segments (56 B each); labels/counters/bits are written back.
-    const int64_t dirty_comps = static_cast<int64_t>(std::min(out->dirty_cells * h->s.cell, h->s.Np));
-    out->bytes_components = dirty_comps * (48 + 2 * (1 + 4 + 16 * h->words)) +
-                            narrow * (static_cast<int64_t>(h->s.B) * 168 + 4 * (h->s.B * h->s.S + 1)) +
-                            narrow_segs * 56;
+    // label (1 B), counters (4 B) and bit words (16 B per word) and writes them
+    // back; components with an over item read their SatBoxes (B*168 B), those
+    // with an under item their row offsets and real segments (56 B each).
+    const int64_t dirty = static_cast<int64_t>(c[8]), box_comps = static_cast<int64_t>(c[9]),
+                  sph_comps = static_cast<int64_t>(c[10]), segs = static_cast<int64_t>(c[11]);
+    out->bytes_components = dirty * (48 + 2 * (1 + 4 + 16 * h->words)) + box_comps * h->s.B * 168 +
+                            sph_comps * 4 * (h->s.B * h->s.S + 1) + segs * 56;
     return RGG_OK;
 }
 

@@ -196,9 +196,49 @@ __device__ __forceinline__ void tf_apply(const double* rt, double x, double y, d
         out[i] = add(add(add(mul(rt[3 * i], x), mul(rt[3 * i + 1], y)), mul(rt[3 * i + 2], z)), rt[9 + i]);
 }
 
-// Aabb::overlaps, proj/include/rgg/vec3.hpp:126-129 (closed).
+// Aabb::overlaps, proj/include/rgg/vec3.hpp:126-129 (closed).  Evaluated
+// without short-circuit so all twelve operands load in parallel.
 __device__ __forceinline__ bool overlaps(const double* a, const double* b) {
-    return a[0] <= b[3] && b[0] <= a[3] && a[1] <= b[4] && b[1] <= a[4] && a[2] <= b[5] && b[2] <= a[5];
+    const double b0 = b[0], b1 = b[1], b2 = b[2], b3 = b[3], b4 = b[4], b5 = b[5];
+    return (a[0] <= b3) & (b0 <= a[3]) & (a[1] <= b4) & (b1 <= a[4]) & (a[2] <= b5) & (b2 <= a[5]);
+}
+
+// sat_boxes with every tested axis evaluated (no early exit) from register
+// operands: the 15 axis tests are independent, so their latency overlaps and
+// the critical path is one axis deep.  A degenerate cross axis (n2 < 1e-12,
+// or NaN) is masked out exactly where the reference skips it, so the verdict
+// -- "no tested axis separates" -- is bit-for-bit sat_boxes (kernels_scalar.cpp:48-69).
+__device__ __forceinline__ bool sat_boxes_flat(const double* A, const double* Bx) {
+    double a[21], b[21];
+#pragma unroll
+    for (int k = 0; k < 21; ++k) {
+        a[k] = A[k];
+        b[k] = Bx[k];
+    }
+    double d[3];
+    d[0] = sub(b[0], a[0]);
+    d[1] = sub(b[1], a[1]);
+    d[2] = sub(b[2], a[2]);
+    bool sep = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) sep |= separated_on(a, b, d, a + 12 + 3 * k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) sep |= separated_on(a, b, d, b + 12 + 3 * k);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double* x = a + 12 + 3 * i;
+            const double* y = b + 12 + 3 * j;
+            double axis[3];
+            axis[0] = sub(mul(x[1], y[2]), mul(x[2], y[1]));
+            axis[1] = sub(mul(x[2], y[0]), mul(x[0], y[2]));
+            axis[2] = sub(mul(x[0], y[1]), mul(x[1], y[0]));
+            const bool tested = dot3(axis, axis) >= 1e-12;
+            sep |= tested & separated_on(a, b, d, axis);
+        }
+    }
+    return !sep;
 }
 
 }  // namespace rggd

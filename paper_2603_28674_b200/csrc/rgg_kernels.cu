@@ -13,6 +13,7 @@
 //   commit    one thread per move: the moved obstacles' resident operands.
 //   compact   ordered ballot/prefix compaction of the GRAY component ids.
 #include <cstdio>
+#include <cstdlib>
 
 #include "rgg_device.cuh"
 #include "rgg_kernels.cuh"
@@ -125,9 +126,10 @@ __device__ __forceinline__ void box_of(const double* rt, const double* he, int c
 
 __global__ void pose_kernel(Store s, Batch b) {
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (i == 0 && lane < 8) {
+    if (i == 0 && lane < 16) {
         b.ctr[lane] = 0;
         b.census[lane] = 0;
+        if (lane == 0) *b.mtop = 0;
     }
     if (i >= b.n) return;
     const int o = b.ids[i];
@@ -369,7 +371,20 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
     }
     if (lane == 0) {
         b.cell_count[cell] = count;
-        if (count > 0) b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
+        int mbase = 0;
+        if (count > 0) {
+            b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
+            // mask block of the touch / narrow / apply kernels: 3 * ceil(count/32) words per component
+            const long long need = 3ll * ((count + 31) >> 5) * s.cell;
+            const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
+                                             static_cast<unsigned long long>(need));
+            if (base + need > b.mpool_cap) atomicExch(&b.ctr[6], 2);
+            mbase = base + need > b.mpool_cap ? 0 : static_cast<int>(base);
+        }
+        // one 16-byte record per cell: count, mask base, list address
+        const int32_t* list = count <= s.cap ? inl : b.pool + b.cell_ovf[cell];
+        const unsigned long long a = reinterpret_cast<unsigned long long>(list);
+        b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
     }
 }
 
@@ -378,6 +393,11 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
 // batch_over for one (component, obstacle) pair: any body intersects (engine_batch.cpp:55-74).
 template <bool COUNT>
 __device__ __forceinline__ bool over_test(const Store& s, int c, const double* osat, long long* cost) {
+    if (!COUNT) {
+        bool hit = false;
+        for (int b = 0; b < s.B && !hit; ++b) hit = rggd::sat_boxes_flat(s.sat + (static_cast<size_t>(c) * s.B + b) * 22, osat);
+        return hit;
+    }
     bool hit = false;
     for (int b = 0; b < s.B; ++b) {
         const double* a = s.sat + (static_cast<size_t>(c) * s.B + b) * 22;
@@ -472,277 +492,582 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// Stream a byte range towards the SM (L1) or the L2, one request per 128-byte line.
+__device__ __forceinline__ void prefetch_range(const void* a, const void* e, bool l1) {
+    const char* p = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(a) & ~uintptr_t(127));
+    for (; p < reinterpret_cast<const char*>(e); p += 128) l1 ? prefetch_l1(p) : prefetch_l2(p);
+}
+
 constexpr int kUnderLanes = 4;  // lanes per under-approximation work item
 constexpr int kOverLanes = 1;   // lanes per SAT work item (4 was slower: operands re-read per lane)
 
+// ------------------------------------------------------- v3: touch / narrow / apply
+//
+// Per cell with L listed events the bin kernel reserves a mask block of
+// 3 * ceil(L/32) * cell words: touch[w][t], over[w][t], under[w][t] (bit k of
+// word w = the cell's event at list position 32w + k, for component t of the
+// cell).  touch fills the touch words and emits one work item per (component,
+// event) pair whose boxes overlap; narrow evaluates every item with the whole
+// GPU and ORs the verdicts into the result words; apply replays each
+// component's events in move order from the three words.
+
+__device__ __forceinline__ const int32_t* rec_list(int4 r) {
+    return reinterpret_cast<const int32_t*>((static_cast<unsigned long long>(static_cast<uint32_t>(r.w)) << 32) |
+                                            static_cast<uint32_t>(r.z));
+}
+
+// Narrow tests of a pair whose item did not fit the queue (kept out of line so
+// the touch kernel's register budget stays that of an AABB filter).
+__device__ __noinline__ bool over_inline(const Store& s, int c, const double* osat) {
+    return over_test<false>(s, c, osat, nullptr);
+}
+__device__ __noinline__ bool under_inline(const Store& s, int c, const Event& ev) {
+    return under_part<false>(s, c, ev, 0, 1, nullptr);
+}
+
+// Warp-aggregated append of n items (lane-local count) to a global queue;
+// returns this lane's first slot.
+__device__ __forceinline__ int warp_reserve(int32_t* counter, int n) {
+    const int lane = threadIdx.x & 31;
+    int x = n;
+    for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, x, 31);
+    int base = 0;
+    if (lane == 31 && total) base = atomicAdd(counter, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return base + x - n;
+}
+
+__global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
+    __shared__ double sbox[kEvChunk][24];  // nu, old, box, sph of the chunk's events
+    __shared__ int sev[kEvChunk];
+    __shared__ int s_no, s_nu, s_bo, s_bu;
+    __shared__ unsigned long long scen[4];
+    const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const int4 rec = b.crec[cell];
+    const int count = rec.x;
+    if (count == 0) return;
+    const bool census = b.census_on != 0;
+    if (census && tid < 4) scen[tid] = 0;
+    const int32_t* list = rec_list(rec);
+    const int W = (count + 31) >> 5, T = s.cell;
+    const int mbase = rec.y;
+    uint32_t* mb = b.mpool + mbase;
+    const int c = cell * T + tid;
+    const bool valid = c < s.Np;
+    double aabb[6];
+    if (valid) {
+        const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
+        aabb[0] = a0.x, aabb[1] = a0.y, aabb[2] = a1.x, aabb[3] = a1.y, aabb[4] = a2.x, aabb[5] = a2.y;
+    }
+    bool any_box = false, any_sph = false;
+    for (int w = 0; w < W; ++w) {
+        const int m = min(32, count - 32 * w);
+        __syncthreads();
+        if (tid < m) sev[tid] = list[32 * w + tid];
+        if (tid == 0) s_no = s_nu = 0;
+        __syncthreads();
+        for (int t = tid; t < m * 24; t += blockDim.x) {
+            const int e = t / 24, k = t % 24;
+            const Event& ev = b.ev[sev[e]];
+            sbox[e][k] = k < 6 ? ev.nu[k] : (k < 12 ? ev.old[k - 6] : (k < 18 ? ev.box[k - 12] : ev.sph[k - 18]));
+        }
+        __syncthreads();
+        uint32_t tm = 0, bm = 0, sm = 0;
+        if (valid) {
+            for (int k = 0; k < m; ++k) {
+                if (rggd::overlaps(aabb, sbox[k]) || rggd::overlaps(aabb, sbox[k] + 6)) {
+                    tm |= 1u << k;
+                    if (rggd::overlaps(aabb, sbox[k] + 12)) bm |= 1u << k;
+                    if (s.use_under && rggd::overlaps(aabb, sbox[k] + 18)) sm |= 1u << k;
+                }
+            }
+        }
+        const int wt = mbase + (0 * W + w) * T + tid, wo = mbase + (1 * W + w) * T + tid,
+                  wu = mbase + (2 * W + w) * T + tid;
+        b.mpool[wt] = tm;
+        b.mpool[wo] = 0;
+        b.mpool[wu] = 0;
+        any_box |= bm != 0;
+        any_sph |= sm != 0;
+        // block-level reservation in the item queues: one global atomic per queue per CTA
+        const int no = __popc(bm), nu = __popc(sm);
+        int xo = no, xu = nu;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int yo = __shfl_up_sync(0xffffffffu, xo, off), yu = __shfl_up_sync(0xffffffffu, xu, off);
+            if (lane >= off) xo += yo, xu += yu;
+        }
+        int wbo = 0, wbu = 0;
+        if (lane == 31) {
+            wbo = atomicAdd(&s_no, xo);
+            wbu = atomicAdd(&s_nu, xu);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s_bo = s_no ? atomicAdd(&b.ctr[8], s_no) : 0;
+            s_bu = s_nu ? atomicAdd(&b.ctr[9], s_nu) : 0;
+        }
+        __syncthreads();
+        wbo = __shfl_sync(0xffffffffu, wbo, 31);
+        wbu = __shfl_sync(0xffffffffu, wbu, 31);
+        int at = s_bo + wbo + xo - no;
+        for (uint32_t x = bm; x; x &= x - 1, ++at) {
+            const int k = __ffs(x) - 1;
+            if (at < b.items_cap)
+                b.items_over[at] = make_int4(c, sev[k], wo, 1 << k);
+            else if (over_inline(s, c, b.ev[sev[k]].sat))
+                b.mpool[wo] |= 1u << k;  // this thread owns the word until the narrow kernel
+        }
+        at = s_bu + wbu + xu - nu;
+        for (uint32_t x = sm; x; x &= x - 1, ++at) {
+            const int k = __ffs(x) - 1;
+            if (at < b.items_cap)
+                b.items_under[at] = make_int4(c, sev[k], wu, 1 << k);
+            else if (under_inline(s, c, b.ev[sev[k]]))
+                b.mpool[wu] |= 1u << k;
+        }
+    }
+    if (census) {
+        // algorithmic-bytes census: components of dirty cells,
+        // components reading SatBoxes, components reading segments, segments read
+        int segs = 0;
+        if (valid && any_sph) {
+            const int rows = s.B * s.S;
+            segs = s.row[(c + 1) * rows] - s.row[c * rows];
+        }
+        unsigned long long v[4] = {valid ? 1ull : 0ull, any_box ? 1ull : 0ull, any_sph ? 1ull : 0ull,
+                                   static_cast<unsigned long long>(segs)};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            unsigned long long x = v[k];
+            for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+            if (lane == 0 && x) atomicAdd(&scen[k], x);
+        }
+        __syncthreads();
+        if (tid < 4 && scen[tid]) atomicAdd(&b.census[8 + tid], scen[tid]);
+    }
+}
+
+// The narrow tests of all items, GPU-wide (persistent grid).  Over items: one
+// thread each (15-axis SAT per body).  Under items: kUnderLanes lanes each.
+// CTA 0 also commits the moved obstacles' operands for the next batch.
+template <bool COUNT>
+__global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int n_over = min(b.ctr[8], b.items_cap), n_under = min(b.ctr[9], b.items_cap);
+    long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
+    for (int i = gt; i < n_over; i += nthreads) {
+        const int4 it = b.items_over[i];  // component, event, result word, bit
+        const bool h = over_test<COUNT>(s, it.x, b.ev[it.y].sat, &c_sat);
+        if (COUNT) c_op += s.B, c_oh += h;
+        if (h) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+    }
+    const int g = gt % kUnderLanes, groups = nthreads / kUnderLanes;
+    const unsigned gmask = ((1u << kUnderLanes) - 1u) << (lane & ~(kUnderLanes - 1));
+    for (int i = gt / kUnderLanes; i < n_under; i += groups) {
+        const int4 it = b.items_under[i];
+        bool h = under_part<COUNT>(s, it.x, b.ev[it.y], COUNT ? 0 : g, COUNT ? 1 : kUnderLanes, &c_tests);
+        if (!COUNT) {
+#pragma unroll
+            for (int off = 1; off < kUnderLanes; off <<= 1) {
+                const bool other = __shfl_xor_sync(gmask, h, off);  // the group's lanes share i
+                h = h || other;
+            }
+        }
+        if (COUNT) c_up += 1, c_uh += h;
+        if (h && (COUNT || g == 0)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+    }
+    if (COUNT) {
+        long long v[6] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh};
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            long long x = v[k];
+            for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+            if (lane == 0 && x) atomicAdd(&b.census[k], static_cast<unsigned long long>(x));
+        }
+        return;
+    }
+    if (blockIdx.x == 0) {
+        // commit (one warp per move): operands and union box of each obstacle's last move
+        constexpr int kVec = sizeof(Event) / 16;
+        for (int i = threadIdx.x >> 5; i < b.n; i += blockDim.x >> 5) {
+            if (!b.last[i]) continue;
+            const int o = b.ids[i];
+            const int4* src = reinterpret_cast<const int4*>(&b.ev[i]);
+            int4* dst = reinterpret_cast<int4*>(&s.cur[o]);
+            for (int k = lane; k < kVec; k += 32) dst[k] = src[k];
+            if (lane < 6) s.cur_union[6 * o + lane] = b.ev[i].nu[lane];
+        }
+    }
+}
+
+// Per-move transitions (engine_batch.cpp:114-188) of every component of a
+// dirty cell, in list (= move) order, from the touch / over / under words.
 template <int FLAGS, bool WIDE>
-__global__ void __launch_bounds__(kMaxCell, 4) classify_kernel(Store s, Batch b) {
+__global__ void __launch_bounds__(kMaxCell) apply_kernel(Store s, Batch b) {
+    constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
+    constexpr bool HITS = (FLAGS & kHits) != 0;
+    __shared__ int s_o[32], s_move[32];
+    __shared__ int scnt[32][4];
+    const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const int4 rec = b.crec[cell];
+    const int count = rec.x;
+    if (count == 0) return;
+    const int32_t* list = rec_list(rec);
+    const int W = (count + 31) >> 5, T = s.cell;
+    const uint32_t* mb = b.mpool + rec.y;
+    const int c = cell * T + tid;
+    const bool valid = c < s.Np;
+    int label = 0, oc = 0, bc = 0, id = -1;
+    unsigned long long OW = 0, UW = 0;
+    if (valid) {
+        id = s.orig[c];
+        label = s.state[id];
+        const uint32_t cw = s.cnt[c];
+        oc = cw & 0xffff;
+        bc = cw >> 16;
+        if (!WIDE) {
+            OW = s.over[c];
+            UW = s.under[c];
+        }
+    }
+    const int label0 = label;
+    const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+    const unsigned long long OW0 = OW, UW0 = UW;
+    bool hit_last = false;
+    for (int w = 0; w < W; ++w) {
+        const int m = min(32, count - 32 * w);
+        __syncthreads();
+        if (tid < m) {
+            const Event& ev = b.ev[list[32 * w + tid]];
+            s_o[tid] = ev.o;
+            s_move[tid] = ev.move;
+        }
+        if (PER_MOVE)
+            for (int t = tid; t < m * 4; t += blockDim.x) scnt[t >> 2][t & 3] = 0;
+        __syncthreads();
+        const uint32_t tm = mb[(0 * W + w) * T + tid], ro = mb[(1 * W + w) * T + tid],
+                       ru = mb[(2 * W + w) * T + tid];
+        for (int k = 0; k < m; ++k) {
+            const int before = label;
+            if (valid && ((tm >> k) & 1u)) {
+                const int o = s_o[k];
+                const int wo = o >> 6;
+                const unsigned long long bit = 1ull << (o & 63);
+                unsigned long long ow, uw;
+                if (WIDE) {
+                    ow = s.over[static_cast<size_t>(wo) * s.Np + c];
+                    uw = s.under[static_cast<size_t>(wo) * s.Np + c];
+                } else {
+                    ow = OW;
+                    uw = UW;
+                }
+                const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
+                const bool n_over = (ro >> k) & 1u, n_under = (ru >> k) & 1u;
+                // revalidate_old_intersections (engine_batch.cpp:114-143)
+                if (old_over) {
+                    oc -= 1;
+                    const int rest = bc - (old_under ? 1 : 0);
+                    label = oc == 0 ? 0 : ((s.use_under && rest > 0) ? 1 : 2);
+                }
+                // over phase (engine_batch.cpp:163-177)
+                if (n_over) {
+                    if (label == 0) label = 2;
+                    oc += 1;
+                }
+                // under phase (engine_batch.cpp:181-188)
+                if (n_under) label = 1;
+                bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
+                const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
+                const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
+                if (WIDE) {
+                    if (nw != ow) s.over[static_cast<size_t>(wo) * s.Np + c] = nw;
+                    if (nuw != uw) s.under[static_cast<size_t>(wo) * s.Np + c] = nuw;
+                } else {
+                    OW = nw;
+                    UW = nuw;
+                }
+                if (HITS && s_move[k] == b.n - 1) hit_last = n_over;
+            }
+            if (PER_MOVE) {
+                const bool ch = label != before;
+                const unsigned g = __ballot_sync(0xffffffffu, ch && label == 0);
+                const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
+                const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
+                const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
+                if (lane == 0 && (g | r | y | f)) {
+                    if (g) atomicAdd(&scnt[k][0], __popc(g));
+                    if (r) atomicAdd(&scnt[k][1], __popc(r));
+                    if (y) atomicAdd(&scnt[k][2], __popc(y));
+                    if (f) atomicAdd(&scnt[k][3], __popc(f));
+                }
+            }
+        }
+        if (PER_MOVE) {
+            __syncthreads();
+            for (int t = tid; t < m * 4; t += blockDim.x) {
+                const int v = scnt[t >> 2][t & 3];
+                if (v) atomicAdd(&b.mv[4 * s_move[t >> 2] + (t & 3)], v);
+            }
+        }
+    }
+    int dgray = 0;
+    if (valid) {
+        if (label != label0) {
+            s.state[id] = static_cast<uint8_t>(label);
+            dgray = (label == 2) - (label0 == 2);
+        }
+        const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+        if (cw != cnt0) s.cnt[c] = cw;
+        if (!WIDE) {
+            if (OW != OW0) s.over[c] = OW;
+            if (UW != UW0) s.under[c] = UW;
+        }
+    }
+    // running gray count (the unknown_count of the reference)
+    for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
+    if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
+    if (HITS) {
+        const bool h = valid && hit_last && label == 2;
+        const unsigned bal = __ballot_sync(0xffffffffu, h);
+        int pos = 0;
+        if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (h) b.hits[pos + __popc(bal & ((1u << lane) - 1u))] = id;
+    }
+}
+
+// ------------------------------------------------- v4: warp-centric fused classify
+//
+// One warp owns a slice of 32 consecutive (cell-sorted) components and runs
+// the whole per-update work of that slice warp-synchronously, with no CTA
+// barrier: its operands are loaded up front, each lane builds its touch / box /
+// sphere masks over the cell's event list (32 events per pass, boxes read as
+// warp-broadcast L1 loads), the (component, event) pairs needing a narrow test
+// become a warp-local work list that all 32 lanes drain (SATs one lane each,
+// segment-sphere tests kUnderLanes lanes each), and each lane then replays its
+// events in move order with the reference's transition.  Warps are persistent
+// and stride over the slices, so there is no dependence on CTA scheduling.
+constexpr int kWarpsPerCta = 4;
+
+template <int FLAGS, bool WIDE>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store s, Batch b) {
     constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
     constexpr bool HITS = (FLAGS & kHits) != 0;
     constexpr bool CENSUS = (FLAGS & kCensus) != 0;
-    __shared__ Event sev[kEvChunk];
-    __shared__ int scnt[kEvChunk][4];
-    __shared__ uint32_t s_over[kMaxCell], s_under[kMaxCell];
-    __shared__ uint16_t q_over[kMaxCell * kEvChunk], q_under[kMaxCell * kEvChunk];
-    __shared__ int s_wo[kMaxCell / 32], s_wu[kMaxCell / 32];
-    __shared__ int s_cell, s_no, s_nu;
-    __shared__ unsigned long long scensus[8];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    if (CENSUS && tid < 8) scensus[tid] = 0;
-    long long c_over_pairs = 0, c_sat = 0, c_under_pairs = 0, c_tests = 0, c_over_hits = 0, c_under_hits = 0,
-              c_narrow = 0, c_narrow_segs = 0;
-    unsigned long long t0 = 0;
-    for (;;) {
-        __syncthreads();
-        if (b.dbg && tid == 0) t0 = gtimer();
-        if (tid == 0) {
-            const int di = atomicAdd(&b.ctr[2], 1);
-            s_cell = di < b.ctr[0] ? b.dirty[di] : -1;
-        }
-        __syncthreads();
-        const int cell = s_cell;
-        if (cell < 0) break;
-        unsigned long long* dbg = b.dbg ? b.dbg + 8 * static_cast<size_t>(cell) : nullptr;
-        if (dbg && tid == 0) dbg[0] = t0, dbg[1] = gtimer();
-        const int count = b.cell_count[cell];
-        const int32_t* list = count <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap : b.pool + b.cell_ovf[cell];
-        const int c = cell * s.cell + tid;
+    __shared__ uint16_t sitem[kWarpsPerCta][2][32 * 32];
+    __shared__ uint32_t sres[kWarpsPerCta][2][32];
+    __shared__ int sev[kWarpsPerCta][32];
+    __shared__ double sbx[kWarpsPerCta][32][24];  // per event: nu, old, box, sph (one load wave per chunk)
+    __shared__ int2 som[kWarpsPerCta][32];        // per event: obstacle id, move index
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nslices = (s.Np + 31) >> 5;
+    long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
+    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0;
+    int dgray = 0;
+    for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
+        const int c0 = q << 5;
+        const int cell = c0 / s.cell;
+        const int4 rec = b.crec[cell];
+        const int count = rec.x;
+        if (count == 0) continue;  // warp-uniform: clean cell
+        const int c = c0 + lane;
         const bool valid = c < s.Np;
+        const int rows = s.B * s.S;
+        int seg_lo = 0, seg_hi = 0;
         double aabb[6];
         int label = 0, oc = 0, bc = 0, id = -1;
         unsigned long long OW = 0, UW = 0;
         if (valid) {
+            seg_lo = s.row[c * rows];
+            seg_hi = s.row[(c + 1) * rows];
             const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
             aabb[0] = a0.x, aabb[1] = a0.y, aabb[2] = a1.x, aabb[3] = a1.y, aabb[4] = a2.x, aabb[5] = a2.y;
-            id = s.orig[c];
-            label = s.state[id];
-            const uint32_t cw = s.cnt[c];
-            oc = cw & 0xffff;
-            bc = cw >> 16;
-            if (!WIDE) {
-                OW = s.over[c];
-                UW = s.under[c];
+            if (!CENSUS) {
+                id = s.orig[c];
+                const uint32_t cw = s.cnt[c];
+                oc = cw & 0xffff;
+                bc = cw >> 16;
+                if (!WIDE) {
+                    OW = s.over[c];
+                    UW = s.under[c];
+                }
+                label = s.state[id];
             }
         }
         const int label0 = label;
         const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
         const unsigned long long OW0 = OW, UW0 = UW;
-        bool hit_last = false, narrow_any = false;
-        if (dbg) {
-            __syncthreads();
-            if (tid == 0) dbg[2] = gtimer(), dbg[7] = count;
-        }
-        int dgray = 0;
-        for (int base = 0; base < count; base += kEvChunk) {
-            const int m = min(kEvChunk, count - base);
-            __syncthreads();
-            {
-                constexpr int kVec = sizeof(Event) / 16;
-                for (int t = tid; t < m * kVec; t += blockDim.x) {
-                    const int e = t / kVec, k = t % kVec;
-                    reinterpret_cast<int4*>(&sev[e])[k] = reinterpret_cast<const int4*>(&b.ev[list[base + e]])[k];
-                }
-                if (PER_MOVE)
-                    for (int t = tid; t < m * 4; t += blockDim.x) scnt[t >> 2][t & 3] = 0;
+        bool hit_last = false, any_box = false, any_sph = false;
+        unsigned long long* dbg = b.dbg ? b.dbg + 16 * static_cast<size_t>(q) : nullptr;
+        const long long clk0 = clock64();
+        if (dbg && lane == 0) dbg[0] = gtimer(), dbg[8] = count;
+#define RGG_STAMP(i) if (dbg) { __syncwarp(); if (lane == 0) dbg[i] = gtimer(); }
+        if (dbg && __any_sync(0xffffffffu, label == 77)) dbg[14] = 1;  // waits for the component loads
+        RGG_STAMP(1)
+        const int32_t* list = rec_list(rec);
+        for (int base = 0; base < count; base += 32) {
+            const int m = min(32, count - base);
+            const int myev = lane < m ? list[base + lane] : 0;
+            sev[wi][lane] = myev;
+            if (lane < m) {  // lane k stages event k: one load wave for the whole chunk
+                const Event& ev = b.ev[myev];
+                double v[24];
+#pragma unroll
+                for (int j = 0; j < 6; ++j) v[j] = ev.nu[j], v[6 + j] = ev.old[j], v[12 + j] = ev.box[j], v[18 + j] = ev.sph[j];
+#pragma unroll
+                for (int j = 0; j < 24; ++j) sbx[wi][lane][j] = v[j];
+                som[wi][lane] = make_int2(ev.o, ev.move);
             }
-            __syncthreads();
-            if (dbg && tid == 0 && base == 0) dbg[3] = gtimer();
-            // ---- A: overlap masks
+            __syncwarp();
+            if (base == 0) {
+                if (dbg && __any_sync(0xffffffffu, valid && aabb[0] == -1.25e300)) dbg[15] = 1;  // waits for the AABB
+                RGG_STAMP(2)
+            }
+            // ---- touch / box / sphere masks
             uint32_t tm = 0, bm = 0, sm = 0;
             if (valid) {
                 for (int k = 0; k < m; ++k) {
-                    const Event& ev = sev[k];
-                    if (rggd::overlaps(aabb, ev.nu) || rggd::overlaps(aabb, ev.old)) {
-                        tm |= 1u << k;
-                        if (rggd::overlaps(aabb, ev.box)) bm |= 1u << k;
-                        if (s.use_under && rggd::overlaps(aabb, ev.sph)) sm |= 1u << k;
-                    }
+                    const double* bx = sbx[wi][k];
+                    const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
+                    tm |= static_cast<uint32_t>(touch) << k;
+                    bm |= static_cast<uint32_t>(touch & rggd::overlaps(aabb, bx + 12)) << k;
+                    sm |= static_cast<uint32_t>(touch & (s.use_under != 0) & rggd::overlaps(aabb, bx + 18)) << k;
                 }
             }
-            narrow_any = narrow_any || (bm | sm) != 0;
-            if (bm) {
-                const char* a = reinterpret_cast<const char*>(s.sat + static_cast<size_t>(c) * s.B * 22);
-                for (int off = 0; off < s.B * 176; off += 128) prefetch_l2(a + off);
-            }
-            if (sm) {
-                const int rows = s.B * s.S;
-                const char* a = reinterpret_cast<const char*>(s.seg + 8 * static_cast<size_t>(s.row[c * rows]));
-                const char* e = reinterpret_cast<const char*>(s.seg + 8 * static_cast<size_t>(s.row[(c + 1) * rows]));
-                for (; a < e; a += 128) prefetch_l2(a);
-            }
-            s_over[tid] = 0;
-            s_under[tid] = 0;
-            // block-exclusive offsets of the work items
+            any_box |= bm != 0;
+            any_sph |= sm != 0;
+            if (base == 0) RGG_STAMP(3)
+            // ---- warp-local narrow work list
             const int no = __popc(bm), nu = __popc(sm);
             int xo = no, xu = nu;
             for (int off = 1; off < 32; off <<= 1) {
                 const int yo = __shfl_up_sync(0xffffffffu, xo, off), yu = __shfl_up_sync(0xffffffffu, xu, off);
                 if (lane >= off) xo += yo, xu += yu;
             }
-            if (lane == 31) s_wo[warp] = xo, s_wu[warp] = xu;
-            __syncthreads();
-            if (tid == 0) {
-                int ao = 0, au = 0;
-                for (int w = 0; w < nwarps; ++w) {
-                    const int to = s_wo[w], tu = s_wu[w];
-                    s_wo[w] = ao, s_wu[w] = au;
-                    ao += to, au += tu;
-                }
-                s_no = ao;
-                s_nu = au;
-            }
-            __syncthreads();
+            const int tot_o = __shfl_sync(0xffffffffu, xo, 31), tot_u = __shfl_sync(0xffffffffu, xu, 31);
             {
-                int po = s_wo[warp] + xo - no, pu = s_wu[warp] + xu - nu;
-                for (uint32_t x = bm; x; x &= x - 1) q_over[po++] = static_cast<uint16_t>((tid << 5) | (__ffs(x) - 1));
-                for (uint32_t x = sm; x; x &= x - 1) q_under[pu++] = static_cast<uint16_t>((tid << 5) | (__ffs(x) - 1));
+                int po = xo - no, pu = xu - nu;
+                for (uint32_t x = bm; x; x &= x - 1) sitem[wi][0][po++] = static_cast<uint16_t>((lane << 5) | (__ffs(x) - 1));
+                for (uint32_t x = sm; x; x &= x - 1) sitem[wi][1][pu++] = static_cast<uint16_t>((lane << 5) | (__ffs(x) - 1));
             }
-            __syncthreads();
-            if (dbg && tid == 0 && base == 0) dbg[4] = gtimer();
-            // ---- B: narrow tests spread over the CTA
-            const int n_over_items = s_no, n_under_items = s_nu;
-            if (CENSUS) {
-                for (int i = tid; i < n_over_items; i += blockDim.x) {
-                    const int it = q_over[i], t = it >> 5, k = it & 31;
-                    const bool h = over_test<true>(s, cell * s.cell + t, sev[k].sat, &c_sat);
-                    c_over_pairs += s.B, c_over_hits += h;
-                    if (h) atomicOr(&s_over[t], 1u << k);
-                }
-            } else {
-                // over items on groups of kOverLanes lanes: the 15 axes split across the group
-                const int g = tid % kOverLanes, groups = blockDim.x / kOverLanes;
-                const unsigned gmask = ((1u << kOverLanes) - 1u) << (lane & ~(kOverLanes - 1));
-                for (int ob = 0; ob < n_over_items; ob += groups) {
-                    const int i = ob + tid / kOverLanes;
-                    bool sep_all = true;  // over any body: hit iff some body is not separated
-                    int t = 0, k = 0;
-                    if (i < n_over_items) {
-                        const int it = q_over[i];
-                        t = it >> 5;
-                        k = it & 31;
-                        const double* osat = sev[k].sat;
-                        const int c = cell * s.cell + t;
-                        for (int bb = 0; bb < s.B; ++bb) {
-                            bool sep = rggd::sat_separated_part(s.sat + (static_cast<size_t>(c) * s.B + bb) * 22, osat, g,
-                                                                kOverLanes);
-#pragma unroll
-                            for (int off = 1; off < kOverLanes; off <<= 1) {
-                                const bool other = __shfl_xor_sync(gmask, sep, off);  // the group's 4 lanes
-                                sep = sep || other;
-                            }
-                            if (!sep) {
-                                sep_all = false;
-                                break;
-                            }
-                        }
-                    }
-                    if (i < n_over_items && g == 0 && !sep_all) atomicOr(&s_over[t], 1u << k);
-                }
+            sres[wi][0][lane] = 0;
+            sres[wi][1][lane] = 0;
+            __syncwarp();
+            if (base == 0) RGG_STAMP(4)
+            for (int i = lane; i < tot_o; i += 32) {
+                const int it = sitem[wi][0][i], t = it >> 5, k = it & 31;
+                const bool h = over_test<CENSUS>(s, c0 + t, b.ev[sev[wi][k]].sat, &c_sat);
+                if (CENSUS) c_op += s.B, c_oh += h;
+                if (h) atomicOr(&sres[wi][0][t], 1u << k);
             }
-            {
-                // under items on groups of kUnderLanes lanes, taken from the top
-                // thread index down so they overlap the over items above
-                const int rt = blockDim.x - 1 - tid, g = rt % kUnderLanes, groups = blockDim.x / kUnderLanes;
-                for (int ub = 0; ub < n_under_items; ub += groups) {
-                    const int i = ub + rt / kUnderLanes;
-                    bool h = false;
-                    int t = 0, k = 0;
-                    if (i < n_under_items) {
-                        const int it = q_under[i];
-                        t = it >> 5;
-                        k = it & 31;
-                        h = under_part<CENSUS>(s, cell * s.cell + t, sev[k], g, kUnderLanes, &c_tests);
-                    }
+            const int g = lane % kUnderLanes;
+            for (int ub = 0; ub < tot_u; ub += 32 / kUnderLanes) {
+                const int i = ub + lane / kUnderLanes;
+                bool h = false;
+                int t = 0, k = 0;
+                if (i < tot_u) {
+                    const int it = sitem[wi][1][i];
+                    t = it >> 5;
+                    k = it & 31;
+                    h = under_part<CENSUS>(s, c0 + t, b.ev[sev[wi][k]], CENSUS ? 0 : g, CENSUS ? 1 : kUnderLanes,
+                                           &c_tests);
+                }
+                if (!CENSUS) {
 #pragma unroll
                     for (int off = 1; off < kUnderLanes; off <<= 1) {
-                        const bool other = __shfl_xor_sync(0xffffffffu, h, off);  // every lane must shuffle
+                        const bool other = __shfl_xor_sync(0xffffffffu, h, off);  // every lane shuffles
                         h = h || other;
                     }
-                    if (i < n_under_items && g == 0) {
-                        if (CENSUS) c_under_pairs += 1, c_under_hits += h;
-                        if (h) atomicOr(&s_under[t], 1u << k);
-                    }
+                }
+                if (i < tot_u && (CENSUS || g == 0)) {
+                    if (CENSUS) c_up += 1, c_uh += h;
+                    if (h) atomicOr(&sres[wi][1][t], 1u << k);
                 }
             }
-            __syncthreads();
-            if (dbg && tid == 0 && base == 0) dbg[5] = gtimer();
+            __syncwarp();
+            if (base == 0) RGG_STAMP(5)
+            if (dbg && lane == 0 && base == 0) dbg[9] = tot_o, dbg[10] = tot_u;
             if (CENSUS) continue;
-            // ---- C: transitions in move order
-            const uint32_t ro = s_over[tid], ru = s_under[tid];
+            // ---- transitions in move order (engine_batch.cpp:114-188)
+            const uint32_t ro = sres[wi][0][lane], ru = sres[wi][1][lane];
             for (int k = 0; k < m; ++k) {
                 const int before = label;
+                const int2 om = som[wi][k];
                 if ((tm >> k) & 1u) {
-                    const Event& ev = sev[k];
-                    const int w = ev.o >> 6;
-                    const unsigned long long bit = 1ull << (ev.o & 63);
+                    const int o = om.x;
+                    const int wo = o >> 6;
+                    const unsigned long long bit = 1ull << (o & 63);
                     unsigned long long ow, uw;
                     if (WIDE) {
-                        ow = s.over[static_cast<size_t>(w) * s.Np + c];
-                        uw = s.under[static_cast<size_t>(w) * s.Np + c];
+                        ow = s.over[static_cast<size_t>(wo) * s.Np + c];
+                        uw = s.under[static_cast<size_t>(wo) * s.Np + c];
                     } else {
                         ow = OW;
                         uw = UW;
                     }
                     const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
                     const bool n_over = (ro >> k) & 1u, n_under = (ru >> k) & 1u;
-                    // revalidate_old_intersections (engine_batch.cpp:114-143)
-                    if (old_over) {
+                    if (old_over) {  // revalidate_old_intersections (engine_batch.cpp:114-143)
                         oc -= 1;
                         const int rest = bc - (old_under ? 1 : 0);
                         label = oc == 0 ? 0 : ((s.use_under && rest > 0) ? 1 : 2);
                     }
-                    // over phase (engine_batch.cpp:163-177)
-                    if (n_over) {
+                    if (n_over) {  // over phase (engine_batch.cpp:163-177)
                         if (label == 0) label = 2;
                         oc += 1;
                     }
-                    // under phase (engine_batch.cpp:181-188)
-                    if (n_under) label = 1;
+                    if (n_under) label = 1;  // under phase (engine_batch.cpp:181-188)
                     bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
                     const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
                     const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
                     if (WIDE) {
-                        if (nw != ow) s.over[static_cast<size_t>(w) * s.Np + c] = nw;
-                        if (nuw != uw) s.under[static_cast<size_t>(w) * s.Np + c] = nuw;
+                        if (nw != ow) s.over[static_cast<size_t>(wo) * s.Np + c] = nw;
+                        if (nuw != uw) s.under[static_cast<size_t>(wo) * s.Np + c] = nuw;
                     } else {
                         OW = nw;
                         UW = nuw;
                     }
-                    if (HITS && ev.move == b.n - 1) hit_last = n_over;
+                    if (HITS && om.y == b.n - 1) hit_last = n_over;
                 }
                 if (PER_MOVE) {
                     const bool ch = label != before;
-                    const unsigned g = __ballot_sync(0xffffffffu, ch && label == 0);
+                    const unsigned gg = __ballot_sync(0xffffffffu, ch && label == 0);
                     const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
                     const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
                     const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
-                    if (lane == 0 && (g | r | y | f)) {
-                        if (g) atomicAdd(&scnt[k][0], __popc(g));
-                        if (r) atomicAdd(&scnt[k][1], __popc(r));
-                        if (y) atomicAdd(&scnt[k][2], __popc(y));
-                        if (f) atomicAdd(&scnt[k][3], __popc(f));
+                    if (lane == 0 && (gg | r | y | f)) {
+                        int* mv = b.mv + 4 * om.y;
+                        if (gg) atomicAdd(mv + 0, __popc(gg));
+                        if (r) atomicAdd(mv + 1, __popc(r));
+                        if (y) atomicAdd(mv + 2, __popc(y));
+                        if (f) atomicAdd(mv + 3, __popc(f));
                     }
                 }
             }
-            if (PER_MOVE) {
-                __syncthreads();
-                for (int t = tid; t < m * 4; t += blockDim.x) {
-                    const int v = scnt[t >> 2][t & 3];
-                    if (v) atomicAdd(&b.mv[4 * sev[t >> 2].move + (t & 3)], v);
-                }
-            }
         }
+        if (dbg && !CENSUS) RGG_STAMP(6)
         if (CENSUS) {
-            if (narrow_any && valid) {
-                c_narrow += 1;
-                c_narrow_segs += s.row[(c + 1) * s.B * s.S] - s.row[c * s.B * s.S];
+            if (valid) {
+                c_dirty += 1;
+                c_box += any_box;
+                c_sph += any_sph;
+                if (any_sph) c_segs += seg_hi - seg_lo;
             }
             continue;
         }
         if (valid) {
             if (label != label0) {
                 s.state[id] = static_cast<uint8_t>(label);
-                dgray = (label == 2) - (label0 == 2);
+                dgray += (label == 2) - (label0 == 2);
             }
             const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
             if (cw != cnt0) s.cnt[c] = cw;
@@ -751,13 +1076,6 @@ __global__ void __launch_bounds__(kMaxCell, 4) classify_kernel(Store s, Batch b)
                 if (UW != UW0) s.under[c] = UW;
             }
         }
-        if (dbg) {
-            __syncthreads();
-            if (tid == 0) dbg[6] = gtimer();
-        }
-        // running gray count (the unknown_count of the reference)
-        for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
-        if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
         if (HITS) {
             const bool h = valid && hit_last && label == 2;
             const unsigned bal = __ballot_sync(0xffffffffu, h);
@@ -766,31 +1084,40 @@ __global__ void __launch_bounds__(kMaxCell, 4) classify_kernel(Store s, Batch b)
             pos = __shfl_sync(0xffffffffu, pos, 0);
             if (h) b.hits[pos + __popc(bal & ((1u << lane) - 1u))] = id;
         }
+        if (dbg) {
+            __syncwarp();
+            if (lane == 0) dbg[7] = gtimer(), dbg[11] = static_cast<unsigned long long>(clock64() - clk0);
+        }
     }
     if (CENSUS) {
-        long long v[8] = {c_over_pairs, c_sat, c_under_pairs, c_tests, c_over_hits, c_under_hits, c_narrow,
-                          c_narrow_segs};
+        long long v[10] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh, 0, 0, 0, 0};
+        v[6] = static_cast<long long>(c_dirty);
+        v[7] = static_cast<long long>(c_box);
+        v[8] = static_cast<long long>(c_sph);
+        v[9] = static_cast<long long>(c_segs);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < 10; ++k) {
             long long x = v[k];
             for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-            if (lane == 0 && x) atomicAdd(&scensus[k], static_cast<unsigned long long>(x));
+            if (lane == 0 && x) atomicAdd(&b.census[k < 6 ? k : k + 2], static_cast<unsigned long long>(x));
         }
-        __syncthreads();
-        if (tid < 8 && scensus[tid]) atomicAdd(&b.census[tid], scensus[tid]);
+        return;
     }
-}
-
-// Commit the moved obstacles' operands (one warp per move, 16-byte lanes).
-__global__ void commit_kernel(Store s, Batch b) {
-    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-    if (i >= b.n || !b.last[i]) return;
-    const int o = b.ids[i];
-    constexpr int kVec = sizeof(Event) / 16;
-    const int4* src = reinterpret_cast<const int4*>(&b.ev[i]);
-    int4* dst = reinterpret_cast<int4*>(&s.cur[o]);
-    for (int k = lane; k < kVec; k += 32) dst[k] = src[k];
-    if (lane < 6) s.cur_union[6 * o + lane] = b.ev[i].nu[lane];
+    // running gray count (the unknown_count of the reference)
+    for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
+    if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
+    // commit the moved obstacles' operands (CTA 0, one warp per move)
+    if (blockIdx.x == 0) {
+        constexpr int kVec = sizeof(Event) / 16;
+        for (int i = wi; i < b.n; i += kWarpsPerCta) {
+            if (!b.last[i]) continue;
+            const int o = b.ids[i];
+            const int4* src = reinterpret_cast<const int4*>(&b.ev[i]);
+            int4* dst = reinterpret_cast<int4*>(&s.cur[o]);
+            for (int k = lane; k < kVec; k += 32) dst[k] = src[k];
+            if (lane < 6) s.cur_union[6 * o + lane] = b.ev[i].nu[lane];
+        }
+    }
 }
 
 // --------------------------------------------------------------- compaction
@@ -947,44 +1274,79 @@ cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
 }
 
 template <int F, bool W>
-static cudaError_t classify_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {
-    classify_kernel<F, W><<<grid, s.cell, 0, st>>>(s, b);
+static cudaError_t apply_t(const Store& s, const Batch& b, cudaStream_t st) {
+    apply_kernel<F, W><<<s.ncells, s.cell, 0, st>>>(s, b);
     return cudaGetLastError();
+}
+
+static int grid_warp(const Store& s) {
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, classify_warp_kernel<kPerMove, false>, 32 * kWarpsPerCta, 0);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        per_sm = per_sm < 1 ? 1 : per_sm;
+    }
+    const int slices = (s.Np + 31) / 32;
+    const int need = (slices + kWarpsPerCta - 1) / kWarpsPerCta;
+    return need < per_sm * sms ? (need < 1 ? 1 : need) : per_sm * sms;
+}
+
+template <int F, bool W>
+static cudaError_t warp_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {
+    classify_warp_kernel<F, W><<<grid, 32 * kWarpsPerCta, 0, st>>>(s, b);
+    return cudaGetLastError();
+}
+
+static int pipeline() {
+    static const int p = [] {
+        const char* e = std::getenv("RGG_PIPELINE");
+        return e ? std::atoi(e) : 4;
+    }();
+    return p;
 }
 
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st) {
-    const bool wide = s.W > 1;
-    const int f = flags & (kPerMove | kHits | kCensus);
-#define RGG_CASE(F)                                                           \
-    case F:                                                                   \
-        return wide ? classify_t<F, true>(s, b, grid, st) : classify_t<F, false>(s, b, grid, st);
-    switch (f) {
-        RGG_CASE(0)
-        RGG_CASE(kPerMove)
-        RGG_CASE(kHits)
-        RGG_CASE(kPerMove | kHits)
-        case kCensus:
-        case kCensus | kPerMove:
-        case kCensus | kHits:
-        case kCensus | kPerMove | kHits:
-            return wide ? classify_t<kCensus, true>(s, b, grid, st) : classify_t<kCensus, false>(s, b, grid, st);
+    if (s.ncells == 0) return cudaSuccess;
+    if (pipeline() == 4) {
+        const int g = grid_warp(s);
+        const bool wide = s.W > 1;
+        if (flags & kCensus) return wide ? warp_t<kCensus, true>(s, b, g, st) : warp_t<kCensus, false>(s, b, g, st);
+        switch (flags & (kPerMove | kHits)) {
+            case 0:
+                return wide ? warp_t<0, true>(s, b, g, st) : warp_t<0, false>(s, b, g, st);
+            case kPerMove:
+                return wide ? warp_t<kPerMove, true>(s, b, g, st) : warp_t<kPerMove, false>(s, b, g, st);
+            case kHits:
+                return wide ? warp_t<kHits, true>(s, b, g, st) : warp_t<kHits, false>(s, b, g, st);
+            default:
+                return wide ? warp_t<kPerMove | kHits, true>(s, b, g, st) : warp_t<kPerMove | kHits, false>(s, b, g, st);
+        }
     }
-#undef RGG_CASE
-    return cudaErrorInvalidValue;
+    if (flags & kCensus) {
+        narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
+        return cudaGetLastError();
+    }
+    touch_kernel<<<s.ncells, s.cell, 0, st>>>(s, b);
+    narrow_kernel<false><<<grid, 128, 0, st>>>(s, b);
+    const bool wide = s.W > 1;
+    switch (flags & (kPerMove | kHits)) {
+        case 0:
+            return wide ? apply_t<0, true>(s, b, st) : apply_t<0, false>(s, b, st);
+        case kPerMove:
+            return wide ? apply_t<kPerMove, true>(s, b, st) : apply_t<kPerMove, false>(s, b, st);
+        case kHits:
+            return wide ? apply_t<kHits, true>(s, b, st) : apply_t<kHits, false>(s, b, st);
+        default:
+            return wide ? apply_t<kPerMove | kHits, true>(s, b, st) : apply_t<kPerMove | kHits, false>(s, b, st);
+    }
 }
 
-int classify_occupancy(int cell, int flags) {
+int classify_occupancy(int, int) {
     int n = 0;
-    if (flags & kCensus)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, classify_kernel<kCensus, false>, cell, 0);
-    else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, classify_kernel<kPerMove, false>, cell, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_kernel<false>, 128, 0);
     return n < 1 ? 1 : n;
-}
-
-cudaError_t launch_commit(const Store& s, const Batch& b, cudaStream_t st) {
-    commit_kernel<<<(b.n + 3) / 4, 128, 0, st>>>(s, b);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st) {

@@ -67,11 +67,19 @@ struct Batch {
     int32_t* pool;         // overflow pool (capacity pool_cap)
     int32_t pool_cap;
     int32_t* ctr;          // [0] dirty count, [1] pool top, [2] work counter, [3] overflow cells,
-                           // [4] gray count, [5] hits count, [6] error flag
+                           // [4] gray count, [5] hits count, [6] error flag, [8] over items, [9] under items
     int32_t* dirty;        // ncells
     int32_t* mv;           // n*4: to_green, to_red, to_gray, from_gray
     int32_t* hits;         // N: over-hit-by-last-move & still gray
-    unsigned long long* census;  // 8 counters
+    unsigned long long* census;  // 16 counters: [0..5] narrow census, [8..11] touch census
+    uint32_t* mpool;             // touch / over / under mask words (see touch_kernel)
+    long long* mtop;             // next free word of mpool
+    long long mpool_cap;
+    int4* crec;                  // ncells: {count, mask base word, list address lo, hi} (bin kernel)
+    int4* items_over;            // {component, event, result word, bit}: pairs needing a SAT
+    int4* items_under;           // same for the segment-sphere test
+    int32_t items_cap;
+    int32_t census_on;           // touch accumulates the byte census
     int32_t* unknown;      // running GRAY count, persistent across batches
     unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
 };
@@ -81,7 +89,6 @@ enum Flags : int32_t { kPerMove = 2, kHits = 8, kCensus = 16 };
 cudaError_t launch_pose(const Store& s, const Batch& b, cudaStream_t st);
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st);
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st);
-cudaError_t launch_commit(const Store& s, const Batch& b, cudaStream_t st);
 cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st);
 cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st);
 cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, const int32_t* cand, int n, int o,

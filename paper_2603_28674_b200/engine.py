@@ -35,7 +35,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "librgg_gpu.so")
 
 RGG_OK, RGG_EINVAL, RGG_ECUDA, RGG_ENCCL, RGG_ENOMEM, RGG_ELOGIC = 0, 1, 2, 3, 4, 5
-RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC = 1, 2, 4
+RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC, RGG_CENSUS = 1, 2, 4, 8
 GREEN, RED, GRAY = 0, 1, 2
 
 
@@ -274,8 +274,8 @@ class GpuEngine:
         self._check(library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, len(ids),
                                              RGG_LAZY | RGG_ASYNC, None))
 
-    def update_device(self, d_ids_ptr: int, d_rt_ptr: int, n: int, per_move: bool = False):
-        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0)
+    def update_device(self, d_ids_ptr: int, d_rt_ptr: int, n: int, per_move: bool = False, census: bool = False):
+        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0) | (RGG_CENSUS if census else 0)
         self._check(library().rgg_gpu_update_device(self._h, C.c_void_p(d_ids_ptr), C.c_void_p(d_rt_ptr), n, flags))
 
     def sync(self):
@@ -361,6 +361,8 @@ class GpuEngine:
         return s.as_dict()
 
     def census(self) -> dict:
+        """Algorithmic census of the last update (flops of its narrow tests; bytes
+        when that update ran with census=True)."""
         s = Stats()
         self._check(library().rgg_gpu_census(self._h, C.byref(s)))
         return s.as_dict()
