@@ -1,0 +1,251 @@
+// engine_gpu.hpp — rgg::GpuEngine: the B200 drop-in for rgg::BatchEngine.
+//
+// Same public surface as the reference's update API
+//   class rgg::BatchEngine    proj/include/rgg/engine_batch.hpp:17-63
+// (constructor over ComponentSet + Scene&, update_obstacle, batch_update,
+// resolve_all_unknown, states, obstacle_bits, unknown_count, layout,
+// batch_over, batch_under), header-only over the C-ABI of include/rgg_gpu.h
+// (link paper_2603_28674_b200/lib/librgg_gpu.so).  A maintainer compiles it
+// against the reference's own headers; see INTEGRATION.md.
+//
+// Semantics kept from the reference:
+//  * the engine keeps a non-owning pointer to the ComponentSet and mutates
+//    Scene& (obstacles[o].pose, .active) on every move (engine_batch.cpp:156-158);
+//  * std::invalid_argument("unknown obstacle id") / ("obstacle bitsets support at
+//    most 64 obstacles") are thrown with the reference's texts;
+//  * lazy updates are resolved entirely on the GPU; eager updates resolve the
+//    GRAY over-hits of each move with the reference's exact_component_valid on
+//    the host (roadmap.cpp:129-163) and write the labels back, move by move.
+// Not provided: grid() (the GPU engine has no SpatialGrid; its cells are the
+// cell-sorted component blocks of rgg_gpu_create).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rgg/batch_layout.hpp"
+#include "rgg/roadmap.hpp"
+#include "rgg/update_report.hpp"
+#include "rgg_gpu.h"
+
+namespace rgg {
+
+class GpuEngine {
+public:
+    GpuEngine(const ComponentSet& components, Scene& scene, EngineOptions options = {}, int cell_capacity = 1024,
+              int device = 0, bool allow_wide = false)
+        : components_(&components), scene_(scene), options_(options),
+          layout_(BatchLayout::serialize(components, scene.obstacles)) {
+        if (scene.obstacles.size() > 64 && !allow_wide)
+            throw std::invalid_argument("obstacle bitsets support at most 64 obstacles");
+        // CSR view of the padded layout: real segments only (seg_count per row)
+        const size_t rows = layout_.seg_count.size();
+        row_off_.assign(rows + 1, 0);
+        for (size_t r = 0; r < rows; ++r) row_off_[r + 1] = row_off_[r] + layout_.seg_count[r];
+        segs_.resize(static_cast<size_t>(row_off_[rows]) * 7);
+        for (size_t r = 0, at = 0; r < rows; ++r)
+            for (std::int32_t k = 0; k < layout_.seg_count[r]; ++k, ++at) {
+                const kern::SegPrep& s = layout_.seg_prep[r * layout_.max_segments + k];
+                double* d = &segs_[at * 7];
+                for (int j = 0; j < 3; ++j) d[j] = s.a[j], d[3 + j] = s.d[j];
+                d[6] = s.dd;
+            }
+        edge_sat_.resize(layout_.edge_sat.size() * 21);
+        for (size_t i = 0; i < layout_.edge_sat.size(); ++i) {
+            const kern::SatBox& b = layout_.edge_sat[i];
+            double* d = &edge_sat_[i * 21];
+            for (int j = 0; j < 3; ++j) d[j] = b.center[j];
+            for (int k = 0; k < 3; ++k)
+                for (int j = 0; j < 3; ++j) d[3 + 3 * k + j] = b.e[k][j], d[12 + 3 * k + j] = b.u[k][j];
+        }
+        comp_aabb_.resize(static_cast<size_t>(layout_.n_components) * 6);
+        for (int c = 0; c < layout_.n_components; ++c) {
+            const Aabb& a = layout_.component_aabb[c];
+            const double v[6] = {a.min.x, a.min.y, a.min.z, a.max.x, a.max.y, a.max.z};
+            for (int j = 0; j < 6; ++j) comp_aabb_[6 * c + j] = v[j];
+        }
+        const int M = layout_.n_obstacles, C = layout_.n_spheres;
+        obst_he_.resize(static_cast<size_t>(M) * 3);
+        obst_sl_.assign(static_cast<size_t>(M) * C * 3, 0.0);
+        for (int o = 0; o < M; ++o) {
+            const ObstacleModel& m = scene.obstacles[o];
+            obst_he_[3 * o] = m.half_extents.x, obst_he_[3 * o + 1] = m.half_extents.y, obst_he_[3 * o + 2] = m.half_extents.z;
+            for (size_t s = 0; s < m.inner.size(); ++s) {
+                double* d = &obst_sl_[(static_cast<size_t>(o) * C + s) * 3];
+                d[0] = m.inner[s].center.x, d[1] = m.inner[s].center.y, d[2] = m.inner[s].center.z;
+            }
+        }
+        rgg_layout_view v{layout_.n_components, layout_.n_bodies, layout_.n_slots, M, C, edge_sat_.data(),
+                          comp_aabb_.data(), row_off_.data(), segs_.data(), layout_.spline_radius.data(),
+                          obst_he_.data(), obst_sl_.data(), layout_.o_minus_r.data(), layout_.o_sphere_count.data()};
+        rgg_gpu_options opt{};
+        opt.device = device;
+        opt.use_under = options.use_under ? 1 : 0;
+        opt.cell_capacity = cell_capacity < 1 ? 1 : (cell_capacity > 256 ? 256 : cell_capacity);
+        opt.allow_wide = allow_wide ? 1 : 0;
+        const int rc = rgg_gpu_create(&v, &opt, &h_);
+        if (rc != RGG_OK) {
+            const std::string msg = rgg_gpu_last_error(h_);
+            rgg_gpu_destroy(h_);
+            h_ = nullptr;
+            raise(rc, msg);
+        }
+        rgg_gpu_count(h_, nullptr, nullptr, &words_);
+        states_.assign(layout_.n_components, ValidityState::Valid);
+        bits_.assign(static_cast<size_t>(layout_.n_components) * words_, 0);
+    }
+
+    ~GpuEngine() { rgg_gpu_destroy(h_); }
+    GpuEngine(const GpuEngine&) = delete;
+    GpuEngine& operator=(const GpuEngine&) = delete;
+
+    UpdateReport update_obstacle(ObstacleId o, const Transform& pose, bool lazy) {
+        return batch_update({{o, pose}}, lazy).at(0);
+    }
+
+    std::vector<UpdateReport> batch_update(const std::vector<std::pair<ObstacleId, Transform>>& moves, bool lazy) {
+        std::vector<UpdateReport> out;
+        if (moves.empty()) return out;
+        if (!lazy) {  // eager: move by move, exact resolve of the gray over-hits on the host
+            for (const auto& m : moves) out.push_back(eager_move(m.first, m.second));
+            return out;
+        }
+        std::vector<std::int32_t> ids;
+        std::vector<double> rt;
+        for (const auto& [o, pose] : moves) {
+            ids.push_back(o);
+            for (double r : pose.r) rt.push_back(r);
+            rt.push_back(pose.t.x), rt.push_back(pose.t.y), rt.push_back(pose.t.z);
+        }
+        std::vector<rgg_update_report> rep(moves.size());
+        const int rc = rgg_gpu_update(h_, ids.data(), rt.data(), static_cast<std::int32_t>(ids.size()),
+                                      RGG_LAZY | RGG_PER_MOVE, rep.data());
+        // the moves the device applied (all, or those before an unknown id) mutate the scene
+        size_t applied = moves.size();
+        if (rc == RGG_EINVAL)
+            for (applied = 0; applied < moves.size() && moves[applied].first >= 0 &&
+                              moves[applied].first < static_cast<ObstacleId>(scene_.obstacles.size());
+                 ++applied) {
+            }
+        for (size_t i = 0; i < applied; ++i) {
+            scene_.obstacles[moves[i].first].pose = moves[i].second;
+            scene_.obstacles[moves[i].first].active = true;
+        }
+        stale_ = true;
+        if (rc != RGG_OK) raise(rc, rgg_gpu_last_error(h_));
+        for (const rgg_update_report& r : rep) out.push_back(convert(r));
+        return out;
+    }
+
+    int resolve_all_unknown() {
+        std::int32_t n = 0;
+        check(rgg_gpu_gray_ids(h_, nullptr, 0, &n));
+        std::vector<std::int32_t> ids(n);
+        if (n) check(rgg_gpu_gray_ids(h_, ids.data(), n, &n));
+        std::vector<std::uint8_t> st(n);
+        for (std::int32_t i = 0; i < n; ++i)
+            st[i] = exact_component_valid(components_->cfgs[ids[i]], scene_.robot, scene_) ? 0 : 1;
+        if (n) check(rgg_gpu_write_states(h_, ids.data(), st.data(), n));
+        stale_ = true;
+        return n;
+    }
+
+    const std::vector<ValidityState>& states() const {
+        refresh();
+        return states_;
+    }
+    const std::vector<std::uint64_t>& obstacle_bits() const {
+        refresh();
+        return bits_;
+    }
+    int unknown_count() const {
+        std::int32_t n = 0;
+        check(rgg_gpu_unknown_count(h_, &n));
+        return n;
+    }
+    const BatchLayout& layout() const { return layout_; }
+    int words_per_component() const { return words_; }
+
+    void batch_over(const std::vector<ComponentId>& candidates, ObstacleId o, std::vector<std::uint8_t>& mask) {
+        mask.assign(candidates.size(), 0);
+        check(rgg_gpu_pair_masks(h_, 0, candidates.data(), static_cast<std::int32_t>(candidates.size()), o, mask.data()));
+    }
+    void batch_under(const std::vector<ComponentId>& candidates, ObstacleId o, std::vector<std::uint8_t>& mask) {
+        mask.assign(candidates.size(), 0);
+        check(rgg_gpu_pair_masks(h_, 1, candidates.data(), static_cast<std::int32_t>(candidates.size()), o, mask.data()));
+    }
+
+private:
+    [[noreturn]] static void raise(int rc, const std::string& msg) {
+        if (rc == RGG_EINVAL) throw std::invalid_argument(msg);
+        if (rc == RGG_ELOGIC) throw std::logic_error(msg);
+        throw std::runtime_error("rgg_gpu error " + std::to_string(rc) + ": " + msg);
+    }
+    void check(int rc) const {
+        if (rc != RGG_OK) raise(rc, rgg_gpu_last_error(h_));
+    }
+    static UpdateReport convert(const rgg_update_report& r) {
+        UpdateReport u;
+        u.obstacle = r.obstacle;
+        u.new_green = r.new_green;
+        u.new_red = r.new_red;
+        u.new_gray = r.new_gray;
+        u.reval_us = r.reval_us;
+        u.over_us = r.over_us;
+        u.under_us = r.under_us;
+        u.resolve_us = r.resolve_us;
+        u.unknown_after_heuristic = r.unknown_after_heuristic;
+        u.residual_unknown = r.residual_unknown;
+        u.resolve_checks = r.resolve_checks;
+        return u;
+    }
+    void refresh() const {
+        if (!stale_) return;
+        std::vector<std::uint8_t> st(states_.size());
+        check(rgg_gpu_read_states(h_, st.data()));
+        for (size_t i = 0; i < st.size(); ++i) states_[i] = static_cast<ValidityState>(st[i]);
+        check(rgg_gpu_read_bits(h_, bits_.data(), words_));
+        stale_ = false;
+    }
+    // engine_batch.cpp:190-202: the over-hits of this move still Unknown after the
+    // heuristic are resolved exactly; finish_counts compares pre-move and final labels.
+    UpdateReport eager_move(ObstacleId o, const Transform& pose) {
+        refresh();
+        const std::vector<ValidityState> before = states_;
+        UpdateReport r = batch_update({{o, pose}}, true).at(0);
+        std::int32_t n = 0;
+        check(rgg_gpu_last_hits(h_, nullptr, 0, &n));
+        std::vector<std::int32_t> hits(n);
+        if (n) check(rgg_gpu_last_hits(h_, hits.data(), n, &n));
+        std::vector<std::uint8_t> st(n);
+        for (std::int32_t i = 0; i < n; ++i) {
+            const ComponentId c = hits[i];
+            st[i] = exact_component_valid(components_->cfgs[c], scene_.robot, scene_) ? 0 : 1;
+            if (before[c] != ValidityState::Unknown) --r.new_gray;
+            if (st[i] == 0 && before[c] != ValidityState::Valid) ++r.new_green;
+            if (st[i] == 1 && before[c] != ValidityState::Invalid) ++r.new_red;
+        }
+        if (n) check(rgg_gpu_write_states(h_, hits.data(), st.data(), n));
+        r.resolve_checks = n;
+        r.residual_unknown = unknown_count();
+        stale_ = true;
+        return r;
+    }
+
+    const ComponentSet* components_;
+    Scene& scene_;
+    EngineOptions options_;
+    BatchLayout layout_;
+    std::vector<double> edge_sat_, comp_aabb_, segs_, obst_he_, obst_sl_;
+    std::vector<std::int32_t> row_off_;
+    rgg_gpu* h_ = nullptr;
+    std::int32_t words_ = 1;
+    mutable bool stale_ = false;
+    mutable std::vector<ValidityState> states_;
+    mutable std::vector<std::uint64_t> bits_;
+};
+
+}  // namespace rgg

@@ -1,0 +1,191 @@
+// test_gpu_engine.cpp — the C++ drop-in rgg::GpuEngine (include/rgg/engine_gpu.hpp)
+// against the reference engines, compiled against the reference's own headers
+// and linked with the unmodified reference library (oracle/_ref/librgg_ref.so)
+// and the CUDA engine (paper_2603_28674_b200/lib/librgg_gpu.so).
+//
+// The cases restate the reference's own suites for the batch engine:
+//   proj/tests/test_batch.cpp:208-234  batch_over / batch_under == sequential narrow tests
+//   proj/tests/test_batch.cpp:260-285  states + bits + report counts == sequential after every move
+//   proj/tests/test_batch.cpp:287-295  empty move list
+//   proj/tests/test_sequential.cpp:106-126, :229-252  eager resolve semantics
+//   proj/src/bench.cpp:57-83           scenario replay with equivalence after every iteration
+// Built by `make -C oracle dropin` (needs /root/reference); run by tests/test_cpp_dropin.py on a GPU.
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <sstream>
+#include <string>
+
+#include "rgg/engine_batch.hpp"
+#include "rgg/engine_gpu.hpp"
+#include "rgg/engine_sequential.hpp"
+#include "rgg/rng.hpp"
+#include "rgg/scenario.hpp"
+
+using namespace rgg;
+
+static int g_fail = 0, g_checks = 0;
+#define EXPECT(cond, ...)                                                   \
+    do {                                                                    \
+        ++g_checks;                                                         \
+        if (!(cond)) {                                                      \
+            ++g_fail;                                                       \
+            std::fprintf(stderr, "FAIL %s:%d: %s ", __FILE__, __LINE__, #cond); \
+            std::fprintf(stderr, __VA_ARGS__);                              \
+            std::fprintf(stderr, "\n");                                     \
+        }                                                                   \
+    } while (0)
+
+// The random scene of proj/tests/test_batch.cpp's fixture: free cube robot,
+// +-env_half workspace, 1-3 random box obstacles, a seeded PRM (k = 6).
+struct Scenelet {
+    Scene scene;
+    Roadmap roadmap;
+    ComponentSet components;
+    Scenelet(int nodes, int n_obstacles, std::uint64_t seed, double env_half = 6.0) {
+        scene.bounds = {{-env_half, -env_half, -env_half}, {env_half, env_half, env_half}};
+        scene.robot = make_free_flying_box({0.5, 0.5, 0.5});
+        Rng rng(seed);
+        for (int i = 0; i < n_obstacles; ++i) {
+            const Vec3 he{rng.uniform(0.4, 1.6), rng.uniform(0.4, 1.6), rng.uniform(0.4, 1.6)};
+            scene.obstacles.push_back(make_box_obstacle(he, rng.uniform_int(1, 4)));
+        }
+        roadmap = build_prm(scene, nodes, 6, 0.25, seed);
+        components = build_components(roadmap, scene.robot, default_body_spheres(scene.robot), 0.25, 16);
+    }
+};
+
+static bool same_reports(const UpdateReport& a, const UpdateReport& b) {
+    return a.new_green == b.new_green && a.new_red == b.new_red && a.new_gray == b.new_gray &&
+           a.unknown_after_heuristic == b.unknown_after_heuristic && a.residual_unknown == b.residual_unknown;
+}
+
+static void equivalence_after_every_move() {
+    for (int trial = 0; trial < 6; ++trial) {
+        Scenelet fx(40 + trial * 25, 1 + trial % 3, 700 + trial);
+        Scene seq_scene = fx.scene, gpu_scene = fx.scene;
+        SequentialEngine seq(fx.components, seq_scene, {});
+        GpuEngine gpu(fx.components, gpu_scene, {});
+        const bool lazy = trial % 2 == 0;
+        Rng rng(9000 + trial);
+        for (int move = 0; move < 30; ++move) {
+            const ObstacleId o = rng.uniform_int(0, static_cast<int>(fx.scene.obstacles.size()) - 1);
+            Transform pose = Transform::from_euler_xyz(rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(-3, 3));
+            pose.t = {rng.uniform(-5, 5), rng.uniform(-5, 5), rng.uniform(-5, 5)};
+            const UpdateReport rs = seq.update_obstacle(o, pose, lazy);
+            const UpdateReport rg = gpu.update_obstacle(o, pose, lazy);
+            EXPECT(seq.states() == gpu.states(), "trial %d move %d (%s): states differ", trial, move, lazy ? "lazy" : "eager");
+            EXPECT(seq.obstacle_bits() == gpu.obstacle_bits(), "trial %d move %d: bits differ", trial, move);
+            EXPECT(same_reports(rs, rg), "trial %d move %d: reports seq(%d,%d,%d,%d,%d) gpu(%d,%d,%d,%d,%d)", trial, move,
+                   rs.new_green, rs.new_red, rs.new_gray, rs.unknown_after_heuristic, rs.residual_unknown, rg.new_green,
+                   rg.new_red, rg.new_gray, rg.unknown_after_heuristic, rg.residual_unknown);
+            EXPECT(gpu_scene.obstacles[o].active && gpu_scene.obstacles[o].pose.t == pose.t, "scene not mutated");
+        }
+    }
+}
+
+static void narrow_masks_match_sequential() {
+    Scenelet fx(60, 3, 53);
+    Scene seq_scene = fx.scene, gpu_scene = fx.scene;
+    SequentialEngine seq(fx.components, seq_scene, {});
+    GpuEngine gpu(fx.components, gpu_scene, {});
+    Rng rng(99);
+    std::vector<ComponentId> all;
+    for (ComponentId c = 0; c < fx.components.count(); ++c) all.push_back(c);
+    for (int move = 0; move < 20; ++move) {
+        const ObstacleId o = move % 3;
+        const Transform pose = Transform::translation({rng.uniform(-5, 5), rng.uniform(-5, 5), rng.uniform(-5, 5)});
+        seq.update_obstacle(o, pose, true);
+        gpu.update_obstacle(o, pose, true);
+        std::vector<std::uint8_t> over, under;
+        gpu.batch_over(all, o, over);
+        gpu.batch_under(all, o, under);
+        for (ComponentId c = 0; c < fx.components.count(); ++c) {
+            EXPECT(static_cast<bool>(over[c]) == seq.narrow_over_test(o, c), "over mask c=%d move %d", c, move);
+            EXPECT(static_cast<bool>(under[c]) == seq.narrow_under_test(o, c), "under mask c=%d move %d", c, move);
+        }
+    }
+}
+
+static void batch_update_matches_batch_engine() {
+    Scenelet fx(80, 3, 61);
+    Scene bat_scene = fx.scene, gpu_scene = fx.scene;
+    BatchEngine bat(fx.components, bat_scene, {});
+    GpuEngine gpu(fx.components, gpu_scene, {});
+    Rng rng(61);
+    for (int it = 0; it < 10; ++it) {
+        std::vector<std::pair<ObstacleId, Transform>> moves;
+        for (int i = 0; i < 7; ++i)
+            moves.push_back({rng.uniform_int(0, 2),
+                             Transform::translation({rng.uniform(-5, 5), rng.uniform(-5, 5), rng.uniform(-5, 5)})});
+        const auto rb = bat.batch_update(moves, true);
+        const auto rg = gpu.batch_update(moves, true);
+        EXPECT(rb.size() == rg.size(), "report count");
+        for (size_t i = 0; i < rb.size(); ++i) EXPECT(same_reports(rb[i], rg[i]), "iteration %d move %zu report", it, i);
+        EXPECT(bat.states() == gpu.states(), "iteration %d states", it);
+        EXPECT(bat.obstacle_bits() == gpu.obstacle_bits(), "iteration %d bits", it);
+        EXPECT(bat.unknown_count() == gpu.unknown_count(), "iteration %d unknown count", it);
+    }
+    EXPECT(gpu.batch_update({}, true).empty(), "empty move list");
+    bool threw = false;
+    try {
+        gpu.update_obstacle(99, Transform::identity(), true);
+    } catch (const std::invalid_argument& e) {
+        threw = std::string(e.what()) == "unknown obstacle id";
+    }
+    EXPECT(threw, "unknown obstacle id must throw std::invalid_argument");
+    // resolve_all_unknown leaves no gray, like the reference (engine_batch.cpp:217-227)
+    const int nb = bat.resolve_all_unknown();
+    const int ng = gpu.resolve_all_unknown();
+    EXPECT(nb == ng, "resolve_all_unknown resolved %d vs %d", nb, ng);
+    EXPECT(bat.states() == gpu.states(), "states after resolve_all_unknown");
+    EXPECT(gpu.unknown_count() == 0, "gray left after resolve_all_unknown");
+}
+
+static void scenario_replay(const std::string& path) {
+    std::ifstream f(path);
+    if (!f) {
+        std::fprintf(stderr, "skip %s (absent)\n", path.c_str());
+        return;
+    }
+    std::stringstream ss;
+    ss << f.rdbuf();
+    const Scenario s = parse_scenario_text(ss.str(), path);
+    Scene build_scene{s.env, {}, s.robot};
+    const Roadmap roadmap = build_prm(build_scene, s.nodes, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed);
+    const ComponentSet comps =
+        build_components(roadmap, s.robot, default_body_spheres(s.robot), s.effective_epsilon(), s.max_segments);
+    Scene seq_scene{s.env, s.make_obstacles(), s.robot}, gpu_scene{s.env, s.make_obstacles(), s.robot};
+    SequentialEngine seq(comps, seq_scene, {});
+    GpuEngine gpu(comps, gpu_scene, {});
+    const bool lazy = s.mode == UpdateMode::Lazy;
+    const auto moves = s.make_moves();
+    const int per = static_cast<int>(s.obstacles.size());
+    const int iterations = std::min(s.iterations, lazy ? s.iterations : 4);
+    for (int it = 0; it < iterations; ++it) {
+        for (int m = 0; m < per; ++m) {
+            const auto& [o, pose] = moves[static_cast<size_t>(it) * per + m];
+            const UpdateReport rs = seq.update_obstacle(o, pose, lazy);
+            const UpdateReport rg = gpu.update_obstacle(o, pose, lazy);
+            EXPECT(same_reports(rs, rg), "%s it %d move %d report", s.name.c_str(), it, m);
+        }
+        EXPECT(seq.states() == gpu.states(), "%s iteration %d states", s.name.c_str(), it + 1);
+        EXPECT(seq.obstacle_bits() == gpu.obstacle_bits(), "%s iteration %d bits", s.name.c_str(), it + 1);
+    }
+    std::printf("scenario %s (%s): %d components, %d iterations compared\n", s.name.c_str(), lazy ? "lazy" : "eager",
+                comps.count(), iterations);
+}
+
+int main(int argc, char** argv) {
+    const std::string dir = argc > 1 ? argv[1] : "";
+    equivalence_after_every_move();
+    narrow_masks_match_sequential();
+    batch_update_matches_batch_engine();
+    if (!dir.empty()) {
+        scenario_replay(dir + "/quick_smoke.scn");
+        scenario_replay(dir + "/table4_obstacles_1000_5x.scn");
+        scenario_replay(dir + "/table5_manipulator_100.scn");
+    }
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
