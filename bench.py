@@ -236,20 +236,24 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
     ids_d = torch.from_numpy(ids_h).to(dev)
     rts_d = torch.from_numpy(rts_h).to(dev)
-    counters = torch.zeros((m_step, 4), dtype=torch.int32, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
+    up = None
+    if dist is not None:
+        from paper_2603_28674_b200.dist import DistributedUpdater
+
+        up = DistributedUpdater(eng, dev)
+
     def step_device(it):
-        with torch.cuda.stream(stream):
-            if dist is not None:
-                dist.broadcast(ids_d[it], 0)
-                dist.broadcast(rts_d[it], 0)
-        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True)
-        if dist is not None:
-            with torch.cuda.stream(stream):
-                eng.copy_counters(counters.data_ptr(), m_step)
-                dist.all_reduce(counters)
+        if up is None:
+            eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True)
+        else:  # broadcast of the moves from rank 0, shard update, all-reduce of the report counters
+            up.update(ids_d[it], rts_d[it], per_move=True)
+
+    # N = 1: the engine's own stream carries everything; N > 1: the collectives run on
+    # torch's current stream and DistributedUpdater orders the engine stream against it
+    tstream = stream if dist is None else torch.cuda.current_stream(dev)
 
     # ---- warm-up (device path), then K timed steps with L2 flushed in between
     for it in range(args.warmup):
@@ -262,11 +266,11 @@ def main():
     with ClockSampler(local) as clk:
         t_clock0 = time.perf_counter()
         for k in range(args.steps):
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(tstream):
                 flush.zero_()
-            ev[k][0].record(stream)
+            ev[k][0].record(tstream)
             step_device(args.warmup + k)
-            ev[k][1].record(stream)
+            ev[k][1].record(tstream)
             st = eng.last_stats()
             classify_ms.append(st["classify_ms"])
             stats.append(st)
@@ -292,6 +296,11 @@ def main():
 
     # ---- e2e through the public API with host buffers (rank 0 drives; N>1 via torch collectives)
     eng_e2e = E.GpuEngine(lv, device=local)
+    up_e2e = None
+    if dist is not None:
+        from paper_2603_28674_b200.dist import DistributedUpdater
+
+        up_e2e = DistributedUpdater(eng_e2e, dev)
     e2e_s = []
     for it in range(iterations):
         if it >= args.warmup:
@@ -304,14 +313,7 @@ def main():
         else:
             ids_t = torch.from_numpy(ids_h[it]).pin_memory().to(dev, non_blocking=True)
             rts_t = torch.from_numpy(rts_h[it]).pin_memory().to(dev, non_blocking=True)
-            dist.broadcast(ids_t, 0)
-            dist.broadcast(rts_t, 0)
-            torch.cuda.current_stream().synchronize()
-            eng_e2e.update_device(ids_t.data_ptr(), rts_t.data_ptr(), m_step, per_move=True)
-            with torch.cuda.stream(stream):
-                eng_e2e.copy_counters(counters.data_ptr(), m_step)
-                dist.all_reduce(counters)
-            reps = counters.cpu()
+            reps = up_e2e.update(ids_t, rts_t, per_move=True).cpu()
         t1 = time.perf_counter()
         if it >= args.warmup:
             e2e_s.append(t1 - t0)

@@ -281,6 +281,20 @@ class GpuEngine:
     def sync(self):
         self._check(library().rgg_gpu_sync(self._h))
 
+    # torch-tensor entry points used by the multi-GPU driver (paper_2603_28674_b200/dist.py)
+    def update_tensors(self, ids, rts, per_move: bool = True):
+        """ids int32[n] / rts float64[n, 12] CUDA tensors, enqueued on the engine stream
+        after the producer stream's work (so a preceding broadcast is visible)."""
+        import torch
+
+        torch.cuda.current_stream(ids.device).synchronize()
+        self.update_device(ids.data_ptr(), rts.data_ptr(), int(ids.numel()), per_move=per_move)
+
+    def counters_into(self, out, n: int):
+        """Per-move counters of the last update into a CUDA int32 tensor (n, 4); waits for them."""
+        self.copy_counters(out.data_ptr(), n)
+        self.sync()
+
     def copy_counters(self, dst_ptr: int, n: int):
         """Per-move counters of the last update -> device buffer (n x 4 int32), engine stream."""
         self._check(library().rgg_gpu_copy_counters(self._h, C.c_void_p(dst_ptr), int(n)))

@@ -154,3 +154,35 @@ def test_use_under_false_never_red(eng_mod):
     st = eng.states()
     assert not np.any(st == 1)
     assert np.any(st == 2)
+
+
+@pytest.mark.parametrize("name", ["scn_table4_obstacles_1000_5x", "syn_se2_m80"])
+def test_interleaved_cell_shards_compose(eng_mod, name):
+    """rgg_gpu_options.shard_rank/shard_count: two shard handles (one per future GPU)
+    own disjoint cells; their labels compose to the reference's and their per-move
+    counters sum to the reference's reports (the all-reduce of dist.py)."""
+    import torch
+
+    g = load_golden(name)
+    lv = _layout(g)
+    shards = [eng_mod.GpuEngine(lv, shard_rank=r, shard_count=2, cell_size=64) for r in range(2)]
+    n = len(g["ids"])
+    ids = torch.from_numpy(g["ids"].astype(np.int32)).cuda()
+    rts = torch.from_numpy(g["rts"]).cuda()
+    total = torch.zeros((n, 4), dtype=torch.int32, device="cuda")
+    for sh in shards:
+        sh.update_tensors(ids, rts, per_move=True)
+        c = torch.zeros((n, 4), dtype=torch.int32, device="cuda")
+        sh.counters_into(c, n)
+        total += c
+    st = [sh.states() for sh in shards]
+    own = [s != 0xFF for s in st]
+    assert not np.any(own[0] & own[1]) and np.all(own[0] | own[1]), "shards must partition the components"
+    merged = np.where(own[0], st[0], st[1])
+    assert np.array_equal(merged, g["snap_states"][-1])
+    if int(g["groups"]) == 1:
+        from paper_2603_28674_b200.dist import DistributedUpdater
+
+        reps = DistributedUpdater.reports(total, 0)
+        got = np.array([[r["new_green"], r["new_red"], r["new_gray"], r["unknown_after_heuristic"]] for r in reps])
+        assert np.array_equal(got, g["reports"][:, :4])
