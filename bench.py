@@ -346,7 +346,19 @@ def main():
         roof = {"bound": "hbm", "achieved": byts / (mean_classify * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # dram__bytes_read.sum + dram__bytes_write.sum of the classify kernel from the committed
+    # `ncu --set full` capture (profiles/r1_classify_warp_ncu.json); null when absent
     roof["traffic"] = None
+    pf = os.path.join(ROOT, "profiles", "r1_classify_warp_ncu.json")
+    if os.path.exists(pf):
+        try:
+            p = json.load(open(pf))
+            unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rd, wr = p["dram__bytes_read.sum"], p["dram__bytes_write.sum"]
+            roof["traffic"] = float(rd[0]) * unit[rd[1]] + float(wr[0]) * unit[wr[1]]
+            roof["traffic_source"] = "profiles/r1_classify_warp_ncu.json (ncu --set full, one c2 launch)"
+        except (KeyError, ValueError):
+            pass
     roof["kernel"] = "classify_warp_kernel (paper_2603_28674_b200/csrc/rgg_kernels.cu)"
     roof["algorithmic"] = {"flops_per_launch": flops, "bytes_per_launch": byts, "classify_ms_mean": mean_classify,
                            "roof_ms": 1e3 * max(t_fl, t_by), "census": census}
