@@ -6,7 +6,9 @@
 // present, and every compute entry launches the kernels of rgg_kernels.cu.
 #include <algorithm>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
+#include <limits>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -28,12 +30,15 @@ struct rgg_gpu {
     // device allocations
     double2* d_aabb = nullptr;
     double* d_sat = nullptr;
+    rggd::Box32* d_sat32 = nullptr;
     int32_t* d_row = nullptr;
     double* d_seg = nullptr;
     double* d_spline = nullptr;
     int32_t* d_orig = nullptr;
     int32_t* d_rank = nullptr;
     double* d_cell_aabb = nullptr;
+    double* d_super_aabb = nullptr;
+    double* d_evbox = nullptr;
     double* d_ohe = nullptr;
     double* d_osl = nullptr;
     double* d_osr = nullptr;
@@ -137,6 +142,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     cudaFree(h->d_rt);
     cudaFree(h->d_last);
     cudaFree(h->d_ev);
+    cudaFree(h->d_evbox);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
     cudaFree(h->d_mpool);
@@ -144,6 +150,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     CK(dalloc(&h->d_rt, static_cast<size_t>(cap) * 12));
     CK(dalloc(&h->d_last, cap));
     CK(dalloc(&h->d_ev, cap));
+    CK(dalloc(&h->d_evbox, static_cast<size_t>(cap) * 12));
     CK(dalloc(&h->d_mv, static_cast<size_t>(cap) * 4));
     // every (cell, event) pair fits: the overflow pool can never run out
     h->pool_cap = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * cap);
@@ -177,6 +184,7 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.rt = h->d_rt;
     b.last = h->d_last;
     b.ev = h->d_ev;
+    b.evbox = h->d_evbox;
     b.cell_count = h->d_cell_count;
     b.cell_list = h->d_cell_list;
     b.cell_ovf = h->d_cell_ovf;
@@ -289,6 +297,9 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
                              acc[hv][3] / cnt[hv] * 1e-3, acc[hv][4] / cnt[hv] * 1e-3, acc[hv][5] / cnt[hv] * 1e-3,
                              acc[hv][6] / cnt[hv] * 1e-3, (hi - lo) * 1e-3);
         CK(cudaMemsetAsync(b.dbg, 0, t.size() * 8, h->stream));
+        unsigned long long fs[4];
+        rggk::filter_stats(fs, true);
+        std::fprintf(stderr, "[rgg] fp64 rechecks: SAT %llu, seg-sphere %llu\n", fs[1], fs[3]);
     }
     CK(cudaEventRecord(h->ev[3], h->stream));
     CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
@@ -439,18 +450,46 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         }
         std::memcpy(&cell_aabb[6 * static_cast<size_t>(g)], box, sizeof(box));
     }
+    const int32_t nsuper = (ncells + rggk::kSuperCells - 1) / rggk::kSuperCells;
+    std::vector<double> super_aabb(static_cast<size_t>(std::max(nsuper, 1)) * 6);
+    for (int32_t g = 0; g < nsuper; ++g) {
+        double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+        for (int32_t c = g * rggk::kSuperCells; c < std::min(ncells, (g + 1) * rggk::kSuperCells); ++c)
+            for (int k = 0; k < 3; ++k) {
+                box[k] = std::min(box[k], cell_aabb[6 * static_cast<size_t>(c) + k]);
+                box[3 + k] = std::max(box[3 + k], cell_aabb[6 * static_cast<size_t>(c) + 3 + k]);
+            }
+        std::memcpy(&super_aabb[6 * static_cast<size_t>(g)], box, sizeof(box));
+    }
     std::vector<int32_t> rankv(static_cast<size_t>(N), -1);
     for (int32_t i = 0; i < Np; ++i) rankv[owned[i]] = i;
 
     // ---- device store
     CK(dalloc(&h->d_aabb, aabb.size()));
     CK(dalloc(&h->d_sat, sat.size()));
+    // fp32 filter operands (rgg_device.cuh Box32): e, u rounded to nearest, L = sum |e_k|_1 rounded up
+    std::vector<rggd::Box32> sat32(static_cast<size_t>(Np) * B);
+    for (size_t i = 0; i < sat32.size(); ++i) {
+        const double* a = &sat[i * 22];
+        double l1 = 0.0;
+        for (int k = 0; k < 9; ++k) {
+            sat32[i].e[k] = static_cast<float>(a[3 + k]);
+            sat32[i].u[k] = static_cast<float>(a[12 + k]);
+            l1 += std::fabs(a[3 + k]);
+        }
+        const float lf = static_cast<float>(l1 * (1.0 + 1e-15));
+        sat32[i].L = std::nextafter(lf, std::numeric_limits<float>::infinity());
+        sat32[i].pad = 0.0f;
+    }
+    CK(dalloc(&h->d_sat32, sat32.size()));
+    CK(cudaMemcpyAsync(h->d_sat32, sat32.data(), sat32.size() * sizeof(rggd::Box32), cudaMemcpyHostToDevice, h->stream));
     CK(dalloc(&h->d_row, row.size()));
     CK(dalloc(&h->d_seg, seg.size()));
     CK(dalloc(&h->d_spline, static_cast<size_t>(B) * S));
     CK(dalloc(&h->d_orig, Np));
     CK(dalloc(&h->d_rank, N));
     CK(dalloc(&h->d_cell_aabb, cell_aabb.size()));
+    CK(dalloc(&h->d_super_aabb, super_aabb.size()));
     CK(dalloc(&h->d_ohe, static_cast<size_t>(M) * 3));
     CK(dalloc(&h->d_osl, static_cast<size_t>(M) * std::max(C, 1) * 3));
     CK(dalloc(&h->d_osr, M));
@@ -488,6 +527,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(up(h->d_orig, owned.data(), owned.size() * sizeof(int32_t)));
     CK(up(h->d_rank, rankv.data(), rankv.size() * sizeof(int32_t)));
     CK(up(h->d_cell_aabb, cell_aabb.data(), cell_aabb.size() * sizeof(double)));
+    CK(up(h->d_super_aabb, super_aabb.data(), super_aabb.size() * sizeof(double)));
     CK(up(h->d_ohe, v->obst_he, static_cast<size_t>(M) * 3 * sizeof(double)));
     CK(up(h->d_osl, v->obst_sph_local, static_cast<size_t>(M) * C * 3 * sizeof(double)));
     CK(up(h->d_osr, v->obst_sph_r, static_cast<size_t>(M) * sizeof(double)));
@@ -520,11 +560,13 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.use_under = o.use_under ? 1 : 0;
     s.aabb = h->d_aabb;
     s.sat = h->d_sat;
+    s.sat32 = h->d_sat32;
     s.row = h->d_row;
     s.seg = h->d_seg;
     s.spline_r = h->d_spline;
     s.orig = h->d_orig;
     s.cell_aabb = h->d_cell_aabb;
+    s.super_aabb = h->d_super_aabb;
     s.ohe = h->d_ohe;
     s.osl = h->d_osl;
     s.osr = h->d_osr;
@@ -549,7 +591,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* dev[] = {h->d_aabb, h->d_sat, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_last, h->d_unknown, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
@@ -825,9 +867,13 @@ int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
     // label (1 B), counters (4 B) and bit words (16 B per word) and writes them
     // back; components with an over item read their SatBoxes (B*168 B), those
     // with an under item their row offsets and real segments (56 B each).
+    //   (bit words: W = 1 keeps both words of a component in registers -> 16 B read + 16 B
+    //   written per component; W > 1 touches one over + one under word per touched pair)
     const int64_t dirty = static_cast<int64_t>(c[8]), box_comps = static_cast<int64_t>(c[9]),
-                  sph_comps = static_cast<int64_t>(c[10]), segs = static_cast<int64_t>(c[11]);
-    out->bytes_components = dirty * (48 + 2 * (1 + 4 + 16 * h->words)) + box_comps * h->s.B * 168 +
+                  sph_comps = static_cast<int64_t>(c[10]), segs = static_cast<int64_t>(c[11]),
+                  touched = static_cast<int64_t>(c[12]);
+    const int64_t bit_bytes = h->words == 1 ? dirty * 32 : touched * 32;
+    out->bytes_components = dirty * (48 + 2 * (1 + 4)) + bit_bytes + box_comps * h->s.B * 168 +
                             sph_comps * 4 * (h->s.B * h->s.S + 1) + segs * 56;
     return RGG_OK;
 }

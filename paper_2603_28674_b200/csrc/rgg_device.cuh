@@ -165,6 +165,120 @@ __device__ __forceinline__ bool seg_sphere_fast(const double* s, const double* c
     return __dsqrt_rn(x) <= r_total;
 }
 
+// ---------------------------------------------------------------- fp32 filters
+//
+// fp32 versions of the two predicates that return 0 (false for sure), 1 (true
+// for sure) or 2 (undecided).  Each carries a rigorous bound on the distance
+// between its fp32 result and the exact-arithmetic value, and only calls a
+// decision when the margin clears that bound plus the reference's own fp64
+// rounding (which is ~1e-16 relative, far below it).  Undecided pairs are
+// re-evaluated with the exact fp64 sequence, so the verdicts are still the
+// reference's bit for bit.  u = 2^-24 (fp32 unit roundoff).
+//
+// Box32 (fp32 operand of a SatBox): e[9], u[9] rounded to nearest, L = sum of
+// |e_k|_1 rounded up, pad.  The centre stays fp64 (d is formed in fp64).
+struct __align__(16) Box32 {
+    float e[9];
+    float u[9];
+    float L;
+    float pad;
+};
+
+__device__ __forceinline__ float dot3f(const float* x, const float* y) {
+    return fmaf(x[2], y[2], fmaf(x[1], y[1], x[0] * y[0]));
+}
+
+// margin |d.ax| - (ra + rb) of one axis in fp32
+__device__ __forceinline__ float margin32(const float* d, const Box32& a, const Box32& b, const float* ax) {
+    const float ra = fabsf(dot3f(a.e, ax)) + fabsf(dot3f(a.e + 3, ax)) + fabsf(dot3f(a.e + 6, ax));
+    const float rb = fabsf(dot3f(b.e, ax)) + fabsf(dot3f(b.e + 3, ax)) + fabsf(dot3f(b.e + 6, ax));
+    return fabsf(dot3f(d, ax)) - (ra + rb);
+}
+
+// sat_boxes filter.  Error model per axis (|axis_i| <= A): |m32 - m| <= 10 u S A
+// for face axes (inputs rounded, one rounding per FMA / add, S = |d|_1 + La + Lb);
+// cross axes add the axis' own error E_i <= 4u(|x1 y2| + |x2 y1|): |dm| <= S max E.
+// Margins below twice those bounds are undecided; so are cross axes whose
+// n2 >= 1e-12 decision (kernels_scalar.cpp:64-65) is within its error.
+__device__ __forceinline__ int sat_filter32(const double* ca, const Box32& a, const double* cb, const Box32& b) {
+    constexpr float u = 5.9604645e-8f;  // 2^-24
+    float d[3];
+    d[0] = __double2float_rn(__dsub_rn(cb[0], ca[0]));
+    d[1] = __double2float_rn(__dsub_rn(cb[1], ca[1]));
+    d[2] = __double2float_rn(__dsub_rn(cb[2], ca[2]));
+    const float S = (fabsf(d[0]) + fabsf(d[1]) + fabsf(d[2]) + a.L + b.L) * (1.0f + 16.0f * u);
+    if (!(S < 3.0e37f)) return 2;  // non-finite or huge operands: let fp64 decide
+    const float tol_face = 20.0f * u * S;
+    bool sep = false, undecided = false;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const float* ax = k < 3 ? a.u + 3 * k : b.u + 3 * (k - 3);
+        const float m = margin32(d, a, b, ax);
+        sep |= m > tol_face;
+        undecided |= fabsf(m) <= tol_face;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float* x = a.u + 3 * i;
+            const float* y = b.u + 3 * j;
+            float ax[3], er[3];
+            ax[0] = fmaf(x[1], y[2], -x[2] * y[1]);
+            ax[1] = fmaf(x[2], y[0], -x[0] * y[2]);
+            ax[2] = fmaf(x[0], y[1], -x[1] * y[0]);
+            er[0] = 8.0f * u * (fabsf(x[1] * y[2]) + fabsf(x[2] * y[1]));
+            er[1] = 8.0f * u * (fabsf(x[2] * y[0]) + fabsf(x[0] * y[2]));
+            er[2] = 8.0f * u * (fabsf(x[0] * y[1]) + fabsf(x[1] * y[0]));
+            const float n2 = dot3f(ax, ax);
+            const float n2err = (2.0f * fabsf(ax[0]) + 2.0f * er[0]) * er[0] + (2.0f * fabsf(ax[1]) + 2.0f * er[1]) * er[1] +
+                                (2.0f * fabsf(ax[2]) + 2.0f * er[2]) * er[2] + 8.0f * u * n2 + 1e-18f;
+            const bool tested = n2 - n2err >= 1e-12f * (1.0f + 1e-6f);
+            const bool maybe = !tested && n2 + n2err >= 1e-12f * (1.0f - 1e-6f);
+            const float A = fmaxf(fabsf(ax[0]), fmaxf(fabsf(ax[1]), fabsf(ax[2])));
+            const float E = fmaxf(er[0], fmaxf(er[1], er[2]));
+            const float tol = 2.0f * S * (E + 10.0f * u * A);
+            const float m = margin32(d, a, b, ax);
+            sep |= tested & (m > tol);
+            undecided |= (tested & (fabsf(m) <= tol)) | (maybe & (m > -tol));
+        }
+    }
+    if (sep) return 0;           // a tested axis separates for sure
+    return undecided ? 2 : 1;    // every tested axis overlaps for sure -> intersect
+}
+
+// seg_sphere filter.  p and d come from the fp64 operands; t uses a fast
+// reciprocal.  |x32 - |p - t* d|^2| <= 32 u (|p| + |d|)^2 covers the roundings
+// and the t error (quadratic at an interior optimum, exact at the clamps, and
+// a near-clamp flip moves x by <= 2 t |p.d| with t at rounding level); the
+// reference's x is within 1e-15 of the same value and its sqrt(x) <= r is
+// x <= r^2 up to half an ulp.
+__device__ __forceinline__ int seg_filter32(const double* s, const double* c, double r_total) {
+    constexpr float u = 5.9604645e-8f;
+    if (!(r_total >= 0.0)) return 0;
+    const float px = __double2float_rn(__dsub_rn(c[0], s[0]));
+    const float py = __double2float_rn(__dsub_rn(c[1], s[1]));
+    const float pz = __double2float_rn(__dsub_rn(c[2], s[2]));
+    const float dx = __double2float_rn(s[3]), dy = __double2float_rn(s[4]), dz = __double2float_rn(s[5]);
+    const float dd = __double2float_rn(s[6]);
+    float t = 0.0f;
+    if (dd > 0.0f) {
+        const float num = fmaf(pz, dz, fmaf(py, dy, px * dx));
+        t = fminf(fmaxf(num * __frcp_rn(dd), 0.0f), 1.0f);
+    }
+    const float qx = fmaf(-t, dx, px), qy = fmaf(-t, dy, py), qz = fmaf(-t, dz, pz);
+    const float x = fmaf(qz, qz, fmaf(qy, qy, qx * qx));
+    const float P = fabsf(px) + fabsf(py) + fabsf(pz) + fabsf(dx) + fabsf(dy) + fabsf(dz);
+    const float err = 64.0f * u * P * P + 1e-30f;
+    const float r = static_cast<float>(r_total);
+    const float r2 = r * r;
+    const float r2err = 8.0f * u * r2;
+    if (!(x == x) || !(P < 3.0e18f)) return 2;  // non-finite inputs: let fp64 decide
+    if (x + err < r2 - r2err) return 1;
+    if (x - err > r2 + r2err) return 0;
+    return 2;
+}
+
 // sat_prep, proj/src/kernels_scalar.cpp:7-30.
 __device__ __forceinline__ void sat_prep(const double* c, double* s) {
 #pragma unroll

@@ -225,6 +225,19 @@ __global__ void pose_kernel(Store s, Batch b) {
         for (int k = 0; k < 3; ++k) {
             ev.sat[3 + 3 * lane + k] = e[k];
             ev.sat[12 + 3 * lane + k] = u[k];
+            ev.b32.e[3 * lane + k] = __double2float_rn(e[k]);
+            ev.b32.u[3 * lane + k] = __double2float_rn(u[k]);
+        }
+    }
+    {
+        // L = sum_k |e_k|_1, rounded up (the filter's scale)
+        double l1 = 0.0;
+        if (lane < 3) l1 = fabs(e[0]) + fabs(e[1]) + fabs(e[2]);
+        l1 += __shfl_down_sync(0xffffffffu, l1, 1);
+        l1 += __shfl_down_sync(0xffffffffu, l1, 2);  // lanes 0..2 summed on lane 0 (lane 3 adds 0)
+        if (lane == 0) {
+            ev.b32.L = __double2float_ru(l1 * (1.0 + 1e-15));
+            ev.b32.pad = 0.0f;
         }
     }
     // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
@@ -270,8 +283,12 @@ __global__ void pose_kernel(Store s, Batch b) {
     if (lane < 6) {
         ev.box[lane] = bn[lane];
         ev.sph[lane] = bs[lane];
-        ev.nu[lane] = lane < 3 ? fmin(bn[lane], bs[lane]) : fmax(bn[lane], bs[lane]);
-        ev.old[lane] = p >= 0 ? os[lane] : s.cur_union[6 * o + lane];
+        const double nu = lane < 3 ? fmin(bn[lane], bs[lane]) : fmax(bn[lane], bs[lane]);
+        const double ol = p >= 0 ? os[lane] : s.cur_union[6 * o + lane];
+        ev.nu[lane] = nu;
+        ev.old[lane] = ol;
+        b.evbox[12 * static_cast<size_t>(i) + lane] = nu;  // compact copy for the binning
+        b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol;
     }
     if (lane >= 16 && lane - 16 < nsph) {
         ev.cen[3 * (lane - 16)] = pt[0];
@@ -297,6 +314,14 @@ __global__ void init_obstacles_kernel(Store s) {
     Event& e = s.cur[o];
     int nsph = 0;
     obstacle_at<true>(s, o, id, e.sat, e.box, e.sph, e.cen, &nsph);
+    double l1 = 0.0;
+    for (int k = 0; k < 9; ++k) {
+        e.b32.e[k] = __double2float_rn(e.sat[3 + k]);
+        e.b32.u[k] = __double2float_rn(e.sat[12 + k]);
+        l1 += fabs(e.sat[3 + k]);
+    }
+    e.b32.L = __double2float_ru(l1 * (1.0 + 1e-15));
+    e.b32.pad = 0.0f;
     e.r = s.osr[o];
     e.o = o;
     e.nsph = nsph;
@@ -307,43 +332,87 @@ __global__ void init_obstacles_kernel(Store s) {
 }
 
 // ------------------------------------------------------------------ binning
+//
+// One CTA per group of 16 cells (a Morton-contiguous "super-cell", union box
+// precomputed), one warp per cell.  Events stream through in chunks of 512:
+// each thread loads one event's new/old boxes (compact evbox array, coalesced)
+// and tests them against the super-cell box; an ordered block-wide ballot
+// compaction leaves the chunk's candidates in shared memory; each warp then
+// tests its cell against the candidates and appends hits, in event order, to
+// the cell's fixed-capacity list (overflow -> pool) with warp ballots.  Work is
+// O(supercells x events + cells x candidates) instead of O(cells x events).
 
-constexpr int kBinThreads = 512;  // 16 warps = 16 cells per CTA
-constexpr int kBinChunk = 256;    // event boxes staged per pass
+constexpr int kBinThreads = 512;  // 16 warps = 16 cells per CTA (one super-cell)
+constexpr int kBinChunk = 256;    // events filtered per pass (threads >= kBinChunk idle in the filter)
 
 __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
-    __shared__ double sbox[kBinChunk][12];
+    __shared__ double cbox[kBinChunk][12];
+    __shared__ int cidx[kBinChunk];
+    __shared__ int wsum[kBinThreads / 32];
+    __shared__ int s_nc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cell = blockIdx.x * (kBinThreads / 32) + warp;
     const bool live = cell < s.ncells;
-    double cb[6];
+    double sb[6], cb[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sb[k] = s.super_aabb[6 * static_cast<size_t>(blockIdx.x) + k];
     if (live)
         for (int k = 0; k < 6; ++k) cb[k] = s.cell_aabb[6 * static_cast<size_t>(cell) + k];
     int count = 0;
     int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
     for (int base = 0; base < b.n; base += kBinChunk) {
+        // ---- super-cell filter, ordered compaction of the chunk's candidates
+        const int e = base + threadIdx.x;
+        double bx[12];
+        bool cand = false;
+        if (threadIdx.x < kBinChunk && e < b.n) {
+            const double2* p = reinterpret_cast<const double2*>(b.evbox + 12 * static_cast<size_t>(e));
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {
+                const double2 v = p[k];
+                bx[2 * k] = v.x;
+                bx[2 * k + 1] = v.y;
+            }
+            cand = rggd::overlaps(sb, bx) | rggd::overlaps(sb, bx + 6);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, cand);
         __syncthreads();
-        const int m = min(kBinChunk, b.n - base);
-        for (int t = threadIdx.x; t < m * 12; t += kBinThreads) {
-            const int e = t / 12, k = t % 12;
-            sbox[e][k] = k < 6 ? b.ev[base + e].nu[k] : b.ev[base + e].old[k - 6];
+        if (lane == 0) wsum[warp] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int w = 0; w < kBinThreads / 32; ++w) {
+                const int t = wsum[w];
+                wsum[w] = acc;
+                acc += t;
+            }
+            s_nc = acc;
         }
         __syncthreads();
+        if (cand) {
+            const int pos = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+            cidx[pos] = e;
+#pragma unroll
+            for (int k = 0; k < 12; ++k) cbox[pos][k] = bx[k];
+        }
+        __syncthreads();
+        const int nc = s_nc;
         if (!live) continue;
-        for (int j = 0; j < m; j += 32) {
-            const int e = j + lane;
-            const bool hit = e < m && (rggd::overlaps(cb, sbox[e]) || rggd::overlaps(cb, sbox[e] + 6));
-            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        // ---- per-cell test of the candidates, ordered ballot append
+        for (int j = 0; j < nc; j += 32) {
+            const int q = j + lane;
+            const bool hit = q < nc && (rggd::overlaps(cb, cbox[q]) | rggd::overlaps(cb, cbox[q] + 6));
+            const unsigned hb = __ballot_sync(0xffffffffu, hit);
             if (hit) {
-                const int pos = count + __popc(bal & ((1u << lane) - 1u));
-                if (pos < s.cap) inl[pos] = base + e;
+                const int pos = count + __popc(hb & ((1u << lane) - 1u));
+                if (pos < s.cap) inl[pos] = cidx[q];
             }
-            count += __popc(bal);
+            count += __popc(hb);
         }
     }
     if (!live) return;
     if (count > s.cap) {
-        // Overflow: the full ordered list goes to the pool (second pass).
+        // Overflow: the full ordered list goes to the pool (second pass over the events).
         int pbase = 0;
         if (lane == 0) {
             pbase = atomicAdd(&b.ctr[1], count);
@@ -359,8 +428,8 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
                 const int e = e0 + lane;
                 bool hit = false;
                 if (e < b.n) {
-                    const Event& ev = b.ev[e];
-                    hit = rggd::overlaps(cb, ev.nu) || rggd::overlaps(cb, ev.old);
+                    const double* bx = b.evbox + 12 * static_cast<size_t>(e);
+                    hit = rggd::overlaps(cb, bx) || rggd::overlaps(cb, bx + 6);
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, hit);
                 if (hit) b.pool[pbase + at + __popc(bal & ((1u << lane) - 1u))] = e;
@@ -374,7 +443,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
         int mbase = 0;
         if (count > 0) {
             b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
-            // mask block of the touch / narrow / apply kernels: 3 * ceil(count/32) words per component
+            // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
             const long long need = 3ll * ((count + 31) >> 5) * s.cell;
             const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
                                              static_cast<unsigned long long>(need));
@@ -391,11 +460,33 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
 // ----------------------------------------------------------------- classify
 
 // batch_over for one (component, obstacle) pair: any body intersects (engine_batch.cpp:55-74).
+// filter outcome counters (tests / RGG_DEBUG_TIMING): [0] SAT filtered, [1] SAT rechecked in
+// fp64, [2] seg-sphere filtered, [3] seg-sphere rechecked
+__device__ unsigned long long g_filter_stats[4];
+
+// The exact fp64 rechecks run for a handful of pairs per update; kept out of
+// line so their register footprint does not cap the classify kernel's occupancy.
+__device__ __noinline__ bool sat_exact(const double* a, const double* b) {
+    atomicAdd(&g_filter_stats[1], 1ull);
+    return rggd::sat_boxes<false>(a, b, nullptr);
+}
+__device__ __noinline__ bool seg_exact(const double* seg, const double* c, double r_total) {
+    atomicAdd(&g_filter_stats[3], 1ull);
+    return rggd::seg_sphere_fast(seg, c, r_total);
+}
+
 template <bool COUNT>
-__device__ __forceinline__ bool over_test(const Store& s, int c, const double* osat, long long* cost) {
+__device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev, long long* cost) {
+    const double* osat = ev.sat;
     if (!COUNT) {
+        // fp32 filter with an exact fp64 recheck of undecided pairs (rgg_device.cuh)
         bool hit = false;
-        for (int b = 0; b < s.B && !hit; ++b) hit = rggd::sat_boxes_flat(s.sat + (static_cast<size_t>(c) * s.B + b) * 22, osat);
+        for (int b = 0; b < s.B && !hit; ++b) {
+            const size_t i = static_cast<size_t>(c) * s.B + b;
+            const double* a = s.sat + i * 22;
+            const int f = rggd::sat_filter32(a, s.sat32[i], osat, ev.b32);
+            hit = f == 2 ? sat_exact(a, osat) : f == 1;
+        }
         return hit;
     }
     bool hit = false;
@@ -472,10 +563,12 @@ __device__ __forceinline__ bool under_part(const Store& s, int c, const Event& e
         const double2 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3];
         const double seg[7] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x};
         for (int sp = 0; sp < ev.nsph; ++sp) {
-            if (COUNT) *tests += 1;
-            if (rggd::seg_sphere_fast(seg, ev.cen + 3 * sp, r_total)) {
-                hit = true;
-                if (!COUNT) return true;
+            if (COUNT) {
+                *tests += 1;
+                hit |= rggd::seg_sphere_fast(seg, ev.cen + 3 * sp, r_total);
+            } else {
+                const int f = rggd::seg_filter32(seg, ev.cen + 3 * sp, r_total);
+                if (f == 1 || (f == 2 && seg_exact(seg, ev.cen + 3 * sp, r_total))) return true;
             }
         }
     }
@@ -522,8 +615,8 @@ __device__ __forceinline__ const int32_t* rec_list(int4 r) {
 
 // Narrow tests of a pair whose item did not fit the queue (kept out of line so
 // the touch kernel's register budget stays that of an AABB filter).
-__device__ __noinline__ bool over_inline(const Store& s, int c, const double* osat) {
-    return over_test<false>(s, c, osat, nullptr);
+__device__ __noinline__ bool over_inline(const Store& s, int c, const Event& ev) {
+    return over_test<false>(s, c, ev, nullptr);
 }
 __device__ __noinline__ bool under_inline(const Store& s, int c, const Event& ev) {
     return under_part<false>(s, c, ev, 0, 1, nullptr);
@@ -622,7 +715,7 @@ __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
             const int k = __ffs(x) - 1;
             if (at < b.items_cap)
                 b.items_over[at] = make_int4(c, sev[k], wo, 1 << k);
-            else if (over_inline(s, c, b.ev[sev[k]].sat))
+            else if (over_inline(s, c, b.ev[sev[k]]))
                 b.mpool[wo] |= 1u << k;  // this thread owns the word until the narrow kernel
         }
         at = s_bu + wbu + xu - nu;
@@ -666,7 +759,7 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
     for (int i = gt; i < n_over; i += nthreads) {
         const int4 it = b.items_over[i];  // component, event, result word, bit
-        const bool h = over_test<COUNT>(s, it.x, b.ev[it.y].sat, &c_sat);
+        const bool h = over_test<COUNT>(s, it.x, b.ev[it.y], &c_sat);
         if (COUNT) c_op += s.B, c_oh += h;
         if (h) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
     }
@@ -871,7 +964,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
-    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0;
+    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
     int dgray = 0;
     for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
         const int c0 = q << 5;
@@ -945,6 +1038,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
             }
             any_box |= bm != 0;
             any_sph |= sm != 0;
+            if (CENSUS) c_touch += __popc(tm);
+            // pull this lane's narrow operands towards the SM now: the work list is
+            // drained by other lanes of the warp, which then hit in L1
+            if (bm) {
+                const size_t i0 = static_cast<size_t>(c) * s.B;
+                prefetch_range(s.sat + i0 * 22, s.sat + (i0 + s.B) * 22, true);
+                prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, true);
+            }
+            if (sm) prefetch_range(s.seg + 8 * static_cast<size_t>(seg_lo), s.seg + 8 * static_cast<size_t>(seg_hi), true);
             if (base == 0) RGG_STAMP(3)
             // ---- warp-local narrow work list
             const int no = __popc(bm), nu = __popc(sm);
@@ -965,7 +1067,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
             if (base == 0) RGG_STAMP(4)
             for (int i = lane; i < tot_o; i += 32) {
                 const int it = sitem[wi][0][i], t = it >> 5, k = it & 31;
-                const bool h = over_test<CENSUS>(s, c0 + t, b.ev[sev[wi][k]].sat, &c_sat);
+                const bool h = over_test<CENSUS>(s, c0 + t, b.ev[sev[wi][k]], &c_sat);
                 if (CENSUS) c_op += s.B, c_oh += h;
                 if (h) atomicOr(&sres[wi][0][t], 1u << k);
             }
@@ -974,7 +1076,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
                 const int i = ub + lane / kUnderLanes;
                 bool h = false;
                 int t = 0, k = 0;
-                if (i < tot_u) {
+                if (i < tot_u && (!CENSUS || g == 0)) {  // census: one lane counts the whole item
                     const int it = sitem[wi][1][i];
                     t = it >> 5;
                     k = it & 31;
@@ -988,7 +1090,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
                         h = h || other;
                     }
                 }
-                if (i < tot_u && (CENSUS || g == 0)) {
+                if (i < tot_u && g == 0) {
                     if (CENSUS) c_up += 1, c_uh += h;
                     if (h) atomicOr(&sres[wi][1][t], 1u << k);
                 }
@@ -1090,13 +1192,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
         }
     }
     if (CENSUS) {
-        long long v[10] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh, 0, 0, 0, 0};
+        long long v[11] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh, 0, 0, 0, 0, 0};
         v[6] = static_cast<long long>(c_dirty);
         v[7] = static_cast<long long>(c_box);
         v[8] = static_cast<long long>(c_sph);
         v[9] = static_cast<long long>(c_segs);
+        v[10] = static_cast<long long>(c_touch);
 #pragma unroll
-        for (int k = 0; k < 10; ++k) {
+        for (int k = 0; k < 11; ++k) {
             long long x = v[k];
             for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
             if (lane == 0 && x) atomicAdd(&b.census[k < 6 ? k : k + 2], static_cast<unsigned long long>(x));
@@ -1226,9 +1329,7 @@ __global__ void pair_masks_kernel(Store s, const int32_t* rank, int kind, const 
     const Event& ev = s.cur[o];
     bool h;
     if (kind == 0) {
-        double osat[21];
-        for (int k = 0; k < 21; ++k) osat[k] = ev.sat[k];
-        h = over_test<false>(s, c, osat, nullptr);
+        h = over_test<false>(s, c, ev, nullptr);
     } else {
         h = under_test<false>(s, c, ev, nullptr);
     }
@@ -1268,7 +1369,7 @@ cudaError_t launch_init_obstacles(const Store& s, Event*, cudaStream_t st) {
 }
 
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
-    const int cells_per = kBinThreads / 32;
+    const int cells_per = kBinThreads / 32;  // = kSuperCells
     bin_kernel<<<(s.ncells + cells_per - 1) / cells_per, kBinThreads, 0, st>>>(s, b);
     return cudaGetLastError();
 }
@@ -1340,6 +1441,14 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
             return wide ? apply_t<kHits, true>(s, b, st) : apply_t<kHits, false>(s, b, st);
         default:
             return wide ? apply_t<kPerMove | kHits, true>(s, b, st) : apply_t<kPerMove | kHits, false>(s, b, st);
+    }
+}
+
+void filter_stats(unsigned long long* out, bool reset) {
+    cudaMemcpyFromSymbol(out, g_filter_stats, sizeof(g_filter_stats));
+    if (reset) {
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_filter_stats, z, sizeof(z));
     }
 }
 

@@ -5,11 +5,14 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "rgg_device.cuh"
+
 namespace rggk {
 
 constexpr int kMaxSpheres = 16;  // obstacle inner spheres per event (C)
 constexpr int kEvChunk = 32;     // events staged in shared memory per pass (one bit each)
-constexpr int kMaxCell = 128;    // components per cell = threads per classify CTA
+constexpr int kMaxCell = 128;
+constexpr int kSuperCells = 16;  // cells per binning super-cell (= warps per bin CTA)    // components per cell = threads per classify CTA
 
 // One obstacle move after re-posing (BatchLayout::update_transforms,
 // proj/src/batch_layout.cpp:148-172), plus the obstacle's previous union box.
@@ -21,6 +24,7 @@ struct alignas(16) Event {
     double nu[6];    // box U sph (new pose)
     double old[6];   // box U sph at the pose before this move (empty if inactive)
     double cen[kMaxSpheres * 3];
+    rggd::Box32 b32;  // fp32 operand of sat (filter), L rounded up
     int32_t o;
     int32_t nsph;
     int32_t move;  // index of the move in the batch
@@ -37,11 +41,13 @@ struct Store {
     int32_t use_under;
     const double2* aabb;       // 3 planes of Np double2: (minx,miny) (minz,maxx) (maxy,maxz)
     const double* sat;         // Np*B*22 (21 + pad)
+    const rggd::Box32* sat32;  // Np*B fp32 filter operands of sat
     const int32_t* row;        // Np*B*S+1
     const double* seg;         // T*8 (a, d, dd, pad)
     const double* spline_r;    // B*S
     const int32_t* orig;       // Np: sorted -> component id
     const double* cell_aabb;   // ncells*6
+    const double* super_aabb;  // ceil(ncells/16)*6: union box of 16 consecutive cells (binning filter)
     const double* ohe;         // M*3
     const double* osl;         // M*C*3
     const double* osr;         // M
@@ -61,6 +67,7 @@ struct Batch {
     const double* rt;
     uint8_t* last;         // 1 if this is the obstacle's last move in this batch (pose kernel)
     Event* ev;             // n
+    double* evbox;         // n*12: new and old union box of each event (compact, for the binning)
     int32_t* cell_count;   // ncells
     int32_t* cell_list;    // ncells*cap
     int32_t* cell_ovf;     // ncells: base in pool when count > cap
@@ -96,5 +103,6 @@ cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, con
 cudaError_t launch_init_obstacles(const Store& s, Event* scratch, cudaStream_t st);
 cudaError_t launch_fp64_peak(double* sink, int iters, int grid, int block, cudaStream_t st);
 int classify_occupancy(int cell, int flags);
+void filter_stats(unsigned long long* out, bool reset);
 
 }  // namespace rggk

@@ -1,0 +1,114 @@
+"""Adversarial parity for the fp32 filters + fp64 recheck (rgg_device.cuh sat_filter32 /
+seg_filter32): boxes and segments placed exactly at, and a few ulps / 1e-12 .. 1e-7
+around, the contact configuration, with random rotations (so cross axes decide).
+The GPU verdicts (batch_over / batch_under, the filter path) must equal the exact
+fp64 reference sequence of the C oracle on every pair."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+OFFSETS = [0.0, 1e-15, -1e-15, 1e-12, -1e-12, 1e-9, -1e-9, 1e-7, -1e-7, 3e-6, -3e-6]
+
+
+def rot(rng):
+    q = rng.normal(size=4)
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                     [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                     [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+
+
+def corners(c, R, he):
+    out = []
+    for i in range(8):
+        p = c.copy()
+        for k in range(3):
+            s = 1.0 if (i >> k) & 1 else -1.0
+            p = p + s * he[k] * R[:, k]
+        out.append(p)
+    return np.concatenate(out)
+
+
+def test_sat_filter_adversarial():
+    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+
+    rng = np.random.default_rng(7)
+    he_o = np.array([1.3, 0.7, 0.9])
+    Ro = rot(rng)
+    pose = np.concatenate([Ro.reshape(-1), [0.4, -0.3, 0.2]])
+    osat, _, _, _ = oracle.obstacle_operands(he_o, np.zeros((1, 3)), 1, 0.1, pose)
+    boxes = []
+    for trial in range(300):
+        R = rot(rng) if trial % 3 else np.eye(3)
+        he = rng.uniform(0.05, 2.0, 3)
+        n = rng.normal(size=3)
+        n /= np.linalg.norm(n)
+        if trial % 3 == 0:  # face contact along the obstacle's own axis
+            R = Ro.copy()
+            n = Ro[:, trial % 3]
+        # bisection for the contact distance along n (exact fp64 verdicts)
+        lo, hi = 0.0, 20.0
+        for _ in range(80):
+            mid = 0.5 * (lo + hi)
+            s = oracle.sat_prep(corners(pose[9:] + mid * n, R, he))
+            lo, hi = (mid, hi) if oracle.sat_boxes(s, osat) else (lo, mid)
+        for off in OFFSETS:
+            t = lo * (1 + off) + off
+            boxes.append(oracle.sat_prep(corners(pose[9:] + t * n, R, he)))
+        boxes.append(oracle.sat_prep(corners(pose[9:] + np.nextafter(lo, 0) * n, R, he)))
+        boxes.append(oracle.sat_prep(corners(pose[9:] + np.nextafter(hi, 30) * n, R, he)))
+    boxes = np.array(boxes)
+    N = len(boxes)
+    lv = LayoutView(N=N, B=1, S=1, M=1, C=1, edge_sat=boxes,
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (N, 1)).astype(np.float64),
+                    row_off=np.zeros(N + 1, np.int32), segs=np.zeros((0, 7)), spline_r=np.zeros(1),
+                    obst_he=he_o[None, :], obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.array([0.1]),
+                    obst_sph_n=np.ones(1, np.int32))
+    eng = GpuEngine(lv)
+    eng.update_obstacle(0, pose)
+    got = eng.batch_over(np.arange(N, dtype=np.int32), 0)
+    exp = oracle.sat_batch(boxes, np.arange(N, dtype=np.int32), osat)
+    assert 0 < exp.sum() < N
+    assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
+
+
+def test_seg_filter_adversarial():
+    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+
+    rng = np.random.default_rng(11)
+    r = 0.7
+    centre = np.array([1.1, -2.3, 0.6])
+    segs = []
+    for trial in range(400):
+        n = rng.normal(size=3)
+        n /= np.linalg.norm(n)
+        t = np.cross(n, rng.normal(size=3))
+        t /= np.linalg.norm(t)
+        L = rng.uniform(0.0, 2.0) if trial % 5 else 0.0  # include point segments
+        shift = rng.uniform(-1.0, 1.0) * L
+        for off in OFFSETS:
+            base = centre + n * r * (1 + off)
+            a = base + t * (shift - L)
+            b = base + t * (shift + L)
+            if trial % 7 == 3:  # endpoint contact instead of interior contact
+                a = base
+                b = base + n * L
+            segs.append(oracle.seg_prep(np.concatenate([a, b])))
+    segs = np.array(segs)
+    N = len(segs)
+    pose = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, *centre])
+    lv = LayoutView(N=N, B=1, S=1, M=1, C=1, edge_sat=np.zeros((N, 21)),
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (N, 1)).astype(np.float64),
+                    row_off=np.arange(N + 1, dtype=np.int32), segs=segs, spline_r=np.array([r]),
+                    obst_he=np.ones((1, 3)), obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.zeros(1),
+                    obst_sph_n=np.ones(1, np.int32))
+    eng = GpuEngine(lv)
+    eng.update_obstacle(0, pose)
+    got = eng.batch_under(np.arange(N, dtype=np.int32), 0)
+    exp = oracle.seg_sphere_batch(segs, np.arange(N, dtype=np.int32), centre, r)
+    assert 0 < exp.sum() < N
+    assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} segment-sphere verdicts differ"
