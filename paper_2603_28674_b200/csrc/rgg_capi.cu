@@ -164,6 +164,20 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     return RGG_OK;
 }
 
+int grow_items(rgg_gpu* h, int64_t need) {
+    const int64_t cap = std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(2 * need, h->items_cap));
+    if (cap <= h->items_cap) return fail(h, RGG_ENOMEM, "narrow item queue cannot grow further; split the batch");
+    cudaFree(h->d_items_over);
+    cudaFree(h->d_items_under);
+    h->d_items_over = nullptr;
+    h->d_items_under = nullptr;
+    CK(dalloc(&h->d_items_over, static_cast<size_t>(cap)));
+    CK(dalloc(&h->d_items_under, static_cast<size_t>(cap)));
+    h->items_cap = static_cast<int32_t>(cap);
+    ++h->gen;  // captured graphs hold the old queue pointers
+    return RGG_OK;
+}
+
 int grow_pinned(rgg_gpu* h, int32_t n) {
     if (n <= h->cap_pin) return RGG_OK;
     const int32_t cap = std::max(n, std::max(64, h->cap_pin * 2));
@@ -273,7 +287,25 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     CK(cudaEventRecord(h->ev[2], h->stream));
     CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
     if (phase("classify")) return RGG_ECUDA;
-    if (b.dbg) {
+    if (b.dbg && std::getenv("RGG_DEBUG_NARROW")) {
+        const size_t nw = static_cast<size_t>(h->grid_classify) * 4;
+        std::vector<unsigned long long> t(nw * 4);
+        CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        unsigned long long lo = ~0ull, hi = 0;
+        std::vector<double> st, du;
+        for (size_t w = 0; w < nw; ++w)
+            if (t[4 * w] && t[4 * w + 1]) lo = std::min(lo, t[4 * w]), hi = std::max(hi, t[4 * w + 1]);
+        for (size_t w = 0; w < nw; ++w)
+            if (t[4 * w] && t[4 * w + 1]) st.push_back((t[4 * w] - lo) * 1e-3), du.push_back((t[4 * w + 1] - t[4 * w]) * 1e-3);
+        std::sort(st.begin(), st.end());
+        std::sort(du.begin(), du.end());
+        const size_t n = st.size();
+        if (n)
+            std::fprintf(stderr, "[rgg] narrow warps %zu span %.1f us | start p50 %.1f p90 %.1f max %.1f | dur p50 %.1f p90 %.1f max %.1f | items %llu/%llu\n",
+                         n, (hi - lo) * 1e-3, st[n / 2], st[n * 9 / 10], st[n - 1], du[n / 2], du[n * 9 / 10], du[n - 1], t[2], t[3]);
+        CK(cudaMemsetAsync(b.dbg, 0, t.size() * 8, h->stream));
+    } else if (b.dbg) {
         const size_t ns = static_cast<size_t>((h->s.Np + 31) / 32);
         std::vector<unsigned long long> t(ns * 16);
         CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -505,7 +537,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_unknown, 1));
     CK(dalloc(&h->d_census, 16));
     CK(dalloc(&h->d_crec, ncells));
-    h->items_cap = static_cast<int32_t>(std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(1 << 16, 4ll * Np)));
+    h->items_cap = static_cast<int32_t>(std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(1 << 16, 8ll * Np)));
     CK(dalloc(&h->d_items_over, h->items_cap));
     CK(dalloc(&h->d_items_under, h->items_cap));
     CK(dalloc(&h->d_gray, N));
@@ -515,7 +547,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_cell_list, static_cast<size_t>(ncells) * cap));
     CK(dalloc(&h->d_cell_ovf, ncells));
     CK(dalloc(&h->d_dirty, ncells));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 8 * sizeof(int32_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 16 * sizeof(int32_t), 0));
     auto up = [&](void* dst, const void* src, size_t bytes) {
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream) : cudaSuccess;
     };
@@ -558,6 +590,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.ncells = ncells;
     s.cap = cap;
     s.use_under = o.use_under ? 1 : 0;
+    s.dbg_flags = std::getenv("RGG_DEBUG_FLAGS") ? std::atoi(std::getenv("RGG_DEBUG_FLAGS")) : 0;
     s.aabb = h->d_aabb;
     s.sat = h->d_sat;
     s.sat32 = h->d_sat32;
@@ -644,8 +677,25 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
                                             cudaMemcpyDeviceToHost, h->stream));
             CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 7 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaMemcpyAsync(h->h_ctr + 7, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(h->h_ctr + 8, h->d_ctr + 8, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
-            if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, h->h_ctr[6] == 1 ? "overflow pool exhausted" : "mask pool exhausted");
+            for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {
+                // the update was not applied (apply kernel skipped): grow the queue and replay it
+                rc = grow_items(h, std::max<int64_t>(h->h_ctr[8], h->h_ctr[9]));
+                if (rc) return rc;
+                rc = enqueue(h, k, flags);
+                if (rc) return rc;
+                if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
+                                                cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 7 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(h->h_ctr + 7, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(h->h_ctr + 8, h->d_ctr + 8, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+            }
+            if (h->h_ctr[6])
+                return fail(h, RGG_ELOGIC, h->h_ctr[6] == 1   ? "overflow pool exhausted"
+                                           : h->h_ctr[6] == 2 ? "mask pool exhausted"
+                                                              : "narrow item queue full (split the batch)");
             h->unknown = h->h_ctr[7];
             h->unknown_stale = false;
             if (reports) {
@@ -697,7 +747,17 @@ int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12
 int rgg_gpu_sync(rgg_gpu* h) {
     if (!h) return RGG_EINVAL;
     CK(cudaSetDevice(h->device));
+    int32_t err = 0;
+    CK(cudaMemcpyAsync(&err, h->d_ctr + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (err == 3) {
+        int32_t need[2] = {0, 0};
+        CK(cudaMemcpy(need, h->d_ctr + 8, sizeof(need), cudaMemcpyDeviceToHost));
+        const int rc = grow_items(h, std::max(need[0], need[1]));
+        if (rc) return rc;
+        return fail(h, RGG_ELOGIC, "narrow item queue was full: the last asynchronous update was not applied "
+                                   "(queue grown; resubmit it)");
+    }
     return RGG_OK;
 }
 

@@ -608,6 +608,23 @@ constexpr int kOverLanes = 1;   // lanes per SAT work item (4 was slower: operan
 // GPU and ORs the verdicts into the result words; apply replays each
 // component's events in move order from the three words.
 
+// Commit the moved obstacles' operands for the next batch (s.cur, s.cur_union):
+// one 16-byte word per thread over the whole grid.  Nothing between the pose
+// kernel and the end of the update reads s.cur / s.cur_union.
+__device__ __forceinline__ void commit_grid(const Store& s, const Batch& b) {
+    constexpr int kVec = sizeof(Event) / 16 + 1;  // + the 6-double union box
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int w = gt; w < b.n * kVec; w += gridDim.x * blockDim.x) {
+        const int i = w / kVec, k = w % kVec;
+        if (!b.last[i]) continue;
+        const int o = b.ids[i];
+        if (k < kVec - 1)
+            reinterpret_cast<int4*>(&s.cur[o])[k] = reinterpret_cast<const int4*>(&b.ev[i])[k];
+        else
+            for (int j = 0; j < 6; ++j) s.cur_union[6 * o + j] = b.ev[i].nu[j];
+    }
+}
+
 __device__ __forceinline__ const int32_t* rec_list(int4 r) {
     return reinterpret_cast<const int32_t*>((static_cast<unsigned long long>(static_cast<uint32_t>(r.w)) << 32) |
                                             static_cast<uint32_t>(r.z));
@@ -644,6 +661,7 @@ __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
     __shared__ int s_no, s_nu, s_bo, s_bu;
     __shared__ unsigned long long scen[4];
     const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    commit_grid(s, b);
     const int4 rec = b.crec[cell];
     const int count = rec.x;
     if (count == 0) return;
@@ -755,6 +773,8 @@ template <bool COUNT>
 __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
+    unsigned long long* dbgw = (!COUNT && b.dbg) ? b.dbg + 4 * static_cast<size_t>(gt >> 5) : nullptr;
+    if (dbgw && lane == 0) dbgw[0] = gtimer();
     const int n_over = min(b.ctr[8], b.items_cap), n_under = min(b.ctr[9], b.items_cap);
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
     for (int i = gt; i < n_over; i += nthreads) {
@@ -778,6 +798,10 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
         if (COUNT) c_up += 1, c_uh += h;
         if (h && (COUNT || g == 0)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
     }
+    if (dbgw) {
+        __syncwarp();
+        if (lane == 0) dbgw[1] = gtimer(), dbgw[2] = static_cast<unsigned long long>(n_over), dbgw[3] = n_under;
+    }
     if (COUNT) {
         long long v[6] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh};
 #pragma unroll
@@ -787,18 +811,6 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
             if (lane == 0 && x) atomicAdd(&b.census[k], static_cast<unsigned long long>(x));
         }
         return;
-    }
-    if (blockIdx.x == 0) {
-        // commit (one warp per move): operands and union box of each obstacle's last move
-        constexpr int kVec = sizeof(Event) / 16;
-        for (int i = threadIdx.x >> 5; i < b.n; i += blockDim.x >> 5) {
-            if (!b.last[i]) continue;
-            const int o = b.ids[i];
-            const int4* src = reinterpret_cast<const int4*>(&b.ev[i]);
-            int4* dst = reinterpret_cast<int4*>(&s.cur[o]);
-            for (int k = lane; k < kVec; k += 32) dst[k] = src[k];
-            if (lane < 6) s.cur_union[6 * o + lane] = b.ev[i].nu[lane];
-        }
     }
 }
 
@@ -963,10 +975,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
     __shared__ int2 som[kWarpsPerCta][32];        // per event: obstacle id, move index
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
+    if (!CENSUS) commit_grid(s, b);
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
     unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
     int dgray = 0;
-    for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
+    // slices near an obstacle are Morton-adjacent and heavy: spread them over warps / SMs by
+    // walking the slices with a prime stride (a bijection when it does not divide nslices)
+    const long long stride = (nslices % 7919) ? 7919 : 1;
+    for (int q0 = blockIdx.x * kWarpsPerCta + wi; q0 < nslices; q0 += gridDim.x * kWarpsPerCta) {
+        const int q = static_cast<int>((q0 * stride) % nslices);
         const int c0 = q << 5;
         const int cell = c0 / s.cell;
         const int4 rec = b.crec[cell];
@@ -1067,6 +1084,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
             if (base == 0) RGG_STAMP(4)
             for (int i = lane; i < tot_o; i += 32) {
                 const int it = sitem[wi][0][i], t = it >> 5, k = it & 31;
+                if (!CENSUS && (s.dbg_flags & 1)) {  // ablation: no test
+                    if ((s.dbg_flags & 2) == 0 && s.sat[(c0 + t) * 22] == 12345.0) atomicOr(&sres[wi][0][t], 1u << k);
+                    continue;
+                }
                 const bool h = over_test<CENSUS>(s, c0 + t, b.ev[sev[wi][k]], &c_sat);
                 if (CENSUS) c_op += s.B, c_oh += h;
                 if (h) atomicOr(&sres[wi][0][t], 1u << k);
@@ -1080,6 +1101,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
                     const int it = sitem[wi][1][i];
                     t = it >> 5;
                     k = it & 31;
+                    if (!CENSUS && (s.dbg_flags & 1))  // ablation: no test
+                        h = (s.dbg_flags & 2) == 0 && s.seg[8 * static_cast<size_t>(seg_lo)] == 12345.0;
+                    else
                     h = under_part<CENSUS>(s, c0 + t, b.ev[sev[wi][k]], CENSUS ? 0 : g, CENSUS ? 1 : kUnderLanes,
                                            &c_tests);
                 }
@@ -1209,18 +1233,255 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
     // running gray count (the unknown_count of the reference)
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
     if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
-    // commit the moved obstacles' operands (CTA 0, one warp per move)
-    if (blockIdx.x == 0) {
-        constexpr int kVec = sizeof(Event) / 16;
-        for (int i = wi; i < b.n; i += kWarpsPerCta) {
-            if (!b.last[i]) continue;
-            const int o = b.ids[i];
-            const int4* src = reinterpret_cast<const int4*>(&b.ev[i]);
-            int4* dst = reinterpret_cast<int4*>(&s.cur[o]);
-            for (int k = lane; k < kVec; k += 32) dst[k] = src[k];
-            if (lane < 6) s.cur_union[6 * o + lane] = b.ev[i].nu[lane];
+}
+
+// ------------------------------------------------- v6: warp-slice touch / GPU-wide narrow / warp-slice apply
+//
+// v4 split at its narrow phase.  A warp owns a 32-component slice (as in v4)
+// for the touch masks and for the transitions, but the narrow tests of all
+// slices are drained by one GPU-wide kernel (one (component, event) item per
+// thread, 4 lanes per segment-sphere item), so a slice next to an obstacle no
+// longer serialises its SAT / segment rounds on one warp.  Masks live in the
+// per-cell mask blocks the bin kernel reserves (word (kind*W + w)*cell + t).
+
+template <bool CENSUS>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, Batch b) {
+    __shared__ double sbx[kWarpsPerCta][32][24];
+    __shared__ int sev[kWarpsPerCta][32];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nslices = (s.Np + 31) >> 5;
+    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
+    for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
+        const int c0 = q << 5;
+        const int cell = c0 / s.cell;
+        const int4 rec = b.crec[cell];
+        const int count = rec.x;
+        if (count == 0) continue;  // warp-uniform: clean cell
+        const int c = c0 + lane, t = c - cell * s.cell;
+        const bool valid = c < s.Np;
+        double aabb[6];
+        int seg_lo = 0, seg_hi = 0;
+        if (valid) {
+            const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
+            aabb[0] = a0.x, aabb[1] = a0.y, aabb[2] = a1.x, aabb[3] = a1.y, aabb[4] = a2.x, aabb[5] = a2.y;
+            seg_lo = s.row[c * s.B * s.S];
+            seg_hi = s.row[(c + 1) * s.B * s.S];
+        }
+        const int32_t* list = rec_list(rec);
+        const int W = (count + 31) >> 5;
+        bool any_box = false, any_sph = false;
+        for (int base = 0, w = 0; base < count; base += 32, ++w) {
+            const int m = min(32, count - base);
+            const int myev = lane < m ? list[base + lane] : 0;
+            sev[wi][lane] = myev;
+            if (lane < m) {
+                const Event& ev = b.ev[myev];
+                double v[24];
+#pragma unroll
+                for (int j = 0; j < 6; ++j) v[j] = ev.nu[j], v[6 + j] = ev.old[j], v[12 + j] = ev.box[j], v[18 + j] = ev.sph[j];
+#pragma unroll
+                for (int j = 0; j < 24; ++j) sbx[wi][lane][j] = v[j];
+            }
+            __syncwarp();
+            uint32_t tm = 0, bm = 0, sm = 0;
+            if (valid) {
+                for (int k = 0; k < m; ++k) {
+                    const double* bx = sbx[wi][k];
+                    const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
+                    tm |= static_cast<uint32_t>(touch) << k;
+                    bm |= static_cast<uint32_t>(touch & rggd::overlaps(aabb, bx + 12)) << k;
+                    sm |= static_cast<uint32_t>(touch & (s.use_under != 0) & rggd::overlaps(aabb, bx + 18)) << k;
+                }
+            }
+            any_box |= bm != 0;
+            any_sph |= sm != 0;
+            if (CENSUS) {
+                c_touch += __popc(tm);
+                __syncwarp();
+                continue;
+            }
+            // the narrow kernel (next launch) reads exactly these operands: stage them in L2 now
+            if (bm && w == 0) {
+                const size_t i0 = static_cast<size_t>(c) * s.B;
+                prefetch_range(s.sat + i0 * 22, s.sat + (i0 + s.B) * 22, false);
+                prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, false);
+            }
+            if (sm && w == 0) {
+                prefetch_l2(s.row + c * s.B * s.S);
+                prefetch_range(s.seg + 8 * static_cast<size_t>(seg_lo), s.seg + 8 * static_cast<size_t>(seg_hi), false);
+            }
+            const int wt = rec.y + (0 * W + w) * s.cell + t, wo = rec.y + (1 * W + w) * s.cell + t,
+                      wu = rec.y + (2 * W + w) * s.cell + t;
+            if (valid) {
+                b.mpool[wt] = tm;
+                b.mpool[wo] = 0;
+                b.mpool[wu] = 0;
+            }
+            // one warp-aggregated reservation per queue and chunk
+            // (the queues hold 8 items per owned component; a fuller queue is reported, ctr[6] = 3)
+            int at = warp_reserve(&b.ctr[8], __popc(bm));
+            for (uint32_t x = bm; x; x &= x - 1, ++at) {
+                const int k = __ffs(x) - 1;
+                if (at < b.items_cap) b.items_over[at] = make_int4(c, sev[wi][k], wo, 1 << k);
+                else b.ctr[6] = 3;
+            }
+            at = warp_reserve(&b.ctr[9], __popc(sm));
+            for (uint32_t x = sm; x; x &= x - 1, ++at) {
+                const int k = __ffs(x) - 1;
+                if (at < b.items_cap) b.items_under[at] = make_int4(c, sev[wi][k], wu, 1 << k);
+                else b.ctr[6] = 3;
+            }
+            __syncwarp();
+        }
+        if (CENSUS && valid) {
+            c_dirty += 1;
+            c_box += any_box;
+            c_sph += any_sph;
+            if (any_sph) c_segs += seg_hi - seg_lo;
         }
     }
+    if (CENSUS) {
+        unsigned long long v[5] = {c_dirty, c_box, c_sph, c_segs, c_touch};
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            unsigned long long x = v[k];
+            for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+            if (lane == 0 && x) atomicAdd(&b.census[8 + k], x);
+        }
+    }
+}
+
+template <int FLAGS, bool WIDE>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, Batch b) {
+    constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
+    constexpr bool HITS = (FLAGS & kHits) != 0;
+    __shared__ int2 som[kWarpsPerCta][32];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nslices = (s.Np + 31) >> 5;
+    int dgray = 0;
+    // a full narrow-item queue left some verdicts uncomputed: apply nothing, so the
+    // engine stays at its pre-update state and the host can grow the queue and replay
+    if (b.ctr[6] == 3) return;
+    commit_grid(s, b);
+    for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
+        const int c0 = q << 5;
+        const int cell = c0 / s.cell;
+        const int4 rec = b.crec[cell];
+        const int count = rec.x;
+        if (count == 0) continue;
+        const int c = c0 + lane, t = c - cell * s.cell;
+        const bool valid = c < s.Np;
+        int label = 0, oc = 0, bc = 0, id = -1;
+        unsigned long long OW = 0, UW = 0;
+        if (valid) {
+            id = s.orig[c];
+            const uint32_t cw = s.cnt[c];
+            oc = cw & 0xffff;
+            bc = cw >> 16;
+            if (!WIDE) {
+                OW = s.over[c];
+                UW = s.under[c];
+            }
+            label = s.state[id];
+        }
+        const int label0 = label;
+        const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+        const unsigned long long OW0 = OW, UW0 = UW;
+        bool hit_last = false;
+        const int32_t* list = rec_list(rec);
+        const int W = (count + 31) >> 5;
+        for (int base = 0, w = 0; base < count; base += 32, ++w) {
+            const int m = min(32, count - base);
+            if (lane < m) {
+                const Event& ev = b.ev[list[base + lane]];
+                som[wi][lane] = make_int2(ev.o, ev.move);
+            }
+            uint32_t tm = 0, ro = 0, ru = 0;
+            if (valid) {
+                tm = b.mpool[rec.y + (0 * W + w) * s.cell + t];
+                ro = b.mpool[rec.y + (1 * W + w) * s.cell + t];
+                ru = b.mpool[rec.y + (2 * W + w) * s.cell + t];
+            }
+            __syncwarp();
+            for (int k = 0; k < m; ++k) {
+                const int before = label;
+                const int2 om = som[wi][k];
+                if ((tm >> k) & 1u) {
+                    const int o = om.x;
+                    const int wo = o >> 6;
+                    const unsigned long long bit = 1ull << (o & 63);
+                    unsigned long long ow, uw;
+                    if (WIDE) {
+                        ow = s.over[static_cast<size_t>(wo) * s.Np + c];
+                        uw = s.under[static_cast<size_t>(wo) * s.Np + c];
+                    } else {
+                        ow = OW;
+                        uw = UW;
+                    }
+                    const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
+                    const bool n_over = (ro >> k) & 1u, n_under = (ru >> k) & 1u;
+                    if (old_over) {  // revalidate_old_intersections (engine_batch.cpp:114-143)
+                        oc -= 1;
+                        const int rest = bc - (old_under ? 1 : 0);
+                        label = oc == 0 ? 0 : ((s.use_under && rest > 0) ? 1 : 2);
+                    }
+                    if (n_over) {  // over phase (engine_batch.cpp:163-177)
+                        if (label == 0) label = 2;
+                        oc += 1;
+                    }
+                    if (n_under) label = 1;  // under phase (engine_batch.cpp:181-188)
+                    bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
+                    const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
+                    const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
+                    if (WIDE) {
+                        if (nw != ow) s.over[static_cast<size_t>(wo) * s.Np + c] = nw;
+                        if (nuw != uw) s.under[static_cast<size_t>(wo) * s.Np + c] = nuw;
+                    } else {
+                        OW = nw;
+                        UW = nuw;
+                    }
+                    if (HITS && om.y == b.n - 1) hit_last = n_over;
+                }
+                if (PER_MOVE) {
+                    const bool ch = label != before;
+                    const unsigned gg = __ballot_sync(0xffffffffu, ch && label == 0);
+                    const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
+                    const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
+                    const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
+                    if (lane == 0 && (gg | r | y | f)) {
+                        int* mv = b.mv + 4 * om.y;
+                        if (gg) atomicAdd(mv + 0, __popc(gg));
+                        if (r) atomicAdd(mv + 1, __popc(r));
+                        if (y) atomicAdd(mv + 2, __popc(y));
+                        if (f) atomicAdd(mv + 3, __popc(f));
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        if (valid) {
+            if (label != label0) {
+                s.state[id] = static_cast<uint8_t>(label);
+                dgray += (label == 2) - (label0 == 2);
+            }
+            const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+            if (cw != cnt0) s.cnt[c] = cw;
+            if (!WIDE) {
+                if (OW != OW0) s.over[c] = OW;
+                if (UW != UW0) s.under[c] = UW;
+            }
+        }
+        if (HITS) {
+            const bool h = valid && hit_last && label == 2;
+            const unsigned bal = __ballot_sync(0xffffffffu, h);
+            int pos = 0;
+            if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
+            pos = __shfl_sync(0xffffffffu, pos, 0);
+            if (h) b.hits[pos + __popc(bal & ((1u << lane) - 1u))] = id;
+        }
+    }
+    for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
+    if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
 }
 
 // --------------------------------------------------------------- compaction
@@ -1403,13 +1664,57 @@ static cudaError_t warp_t(const Store& s, const Batch& b, int grid, cudaStream_t
 static int pipeline() {
     static const int p = [] {
         const char* e = std::getenv("RGG_PIPELINE");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : 6;
     }();
     return p;
 }
 
+template <int F, bool W>
+static cudaError_t apply6_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {
+    apply_warp_kernel<F, W><<<grid, 32 * kWarpsPerCta, 0, st>>>(s, b);
+    return cudaGetLastError();
+}
+
+static int grid_slices(const Store& s, const void* fn) {
+    int per_sm = 0, sms = 0, dev = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarpsPerCta, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    per_sm = per_sm < 1 ? 1 : per_sm;
+    const int need = ((s.Np + 31) / 32 + kWarpsPerCta - 1) / kWarpsPerCta;
+    return need < per_sm * sms ? (need < 1 ? 1 : need) : per_sm * sms;
+}
+
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st) {
     if (s.ncells == 0) return cudaSuccess;
+    if (pipeline() == 6) {
+        static int g_touch = 0, g_touch_c = 0, g_apply = 0;
+        if (!g_touch) {
+            g_touch = grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>));
+            g_touch_c = grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<true>));
+            g_apply = grid_slices(s, reinterpret_cast<const void*>(apply_warp_kernel<kPerMove, false>));
+        }
+        if (flags & kCensus) {
+            touch_warp_kernel<true><<<g_touch_c, 32 * kWarpsPerCta, 0, st>>>(s, b);
+            narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
+            return cudaGetLastError();
+        }
+        touch_warp_kernel<false><<<g_touch, 32 * kWarpsPerCta, 0, st>>>(s, b);
+        narrow_kernel<false><<<grid, 128, 0, st>>>(s, b);
+        const bool wide = s.W > 1;
+        const int ga = g_apply;
+        switch (flags & (kPerMove | kHits)) {
+            case 0:
+                return wide ? apply6_t<0, true>(s, b, ga, st) : apply6_t<0, false>(s, b, ga, st);
+            case kPerMove:
+                return wide ? apply6_t<kPerMove, true>(s, b, ga, st) : apply6_t<kPerMove, false>(s, b, ga, st);
+            case kHits:
+                return wide ? apply6_t<kHits, true>(s, b, ga, st) : apply6_t<kHits, false>(s, b, ga, st);
+            default:
+                return wide ? apply6_t<kPerMove | kHits, true>(s, b, ga, st)
+                            : apply6_t<kPerMove | kHits, false>(s, b, ga, st);
+        }
+    }
     if (pipeline() == 4) {
         const int g = grid_warp(s);
         const bool wide = s.W > 1;

@@ -4,6 +4,30 @@
 #include <cuda_runtime.h>
 #include "../paper_2603_28674_b200/csrc/rgg_device.cuh"
 
+__global__ void filt_k(const double* boxes, const rggd::Box32* b32, const double* obst, int rounds,
+                       unsigned long long* cyc, int* sink) {
+    const int lane = threadIdx.x & 31;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) % 4096;
+    int acc = 0;
+    const long long t0 = clock64();
+    for (int r = 0; r < rounds; ++r) acc += rggd::sat_filter32(boxes + 22 * i, b32[i], obst + 22 * (r & 7), b32[r & 7]);
+    const long long t1 = clock64();
+    if (lane == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
+    if (acc == 12345) sink[0] = acc;
+}
+
+__global__ void segf_k(const double* segs, const double* cen, int rounds, unsigned long long* cyc, int* sink) {
+    const int lane = threadIdx.x & 31;
+    const double* s = segs + 8 * ((blockIdx.x * blockDim.x + threadIdx.x) % 4096);
+    int acc = 0;
+    const long long t0 = clock64();
+    for (int r = 0; r < rounds; ++r)
+        for (int sp = 0; sp < 5; ++sp) acc += rggd::seg_filter32(s, cen + 3 * ((r + sp) & 7), 0.6);
+    const long long t1 = clock64();
+    if (lane == 0) atomicAdd(cyc, (unsigned long long)(t1 - t0));
+    if (acc == 12345) sink[0] = acc;
+}
+
 template <int MODE>
 __global__ void sat_k(const double* boxes, const double* obst, int rounds, unsigned long long* cyc, int* sink) {
     const int lane = threadIdx.x & 31;
@@ -57,10 +81,13 @@ int main() {
     cudaMemcpy(dseg, hb, nb * 8 * 8, cudaMemcpyHostToDevice);
     cudaMalloc(&dcen, 8 * 3 * 8);
     cudaMemcpy(dcen, hb, 24 * 8, cudaMemcpyHostToDevice);
+    rggd::Box32* b32h = new rggd::Box32[nb];
+    for (int i = 0; i < nb; ++i) { double l = 0; for (int k = 0; k < 9; ++k) { b32h[i].e[k] = hb[22*i+3+k]; b32h[i].u[k] = hb[22*i+12+k]; l += fabs(hb[22*i+3+k]); } b32h[i].L = l * 1.0001; }
+    rggd::Box32* db32; cudaMalloc(&db32, nb * sizeof(rggd::Box32)); cudaMemcpy(db32, b32h, nb * sizeof(rggd::Box32), cudaMemcpyHostToDevice);
     unsigned long long* cyc; int* sink;
     cudaMalloc(&cyc, 8); cudaMalloc(&sink, 4);
     for (int warps_per_sm : {1, 4, 16, 32}) {
-        for (int mode = 0; mode < 3; ++mode) {
+        for (int mode = 0; mode < 5; ++mode) {
             cudaMemset(cyc, 0, 8);
             const int rounds = 64;
             const int block = 128, grid = 148 * warps_per_sm / 4 > 0 ? 148 * warps_per_sm / 4 : 148;
@@ -69,11 +96,13 @@ int main() {
             if (mode == 0) sat_k<0><<<g, bs>>>(db, dobst, rounds, cyc, sink);
             if (mode == 1) sat_k<1><<<g, bs>>>(db, dobst, rounds, cyc, sink);
             if (mode == 2) seg_k<<<g, bs>>>(dseg, dcen, rounds, cyc, sink);
+            if (mode == 3) filt_k<<<g, bs>>>(db, db32, db, rounds, cyc, sink);
+            if (mode == 4) segf_k<<<g, bs>>>(dseg, dcen, rounds, cyc, sink);
             cudaDeviceSynchronize();
             unsigned long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
             const double warps = double(g) * bs / 32;
             printf("warps/SM %2d %-14s cycles per warp-round %8.0f\n", warps_per_sm,
-                   mode == 0 ? "sat flat" : mode == 1 ? "sat early-exit" : "seg x5 spheres", c / warps / rounds);
+                   mode == 0 ? "sat flat" : mode == 1 ? "sat early-exit" : mode == 2 ? "seg x5 spheres" : mode == 3 ? "sat filter32" : "seg filter32 x5", c / warps / rounds);
         }
     }
     return 0;
