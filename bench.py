@@ -255,7 +255,10 @@ def main():
     # torch's current stream and DistributedUpdater orders the engine stream against it
     tstream = stream if dist is None else torch.cuda.current_stream(dev)
 
-    # ---- warm-up (device path), then K timed steps with L2 flushed in between
+    # ---- warm-up (device path), then K timed steps with L2 flushed in between; the
+    # per-kernel phase split is sampled afterwards (its events would serialise the
+    # pipeline's programmatic launches inside the timed steps)
+    eng.set_phase_timing(False)
     for it in range(args.warmup):
         step_device(it)
     torch.cuda.synchronize()
@@ -271,15 +274,22 @@ def main():
             ev[k][0].record(tstream)
             step_device(args.warmup + k)
             ev[k][1].record(tstream)
-            st = eng.last_stats()
-            classify_ms.append(st["classify_ms"])
-            stats.append(st)
         torch.cuda.synchronize()
         # keep the same load under the sampler for >= 1 s so clocks are observed under load
         while time.perf_counter() - t_clock0 < args.clock_window_s:
             step_device(args.warmup + (args.steps - 1))
             torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    # phase split (untimed): the same last steps again with per-kernel events
+    eng.set_phase_timing(True)
+    for k in range(min(5, args.steps)):
+        with torch.cuda.stream(tstream):
+            flush.zero_()
+        step_device(args.warmup + args.steps - 1 - k)
+        st = eng.last_stats()
+        classify_ms.append(st["classify_ms"])
+        stats.append(st)
+    eng.set_phase_timing(False)
     total_ms = float(sum(step_ms))
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)

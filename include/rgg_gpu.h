@@ -127,6 +127,9 @@ int rgg_gpu_sync(rgg_gpu* h);
  * counters, n x {to_green, to_red, to_gray, from_gray} int32 — the per-shard
  * report terms a multi-GPU driver sums with one all-reduce. */
 int rgg_gpu_copy_counters(rgg_gpu* h, void* dst_device, int32_t n);
+/* Per-kernel phase events in rgg_gpu_last_stats (default on).  Off lets the
+ * pipeline's kernels overlap their launch (PDL); only total_ms is then filled. */
+int rgg_gpu_set_phase_timing(rgg_gpu* h, int32_t on);
 
 int rgg_gpu_count(const rgg_gpu* h, int32_t* n_components, int32_t* n_obstacles, int32_t* words_per_comp);
 /* states(): N labels in component-id order (sharded handles: unowned entries are 0xFF). */

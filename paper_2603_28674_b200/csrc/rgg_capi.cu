@@ -98,6 +98,7 @@ struct rgg_gpu {
     };
     std::vector<GraphEntry> graphs;
     int32_t gen = 0;
+    bool phase_timing = true;  // per-kernel phase events (rgg_gpu_set_phase_timing)
     bool timed = false;
     int grid_classify = 1;
     int64_t total_segs_owned = 0;
@@ -243,7 +244,8 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     };
     static const bool no_graph = std::getenv("RGG_NO_GRAPH") != nullptr;
     const bool use_graph = !debug && !b.dbg && !no_graph;
-    const int32_t key = kf | (b.census_on ? 64 : 0);
+    const bool phases = h->phase_timing;
+    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0);
     if (use_graph) {
         cudaGraphExec_t exec = nullptr;
         for (const auto& g : h->graphs)
@@ -251,7 +253,12 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         if (!exec) {
             // capture the launch sequence once (pose, bin, classify, compaction + phase events)
             // phase events become event-record nodes (cudaEventRecordExternal), so they time the replay
-            const auto rec = [&](cudaEvent_t ev) { return cudaEventRecordWithFlags(ev, h->stream, cudaEventRecordExternal); };
+            // inner phase events break the programmatic (PDL) edges between kernels, so they are
+            // recorded only when phase timing is on; ev[0] / ev[4] always bracket the update
+            const auto rec = [&](cudaEvent_t ev) {
+                if (!phases && ev != h->ev[0] && ev != h->ev[4]) return cudaSuccess;
+                return cudaEventRecordWithFlags(ev, h->stream, cudaEventRecordExternal);
+            };
             CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
             cudaError_t e = rec(h->ev[0]);
             if (e == cudaSuccess) e = rggk::launch_pose(h->s, b, h->stream);
@@ -888,7 +895,8 @@ int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out) {
     CK(cudaSetDevice(h->device));
     CK(cudaStreamSynchronize(h->stream));
     float t[5] = {0, 0, 0, 0, 0};
-    for (int p = 0; p < 4; ++p) CK(cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]));
+    if (h->phase_timing)
+        for (int p = 0; p < 4; ++p) CK(cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]));
     CK(cudaEventElapsedTime(&t[4], h->ev[0], h->ev[4]));
     out->pose_ms = t[0];
     out->bin_ms = t[1];
@@ -972,6 +980,12 @@ int rgg_gpu_fp64_peak(int device, double* gflops) {
 }
 
 }  // extern "C"
+
+extern "C" int rgg_gpu_set_phase_timing(rgg_gpu* h, int32_t on) {
+    if (!h) return RGG_EINVAL;
+    h->phase_timing = on != 0;
+    return RGG_OK;
+}
 
 extern "C" int rgg_gpu_copy_counters(rgg_gpu* h, void* dst_device, int32_t n) {
     if (!h || !dst_device) return RGG_EINVAL;

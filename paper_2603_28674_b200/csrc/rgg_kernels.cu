@@ -26,6 +26,14 @@ using rggd::sub;
 
 namespace {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; pdl_wait() blocks until the predecessor's writes are
+// visible, pdl_trigger() lets the successor's CTAs be scheduled early.
+// Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void aabb_empty(double* a) {
     a[0] = a[1] = a[2] = __longlong_as_double(0x7ff0000000000000ll);   // +inf
     a[3] = a[4] = a[5] = __longlong_as_double(0xfff0000000000000ll);   // -inf
@@ -346,6 +354,8 @@ constexpr int kBinThreads = 512;  // 16 warps = 16 cells per CTA (one super-cell
 constexpr int kBinChunk = 256;    // events filtered per pass (threads >= kBinChunk idle in the filter)
 
 __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double cbox[kBinChunk][12];
     __shared__ int cidx[kBinChunk];
     __shared__ int wsum[kBinThreads / 32];
@@ -771,6 +781,8 @@ __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
 // CTA 0 also commits the moved obstacles' operands for the next batch.
 template <bool COUNT>
 __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
+    pdl_wait();
+    pdl_trigger();
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     unsigned long long* dbgw = (!COUNT && b.dbg) ? b.dbg + 4 * static_cast<size_t>(gt >> 5) : nullptr;
@@ -1246,6 +1258,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
 
 template <bool CENSUS>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, Batch b) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ double sbx[kWarpsPerCta][32][24];
     __shared__ int sev[kWarpsPerCta][32];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1318,14 +1332,30 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
                 b.mpool[wu] = 0;
             }
             // one warp-aggregated reservation per queue and chunk
-            // (the queues hold 8 items per owned component; a fuller queue is reported, ctr[6] = 3)
-            int at = warp_reserve(&b.ctr[8], __popc(bm));
+            // one packed reservation for both queues (ctr[8] over count, ctr[9] under count);
+            // a full queue is reported through ctr[6] = 3 (the apply kernel then applies nothing)
+            int at, atu;
+            {
+                const unsigned long long mine = static_cast<unsigned long long>(__popc(bm)) |
+                                                (static_cast<unsigned long long>(__popc(sm)) << 32);
+                unsigned long long x = mine;
+                for (int off = 1; off < 32; off <<= 1) {
+                    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, off);
+                    if (lane >= off) x += y;
+                }
+                const unsigned long long total = __shfl_sync(0xffffffffu, x, 31);
+                unsigned long long base = 0;
+                if (lane == 31 && total) base = atomicAdd(reinterpret_cast<unsigned long long*>(&b.ctr[8]), total);
+                base = __shfl_sync(0xffffffffu, base, 31) + x - mine;
+                at = static_cast<int>(base & 0xffffffffu);
+                atu = static_cast<int>(base >> 32);
+            }
             for (uint32_t x = bm; x; x &= x - 1, ++at) {
                 const int k = __ffs(x) - 1;
                 if (at < b.items_cap) b.items_over[at] = make_int4(c, sev[wi][k], wo, 1 << k);
                 else b.ctr[6] = 3;
             }
-            at = warp_reserve(&b.ctr[9], __popc(sm));
+            at = atu;
             for (uint32_t x = sm; x; x &= x - 1, ++at) {
                 const int k = __ffs(x) - 1;
                 if (at < b.items_cap) b.items_under[at] = make_int4(c, sev[wi][k], wu, 1 << k);
@@ -1353,6 +1383,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
 
 template <int FLAGS, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, Batch b) {
+    pdl_wait();
+    pdl_trigger();
     constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
     constexpr bool HITS = (FLAGS & kHits) != 0;
     __shared__ int2 som[kWarpsPerCta][32];
@@ -1512,6 +1544,8 @@ __device__ __forceinline__ uint4 load_labels(const uint8_t* st, int N, int base)
 }
 
 __global__ void __launch_bounds__(kCompactThreads) gray_count_kernel(const uint8_t* st, int N, int32_t* tile_cnt) {
+    pdl_wait();
+    pdl_trigger();
     const int base = blockIdx.x * kTile + threadIdx.x * kCompactPer;
     const int n = base < N ? gray_count16(load_labels(st, N, base)) : 0;
     int x = n;
@@ -1528,6 +1562,8 @@ __global__ void __launch_bounds__(kCompactThreads) gray_count_kernel(const uint8
 
 __global__ void __launch_bounds__(kCompactThreads) gray_write_kernel(const uint8_t* st, int N, const int32_t* tile_cnt,
                                                                      int ntiles, int32_t* out, int32_t* gray_n) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int ws[kCompactThreads / 32];
     __shared__ int s_base;
     // tile base = sum of earlier tiles
@@ -1617,6 +1653,25 @@ __global__ void fp64_peak_kernel(double* sink, int iters) {
 
 // ------------------------------------------------------------------ launchers
 
+// Launch with programmatic stream serialization (PDL): the kernel's CTAs may be
+// scheduled while the previous kernel on the stream drains; they wait in
+// pdl_wait() for its results.  Captured into CUDA graphs as programmatic edges.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    static const bool off = std::getenv("RGG_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_pose(const Store& s, const Batch& b, cudaStream_t st) {
     const int warps = 4;  // moves per CTA
     pose_kernel<<<(b.n + warps - 1) / warps, 32 * warps, 0, st>>>(s, b);
@@ -1631,8 +1686,7 @@ cudaError_t launch_init_obstacles(const Store& s, Event*, cudaStream_t st) {
 
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
     const int cells_per = kBinThreads / 32;  // = kSuperCells
-    bin_kernel<<<(s.ncells + cells_per - 1) / cells_per, kBinThreads, 0, st>>>(s, b);
-    return cudaGetLastError();
+    return launch_pdl(bin_kernel, dim3((s.ncells + cells_per - 1) / cells_per), dim3(kBinThreads), st, s, b);
 }
 
 template <int F, bool W>
@@ -1671,8 +1725,7 @@ static int pipeline() {
 
 template <int F, bool W>
 static cudaError_t apply6_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {
-    apply_warp_kernel<F, W><<<grid, 32 * kWarpsPerCta, 0, st>>>(s, b);
-    return cudaGetLastError();
+    return launch_pdl(apply_warp_kernel<F, W>, dim3(grid), dim3(32 * kWarpsPerCta), st, s, b);
 }
 
 static int grid_slices(const Store& s, const void* fn) {
@@ -1699,8 +1752,9 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
             narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
             return cudaGetLastError();
         }
-        touch_warp_kernel<false><<<g_touch, 32 * kWarpsPerCta, 0, st>>>(s, b);
-        narrow_kernel<false><<<grid, 128, 0, st>>>(s, b);
+        cudaError_t e = launch_pdl(touch_warp_kernel<false>, dim3(g_touch), dim3(32 * kWarpsPerCta), st, s, b);
+        if (e == cudaSuccess) e = launch_pdl(narrow_kernel<false>, dim3(grid), dim3(128), st, s, b);
+        if (e != cudaSuccess) return e;
         const bool wide = s.W > 1;
         const int ga = g_apply;
         switch (flags & (kPerMove | kHits)) {
@@ -1766,9 +1820,11 @@ int classify_occupancy(int, int) {
 cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st) {
     const int ntiles = (s.N + kTile - 1) / kTile;
     if (ntiles == 0) return cudaMemsetAsync(gray_n, 0, sizeof(int32_t), st);
-    gray_count_kernel<<<ntiles, kCompactThreads, 0, st>>>(s.state, s.N, tile_cnt);
-    gray_write_kernel<<<ntiles, kCompactThreads, 0, st>>>(s.state, s.N, tile_cnt, ntiles, out_ids, gray_n);
-    return cudaGetLastError();
+    cudaError_t e = launch_pdl(gray_count_kernel, dim3(ntiles), dim3(kCompactThreads), st,
+                               static_cast<const uint8_t*>(s.state), s.N, tile_cnt);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(gray_write_kernel, dim3(ntiles), dim3(kCompactThreads), st, static_cast<const uint8_t*>(s.state),
+                      s.N, static_cast<const int32_t*>(tile_cnt), ntiles, out_ids, gray_n);
 }
 
 cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st) {

@@ -105,6 +105,7 @@ def library() -> C.CDLL:
         L.rgg_gpu_stream.restype = vp
         L.rgg_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
         L.rgg_gpu_copy_counters.argtypes = [vp, vp, i32]
+        L.rgg_gpu_set_phase_timing.argtypes = [vp, i32]
         _lib = L
     return _lib
 
@@ -113,7 +114,7 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_
             "rgg_gpu_sync", "rgg_gpu_count", "rgg_gpu_read_states", "rgg_gpu_read_bits", "rgg_gpu_unknown_count",
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
-            "rgg_gpu_copy_counters"]
+            "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing"]
 
 
 @dataclass
@@ -294,6 +295,10 @@ class GpuEngine:
         """Per-move counters of the last update into a CUDA int32 tensor (n, 4); waits for them."""
         self.copy_counters(out.data_ptr(), n)
         self.sync()
+
+    def set_phase_timing(self, on: bool):
+        """Per-kernel phase events in last_stats(); off lets the kernels overlap (PDL)."""
+        self._check(library().rgg_gpu_set_phase_timing(self._h, int(bool(on))))
 
     def copy_counters(self, dst_ptr: int, n: int):
         """Per-move counters of the last update -> device buffer (n x 4 int32), engine stream."""
