@@ -295,7 +295,7 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    launches_per_step = 7
+    launches_per_step = 5  # pose, bin, touch, narrow, apply (one CUDA graph); gray ids are compacted on demand
     # one more (untimed) update of the last step's moves with the byte census on, then the flop census
     eng.update_device(ids_d[args.warmup + args.steps - 1].data_ptr(), rts_d[args.warmup + args.steps - 1].data_ptr(),
                       m_step, per_move=True, census=True)

@@ -42,6 +42,7 @@ extern "C" {
 #define RGG_PER_MOVE 2  /* fill one rgg_update_report per move (finish_counts semantics) */
 #define RGG_ASYNC 4     /* enqueue only; the call returns before the device finishes */
 #define RGG_CENSUS 8    /* also count the algorithmic bytes of this update (read by rgg_gpu_census) */
+#define RGG_GRAY_LIST 16 /* compact the GRAY ids inside the update (else lazily in rgg_gpu_gray_ids) */
 
 /* The serialized store, borrowed for the duration of rgg_gpu_create.  It is the
  * reference's BatchLayout (proj/include/rgg/batch_layout.hpp:23-66) with the padded

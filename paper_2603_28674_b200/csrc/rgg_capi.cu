@@ -64,6 +64,7 @@ struct rgg_gpu {
     int32_t cap_moves = 0;
     int32_t* d_ids = nullptr;
     double* d_rt = nullptr;
+    size_t in_off = 0;
     uint8_t* d_last = nullptr;
     int32_t* d_unknown = nullptr;
     unsigned long long* d_dbg = nullptr;
@@ -80,6 +81,7 @@ struct rgg_gpu {
     int32_t cap_pin = 0;
     int32_t* h_ids = nullptr;
     double* h_rt = nullptr;
+    size_t pin_off = 0;
     int32_t* h_mv = nullptr;
     int32_t* h_ctr = nullptr;
     // host mirrors
@@ -99,6 +101,7 @@ struct rgg_gpu {
     std::vector<GraphEntry> graphs;
     int32_t gen = 0;
     bool phase_timing = true;  // per-kernel phase events (rgg_gpu_set_phase_timing)
+    bool gray_fresh = true;    // d_gray holds the ids of the current labels
     bool timed = false;
     int grid_classify = 1;
     int64_t total_segs_owned = 0;
@@ -139,16 +142,17 @@ uint64_t spread3(uint64_t x) {
 int grow_batch(rgg_gpu* h, int32_t n) {
     if (n <= h->cap_moves && static_cast<int64_t>(h->s.ncells) * n <= h->pool_cap) return RGG_OK;
     const int32_t cap = std::max(n, std::max(64, h->cap_moves * 2));
-    cudaFree(h->d_ids);
-    cudaFree(h->d_rt);
+    cudaFree(h->d_ids);  // ids and poses share one allocation (d_rt points into it)
     cudaFree(h->d_last);
     cudaFree(h->d_ev);
     cudaFree(h->d_evbox);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
     cudaFree(h->d_mpool);
-    CK(dalloc(&h->d_ids, cap));
-    CK(dalloc(&h->d_rt, static_cast<size_t>(cap) * 12));
+    // moves: ids then poses in one block, so the host path needs a single H2D copy
+    h->in_off = ((static_cast<size_t>(cap) * 4 + 15) / 16) * 16;
+    CK(dalloc(reinterpret_cast<char**>(&h->d_ids), h->in_off + static_cast<size_t>(cap) * 96));
+    h->d_rt = reinterpret_cast<double*>(reinterpret_cast<char*>(h->d_ids) + h->in_off);
     CK(dalloc(&h->d_last, cap));
     CK(dalloc(&h->d_ev, cap));
     CK(dalloc(&h->d_evbox, static_cast<size_t>(cap) * 12));
@@ -183,10 +187,10 @@ int grow_pinned(rgg_gpu* h, int32_t n) {
     if (n <= h->cap_pin) return RGG_OK;
     const int32_t cap = std::max(n, std::max(64, h->cap_pin * 2));
     cudaFreeHost(h->h_ids);
-    cudaFreeHost(h->h_rt);
     cudaFreeHost(h->h_mv);
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), cap * sizeof(int32_t), 0));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_rt), cap * 12 * sizeof(double), 0));
+    h->pin_off = ((static_cast<size_t>(cap) * 4 + 15) / 16) * 16;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), h->pin_off + static_cast<size_t>(cap) * 96, 0));
+    h->h_rt = reinterpret_cast<double*>(reinterpret_cast<char*>(h->h_ids) + h->pin_off);
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), 0));
     h->cap_pin = cap;
     return RGG_OK;
@@ -245,7 +249,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     static const bool no_graph = std::getenv("RGG_NO_GRAPH") != nullptr;
     const bool use_graph = !debug && !b.dbg && !no_graph;
     const bool phases = h->phase_timing;
-    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0);
+    // the gray id list is compacted in the update only on request; otherwise lazily
+    // by rgg_gpu_gray_ids (labels, reports and the gray count never need it)
+    const bool gray_list = (flags & RGG_GRAY_LIST) != 0;
+    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0);
     if (use_graph) {
         cudaGraphExec_t exec = nullptr;
         for (const auto& g : h->graphs)
@@ -267,7 +274,8 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess) e = rec(h->ev[2]);
             if (e == cudaSuccess) e = rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[3]);
-            if (e == cudaSuccess) e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
+            if (e == cudaSuccess && gray_list)
+                e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[4]);
             cudaGraph_t graph = nullptr;
             const cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
@@ -278,6 +286,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             h->graphs.push_back({n, key, h->gen, exec});
         }
         CK(cudaGraphLaunch(exec, h->stream));
+        h->gray_fresh = gray_list;
         h->last_n = n;
         h->last_flags = flags;
         h->last_hits_valid = n == 1;
@@ -341,8 +350,9 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         std::fprintf(stderr, "[rgg] fp64 rechecks: SAT %llu, seg-sphere %llu\n", fs[1], fs[3]);
     }
     CK(cudaEventRecord(h->ev[3], h->stream));
-    CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+    if (gray_list) CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
     CK(cudaEventRecord(h->ev[4], h->stream));
+    h->gray_fresh = gray_list;
     h->last_n = n;
     h->last_flags = flags;
     h->last_hits_valid = n == 1;
@@ -539,9 +549,9 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_under, static_cast<size_t>(h->words) * Np));
     CK(dalloc(&h->d_cur, M));
     CK(dalloc(&h->d_cur_union, static_cast<size_t>(M) * 6));
-    CK(dalloc(&h->d_ctr, 16));
+    CK(dalloc(&h->d_ctr, 32));  // [0..15] per batch (zeroed by pose), [16] running gray count
     CK(dalloc(&h->d_mtop, 1));
-    CK(dalloc(&h->d_unknown, 1));
+    h->d_unknown = h->d_ctr + 16;
     CK(dalloc(&h->d_census, 16));
     CK(dalloc(&h->d_crec, ncells));
     h->items_cap = static_cast<int32_t>(std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(1 << 16, 8ll * Np)));
@@ -554,7 +564,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_cell_list, static_cast<size_t>(ncells) * cap));
     CK(dalloc(&h->d_cell_ovf, ncells));
     CK(dalloc(&h->d_dirty, ncells));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 16 * sizeof(int32_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 32 * sizeof(int32_t), 0));
     auto up = [&](void* dst, const void* src, size_t bytes) {
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream) : cudaSuccess;
     };
@@ -582,8 +592,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(cudaMemsetAsync(h->d_cnt, 0, static_cast<size_t>(Np) * sizeof(uint32_t), h->stream));
     CK(cudaMemsetAsync(h->d_over, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
     CK(cudaMemsetAsync(h->d_under, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
-    CK(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(int32_t), h->stream));
-    CK(cudaMemsetAsync(h->d_unknown, 0, sizeof(int32_t), h->stream));
+    CK(cudaMemsetAsync(h->d_ctr, 0, 32 * sizeof(int32_t), h->stream));
 
     Store& s = h->s;
     s.N = N;
@@ -634,11 +643,11 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
-                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_rt, h->d_last, h->d_unknown, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
+                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
                    h->d_mv, h->d_pool};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* pin[] = {h->h_ids, h->h_rt, h->h_mv, h->h_ctr};
+    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr};
     for (void* p : pin)
         if (p) cudaFreeHost(p);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
@@ -674,17 +683,19 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
         if (rc) return rc;
         std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
         std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 12 * sizeof(double));
-        CK(cudaMemcpyAsync(h->d_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->d_rt, h->h_rt, static_cast<size_t>(k) * 12 * sizeof(double), cudaMemcpyHostToDevice,
-                           h->stream));
+        if (h->pin_off == h->in_off) {  // same layout on both sides: one copy
+            CK(cudaMemcpyAsync(h->d_ids, h->h_ids, h->in_off + static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice,
+                               h->stream));
+        } else {
+            CK(cudaMemcpyAsync(h->d_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaMemcpyAsync(h->d_rt, h->h_rt, static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice, h->stream));
+        }
         rc = enqueue(h, k, flags);
         if (rc) return rc;
         if (!(flags & RGG_ASYNC) || bad) {
             if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
                                             cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 7 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(h->h_ctr + 7, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(h->h_ctr + 8, h->d_ctr + 8, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 17 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
             for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {
                 // the update was not applied (apply kernel skipped): grow the queue and replay it
@@ -694,20 +705,19 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
                 if (rc) return rc;
                 if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
                                                 cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 7 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaMemcpyAsync(h->h_ctr + 7, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaMemcpyAsync(h->h_ctr + 8, h->d_ctr + 8, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 17 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaStreamSynchronize(h->stream));
             }
             if (h->h_ctr[6])
                 return fail(h, RGG_ELOGIC, h->h_ctr[6] == 1   ? "overflow pool exhausted"
                                            : h->h_ctr[6] == 2 ? "mask pool exhausted"
                                                               : "narrow item queue full (split the batch)");
-            h->unknown = h->h_ctr[7];
+            h->unknown = h->h_ctr[16];
             h->unknown_stale = false;
             if (reports) {
                 float t[4] = {0, 0, 0, 0};
-                for (int p = 0; p < 4; ++p) cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]);
+                if (h->phase_timing)
+                    for (int p = 0; p < 4; ++p) cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]);
                 int32_t u = u0;
                 for (int32_t i = 0; i < k; ++i) {
                     rgg_update_report& r = reports[i];
@@ -815,6 +825,10 @@ int rgg_gpu_unknown_count(rgg_gpu* h, int32_t* out) {
 int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
     if (!h || !n) return RGG_EINVAL;
     CK(cudaSetDevice(h->device));
+    if (!h->gray_fresh) {  // ordered ballot/prefix compaction of the current labels
+        CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+        h->gray_fresh = true;
+    }
     const int rc = refresh_unknown(h);
     if (rc) return rc;
     *n = h->unknown;
@@ -860,6 +874,7 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
     CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
     CK(cudaMemcpyAsync(h->d_unknown, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    h->gray_fresh = true;
     cudaFree(d_ids);
     cudaFree(d_st);
     h->unknown_stale = true;

@@ -35,7 +35,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "librgg_gpu.so")
 
 RGG_OK, RGG_EINVAL, RGG_ECUDA, RGG_ENCCL, RGG_ENOMEM, RGG_ELOGIC = 0, 1, 2, 3, 4, 5
-RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC, RGG_CENSUS = 1, 2, 4, 8
+RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC, RGG_CENSUS, RGG_GRAY_LIST = 1, 2, 4, 8, 16
 GREEN, RED, GRAY = 0, 1, 2
 
 
@@ -165,6 +165,38 @@ class UpdateReport:
     resolve_checks: int = 0
 
 
+_REPORT_FIELDS = [f for f, _ in _Report._fields_[:-1]]
+
+
+class Reports:
+    """The per-move UpdateReports of one batch_update, backed by the C report array
+    (numpy view ``.array``); items materialise as UpdateReport on access."""
+
+    def __init__(self, raw):
+        self._raw = raw
+        self.array = np.ctypeslib.as_array(raw)
+
+    def __len__(self):
+        return len(self._raw)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        r = self._raw[i]
+        return UpdateReport(*[getattr(r, f) for f in _REPORT_FIELDS])
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def counts(self) -> np.ndarray:
+        """(n, 4) new_green, new_red, new_gray, unknown_after_heuristic."""
+        a = self.array
+        return np.stack([a["new_green"], a["new_red"], a["new_gray"], a["unknown_after_heuristic"]], 1)
+
+
 def _pose12(pose) -> np.ndarray:
     p = np.ascontiguousarray(pose, dtype=np.float64).reshape(-1)
     if p.size != 12:
@@ -243,7 +275,7 @@ class GpuEngine:
         flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0)
         rc = library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, n, flags, reps)
         self._check(rc)
-        return [UpdateReport(*[getattr(r, f) for f, _ in _Report._fields_[:-1]]) for r in reps]
+        return Reports(reps)
 
     def update_obstacle(self, o: int, pose, lazy: bool = True,
                         resolve: Callable[[np.ndarray], np.ndarray] | None = None) -> UpdateReport:
@@ -307,8 +339,13 @@ class GpuEngine:
     @staticmethod
     def _moves(moves):
         if isinstance(moves, tuple) and len(moves) == 2 and not np.isscalar(moves[0]):
-            ids = np.ascontiguousarray(moves[0], dtype=np.int32).reshape(-1)
-            rts = np.ascontiguousarray(moves[1], dtype=np.float64).reshape(len(ids), 12)
+            ids, rts = moves
+            if not (isinstance(ids, np.ndarray) and ids.dtype == np.int32 and ids.flags.c_contiguous):
+                ids = np.ascontiguousarray(ids, dtype=np.int32)
+            if not (isinstance(rts, np.ndarray) and rts.dtype == np.float64 and rts.flags.c_contiguous):
+                rts = np.ascontiguousarray(rts, dtype=np.float64)
+            ids = ids.reshape(-1)
+            rts = rts.reshape(len(ids), 12)
         else:
             moves = list(moves)
             ids = np.array([int(o) for o, _ in moves], dtype=np.int32)
