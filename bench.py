@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--json-out", default="")
     p.add_argument("--clock-window-s", type=float, default=1.0)
+    p.add_argument("--extra-configs", default="c5",
+                   help="comma list of configs also measured on rank 0 (N=1) and reported under 'extra'")
     return p.parse_args()
 
 
@@ -195,6 +197,51 @@ def config_dict(args, n_components, world=1):
             "components_per_gpu": n_components, "obstacles_per_gpu": m, "moves_per_step": m * world,
             "l2": "flushed (512 MB write) between timed steps", "parallelism": f"tiles x{world} (weak)",
             "precision": "fp64-exact (reference op order, no FMA)"}
+
+
+def measure_extra(config, seed, device, steps=10, warmup=3):
+    """A further BASELINE config on one GPU (device-resident moves, L2 flushed between
+    updates): per-update latency and edges/s, the flop/byte census of one update."""
+    import torch
+
+    from paper_2603_28674_b200 import engine as E
+    from paper_2603_28674_b200 import producer
+
+    t0 = time.time()
+    rm, obs, _ = tile_workload(config, 0, seed, warmup + steps)
+    lv = producer.layout_for(rm, obs)
+    build_s = time.time() - t0
+    eng = E.GpuEngine(lv, device=device)
+    ids_h, rts_h = world_moves(config, 1, seed, warmup + steps)
+    dev = torch.device("cuda", device)
+    ids_d = torch.from_numpy(ids_h).to(dev)
+    rts_d = torch.from_numpy(rts_h).to(dev)
+    m = ids_h.shape[1]
+    stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    eng.set_phase_timing(False)
+    for it in range(warmup):
+        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m, per_move=True)
+    torch.cuda.synchronize()
+    ms = []
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.update_device(ids_d[warmup + k].data_ptr(), rts_d[warmup + k].data_ptr(), m, per_move=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    eng.update_device(ids_d[warmup + steps - 1].data_ptr(), rts_d[warmup + steps - 1].data_ptr(), m,
+                      per_move=True, census=True)
+    cen = eng.census()
+    per = statistics.mean(ms)
+    return {"workload": config_dict(argparse.Namespace(config=config), lv.N)["workload"],
+            "components": lv.N, "moves_per_update": m, "per_update_ms": per, "value": lv.N / (per * 1e-3),
+            "unit": "edges/s", "steps": steps, "build_s": round(build_s, 1),
+            "census": {k: cen[k] for k in ("over_pairs", "sat_flops", "under_pairs", "seg_sphere_tests",
+                                           "bytes_components")}}
 
 
 def main():
@@ -359,17 +406,18 @@ def main():
     # dram__bytes_read.sum + dram__bytes_write.sum of the classify kernel from the committed
     # `ncu --set full` capture (profiles/r1_classify_warp_ncu.json); null when absent
     roof["traffic"] = None
-    pf = os.path.join(ROOT, "profiles", "r1_classify_warp_ncu.json")
+    pf = os.path.join(ROOT, "profiles", "r1_classify_ncu.json")
     if os.path.exists(pf):
         try:
             p = json.load(open(pf))
             unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             rd, wr = p["dram__bytes_read.sum"], p["dram__bytes_write.sum"]
             roof["traffic"] = float(rd[0]) * unit[rd[1]] + float(wr[0]) * unit[wr[1]]
-            roof["traffic_source"] = "profiles/r1_classify_warp_ncu.json (ncu --set full, one c2 launch)"
+            roof["traffic_source"] = "profiles/r1_classify_ncu.json (ncu --set full, one c2 update, 3 kernels)"
         except (KeyError, ValueError):
             pass
-    roof["kernel"] = "classify_warp_kernel (paper_2603_28674_b200/csrc/rgg_kernels.cu)"
+    roof["kernel"] = ("classify stage = touch_warp_kernel + narrow_kernel + apply_warp_kernel "
+                      "(paper_2603_28674_b200/csrc/rgg_kernels.cu), timed together by the phase events")
     roof["algorithmic"] = {"flops_per_launch": flops, "bytes_per_launch": byts, "classify_ms_mean": mean_classify,
                            "roof_ms": 1e3 * max(t_fl, t_by), "census": census}
     line = {
@@ -387,6 +435,13 @@ def main():
         "dirty_cells_mean": statistics.mean(s["dirty_cells"] for s in stats),
         "roofline": roof, "clocks": clk.summary(),
     }
+    if world == 1 and args.extra_configs and args.config == "c2":
+        line["extra"] = {}
+        for cfg in [c for c in args.extra_configs.split(",") if c and c != args.config]:
+            try:
+                line["extra"][cfg] = measure_extra(cfg, args.seed, local)
+            except Exception as ex:  # keep the headline line even if an extra config fails
+                line["extra"][cfg] = {"error": str(ex)[:200]}
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n, done, spent, per_step, _ = cpu_reference_run(args.config, args.seed, iterations, args.cpu_sample_s,

@@ -85,11 +85,11 @@ typedef struct rgg_gpu_options {
     int32_t shard_count;   /* 0 or 1: unsharded */
 } rgg_gpu_options;
 
-/* Mirrors rgg::UpdateReport (proj/include/rgg/update_report.hpp:11-25).  The
- * *_us fields carry device-event microseconds of the batch split into the
- * phases of this engine (pose -> reval_us, binning -> over_us, classify ->
- * under_us, compaction -> resolve_us); they are filled on the last report of
- * a batch only. */
+/* Mirrors rgg::UpdateReport (proj/include/rgg/update_report.hpp:11-25).  With
+ * phase timing on (rgg_gpu_set_phase_timing), the *_us fields carry
+ * device-event microseconds of the batch split into the phases of this engine
+ * (pose -> reval_us, binning -> over_us, classify -> under_us, compaction ->
+ * resolve_us), on the last report of a batch only; otherwise they are 0. */
 typedef struct rgg_update_report {
     int32_t obstacle;
     int32_t new_green;
@@ -128,8 +128,9 @@ int rgg_gpu_sync(rgg_gpu* h);
  * counters, n x {to_green, to_red, to_gray, from_gray} int32 — the per-shard
  * report terms a multi-GPU driver sums with one all-reduce. */
 int rgg_gpu_copy_counters(rgg_gpu* h, void* dst_device, int32_t n);
-/* Per-kernel phase events in rgg_gpu_last_stats (default on).  Off lets the
- * pipeline's kernels overlap their launch (PDL); only total_ms is then filled. */
+/* Per-kernel phase events in rgg_gpu_last_stats and the reports' *_us fields
+ * (default off).  Each event record between two kernels costs ~5 us of device
+ * idle time and breaks their PDL overlap; off, only total_ms is filled. */
 int rgg_gpu_set_phase_timing(rgg_gpu* h, int32_t on);
 
 int rgg_gpu_count(const rgg_gpu* h, int32_t* n_components, int32_t* n_obstacles, int32_t* words_per_comp);

@@ -68,6 +68,7 @@ struct rgg_gpu {
     uint8_t* d_last = nullptr;
     int32_t* d_unknown = nullptr;
     unsigned long long* d_dbg = nullptr;
+    unsigned long long* d_tl = nullptr;  // RGG_DEBUG_TIMELINE: 16 x 8 words (rgg_kernels.cu tl_stop)
     Event* d_ev = nullptr;
     int32_t* d_mv = nullptr;
     int32_t* d_pool = nullptr;
@@ -100,7 +101,7 @@ struct rgg_gpu {
     };
     std::vector<GraphEntry> graphs;
     int32_t gen = 0;
-    bool phase_timing = true;  // per-kernel phase events (rgg_gpu_set_phase_timing)
+    bool phase_timing = false;  // per-kernel phase events (rgg_gpu_set_phase_timing)
     bool gray_fresh = true;    // d_gray holds the ids of the current labels
     bool timed = false;
     int grid_classify = 1;
@@ -229,8 +230,37 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
         cudaMemset(h->d_dbg, 0, dbg_n * 8);
     }
     b.dbg = h->d_dbg;
+    static const bool timeline = std::getenv("RGG_DEBUG_TIMELINE") != nullptr;
+    if (timeline && !h->d_tl) cudaMalloc(reinterpret_cast<void**>(&h->d_tl), 128 * 8);
+    b.tl = h->d_tl;
     return b;
 }
+
+// RGG_DEBUG_TIMELINE: one stderr line per update, microseconds from the first
+// pose warp: per kernel first start / last start / first end / last end / mean
+// warp duration, then each PDL kernel's earliest arrival before its wait.
+void dump_timeline(rgg_gpu* h) {
+    if (!h->d_tl) return;
+    unsigned long long t[128];
+    if (cudaMemcpy(t, h->d_tl, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess) return;
+    const double z = static_cast<double>(~t[0]);
+    const auto us = [&](unsigned long long v) { return (static_cast<double>(v) - z) * 1e-3; };
+    static const char* name[5] = {"pose", "bin", "touch", "narrow", "apply"};
+    std::fprintf(stderr, "[tl]");
+    for (int k = 0; k < 5; ++k) {
+        const unsigned long long* p = t + 8 * k;
+        if (!p[5]) continue;
+        std::fprintf(stderr, " %s %.1f %.1f %.1f %.1f %.2f |", name[k], us(~p[0]), us(p[1]), us(~p[2]), us(p[3]),
+                     p[4] * 1e-3 / p[5]);
+    }
+    std::fprintf(stderr, " arrive");
+    for (int k = 5; k < 9; ++k)
+        if (t[8 * k + 5]) std::fprintf(stderr, " %.1f", us(~t[8 * k]));
+    std::fprintf(stderr, "\n");
+}
+
+// Narrow items pack the event index with a 5-bit position (rgg_kernels.cu).
+constexpr int32_t kMaxBatch = 1 << 26;
 
 // Enqueue the whole pipeline for n moves already in d_ids/d_rt.
 int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
@@ -285,6 +315,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             cudaGraphDestroy(graph);
             h->graphs.push_back({n, key, h->gen, exec});
         }
+        if (h->d_tl) CK(cudaMemsetAsync(h->d_tl, 0, 128 * 8, h->stream));
         CK(cudaGraphLaunch(exec, h->stream));
         h->gray_fresh = gray_list;
         h->last_n = n;
@@ -303,11 +334,13 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     CK(cudaEventRecord(h->ev[2], h->stream));
     CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
     if (phase("classify")) return RGG_ECUDA;
-    if (b.dbg && std::getenv("RGG_DEBUG_NARROW")) {
-        const size_t nw = static_cast<size_t>(h->grid_classify) * 4;
+    if (b.dbg && std::getenv("RGG_DEBUG_NARROW")) for (int region = 0; region < 2; ++region) {
+        const size_t ns = (h->s.Np + 31) / 32;
+        const size_t nw = region == 0 ? static_cast<size_t>(h->grid_classify) * 4 : ns;
         std::vector<unsigned long long> t(nw * 4);
-        CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(t.data(), b.dbg + (region ? 8 * ns : 0), t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        std::fprintf(stderr, "[rgg] %s ", region == 0 ? "narrow" : "touch ");
         unsigned long long lo = ~0ull, hi = 0;
         std::vector<double> st, du;
         for (size_t w = 0; w < nw; ++w)
@@ -318,9 +351,9 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         std::sort(du.begin(), du.end());
         const size_t n = st.size();
         if (n)
-            std::fprintf(stderr, "[rgg] narrow warps %zu span %.1f us | start p50 %.1f p90 %.1f max %.1f | dur p50 %.1f p90 %.1f max %.1f | items %llu/%llu\n",
+            std::fprintf(stderr, "warps %zu span %.1f us | start p50 %.1f p90 %.1f max %.1f | dur p50 %.1f p90 %.1f max %.1f | %llu/%llu\n",
                          n, (hi - lo) * 1e-3, st[n / 2], st[n * 9 / 10], st[n - 1], du[n / 2], du[n * 9 / 10], du[n - 1], t[2], t[3]);
-        CK(cudaMemsetAsync(b.dbg, 0, t.size() * 8, h->stream));
+        CK(cudaMemsetAsync(b.dbg + (region ? 8 * ns : 0), 0, t.size() * 8, h->stream));
     } else if (b.dbg) {
         const size_t ns = static_cast<size_t>((h->s.Np + 31) / 32);
         std::vector<unsigned long long> t(ns * 16);
@@ -485,7 +518,10 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
             const int64_t src = static_cast<int64_t>(c) * B * S + r;
             int64_t dst = row[static_cast<size_t>(i) * B * S + r];
             for (int64_t k = v->row_off[src]; k < v->row_off[src + 1]; ++k, ++dst)
+            {
                 std::memcpy(&seg[dst * 8], v->segs + 7 * k, 7 * sizeof(double));
+                seg[dst * 8 + 7] = v->spline_radius[r];  // the under items' r_total needs no row lookup
+            }
         }
     }
     for (int32_t g = 0; g < ncells; ++g) {
@@ -520,6 +556,8 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     std::vector<rggd::Box32> sat32(static_cast<size_t>(Np) * B);
     for (size_t i = 0; i < sat32.size(); ++i) {
         const double* a = &sat[i * 22];
+        sat32[i] = rggd::Box32{};
+        for (int k = 0; k < 3; ++k) sat32[i].c[k] = a[k];
         double l1 = 0.0;
         for (int k = 0; k < 9; ++k) {
             sat32[i].e[k] = static_cast<float>(a[3 + k]);
@@ -528,7 +566,6 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         }
         const float lf = static_cast<float>(l1 * (1.0 + 1e-15));
         sat32[i].L = std::nextafter(lf, std::numeric_limits<float>::infinity());
-        sat32[i].pad = 0.0f;
     }
     CK(dalloc(&h->d_sat32, sat32.size()));
     CK(cudaMemcpyAsync(h->d_sat32, sat32.data(), sat32.size() * sizeof(rggd::Box32), cudaMemcpyHostToDevice, h->stream));
@@ -644,7 +681,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
-                   h->d_mv, h->d_pool};
+                   h->d_mv, h->d_pool, h->d_tl, h->d_dbg};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* pin[] = {h->h_ids, h->h_mv, h->h_ctr};
@@ -662,6 +699,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
     if (!h) return RGG_EINVAL;
     clear_stale_error();
     if (n < 0 || (n > 0 && (!ids || !rt12))) return fail(h, RGG_EINVAL, "bad move list");
+    if (n >= kMaxBatch) return fail(h, RGG_EINVAL, "at most 2^26 - 1 moves per batch (split it)");
     if (!(flags & RGG_LAZY))
         return fail(h, RGG_EINVAL, "eager updates resolve gray components on the host: call with RGG_LAZY per move, "
                                    "then rgg_gpu_last_hits + rgg_gpu_write_states");
@@ -697,6 +735,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
                                             cudaMemcpyDeviceToHost, h->stream));
             CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 17 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
+            dump_timeline(h);
             for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {
                 // the update was not applied (apply kernel skipped): grow the queue and replay it
                 rc = grow_items(h, std::max<int64_t>(h->h_ctr[8], h->h_ctr[9]));
@@ -751,6 +790,7 @@ int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12
     clear_stale_error();
     if (n <= 0) return RGG_OK;
     if (!(flags & RGG_LAZY)) return fail(h, RGG_EINVAL, "only lazy updates run on device");
+    if (n >= kMaxBatch) return fail(h, RGG_EINVAL, "at most 2^26 - 1 moves per batch (split it)");
     CK(cudaSetDevice(h->device));
     const int rc = grow_batch(h, n);
     if (rc) return rc;
@@ -767,6 +807,7 @@ int rgg_gpu_sync(rgg_gpu* h) {
     int32_t err = 0;
     CK(cudaMemcpyAsync(&err, h->d_ctr + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    dump_timeline(h);
     if (err == 3) {
         int32_t need[2] = {0, 0};
         CK(cudaMemcpy(need, h->d_ctr + 8, sizeof(need), cudaMemcpyDeviceToHost));

@@ -175,14 +175,18 @@ __device__ __forceinline__ bool seg_sphere_fast(const double* s, const double* c
 // re-evaluated with the exact fp64 sequence, so the verdicts are still the
 // reference's bit for bit.  u = 2^-24 (fp32 unit roundoff).
 //
-// Box32 (fp32 operand of a SatBox): e[9], u[9] rounded to nearest, L = sum of
-// |e_k|_1 rounded up, pad.  The centre stays fp64 (d is formed in fp64).
+// Box32 (filter operand of a SatBox, one 128-byte line): the fp64 centre (d is
+// formed in fp64), e[9], u[9] rounded to nearest, L = sum of |e_k|_1 rounded up.
+// The filter reads only this line; the 176-byte fp64 SatBox is read only for the
+// rare undecided pair.
 struct __align__(16) Box32 {
+    double c[3];
     float e[9];
     float u[9];
     float L;
-    float pad;
+    float pad[7];
 };
+static_assert(sizeof(Box32) == 128, "Box32 is one cache line");
 
 __device__ __forceinline__ float dot3f(const float* x, const float* y) {
     return fmaf(x[2], y[2], fmaf(x[1], y[1], x[0] * y[0]));

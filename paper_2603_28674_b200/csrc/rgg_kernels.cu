@@ -34,6 +34,28 @@ namespace {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Update timeline (RGG_DEBUG_TIMELINE): per kernel k, 8 words at b.tl + 8k:
+// ~first start, last start, ~first end, last end, sum of warp durations, warps
+// (all max-reduced from zero; "first" stored complemented).
+__device__ __forceinline__ unsigned long long tl_start(const unsigned long long* tl) { return tl ? gtimer() : 0; }
+__device__ __forceinline__ void tl_stop(unsigned long long* tl, int k, unsigned long long t0) {
+    if (!tl || (threadIdx.x & 31) != 0) return;
+    const unsigned long long t1 = gtimer();
+    unsigned long long* p = tl + 8 * k;
+    atomicMax(p + 0, ~t0);
+    atomicMax(p + 1, t0);
+    atomicMax(p + 2, ~t1);
+    atomicMax(p + 3, t1);
+    atomicAdd(p + 4, t1 - t0);
+    atomicAdd(p + 5, 1ull);
+}
+
 __device__ __forceinline__ void aabb_empty(double* a) {
     a[0] = a[1] = a[2] = __longlong_as_double(0x7ff0000000000000ll);   // +inf
     a[3] = a[4] = a[5] = __longlong_as_double(0xfff0000000000000ll);   // -inf
@@ -133,6 +155,8 @@ __device__ __forceinline__ void box_of(const double* rt, const double* he, int c
 }
 
 __global__ void pose_kernel(Store s, Batch b) {
+    const unsigned long long t0 = tl_start(b.tl);
+    pdl_trigger();  // the bin kernel's CTAs may land now; they wait for these events in pdl_wait()
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i == 0 && lane < 16) {
         b.ctr[lane] = 0;
@@ -245,7 +269,7 @@ __global__ void pose_kernel(Store s, Batch b) {
         l1 += __shfl_down_sync(0xffffffffu, l1, 2);  // lanes 0..2 summed on lane 0 (lane 3 adds 0)
         if (lane == 0) {
             ev.b32.L = __double2float_ru(l1 * (1.0 + 1e-15));
-            ev.b32.pad = 0.0f;
+            
         }
     }
     // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
@@ -311,6 +335,7 @@ __global__ void pose_kernel(Store s, Batch b) {
         b.last[i] = is_last ? 1 : 0;
         reinterpret_cast<int4*>(b.mv)[i] = make_int4(0, 0, 0, 0);
     }
+    tl_stop(b.tl, 0, t0);
 }
 
 // Identity pose for every obstacle: serialize() poses obstacles at their
@@ -329,7 +354,7 @@ __global__ void init_obstacles_kernel(Store s) {
         l1 += fabs(e.sat[3 + k]);
     }
     e.b32.L = __double2float_ru(l1 * (1.0 + 1e-15));
-    e.b32.pad = 0.0f;
+    
     e.r = s.osr[o];
     e.o = o;
     e.nsph = nsph;
@@ -354,8 +379,11 @@ constexpr int kBinThreads = 512;  // 16 warps = 16 cells per CTA (one super-cell
 constexpr int kBinChunk = 256;    // events filtered per pass (threads >= kBinChunk idle in the filter)
 
 __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
+    const unsigned long long tw = tl_start(b.tl);
     pdl_wait();
     pdl_trigger();
+    const unsigned long long t0 = tl_start(b.tl);
+    tl_stop(b.tl, 5, tw);
     __shared__ double cbox[kBinChunk][12];
     __shared__ int cidx[kBinChunk];
     __shared__ int wsum[kBinThreads / 32];
@@ -465,6 +493,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
         const unsigned long long a = reinterpret_cast<unsigned long long>(list);
         b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
     }
+    tl_stop(b.tl, 1, t0);
 }
 
 // ----------------------------------------------------------------- classify
@@ -493,9 +522,9 @@ __device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev
         bool hit = false;
         for (int b = 0; b < s.B && !hit; ++b) {
             const size_t i = static_cast<size_t>(c) * s.B + b;
-            const double* a = s.sat + i * 22;
-            const int f = rggd::sat_filter32(a, s.sat32[i], osat, ev.b32);
-            hit = f == 2 ? sat_exact(a, osat) : f == 1;
+            const rggd::Box32& a32 = s.sat32[i];
+            const int f = rggd::sat_filter32(a32.c, a32, osat, ev.b32);
+            hit = f == 2 ? sat_exact(s.sat + i * 22, osat) : f == 1;
         }
         return hit;
     }
@@ -585,10 +614,29 @@ __device__ __forceinline__ bool under_part(const Store& s, int c, const Event& e
     return hit;
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
+// batch_under for one pair from its item (narrow kernel): the component's real
+// segments [lo, hi); word 7 of each segment record carries its row's spline
+// radius (rgg_capi.cu upload), so no row lookup is needed.  Lanes g, g+G, ...
+template <bool COUNT>
+__device__ __forceinline__ bool under_range(const Store& s, int lo, int hi, const Event& ev, int g, int G,
+                                            long long* tests) {
+    bool hit = false;
+    for (int j = lo + g; j < hi; j += G) {
+        const double2* p = reinterpret_cast<const double2*>(s.seg + 8 * static_cast<size_t>(j));
+        const double2 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3];
+        const double seg[7] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x};
+        const double r_total = add(ev.r, v3.y);  // o_minus_r + spline_radius[row] (engine_batch.cpp:97)
+        for (int sp = 0; sp < ev.nsph; ++sp) {
+            if (COUNT) {
+                *tests += 1;
+                hit |= rggd::seg_sphere_fast(seg, ev.cen + 3 * sp, r_total);
+            } else {
+                const int f = rggd::seg_filter32(seg, ev.cen + 3 * sp, r_total);
+                if (f == 1 || (f == 2 && seg_exact(seg, ev.cen + 3 * sp, r_total))) return true;
+            }
+        }
+    }
+    return hit;
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -747,10 +795,11 @@ __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
                 b.mpool[wo] |= 1u << k;  // this thread owns the word until the narrow kernel
         }
         at = s_bu + wbu + xu - nu;
+        const int ulo = sm ? s.row[c * s.B * s.S] : 0, uhi = sm ? s.row[(c + 1) * s.B * s.S] : 0;
         for (uint32_t x = sm; x; x &= x - 1, ++at) {
             const int k = __ffs(x) - 1;
             if (at < b.items_cap)
-                b.items_under[at] = make_int4(c, sev[k], wu, 1 << k);
+                b.items_under[at] = make_int4(ulo, uhi, wu, (sev[k] << 5) | k);
             else if (under_inline(s, c, b.ev[sev[k]]))
                 b.mpool[wu] |= 1u << k;
         }
@@ -776,13 +825,17 @@ __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
     }
 }
 
-// The narrow tests of all items, GPU-wide (persistent grid).  Over items: one
-// thread each (15-axis SAT per body).  Under items: kUnderLanes lanes each.
-// CTA 0 also commits the moved obstacles' operands for the next batch.
-template <bool COUNT>
+// The narrow tests of all items, GPU-wide (persistent grid).  Over items
+// {component, event, result word, bit}: one thread each (15-axis SAT per body).
+// Under items {first segment, end segment, result word, event << 5 | bit}: G
+// lanes each.
+template <bool COUNT, int G>
 __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
+    const unsigned long long tw = COUNT ? 0 : tl_start(b.tl);
     pdl_wait();
     pdl_trigger();
+    const unsigned long long t0 = COUNT ? 0 : tl_start(b.tl);
+    if (!COUNT) tl_stop(b.tl, 7, tw);
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     unsigned long long* dbgw = (!COUNT && b.dbg) ? b.dbg + 4 * static_cast<size_t>(gt >> 5) : nullptr;
@@ -795,25 +848,24 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
         if (COUNT) c_op += s.B, c_oh += h;
         if (h) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
     }
-    const int g = gt % kUnderLanes, groups = nthreads / kUnderLanes;
-    const unsigned gmask = ((1u << kUnderLanes) - 1u) << (lane & ~(kUnderLanes - 1));
-    for (int i = gt / kUnderLanes; i < n_under; i += groups) {
+    const int g = gt % G, groups = nthreads / G;
+    const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (lane & ~(G - 1));
+    for (int i = gt / G; i < n_under; i += groups) {
         const int4 it = b.items_under[i];
-        bool h = under_part<COUNT>(s, it.x, b.ev[it.y], COUNT ? 0 : g, COUNT ? 1 : kUnderLanes, &c_tests);
-        if (!COUNT) {
+        bool h = under_range<COUNT>(s, it.x, it.y, b.ev[it.w >> 5], g, G, &c_tests);
 #pragma unroll
-            for (int off = 1; off < kUnderLanes; off <<= 1) {
-                const bool other = __shfl_xor_sync(gmask, h, off);  // the group's lanes share i
-                h = h || other;
-            }
+        for (int off = 1; off < G; off <<= 1) {
+            const bool other = __shfl_xor_sync(gmask, h, off);  // the group's lanes share i
+            h = h || other;
         }
         if (COUNT) c_up += 1, c_uh += h;
-        if (h && (COUNT || g == 0)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+        if (h && g == 0) atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
     }
     if (dbgw) {
         __syncwarp();
         if (lane == 0) dbgw[1] = gtimer(), dbgw[2] = static_cast<unsigned long long>(n_over), dbgw[3] = n_under;
     }
+    if (!COUNT) tl_stop(b.tl, 3, t0);
     if (COUNT) {
         long long v[6] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh};
 #pragma unroll
@@ -1182,7 +1234,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
                     const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
                     const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
                     const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
-                    if (lane == 0 && (gg | r | y | f)) {
+                    if (lane == 0 && (gg | r | y | f) && !(s.dbg_flags & 4)) {  // 4: ablation, no counters
                         int* mv = b.mv + 4 * om.y;
                         if (gg) atomicAdd(mv + 0, __popc(gg));
                         if (r) atomicAdd(mv + 1, __popc(r));
@@ -1258,13 +1310,21 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
 
 template <bool CENSUS>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, Batch b) {
+    const unsigned long long tw = CENSUS ? 0 : tl_start(b.tl);
     pdl_wait();
     pdl_trigger();
+    const unsigned long long t0 = CENSUS ? 0 : tl_start(b.tl);
+    if (!CENSUS) tl_stop(b.tl, 6, tw);
     __shared__ double sbx[kWarpsPerCta][32][24];
     __shared__ int sev[kWarpsPerCta][32];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
     unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
+    unsigned long long* dbgw = (!CENSUS && b.dbg) ? b.dbg + 8 * static_cast<size_t>(nslices) +
+                                                        4 * static_cast<size_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5)
+                                                  : nullptr;
+    if (dbgw && lane == 0) dbgw[0] = gtimer();
+    int dbg_slices = 0;
     for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
         const int c0 = q << 5;
         const int cell = c0 / s.cell;
@@ -1317,7 +1377,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             // the narrow kernel (next launch) reads exactly these operands: stage them in L2 now
             if (bm && w == 0) {
                 const size_t i0 = static_cast<size_t>(c) * s.B;
-                prefetch_range(s.sat + i0 * 22, s.sat + (i0 + s.B) * 22, false);
                 prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, false);
             }
             if (sm && w == 0) {
@@ -1358,7 +1417,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             at = atu;
             for (uint32_t x = sm; x; x &= x - 1, ++at) {
                 const int k = __ffs(x) - 1;
-                if (at < b.items_cap) b.items_under[at] = make_int4(c, sev[wi][k], wu, 1 << k);
+                if (at < b.items_cap) b.items_under[at] = make_int4(seg_lo, seg_hi, wu, (sev[wi][k] << 5) | k);
                 else b.ctr[6] = 3;
             }
             __syncwarp();
@@ -1369,7 +1428,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             c_sph += any_sph;
             if (any_sph) c_segs += seg_hi - seg_lo;
         }
+        ++dbg_slices;
     }
+    if (dbgw) {
+        __syncwarp();
+        if (lane == 0) dbgw[1] = gtimer(), dbgw[2] = dbg_slices, dbgw[3] = 0;
+    }
+    if (!CENSUS) tl_stop(b.tl, 2, t0);
     if (CENSUS) {
         unsigned long long v[5] = {c_dirty, c_box, c_sph, c_segs, c_touch};
 #pragma unroll
@@ -1383,8 +1448,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
 
 template <int FLAGS, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, Batch b) {
+    const unsigned long long tw = tl_start(b.tl);
     pdl_wait();
     pdl_trigger();
+    const unsigned long long t0 = tl_start(b.tl);
+    tl_stop(b.tl, 8, tw);
     constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
     constexpr bool HITS = (FLAGS & kHits) != 0;
     __shared__ int2 som[kWarpsPerCta][32];
@@ -1394,7 +1462,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     // a full narrow-item queue left some verdicts uncomputed: apply nothing, so the
     // engine stays at its pre-update state and the host can grow the queue and replay
     if (b.ctr[6] == 3) return;
-    commit_grid(s, b);
+    if (!(s.dbg_flags & 8)) commit_grid(s, b);  // 8: ablation, no commit
     for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
         const int c0 = q << 5;
         const int cell = c0 / s.cell;
@@ -1480,7 +1548,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                     const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
                     const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
                     const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
-                    if (lane == 0 && (gg | r | y | f)) {
+                    if (lane == 0 && (gg | r | y | f) && !(s.dbg_flags & 4)) {  // 4: ablation, no counters
                         int* mv = b.mv + 4 * om.y;
                         if (gg) atomicAdd(mv + 0, __popc(gg));
                         if (r) atomicAdd(mv + 1, __popc(r));
@@ -1514,6 +1582,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     }
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
     if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
+    tl_stop(b.tl, 4, t0);
 }
 
 // --------------------------------------------------------------- compaction
@@ -1656,9 +1725,28 @@ __global__ void fp64_peak_kernel(double* sink, int iters) {
 // Launch with programmatic stream serialization (PDL): the kernel's CTAs may be
 // scheduled while the previous kernel on the stream drains; they wait in
 // pdl_wait() for its results.  Captured into CUDA graphs as programmatic edges.
+// One shared-memory carveout for every kernel of the update: an SM whose
+// L1/shared split differs from the next kernel's must drain before that
+// kernel's CTAs can land on it (RGG_CARVEOUT = percent, <0 leaves the driver's
+// per-kernel choice).
+static void carveout(const void* fn) {
+    static const int pct = [] {
+        const char* e = std::getenv("RGG_CARVEOUT");
+        return e ? std::atoi(e) : -1;
+    }();
+    if (pct < 0) return;
+    static const void* done[64];
+    static int ndone = 0;
+    for (int i = 0; i < ndone; ++i)
+        if (done[i] == fn) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    if (ndone < 64) done[ndone++] = fn;
+}
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
     static const bool off = std::getenv("RGG_NO_PDL") != nullptr;
+    carveout(reinterpret_cast<const void*>(k));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -1674,6 +1762,7 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaSt
 
 cudaError_t launch_pose(const Store& s, const Batch& b, cudaStream_t st) {
     const int warps = 4;  // moves per CTA
+    carveout(reinterpret_cast<const void*>(pose_kernel));
     pose_kernel<<<(b.n + warps - 1) / warps, 32 * warps, 0, st>>>(s, b);
     return cudaGetLastError();
 }
@@ -1738,6 +1827,30 @@ static int grid_slices(const Store& s, const void* fn) {
     return need < per_sm * sms ? (need < 1 ? 1 : need) : per_sm * sms;
 }
 
+// lanes per under item (RGG_UNDER_LANES = 1, 2 or 4)
+static int under_lanes() {
+    static const int g = [] {
+        const char* e = std::getenv("RGG_UNDER_LANES");
+        const int v = e ? std::atoi(e) : 1;
+        return v == 2 || v == 4 ? v : 1;
+    }();
+    return g;
+}
+
+static cudaError_t launch_narrow(const Store& s, const Batch& b, int grid, cudaStream_t st, bool pdl) {
+    switch (under_lanes()) {
+        case 2:
+            return pdl ? launch_pdl(narrow_kernel<false, 2>, dim3(grid), dim3(128), st, s, b)
+                       : (narrow_kernel<false, 2><<<grid, 128, 0, st>>>(s, b), cudaGetLastError());
+        case 4:
+            return pdl ? launch_pdl(narrow_kernel<false, 4>, dim3(grid), dim3(128), st, s, b)
+                       : (narrow_kernel<false, 4><<<grid, 128, 0, st>>>(s, b), cudaGetLastError());
+        default:
+            return pdl ? launch_pdl(narrow_kernel<false, 1>, dim3(grid), dim3(128), st, s, b)
+                       : (narrow_kernel<false, 1><<<grid, 128, 0, st>>>(s, b), cudaGetLastError());
+    }
+}
+
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st) {
     if (s.ncells == 0) return cudaSuccess;
     if (pipeline() == 6) {
@@ -1749,11 +1862,11 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
         }
         if (flags & kCensus) {
             touch_warp_kernel<true><<<g_touch_c, 32 * kWarpsPerCta, 0, st>>>(s, b);
-            narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
+            narrow_kernel<true, 1><<<grid, 128, 0, st>>>(s, b);
             return cudaGetLastError();
         }
         cudaError_t e = launch_pdl(touch_warp_kernel<false>, dim3(g_touch), dim3(32 * kWarpsPerCta), st, s, b);
-        if (e == cudaSuccess) e = launch_pdl(narrow_kernel<false>, dim3(grid), dim3(128), st, s, b);
+        if (e == cudaSuccess) e = launch_narrow(s, b, grid, st, true);
         if (e != cudaSuccess) return e;
         const bool wide = s.W > 1;
         const int ga = g_apply;
@@ -1785,11 +1898,11 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
         }
     }
     if (flags & kCensus) {
-        narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
+        narrow_kernel<true, 1><<<grid, 128, 0, st>>>(s, b);
         return cudaGetLastError();
     }
     touch_kernel<<<s.ncells, s.cell, 0, st>>>(s, b);
-    narrow_kernel<false><<<grid, 128, 0, st>>>(s, b);
+    launch_narrow(s, b, grid, st, false);
     const bool wide = s.W > 1;
     switch (flags & (kPerMove | kHits)) {
         case 0:
@@ -1813,7 +1926,7 @@ void filter_stats(unsigned long long* out, bool reset) {
 
 int classify_occupancy(int, int) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_kernel<false>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_kernel<false, 1>, 128, 0);
     return n < 1 ? 1 : n;
 }
 

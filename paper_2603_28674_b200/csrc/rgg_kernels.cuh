@@ -90,6 +90,7 @@ struct Batch {
     int32_t census_on;           // touch accumulates the byte census
     int32_t* unknown;      // running GRAY count, persistent across batches
     unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
+    unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null
 };
 
 enum Flags : int32_t { kPerMove = 2, kHits = 8, kCensus = 16 };

@@ -60,6 +60,9 @@ class _Report(C.Structure):
                 ("residual_unknown", C.c_int32), ("resolve_checks", C.c_int32), ("_pad", C.c_int32)]
 
 
+_REPORT_DTYPE = np.dtype(_Report)
+
+
 class Stats(C.Structure):
     _fields_ = [("pose_ms", C.c_float), ("bin_ms", C.c_float), ("classify_ms", C.c_float),
                 ("compact_ms", C.c_float), ("total_ms", C.c_float), ("dirty_cells", C.c_int32),
@@ -174,7 +177,13 @@ class Reports:
 
     def __init__(self, raw):
         self._raw = raw
-        self.array = np.ctypeslib.as_array(raw)
+        self._array = None
+
+    @property
+    def array(self) -> np.ndarray:
+        if self._array is None:
+            self._array = np.frombuffer(self._raw, dtype=_REPORT_DTYPE)
+        return self._array
 
     def __len__(self):
         return len(self._raw)
