@@ -44,6 +44,7 @@ struct rgg_gpu {
     double* d_osr = nullptr;
     int32_t* d_osn = nullptr;
     uint8_t* d_state = nullptr;
+    uint8_t* d_state_c = nullptr;  // cell-order copy of the owned labels (Store::state_c)
     uint32_t* d_cnt = nullptr;
     unsigned long long* d_over = nullptr;
     unsigned long long* d_under = nullptr;
@@ -351,8 +352,23 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         std::sort(du.begin(), du.end());
         const size_t n = st.size();
         if (n)
-            std::fprintf(stderr, "warps %zu span %.1f us | start p50 %.1f p90 %.1f max %.1f | dur p50 %.1f p90 %.1f max %.1f | %llu/%llu\n",
-                         n, (hi - lo) * 1e-3, st[n / 2], st[n * 9 / 10], st[n - 1], du[n / 2], du[n * 9 / 10], du[n - 1], t[2], t[3]);
+            std::fprintf(stderr, "warps %zu span %.1f us | start p50 %.1f p90 %.1f max %.1f | dur p50 %.1f p90 %.1f max %.1f\n",
+                         n, (hi - lo) * 1e-3, st[n / 2], st[n * 9 / 10], st[n - 1], du[n / 2], du[n * 9 / 10], du[n - 1]);
+        if (region == 0) {
+            // the slowest narrow warps: start, duration, lane-max items and segments
+            std::vector<std::pair<double, size_t>> order;
+            for (size_t w = 0; w < nw; ++w)
+                if (t[4 * w] && t[4 * w + 1]) order.push_back({(t[4 * w + 1] - t[4 * w]) * 1e-3, w});
+            std::sort(order.rbegin(), order.rend());
+            for (size_t r = 0; r < std::min<size_t>(8, order.size()); ++r) {
+                const size_t w = order[r].second;
+                std::fprintf(stderr, "   warp %zu start %.1f dur %.1f items %llu segs %llu\n", w, (t[4 * w] - lo) * 1e-3,
+                             order[r].first, t[4 * w + 2], t[4 * w + 3]);
+            }
+            double si = 0;
+            for (size_t w = 0; w < nw; ++w) si += t[4 * w + 2];
+            std::fprintf(stderr, "   mean lane-max items %.2f\n", si / std::max<size_t>(1, n));
+        }
         CK(cudaMemsetAsync(b.dbg + (region ? 8 * ns : 0), 0, t.size() * 8, h->stream));
     } else if (b.dbg) {
         const size_t ns = static_cast<size_t>((h->s.Np + 31) / 32);
@@ -581,6 +597,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_osr, M));
     CK(dalloc(&h->d_osn, M));
     CK(dalloc(&h->d_state, static_cast<size_t>(N) + 16));
+    CK(dalloc(&h->d_state_c, static_cast<size_t>(Np) + 16));
     CK(dalloc(&h->d_cnt, Np));
     CK(dalloc(&h->d_over, static_cast<size_t>(h->words) * Np));
     CK(dalloc(&h->d_under, static_cast<size_t>(h->words) * Np));
@@ -626,6 +643,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         CK(cudaMemcpyAsync(h->d_state, st.data(), st.size(), cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     }
+    CK(cudaMemsetAsync(h->d_state_c, 0, static_cast<size_t>(Np) + 16, h->stream));
     CK(cudaMemsetAsync(h->d_cnt, 0, static_cast<size_t>(Np) * sizeof(uint32_t), h->stream));
     CK(cudaMemsetAsync(h->d_over, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
     CK(cudaMemsetAsync(h->d_under, 0, static_cast<size_t>(h->words) * Np * 8, h->stream));
@@ -658,6 +676,8 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.osr = h->d_osr;
     s.osn = h->d_osn;
     s.state = h->d_state;
+    s.state_c = h->d_state_c;
+    s.rank = h->d_rank;
     s.cnt = h->d_cnt;
     s.over = h->d_over;
     s.under = h->d_under;
@@ -678,7 +698,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
-                   h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_cnt, h->d_over, h->d_under, h->d_cur,
+                   h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
                    h->d_mv, h->d_pool, h->d_tl, h->d_dbg};

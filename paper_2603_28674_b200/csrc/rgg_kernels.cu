@@ -842,7 +842,42 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     if (dbgw && lane == 0) dbgw[0] = gtimer();
     const int n_over = min(b.ctr[8], b.items_cap), n_under = min(b.ctr[9], b.items_cap);
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
-    for (int i = gt; i < n_over; i += nthreads) {
+    if (!COUNT && G == 1) {
+        // One pass over both queues (over items first).  The next item is loaded
+        // while the current one is tested, and an under item's segment records
+        // are prefetched into L1 before they are walked: about one exposed memory
+        // round trip per item instead of one per load.
+        const int total = n_over + n_under;
+        const auto item = [&](int i) {
+            return i < n_over ? b.items_over[i] : b.items_under[i - n_over];
+        };
+        int i = gt;
+        int4 it = i < total ? item(i) : make_int4(0, 0, 0, 0);
+        unsigned long long d_items = 0, d_segs = 0;
+        while (i < total) {
+            if (dbgw) d_items += 1, d_segs += i < n_over ? 0 : it.y - it.x;
+            const int inext = i + nthreads;
+            const int4 nx = inext < total ? item(inext) : make_int4(0, 0, 0, 0);
+            if (i < n_over) {
+                if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+            } else {
+                for (int j = it.x; j < it.y; ++j) prefetch_l1(s.seg + 8 * static_cast<size_t>(j));
+                if (under_range<false>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, nullptr))
+                    atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
+            }
+            it = nx;
+            i = inext;
+        }
+        if (dbgw) {
+            // lane maxima: items, segments
+            for (int off = 16; off; off >>= 1) {
+                d_items = max(d_items, __shfl_xor_sync(0xffffffffu, d_items, off));
+                d_segs = max(d_segs, __shfl_xor_sync(0xffffffffu, d_segs, off));
+            }
+        }
+        if (dbgw && lane == 0) dbgw[2] = d_items, dbgw[3] = d_segs;
+    }
+    for (int i = gt; i < (COUNT || G > 1 ? n_over : 0); i += nthreads) {
         const int4 it = b.items_over[i];  // component, event, result word, bit
         const bool h = over_test<COUNT>(s, it.x, b.ev[it.y], &c_sat);
         if (COUNT) c_op += s.B, c_oh += h;
@@ -850,7 +885,7 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     }
     const int g = gt % G, groups = nthreads / G;
     const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (lane & ~(G - 1));
-    for (int i = gt / G; i < n_under; i += groups) {
+    for (int i = gt / G; i < (COUNT || G > 1 ? n_under : 0); i += groups) {
         const int4 it = b.items_under[i];
         bool h = under_range<COUNT>(s, it.x, it.y, b.ev[it.w >> 5], g, G, &c_tests);
 #pragma unroll
@@ -863,7 +898,7 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     }
     if (dbgw) {
         __syncwarp();
-        if (lane == 0) dbgw[1] = gtimer(), dbgw[2] = static_cast<unsigned long long>(n_over), dbgw[3] = n_under;
+        if (lane == 0) dbgw[1] = gtimer();
     }
     if (!COUNT) tl_stop(b.tl, 3, t0);
     if (COUNT) {
@@ -992,6 +1027,7 @@ __global__ void __launch_bounds__(kMaxCell) apply_kernel(Store s, Batch b) {
     if (valid) {
         if (label != label0) {
             s.state[id] = static_cast<uint8_t>(label);
+            s.state_c[c] = static_cast<uint8_t>(label);
             dgray = (label == 2) - (label0 == 2);
         }
         const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
@@ -1257,6 +1293,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
         if (valid) {
             if (label != label0) {
                 s.state[id] = static_cast<uint8_t>(label);
+                s.state_c[c] = static_cast<uint8_t>(label);
                 dgray += (label == 2) - (label0 == 2);
             }
             const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
@@ -1461,29 +1498,32 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     int dgray = 0;
     // a full narrow-item queue left some verdicts uncomputed: apply nothing, so the
     // engine stays at its pre-update state and the host can grow the queue and replay
-    if (b.ctr[6] == 3) return;
-    if (!(s.dbg_flags & 8)) commit_grid(s, b);  // 8: ablation, no commit
+    const int full = b.ctr[6];
     for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
         const int c0 = q << 5;
         const int cell = c0 / s.cell;
-        const int4 rec = b.crec[cell];
-        const int count = rec.x;
-        if (count == 0) continue;
         const int c = c0 + lane, t = c - cell * s.cell;
         const bool valid = c < s.Np;
+        // the slice's state (coalesced, cell order) is loaded together with the
+        // cell record, so one memory round trip serves both
         int label = 0, oc = 0, bc = 0, id = -1;
         unsigned long long OW = 0, UW = 0;
+        uint32_t cw = 0;
         if (valid) {
             id = s.orig[c];
-            const uint32_t cw = s.cnt[c];
-            oc = cw & 0xffff;
-            bc = cw >> 16;
+            cw = s.cnt[c];
             if (!WIDE) {
                 OW = s.over[c];
                 UW = s.under[c];
             }
-            label = s.state[id];
+            label = s.state_c[c];
         }
+        const int4 rec = b.crec[cell];
+        const int count = rec.x;
+        if (full == 3) return;
+        if (count == 0) continue;
+        oc = cw & 0xffff;
+        bc = cw >> 16;
         const int label0 = label;
         const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
         const unsigned long long OW0 = OW, UW0 = UW;
@@ -1562,6 +1602,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
         if (valid) {
             if (label != label0) {
                 s.state[id] = static_cast<uint8_t>(label);
+                s.state_c[c] = static_cast<uint8_t>(label);
                 dgray += (label == 2) - (label0 == 2);
             }
             const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
@@ -1582,6 +1623,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     }
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
     if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
+    if (full != 3 && !(s.dbg_flags & 8)) commit_grid(s, b);  // 8: ablation, no commit
     tl_stop(b.tl, 4, t0);
 }
 
@@ -1678,9 +1720,12 @@ __global__ void __launch_bounds__(kCompactThreads) gray_write_kernel(const uint8
     }
 }
 
-__global__ void write_states_kernel(uint8_t* state, const int32_t* ids, const uint8_t* st, int n) {
+__global__ void write_states_kernel(Store s, const int32_t* ids, const uint8_t* st, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) state[ids[i]] = st[i];
+    if (i >= n) return;
+    s.state[ids[i]] = st[i];
+    const int c = s.rank[ids[i]];
+    if (c >= 0) s.state_c[c] = st[i];
 }
 
 __global__ void pair_masks_kernel(Store s, const int32_t* rank, int kind, const int32_t* cand, int n, int o,
@@ -1838,6 +1883,8 @@ static int under_lanes() {
 }
 
 static cudaError_t launch_narrow(const Store& s, const Batch& b, int grid, cudaStream_t st, bool pdl) {
+    static const int forced = std::getenv("RGG_NARROW_CTAS") ? std::atoi(std::getenv("RGG_NARROW_CTAS")) : 0;
+    if (forced > 0) grid = forced;
     switch (under_lanes()) {
         case 2:
             return pdl ? launch_pdl(narrow_kernel<false, 2>, dim3(grid), dim3(128), st, s, b)
@@ -1867,6 +1914,7 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
         }
         cudaError_t e = launch_pdl(touch_warp_kernel<false>, dim3(g_touch), dim3(32 * kWarpsPerCta), st, s, b);
         if (e == cudaSuccess) e = launch_narrow(s, b, grid, st, true);
+        if (e == cudaSuccess && (s.dbg_flags & 16)) e = launch_narrow(s, b, grid, st, true);  // 16: run twice (warm)
         if (e != cudaSuccess) return e;
         const bool wide = s.W > 1;
         const int ga = g_apply;
@@ -1942,7 +1990,7 @@ cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, 
 
 cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    write_states_kernel<<<(n + 255) / 256, 256, 0, st>>>(s.state, ids, st_in, n);
+    write_states_kernel<<<(n + 255) / 256, 256, 0, st>>>(s, ids, st_in, n);
     return cudaGetLastError();
 }
 

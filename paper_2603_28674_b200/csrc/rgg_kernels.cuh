@@ -54,6 +54,8 @@ struct Store {
     const double* osr;         // M
     const int32_t* osn;        // M
     uint8_t* state;            // N labels (component-id order)
+    uint8_t* state_c;          // Np labels (cell order): the apply kernels' coalesced working copy
+    const int32_t* rank;       // N: component id -> cell-order index, -1 if another shard's
     uint32_t* cnt;             // Np: over_cnt | both_cnt << 16
     unsigned long long* over;  // W*Np, word-major
     unsigned long long* under; // W*Np
