@@ -13,9 +13,13 @@
 //    Scene& (obstacles[o].pose, .active) on every move (engine_batch.cpp:156-158);
 //  * std::invalid_argument("unknown obstacle id") / ("obstacle bitsets support at
 //    most 64 obstacles") are thrown with the reference's texts;
-//  * lazy updates are resolved entirely on the GPU; eager updates resolve the
-//    GRAY over-hits of each move with the reference's exact_component_valid on
-//    the host (roadmap.cpp:129-163) and write the labels back, move by move.
+//  * lazy and eager updates and resolve_all_unknown run on the GPU.  The exact
+//    resolve (exact_component_valid, roadmap.cpp:129-163) needs the world pose of
+//    every body at every discretized configuration: on first use the wrapper
+//    evaluates the reference's own forward_kinematics (robot.cpp:66-84) over
+//    components.cfgs once and uploads it (rgg_gpu_set_resolver).  The GPU checks
+//    against the obstacles this engine has moved, so a Scene whose obstacles are
+//    active before the engine moves them is rejected with std::logic_error.
 // Not provided: grid() (the GPU engine has no SpatialGrid; its cells are the
 // cell-sorted component blocks of rgg_gpu_create).
 #pragma once
@@ -28,6 +32,7 @@
 
 #include "rgg/batch_layout.hpp"
 #include "rgg/roadmap.hpp"
+#include "rgg/robot.hpp"
 #include "rgg/update_report.hpp"
 #include "rgg_gpu.h"
 
@@ -109,10 +114,7 @@ public:
     std::vector<UpdateReport> batch_update(const std::vector<std::pair<ObstacleId, Transform>>& moves, bool lazy) {
         std::vector<UpdateReport> out;
         if (moves.empty()) return out;
-        if (!lazy) {  // eager: move by move, exact resolve of the gray over-hits on the host
-            for (const auto& m : moves) out.push_back(eager_move(m.first, m.second));
-            return out;
-        }
+        if (!lazy) ensure_resolver();
         std::vector<std::int32_t> ids;
         std::vector<double> rt;
         for (const auto& [o, pose] : moves) {
@@ -121,8 +123,9 @@ public:
             rt.push_back(pose.t.x), rt.push_back(pose.t.y), rt.push_back(pose.t.z);
         }
         std::vector<rgg_update_report> rep(moves.size());
+        // eager: move by move on the device, each move's gray over-hits resolved exactly
         const int rc = rgg_gpu_update(h_, ids.data(), rt.data(), static_cast<std::int32_t>(ids.size()),
-                                      RGG_LAZY | RGG_PER_MOVE, rep.data());
+                                      (lazy ? RGG_LAZY : RGG_EAGER) | RGG_PER_MOVE, rep.data());
         // the moves the device applied (all, or those before an unknown id) mutate the scene
         size_t applied = moves.size();
         if (rc == RGG_EINVAL)
@@ -133,6 +136,7 @@ public:
         for (size_t i = 0; i < applied; ++i) {
             scene_.obstacles[moves[i].first].pose = moves[i].second;
             scene_.obstacles[moves[i].first].active = true;
+            moved_[moves[i].first] = 1;
         }
         stale_ = true;
         if (rc != RGG_OK) raise(rc, rgg_gpu_last_error(h_));
@@ -141,14 +145,9 @@ public:
     }
 
     int resolve_all_unknown() {
+        ensure_resolver();
         std::int32_t n = 0;
-        check(rgg_gpu_gray_ids(h_, nullptr, 0, &n));
-        std::vector<std::int32_t> ids(n);
-        if (n) check(rgg_gpu_gray_ids(h_, ids.data(), n, &n));
-        std::vector<std::uint8_t> st(n);
-        for (std::int32_t i = 0; i < n; ++i)
-            st[i] = exact_component_valid(components_->cfgs[ids[i]], scene_.robot, scene_) ? 0 : 1;
-        if (n) check(rgg_gpu_write_states(h_, ids.data(), st.data(), n));
+        check(rgg_gpu_resolve_all(h_, &n));
         stale_ = true;
         return n;
     }
@@ -210,29 +209,36 @@ private:
         check(rgg_gpu_read_bits(h_, bits_.data(), words_));
         stale_ = false;
     }
-    // engine_batch.cpp:190-202: the over-hits of this move still Unknown after the
-    // heuristic are resolved exactly; finish_counts compares pre-move and final labels.
-    UpdateReport eager_move(ObstacleId o, const Transform& pose) {
-        refresh();
-        const std::vector<ValidityState> before = states_;
-        UpdateReport r = batch_update({{o, pose}}, true).at(0);
-        std::int32_t n = 0;
-        check(rgg_gpu_last_hits(h_, nullptr, 0, &n));
-        std::vector<std::int32_t> hits(n);
-        if (n) check(rgg_gpu_last_hits(h_, hits.data(), n, &n));
-        std::vector<std::uint8_t> st(n);
-        for (std::int32_t i = 0; i < n; ++i) {
-            const ComponentId c = hits[i];
-            st[i] = exact_component_valid(components_->cfgs[c], scene_.robot, scene_) ? 0 : 1;
-            if (before[c] != ValidityState::Unknown) --r.new_gray;
-            if (st[i] == 0 && before[c] != ValidityState::Valid) ++r.new_green;
-            if (st[i] == 1 && before[c] != ValidityState::Invalid) ++r.new_red;
-        }
-        if (n) check(rgg_gpu_write_states(h_, hits.data(), st.data(), n));
-        r.resolve_checks = n;
-        r.residual_unknown = unknown_count();
-        stale_ = true;
-        return r;
+    // The exact resolve's inputs, once: forward_kinematics of every configuration
+    // (body-major per configuration) and the body half extents.
+    void ensure_resolver() {
+        for (size_t o = 0; o < scene_.obstacles.size(); ++o)
+            if (scene_.obstacles[o].active && !moved_[o])
+                throw std::logic_error("GPU exact resolve: obstacle active before this engine moved it");
+        if (resolver_ready_) return;
+        const RobotModel& m = scene_.robot;
+        const int B = static_cast<int>(m.bodies.size());
+        const size_t N = components_->cfgs.size();
+        std::vector<std::int64_t> off(N + 1, 0);
+        for (size_t c = 0; c < N; ++c) off[c + 1] = off[c] + static_cast<std::int64_t>(components_->cfgs[c].size());
+        std::vector<double> poses(static_cast<size_t>(off[N]) * B * 12);
+        std::vector<double> he(static_cast<size_t>(B) * 3);
+        for (int b = 0; b < B; ++b)
+            he[3 * b] = m.bodies[b].half_extents.x, he[3 * b + 1] = m.bodies[b].half_extents.y,
+                   he[3 * b + 2] = m.bodies[b].half_extents.z;
+        size_t k = 0;
+        for (size_t c = 0; c < N; ++c)
+            for (const Configuration& cfg : components_->cfgs[c]) {
+                const std::vector<Transform> fk = forward_kinematics(m, cfg);
+                for (int b = 0; b < B; ++b, ++k) {
+                    double* d = &poses[k * 12];
+                    for (int j = 0; j < 9; ++j) d[j] = fk[b].r[j];
+                    d[9] = fk[b].t.x, d[10] = fk[b].t.y, d[11] = fk[b].t.z;
+                }
+            }
+        const rgg_resolve_view v{static_cast<std::int32_t>(N), B, he.data(), off.data(), poses.data()};
+        check(rgg_gpu_set_resolver(h_, &v));
+        resolver_ready_ = true;
     }
 
     const ComponentSet* components_;
@@ -244,6 +250,8 @@ private:
     rgg_gpu* h_ = nullptr;
     std::int32_t words_ = 1;
     mutable bool stale_ = false;
+    bool resolver_ready_ = false;
+    std::vector<std::uint8_t> moved_ = std::vector<std::uint8_t>(scene_.obstacles.size(), 0);
     mutable std::vector<ValidityState> states_;
     mutable std::vector<std::uint64_t> bits_;
 };

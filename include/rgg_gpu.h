@@ -38,11 +38,14 @@ extern "C" {
 #define RGG_GRAY 2
 
 /* rgg_gpu_update flags */
-#define RGG_LAZY 1      /* lazy update (the only mode the GPU resolves by itself) */
+#define RGG_LAZY 1      /* lazy update: over-hit components stay GRAY */
 #define RGG_PER_MOVE 2  /* fill one rgg_update_report per move (finish_counts semantics) */
 #define RGG_ASYNC 4     /* enqueue only; the call returns before the device finishes */
 #define RGG_CENSUS 8    /* also count the algorithmic bytes of this update (read by rgg_gpu_census) */
 #define RGG_GRAY_LIST 16 /* compact the GRAY ids inside the update (else lazily in rgg_gpu_gray_ids) */
+#define RGG_EAGER 32    /* eager update (update_obstacle(o, pose, lazy = false), engine_batch.cpp:193-200):
+                           each move's GRAY over-hits are resolved exactly on the GPU before the next move.
+                           Needs rgg_gpu_set_resolver; implies PER_MOVE; not ASYNC. */
 
 /* The serialized store, borrowed for the duration of rgg_gpu_create.  It is the
  * reference's BatchLayout (proj/include/rgg/batch_layout.hpp:23-66) with the padded
@@ -146,6 +149,29 @@ int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
 int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
 /* Eager / resolve_all_unknown write-back: states[ids[i]] = st[i] (bits untouched). */
 int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int32_t n);
+/* Exact resolve on the GPU (exact_component_valid, proj/src/roadmap.cpp:129-163).
+ * The forward kinematics of every discretized configuration (robot.cpp:66-84) is
+ * evaluated on the host once and uploaded: for component c (id order), its
+ * configurations are [pose_off[c], pose_off[c+1]), and configuration k's body b
+ * has the world pose poses[(k*B + b)*12 ..] (row-major rotation r[9], then t[3]),
+ * i.e. forward_kinematics(robot, cfgs[c][j])[b].  Obstacles are exact-checked at
+ * the poses this engine's moves gave them (active after their first move, like
+ * the reference's Scene when it starts with inactive obstacles). */
+typedef struct rgg_resolve_view {
+    int32_t n_components;           /* N */
+    int32_t n_bodies;               /* B (the layout's) */
+    const double* body_half_extents; /* B*3 */
+    const int64_t* pose_off;        /* N+1 */
+    const double* poses;            /* pose_off[N]*B*12 */
+} rgg_resolve_view;
+int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* view);
+/* resolve_all_unknown (engine_batch.cpp:217-227): every GRAY component becomes
+ * GREEN (free) or RED; *resolved = how many were GRAY. */
+int rgg_gpu_resolve_all(rgg_gpu* h, int32_t* resolved);
+/* exact_component_valid of ids[0..n) at the current obstacle poses, without
+ * changing any label: out[i] = RGG_GREEN (free) or RGG_RED. */
+int rgg_gpu_exact_check(rgg_gpu* h, const int32_t* ids, int32_t n, uint8_t* out);
+
 /* batch_over (kind 0) / batch_under (kind 1) on explicit candidates against
  * obstacle o at its current pose (engine_batch.hpp:34-37). */
 int rgg_gpu_pair_masks(rgg_gpu* h, int32_t kind, const int32_t* cand, int32_t n, int32_t o, uint8_t* mask);

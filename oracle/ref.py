@@ -50,6 +50,10 @@ def lib():
         L.rr_engine_free.argtypes = [C.c_void_p]
         L.rr_engine_update.argtypes = [C.c_void_p, C.c_int32, _dp, C.c_int, _lp]
         L.rr_engine_run.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.POINTER(C.c_double)]
+        L.rr_world_poses.argtypes = [C.c_void_p, _lp, C.c_void_p]
+        L.rr_world_body_he.argtypes = [C.c_void_p, _dp]
+        L.rr_engine_exact.argtypes = [C.c_void_p, C.c_int, _ip, _up]
+        L.rr_engine_resolve_all.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.rr_engine_states.argtypes = [C.c_void_p, _up]
         L.rr_engine_bits.argtypes = [C.c_void_p, _qp]
         L.rr_engine_groups.argtypes = [C.c_void_p]
@@ -158,6 +162,21 @@ class World:
         _check(lib().rr_world_obbs(self.h, out.reshape(-1)))
         return out
 
+    def poses(self):
+        """(off int64[N+1], poses float64[total, B, 12]): forward_kinematics of every
+        discretized configuration, the exact resolve's inputs (rr_world_poses)."""
+        k = self.counts()
+        off = np.zeros(k["N"] + 1, np.int64)
+        _check(lib().rr_world_poses(self.h, off, None))
+        poses = np.zeros((int(off[-1]), k["B"], 12))
+        _check(lib().rr_world_poses(self.h, off, poses.ctypes.data_as(C.c_void_p)))
+        return off, poses
+
+    def body_half_extents(self):
+        he = np.zeros((self.counts()["B"], 3))
+        _check(lib().rr_world_body_he(self.h, he.reshape(-1)))
+        return he
+
     def obstacle_operands(self, o: int, rt12):
         k = self.counts()
         sat, aabb, cen, saabb = np.zeros(21), np.zeros(6), np.zeros(k["C"] * 3), np.zeros(6)
@@ -185,6 +204,18 @@ class Engine:
         rep = np.zeros(11, np.int64)
         _check(lib().rr_engine_update(self.h, int(o), np.ascontiguousarray(rt12, np.float64), int(lazy), rep))
         return rep
+
+    def exact_free(self, ids) -> np.ndarray:
+        """exact_component_valid of ids at this engine's obstacle poses (1 = free)."""
+        ids = np.ascontiguousarray(ids, np.int32)
+        out = np.zeros(len(ids), np.uint8)
+        _check(lib().rr_engine_exact(self.h, len(ids), ids, out))
+        return out
+
+    def resolve_all_unknown(self) -> int:
+        n = C.c_int32(0)
+        _check(lib().rr_engine_resolve_all(self.h, C.byref(n)))
+        return n.value
 
     def run(self, ids, rts, lazy=True) -> float:
         ids = np.ascontiguousarray(ids, np.int32)

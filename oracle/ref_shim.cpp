@@ -390,6 +390,62 @@ int rr_engine_run(void* ep, int n, const std::int32_t* ids, const double* rt12, 
     });
 }
 
+// Exact-resolve inputs: forward_kinematics (proj/src/robot.cpp:66-84) of every
+// discretized configuration of every component (build_components,
+// roadmap.cpp:104-127), body-major per configuration: off[N+1] (configurations),
+// poses[total*B*12] (r[9], t[3]).  Pass poses = nullptr to size the buffer.
+int rr_world_poses(void* wp, std::int64_t* off, double* poses) {
+    const World* w = static_cast<const World*>(wp);
+    return guarded([&] {
+        const RobotModel& m = w->scene.robot;
+        const int B = static_cast<int>(m.bodies.size());
+        std::int64_t k = 0;
+        off[0] = 0;
+        for (size_t c = 0; c < w->comps.cfgs.size(); ++c) {
+            for (const Configuration& cfg : w->comps.cfgs[c]) {
+                if (poses) {
+                    const std::vector<Transform> fk = forward_kinematics(m, cfg);
+                    for (int b = 0; b < B; ++b) put_tf(fk[b], poses + (k * B + b) * 12);
+                }
+                ++k;
+            }
+            off[c + 1] = k;
+        }
+    });
+}
+
+// Robot body half extents (robot.hpp BoxBody), B*3.
+int rr_world_body_he(void* wp, double* he) {
+    const World* w = static_cast<const World*>(wp);
+    return guarded([&] {
+        for (size_t b = 0; b < w->scene.robot.bodies.size(); ++b) {
+            const Vec3& v = w->scene.robot.bodies[b].half_extents;
+            he[3 * b] = v.x, he[3 * b + 1] = v.y, he[3 * b + 2] = v.z;
+        }
+    });
+}
+
+// exact_component_valid (roadmap.cpp:129-163) of ids against the scene of a
+// single-group engine (its obstacles posed and activated by its moves).
+int rr_engine_exact(void* ep, int n, const std::int32_t* ids, std::uint8_t* free_out) {
+    Engine* e = static_cast<Engine*>(ep);
+    return guarded([&] {
+        if (e->groups.size() != 1) throw std::invalid_argument("exact checks need a single obstacle group");
+        const Scene& sc = e->groups[0]->scene;
+        for (int i = 0; i < n; ++i)
+            free_out[i] = exact_component_valid(e->world->comps.cfgs[ids[i]], sc.robot, sc) ? 1 : 0;
+    });
+}
+
+// BatchEngine::resolve_all_unknown (engine_batch.cpp:217-227), single group.
+int rr_engine_resolve_all(void* ep, std::int32_t* resolved) {
+    Engine* e = static_cast<Engine*>(ep);
+    return guarded([&] {
+        if (e->groups.size() != 1 || !e->groups[0]->bat) throw std::invalid_argument("single batch engine only");
+        *resolved = e->groups[0]->bat->resolve_all_unknown();
+    });
+}
+
 // Combined labels: red > gray > green over groups.
 int rr_engine_states(void* ep, std::uint8_t* out) {
     Engine* e = static_cast<Engine*>(ep);

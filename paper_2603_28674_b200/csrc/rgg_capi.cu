@@ -55,6 +55,17 @@ struct rgg_gpu {
     int32_t* d_gray = nullptr;
     int32_t* d_tiles = nullptr;
     int32_t* d_hits = nullptr;
+    uint8_t* d_hits_prev = nullptr;
+    // exact resolve (rgg_resolve.cu): per-configuration body poses, obstacle polytopes
+    bool res_ready = false;
+    int32_t res_B = 0;
+    double* d_res_he = nullptr;
+    long long* d_res_off = nullptr;
+    double* d_res_pose = nullptr;
+    rggk::ObsPoly* d_opoly = nullptr;
+    int32_t* d_res_ids = nullptr;  // N: scratch id list (rgg_gpu_exact_check)
+    int32_t* d_res_cnt = nullptr;
+    uint8_t* d_res_out = nullptr;  // N
     int32_t* d_cell_count = nullptr;
     int32_t* d_cell_list = nullptr;
     int32_t* d_cell_ovf = nullptr;
@@ -215,6 +226,7 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.dirty = h->d_dirty;
     b.mv = h->d_mv;
     b.hits = h->d_hits;
+    b.hits_prev = h->d_hits_prev;
     b.census = h->d_census;
     b.unknown = h->d_unknown;
     b.mpool = h->d_mpool;
@@ -263,6 +275,19 @@ void dump_timeline(rgg_gpu* h) {
 // Narrow items pack the event index with a 5-bit position (rgg_kernels.cu).
 constexpr int32_t kMaxBatch = 1 << 26;
 
+rggk::Resolver resolver_of(rgg_gpu* h) {
+    rggk::Resolver r{};
+    r.B = h->res_B;
+    r.he = h->d_res_he;
+    r.off = h->d_res_off;
+    r.pose = h->d_res_pose;
+    r.opoly = h->d_opoly;
+    return r;
+}
+
+// grid bound of the eager resolve (a move's gray over-hits; the kernel strides)
+constexpr int kEagerResolveGrid = 2048;
+
 // Enqueue the whole pipeline for n moves already in d_ids/d_rt.
 int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     Batch b = batch_of(h, n);
@@ -283,7 +308,12 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // the gray id list is compacted in the update only on request; otherwise lazily
     // by rgg_gpu_gray_ids (labels, reports and the gray count never need it)
     const bool gray_list = (flags & RGG_GRAY_LIST) != 0;
-    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0);
+    const bool eager = (flags & RGG_EAGER) != 0;  // n == 1: resolve the move's gray over-hits
+    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0) | (eager ? 512 : 0);
+    const auto resolve_hits = [&]() {
+        return rggk::launch_resolve(h->s, resolver_of(h), b, h->d_hits, h->d_ctr + 5, kEagerResolveGrid, rggk::kEager,
+                                    nullptr, h->stream);
+    };
     if (use_graph) {
         cudaGraphExec_t exec = nullptr;
         for (const auto& g : h->graphs)
@@ -304,6 +334,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[2]);
             if (e == cudaSuccess) e = rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
+            if (e == cudaSuccess && eager) e = resolve_hits();
             if (e == cudaSuccess) e = rec(h->ev[3]);
             if (e == cudaSuccess && gray_list)
                 e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
@@ -321,7 +352,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         h->gray_fresh = gray_list;
         h->last_n = n;
         h->last_flags = flags;
-        h->last_hits_valid = n == 1;
+        h->last_hits_valid = n == 1 && !eager;
         h->timed = true;
         h->unknown_stale = true;
         return RGG_OK;
@@ -398,13 +429,14 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         rggk::filter_stats(fs, true);
         std::fprintf(stderr, "[rgg] fp64 rechecks: SAT %llu, seg-sphere %llu\n", fs[1], fs[3]);
     }
+    if (eager) CK(resolve_hits());
     CK(cudaEventRecord(h->ev[3], h->stream));
     if (gray_list) CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
     CK(cudaEventRecord(h->ev[4], h->stream));
     h->gray_fresh = gray_list;
     h->last_n = n;
     h->last_flags = flags;
-    h->last_hits_valid = n == 1;
+    h->last_hits_valid = n == 1 && !eager;
     h->timed = true;
     h->unknown_stale = true;
     return RGG_OK;
@@ -614,6 +646,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_gray, N));
     CK(dalloc(&h->d_tiles, N / 4096 + 2));
     CK(dalloc(&h->d_hits, N));
+    CK(dalloc(&h->d_hits_prev, static_cast<size_t>(N) + 16));
     CK(dalloc(&h->d_cell_count, ncells));
     CK(dalloc(&h->d_cell_list, static_cast<size_t>(ncells) * cap));
     CK(dalloc(&h->d_cell_ovf, ncells));
@@ -701,7 +734,8 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
-                   h->d_mv, h->d_pool, h->d_tl, h->d_dbg};
+                   h->d_mv, h->d_pool, h->d_tl, h->d_dbg, h->d_hits_prev,
+                   h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_ids, h->d_res_cnt, h->d_res_out};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* pin[] = {h->h_ids, h->h_mv, h->h_ctr};
@@ -714,16 +748,34 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     delete h;
 }
 
+static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
+                       rgg_update_report* reports);
+
 int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
                    rgg_update_report* reports) {
     if (!h) return RGG_EINVAL;
     clear_stale_error();
     if (n < 0 || (n > 0 && (!ids || !rt12))) return fail(h, RGG_EINVAL, "bad move list");
     if (n >= kMaxBatch) return fail(h, RGG_EINVAL, "at most 2^26 - 1 moves per batch (split it)");
-    if (!(flags & RGG_LAZY))
-        return fail(h, RGG_EINVAL, "eager updates resolve gray components on the host: call with RGG_LAZY per move, "
-                                   "then rgg_gpu_last_hits + rgg_gpu_write_states");
-    if ((flags & RGG_ASYNC) && reports) return fail(h, RGG_EINVAL, "reports need a synchronous update");
+    if (!(flags & (RGG_LAZY | RGG_EAGER)))
+        return fail(h, RGG_EINVAL, "pass RGG_LAZY or RGG_EAGER");
+    if ((flags & RGG_ASYNC) && (reports || (flags & RGG_EAGER)))
+        return fail(h, RGG_EINVAL, "reports and eager updates need a synchronous update");
+    if (!(flags & RGG_EAGER)) return update_core(h, ids, rt12, n, flags, reports);
+    // eager: one move at a time, each resolving its gray over-hits before the next
+    // (BatchEngine::batch_update(moves, false) = update_obstacle per move)
+    if (!h->res_ready) return fail(h, RGG_EINVAL, "eager updates need rgg_gpu_set_resolver");
+    if (!rggk::split_pipeline()) return fail(h, RGG_EINVAL, "eager updates need RGG_PIPELINE=6");
+    for (int32_t i = 0; i < n; ++i) {
+        const int rc = update_core(h, ids + i, rt12 + 12 * static_cast<size_t>(i), 1,
+                                   (flags & ~RGG_LAZY) | RGG_EAGER | RGG_PER_MOVE, reports ? reports + i : nullptr);
+        if (rc) return rc;
+    }
+    return RGG_OK;
+}
+
+static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
+                       rgg_update_report* reports) {
     CK(cudaSetDevice(h->device));
     // the reference applies moves in order and throws at the first bad id
     int32_t k = 0;
@@ -753,7 +805,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
         if (!(flags & RGG_ASYNC) || bad) {
             if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
                                             cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 17 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
             dump_timeline(h);
             for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {
@@ -764,7 +816,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
                 if (rc) return rc;
                 if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
                                                 cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 17 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaStreamSynchronize(h->stream));
             }
             if (h->h_ctr[6])
@@ -791,6 +843,14 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
                         r.residual_unknown = u;
                     } else {
                         r.unknown_after_heuristic = r.residual_unknown = h->unknown;
+                    }
+                    if (flags & RGG_EAGER) {  // n == 1: the resolve's finish_counts terms
+                        const int32_t checks = h->h_ctr[5];
+                        r.new_green += h->h_ctr[20];
+                        r.new_red += h->h_ctr[21];
+                        r.new_gray += h->h_ctr[22];
+                        r.resolve_checks = checks;
+                        r.residual_unknown = r.unknown_after_heuristic - checks;
                     }
                 }
                 rgg_update_report& last = reports[k - 1];
@@ -940,6 +1000,85 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
     cudaFree(d_st);
     h->unknown_stale = true;
     h->last_hits_valid = false;
+    return RGG_OK;
+}
+
+int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* v) {
+    if (!h || !v) return RGG_EINVAL;
+    clear_stale_error();
+    if (v->n_components != h->s.N) return fail(h, RGG_EINVAL, "resolver: component count differs from the layout");
+    if (v->n_bodies != h->s.B) return fail(h, RGG_EINVAL, "resolver: body count differs from the layout");
+    if (!v->body_half_extents || !v->pose_off || (!v->poses && v->pose_off[v->n_components] > 0))
+        return fail(h, RGG_EINVAL, "resolver: null array");
+    const int32_t N = v->n_components, B = v->n_bodies;
+    if (v->pose_off[0] != 0) return fail(h, RGG_EINVAL, "resolver: pose_off[0] must be 0");
+    for (int32_t c = 0; c < N; ++c)
+        if (v->pose_off[c + 1] < v->pose_off[c]) return fail(h, RGG_EINVAL, "resolver: pose_off not ascending");
+    for (int k = 0; k < 3 * B; ++k)
+        if (!(v->body_half_extents[k] > 0.0)) return fail(h, RGG_EINVAL, "degenerate polytope");  // geometry.cpp:280
+    const int64_t total = v->pose_off[N];
+    CK(cudaSetDevice(h->device));
+    cudaFree(h->d_res_he);
+    cudaFree(h->d_res_off);
+    cudaFree(h->d_res_pose);
+    h->d_res_he = nullptr, h->d_res_off = nullptr, h->d_res_pose = nullptr;
+    CK(dalloc(&h->d_res_he, static_cast<size_t>(B) * 3));
+    CK(dalloc(&h->d_res_off, static_cast<size_t>(N) + 1));
+    CK(dalloc(&h->d_res_pose, static_cast<size_t>(total) * B * 12));
+    if (!h->d_opoly) CK(dalloc(&h->d_opoly, static_cast<size_t>(std::max(1, h->s.M))));
+    if (!h->d_res_ids) CK(dalloc(&h->d_res_ids, static_cast<size_t>(N) + 1));
+    if (!h->d_res_out) CK(dalloc(&h->d_res_out, static_cast<size_t>(N) + 1));
+    if (!h->d_res_cnt) CK(dalloc(&h->d_res_cnt, 1));
+    CK(cudaMemcpy(h->d_res_he, v->body_half_extents, static_cast<size_t>(B) * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    static_assert(sizeof(long long) == sizeof(int64_t), "int64 offsets");
+    CK(cudaMemcpy(h->d_res_off, v->pose_off, (static_cast<size_t>(N) + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (total > 0)
+        CK(cudaMemcpy(h->d_res_pose, v->poses, static_cast<size_t>(total) * B * 12 * sizeof(double),
+                      cudaMemcpyHostToDevice));
+    h->res_B = B;
+    h->res_ready = true;
+    return RGG_OK;
+}
+
+int rgg_gpu_resolve_all(rgg_gpu* h, int32_t* resolved) {
+    if (!h) return RGG_EINVAL;
+    clear_stale_error();
+    if (!h->res_ready) return fail(h, RGG_EINVAL, "resolve_all_unknown needs rgg_gpu_set_resolver");
+    CK(cudaSetDevice(h->device));
+    int32_t n = 0;
+    int rc = rgg_gpu_gray_ids(h, nullptr, 0, &n);  // compacts the gray list on the device
+    if (rc) return rc;
+    if (n > 0) {
+        const Batch b = batch_of(h, 1);
+        CK(rggk::launch_resolve(h->s, resolver_of(h), b, h->d_gray, h->d_ctr + 4, n, rggk::kResolve, nullptr,
+                                h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    h->gray_fresh = false;
+    h->unknown_stale = true;
+    h->last_hits_valid = false;
+    rc = refresh_unknown(h);
+    if (rc) return rc;
+    if (resolved) *resolved = n;
+    return RGG_OK;
+}
+
+int rgg_gpu_exact_check(rgg_gpu* h, const int32_t* ids, int32_t n, uint8_t* out) {
+    if (!h) return RGG_EINVAL;
+    clear_stale_error();
+    if (!h->res_ready) return fail(h, RGG_EINVAL, "exact checks need rgg_gpu_set_resolver");
+    if (n < 0 || n > h->s.N || (n > 0 && (!ids || !out))) return fail(h, RGG_EINVAL, "bad id list");
+    for (int32_t i = 0; i < n; ++i)
+        if (ids[i] < 0 || ids[i] >= h->s.N) return fail(h, RGG_EINVAL, "unknown component id");
+    if (n == 0) return RGG_OK;
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpyAsync(h->d_res_ids, ids, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_res_cnt, &n, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+    const Batch b = batch_of(h, 1);
+    CK(rggk::launch_resolve(h->s, resolver_of(h), b, h->d_res_ids, h->d_res_cnt, n, rggk::kCheck, h->d_res_out,
+                            h->stream));
+    CK(cudaMemcpyAsync(out, h->d_res_out, n, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     return RGG_OK;
 }
 

@@ -161,6 +161,7 @@ __global__ void pose_kernel(Store s, Batch b) {
     if (i == 0 && lane < 16) {
         b.ctr[lane] = 0;
         b.census[lane] = 0;
+        if (lane < 4) b.ctr[20 + lane] = 0;  // eager resolve report deltas
         if (lane == 0) *b.mtop = 0;
     }
     if (i >= b.n) return;
@@ -322,6 +323,7 @@ __global__ void pose_kernel(Store s, Batch b) {
         b.evbox[12 * static_cast<size_t>(i) + lane] = nu;  // compact copy for the binning
         b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol;
     }
+    if (lane < 12) ev.rt[lane] = b.rt[12 * static_cast<size_t>(i) + lane];
     if (lane >= 16 && lane - 16 < nsph) {
         ev.cen[3 * (lane - 16)] = pt[0];
         ev.cen[3 * (lane - 16) + 1] = pt[1];
@@ -359,6 +361,7 @@ __global__ void init_obstacles_kernel(Store s) {
     e.o = o;
     e.nsph = nsph;
     e.move = -1;
+    for (int k = 0; k < 12; ++k) e.rt[k] = id[k];
     aabb_union(e.box, e.sph, e.nu);
     aabb_empty(e.old);
     aabb_empty(s.cur_union + 6 * o);
@@ -1046,7 +1049,11 @@ __global__ void __launch_bounds__(kMaxCell) apply_kernel(Store s, Batch b) {
         int pos = 0;
         if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
         pos = __shfl_sync(0xffffffffu, pos, 0);
-        if (h) b.hits[pos + __popc(bal & ((1u << lane) - 1u))] = id;
+        if (h) {
+                const int at = pos + __popc(bal & ((1u << lane) - 1u));
+                b.hits[at] = id;
+                b.hits_prev[at] = static_cast<uint8_t>(label0);
+            }
     }
 }
 
@@ -1309,7 +1316,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
             int pos = 0;
             if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
             pos = __shfl_sync(0xffffffffu, pos, 0);
-            if (h) b.hits[pos + __popc(bal & ((1u << lane) - 1u))] = id;
+            if (h) {
+                const int at = pos + __popc(bal & ((1u << lane) - 1u));
+                b.hits[at] = id;
+                b.hits_prev[at] = static_cast<uint8_t>(label0);
+            }
         }
         if (dbg) {
             __syncwarp();
@@ -1618,7 +1629,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
             int pos = 0;
             if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
             pos = __shfl_sync(0xffffffffu, pos, 0);
-            if (h) b.hits[pos + __popc(bal & ((1u << lane) - 1u))] = id;
+            if (h) {
+                const int at = pos + __popc(bal & ((1u << lane) - 1u));
+                b.hits[at] = id;
+                b.hits_prev[at] = static_cast<uint8_t>(label0);
+            }
         }
     }
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
@@ -1856,6 +1871,8 @@ static int pipeline() {
     }();
     return p;
 }
+
+bool split_pipeline() { return pipeline() == 6; }
 
 template <int F, bool W>
 static cudaError_t apply6_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {

@@ -25,6 +25,7 @@ struct alignas(16) Event {
     double old[6];   // box U sph at the pose before this move (empty if inactive)
     double cen[kMaxSpheres * 3];
     rggd::Box32 b32;  // fp32 operand of sat (filter), L rounded up
+    double rt[12];    // the pose (row-major rotation, translation): the exact resolve's obstacle
     int32_t o;
     int32_t nsph;
     int32_t move;  // index of the move in the batch
@@ -81,6 +82,7 @@ struct Batch {
     int32_t* dirty;        // ncells
     int32_t* mv;           // n*4: to_green, to_red, to_gray, from_gray
     int32_t* hits;         // N: over-hit-by-last-move & still gray
+    uint8_t* hits_prev;    // N: their labels before the move (eager report counts)
     unsigned long long* census;  // 16 counters: [0..5] narrow census, [8..11] touch census
     uint32_t* mpool;             // touch / over / under mask words (see touch_kernel)
     long long* mtop;             // next free word of mpool
@@ -94,6 +96,32 @@ struct Batch {
     unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
     unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null
 };
+
+// Exact resolve operands (rgg_resolve.cu).
+struct __align__(16) ObsPoly {  // one obstacle as polytopes_intersect sees it
+    double v[24];               // ConvexPolytope::box vertices
+    double ax[9];               // face axes
+    double ed[36];              // 12 edge directions
+    double box[6];              // aabb_of_obb(world_outer())
+    int32_t active;
+    int32_t pad[3];
+};
+
+struct Resolver {
+    int32_t B;               // robot bodies
+    const double* he;        // B*3 body half extents
+    const long long* off;    // N+1: configurations of component c are [off[c], off[c+1])
+    const double* pose;      // off[N]*B*12: world pose of each body box per configuration
+    ObsPoly* opoly;          // M
+};
+
+bool split_pipeline();  // RGG_PIPELINE == 6 (the default): touch / narrow / apply
+
+enum ResolveMode : int { kResolve = 0, kEager = 1, kCheck = 2 };
+// exact check of ids[0..*count_dev) (max_count bounds the grid), after
+// refreshing the obstacle polytopes
+cudaError_t launch_resolve(const Store& s, const Resolver& r, const Batch& b, const int32_t* ids,
+                           const int32_t* count_dev, int max_count, int mode, uint8_t* out, cudaStream_t st);
 
 enum Flags : int32_t { kPerMove = 2, kHits = 8, kCensus = 16 };
 

@@ -35,7 +35,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "librgg_gpu.so")
 
 RGG_OK, RGG_EINVAL, RGG_ECUDA, RGG_ENCCL, RGG_ENOMEM, RGG_ELOGIC = 0, 1, 2, 3, 4, 5
-RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC, RGG_CENSUS, RGG_GRAY_LIST = 1, 2, 4, 8, 16
+RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC, RGG_CENSUS, RGG_GRAY_LIST, RGG_EAGER = 1, 2, 4, 8, 16, 32
 GREEN, RED, GRAY = 0, 1, 2
 
 
@@ -61,6 +61,11 @@ class _Report(C.Structure):
 
 
 _REPORT_DTYPE = np.dtype(_Report)
+
+
+class _ResolveView(C.Structure):
+    _fields_ = [("n_components", C.c_int32), ("n_bodies", C.c_int32), ("body_half_extents", C.c_void_p),
+                ("pose_off", C.c_void_p), ("poses", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -109,6 +114,9 @@ def library() -> C.CDLL:
         L.rgg_gpu_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
         L.rgg_gpu_copy_counters.argtypes = [vp, vp, i32]
         L.rgg_gpu_set_phase_timing.argtypes = [vp, i32]
+        L.rgg_gpu_set_resolver.argtypes = [vp, C.POINTER(_ResolveView)]
+        L.rgg_gpu_resolve_all.argtypes = [vp, ip]
+        L.rgg_gpu_exact_check.argtypes = [vp, vp, i32, vp]
         _lib = L
     return _lib
 
@@ -117,7 +125,8 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_
             "rgg_gpu_sync", "rgg_gpu_count", "rgg_gpu_read_states", "rgg_gpu_read_bits", "rgg_gpu_unknown_count",
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
-            "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing"]
+            "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
+            "rgg_gpu_exact_check"]
 
 
 @dataclass
@@ -243,6 +252,7 @@ class GpuEngine:
         L.rgg_gpu_count(h, C.byref(n), C.byref(m), C.byref(w))
         self.n_components, self.n_obstacles, self.words = n.value, m.value, w.value
         self.layout = lv
+        self._resolver = None
 
     # ------------------------------------------------------------- plumbing
     @staticmethod
@@ -276,6 +286,14 @@ class GpuEngine:
         """moves: list of (obstacle, pose12) pairs, or a tuple (ids int32[n], rt12 float64[n, 12])."""
         ids, rts = self._moves(moves)
         if not lazy:
+            if self._resolver is not None and resolve is None:  # exact resolve on the GPU, move by move
+                n = len(ids)
+                if n == 0:
+                    return []
+                reps = (_Report * n)()
+                self._check(library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, n,
+                                                     RGG_EAGER | RGG_PER_MOVE, reps))
+                return Reports(reps)
             return [self.update_obstacle(int(o), r, lazy=False, resolve=resolve) for o, r in zip(ids, rts)]
         n = len(ids)
         if n == 0:
@@ -294,7 +312,9 @@ class GpuEngine:
         if lazy:
             return self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=True)[0]
         if resolve is None:
-            raise ValueError("eager updates need an exact resolver for the gray over-hits")
+            if self._resolver is None:
+                raise ValueError("eager updates need set_resolver() (GPU exact resolve) or a resolve callable")
+            return self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=False)[0]
         before = self.states()
         rep = self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=True)[0]
         hits = self.last_hits()
@@ -309,6 +329,41 @@ class GpuEngine:
             rep.new_red += int(np.sum((st == RED) & (b0 != RED)))
         rep.residual_unknown = self.unknown_count()
         return rep
+
+    # ------------------------------------------------------ exact resolve
+    def set_resolver(self, pose_off, poses, body_half_extents):
+        """Upload the exact resolve's inputs (include/rgg_gpu.h rgg_resolve_view):
+        pose_off int64[N+1], poses float64[total, B, 12] = forward_kinematics of every
+        discretized configuration (robot.cpp:66-84), body_half_extents (B, 3)."""
+        off = np.ascontiguousarray(pose_off, np.int64)
+        ps = np.ascontiguousarray(poses, np.float64)
+        he = np.ascontiguousarray(body_half_extents, np.float64).reshape(-1, 3)
+        if off.shape != (self.n_components + 1,):
+            raise ValueError("resolver: component count differs from the layout")
+        if ps.size != int(off[-1]) * he.shape[0] * 12:
+            raise ValueError("resolver: poses must hold pose_off[N] x B x 12 doubles")
+        v = _ResolveView(self.n_components, he.shape[0], he.ctypes.data, off.ctypes.data, ps.ctypes.data)
+        self._check(library().rgg_gpu_set_resolver(self._h, C.byref(v)))
+        self._resolver = (off, he)
+
+    def resolve_all_unknown(self, resolve: Callable[[np.ndarray], np.ndarray] | None = None) -> int:
+        """BatchEngine::resolve_all_unknown (engine_batch.cpp:217-227): on the GPU after
+        set_resolver(), or with an exact check supplied by the caller."""
+        if resolve is not None:
+            ids = self.gray_ids()
+            if len(ids):
+                self.write_states(ids, np.asarray(resolve(ids), np.uint8))
+            return len(ids)
+        n = C.c_int32(0)
+        self._check(library().rgg_gpu_resolve_all(self._h, C.byref(n)))
+        return n.value
+
+    def exact_check(self, ids) -> np.ndarray:
+        """exact_component_valid (roadmap.cpp:129-163) of ids: uint8 GREEN (free) / RED."""
+        ids = np.ascontiguousarray(ids, np.int32)
+        out = np.empty(len(ids), np.uint8)
+        self._check(library().rgg_gpu_exact_check(self._h, ids.ctypes.data, len(ids), out.ctypes.data))
+        return out
 
     def update_async(self, ids, rts):
         """Enqueue a lazy batch without waiting (timed device path)."""
@@ -397,14 +452,6 @@ class GpuEngine:
         ids = np.ascontiguousarray(ids, np.int32)
         st = np.ascontiguousarray(st, np.uint8)
         self._check(library().rgg_gpu_write_states(self._h, ids.ctypes.data, st.ctypes.data, len(ids)))
-
-    def resolve_all_unknown(self, resolve: Callable[[np.ndarray], np.ndarray]) -> int:
-        """BatchEngine::resolve_all_unknown (engine_batch.cpp:217-227) with the exact
-        check supplied by the caller."""
-        ids = self.gray_ids()
-        if len(ids):
-            self.write_states(ids, np.asarray(resolve(ids), np.uint8))
-        return len(ids)
 
     def _mask(self, kind, candidates, o) -> np.ndarray:
         cands = np.ascontiguousarray(candidates, np.int32)

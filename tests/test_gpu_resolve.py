@@ -1,0 +1,133 @@
+"""GPU exact resolve against the live reference.
+
+exact_component_valid (proj/src/roadmap.cpp:129-163) is restated on the GPU in
+paper_2603_28674_b200/csrc/rgg_resolve.cu.  These tests drive the reference's own
+engines from oracle/_ref (built from /root/reference by oracle/Makefile; the
+prebuilt library travels to the GPU box) and require bit-identical verdicts:
+  * per-component exact checks after lazy moves    roadmap.cpp:129-163
+  * eager updates, labels + reports after every move  engine_batch.cpp:190-203
+  * resolve_all_unknown after a lazy script       engine_batch.cpp:217-227
+on the bundled scenarios, including the 6-body serial-chain manipulator.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SCN = ["quick_smoke", "table4_obstacles_1000_5x", "table5_manipulator_100"]
+
+
+@pytest.fixture(scope="module")
+def mods():
+    import sys
+
+    sys.path.insert(0, os.path.dirname(HERE))
+    from oracle import ref
+    from paper_2603_28674_b200 import engine
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    engine.library()
+    return ref, engine
+
+
+def _world(ref, name):
+    return ref.World.from_scn(open(os.path.join(HERE, "golden", "scenarios", name + ".scn")).read())
+
+
+def _gpu(engine, w):
+    from paper_2603_28674_b200.engine import LayoutView
+
+    eng = engine.GpuEngine(LayoutView.from_any(w.layout()))
+    off, poses = w.poses()
+    eng.set_resolver(off, poses, w.body_half_extents())
+    return eng
+
+
+@pytest.mark.parametrize("name", SCN)
+def test_exact_check_matches_reference(mods, name):
+    ref, engine = mods
+    w = _world(ref, name)
+    ids, rts = w.moves()
+    n = min(len(ids), 40)
+    re = ref.Engine(w, kind=0)
+    eng = _gpu(engine, w)
+    N = w.counts()["N"]
+    allc = np.arange(N, dtype=np.int32)
+    rng = np.random.default_rng(7)
+    checked = 0
+    for i in range(n):
+        re.update(ids[i], rts[i], lazy=True)
+        eng.update_obstacle(int(ids[i]), rts[i])
+        if i % 8 == 7 or i == n - 1:
+            sample = allc if N <= 2000 else np.sort(rng.choice(allc, 2000, replace=False)).astype(np.int32)
+            exp = np.where(re.exact_free(sample) == 1, 0, 1).astype(np.uint8)
+            got = eng.exact_check(sample)
+            assert np.array_equal(got, exp), f"{name}: {np.sum(got != exp)} verdicts differ after move {i}"
+            checked += len(sample)
+            assert 0 < int(np.sum(exp == 1)) or i < 4
+    assert checked > 0
+
+
+@pytest.mark.parametrize("name", SCN)
+def test_eager_updates_match_reference(mods, name):
+    ref, engine = mods
+    w = _world(ref, name)
+    ids, rts = w.moves()
+    n = min(len(ids), 30)
+    re = ref.Engine(w, kind=0)
+    eng = _gpu(engine, w)
+    checks = 0
+    for i in range(n):
+        exp = re.update(ids[i], rts[i], lazy=False)
+        rep = eng.update_obstacle(int(ids[i]), rts[i], lazy=False)
+        got = [rep.new_green, rep.new_red, rep.new_gray, rep.unknown_after_heuristic, rep.residual_unknown,
+               rep.resolve_checks]
+        want = [int(exp[1]), int(exp[2]), int(exp[3]), int(exp[8]), int(exp[9]), int(exp[10])]
+        assert got == want, f"{name} move {i}: report {got} != {want}"
+        assert np.array_equal(eng.states(), re.states()), f"{name}: labels differ after eager move {i}"
+        checks += rep.resolve_checks
+    assert eng.unknown_count() == int(np.sum(re.states() == 2))
+    assert checks > 0, "the script never exercised the resolve"
+
+
+@pytest.mark.parametrize("name", SCN)
+def test_resolve_all_unknown_matches_reference(mods, name):
+    ref, engine = mods
+    w = _world(ref, name)
+    ids, rts = w.moves()
+    n = min(len(ids), 50)
+    re = ref.Engine(w, kind=0)
+    eng = _gpu(engine, w)
+    for i in range(n):
+        re.update(ids[i], rts[i], lazy=True)
+    eng.batch_update((ids[:n], rts[:n]))
+    assert np.array_equal(eng.states(), re.states())
+    gray = int(np.sum(re.states() == 2))
+    assert gray > 0
+    assert eng.resolve_all_unknown() == re.resolve_all_unknown() == gray
+    assert np.array_equal(eng.states(), re.states())
+    assert eng.unknown_count() == 0
+    # the engine keeps going after a resolve: more lazy moves stay in lock-step
+    for i in range(n, min(len(ids), n + 10)):
+        re.update(ids[i], rts[i], lazy=True)
+    eng.batch_update((ids[n:n + 10], rts[n:n + 10]))
+    assert np.array_equal(eng.states(), re.states())
+
+
+def test_resolver_shape_errors(mods):
+    ref, engine = mods
+    w = _world(ref, "quick_smoke")
+    from paper_2603_28674_b200.engine import LayoutView
+
+    eng = engine.GpuEngine(LayoutView.from_any(w.layout()))
+    off, poses = w.poses()
+    with pytest.raises(ValueError, match="component count"):
+        eng.set_resolver(off[:-1], poses, w.body_half_extents())
+    with pytest.raises(ValueError, match="set_resolver"):
+        eng.update_obstacle(0, np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0.0]), lazy=False)
+    with pytest.raises(ValueError, match="set_resolver"):
+        eng.resolve_all_unknown()
