@@ -57,6 +57,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--json-out", default="")
     p.add_argument("--clock-window-s", type=float, default=1.0)
+    p.add_argument("--no-resolve", action="store_true", help="skip the exact-resolve measurement")
     p.add_argument("--extra-configs", default="c5",
                    help="comma list of configs also measured on rank 0 (N=1) and reported under 'extra'")
     return p.parse_args()
@@ -242,6 +243,66 @@ def measure_extra(config, seed, device, steps=10, warmup=3):
             "unit": "edges/s", "steps": steps, "build_s": round(build_s, 1),
             "census": {k: cen[k] for k in ("over_pairs", "sat_flops", "under_pairs", "seg_sphere_tests",
                                            "bytes_components")}}
+
+
+def measure_resolve(config, seed, device, rounds=4, cpu=True):
+    """The exact resolve on the GPU: resolve_all_unknown after
+    each lazy update, and one eager update, through the host API; the reference's
+    own resolve_all_unknown / eager update_obstacle on the same roadmap and moves."""
+    import numpy as np
+
+    from paper_2603_28674_b200 import engine as E
+    from paper_2603_28674_b200 import producer
+
+    rm, obs, _ = tile_workload(config, 0, seed, rounds + 1)
+    lv = producer.layout_for(rm, obs, with_poses=True)
+    ids, rts = world_moves(config, 1, seed, rounds + 1)
+    eng = E.GpuEngine(lv, device=device)
+    t0 = time.perf_counter()
+    eng.set_resolver(*lv.resolver)
+    upload_s = time.perf_counter() - t0
+    gpu_ms, grays = [], []
+    for r in range(rounds):
+        eng.batch_update((ids[r], rts[r]))
+        grays.append(eng.unknown_count())
+        t0 = time.perf_counter()
+        n = eng.resolve_all_unknown()
+        gpu_ms.append(1e3 * (time.perf_counter() - t0))
+        assert n == grays[-1]
+    t0 = time.perf_counter()
+    reps = eng.batch_update((ids[rounds], rts[rounds]), lazy=False)
+    eager_ms = 1e3 * (time.perf_counter() - t0)
+    checks = int(sum(r.resolve_checks for r in reps))
+    out = {"what": "resolve_all_unknown after each lazy update (64 moves), then one eager update (64 moves, each "
+                   "move's gray over-hits resolved before the next); host API wall time incl. gray compaction",
+           "configs": int(lv.resolver[0][-1]), "pose_upload_s": round(upload_s, 3),
+           "resolve_all": {"gray_per_call": grays, "gpu_ms": gpu_ms,
+                           "gpu_components_per_s": sum(grays) / (1e-3 * sum(gpu_ms))},
+           "eager_update": {"moves": int(len(ids[rounds])), "resolve_checks": checks, "gpu_ms": eager_ms}}
+    if cpu:
+        from oracle import ref
+
+        w = ref.World.from_roadmap(rm.robot_he, rm.env, rm.nodes, rm.edges, rm.eps, rm.max_segments)
+        for he, ns in zip(obs.he, obs.spheres):
+            w.add_obstacle(he, int(ns))
+        re = ref.Engine(w, kind=0, threads=os.cpu_count() or 1)
+        cpu_ms = []
+        for r in range(min(rounds, 2)):  # bounded sample
+            re.run(ids[r], rts[r], lazy=True)
+            t0 = time.perf_counter()
+            re.resolve_all_unknown()
+            cpu_ms.append(1e3 * (time.perf_counter() - t0))
+        out["resolve_all"]["cpu_ref_ms"] = cpu_ms
+        out["resolve_all"]["speedup"] = statistics.mean(cpu_ms) / statistics.mean(gpu_ms[: len(cpu_ms)])
+        # lock-step check: same labels after the same lazy updates + resolves
+        for r in range(min(rounds, 2), rounds):
+            re.run(ids[r], rts[r], lazy=True)
+            re.resolve_all_unknown()
+        t0 = time.perf_counter()
+        re.run(ids[rounds], rts[rounds], lazy=False)
+        out["eager_update"]["cpu_ref_ms"] = 1e3 * (time.perf_counter() - t0)
+        out["labels_equal_reference"] = bool(np.array_equal(eng.states(), re.states()))
+    return out
 
 
 def main():
@@ -442,6 +503,11 @@ def main():
                 line["extra"][cfg] = measure_extra(cfg, args.seed, local)
             except Exception as ex:  # keep the headline line even if an extra config fails
                 line["extra"][cfg] = {"error": str(ex)[:200]}
+    if world == 1 and args.config == "c2" and not args.no_resolve:
+        try:
+            line["resolve"] = measure_resolve(args.config, args.seed, local, cpu=not args.no_cpu_baseline)
+        except Exception as ex:
+            line["resolve"] = {"error": str(ex)[:200]}
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n, done, spent, per_step, _ = cpu_reference_run(args.config, args.seed, iterations, args.cpu_sample_s,

@@ -26,6 +26,15 @@ typedef struct rgg_built rgg_built;
  * threads <= 0: hardware concurrency.  Returns 0, or -1 (see rgg_build_last_error). */
 int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
                      const int32_t* edges, double eps, int32_t max_segments, int32_t threads, rgg_built** out);
+/* Same, with flags: RGG_BUILD_POSES keeps forward_kinematics of every discretized
+ * configuration for the GPU exact resolve (rgg_gpu_set_resolver, include/rgg_gpu.h). */
+#define RGG_BUILD_POSES 1
+int rgg_build_layout_ex(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
+                        const int32_t* edges, double eps, int32_t max_segments, int32_t threads, int32_t flags,
+                        rgg_built** out);
+/* The kept poses: *n_configs = pose_off[N]; pose_off N+1; poses n_configs*12 (r[9], t[3]).
+ * Any pointer may be null. */
+int rgg_built_poses(const rgg_built* b, int64_t* n_configs, int64_t* pose_off, double* poses);
 /* out[0..3] = N, B, S, T (real segments) */
 int rgg_built_counts(const rgg_built* b, int64_t* out);
 /* Any pointer may be null.  edge_sat N*B*21, comp_aabb N*6, row_off N*B*S+1, segs T*7,

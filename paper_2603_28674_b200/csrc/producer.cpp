@@ -325,6 +325,7 @@ void cap_split(const std::vector<V3>& raw, const std::vector<int>& kept, double 
 struct Comp {
     Box over;
     std::vector<Spline> under;
+    std::vector<Tf> fk;  // forward_kinematics per configuration (kept for the exact resolve)
 };
 
 struct Robot {
@@ -361,7 +362,7 @@ Tf body_pose(const double* c) {
     return world.compose(Tf{});
 }
 
-Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K) {
+Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K, bool keep_poses) {
     // discretize_edge (robot.cpp:39-64)
     double len2 = 0.0;
     for (int i = 0; i < 6; ++i) {
@@ -418,6 +419,7 @@ Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, i
         const std::vector<int> kept = simplify(raw, rb.tol[si]);
         cap_split(raw, kept, rad, rb.tol[si], K, static_cast<int>(si), comp.under);
     }
+    if (keep_poses) comp.fk = std::move(fk);
     return comp;
 }
 
@@ -427,6 +429,8 @@ struct rgg_built {
     int32_t N = 0, B = 1, S = 1;
     std::vector<double> edge_sat, comp_aabb, segs, spline_r, obb15;
     std::vector<int32_t> row_off;
+    std::vector<int64_t> pose_off;  // RGG_BUILD_POSES: N+1
+    std::vector<double> poses;      // pose_off[N] * 12 (one body)
 };
 
 extern "C" {
@@ -435,6 +439,13 @@ const char* rgg_build_last_error(void) { return g_err.c_str(); }
 
 int rgg_build_layout(const double* he3, int32_t n_nodes, const double* nodes, int32_t n_edges, const int32_t* edges,
                      double eps, int32_t K, int32_t threads, rgg_built** out) {
+    return rgg_build_layout_ex(he3, n_nodes, nodes, n_edges, edges, eps, K, threads, 0, out);
+}
+
+int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
+                        const int32_t* edges, double eps, int32_t K, int32_t threads, int32_t flags,
+                        rgg_built** out) {
+    const bool keep_poses = (flags & RGG_BUILD_POSES) != 0;
     try {
         if (!out) throw std::invalid_argument("null output");
         if (!(eps > 0)) throw std::invalid_argument("resolution must be positive");
@@ -464,7 +475,7 @@ int rgg_build_layout(const double* he3, int32_t n_nodes, const double* nodes, in
                             a = nodes + 6 * static_cast<size_t>(edges[2 * e]);
                             b = nodes + 6 * static_cast<size_t>(edges[2 * e + 1]);
                         }
-                        comps[c] = build_comp(rb, a, b, eps, K);
+                        comps[c] = build_comp(rb, a, b, eps, K, keep_poses);
                     }
                 }
             } catch (const std::exception& ex) {
@@ -546,6 +557,19 @@ int rgg_build_layout(const double* he3, int32_t n_nodes, const double* nodes, in
                 }
             }
         }
+        if (keep_poses) {
+            L->pose_off.assign(static_cast<size_t>(N) + 1, 0);
+            for (int32_t c = 0; c < N; ++c)
+                L->pose_off[c + 1] = L->pose_off[c] + static_cast<int64_t>(comps[c].fk.size());
+            L->poses.resize(static_cast<size_t>(L->pose_off[N]) * 12);
+            for (int32_t c = 0; c < N; ++c)
+                for (size_t k = 0; k < comps[c].fk.size(); ++k) {
+                    double* d = &L->poses[(static_cast<size_t>(L->pose_off[c]) + k) * 12];
+                    const Tf& T = comps[c].fk[k];
+                    std::memcpy(d, T.r, 9 * sizeof(double));
+                    d[9] = T.t.x, d[10] = T.t.y, d[11] = T.t.z;
+                }
+        }
         *out = L;
         return 0;
     } catch (const std::exception& ex) {
@@ -575,6 +599,18 @@ int rgg_built_export(const rgg_built* b, double* edge_sat, double* comp_aabb, in
     cp(segs, b->segs);
     cp(spline_r, b->spline_r);
     cp(obb15, b->obb15);
+    return 0;
+}
+
+int rgg_built_poses(const rgg_built* b, int64_t* n_configs, int64_t* pose_off, double* poses) {
+    if (!b) return -1;
+    if (b->pose_off.empty()) {
+        g_err = "layout was built without RGG_BUILD_POSES";
+        return -1;
+    }
+    if (n_configs) *n_configs = b->pose_off.back();
+    if (pose_off) std::memcpy(pose_off, b->pose_off.data(), b->pose_off.size() * sizeof(int64_t));
+    if (poses && !b->poses.empty()) std::memcpy(poses, b->poses.data(), b->poses.size() * sizeof(double));
     return 0;
 }
 

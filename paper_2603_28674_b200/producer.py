@@ -29,6 +29,9 @@ def library():
         vp = C.c_void_p
         L.rgg_build_layout.argtypes = [vp, C.c_int32, vp, C.c_int32, vp, C.c_double, C.c_int32, C.c_int32,
                                        C.POINTER(vp)]
+        L.rgg_build_layout_ex.argtypes = [vp, C.c_int32, vp, C.c_int32, vp, C.c_double, C.c_int32, C.c_int32,
+                                          C.c_int32, C.POINTER(vp)]
+        L.rgg_built_poses.argtypes = [vp, vp, vp, vp]
         L.rgg_built_counts.argtypes = [vp, vp]
         L.rgg_built_export.argtypes = [vp] * 7
         L.rgg_built_free.argtypes = [vp]
@@ -39,15 +42,17 @@ def library():
     return _lib
 
 
-def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False):
-    """Components (nodes first, then edges) of a free-flying box robot -> store arrays."""
+def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False, with_poses=False):
+    """Components (nodes first, then edges) of a free-flying box robot -> store arrays.
+    with_poses: also a["pose_off"] (N+1) and a["poses"] (configs, 1, 12), the
+    forward kinematics of every discretized configuration (GPU exact resolve)."""
     L = library()
     he = np.ascontiguousarray(robot_he, np.float64)
     nodes = np.ascontiguousarray(nodes, np.float64)
     edges = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
     h = C.c_void_p()
-    rc = L.rgg_build_layout(he.ctypes.data, len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
-                            float(eps), int(max_segments), int(threads), C.byref(h))
+    rc = L.rgg_build_layout_ex(he.ctypes.data, len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
+                               float(eps), int(max_segments), int(threads), 1 if with_poses else 0, C.byref(h))
     if rc != 0:
         raise RuntimeError(L.rgg_build_last_error().decode())
     try:
@@ -57,6 +62,13 @@ def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, w
         a = dict(edge_sat=np.empty((N * B, 21)), comp_aabb=np.empty((N, 6)), row_off=np.empty(N * B * S + 1, np.int32),
                  segs=np.empty((T, 7)), spline_r=np.empty(B * S), obb15=np.empty((N * B, 15)) if with_obbs else None)
         L.rgg_built_export(h, *[(v.ctypes.data if v is not None else None) for v in a.values()])
+        if with_poses:
+            nc = C.c_int64()
+            if L.rgg_built_poses(h, C.byref(nc), None, None) != 0:
+                raise RuntimeError(L.rgg_build_last_error().decode())
+            a["pose_off"] = np.empty(N + 1, np.int64)
+            a["poses"] = np.empty((nc.value, 1, 12))
+            L.rgg_built_poses(h, None, a["pose_off"].ctypes.data, a["poses"].ctypes.data)
     finally:
         L.rgg_built_free(h)
     return N, B, S, a
@@ -73,9 +85,11 @@ def obstacle_spheres(he, count):
     return cen, r.value
 
 
-def layout_for(roadmap: synth.Roadmap, obstacles: synth.Obstacles, threads=0) -> LayoutView:
+def layout_for(roadmap: synth.Roadmap, obstacles: synth.Obstacles, threads=0, with_poses=False) -> LayoutView:
+    """with_poses: the view also carries .resolver = (pose_off, poses, body_half_extents)
+    for GpuEngine.set_resolver."""
     N, B, S, a = build_layout(roadmap.robot_he, roadmap.nodes, roadmap.edges, roadmap.eps, roadmap.max_segments,
-                              threads)
+                              threads, with_poses=with_poses)
     M = len(obstacles.he)
     Cmax = int(obstacles.spheres.max()) if M else 1
     sl = np.zeros((M, Cmax, 3))
@@ -84,11 +98,14 @@ def layout_for(roadmap: synth.Roadmap, obstacles: synth.Obstacles, threads=0) ->
         cen, r = obstacle_spheres(obstacles.he[o], obstacles.spheres[o])
         sl[o, : len(cen)] = cen
         sr[o] = r
-    return LayoutView(N=N, B=B, S=S, M=M, C=Cmax, edge_sat=a["edge_sat"], comp_aabb=a["comp_aabb"],
-                      row_off=a["row_off"], segs=a["segs"], spline_r=a["spline_r"],
-                      obst_he=np.ascontiguousarray(obstacles.he, np.float64), obst_sph_local=sl, obst_sph_r=sr,
-                      obst_sph_n=np.ascontiguousarray(obstacles.spheres, np.int32),
-                      meta=dict(n_nodes=len(roadmap.nodes), n_edges=len(roadmap.edges)))
+    lv = LayoutView(N=N, B=B, S=S, M=M, C=Cmax, edge_sat=a["edge_sat"], comp_aabb=a["comp_aabb"],
+                    row_off=a["row_off"], segs=a["segs"], spline_r=a["spline_r"],
+                    obst_he=np.ascontiguousarray(obstacles.he, np.float64), obst_sph_local=sl, obst_sph_r=sr,
+                    obst_sph_n=np.ascontiguousarray(obstacles.spheres, np.int32),
+                    meta=dict(n_nodes=len(roadmap.nodes), n_edges=len(roadmap.edges)))
+    if with_poses:
+        lv.resolver = (a["pose_off"], a["poses"], np.asarray(roadmap.robot_he, np.float64).reshape(1, 3))
+    return lv
 
 
 def workload(name: str, seed: int = 12345, iterations: int = 1, threads: int = 0, scale: float = 1.0):

@@ -28,3 +28,17 @@ def test_obstacle_spheres_rule():
     cen, r = producer.obstacle_spheres([5.0, 1.0, 1.0], 5)
     assert r == 1.0
     assert np.allclose(cen[:, 0], [-4, -2, 0, 2, 4]) and np.all(cen[:, 1:] == 0)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("kind,n,k,half,seed", [("se2", 200, 10, 6.0, 8), ("3d", 120, 8, 4.0, 9)])
+def test_producer_poses_match_reference_fk(kind, n, k, half, seed):
+    """The exact resolve's inputs: forward_kinematics (proj/src/robot.cpp:66-84) of
+    every configuration of discretize_edge (:39-64), bit for bit."""
+    rm = synth.make_roadmap(kind, n, k, half, seed)
+    N, B, S, a = producer.build_layout(rm.robot_he, rm.nodes, rm.edges, threads=4, with_poses=True)
+    w = ref.World.from_roadmap(rm.robot_he, rm.env, rm.nodes, rm.edges)
+    off, poses = w.poses()
+    assert np.array_equal(a["pose_off"], off)
+    assert np.array_equal(a["poses"].view(np.uint64), poses.view(np.uint64))
+    assert np.array_equal(w.body_half_extents(), np.asarray(rm.robot_he).reshape(1, 3))
