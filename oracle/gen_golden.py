@@ -119,9 +119,49 @@ def kats():
     print("kats written")
 
 
+def kat_boxes(n=1200, seed=31):
+    """Near-contact box pairs for the exact resolve (polytopes_intersect, geometry.cpp:278-303):
+    random rotations (axis-angle and yaw-only, the latter with parallel edges whose cross
+    products vanish), ~half intersecting, plus exactly touching axis-aligned pairs."""
+    rng = np.random.default_rng(seed)
+    rt_a, rt_b, he_a, he_b, out = [], [], [], [], []
+    for c in range(n):
+        ha, hb = rng.uniform(0.2, 1.5, 3), rng.uniform(0.2, 1.5, 3)
+        kind = c % 10
+        if kind == 0:  # touching faces along x: the reference counts touching as intersecting
+            a = ref.tf_euler(0.0, 0.0, 0.0)
+            b = ref.tf_euler(0.0, 0.0, 0.0)
+            a[9:] = [50.0 * c, 0.25, -0.5]
+            b[9:] = [50.0 * c + ha[0] + hb[0], 0.25 + rng.uniform(-0.1, 0.1), -0.5]
+        else:
+            if kind < 4:
+                a = ref.tf_euler(0.0, 0.0, rng.uniform(-np.pi, np.pi))
+                b = ref.tf_euler(0.0, 0.0, rng.uniform(-np.pi, np.pi))
+            else:
+                ax, bx = rng.normal(size=3), rng.normal(size=3)
+                a = ref.tf_axis_angle(ax / np.linalg.norm(ax), rng.uniform(-np.pi, np.pi))
+                b = ref.tf_axis_angle(bx / np.linalg.norm(bx), rng.uniform(-np.pi, np.pi))
+            a[9:] = [50.0 * c + rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(-1, 1)]
+            u = rng.normal(size=3)
+            u /= np.linalg.norm(u)
+            d = rng.uniform(0.35, 1.05) * (np.linalg.norm(ha) + np.linalg.norm(hb))
+            b[9:] = a[9:] + d * u
+        rt_a.append(a), rt_b.append(b), he_a.append(ha), he_b.append(hb)
+        out.append(1 if ref.box_intersect(a, ha, b, hb) else 0)
+    out = np.array(out, np.uint8)
+    np.savez_compressed(os.path.join(OUT, "kat_boxes.npz"), rt_a=np.array(rt_a), he_a=np.array(he_a),
+                        rt_b=np.array(rt_b), he_b=np.array(he_b), out=out)
+    print("kat_boxes written:", int(out.sum()), "of", n, "intersect")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `gen_golden.py kat_boxes`
+        for name in sys.argv[1:]:
+            globals()[name]()
+        return
     kats()
+    kat_boxes()
     scn("quick_smoke", with_corners=True)
     scn("table2_density_100_10x2x2")
     scn("table4_obstacles_1000_5x", snap_every=25, snap_first=10)

@@ -53,6 +53,8 @@ def lib():
         L.ro_seg_sphere_batch.argtypes = [_dp, _ip, C.c_int, _dp, C.c_double, _up]
         L.ro_obstacle_operands.argtypes = [_dp, _dp, C.c_int, C.c_double, _dp, _dp, _dp, _dp, _dp]
         L.ro_engine_new.restype = C.c_void_p
+        L.ro_box_intersect.argtypes = [_dp, _dp, _dp, _dp]
+        L.ro_exact_valid.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, _up, _dp, _dp]
         L.ro_engine_new.argtypes = [C.POINTER(_View), C.c_int]
         L.ro_engine_free.argtypes = [C.c_void_p]
         L.ro_engine_words.argtypes = [C.c_void_p]
@@ -109,6 +111,21 @@ def obstacle_operands(he, sph_local, n_sph, sph_r, rt12):
     lib().ro_obstacle_operands(np.ascontiguousarray(he, np.float64), sph_local if len(sph_local) else np.zeros(3),
                                int(n_sph), float(sph_r), np.ascontiguousarray(rt12, np.float64), sat, aabb, cen, saabb)
     return sat, aabb, cen[: 3 * n_sph].reshape(-1, 3), saabb
+
+
+def box_intersect(rt_a, he_a, rt_b, he_b) -> bool:
+    f = lambda x: np.ascontiguousarray(x, np.float64)
+    return bool(lib().ro_box_intersect(f(rt_a), f(he_a), f(rt_b), f(he_b)))
+
+
+def exact_valid(poses, body_he, active, obst_rt, obst_he) -> bool:
+    """exact_component_valid of one component: poses (configs, B, 12)."""
+    poses = np.ascontiguousarray(poses, np.float64)
+    body_he = np.ascontiguousarray(body_he, np.float64).reshape(-1)
+    return bool(lib().ro_exact_valid(poses.shape[0], poses.shape[1], poses.reshape(-1), body_he, len(active),
+                                     np.ascontiguousarray(active, np.uint8),
+                                     np.ascontiguousarray(obst_rt, np.float64).reshape(-1),
+                                     np.ascontiguousarray(obst_he, np.float64).reshape(-1)))
 
 
 class Engine:

@@ -52,6 +52,7 @@ def lib():
         L.rr_engine_run.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.POINTER(C.c_double)]
         L.rr_world_poses.argtypes = [C.c_void_p, _lp, C.c_void_p]
         L.rr_world_body_he.argtypes = [C.c_void_p, _dp]
+        L.rr_box_intersect.argtypes = [_dp, _dp, _dp, _dp, C.POINTER(C.c_int)]
         L.rr_engine_exact.argtypes = [C.c_void_p, C.c_int, _ip, _up]
         L.rr_engine_resolve_all.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
         L.rr_engine_states.argtypes = [C.c_void_p, _up]
@@ -182,6 +183,14 @@ class World:
         sat, aabb, cen, saabb = np.zeros(21), np.zeros(6), np.zeros(k["C"] * 3), np.zeros(6)
         _check(lib().rr_obstacle_operands(self.h, int(o), np.asarray(rt12, np.float64), sat, aabb, cen, saabb))
         return sat, aabb, cen.reshape(-1, 3), saabb
+
+
+def box_intersect(rt_a, he_a, rt_b, he_b) -> bool:
+    """polytopes_intersect of two boxes (geometry.cpp:228-303)."""
+    out = C.c_int(0)
+    f = lambda x: np.ascontiguousarray(x, np.float64)
+    _check(lib().rr_box_intersect(f(rt_a), f(he_a), f(rt_b), f(he_b), C.byref(out)))
+    return bool(out.value)
 
 
 class Engine:

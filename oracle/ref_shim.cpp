@@ -414,6 +414,16 @@ int rr_world_poses(void* wp, std::int64_t* off, double* poses) {
     });
 }
 
+// polytopes_intersect (geometry.cpp:278-303) of ConvexPolytope::box(he_a, a) and
+// ConvexPolytope::box(he_b, b) (:228-254): the exact resolve's pair predicate.
+int rr_box_intersect(const double* rt_a, const double* he_a, const double* rt_b, const double* he_b, int* out) {
+    return guarded([&] {
+        const ConvexPolytope pa = ConvexPolytope::box({he_a[0], he_a[1], he_a[2]}, tf_of(rt_a));
+        const ConvexPolytope pb = ConvexPolytope::box({he_b[0], he_b[1], he_b[2]}, tf_of(rt_b));
+        *out = polytopes_intersect(pa, pb) ? 1 : 0;
+    });
+}
+
 // Robot body half extents (robot.hpp BoxBody), B*3.
 int rr_world_body_he(void* wp, double* he) {
     const World* w = static_cast<const World*>(wp);

@@ -453,3 +453,136 @@ void ro_engine_census(const ro_engine* e, int64_t* out) {
         }
     }
 }
+
+/* ================================================================ exact resolve
+ * Restated literally from the reference, as the checker of the GPU's reduced
+ * (150-axis) form in paper_2603_28674_b200/csrc/rgg_resolve.cu:
+ *   ConvexPolytope::box      geometry.cpp:228-254 (+ obb_corners :50-62)
+ *   project / separates      geometry.cpp:258-273
+ *   edge_directions          geometry.cpp:275-286 (24 ring edges)
+ *   polytopes_intersect      geometry.cpp:288-303 (all face normals, 24 x 24 crosses)
+ *   aabb_of_obb              geometry.cpp:205-213, apply_transform :307-313
+ *   exact_component_valid    roadmap.cpp:129-163
+ */
+typedef struct ro_poly {
+    double v[8][3];
+    double n[6][3];  /* face normals: +a0, -a0, +a1, -a1, +a2, -a2 */
+} ro_poly;
+
+static const int k_rings[6][4] = {{1, 3, 7, 5}, {0, 4, 6, 2}, {2, 6, 7, 3}, {0, 1, 5, 4}, {4, 5, 7, 6}, {0, 2, 3, 1}};
+
+/* Transform::rotate of unit axis k (vec3.hpp:79-84) */
+static void rot_unit(const double* rt, int k, double* out) {
+    const double p[3] = {k == 0 ? 1.0 : 0.0, k == 1 ? 1.0 : 0.0, k == 2 ? 1.0 : 0.0};
+    for (int i = 0; i < 3; ++i) out[i] = rt[3 * i] * p[0] + rt[3 * i + 1] * p[1] + rt[3 * i + 2] * p[2];
+}
+
+/* obb_corners (geometry.cpp:50-62) of {centre, axes, he} */
+static void obb_corners8(const double* c, double ax[3][3], const double* he, double v[8][3]) {
+    double e[3][3];
+    for (int k = 0; k < 3; ++k)
+        for (int j = 0; j < 3; ++j) e[k][j] = ax[k][j] * he[k];
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double p = (i & 1) ? c[j] + e[0][j] : c[j] - e[0][j];
+            p = (i & 2) ? p + e[1][j] : p - e[1][j];
+            v[i][j] = (i & 4) ? p + e[2][j] : p - e[2][j];
+        }
+}
+
+static void poly_box(const double* he, const double* rt, ro_poly* p) {
+    double ax[3][3];
+    for (int k = 0; k < 3; ++k) rot_unit(rt, k, ax[k]);
+    obb_corners8(rt + 9, ax, he, p->v); /* world.center = pose.t */
+    for (int k = 0; k < 3; ++k)
+        for (int j = 0; j < 3; ++j) {
+            p->n[2 * k][j] = ax[k][j];
+            p->n[2 * k + 1][j] = -ax[k][j];
+        }
+}
+
+static double dot3v(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+static void project(const ro_poly* p, const double* axis, double* lo, double* hi) {
+    *lo = INFINITY;
+    *hi = -INFINITY;
+    for (int i = 0; i < 8; ++i) {
+        const double t = dot3v(p->v[i], axis);
+        *lo = t < *lo ? t : *lo; /* std::min(lo, t) */
+        *hi = *hi < t ? t : *hi; /* std::max(hi, t) */
+    }
+}
+
+static int separates(const ro_poly* a, const ro_poly* b, const double* axis) {
+    double alo, ahi, blo, bhi;
+    project(a, axis, &alo, &ahi);
+    project(b, axis, &blo, &bhi);
+    return ahi < blo || bhi < alo;
+}
+
+static void edge_dirs(const ro_poly* p, double d[24][3]) {
+    int k = 0;
+    for (int f = 0; f < 6; ++f)
+        for (int i = 0; i < 4; ++i, ++k)
+            for (int j = 0; j < 3; ++j) d[k][j] = p->v[k_rings[f][(i + 1) % 4]][j] - p->v[k_rings[f][i]][j];
+}
+
+static int poly_intersect(const ro_poly* a, const ro_poly* b) {
+    for (int f = 0; f < 6; ++f)
+        if (separates(a, b, a->n[f])) return 0;
+    for (int f = 0; f < 6; ++f)
+        if (separates(a, b, b->n[f])) return 0;
+    double ea[24][3], eb[24][3];
+    edge_dirs(a, ea);
+    edge_dirs(b, eb);
+    for (int i = 0; i < 24; ++i)
+        for (int j = 0; j < 24; ++j) {
+            const double ax[3] = {ea[i][1] * eb[j][2] - ea[i][2] * eb[j][1], ea[i][2] * eb[j][0] - ea[i][0] * eb[j][2],
+                                  ea[i][0] * eb[j][1] - ea[i][1] * eb[j][0]};
+            if (dot3v(ax, ax) <= 0.0) continue;
+            if (separates(a, b, ax)) return 0;
+        }
+    return 1;
+}
+
+int ro_box_intersect(const double* rt_a, const double* he_a, const double* rt_b, const double* he_b) {
+    ro_poly a, b;
+    poly_box(he_a, rt_a, &a);
+    poly_box(he_b, rt_b, &b);
+    return poly_intersect(&a, &b);
+}
+
+/* aabb_of_obb(apply_transform(pose, Obb{0, I, he})): centre = pose.apply(0) */
+static void box_aabb(const double* he, const double* rt, double* out6) {
+    double ax[3][3], c[3], v[8][3];
+    for (int k = 0; k < 3; ++k) rot_unit(rt, k, ax[k]);
+    for (int i = 0; i < 3; ++i) c[i] = rt[3 * i] * 0.0 + rt[3 * i + 1] * 0.0 + rt[3 * i + 2] * 0.0 + rt[9 + i];
+    obb_corners8(c, ax, he, v);
+    for (int j = 0; j < 3; ++j) {
+        out6[j] = INFINITY;
+        out6[3 + j] = -INFINITY;
+    }
+    for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 3; ++j) {
+            out6[j] = fmin(out6[j], v[i][j]);
+            out6[3 + j] = fmax(out6[3 + j], v[i][j]);
+        }
+}
+
+int ro_exact_valid(int n_cfg, int n_bodies, const double* poses, const double* body_he, int n_obst,
+                   const uint8_t* active, const double* obst_rt, const double* obst_he) {
+    for (int k = 0; k < n_cfg; ++k)
+        for (int b = 0; b < n_bodies; ++b) {
+            const double* pose = poses + ((size_t)k * n_bodies + b) * 12;
+            double bb[6];
+            box_aabb(body_he + 3 * b, pose, bb);
+            for (int o = 0; o < n_obst; ++o) {
+                if (!active[o]) continue;
+                double ob[6];
+                box_aabb(obst_he + 3 * o, obst_rt + 12 * (size_t)o, ob);
+                if (!aabb_overlaps(bb, ob)) continue;
+                if (ro_box_intersect(pose, body_he + 3 * b, obst_rt + 12 * (size_t)o, obst_he + 3 * o)) return 0;
+            }
+        }
+    return 1;
+}

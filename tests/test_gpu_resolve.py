@@ -131,3 +131,26 @@ def test_resolver_shape_errors(mods):
         eng.update_obstacle(0, np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0.0]), lazy=False)
     with pytest.raises(ValueError, match="set_resolver"):
         eng.resolve_all_unknown()
+
+
+def test_box_pairs_kat_through_engine(mods):
+    """The 1200 golden box pairs (tests/golden/kat_boxes.npz, reference verdicts) through
+    rgg_gpu_exact_check: component c has one configuration posed at box a_c, obstacle c
+    sits at box b_c; pairs are 50 units apart, so the AABB gate isolates each pair."""
+    from conftest import load_golden
+    from paper_2603_28674_b200.engine import LayoutView
+
+    ref, engine = mods
+    g = load_golden("kat_boxes")
+    n = len(g["out"])
+    far = np.tile([1e6, 1e6, 1e6, 1e6 + 1, 1e6 + 1, 1e6 + 1], (n, 1)).astype(np.float64)
+    lv = LayoutView(N=n, B=1, S=1, M=n, C=1, edge_sat=np.zeros((n, 21)), comp_aabb=far,
+                    row_off=np.zeros(n + 1, np.int32), segs=np.zeros((0, 7)), spline_r=np.zeros(1),
+                    obst_he=np.ascontiguousarray(g["he_b"]), obst_sph_local=np.zeros((n, 1, 3)),
+                    obst_sph_r=np.zeros(n), obst_sph_n=np.ones(n, np.int32))
+    eng = engine.GpuEngine(lv, allow_wide=True)
+    eng.set_resolver(np.arange(n + 1, dtype=np.int64), g["rt_a"].reshape(n, 1, 12), g["he_a"])
+    for lo in range(0, n, 256):
+        eng.batch_update((np.arange(lo, min(n, lo + 256), dtype=np.int32), g["rt_b"][lo:lo + 256]), per_move=False)
+    got = eng.exact_check(np.arange(n, dtype=np.int32))
+    assert np.array_equal(got, g["out"]), f"{int(np.sum(got != g['out']))} of {n} pair verdicts differ"

@@ -80,3 +80,28 @@ def test_engine_replay_matches_reference(name):
     o = int(g["mask_obstacle"])
     assert np.array_equal(eng.mask(0, allc, o), g["masks"][0])
     assert np.array_equal(eng.mask(1, allc, o), g["masks"][1])
+
+
+def test_box_intersect_kat():
+    """polytopes_intersect (geometry.cpp:228-303): 1200 near-contact box pairs dumped
+    from the reference (oracle/gen_golden.py kat_boxes), restated literally in C."""
+    g = load_golden("kat_boxes")
+    got = np.array([oracle.box_intersect(a, ha, b, hb) for a, ha, b, hb in
+                    zip(g["rt_a"], g["he_a"], g["rt_b"], g["he_b"])], np.uint8)
+    assert np.array_equal(got, g["out"])
+    assert 0.3 < g["out"].mean() < 0.7
+
+
+def test_exact_valid_gates_inactive_and_far_obstacles():
+    """exact_component_valid (roadmap.cpp:129-163): inactive obstacles never count,
+    no active obstacle -> free, one intersecting (config, body, obstacle) -> invalid."""
+    g = load_golden("kat_boxes")
+    i = int(np.argmax(g["out"]))  # an intersecting pair
+    poses = g["rt_a"][i].reshape(1, 1, 12)
+    far = g["rt_b"][i].copy()
+    far[9:] += 1000.0
+    obst_rt = np.stack([far, g["rt_b"][i]])
+    obst_he = np.stack([g["he_b"][i], g["he_b"][i]])
+    assert oracle.exact_valid(poses, g["he_a"][i], [1, 0], obst_rt, obst_he)
+    assert not oracle.exact_valid(poses, g["he_a"][i], [1, 1], obst_rt, obst_he)
+    assert oracle.exact_valid(poses, g["he_a"][i], [0, 0], obst_rt, obst_he)
