@@ -126,7 +126,8 @@ def kat_boxes(n=1200, seed=31):
     rng = np.random.default_rng(seed)
     rt_a, rt_b, he_a, he_b, out = [], [], [], [], []
     for c in range(n):
-        ha, hb = rng.uniform(0.2, 1.5, 3), rng.uniform(0.2, 1.5, 3)
+        # box a plays the robot body (one half-extent triple for all pairs), box b the obstacle
+        ha, hb = np.array([0.5, 0.3, 0.25]), rng.uniform(0.2, 1.5, 3)
         kind = c % 10
         if kind == 0:  # touching faces along x: the reference counts touching as intersecting
             a = ref.tf_euler(0.0, 0.0, 0.0)

@@ -149,7 +149,8 @@ def test_box_pairs_kat_through_engine(mods):
                     obst_he=np.ascontiguousarray(g["he_b"]), obst_sph_local=np.zeros((n, 1, 3)),
                     obst_sph_r=np.zeros(n), obst_sph_n=np.ones(n, np.int32))
     eng = engine.GpuEngine(lv, allow_wide=True)
-    eng.set_resolver(np.arange(n + 1, dtype=np.int64), g["rt_a"].reshape(n, 1, 12), g["he_a"])
+    assert np.all(g["he_a"] == g["he_a"][0])  # box a is the robot body: one half-extent triple
+    eng.set_resolver(np.arange(n + 1, dtype=np.int64), g["rt_a"].reshape(n, 1, 12), g["he_a"][:1])
     for lo in range(0, n, 256):
         eng.batch_update((np.arange(lo, min(n, lo + 256), dtype=np.int32), g["rt_b"][lo:lo + 256]), per_move=False)
     got = eng.exact_check(np.arange(n, dtype=np.int32))
