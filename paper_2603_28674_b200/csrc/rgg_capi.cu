@@ -66,6 +66,12 @@ struct rgg_gpu {
     int32_t* d_res_ids = nullptr;  // N: scratch id list (rgg_gpu_exact_check)
     int32_t* d_res_cnt = nullptr;
     uint8_t* d_res_out = nullptr;  // N
+    // eager batches: staged moves and per-move report slots (8 ints each)
+    int32_t eager_cap = 0;
+    int32_t* d_eg_ids = nullptr;
+    double* d_eg_rt = nullptr;
+    int32_t* d_eg_rep = nullptr;
+    int32_t* h_eg_rep = nullptr;
     int32_t* d_cell_count = nullptr;
     int32_t* d_cell_list = nullptr;
     int32_t* d_cell_ovf = nullptr;
@@ -735,10 +741,11 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
                    h->d_mv, h->d_pool, h->d_tl, h->d_dbg, h->d_hits_prev,
-                   h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_ids, h->d_res_cnt, h->d_res_out};
+                   h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_ids, h->d_res_cnt, h->d_res_out,
+                   h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr};
+    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr, h->h_eg_rep};
     for (void* p : pin)
         if (p) cudaFreeHost(p);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
@@ -750,6 +757,8 @@ void rgg_gpu_destroy(rgg_gpu* h) {
 
 static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
                        rgg_update_report* reports);
+static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
+                        rgg_update_report* reports);
 
 int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
                    rgg_update_report* reports) {
@@ -766,11 +775,79 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
     // (BatchEngine::batch_update(moves, false) = update_obstacle per move)
     if (!h->res_ready) return fail(h, RGG_EINVAL, "eager updates need rgg_gpu_set_resolver");
     if (!rggk::split_pipeline()) return fail(h, RGG_EINVAL, "eager updates need RGG_PIPELINE=6");
-    for (int32_t i = 0; i < n; ++i) {
-        const int rc = update_core(h, ids + i, rt12 + 12 * static_cast<size_t>(i), 1,
-                                   (flags & ~RGG_LAZY) | RGG_EAGER | RGG_PER_MOVE, reports ? reports + i : nullptr);
+    return update_eager(h, ids, rt12, n, flags, reports);
+}
+
+// Eager batch, chained on the device: per move one single-move graph (pose ..
+// apply + exact resolve of the move's gray over-hits) and one staging kernel;
+// one H2D of all moves before and one D2H of all report slots after.  A single
+// move lists at most one event per cell, so its item queues (>= Np) and pools
+// cannot overflow: no per-move host check is needed.
+static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
+                        rgg_update_report* reports) {
+    CK(cudaSetDevice(h->device));
+    int32_t k = 0;
+    while (k < n && ids[k] >= 0 && ids[k] < h->s.M) ++k;
+    if (k > 0) {
+        int rc = refresh_unknown(h);
         if (rc) return rc;
+        rc = grow_batch(h, 1);
+        if (rc) return rc;
+        rc = grow_pinned(h, k);
+        if (rc) return rc;
+        if (h->items_cap < h->s.Np) {
+            rc = grow_items(h, h->s.Np);
+            if (rc) return rc;
+        }
+        if (k > h->eager_cap) {
+            const int32_t cap = std::max(k, std::max(64, 2 * h->eager_cap));
+            cudaFree(h->d_eg_ids), cudaFree(h->d_eg_rt), cudaFree(h->d_eg_rep), cudaFreeHost(h->h_eg_rep);
+            h->d_eg_ids = nullptr, h->d_eg_rt = nullptr, h->d_eg_rep = nullptr, h->h_eg_rep = nullptr;
+            CK(dalloc(&h->d_eg_ids, cap));
+            CK(dalloc(&h->d_eg_rt, static_cast<size_t>(cap) * 12));
+            CK(dalloc(&h->d_eg_rep, static_cast<size_t>(cap) * 8));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_eg_rep), static_cast<size_t>(cap) * 8 * sizeof(int32_t), 0));
+            h->eager_cap = cap;
+        }
+        std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
+        std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 96);
+        CK(cudaMemcpyAsync(h->d_eg_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->d_eg_rt, h->h_rt, static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice, h->stream));
+        const Batch b = batch_of(h, 1);
+        const int32_t ef = RGG_EAGER | RGG_PER_MOVE | (flags & RGG_GRAY_LIST);
+        for (int32_t i = 0; i <= k; ++i) {
+            CK(rggk::launch_eager_step(b, h->d_ids, h->d_rt, h->d_eg_ids, h->d_eg_rt, h->d_eg_rep, i, k, h->stream));
+            if (i < k) {
+                rc = enqueue(h, 1, ef);
+                if (rc) return rc;
+            }
+        }
+        CK(cudaMemcpyAsync(h->h_eg_rep, h->d_eg_rep, static_cast<size_t>(k) * 8 * sizeof(int32_t),
+                           cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, "eager update: device pool overflow");
+        int32_t u = h->unknown;
+        for (int32_t i = 0; i < k; ++i) {
+            const int32_t* q = h->h_eg_rep + 8 * i;  // mv[4], hits, resolve deltas [3]
+            const int32_t after = u + q[2] - q[3];
+            u = after - q[4];
+            if (!reports) continue;
+            rgg_update_report& r = reports[i];
+            std::memset(&r, 0, sizeof(r));
+            r.obstacle = ids[i];
+            r.new_green = q[0] + q[5];
+            r.new_red = q[1] + q[6];
+            r.new_gray = q[2] + q[7];
+            r.unknown_after_heuristic = after;
+            r.residual_unknown = u;
+            r.resolve_checks = q[4];
+        }
+        if (u != h->h_ctr[16]) return fail(h, RGG_ELOGIC, "eager update: gray count out of step");
+        h->unknown = u;
+        h->unknown_stale = false;
     }
+    if (k < n) return fail(h, RGG_EINVAL, "unknown obstacle id");
     return RGG_OK;
 }
 

@@ -1874,6 +1874,25 @@ static int pipeline() {
 
 bool split_pipeline() { return pipeline() == 6; }
 
+// Eager batches run one single-move graph per move.  Between two graphs this
+// kernel saves move i-1's report terms (apply counters, resolved hits, resolve
+// deltas) to its slot and stages move i into the graph's move slot 0.
+__global__ void eager_step_kernel(Batch b, int32_t* ids0, double* rt0, const int32_t* st_ids, const double* st_rt,
+                                  int32_t* rep, int i, int k) {
+    const int t = threadIdx.x;
+    if (i > 0 && t < 8) rep[8 * (i - 1) + t] = t < 4 ? b.mv[t] : (t == 4 ? b.ctr[5] : b.ctr[20 + t - 5]);
+    if (i < k) {
+        if (t == 0) ids0[0] = st_ids[i];
+        if (t < 12) rt0[t] = st_rt[12 * static_cast<size_t>(i) + t];
+    }
+}
+
+cudaError_t launch_eager_step(const Batch& b, int32_t* ids0, double* rt0, const int32_t* st_ids, const double* st_rt,
+                              int32_t* rep, int i, int k, cudaStream_t st) {
+    eager_step_kernel<<<1, 32, 0, st>>>(b, ids0, rt0, st_ids, st_rt, rep, i, k);
+    return cudaGetLastError();
+}
+
 template <int F, bool W>
 static cudaError_t apply6_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {
     return launch_pdl(apply_warp_kernel<F, W>, dim3(grid), dim3(32 * kWarpsPerCta), st, s, b);

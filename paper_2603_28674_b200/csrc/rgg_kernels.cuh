@@ -116,6 +116,9 @@ struct Resolver {
 };
 
 bool split_pipeline();  // RGG_PIPELINE == 6 (the default): touch / narrow / apply
+// eager batches: save move i-1's report terms to rep[8(i-1)..], stage move i into slot 0
+cudaError_t launch_eager_step(const Batch& b, int32_t* ids0, double* rt0, const int32_t* st_ids, const double* st_rt,
+                              int32_t* rep, int i, int k, cudaStream_t st);
 
 enum ResolveMode : int { kResolve = 0, kEager = 1, kCheck = 2 };
 // exact check of ids[0..*count_dev) (max_count bounds the grid), after
