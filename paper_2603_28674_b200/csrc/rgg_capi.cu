@@ -39,6 +39,9 @@ struct rgg_gpu {
     double* d_cell_aabb = nullptr;
     double* d_super_aabb = nullptr;
     double* d_evbox = nullptr;
+    double* d_evt = nullptr;
+    int2* d_units = nullptr;
+    int32_t units_cap = 0;
     double* d_ohe = nullptr;
     double* d_osl = nullptr;
     double* d_osr = nullptr;
@@ -165,6 +168,8 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     cudaFree(h->d_last);
     cudaFree(h->d_ev);
     cudaFree(h->d_evbox);
+    cudaFree(h->d_evt);
+    cudaFree(h->d_units);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
     cudaFree(h->d_mpool);
@@ -175,6 +180,12 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     CK(dalloc(&h->d_last, cap));
     CK(dalloc(&h->d_ev, cap));
     CK(dalloc(&h->d_evbox, static_cast<size_t>(cap) * 12));
+    CK(dalloc(&h->d_evt, static_cast<size_t>(cap) * 24));
+    // touch work units: at most ceil(cap / 32) chunks per cell
+    const int64_t units = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * ((cap + 31) / 32));
+    if (units > INT32_MAX) return fail(h, RGG_ENOMEM, "batch too large for the touch work list; split it");
+    h->units_cap = static_cast<int32_t>(units);
+    CK(dalloc(&h->d_units, static_cast<size_t>(units)));
     CK(dalloc(&h->d_mv, static_cast<size_t>(cap) * 4));
     // every (cell, event) pair fits: the overflow pool can never run out
     h->pool_cap = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * cap);
@@ -223,6 +234,9 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.last = h->d_last;
     b.ev = h->d_ev;
     b.evbox = h->d_evbox;
+    b.evt = h->d_evt;
+    b.units = h->d_units;
+    b.units_cap = h->units_cap;
     b.cell_count = h->d_cell_count;
     b.cell_list = h->d_cell_list;
     b.cell_ovf = h->d_cell_ovf;
@@ -736,7 +750,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,

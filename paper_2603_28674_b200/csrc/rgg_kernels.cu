@@ -322,6 +322,8 @@ __global__ void pose_kernel(Store s, Batch b) {
         ev.old[lane] = ol;
         b.evbox[12 * static_cast<size_t>(i) + lane] = nu;  // compact copy for the binning
         b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol;
+        double* et = b.evt + 24 * static_cast<size_t>(i);
+        et[lane] = nu, et[6 + lane] = ol, et[12 + lane] = bn[lane], et[18 + lane] = bs[lane];
     }
     if (lane < 12) ev.rt[lane] = b.rt[12 * static_cast<size_t>(i) + lane];
     if (lane >= 16 && lane - 16 < nsph) {
@@ -484,6 +486,10 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
         int mbase = 0;
         if (count > 0) {
             b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
+            // one touch work unit per chunk of 32 listed events
+            const int W = (count + 31) >> 5;
+            const int ub = atomicAdd(&b.ctr[10], W);
+            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int2(cell, w);
             // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
             const long long need = 3ll * ((count + 31) >> 5) * s.cell;
             const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
@@ -657,6 +663,7 @@ __device__ __forceinline__ void prefetch_range(const void* a, const void* e, boo
 }
 
 constexpr int kUnderLanes = 4;  // lanes per under-approximation work item
+constexpr int kStageEv = 128;   // touch stages a whole batch of up to this many events per CTA
 constexpr int kOverLanes = 1;   // lanes per SAT work item (4 was slower: operands re-read per lane)
 
 // ------------------------------------------------------- v3: touch / narrow / apply
@@ -1069,6 +1076,8 @@ __global__ void __launch_bounds__(kMaxCell) apply_kernel(Store s, Batch b) {
 // events in move order with the reference's transition.  Warps are persistent
 // and stride over the slices, so there is no dependence on CTA scheduling.
 constexpr int kWarpsPerCta = 4;
+static_assert(kStageEv <= 32 * kWarpsPerCta, "the touch staging table is the warps' chunk buffers");
+constexpr int kStageIds = 1024;  // apply stages the moved obstacle ids of batches up to this size
 
 template <int FLAGS, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store s, Batch b) {
@@ -1363,18 +1372,58 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     pdl_trigger();
     const unsigned long long t0 = CENSUS ? 0 : tl_start(b.tl);
     if (!CENSUS) tl_stop(b.tl, 6, tw);
-    __shared__ double sbx[kWarpsPerCta][32][24];
+    // event operands: for small batches (n <= kStageEv) the whole batch is staged
+    // once per CTA and the slices index it through their cell lists; otherwise
+    // each warp stages its current chunk of 32 listed events
+    __shared__ double sbx[kWarpsPerCta * 32][24];
     __shared__ int sev[kWarpsPerCta][32];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
+    const bool staged = b.n <= kStageEv && (s.dbg_flags & 64);  // 64: stage the batch in shared memory
+    if (!staged) {  // the batch's operands into this SM's L1 (read per chunk below)
+        const char* p = reinterpret_cast<const char*>(b.evt);
+        const int lines = (b.n * 24 * 8 + 127) >> 7;
+        for (int l = threadIdx.x; l < min(lines, 256); l += blockDim.x) prefetch_l1(p + (static_cast<size_t>(l) << 7));
+    }
+    if (staged) {  // all loads in flight at once, then the stores
+        constexpr int kPer = kStageEv * 12 / (32 * kWarpsPerCta);
+        const double2* src = reinterpret_cast<const double2*>(b.evt);
+        double2* dst = reinterpret_cast<double2*>(&sbx[0][0]);
+        const int nv = b.n * 12;
+        double2 v[kPer];
+#pragma unroll
+        for (int r = 0; r < kPer; ++r) {
+            const int t = threadIdx.x + r * 32 * kWarpsPerCta;
+            if (t < nv) v[r] = src[t];
+        }
+#pragma unroll
+        for (int r = 0; r < kPer; ++r) {
+            const int t = threadIdx.x + r * 32 * kWarpsPerCta;
+            if (t < nv) dst[t] = v[r];
+        }
+        __syncthreads();
+    }
     unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
     unsigned long long* dbgw = (!CENSUS && b.dbg) ? b.dbg + 8 * static_cast<size_t>(nslices) +
                                                         4 * static_cast<size_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5)
                                                   : nullptr;
     if (dbgw && lane == 0) dbgw[0] = gtimer();
     int dbg_slices = 0;
-    for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
+    // Work units: (slice, chunk of <= 32 listed events) from the bin kernel's unit
+    // list, so a cell with many events spreads over several warps.  The census
+    // walks every slice with all its chunks.
+    const int spc = s.cell >> 5;  // slices per cell
+    const int n_units = CENSUS ? nslices : min(b.ctr[10], b.units_cap) * spc;
+    for (int u = blockIdx.x * kWarpsPerCta + wi; u < n_units; u += gridDim.x * kWarpsPerCta) {
+        int q = u, w_first = 0, w_last = 1 << 30;
+        if (!CENSUS) {
+            const int2 un = b.units[u / spc];
+            q = un.x * spc + u % spc;
+            w_first = un.y;
+            w_last = un.y + 1;
+        }
         const int c0 = q << 5;
+        if (c0 >= s.Np) continue;
         const int cell = c0 / s.cell;
         const int4 rec = b.crec[cell];
         const int count = rec.x;
@@ -1392,23 +1441,25 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
         const int32_t* list = rec_list(rec);
         const int W = (count + 31) >> 5;
         bool any_box = false, any_sph = false;
-        for (int base = 0, w = 0; base < count; base += 32, ++w) {
+        for (int w = w_first; w < min(W, w_last); ++w) {
+            const int base = 32 * w;
             const int m = min(32, count - base);
             const int myev = lane < m ? list[base + lane] : 0;
             sev[wi][lane] = myev;
-            if (lane < m) {
-                const Event& ev = b.ev[myev];
-                double v[24];
+            if (!staged && lane < m) {
+                const double2* src = reinterpret_cast<const double2*>(b.evt + 24 * static_cast<size_t>(myev));
 #pragma unroll
-                for (int j = 0; j < 6; ++j) v[j] = ev.nu[j], v[6 + j] = ev.old[j], v[12 + j] = ev.box[j], v[18 + j] = ev.sph[j];
-#pragma unroll
-                for (int j = 0; j < 24; ++j) sbx[wi][lane][j] = v[j];
+                for (int j = 0; j < 12; ++j) {
+                    const double2 v = src[j];
+                    sbx[32 * wi + lane][2 * j] = v.x;
+                    sbx[32 * wi + lane][2 * j + 1] = v.y;
+                }
             }
             __syncwarp();
             uint32_t tm = 0, bm = 0, sm = 0;
             if (valid) {
                 for (int k = 0; k < m; ++k) {
-                    const double* bx = sbx[wi][k];
+                    const double* bx = sbx[staged ? sev[wi][k] : 32 * wi + k];
                     const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
                     tm |= static_cast<uint32_t>(touch) << k;
                     bm |= static_cast<uint32_t>(touch & rggd::overlaps(aabb, bx + 12)) << k;
@@ -1504,8 +1555,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
     constexpr bool HITS = (FLAGS & kHits) != 0;
     __shared__ int2 som[kWarpsPerCta][32];
+    __shared__ int s_ids[kStageIds];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
+    const bool staged = b.n <= kStageIds;
+    if (staged) {
+        for (int t = threadIdx.x; t < b.n; t += blockDim.x) s_ids[t] = b.ids[t];
+        __syncthreads();
+    }
     int dgray = 0;
     // a full narrow-item queue left some verdicts uncomputed: apply nothing, so the
     // engine stays at its pre-update state and the host can grow the queue and replay
@@ -1543,9 +1600,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
         const int W = (count + 31) >> 5;
         for (int base = 0, w = 0; base < count; base += 32, ++w) {
             const int m = min(32, count - base);
-            if (lane < m) {
-                const Event& ev = b.ev[list[base + lane]];
-                som[wi][lane] = make_int2(ev.o, ev.move);
+            if (lane < m) {  // list entries are move indices; the event of move e moves obstacle ids[e]
+                const int e = list[base + lane];
+                som[wi][lane] = make_int2(staged ? s_ids[e] : b.ids[e], e);
             }
             uint32_t tm = 0, ro = 0, ru = 0;
             if (valid) {

@@ -72,6 +72,7 @@ struct Batch {
     uint8_t* last;         // 1 if this is the obstacle's last move in this batch (pose kernel)
     Event* ev;             // n
     double* evbox;         // n*12: new and old union box of each event (compact, for the binning)
+    double* evt;           // n*24: new union, old union, box, sphere box (the touch kernel's operands)
     int32_t* cell_count;   // ncells
     int32_t* cell_list;    // ncells*cap
     int32_t* cell_ovf;     // ncells: base in pool when count > cap
@@ -88,6 +89,8 @@ struct Batch {
     long long* mtop;             // next free word of mpool
     long long mpool_cap;
     int4* crec;                  // ncells: {count, mask base word, list address lo, hi} (bin kernel)
+    int2* units;                 // touch work units {cell, chunk of 32 listed events}; count in ctr[10]
+    int32_t units_cap;
     int4* items_over;            // {component, event, result word, bit}: pairs needing a SAT
     int4* items_under;           // same for the segment-sphere test
     int32_t items_cap;
