@@ -1611,7 +1611,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                 ru = b.mpool[rec.y + (2 * W + w) * s.cell + t];
             }
             __syncwarp();
-            for (int k = 0; k < m; ++k) {
+            // only the events that touch some component of the slice can change a
+            // label or a counter: walk those, in list (= move) order
+            for (uint32_t em = __reduce_or_sync(0xffffffffu, tm); em; em &= em - 1) {
+                const int k = __ffs(em) - 1;
                 const int before = label;
                 const int2 om = som[wi][k];
                 if ((tm >> k) & 1u) {
@@ -1650,7 +1653,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                     }
                     if (HITS && om.y == b.n - 1) hit_last = n_over;
                 }
-                if (PER_MOVE) {
+                if (PER_MOVE && __any_sync(0xffffffffu, label != before)) {
                     const bool ch = label != before;
                     const unsigned gg = __ballot_sync(0xffffffffu, ch && label == 0);
                     const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
