@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
     pdl_trigger();
     const unsigned long long t0 = tl_start(b.tl);
     tl_stop(b.tl, 5, tw);
-    __shared__ double cbox[kBinChunk][12];
+    __shared__ double cbox[12][kBinChunk];  // SoA: lane q reads column q, conflict-free
     __shared__ int cidx[kBinChunk];
     __shared__ int wsum[kBinThreads / 32];
     __shared__ int s_nc;
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
             const int pos = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
             cidx[pos] = e;
 #pragma unroll
-            for (int k = 0; k < 12; ++k) cbox[pos][k] = bx[k];
+            for (int k = 0; k < 12; ++k) cbox[k][pos] = bx[k];
         }
         __syncthreads();
         const int nc = s_nc;
@@ -444,7 +444,13 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
         // ---- per-cell test of the candidates, ordered ballot append
         for (int j = 0; j < nc; j += 32) {
             const int q = j + lane;
-            const bool hit = q < nc && (rggd::overlaps(cb, cbox[q]) | rggd::overlaps(cb, cbox[q] + 6));
+            bool hit = false;
+            if (q < nc) {
+                double qb[12];
+#pragma unroll
+                for (int k = 0; k < 12; ++k) qb[k] = cbox[k][q];
+                hit = rggd::overlaps(cb, qb) | rggd::overlaps(cb, qb + 6);
+            }
             const unsigned hb = __ballot_sync(0xffffffffu, hit);
             if (hit) {
                 const int pos = count + __popc(hb & ((1u << lane) - 1u));
