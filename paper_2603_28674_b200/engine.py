@@ -32,7 +32,7 @@ from typing import Callable, Iterable, Sequence
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "librgg_gpu.so")
+LIB_PATH = os.environ.get("RGG_GPU_LIB") or os.path.join(PKG, "lib", "librgg_gpu.so")  # RGG_GPU_LIB: A/B builds
 
 RGG_OK, RGG_EINVAL, RGG_ECUDA, RGG_ENCCL, RGG_ENOMEM, RGG_ELOGIC = 0, 1, 2, 3, 4, 5
 RGG_LAZY, RGG_PER_MOVE, RGG_ASYNC, RGG_CENSUS, RGG_GRAY_LIST, RGG_EAGER = 1, 2, 4, 8, 16, 32
