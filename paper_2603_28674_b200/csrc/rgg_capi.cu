@@ -40,7 +40,7 @@ struct rgg_gpu {
     double* d_super_aabb = nullptr;
     double* d_evbox = nullptr;
     double* d_evt = nullptr;
-    int2* d_units = nullptr;
+    int4* d_units = nullptr;
     int32_t units_cap = 0;
     double* d_ohe = nullptr;
     double* d_osl = nullptr;

@@ -492,16 +492,17 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
         int mbase = 0;
         if (count > 0) {
             b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
-            // one touch work unit per chunk of 32 listed events
-            const int W = (count + 31) >> 5;
-            const int ub = atomicAdd(&b.ctr[10], W);
-            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int2(cell, w);
             // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
             const long long need = 3ll * ((count + 31) >> 5) * s.cell;
             const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
                                              static_cast<unsigned long long>(need));
             if (base + need > b.mpool_cap) atomicExch(&b.ctr[6], 2);
             mbase = base + need > b.mpool_cap ? 0 : static_cast<int>(base);
+            // one touch work unit per chunk of 32 listed events, carrying what the
+            // touch kernel needs of the cell record
+            const int W = (count + 31) >> 5;
+            const int ub = atomicAdd(&b.ctr[10], W);
+            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int4(cell, w, count, mbase);
         }
         // one 16-byte record per cell: count, mask base, list address
         const int32_t* list = count <= s.cap ? inl : b.pool + b.cell_ovf[cell];
@@ -1422,16 +1423,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     const int n_units = CENSUS ? nslices : min(b.ctr[10], b.units_cap) * spc;
     for (int u = blockIdx.x * kWarpsPerCta + wi; u < n_units; u += gridDim.x * kWarpsPerCta) {
         int q = u, w_first = 0, w_last = 1 << 30;
+        int4 rec;
         if (!CENSUS) {
-            const int2 un = b.units[u / spc];
+            const int4 un = b.units[u / spc];  // {cell, chunk, count, mask base}
             q = un.x * spc + u % spc;
             w_first = un.y;
             w_last = un.y + 1;
+            rec = make_int4(un.z, un.w, 0, 0);
         }
         const int c0 = q << 5;
         if (c0 >= s.Np) continue;
         const int cell = c0 / s.cell;
-        const int4 rec = b.crec[cell];
+        if (CENSUS) rec = b.crec[cell];
         const int count = rec.x;
         if (count == 0) continue;  // warp-uniform: clean cell
         const int c = c0 + lane, t = c - cell * s.cell;
@@ -1444,7 +1447,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             seg_lo = s.row[c * s.B * s.S];
             seg_hi = s.row[(c + 1) * s.B * s.S];
         }
-        const int32_t* list = rec_list(rec);
+        const int32_t* list = CENSUS ? rec_list(rec)
+                                     : (count <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap
+                                                       : b.pool + b.cell_ovf[cell]);
         const int W = (count + 31) >> 5;
         bool any_box = false, any_sph = false;
         for (int w = w_first; w < min(W, w_last); ++w) {

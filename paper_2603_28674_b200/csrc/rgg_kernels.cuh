@@ -89,7 +89,7 @@ struct Batch {
     long long* mtop;             // next free word of mpool
     long long mpool_cap;
     int4* crec;                  // ncells: {count, mask base word, list address lo, hi} (bin kernel)
-    int2* units;                 // touch work units {cell, chunk of 32 listed events}; count in ctr[10]
+    int4* units;                 // touch work units {cell, chunk of 32 listed events, count, mask base}; ctr[10]
     int32_t units_cap;
     int4* items_over;            // {component, event, result word, bit}: pairs needing a SAT
     int4* items_under;           // same for the segment-sphere test
