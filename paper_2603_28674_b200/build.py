@@ -5,6 +5,8 @@
 * ``lib/librgg_gpu.so``   — the CUDA engine (csrc/rgg_kernels.cu + csrc/rgg_capi.cu),
   nvcc for sm_100a only, -lineinfo for ncu source mapping, static cudart.
 * ``lib/librgg_build.so`` — the CPU roadmap producer (csrc/producer.cpp).
+* ``lib/_rggfast*.so``    — CPython binding of the per-update call (csrc/pyfast.c), linked to
+  librgg_gpu.so; engine.GpuEngine uses it for batch_update.
 """
 from __future__ import annotations
 
@@ -56,9 +58,24 @@ def build_producer(force: bool = False) -> str:
     return out
 
 
+def build_pyfast(force: bool = False) -> str:
+    import sysconfig
+
+    os.makedirs(LIB, exist_ok=True)
+    out = os.path.join(LIB, "_rggfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+    src = os.path.join(CSRC, "pyfast.c")
+    deps = [src, os.path.join(ROOT, "include", "rgg_gpu.h"), os.path.join(LIB, "librgg_gpu.so")]
+    if force or _stale(out, deps):
+        cmd = ["gcc", "-O2", "-fPIC", "-shared", "-I", sysconfig.get_paths()["include"], "-o", out, src,
+               "-L", LIB, "-lrgg_gpu", "-Wl,-rpath,$ORIGIN"]
+        subprocess.check_call(cmd)
+    return out
+
+
 def build_all(force: bool = False) -> None:
     build_gpu(force)
     build_producer(force)
+    build_pyfast(force)
 
 
 if __name__ == "__main__":

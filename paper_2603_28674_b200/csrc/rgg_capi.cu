@@ -223,6 +223,7 @@ int grow_pinned(rgg_gpu* h, int32_t n) {
     h->h_rt = reinterpret_cast<double*>(reinterpret_cast<char*>(h->h_ids) + h->pin_off);
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), 0));
     h->cap_pin = cap;
+    ++h->gen;  // graphs with host copies hold the old staging pointers
     return RGG_OK;
 }
 
@@ -294,6 +295,14 @@ void dump_timeline(rgg_gpu* h) {
 
 // Narrow items pack the event index with a 5-bit position (rgg_kernels.cu).
 constexpr int32_t kMaxBatch = 1 << 26;
+// internal enqueue flag: host copies inside the update's graph
+constexpr int32_t kHostIO = 1 << 20;
+
+bool graphs_enabled(const rgg_gpu* h) {
+    static const bool off = std::getenv("RGG_DEBUG_PHASES") || std::getenv("RGG_NO_GRAPH") ||
+                            std::getenv("RGG_DEBUG_TIMING");
+    return !off && !h->d_dbg;
+}
 
 rggk::Resolver resolver_of(rgg_gpu* h) {
     rggk::Resolver r{};
@@ -329,7 +338,11 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // by rgg_gpu_gray_ids (labels, reports and the gray count never need it)
     const bool gray_list = (flags & RGG_GRAY_LIST) != 0;
     const bool eager = (flags & RGG_EAGER) != 0;  // n == 1: resolve the move's gray over-hits
-    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0) | (eager ? 512 : 0);
+    // kHostIO (rgg_gpu_update): the moves' H2D copy and the counters' D2H copies are
+    // nodes of the graph, so a synchronous update is one graph launch and one wait
+    const bool hostio = use_graph && (flags & kHostIO) != 0;
+    const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0) | (eager ? 512 : 0) |
+                        (hostio ? 1024 : 0) | ((flags & RGG_PER_MOVE) && hostio ? 2048 : 0);
     const auto resolve_hits = [&]() {
         return rggk::launch_resolve(h->s, resolver_of(h), b, h->d_hits, h->d_ctr + 5, kEagerResolveGrid, rggk::kEager,
                                     nullptr, h->stream);
@@ -348,7 +361,11 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
                 return cudaEventRecordWithFlags(ev, h->stream, cudaEventRecordExternal);
             };
             CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-            cudaError_t e = rec(h->ev[0]);
+            cudaError_t e = cudaSuccess;
+            if (hostio)
+                e = cudaMemcpyAsync(h->d_ids, h->h_ids, h->in_off + static_cast<size_t>(n) * 96, cudaMemcpyHostToDevice,
+                                    h->stream);
+            if (e == cudaSuccess) e = rec(h->ev[0]);
             if (e == cudaSuccess) e = rggk::launch_pose(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[1]);
             if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);
@@ -359,6 +376,11 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess && gray_list)
                 e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[4]);
+            if (e == cudaSuccess && hostio && (flags & RGG_PER_MOVE))
+                e = cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(n) * 4 * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, h->stream);
+            if (e == cudaSuccess && hostio)
+                e = cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream);
             cudaGraph_t graph = nullptr;
             const cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
             CK(e);
@@ -884,19 +906,28 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
         if (rc) return rc;
         std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
         std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 12 * sizeof(double));
-        if (h->pin_off == h->in_off) {  // same layout on both sides: one copy
+        // synchronous update with matching staging layouts: the copies are graph nodes
+        const bool hostio = !(flags & RGG_ASYNC) && !bad && h->pin_off == h->in_off && graphs_enabled(h);
+        if (hostio) {
+            rc = enqueue(h, k, flags | kHostIO);
+            if (rc) return rc;
+        } else if (h->pin_off == h->in_off) {  // same layout on both sides: one copy
             CK(cudaMemcpyAsync(h->d_ids, h->h_ids, h->in_off + static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice,
                                h->stream));
         } else {
             CK(cudaMemcpyAsync(h->d_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
             CK(cudaMemcpyAsync(h->d_rt, h->h_rt, static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice, h->stream));
         }
-        rc = enqueue(h, k, flags);
-        if (rc) return rc;
+        if (!hostio) {
+            rc = enqueue(h, k, flags);
+            if (rc) return rc;
+        }
         if (!(flags & RGG_ASYNC) || bad) {
-            if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
-                                            cudaMemcpyDeviceToHost, h->stream));
-            CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            if (!hostio) {
+                if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
+                                                cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+            }
             CK(cudaStreamSynchronize(h->stream));
             dump_timeline(h);
             for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {

@@ -121,6 +121,31 @@ def library() -> C.CDLL:
     return _lib
 
 
+_fastmod = False
+
+
+def _fast():
+    """lib/_rggfast (csrc/pyfast.c): rgg_gpu_update over the buffer protocol, ~6 us
+    cheaper per call than ctypes' numpy pointer conversions; None when not built."""
+    global _fastmod
+    if _fastmod is False:
+        library()
+        try:
+            import importlib.util
+
+            import sysconfig
+            path = os.path.join(os.path.dirname(LIB_PATH), "_rggfast" + sysconfig.get_config_var("EXT_SUFFIX"))
+            spec = importlib.util.spec_from_file_location("_rggfast", path)
+            if spec is None or not os.path.exists(path):
+                raise ImportError(path)
+            mod = importlib.util.module_from_spec(spec)
+            spec.loader.exec_module(mod)
+            _fastmod = mod
+        except ImportError:
+            _fastmod = None
+    return _fastmod
+
+
 EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_update", "rgg_gpu_update_device",
             "rgg_gpu_sync", "rgg_gpu_count", "rgg_gpu_read_states", "rgg_gpu_read_bits", "rgg_gpu_unknown_count",
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
@@ -253,6 +278,7 @@ class GpuEngine:
         self.n_components, self.n_obstacles, self.words = n.value, m.value, w.value
         self.layout = lv
         self._resolver = None
+        self._hv = h.value or 0  # the handle as an int (pyfast)
 
     # ------------------------------------------------------------- plumbing
     @staticmethod
@@ -300,7 +326,11 @@ class GpuEngine:
             return []
         reps = (_Report * n)()
         flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0)
-        rc = library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, n, flags, reps)
+        fast = _fast()
+        if fast is not None:
+            rc = fast.update(self._hv, ids, rts, flags, reps)
+        else:
+            rc = library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, n, flags, reps)
         self._check(rc)
         return Reports(reps)
 
