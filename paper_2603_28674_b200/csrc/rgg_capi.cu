@@ -104,8 +104,10 @@ struct rgg_gpu {
     int32_t* h_ids = nullptr;
     double* h_rt = nullptr;
     size_t pin_off = 0;
-    int32_t* h_mv = nullptr;
-    int32_t* h_ctr = nullptr;
+    int32_t* h_mv = nullptr;   // mapped pinned (device view dh_mv)
+    int32_t* h_ctr = nullptr;  // mapped pinned (device view dh_ctr)
+    int32_t* dh_mv = nullptr;
+    int32_t* dh_ctr = nullptr;
     // host mirrors
     std::vector<int32_t> orig;  // sorted -> id (owned)
     int32_t words = 1;
@@ -221,7 +223,8 @@ int grow_pinned(rgg_gpu* h, int32_t n) {
     h->pin_off = ((static_cast<size_t>(cap) * 4 + 15) / 16) * 16;
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), h->pin_off + static_cast<size_t>(cap) * 96, 0));
     h->h_rt = reinterpret_cast<double*>(reinterpret_cast<char*>(h->h_ids) + h->pin_off);
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_mv), h->h_mv, 0));
     h->cap_pin = cap;
     ++h->gen;  // graphs with host copies hold the old staging pointers
     return RGG_OK;
@@ -341,6 +344,13 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // kHostIO (rgg_gpu_update): the moves' H2D copy and the counters' D2H copies are
     // nodes of the graph, so a synchronous update is one graph launch and one wait
     const bool hostio = use_graph && (flags & kHostIO) != 0;
+    // the apply kernel ends the update unless the gray list or an eager resolve follows:
+    // then its last CTA stores the counters into mapped host memory itself
+    const bool out_in_kernel = hostio && !gray_list && !eager && rggk::split_pipeline();
+    if (out_in_kernel) {
+        b.out_mv = h->dh_mv;
+        b.out_ctr = h->dh_ctr;
+    }
     const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0) | (eager ? 512 : 0) |
                         (hostio ? 1024 : 0) | ((flags & RGG_PER_MOVE) && hostio ? 2048 : 0);
     const auto resolve_hits = [&]() {
@@ -376,10 +386,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess && gray_list)
                 e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[4]);
-            if (e == cudaSuccess && hostio && (flags & RGG_PER_MOVE))
+            if (e == cudaSuccess && hostio && !out_in_kernel && (flags & RGG_PER_MOVE))
                 e = cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(n) * 4 * sizeof(int32_t),
                                     cudaMemcpyDeviceToHost, h->stream);
-            if (e == cudaSuccess && hostio)
+            if (e == cudaSuccess && hostio && !out_in_kernel)
                 e = cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream);
             cudaGraph_t graph = nullptr;
             const cudaError_t e2 = cudaStreamEndCapture(h->stream, &graph);
@@ -693,7 +703,8 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_cell_list, static_cast<size_t>(ncells) * cap));
     CK(dalloc(&h->d_cell_ovf, ncells));
     CK(dalloc(&h->d_dirty, ncells));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 32 * sizeof(int32_t), 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 32 * sizeof(int32_t), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_ctr), h->h_ctr, 0));
     auto up = [&](void* dst, const void* src, size_t bytes) {
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream) : cudaSuccess;
     };

@@ -1599,7 +1599,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
         }
         const int4 rec = b.crec[cell];
         const int count = rec.x;
-        if (full == 3) return;
+        if (full == 3) break;  // warp-uniform
         if (count == 0) continue;
         oc = cw & 0xffff;
         bc = cw >> 16;
@@ -1710,6 +1710,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
     if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
     if (full != 3 && !(s.dbg_flags & 8)) commit_grid(s, b);  // 8: ablation, no commit
+    if (b.out_ctr) {
+        // the last CTA to finish hands the counters to the host (mapped pinned memory),
+        // replacing two device-to-host copies after the kernel
+        __shared__ int s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&b.ctr[11], 1) == static_cast<int>(gridDim.x) - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int t = threadIdx.x; t < 4 * b.n; t += blockDim.x) b.out_mv[t] = __ldcg(b.mv + t);
+            for (int t = threadIdx.x; t < 24; t += blockDim.x) b.out_ctr[t] = __ldcg(b.ctr + t);
+        }
+    }
     tl_stop(b.tl, 4, t0);
 }
 

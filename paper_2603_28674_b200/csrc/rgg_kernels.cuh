@@ -98,6 +98,10 @@ struct Batch {
     int32_t* unknown;      // running GRAY count, persistent across batches
     unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
     unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null
+    // host-mapped outputs (synchronous host updates): the apply kernel's last CTA
+    // stores the per-move counters (n*4) and ctr[0..23] there; null otherwise
+    int32_t* out_mv;
+    int32_t* out_ctr;
 };
 
 // Exact resolve operands (rgg_resolve.cu).
