@@ -693,6 +693,8 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_census, 16));
     CK(dalloc(&h->d_crec, ncells));
     h->items_cap = static_cast<int32_t>(std::min<int64_t>(INT32_MAX / 2, std::max<int64_t>(1 << 16, 8ll * Np)));
+    if (const char* e = std::getenv("RGG_ITEMS_CAP"))  // tests: start tiny to exercise the grow-and-replay path
+        h->items_cap = std::max(16, std::atoi(e));
     CK(dalloc(&h->d_items_over, h->items_cap));
     CK(dalloc(&h->d_items_under, h->items_cap));
     CK(dalloc(&h->d_gray, N));

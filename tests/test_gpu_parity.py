@@ -186,3 +186,20 @@ def test_interleaved_cell_shards_compose(eng_mod, name):
         reps = DistributedUpdater.reports(total, 0)
         got = np.array([[r["new_green"], r["new_red"], r["new_gray"], r["unknown_after_heuristic"]] for r in reps])
         assert np.array_equal(got, g["reports"][:, :4])
+
+
+@pytest.mark.parametrize("name", ["scn_table4_obstacles_1000_5x", "syn_se2_m80"])
+def test_item_queue_overflow_replays(eng_mod, name, monkeypatch):
+    """A narrow-item queue too small for the batch: the apply kernel changes nothing,
+    the host grows the queue and replays the update (rgg_capi.cu grow_items); labels,
+    bits and per-move reports still equal the reference's."""
+    g = load_golden(name)
+    monkeypatch.setenv("RGG_ITEMS_CAP", "64")
+    eng = eng_mod.GpuEngine(_layout(g))
+    reps = eng.batch_update((g["ids"], g["rts"]))
+    if int(g["groups"]) == 1:
+        got = np.array([[r.new_green, r.new_red, r.new_gray, r.unknown_after_heuristic] for r in reps])
+        assert np.array_equal(got, g["reports"][:, :4])
+    assert np.array_equal(eng.states(), g["snap_states"][-1])
+    bits = _bits2d(eng.obstacle_bits(), eng.words)
+    assert np.array_equal(bits, g["snap_bits"][-1].reshape(bits.shape))
