@@ -283,6 +283,49 @@ __device__ __forceinline__ int seg_filter32(const double* s, const double* c, do
     return 2;
 }
 
+// seg_filter32 with the segment-only terms hoisted: one Seg32 per (segment,
+// r_total), then one branch-free call per sphere.  Same error model (P summed in
+// another order: the 64u P^2 bound keeps a factor-2 margin over the 32u needed).
+struct Seg32 {
+    float dx, dy, dz, inv_dd, dabs, r2, r2err;
+    bool dd_pos, r_ok;
+};
+
+__device__ __forceinline__ Seg32 seg32_prep(const double* s, double r_total) {
+    constexpr float u = 5.9604645e-8f;
+    Seg32 g;
+    g.r_ok = r_total >= 0.0;
+    g.dx = __double2float_rn(s[3]);
+    g.dy = __double2float_rn(s[4]);
+    g.dz = __double2float_rn(s[5]);
+    const float dd = __double2float_rn(s[6]);
+    g.dd_pos = dd > 0.0f;
+    g.inv_dd = g.dd_pos ? __frcp_rn(dd) : 0.0f;
+    g.dabs = fabsf(g.dx) + fabsf(g.dy) + fabsf(g.dz);
+    const float r = static_cast<float>(r_total);
+    g.r2 = r * r;
+    g.r2err = 8.0f * u * g.r2;
+    return g;
+}
+
+__device__ __forceinline__ int seg_filter32_pre(const double* s, const Seg32& g, const double* c) {
+    constexpr float u = 5.9604645e-8f;
+    const float px = __double2float_rn(__dsub_rn(c[0], s[0]));
+    const float py = __double2float_rn(__dsub_rn(c[1], s[1]));
+    const float pz = __double2float_rn(__dsub_rn(c[2], s[2]));
+    float t = 0.0f;
+    if (g.dd_pos) {
+        const float num = fmaf(pz, g.dz, fmaf(py, g.dy, px * g.dx));
+        t = fminf(fmaxf(num * g.inv_dd, 0.0f), 1.0f);
+    }
+    const float qx = fmaf(-t, g.dx, px), qy = fmaf(-t, g.dy, py), qz = fmaf(-t, g.dz, pz);
+    const float x = fmaf(qz, qz, fmaf(qy, qy, qx * qx));
+    const float P = ((fabsf(px) + fabsf(py)) + fabsf(pz)) + g.dabs;
+    const float err = 64.0f * u * P * P + 1e-30f;
+    const int f = !(x == x) || !(P < 3.0e18f) ? 2 : (x + err < g.r2 - g.r2err ? 1 : (x - err > g.r2 + g.r2err ? 0 : 2));
+    return g.r_ok ? f : 0;
+}
+
 // sat_prep, proj/src/kernels_scalar.cpp:7-30.
 __device__ __forceinline__ void sat_prep(const double* c, double* s) {
 #pragma unroll

@@ -642,15 +642,28 @@ __device__ __forceinline__ bool under_range(const Store& s, int lo, int hi, cons
         const double2 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3];
         const double seg[7] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x};
         const double r_total = add(ev.r, v3.y);  // o_minus_r + spline_radius[row] (engine_batch.cpp:97)
-        for (int sp = 0; sp < ev.nsph; ++sp) {
-            if (COUNT) {
+        if (COUNT) {
+            for (int sp = 0; sp < ev.nsph; ++sp) {
                 *tests += 1;
                 hit |= rggd::seg_sphere_fast(seg, ev.cen + 3 * sp, r_total);
-            } else {
-                const int f = rggd::seg_filter32(seg, ev.cen + 3 * sp, r_total);
-                if (f == 1 || (f == 2 && seg_exact(seg, ev.cen + 3 * sp, r_total))) return true;
             }
+            continue;
         }
+        // every sphere through the filter first (independent chains), then the
+        // exact fp64 check of the undecided ones only if none hit for sure
+        const rggd::Seg32 g32 = rggd::seg32_prep(seg, r_total);
+        const int nsph = ev.nsph;
+        bool sure = false;
+        uint32_t und = 0;
+#pragma unroll 4
+        for (int sp = 0; sp < nsph; ++sp) {
+            const int f = rggd::seg_filter32_pre(seg, g32, ev.cen + 3 * sp);
+            sure |= f == 1;
+            und |= static_cast<uint32_t>(f == 2) << sp;
+        }
+        if (sure) return true;
+        for (; und; und &= und - 1)
+            if (seg_exact(seg, ev.cen + 3 * (__ffs(und) - 1), r_total)) return true;
     }
     return hit;
 }
@@ -876,7 +889,9 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
             const int inext = i + nthreads;
             const int4 nx = inext < total ? item(inext) : make_int4(0, 0, 0, 0);
             if (i < n_over) {
-                if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+                if (!(s.dbg_flags & 128) && over_test<false>(s, it.x, b.ev[it.y], nullptr))  // 128: ablation
+                    atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+            } else if (s.dbg_flags & 256) {  // 256: ablation, no under tests
             } else {
                 for (int j = it.x; j < it.y; ++j) prefetch_l1(s.seg + 8 * static_cast<size_t>(j));
                 if (under_range<false>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, nullptr))
