@@ -21,7 +21,7 @@ ROOT = os.path.dirname(PKG)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-GPU_SOURCES = ["rgg_kernels.cu", "rgg_resolve.cu", "rgg_capi.cu"]
+GPU_SOURCES = ["rgg_kernels.cu", "rgg_resolve.cu", "rgg_store.cu", "rgg_capi.cu"]
 GPU_DEPS = GPU_SOURCES + ["rgg_device.cuh", "rgg_kernels.cuh"]
 PRODUCER_SOURCES = ["producer.cpp"]
 

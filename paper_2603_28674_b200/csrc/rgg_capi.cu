@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <limits>
 #include <cstring>
+#include <chrono>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -151,16 +152,6 @@ inline void clear_stale_error() { (void)cudaGetLastError(); }
 template <class T>
 cudaError_t dalloc(T** p, size_t n) {
     return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(1, n) * sizeof(T));
-}
-
-uint64_t spread3(uint64_t x) {
-    x &= 0x1fffff;
-    x = (x | x << 32) & 0x1f00000000ffffull;
-    x = (x | x << 16) & 0x1f0000ff0000ffull;
-    x = (x | x << 8) & 0x100f00f00f00f00full;
-    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
-    x = (x | x << 2) & 0x1249249249249249ull;
-    return x;
 }
 
 int grow_batch(rgg_gpu* h, int32_t n) {
@@ -537,6 +528,16 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         if (v->row_off[r + 1] < v->row_off[r]) return fail(h, RGG_ELOGIC, "row_off must be non-decreasing");
 
     h->device = o.device;
+    static const bool dbg_create = std::getenv("RGG_DEBUG_CREATE") != nullptr;
+    auto t_create = std::chrono::steady_clock::now();
+    const auto mark = [&](const char* what) {
+        if (!dbg_create) return;
+        cudaDeviceSynchronize();
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[rgg create] %-12s %8.2f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_create).count());
+        t_create = t;
+    };
     clear_stale_error();
     CK(cudaSetDevice(h->device));
     cudaDeviceProp prop{};
@@ -545,137 +546,42 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     h->sms = prop.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     for (auto& e : h->ev) CK(cudaEventCreate(&e));
+    mark("context");
 
-    // ---- cell-sort components by the Morton code of their AABB centre
-    std::vector<int32_t> order(N);
-    std::iota(order.begin(), order.end(), 0);
-    if (N > 1) {
-        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-        std::vector<double> ctr(static_cast<size_t>(N) * 3);
-        for (int32_t c = 0; c < N; ++c) {
-            for (int k = 0; k < 3; ++k) {
-                double x = 0.5 * (v->comp_aabb[6 * c + k] + v->comp_aabb[6 * c + 3 + k]);
-                if (!(x == x)) x = 0;  // NaN guard
-                ctr[3 * c + k] = x;
-                lo[k] = std::min(lo[k], x);
-                hi[k] = std::max(hi[k], x);
-            }
-        }
-        std::vector<uint64_t> key(N);
-        for (int32_t c = 0; c < N; ++c) {
-            uint64_t code = 0;
-            for (int k = 0; k < 3; ++k) {
-                const double span = hi[k] - lo[k];
-                const double t = span > 0 ? (ctr[3 * c + k] - lo[k]) / span : 0.0;
-                const uint64_t q = static_cast<uint64_t>(std::min(std::max(t, 0.0), 1.0) * 2097151.0);
-                code |= spread3(q) << k;
-            }
-            key[c] = code;
-        }
-        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return key[a] < key[b]; });
-    }
-    // ---- shard: interleaved cells of the global order
-    std::vector<int32_t> owned;
-    owned.reserve(N / shards + cell);
+    // ---- the cell-sorted store, built on the device (rgg_store.cu): Morton order of
+    // the AABB centres, shard = interleaved cells of that order, SoA gathers
     const int64_t gcells = (static_cast<int64_t>(N) + cell - 1) / cell;
-    for (int64_t g = 0; g < gcells; ++g) {
-        if (g % shards != rank) continue;
-        for (int64_t i = g * cell; i < std::min<int64_t>(N, (g + 1) * cell); ++i) owned.push_back(order[i]);
-    }
-    const int32_t Np = static_cast<int32_t>(owned.size());
+    int64_t np64 = 0;
+    for (int64_t g = rank; g < gcells; g += shards) np64 += std::min<int64_t>(cell, N - g * cell);
+    const int32_t Np = static_cast<int32_t>(np64);
     const int32_t ncells = (Np + cell - 1) / cell;
-    h->orig = owned;
-    h->words = M <= 64 ? 1 : (M + 63) / 64;
-
-    // ---- host staging in sorted order
-    std::vector<double2> aabb(static_cast<size_t>(Np) * 3);
-    std::vector<double> sat(static_cast<size_t>(Np) * B * 22, 0.0);
-    std::vector<int32_t> row(static_cast<size_t>(Np) * B * S + 1);
-    std::vector<double> cell_aabb(static_cast<size_t>(ncells) * 6);
-    int64_t total = 0;
-    for (int32_t i = 0; i < Np; ++i) {
-        const int32_t c = owned[i];
-        const double* a = v->comp_aabb + 6 * static_cast<size_t>(c);
-        aabb[i] = make_double2(a[0], a[1]);
-        aabb[Np + i] = make_double2(a[2], a[3]);
-        aabb[2 * static_cast<size_t>(Np) + i] = make_double2(a[4], a[5]);
-        for (int b = 0; b < B; ++b)
-            std::memcpy(&sat[(static_cast<size_t>(i) * B + b) * 22], v->edge_sat + (static_cast<size_t>(c) * B + b) * 21,
-                        21 * sizeof(double));
-        for (int r = 0; r < B * S; ++r) {
-            row[static_cast<size_t>(i) * B * S + r] = static_cast<int32_t>(total);
-            const int64_t src = static_cast<int64_t>(c) * B * S + r;
-            total += v->row_off[src + 1] - v->row_off[src];
-        }
-    }
-    row[static_cast<size_t>(Np) * B * S] = static_cast<int32_t>(total);
-    if (total > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
-    h->total_segs_owned = total;
-    std::vector<double> seg(static_cast<size_t>(total) * 8, 0.0);
-    for (int32_t i = 0; i < Np; ++i) {
-        const int32_t c = owned[i];
-        for (int r = 0; r < B * S; ++r) {
-            const int64_t src = static_cast<int64_t>(c) * B * S + r;
-            int64_t dst = row[static_cast<size_t>(i) * B * S + r];
-            for (int64_t k = v->row_off[src]; k < v->row_off[src + 1]; ++k, ++dst)
-            {
-                std::memcpy(&seg[dst * 8], v->segs + 7 * k, 7 * sizeof(double));
-                seg[dst * 8 + 7] = v->spline_radius[r];  // the under items' r_total needs no row lookup
-            }
-        }
-    }
-    for (int32_t g = 0; g < ncells; ++g) {
-        double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
-        for (int32_t i = g * cell; i < std::min(Np, (g + 1) * cell); ++i) {
-            const double* a = v->comp_aabb + 6 * static_cast<size_t>(owned[i]);
-            for (int k = 0; k < 3; ++k) {
-                box[k] = std::min(box[k], a[k]);
-                box[3 + k] = std::max(box[3 + k], a[3 + k]);
-            }
-        }
-        std::memcpy(&cell_aabb[6 * static_cast<size_t>(g)], box, sizeof(box));
-    }
     const int32_t nsuper = (ncells + rggk::kSuperCells - 1) / rggk::kSuperCells;
-    std::vector<double> super_aabb(static_cast<size_t>(std::max(nsuper, 1)) * 6);
-    for (int32_t g = 0; g < nsuper; ++g) {
-        double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
-        for (int32_t c = g * rggk::kSuperCells; c < std::min(ncells, (g + 1) * rggk::kSuperCells); ++c)
-            for (int k = 0; k < 3; ++k) {
-                box[k] = std::min(box[k], cell_aabb[6 * static_cast<size_t>(c) + k]);
-                box[3 + k] = std::max(box[3 + k], cell_aabb[6 * static_cast<size_t>(c) + 3 + k]);
-            }
-        std::memcpy(&super_aabb[6 * static_cast<size_t>(g)], box, sizeof(box));
-    }
-    std::vector<int32_t> rankv(static_cast<size_t>(N), -1);
-    for (int32_t i = 0; i < Np; ++i) rankv[owned[i]] = i;
-
-    // ---- device store
-    CK(dalloc(&h->d_aabb, aabb.size()));
-    CK(dalloc(&h->d_sat, sat.size()));
-    // fp32 filter operands (rgg_device.cuh Box32): e, u rounded to nearest, L = sum |e_k|_1 rounded up
-    std::vector<rggd::Box32> sat32(static_cast<size_t>(Np) * B);
-    for (size_t i = 0; i < sat32.size(); ++i) {
-        const double* a = &sat[i * 22];
-        sat32[i] = rggd::Box32{};
-        for (int k = 0; k < 3; ++k) sat32[i].c[k] = a[k];
-        double l1 = 0.0;
-        for (int k = 0; k < 9; ++k) {
-            sat32[i].e[k] = static_cast<float>(a[3 + k]);
-            sat32[i].u[k] = static_cast<float>(a[12 + k]);
-            l1 += std::fabs(a[3 + k]);
-        }
-        const float lf = static_cast<float>(l1 * (1.0 + 1e-15));
-        sat32[i].L = std::nextafter(lf, std::numeric_limits<float>::infinity());
-    }
-    CK(dalloc(&h->d_sat32, sat32.size()));
-    CK(cudaMemcpyAsync(h->d_sat32, sat32.data(), sat32.size() * sizeof(rggd::Box32), cudaMemcpyHostToDevice, h->stream));
-    CK(dalloc(&h->d_row, row.size()));
-    CK(dalloc(&h->d_seg, seg.size()));
+    h->words = M <= 64 ? 1 : (M + 63) / 64;
+    const int64_t T = v->row_off[nrows];
+    if (T > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
+    CK(dalloc(&h->d_aabb, static_cast<size_t>(Np) * 3));
+    CK(dalloc(&h->d_sat, static_cast<size_t>(Np) * B * 22));
+    CK(dalloc(&h->d_sat32, static_cast<size_t>(Np) * B));
+    CK(dalloc(&h->d_row, static_cast<size_t>(Np) * B * S + 1));
     CK(dalloc(&h->d_spline, static_cast<size_t>(B) * S));
     CK(dalloc(&h->d_orig, Np));
     CK(dalloc(&h->d_rank, N));
-    CK(dalloc(&h->d_cell_aabb, cell_aabb.size()));
-    CK(dalloc(&h->d_super_aabb, super_aabb.size()));
+    CK(dalloc(&h->d_cell_aabb, static_cast<size_t>(std::max(ncells, 1)) * 6));
+    CK(dalloc(&h->d_super_aabb, static_cast<size_t>(std::max(nsuper, 1)) * 6));
+    {
+        rggk::StoreIn in{N, B, S, static_cast<int32_t>(T), Np, cell, shards, rank,
+                         v->comp_aabb, v->edge_sat, v->row_off, v->segs, v->spline_radius};
+        rggk::StoreOut so{};
+        so.aabb = h->d_aabb, so.sat = h->d_sat, so.sat32 = h->d_sat32, so.row = h->d_row, so.spline = h->d_spline;
+        so.orig = h->d_orig, so.rank = h->d_rank, so.cell_aabb = h->d_cell_aabb, so.super_aabb = h->d_super_aabb;
+        mark("allocs");
+        CK(rggk::build_store(in, so, h->stream));
+        mark("build_store");
+        h->d_seg = so.seg;
+        h->total_segs_owned = so.total_segs;
+        h->orig.resize(Np);
+        if (Np) CK(cudaMemcpy(h->orig.data(), h->d_orig, static_cast<size_t>(Np) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
     CK(dalloc(&h->d_ohe, static_cast<size_t>(M) * 3));
     CK(dalloc(&h->d_osl, static_cast<size_t>(M) * std::max(C, 1) * 3));
     CK(dalloc(&h->d_osr, M));
@@ -710,15 +616,6 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     auto up = [&](void* dst, const void* src, size_t bytes) {
         return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream) : cudaSuccess;
     };
-    CK(up(h->d_aabb, aabb.data(), aabb.size() * sizeof(double2)));
-    CK(up(h->d_sat, sat.data(), sat.size() * sizeof(double)));
-    CK(up(h->d_row, row.data(), row.size() * sizeof(int32_t)));
-    CK(up(h->d_seg, seg.data(), seg.size() * sizeof(double)));
-    CK(up(h->d_spline, v->spline_radius, static_cast<size_t>(B) * S * sizeof(double)));
-    CK(up(h->d_orig, owned.data(), owned.size() * sizeof(int32_t)));
-    CK(up(h->d_rank, rankv.data(), rankv.size() * sizeof(int32_t)));
-    CK(up(h->d_cell_aabb, cell_aabb.data(), cell_aabb.size() * sizeof(double)));
-    CK(up(h->d_super_aabb, super_aabb.data(), super_aabb.size() * sizeof(double)));
     CK(up(h->d_ohe, v->obst_he, static_cast<size_t>(M) * 3 * sizeof(double)));
     CK(up(h->d_osl, v->obst_sph_local, static_cast<size_t>(M) * C * 3 * sizeof(double)));
     CK(up(h->d_osr, v->obst_sph_r, static_cast<size_t>(M) * sizeof(double)));
@@ -727,7 +624,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(cudaMemsetAsync(h->d_state, shards > 1 ? 0xFF : 0, static_cast<size_t>(N) + 16, h->stream));
     if (shards > 1) {
         std::vector<uint8_t> st(static_cast<size_t>(N), 0xFF);
-        for (int32_t c : owned) st[c] = 0;
+        for (int32_t c : h->orig) st[c] = 0;
         CK(cudaMemcpyAsync(h->d_state, st.data(), st.size(), cudaMemcpyHostToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     }
@@ -771,11 +668,13 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.under = h->d_under;
     s.cur = h->d_cur;
     s.cur_union = h->d_cur_union;
+    mark("rest");
     CK(rggk::launch_init_obstacles(s, nullptr, h->stream));
     h->grid_classify = std::max(1, std::min(ncells, h->sms * rggk::classify_occupancy(cell, rggk::kPerMove)));
     const int rc = grow_batch(h, 64);
     if (rc) return rc;
     CK(cudaStreamSynchronize(h->stream));
+    mark("batch");
     h->unknown = 0;
     h->unknown_stale = false;
     return RGG_OK;

@@ -127,6 +127,31 @@ bool split_pipeline();  // RGG_PIPELINE == 6 (the default): touch / narrow / app
 cudaError_t launch_eager_step(const Batch& b, int32_t* ids0, double* rt0, const int32_t* st_ids, const double* st_rt,
                               int32_t* rep, int i, int k, cudaStream_t st);
 
+// The cell-sorted store built on the device (rgg_store.cu).  Inputs are the host
+// arrays of rgg_layout_view; outputs are preallocated except `seg`.
+struct StoreIn {
+    int32_t N, B, S, T, np, cell, shards, shard_rank;
+    const double* comp_aabb;  // host N*6
+    const double* edge_sat;   // host N*B*21
+    const int32_t* row_off;   // host N*B*S+1
+    const double* segs;       // host T*7
+    const double* spline;     // host B*S
+};
+struct StoreOut {
+    double2* aabb;         // 3*np
+    double* sat;           // np*B*22
+    rggd::Box32* sat32;    // np*B
+    int32_t* row;          // np*B*S+1
+    double* seg;           // allocated here: total_segs*8
+    double* spline;        // B*S
+    int32_t* orig;         // np
+    int32_t* rank;         // N
+    double* cell_aabb;     // ncells*6
+    double* super_aabb;    // nsuper*6
+    int32_t total_segs;
+};
+cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st);
+
 enum ResolveMode : int { kResolve = 0, kEager = 1, kCheck = 2 };
 // exact check of ids[0..*count_dev) (max_count bounds the grid), after
 // refreshing the obstacle polytopes

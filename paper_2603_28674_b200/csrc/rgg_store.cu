@@ -1,0 +1,261 @@
+// rgg_store.cu — the engine's resident store built on the GPU.
+//
+// rgg_gpu_create receives the serialized layout (BatchLayout::serialize,
+// proj/src/batch_layout.cpp:21-146, as the CSR view of include/rgg_gpu.h).  The
+// engine re-orders it into cell-sorted SoA.  Here that runs on the
+// device after one upload of the raw arrays:
+//   1. centre bounds (block min/max, order-independent), 63-bit Morton keys of
+//      the AABB centres — the same fp64 operations as the former host path;
+//   2. stable radix sort of (key, id) (CUB), shard selection of interleaved cells;
+//   3. gathers: AABB planes, SatBoxes (22-double records), Box32 filter operands,
+//      per-row segment counts -> exclusive scan -> CSR rows, segment records
+//      (+ the row's spline radius), id -> rank map, cell and super-cell boxes.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "rgg_device.cuh"
+#include "rgg_kernels.cuh"
+
+namespace rggk {
+namespace {
+
+// monotone uint64 image of a double (total order of non-NaN values)
+__device__ __forceinline__ unsigned long long ord_of(double x) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double dbl_of(unsigned long long o) {
+    const unsigned long long b = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(static_cast<long long>(b));
+#else
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+#endif
+}
+
+__device__ __forceinline__ double centre_of(const double* a, int k) {
+    double x = 0.5 * (a[k] + a[3 + k]);
+    return x == x ? x : 0.0;  // NaN guard (as the host path)
+}
+
+// bounds[0..2] = min (ordered), bounds[3..5] = max
+__global__ void centre_bounds_kernel(const double* aabb, int n, unsigned long long* bounds) {
+    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0, 0, 0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+        for (int k = 0; k < 3; ++k) {
+            const unsigned long long o = ord_of(centre_of(aabb + 6 * static_cast<size_t>(c), k));
+            lo[k] = min(lo[k], o);
+            hi[k] = max(hi[k], o);
+        }
+    for (int k = 0; k < 3; ++k)
+        for (int off = 16; off; off >>= 1) {
+            lo[k] = min(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], off));
+            hi[k] = max(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], off));
+        }
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 3; ++k) {
+            atomicMin(bounds + k, lo[k]);
+            atomicMax(bounds + 3 + k, hi[k]);
+        }
+}
+
+__device__ __forceinline__ unsigned long long spread3_d(unsigned long long x) {
+    x &= 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+__global__ void morton_kernel(const double* aabb, int n, const unsigned long long* bounds, unsigned long long* key,
+                              int32_t* val) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    unsigned long long code = 0;
+    for (int k = 0; k < 3; ++k) {
+        const double lo = dbl_of(bounds[k]), hi = dbl_of(bounds[3 + k]);
+        const double span = hi - lo;
+        const double t = span > 0 ? (centre_of(aabb + 6 * static_cast<size_t>(c), k) - lo) / span : 0.0;
+        const unsigned long long q = static_cast<unsigned long long>(fmin(fmax(t, 0.0), 1.0) * 2097151.0);
+        code |= spread3_d(q) << k;
+    }
+    key[c] = code;
+    val[c] = c;
+}
+
+// owned[i] = order[global position of the i-th component of this shard's cells]
+__global__ void select_kernel(const int32_t* order, int np, int cell, int shards, int rank, int32_t* owned,
+                              int32_t* rankmap) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    const long long g = rank + static_cast<long long>(i / cell) * shards;
+    const int c = order[g * cell + i % cell];
+    owned[i] = c;
+    rankmap[c] = i;
+}
+
+__global__ void gather_kernel(const int32_t* owned, int np, int B, int BS, const double* aabb, const double* sat21,
+                              const int32_t* row_off, double2* aabb_out, double* sat_out, rggd::Box32* sat32,
+                              int32_t* row_len) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= np) return;
+    const int c = owned[i];
+    const double* a = aabb + 6 * static_cast<size_t>(c);
+    aabb_out[i] = make_double2(a[0], a[1]);
+    aabb_out[np + i] = make_double2(a[2], a[3]);
+    aabb_out[2 * static_cast<size_t>(np) + i] = make_double2(a[4], a[5]);
+    for (int b = 0; b < B; ++b) {
+        const double* s = sat21 + (static_cast<size_t>(c) * B + b) * 21;
+        double* d = sat_out + (static_cast<size_t>(i) * B + b) * 22;
+        rggd::Box32 x{};
+        double l1 = 0.0;
+        for (int k = 0; k < 21; ++k) d[k] = s[k];
+        d[21] = 0.0;
+        for (int k = 0; k < 3; ++k) x.c[k] = s[k];
+        for (int k = 0; k < 9; ++k) {
+            x.e[k] = __double2float_rn(s[3 + k]);
+            x.u[k] = __double2float_rn(s[12 + k]);
+            l1 += fabs(s[3 + k]);
+        }
+        x.L = nextafterf(__double2float_rn(l1 * (1.0 + 1e-15)), __int_as_float(0x7f800000));
+        sat32[static_cast<size_t>(i) * B + b] = x;
+    }
+    for (int r = 0; r < BS; ++r) {
+        const size_t src = static_cast<size_t>(c) * BS + r;
+        row_len[static_cast<size_t>(i) * BS + r] = row_off[src + 1] - row_off[src];
+    }
+}
+
+// one thread per row of the sorted order: its real segments + the slot's spline radius
+__global__ void segs_kernel(const int32_t* owned, long long nrows, int BS, const int32_t* row_off_src,
+                            const int32_t* row_new, const double* segs7, const double* spline, double* seg8) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const int i = static_cast<int>(t / BS), r = static_cast<int>(t % BS);
+    const size_t src = static_cast<size_t>(owned[i]) * BS + r;
+    const int k0 = row_off_src[src], k1 = row_off_src[src + 1];
+    double* d = seg8 + 8 * static_cast<size_t>(row_new[t]);
+    for (int k = k0; k < k1; ++k, d += 8) {
+        const double* s = segs7 + 7 * static_cast<size_t>(k);
+        for (int j = 0; j < 7; ++j) d[j] = s[j];
+        d[7] = spline[r];
+    }
+}
+
+__global__ void cell_box_kernel(const double2* aabb, int np, int cell, int ncells, double* cell_aabb) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= ncells) return;
+    double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+    for (int i = g * cell; i < min(np, (g + 1) * cell); ++i) {
+        const double2 a0 = aabb[i], a1 = aabb[np + i], a2 = aabb[2 * static_cast<size_t>(np) + i];
+        const double a[6] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y};
+        for (int k = 0; k < 3; ++k) {
+            box[k] = fmin(box[k], a[k]);
+            box[3 + k] = fmax(box[3 + k], a[3 + k]);
+        }
+    }
+    for (int k = 0; k < 6; ++k) cell_aabb[6 * static_cast<size_t>(g) + k] = box[k];
+}
+
+__global__ void super_box_kernel(const double* cell_aabb, int ncells, int nsuper, double* super_aabb) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nsuper) return;
+    double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+    for (int c = g * kSuperCells; c < min(ncells, (g + 1) * kSuperCells); ++c)
+        for (int k = 0; k < 3; ++k) {
+            box[k] = fmin(box[k], cell_aabb[6 * static_cast<size_t>(c) + k]);
+            box[3 + k] = fmax(box[3 + k], cell_aabb[6 * static_cast<size_t>(c) + 3 + k]);
+        }
+    for (int k = 0; k < 6; ++k) super_aabb[6 * static_cast<size_t>(g) + k] = box[k];
+}
+
+template <class T>
+cudaError_t alloc(T** p, size_t n) {
+    return cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T));
+}
+
+#define SCK(x)                                   \
+    do {                                         \
+        const cudaError_t e_ = (x);              \
+        if (e_ != cudaSuccess) return e_;        \
+    } while (0)
+
+}  // namespace
+
+cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
+    const int N = in.N, B = in.B, BS = in.B * in.S, np = in.np, cell = in.cell;
+    const long long nrows = static_cast<long long>(np) * BS;
+    const int ncells = (np + cell - 1) / cell, nsuper = (ncells + kSuperCells - 1) / kSuperCells;
+    // 1. raw inputs
+    double *aabb = nullptr, *sat21 = nullptr, *segs7 = nullptr;
+    int32_t* row_off = nullptr;
+    SCK(alloc(&aabb, static_cast<size_t>(N) * 6));
+    SCK(alloc(&sat21, static_cast<size_t>(N) * B * 21));
+    SCK(alloc(&row_off, static_cast<size_t>(N) * BS + 1));
+    SCK(alloc(&segs7, static_cast<size_t>(in.T) * 7));
+    // pageable sources: plain synchronous copies (the driver pipelines them through
+    // its staging buffers; async pageable copies on a non-blocking stream were slower)
+    SCK(cudaStreamSynchronize(st));
+    SCK(cudaMemcpy(aabb, in.comp_aabb, static_cast<size_t>(N) * 6 * 8, cudaMemcpyHostToDevice));
+    SCK(cudaMemcpy(sat21, in.edge_sat, static_cast<size_t>(N) * B * 21 * 8, cudaMemcpyHostToDevice));
+    SCK(cudaMemcpy(row_off, in.row_off, (static_cast<size_t>(N) * BS + 1) * 4, cudaMemcpyHostToDevice));
+    if (in.T) SCK(cudaMemcpy(segs7, in.segs, static_cast<size_t>(in.T) * 7 * 8, cudaMemcpyHostToDevice));
+    SCK(cudaMemcpy(out.spline, in.spline, static_cast<size_t>(BS) * 8, cudaMemcpyHostToDevice));
+    // 2. Morton order
+    unsigned long long *bounds = nullptr, *key = nullptr, *key2 = nullptr;
+    int32_t *val = nullptr, *order = nullptr;
+    SCK(alloc(&bounds, 6));
+    SCK(alloc(&key, N));
+    SCK(alloc(&key2, N));
+    SCK(alloc(&val, N));
+    SCK(alloc(&order, N));
+    const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
+    SCK(cudaMemcpyAsync(bounds, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    const int T256 = 256;
+    if (N > 0) {
+        centre_bounds_kernel<<<std::min(1184, (N + T256 - 1) / T256), T256, 0, st>>>(aabb, N, bounds);
+        morton_kernel<<<(N + T256 - 1) / T256, T256, 0, st>>>(aabb, N, bounds, key, val);
+    }
+    size_t tmp_bytes = 0, scan_bytes = 0;
+    SCK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, val, order, N, 0, 63, st));
+    int32_t *row_len = nullptr;
+    SCK(alloc(&row_len, static_cast<size_t>(nrows) + 1));
+    SCK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, row_len, out.row, nrows + 1, st));
+    void* tmp = nullptr;
+    SCK(cudaMalloc(&tmp, std::max<size_t>(1, std::max(tmp_bytes, scan_bytes))));
+    if (N > 0) SCK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, val, order, N, 0, 63, st));
+    // 3. shard selection, id -> rank, gathers
+    SCK(cudaMemsetAsync(out.rank, 0xFF, static_cast<size_t>(N) * 4, st));
+    if (np > 0) {
+        select_kernel<<<(np + T256 - 1) / T256, T256, 0, st>>>(order, np, cell, in.shards, in.shard_rank, out.orig,
+                                                              out.rank);
+        gather_kernel<<<(np + 127) / 128, 128, 0, st>>>(out.orig, np, B, BS, aabb, sat21, row_off, out.aabb, out.sat,
+                                                       out.sat32, row_len);
+    }
+    SCK(cudaMemsetAsync(row_len + nrows, 0, 4, st));
+    SCK(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, row_len, out.row, nrows + 1, st));
+    SCK(cudaMemcpyAsync(&out.total_segs, out.row + nrows, 4, cudaMemcpyDeviceToHost, st));
+    SCK(cudaStreamSynchronize(st));
+    SCK(alloc(&out.seg, static_cast<size_t>(out.total_segs) * 8));
+    if (nrows > 0)
+        segs_kernel<<<static_cast<unsigned>((nrows + T256 - 1) / T256), T256, 0, st>>>(
+            out.orig, nrows, BS, row_off, out.row, segs7, out.spline, out.seg);
+    if (ncells > 0) {
+        cell_box_kernel<<<(ncells + 127) / 128, 128, 0, st>>>(out.aabb, np, cell, ncells, out.cell_aabb);
+        super_box_kernel<<<(nsuper + 127) / 128, 128, 0, st>>>(out.cell_aabb, ncells, nsuper, out.super_aabb);
+    }
+    SCK(cudaGetLastError());
+    SCK(cudaStreamSynchronize(st));
+    for (void* p : {static_cast<void*>(aabb), static_cast<void*>(sat21), static_cast<void*>(row_off),
+                    static_cast<void*>(segs7), static_cast<void*>(bounds), static_cast<void*>(key),
+                    static_cast<void*>(key2), static_cast<void*>(val), static_cast<void*>(order),
+                    static_cast<void*>(row_len), tmp})
+        cudaFree(p);
+    return cudaSuccess;
+}
+
+}  // namespace rggk
