@@ -9,6 +9,10 @@
 // same contract for its AVX2 backend).
 #pragma once
 
+#include <cmath>
+#include <cstdint>
+#include <limits>
+
 #include <cstdint>
 
 namespace rggd {
@@ -183,8 +187,11 @@ struct __align__(16) Box32 {
     double c[3];
     float e[9];
     float u[9];
-    float L;
-    float pad[7];
+    float L;       // sum_k |e_k|_1 rounded up (sat_filter32)
+    float h[3];    // |e_k|_2 rounded to nearest: the half extents (sat_filter32g)
+    float Lh;      // h_0 + h_1 + h_2 rounded up
+    uint32_t degen;  // some unit axis is zero (zero-extent box): the filters defer to fp64
+    float pad[2];
 };
 static_assert(sizeof(Box32) == 128, "Box32 is one cache line");
 
@@ -249,6 +256,111 @@ __device__ __forceinline__ int sat_filter32(const double* ca, const Box32& a, co
     }
     if (sep) return 0;           // a tested axis separates for sure
     return undecided ? 2 : 1;    // every tested axis overlaps for sure -> intersect
+}
+
+// The Box32 terms of one SatBox (fp64 e[9], u[9] at sat + 3, sat + 12).
+__host__ __device__ inline void box32_terms(const double* sat, Box32& x) {
+    double l1 = 0.0;
+    bool degen = false;
+    for (int k = 0; k < 3; ++k) {
+        double n2 = 0.0, u2 = 0.0;
+        for (int j = 0; j < 3; ++j) {
+            const double e = sat[3 + 3 * k + j], uu = sat[12 + 3 * k + j];
+            x.e[3 * k + j] = static_cast<float>(e);
+            x.u[3 * k + j] = static_cast<float>(uu);
+            l1 += e < 0 ? -e : e;
+            n2 += e * e;
+            u2 += uu * uu;
+        }
+        x.h[k] = static_cast<float>(sqrt(n2));
+        degen |= !(u2 > 0.5);
+    }
+    x.degen = degen ? 1u : 0u;
+    // rounded up: nextafter of the nearest float of a value inflated by 1e-15
+    const float lf = static_cast<float>(l1 * (1.0 + 1e-15));
+    const float hf = static_cast<float>((static_cast<double>(x.h[0]) + x.h[1] + x.h[2]) * (1.0 + 1e-15));
+#ifdef __CUDA_ARCH__
+    x.L = nextafterf(lf, __int_as_float(0x7f800000));
+    x.Lh = nextafterf(hf, __int_as_float(0x7f800000));
+#else
+    x.L = std::nextafter(lf, std::numeric_limits<float>::infinity());
+    x.Lh = std::nextafter(hf, std::numeric_limits<float>::infinity());
+#endif
+}
+
+// sat_boxes filter in the frame of box a (the classic OBB form): with
+// R_ij = a.u_i . b.u_j, t = d in a's frame, t' = d in b's frame and half
+// extents h = |e_k|, the reference's 15 margins (kernels_scalar.cpp:37-69) are
+//   a.u_i:        |t_i|  - (ha_i + sum_j hb_j |R_ij|)
+//   b.u_j:        |t'_j| - (sum_i ha_i |R_ij| + hb_j)
+//   a.u_i x b.u_j: |t_i2 R_i1j - t_i1 R_i2j| - (ha_i1 |R_i2j| + ha_i2 |R_i1j| + hb_j1 |R_ij2| + hb_j2 |R_ij1|)
+// up to the frames' orthogonality (~1e-14 of S for the reference's boxes),
+// for either handedness.  fp32 error (inputs rounded once, dot products by
+// FMA): faces <= 10 u S, crosses <= 26 u S with S = |d|_1 + Lh_a + Lh_b; the
+// tolerances are 16 u S and 32 u S.  The cross axis is skipped by the
+// reference when |u_i x v_j|^2 < 1e-12: |R_ij| <= 1 - 2^-10 is tested for
+// sure; nearer-parallel pairs classify n2 from the explicit cross product as
+// sat_filter32 does (exact zeros stay exact).  Same return as sat_filter32.
+__device__ __forceinline__ int sat_filter32g(const Box32& a, const double* cb, const Box32& b) {
+    constexpr float u = 5.9604645e-8f;  // 2^-24
+    if (a.degen | b.degen) return 2;
+    float d[3];
+    d[0] = __double2float_rn(__dsub_rn(cb[0], a.c[0]));
+    d[1] = __double2float_rn(__dsub_rn(cb[1], a.c[1]));
+    d[2] = __double2float_rn(__dsub_rn(cb[2], a.c[2]));
+    const float S = (fabsf(d[0]) + fabsf(d[1]) + fabsf(d[2]) + a.Lh + b.Lh) * (1.0f + 16.0f * u);
+    if (!(S < 3.0e37f)) return 2;
+    float R[3][3], AR[3][3], t[3], tb[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        t[i] = dot3f(d, a.u + 3 * i);
+        tb[i] = dot3f(d, b.u + 3 * i);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            R[i][j] = dot3f(a.u + 3 * i, b.u + 3 * j);
+            AR[i][j] = fabsf(R[i][j]);
+        }
+    }
+    const float tol_f = 16.0f * u * S, tol_c = 32.0f * u * S;
+    bool sep = false, undecided = false;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float ma = fabsf(t[i]) - (a.h[i] + fmaf(b.h[2], AR[i][2], fmaf(b.h[1], AR[i][1], b.h[0] * AR[i][0])));
+        const float mb = fabsf(tb[i]) - (fmaf(a.h[2], AR[2][i], fmaf(a.h[1], AR[1][i], a.h[0] * AR[0][i])) + b.h[i]);
+        sep |= (ma > tol_f) | (mb > tol_f);
+        undecided |= (fabsf(ma) <= tol_f) | (fabsf(mb) <= tol_f);
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int i1 = i == 2 ? 0 : i + 1, i2 = i == 0 ? 2 : i - 1;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const int j1 = j == 2 ? 0 : j + 1, j2 = j == 0 ? 2 : j - 1;
+            const float m = fabsf(fmaf(t[i2], R[i1][j], -t[i1] * R[i2][j])) -
+                            (fmaf(a.h[i1], AR[i2][j], a.h[i2] * AR[i1][j]) + fmaf(b.h[j1], AR[i][j2], b.h[j2] * AR[i][j1]));
+            bool tested = true, maybe = false;
+            if (AR[i][j] > 1.0f - 9.765625e-4f) {  // near-parallel edges: n2 from the explicit cross product
+                const float* x = a.u + 3 * i;
+                const float* y = b.u + 3 * j;
+                float ax[3], er[3];
+                ax[0] = fmaf(x[1], y[2], -x[2] * y[1]);
+                ax[1] = fmaf(x[2], y[0], -x[0] * y[2]);
+                ax[2] = fmaf(x[0], y[1], -x[1] * y[0]);
+                er[0] = 8.0f * u * (fabsf(x[1] * y[2]) + fabsf(x[2] * y[1]));
+                er[1] = 8.0f * u * (fabsf(x[2] * y[0]) + fabsf(x[0] * y[2]));
+                er[2] = 8.0f * u * (fabsf(x[0] * y[1]) + fabsf(x[1] * y[0]));
+                const float n2 = dot3f(ax, ax);
+                const float n2err = (2.0f * fabsf(ax[0]) + 2.0f * er[0]) * er[0] + (2.0f * fabsf(ax[1]) + 2.0f * er[1]) * er[1] +
+                                    (2.0f * fabsf(ax[2]) + 2.0f * er[2]) * er[2] + 8.0f * u * n2 + 1e-18f;
+                tested = n2 - n2err >= 1e-12f * (1.0f + 1e-6f);
+                maybe = !tested && n2 + n2err >= 1e-12f * (1.0f - 1e-6f);
+            }
+            sep |= tested & (m > tol_c);
+            undecided |= (tested & (fabsf(m) <= tol_c)) | (maybe & (m > -tol_c));
+        }
+    }
+    if (sep) return 0;
+    return undecided ? 2 : 1;
 }
 
 // seg_sphere filter.  p and d come from the fp64 operands; t uses a fast

@@ -258,21 +258,10 @@ __global__ void pose_kernel(Store s, Batch b) {
         for (int k = 0; k < 3; ++k) {
             ev.sat[3 + 3 * lane + k] = e[k];
             ev.sat[12 + 3 * lane + k] = u[k];
-            ev.b32.e[3 * lane + k] = __double2float_rn(e[k]);
-            ev.b32.u[3 * lane + k] = __double2float_rn(u[k]);
         }
     }
-    {
-        // L = sum_k |e_k|_1, rounded up (the filter's scale)
-        double l1 = 0.0;
-        if (lane < 3) l1 = fabs(e[0]) + fabs(e[1]) + fabs(e[2]);
-        l1 += __shfl_down_sync(0xffffffffu, l1, 1);
-        l1 += __shfl_down_sync(0xffffffffu, l1, 2);  // lanes 0..2 summed on lane 0 (lane 3 adds 0)
-        if (lane == 0) {
-            ev.b32.L = __double2float_ru(l1 * (1.0 + 1e-15));
-            
-        }
-    }
+    __syncwarp();
+    if (lane == 0) rggd::box32_terms(ev.sat, ev.b32);  // the filter operands of the obstacle box
     // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
     double bn[6], bo[6], bs[6];
 #pragma unroll
@@ -351,14 +340,8 @@ __global__ void init_obstacles_kernel(Store s) {
     Event& e = s.cur[o];
     int nsph = 0;
     obstacle_at<true>(s, o, id, e.sat, e.box, e.sph, e.cen, &nsph);
-    double l1 = 0.0;
-    for (int k = 0; k < 9; ++k) {
-        e.b32.e[k] = __double2float_rn(e.sat[3 + k]);
-        e.b32.u[k] = __double2float_rn(e.sat[12 + k]);
-        l1 += fabs(e.sat[3 + k]);
-    }
-    e.b32.L = __double2float_ru(l1 * (1.0 + 1e-15));
-    
+    rggd::box32_terms(e.sat, e.b32);
+
     e.r = s.osr[o];
     e.o = o;
     e.nsph = nsph;
@@ -539,7 +522,8 @@ __device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev
         for (int b = 0; b < s.B && !hit; ++b) {
             const size_t i = static_cast<size_t>(c) * s.B + b;
             const rggd::Box32& a32 = s.sat32[i];
-            const int f = rggd::sat_filter32(a32.c, a32, osat, ev.b32);
+            const int f = (s.dbg_flags & 512) ? rggd::sat_filter32(a32.c, a32, osat, ev.b32)  // 512: the axis-form filter
+                                              : rggd::sat_filter32g(a32, osat, ev.b32);
             hit = f == 2 ? sat_exact(s.sat + i * 22, osat) : f == 1;
         }
         return hit;

@@ -112,16 +112,10 @@ __global__ void gather_kernel(const int32_t* owned, int np, int B, int BS, const
         const double* s = sat21 + (static_cast<size_t>(c) * B + b) * 21;
         double* d = sat_out + (static_cast<size_t>(i) * B + b) * 22;
         rggd::Box32 x{};
-        double l1 = 0.0;
         for (int k = 0; k < 21; ++k) d[k] = s[k];
         d[21] = 0.0;
         for (int k = 0; k < 3; ++k) x.c[k] = s[k];
-        for (int k = 0; k < 9; ++k) {
-            x.e[k] = __double2float_rn(s[3 + k]);
-            x.u[k] = __double2float_rn(s[12 + k]);
-            l1 += fabs(s[3 + k]);
-        }
-        x.L = nextafterf(__double2float_rn(l1 * (1.0 + 1e-15)), __int_as_float(0x7f800000));
+        rggd::box32_terms(s, x);
         sat32[static_cast<size_t>(i) * B + b] = x;
     }
     for (int r = 0; r < BS; ++r) {
