@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <limits>
 
@@ -183,17 +184,37 @@ __device__ __forceinline__ bool seg_sphere_fast(const double* s, const double* c
 // formed in fp64), e[9], u[9] rounded to nearest, L = sum of |e_k|_1 rounded up.
 // The filter reads only this line; the 176-byte fp64 SatBox is read only for the
 // rare undecided pair.
+// The first 80 bytes are what sat_filter32g reads (five 16-byte loads, Box32G).
 struct __align__(16) Box32 {
     double c[3];
-    float e[9];
     float u[9];
-    float L;       // sum_k |e_k|_1 rounded up (sat_filter32)
-    float h[3];    // |e_k|_2 rounded to nearest: the half extents (sat_filter32g)
-    float Lh;      // h_0 + h_1 + h_2 rounded up
+    float h[3];      // |e_k|_2 rounded to nearest: the half extents (sat_filter32g)
+    float Lh;        // h_0 + h_1 + h_2 rounded up
     uint32_t degen;  // some unit axis is zero (zero-extent box): the filters defer to fp64
+    float L;         // sum_k |e_k|_1 rounded up (sat_filter32)
+    float e[9];
     float pad[2];
 };
 static_assert(sizeof(Box32) == 128, "Box32 is one cache line");
+
+struct __align__(16) Box32G {
+    double c[3];
+    float u[9];
+    float h[3];
+    float Lh;
+    uint32_t degen;
+};
+static_assert(sizeof(Box32G) == 80 && offsetof(Box32, L) == 80, "Box32G is the head of Box32");
+
+// the head of a Box32 in five vector loads
+__device__ __forceinline__ Box32G load_box32g(const Box32* p) {
+    Box32G x;
+    const float4* q = reinterpret_cast<const float4*>(p);
+    float4* d = reinterpret_cast<float4*>(&x);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d[k] = q[k];
+    return x;
+}
 
 __device__ __forceinline__ float dot3f(const float* x, const float* y) {
     return fmaf(x[2], y[2], fmaf(x[1], y[1], x[0] * y[0]));
@@ -301,7 +322,7 @@ __host__ __device__ inline void box32_terms(const double* sat, Box32& x) {
 // reference when |u_i x v_j|^2 < 1e-12: |R_ij| <= 1 - 2^-10 is tested for
 // sure; nearer-parallel pairs classify n2 from the explicit cross product as
 // sat_filter32 does (exact zeros stay exact).  Same return as sat_filter32.
-__device__ __forceinline__ int sat_filter32g(const Box32& a, const double* cb, const Box32& b) {
+__device__ __forceinline__ int sat_filter32g(const Box32G& a, const double* cb, const Box32G& b) {
     constexpr float u = 5.9604645e-8f;  // 2^-24
     if (a.degen | b.degen) return 2;
     float d[3];

@@ -261,7 +261,10 @@ __global__ void pose_kernel(Store s, Batch b) {
         }
     }
     __syncwarp();
-    if (lane == 0) rggd::box32_terms(ev.sat, ev.b32);  // the filter operands of the obstacle box
+    if (lane == 0) {  // the filter operands of the obstacle box
+        rggd::box32_terms(ev.sat, ev.b32);
+        for (int k = 0; k < 3; ++k) ev.b32.c[k] = ev.sat[k];
+    }
     // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
     double bn[6], bo[6], bs[6];
 #pragma unroll
@@ -341,6 +344,7 @@ __global__ void init_obstacles_kernel(Store s) {
     int nsph = 0;
     obstacle_at<true>(s, o, id, e.sat, e.box, e.sph, e.cen, &nsph);
     rggd::box32_terms(e.sat, e.b32);
+    for (int k = 0; k < 3; ++k) e.b32.c[k] = e.sat[k];
 
     e.r = s.osr[o];
     e.o = o;
@@ -521,9 +525,14 @@ __device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev
         bool hit = false;
         for (int b = 0; b < s.B && !hit; ++b) {
             const size_t i = static_cast<size_t>(c) * s.B + b;
-            const rggd::Box32& a32 = s.sat32[i];
-            const int f = (s.dbg_flags & 512) ? rggd::sat_filter32(a32.c, a32, osat, ev.b32)  // 512: the axis-form filter
-                                              : rggd::sat_filter32g(a32, osat, ev.b32);
+            int f;
+            if (s.dbg_flags & 512) {  // 512: the axis-form filter
+                const rggd::Box32& a32 = s.sat32[i];
+                f = rggd::sat_filter32(a32.c, a32, osat, ev.b32);
+            } else {
+                const rggd::Box32G a32 = rggd::load_box32g(s.sat32 + i), o32 = rggd::load_box32g(&ev.b32);
+                f = rggd::sat_filter32g(a32, o32.c, o32);
+            }
             hit = f == 2 ? sat_exact(s.sat + i * 22, osat) : f == 1;
         }
         return hit;
@@ -873,12 +882,13 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
             const int inext = i + nthreads;
             const int4 nx = inext < total ? item(inext) : make_int4(0, 0, 0, 0);
             if (i < n_over) {
-                if (!(s.dbg_flags & 128) && over_test<false>(s, it.x, b.ev[it.y], nullptr))  // 128: ablation
+                if (!(s.dbg_flags & 128) && over_test<false>(s, it.x, b.ev[it.y], nullptr) &&
+                    !(s.dbg_flags & 1024))  // 128: ablation, no over tests; 1024: no result atomics
                     atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
             } else if (s.dbg_flags & 256) {  // 256: ablation, no under tests
             } else {
                 for (int j = it.x; j < it.y; ++j) prefetch_l1(s.seg + 8 * static_cast<size_t>(j));
-                if (under_range<false>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, nullptr))
+                if (under_range<false>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, nullptr) && !(s.dbg_flags & 1024))
                     atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
             }
             it = nx;
