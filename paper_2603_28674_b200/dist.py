@@ -63,6 +63,29 @@ class DistributedUpdater:
         return [dict(new_green=int(g), new_red=int(r), new_gray=int(y), unknown_after_heuristic=int(u),
                      residual_unknown=int(u)) for (g, r, y, _), u in zip(c, unknown)]
 
+    def states(self, n_global: int) -> np.ndarray:
+        """All labels (component-id order) on every rank: each shard's labels placed at
+        its id offset (tiles) or already in global order with 0xFF for other shards'
+        components (interleaved cells), merged with one MIN all-reduce."""
+        local = np.asarray(self.engine.states(), np.uint8)
+        full = np.full(n_global, 0xFF, np.uint8)
+        full[self.id_offset:self.id_offset + len(local)] = local
+        if self.world == 1:
+            return full
+        t = torch.from_numpy(full).to(self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return t.cpu().numpy()
+
+    def resolve_all_unknown(self) -> int:
+        """resolve_all_unknown on every shard (the exact check is per component, so
+        shard-local); the total count on every rank."""
+        n = int(self.engine.resolve_all_unknown())
+        if self.world == 1:
+            return n
+        t = torch.tensor([n], dtype=torch.int64, device=self.device)
+        dist.all_reduce(t, group=self.group)
+        return int(t.item())
+
     def gray_ids(self) -> np.ndarray | None:
         """All GRAY component ids (ascending) on rank 0, None elsewhere."""
         local = np.asarray(self.engine.gray_ids(), np.int64) + self.id_offset

@@ -56,6 +56,9 @@ class OracleShard:
     def gray_ids(self):
         return np.nonzero(self.eng.states() == 2)[0]
 
+    def states(self):
+        return self.eng.states()
+
 
 def _worker(rank, world, port, name, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -79,8 +82,9 @@ def _worker(rank, world, port, name, out):
         unknown = reps[-1]["unknown_after_heuristic"]
         reports += reps
     gray = up.gray_ids()
+    labels = up.states(N)
     if rank == 0:
-        out.put((reports, gray))
+        out.put((reports, gray, labels))
     dist.destroy_process_group()
 
 
@@ -99,10 +103,11 @@ def test_two_rank_shards_reproduce_reference_reports(name):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
     for p in procs:
         p.start()
-    reports, gray = q.get(timeout=300)
+    reports, gray, labels = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     got = np.array([[r["new_green"], r["new_red"], r["new_gray"], r["unknown_after_heuristic"]] for r in reports])
     assert np.array_equal(got, g["reports"][:, :4]), "sharded per-move reports differ from the reference"
     assert np.array_equal(gray, np.nonzero(g["snap_states"][-1] == 2)[0]), "gathered gray list differs"
+    assert np.array_equal(labels, g["snap_states"][-1]), "merged labels differ"
