@@ -357,7 +357,7 @@ def main():
         if up is None:
             eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True)
         else:  # broadcast of the moves from rank 0, shard update, all-reduce of the report counters
-            up.update(ids_d[it], rts_d[it], per_move=True)
+            up.update(ids_d[it], rts_d[it], per_move=True, check=False)
 
     # N = 1: the engine's own stream carries everything; N > 1: the collectives run on
     # torch's current stream and DistributedUpdater orders the engine stream against it
@@ -387,6 +387,8 @@ def main():
         while time.perf_counter() - t_clock0 < args.clock_window_s:
             step_device(args.warmup + (args.steps - 1))
             torch.cuda.synchronize()
+    if up is not None:
+        up.check()  # device-side errors of the stream-ordered updates
     step_ms = [a.elapsed_time(b) for a, b in ev]
     # phase split (untimed): the same last steps again with per-kernel events
     eng.set_phase_timing(True)

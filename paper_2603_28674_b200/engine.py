@@ -409,18 +409,32 @@ class GpuEngine:
         self._check(library().rgg_gpu_sync(self._h))
 
     # torch-tensor entry points used by the multi-GPU driver (paper_2603_28674_b200/dist.py)
-    def update_tensors(self, ids, rts, per_move: bool = True):
-        """ids int32[n] / rts float64[n, 12] CUDA tensors, enqueued on the engine stream
-        after the producer stream's work (so a preceding broadcast is visible)."""
+    def _torch_stream(self, device):
         import torch
 
-        torch.cuda.current_stream(ids.device).synchronize()
+        if getattr(self, "_ext", None) is None:
+            self._ext = torch.cuda.ExternalStream(self.stream(), device=device)
+        return self._ext
+
+    def update_tensors(self, ids, rts, per_move: bool = True):
+        """ids int32[n] / rts float64[n, 12] CUDA tensors, enqueued on the engine stream
+        after the current torch stream's work (so a preceding broadcast is visible); no
+        host synchronisation."""
+        import torch
+
+        self._torch_stream(ids.device).wait_stream(torch.cuda.current_stream(ids.device))
         self.update_device(ids.data_ptr(), rts.data_ptr(), int(ids.numel()), per_move=per_move)
 
-    def counters_into(self, out, n: int):
-        """Per-move counters of the last update into a CUDA int32 tensor (n, 4); waits for them."""
+    def counters_into(self, out, n: int, check: bool = True):
+        """Per-move counters of the last update into a CUDA int32 tensor (n, 4), ordered
+        before the current torch stream's later work.  check: also wait for the update
+        and raise its device-side errors (rgg_gpu_sync)."""
+        import torch
+
         self.copy_counters(out.data_ptr(), n)
-        self.sync()
+        torch.cuda.current_stream(out.device).wait_stream(self._torch_stream(out.device))
+        if check:
+            self.sync()
 
     def set_phase_timing(self, on: bool):
         """Per-kernel phase events in last_stats(); off lets the kernels overlap (PDL)."""
