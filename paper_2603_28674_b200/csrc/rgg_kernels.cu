@@ -874,13 +874,23 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
         const auto item = [&](int i) {
             return i < n_over ? b.items_over[i] : b.items_under[i - n_over];
         };
+        // two items ahead: the item after next is loaded and the next item's operands
+        // are prefetched into L1 while the current one is tested
         int i = gt;
         int4 it = i < total ? item(i) : make_int4(0, 0, 0, 0);
+        int4 nx = i + nthreads < total ? item(i + nthreads) : make_int4(0, 0, 0, 0);
         unsigned long long d_items = 0, d_segs = 0;
         while (i < total) {
             if (dbgw) d_items += 1, d_segs += i < n_over ? 0 : it.y - it.x;
-            const int inext = i + nthreads;
-            const int4 nx = inext < total ? item(inext) : make_int4(0, 0, 0, 0);
+            const int inext = i + nthreads, i2 = inext + nthreads;
+            const int4 nn = i2 < total ? item(i2) : make_int4(0, 0, 0, 0);
+            if (inext < total) {
+                if (inext < n_over) {
+                    prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
+                } else {
+                    for (int j = nx.x; j < nx.y; j += 2) prefetch_l1(s.seg + 8 * static_cast<size_t>(j));
+                }
+            }
             if (i < n_over) {
                 if (!(s.dbg_flags & 128) && over_test<false>(s, it.x, b.ev[it.y], nullptr) &&
                     !(s.dbg_flags & 1024))  // 128: ablation, no over tests; 1024: no result atomics
@@ -892,6 +902,7 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
                     atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
             }
             it = nx;
+            nx = nn;
             i = inext;
         }
         if (dbgw) {
