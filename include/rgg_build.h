@@ -29,6 +29,8 @@ int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nod
 /* Same, with flags: RGG_BUILD_POSES keeps forward_kinematics of every discretized
  * configuration for the GPU exact resolve (rgg_gpu_set_resolver, include/rgg_gpu.h). */
 #define RGG_BUILD_POSES 1
+/* fit the swept-volume boxes (obb_from_points) on the GPU, bit-identical (device 0) */
+#define RGG_BUILD_GPU_FIT 2
 int rgg_build_layout_ex(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
                         const int32_t* edges, double eps, int32_t max_segments, int32_t threads, int32_t flags,
                         rgg_built** out);

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 GPU_SOURCES = ["rgg_kernels.cu", "rgg_resolve.cu", "rgg_store.cu", "rgg_capi.cu"]
 GPU_DEPS = GPU_SOURCES + ["rgg_device.cuh", "rgg_kernels.cuh"]
-PRODUCER_SOURCES = ["producer.cpp"]
+PRODUCER_SOURCES = ["producer.cpp", "swept_gpu.cu"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -52,9 +52,16 @@ def build_producer(force: bool = False) -> str:
     if not all(os.path.exists(s) for s in srcs):
         return ""
     if force or _stale(out, deps):
-        cmd = ["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
-               "-I", os.path.join(ROOT, "include"), "-o", out] + srcs
-        subprocess.check_call(cmd)
+        # host part with g++ (the reference's flags), the GPU box fit with nvcc -fmad=false
+        obj_cpp = os.path.join(LIB, "producer.o")
+        obj_cu = os.path.join(LIB, "swept_gpu.o")
+        subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-pthread", "-c",
+                               "-I", os.path.join(ROOT, "include"), "-o", obj_cpp, srcs[0]])
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-c",
+                               "-o", obj_cu, srcs[1]])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, obj_cpp, obj_cu, "-Xcompiler", "-pthread"])
+        for o in (obj_cpp, obj_cu):
+            os.remove(o)
     return out
 
 

@@ -16,6 +16,10 @@
 #include <thread>
 #include <vector>
 
+extern "C" int rggp_fit_boxes_gpu(const double* poses, const int64_t* off, int32_t ncomp, const double* he3,
+                                  const double* cos_sin, int32_t device, double* out);
+
+
 namespace {
 
 thread_local std::string g_err;
@@ -362,7 +366,19 @@ Tf body_pose(const double* c) {
     return world.compose(Tf{});
 }
 
-Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K, bool keep_poses) {
+// discretize_edge's configuration count (robot.cpp:39-64)
+int config_count(const double* a, const double* b, double eps) {
+    double len2 = 0.0;
+    for (int i = 0; i < 6; ++i) {
+        const double d = b[i] - a[i];
+        len2 += d * d;
+    }
+    return std::max(2, static_cast<int>(std::ceil(std::sqrt(len2) / eps)) + 1);
+}
+
+// pose_out (gpu_fit): the component's forward-kinematics poses, 12 doubles each
+Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K, bool keep_poses, bool gpu_fit,
+                double* pose_out) {
     // discretize_edge (robot.cpp:39-64)
     double len2 = 0.0;
     for (int i = 0; i < 6; ++i) {
@@ -383,10 +399,15 @@ Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, i
             for (int k = 0; k < 6; ++k) cfg[k] = a[k] + (b[k] - a[k]) * t;
         }
         fk[i] = body_pose(cfg);
+        if (pose_out) {
+            std::memcpy(pose_out + 12 * i, fk[i].r, 9 * sizeof(double));
+            pose_out[12 * i + 9] = fk[i].t.x, pose_out[12 * i + 10] = fk[i].t.y, pose_out[12 * i + 11] = fk[i].t.z;
+        }
     }
     Comp comp;
-    // build_outer_approx (swept.cpp:100-118)
+    // build_outer_approx (swept.cpp:100-118); with gpu_fit the box is fitted later on the GPU
     std::vector<V3> cloud;
+    if (!gpu_fit) {
     cloud.reserve(static_cast<size_t>(n) * 8);
     for (const Tf& T : fk) {
         Box w;
@@ -400,6 +421,7 @@ Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, i
         cloud.insert(cloud.end(), cs, cs + 8);
     }
     comp.over = fit_box(cloud);
+    }
     // build_inner_approx (swept.cpp:188-228)
     for (size_t si = 0; si < rb.spheres.size(); ++si) {
         const double rad = rb.radius[si];
@@ -446,6 +468,7 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                         const int32_t* edges, double eps, int32_t K, int32_t threads, int32_t flags,
                         rgg_built** out) {
     const bool keep_poses = (flags & RGG_BUILD_POSES) != 0;
+    const bool gpu_fit = (flags & RGG_BUILD_GPU_FIT) != 0;
     try {
         if (!out) throw std::invalid_argument("null output");
         if (!(eps > 0)) throw std::invalid_argument("resolution must be positive");
@@ -456,6 +479,30 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         const Robot rb = make_robot({he3[0], he3[1], he3[2]}, eps);
         const int32_t N = n_nodes + n_edges;
         std::vector<Comp> comps(static_cast<size_t>(N));
+        const auto ends = [&](int32_t c, const double** a, const double** b) {
+            if (c < n_nodes) {
+                *a = *b = nodes + 6 * static_cast<size_t>(c);
+            } else {
+                const int32_t e = c - n_nodes;
+                *a = nodes + 6 * static_cast<size_t>(edges[2 * e]);
+                *b = nodes + 6 * static_cast<size_t>(edges[2 * e + 1]);
+            }
+        };
+        // gpu_fit: every component's poses go straight into one buffer (pageable: pinning
+        // the ~100 B per configuration costs more than the copy it would speed up)
+        std::vector<int64_t> pose_off;
+        std::vector<double> pose_buf;
+        double* poses = nullptr;
+        if (gpu_fit) {
+            pose_off.assign(static_cast<size_t>(N) + 1, 0);
+            for (int32_t c = 0; c < N; ++c) {
+                const double *a, *b;
+                ends(c, &a, &b);
+                pose_off[c + 1] = pose_off[c] + config_count(a, b, eps);
+            }
+            pose_buf.resize(static_cast<size_t>(pose_off[N]) * 12);
+            poses = pose_buf.data();
+        }
         int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
         nt = std::max(1, std::min(nt, 256));
         std::atomic<int32_t> next{0};
@@ -468,14 +515,9 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                     if (c0 >= N || failed) break;
                     for (int32_t c = c0; c < std::min(N, c0 + 256); ++c) {
                         const double *a, *b;
-                        if (c < n_nodes) {
-                            a = b = nodes + 6 * static_cast<size_t>(c);
-                        } else {
-                            const int32_t e = c - n_nodes;
-                            a = nodes + 6 * static_cast<size_t>(edges[2 * e]);
-                            b = nodes + 6 * static_cast<size_t>(edges[2 * e + 1]);
-                        }
-                        comps[c] = build_comp(rb, a, b, eps, K, keep_poses);
+                        ends(c, &a, &b);
+                        comps[c] = build_comp(rb, a, b, eps, K, keep_poses, gpu_fit,
+                                              gpu_fit ? poses + 12 * static_cast<size_t>(pose_off[c]) : nullptr);
                     }
                 }
             } catch (const std::exception& ex) {
@@ -488,6 +530,26 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         work();
         for (auto& t : pool) t.join();
         if (failed) throw std::runtime_error(err);
+        if (gpu_fit) {
+            // obb_from_points of every component on the GPU (swept_gpu.cu), from the poses
+            double cs[22];
+            constexpr double kStep = 3.0 * 3.141592653589793 / 180.0;
+            for (int step = -5; step <= 5; ++step) {
+                cs[2 * (step + 5)] = std::cos(step * kStep);
+                cs[2 * (step + 5) + 1] = std::sin(step * kStep);
+            }
+            std::vector<double> boxes(static_cast<size_t>(N) * 15);
+            const int rc = rggp_fit_boxes_gpu(poses, pose_off.data(), N, he3, cs, 0, boxes.data());
+            std::vector<double>().swap(pose_buf);
+            if (rc != 0) throw std::runtime_error("GPU box fit failed (CUDA error " + std::to_string(rc) + ")");
+            for (int32_t c = 0; c < N; ++c) {
+                const double* o = &boxes[15 * static_cast<size_t>(c)];
+                Box& bx = comps[c].over;
+                bx.c = {o[0], o[1], o[2]};
+                for (int k = 0; k < 3; ++k) bx.ax[k] = {o[3 + 3 * k], o[4 + 3 * k], o[5 + 3 * k]};
+                bx.he = {o[12], o[13], o[14]};
+            }
+        }
 
         // ---- serialize (batch_layout.cpp:21-146)
         rgg_built* L = new rgg_built();

@@ -1,0 +1,202 @@
+// swept_gpu.cu — the producer's outer approximation on the GPU.
+//
+// obb_from_points (proj/src/geometry.cpp:134-195) fits each component's swept
+// volume box: PCA frame of the body corners at every discretized configuration
+// (Jacobi), then 3 x 10 rotated candidate frames, keeping the smallest-volume
+// one.  It is ~85 % of the host producer's time.  Here one thread fits one
+// component, regenerating the corners from the forward-kinematics poses on
+// every pass instead of storing the cloud.  Compiled with -fmad=false: every
+// expression is the host producer's (producer.cpp, itself the reference's
+// association), so the boxes are bit-identical; the cosines / sines of the ten
+// candidate angles come from the host's libm.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+namespace {
+
+struct V3 {
+    double x, y, z;
+};
+__device__ inline V3 operator+(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ inline V3 operator-(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ inline V3 operator*(V3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ inline double dotv(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ inline V3 crossv(V3 a, V3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+
+// Transform::rotate / apply of a pose r[9], t[3] (vec3.hpp:72-84)
+__device__ inline V3 rot(const double* r, V3 p) {
+    return {r[0] * p.x + r[1] * p.y + r[2] * p.z, r[3] * p.x + r[4] * p.y + r[5] * p.z,
+            r[6] * p.x + r[7] * p.y + r[8] * p.z};
+}
+
+// corner i of the body box at a pose (producer.cpp build_comp + corners_of)
+__device__ inline V3 corner(const double* T, V3 he, int i) {
+    const V3 c = {T[0] * 0.0 + T[1] * 0.0 + T[2] * 0.0 + T[9], T[3] * 0.0 + T[4] * 0.0 + T[5] * 0.0 + T[10],
+                  T[6] * 0.0 + T[7] * 0.0 + T[8] * 0.0 + T[11]};
+    const V3 e0 = rot(T, {1, 0, 0}) * he.x, e1 = rot(T, {0, 1, 0}) * he.y, e2 = rot(T, {0, 0, 1}) * he.z;
+    V3 p = (i & 1) ? c + e0 : c - e0;
+    p = (i & 2) ? p + e1 : p - e1;
+    return (i & 4) ? p + e2 : p - e2;
+}
+
+__device__ inline double min_ref(double a, double b) { return b < a ? b : a; }
+__device__ inline double max_ref(double a, double b) { return a < b ? b : a; }
+
+__device__ double volume(const double* poses, int n, V3 he, const V3* ax, double* lo, double* hi) {
+    for (int k = 0; k < 3; ++k) lo[k] = __longlong_as_double(0x7ff0000000000000ll), hi[k] = -lo[k];
+    for (int q = 0; q < n; ++q)
+        for (int i = 0; i < 8; ++i) {
+            const V3 p = corner(poses + 12 * static_cast<size_t>(q), he, i);
+            for (int k = 0; k < 3; ++k) {
+                const double t = dotv(p, ax[k]);
+                lo[k] = min_ref(lo[k], t);
+                hi[k] = max_ref(hi[k], t);
+            }
+        }
+    return (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+}
+
+__device__ void jacobi3(double m[3][3], double vals[3], V3 vecs[3]) {
+    double v[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        const double off = fabs(m[0][1]) + fabs(m[0][2]) + fabs(m[1][2]);
+        if (off == 0.0) break;
+        for (int p = 0; p < 2; ++p) {
+            for (int q = p + 1; q < 3; ++q) {
+                if (m[p][q] == 0.0) continue;
+                const double theta = (m[q][q] - m[p][p]) / (2.0 * m[p][q]);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+                const double c = 1.0 / sqrt(t * t + 1.0);
+                const double s = t * c;
+                for (int k = 0; k < 3; ++k) {
+                    const double a = m[k][p], b = m[k][q];
+                    m[k][p] = c * a - s * b;
+                    m[k][q] = s * a + c * b;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    const double a = m[p][k], b = m[q][k];
+                    m[p][k] = c * a - s * b;
+                    m[q][k] = s * a + c * b;
+                }
+                for (int k = 0; k < 3; ++k) {
+                    const double a = v[k][p], b = v[k][q];
+                    v[k][p] = c * a - s * b;
+                    v[k][q] = s * a + c * b;
+                }
+            }
+        }
+    }
+    for (int i = 0; i < 3; ++i) {
+        vals[i] = m[i][i];
+        vecs[i] = {v[0][i], v[1][i], v[2][i]};
+    }
+}
+
+// fit_box (producer.cpp) of the corners of n poses; out = centre, axes[3], half extents
+__global__ void fit_kernel(const double* poses, const int64_t* off, int ncomp, V3 he, const double* cs,
+                           double* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncomp) return;
+    const double* P = poses + 12 * static_cast<size_t>(off[c]);
+    const int n = static_cast<int>(off[c + 1] - off[c]);
+    const double npts = static_cast<double>(8 * n);
+    V3 mean{0, 0, 0};
+    for (int q = 0; q < n; ++q)
+        for (int i = 0; i < 8; ++i) mean = mean + corner(P + 12 * q, he, i);
+    mean = mean * (1.0 / npts);
+    double cov[3][3] = {};
+    for (int q = 0; q < n; ++q)
+        for (int i = 0; i < 8; ++i) {
+            const V3 d = corner(P + 12 * q, he, i) - mean;
+            const double dc[3] = {d.x, d.y, d.z};
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b) cov[a][b] += dc[a] * dc[b];
+        }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) cov[a][b] /= npts;
+    double vals[3];
+    V3 axes[3];
+    jacobi3(cov, vals, axes);
+    int ord[3] = {0, 1, 2};
+    for (int i = 1; i < 3; ++i)
+        for (int j = i; j > 0 && vals[ord[j]] > vals[ord[j - 1]]; --j) {
+            const int t = ord[j];
+            ord[j] = ord[j - 1];
+            ord[j - 1] = t;
+        }
+    V3 best[3] = {axes[ord[0]], axes[ord[1]], axes[ord[2]]};
+    best[2] = crossv(best[0], best[1]);
+    double lo[3], hi[3];
+    double best_vol = volume(P, n, he, best, lo, hi);
+    for (int k = 0; k < 3; ++k) {
+        const V3 pivot = best[k];
+        V3 win[3] = {best[0], best[1], best[2]};
+        for (int step = -5; step <= 5; ++step) {
+            if (step == 0) continue;
+            // Transform::rotation_axis_angle (geometry.cpp:13-29) with the host's cos / sin
+            const double len = sqrt(dotv(pivot, pivot));
+            const double kx = pivot.x / len, ky = pivot.y / len, kz = pivot.z / len;
+            const double co = cs[2 * (step + 5)], si = cs[2 * (step + 5) + 1], v = 1.0 - co;
+            const double r[9] = {kx * kx * v + co, kx * ky * v - kz * si, kx * kz * v + ky * si,
+                                 ky * kx * v + kz * si, ky * ky * v + co, ky * kz * v - kx * si,
+                                 kz * kx * v - ky * si, kz * ky * v + kx * si, kz * kz * v + co};
+            V3 cand[3];
+            for (int j = 0; j < 3; ++j) cand[j] = rot(r, best[j]);
+            const double vol = volume(P, n, he, cand, lo, hi);
+            if (vol < best_vol) {
+                best_vol = vol;
+                for (int j = 0; j < 3; ++j) win[j] = cand[j];
+            }
+        }
+        for (int j = 0; j < 3; ++j) best[j] = win[j];
+    }
+    volume(P, n, he, best, lo, hi);
+    const V3 ctr = best[0] * ((lo[0] + hi[0]) * 0.5) + best[1] * ((lo[1] + hi[1]) * 0.5) + best[2] * ((lo[2] + hi[2]) * 0.5);
+    double* o = out + 15 * static_cast<size_t>(c);
+    o[0] = ctr.x, o[1] = ctr.y, o[2] = ctr.z;
+    for (int k = 0; k < 3; ++k) o[3 + 3 * k] = best[k].x, o[4 + 3 * k] = best[k].y, o[5 + 3 * k] = best[k].z;
+    o[12] = (hi[0] - lo[0]) * 0.5, o[13] = (hi[1] - lo[1]) * 0.5, o[14] = (hi[2] - lo[2]) * 0.5;
+}
+
+}  // namespace
+
+// poses: total x 12 doubles (host), off: ncomp+1, cos_sin: cos/sin of step*3 deg for step = -5..5
+// (index step+5), out: ncomp x 15 doubles (host).  Returns a cudaError_t value.
+extern "C" int rggp_fit_boxes_gpu(const double* poses, const int64_t* off, int32_t ncomp, const double* he3,
+                                  const double* cos_sin, int32_t device, double* out) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return e;
+    const size_t total = static_cast<size_t>(off[ncomp]);
+    double *dp = nullptr, *dcs = nullptr, *dout = nullptr;
+    int64_t* doff = nullptr;
+    if ((e = cudaMalloc(&dp, (total ? total : 1) * 96)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&doff, (static_cast<size_t>(ncomp) + 1) * 8)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&dcs, 22 * 8)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&dout, (static_cast<size_t>(ncomp) + 1) * 15 * 8)) != cudaSuccess) return e;
+    e = cudaMemcpy(dp, poses, total * 96, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(doff, off, (static_cast<size_t>(ncomp) + 1) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dcs, cos_sin, 22 * 8, cudaMemcpyHostToDevice);
+    cudaEvent_t ev0, ev1;
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0);
+    if (e == cudaSuccess && ncomp > 0) {
+        fit_kernel<<<(ncomp + 127) / 128, 128>>>(dp, doff, ncomp, V3{he3[0], he3[1], he3[2]}, dcs, dout);
+        e = cudaGetLastError();
+    }
+    cudaEventRecord(ev1);
+    if (std::getenv("RGG_DEBUG_FIT")) {
+        float ms = 0;
+        cudaEventSynchronize(ev1);
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        std::fprintf(stderr, "[fit] %d components, %zu poses: kernel %.2f ms\n", ncomp, total, ms);
+    }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, static_cast<size_t>(ncomp) * 15 * 8, cudaMemcpyDeviceToHost);
+    cudaFree(dp), cudaFree(doff), cudaFree(dcs), cudaFree(dout);
+    return e;
+}

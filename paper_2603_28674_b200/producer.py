@@ -42,7 +42,8 @@ def library():
     return _lib
 
 
-def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False, with_poses=False):
+def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False, with_poses=False,
+                 gpu_fit=False):
     """Components (nodes first, then edges) of a free-flying box robot -> store arrays.
     with_poses: also a["pose_off"] (N+1) and a["poses"] (configs, 1, 12), the
     forward kinematics of every discretized configuration (GPU exact resolve)."""
@@ -52,7 +53,8 @@ def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, w
     edges = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
     h = C.c_void_p()
     rc = L.rgg_build_layout_ex(he.ctypes.data, len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
-                               float(eps), int(max_segments), int(threads), 1 if with_poses else 0, C.byref(h))
+                               float(eps), int(max_segments), int(threads),
+                               (1 if with_poses else 0) | (2 if gpu_fit else 0), C.byref(h))
     if rc != 0:
         raise RuntimeError(L.rgg_build_last_error().decode())
     try:
@@ -85,11 +87,12 @@ def obstacle_spheres(he, count):
     return cen, r.value
 
 
-def layout_for(roadmap: synth.Roadmap, obstacles: synth.Obstacles, threads=0, with_poses=False) -> LayoutView:
+def layout_for(roadmap: synth.Roadmap, obstacles: synth.Obstacles, threads=0, with_poses=False,
+               gpu_fit=False) -> LayoutView:
     """with_poses: the view also carries .resolver = (pose_off, poses, body_half_extents)
     for GpuEngine.set_resolver."""
     N, B, S, a = build_layout(roadmap.robot_he, roadmap.nodes, roadmap.edges, roadmap.eps, roadmap.max_segments,
-                              threads, with_poses=with_poses)
+                              threads, with_poses=with_poses, gpu_fit=gpu_fit)
     M = len(obstacles.he)
     Cmax = int(obstacles.spheres.max()) if M else 1
     sl = np.zeros((M, Cmax, 3))
