@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--json-out", default="")
     p.add_argument("--clock-window-s", type=float, default=1.0)
     p.add_argument("--no-resolve", action="store_true", help="skip the exact-resolve measurement")
-    p.add_argument("--extra-configs", default="c5",
+    p.add_argument("--extra-configs", default="c5,c4,c3",
                    help="comma list of configs also measured on rank 0 (N=1) and reported under 'extra'")
     return p.parse_args()
 
@@ -89,6 +89,11 @@ def world_moves(config, world, seed, iterations):
         rts_all.append(rts.reshape(iterations, m, 12))
     ids = np.stack(ids_all, 1).reshape(iterations, world * m).astype(np.int32)
     rts = np.stack(rts_all, 1).reshape(iterations, world * m, 12)
+    k = synth.MOVES_PER_STEP.get(config)
+    if k:  # iteration it moves obstacles [k*it, k*it + k) mod m of every tile
+        sel = np.array([[r * m + (k * it + j) % m for r in range(world) for j in range(k)] for it in range(iterations)])
+        ids = np.take_along_axis(ids, sel, 1).astype(np.int32)
+        rts = np.take_along_axis(rts, sel[:, :, None], 1)
     return ids, rts
 
 
@@ -192,9 +197,12 @@ def config_dict(args, n_components, world=1):
     from paper_2603_28674_b200 import synth
 
     kind, nodes, k, half, m, ohalf = synth.CONFIGS[args.config]
+    mv = synth.MOVES_PER_STEP.get(args.config)
+    step = (f"1 step = 1 update = {mv} of the {m} obstacles re-posed (rotating subset, ~5 % of cells dirty)"
+            if mv else f"1 step = 1 update = all {m} obstacles re-posed")
     return {"workload": f"{args.config}: {'SE(2)' if kind == 'se2' else '3D'} roadmap {nodes} nodes k={k} "
                         f"({n_components} components incl. nodes) x {m} moving OBB obstacles per GPU tile; "
-                        f"1 step = 1 update = all {m} obstacles re-posed (per-move reports)",
+                        f"{step} (per-move reports)",
             "components_per_gpu": n_components, "obstacles_per_gpu": m, "moves_per_step": m * world,
             "l2": "flushed (512 MB write) between timed steps", "parallelism": f"tiles x{world} (weak)",
             "precision": "fp64-exact (reference op order, no FMA)"}
@@ -206,7 +214,7 @@ def measure_extra(config, seed, device, steps=10, warmup=3):
     import torch
 
     from paper_2603_28674_b200 import engine as E
-    from paper_2603_28674_b200 import producer
+    from paper_2603_28674_b200 import producer, synth
 
     t0 = time.time()
     rm, obs, _ = tile_workload(config, 0, seed, warmup + steps)
@@ -234,13 +242,25 @@ def measure_extra(config, seed, device, steps=10, warmup=3):
         b.record(stream)
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
+    eng.set_phase_timing(True)
+    eng.update_device(ids_d[warmup + steps - 1].data_ptr(), rts_d[warmup + steps - 1].data_ptr(), m, per_move=True)
+    eng.sync()
+    dirty = eng.last_stats()["dirty_cells"]
+    eng.set_phase_timing(False)
     eng.update_device(ids_d[warmup + steps - 1].data_ptr(), rts_d[warmup + steps - 1].data_ptr(), m,
                       per_move=True, census=True)
     cen = eng.census()
     per = statistics.mean(ms)
+    ncells = (lv.N + 127) // 128
+    byts = cen["bytes_components"] + m * 768
     return {"workload": config_dict(argparse.Namespace(config=config), lv.N)["workload"],
-            "components": lv.N, "moves_per_update": m, "per_update_ms": per, "value": lv.N / (per * 1e-3),
+            "components": lv.N, "moves_per_update": m, "per_update_ms": per,
+            # incremental configs: the components of the dirty cells are the ones relabelled
+            "value": (min(lv.N, dirty * 128) if synth.MOVES_PER_STEP.get(config) else lv.N) / (per * 1e-3),
+            "value_all_components": lv.N / (per * 1e-3),
             "unit": "edges/s", "steps": steps, "build_s": round(build_s, 1),
+            "dirty_cells": dirty, "dirty_fraction": dirty / max(1, ncells),
+            "hbm_frac_of_update": byts / (per * 1e-3) / 1e9 / 6553.3,
             "census": {k: cen[k] for k in ("over_pairs", "sat_flops", "under_pairs", "seg_sphere_tests",
                                            "bytes_components")}}
 

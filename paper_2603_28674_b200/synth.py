@@ -125,3 +125,7 @@ CONFIGS = {
     "c4": ("se2", 87_000, 20, 71.0, 64, 72.0),
     "c5": ("se2", 87_000, 20, 71.0, 1024, 72.0),
 }
+
+# Moves per update where a config moves only a subset of its obstacles (BASELINE configs[3]:
+# incremental updates dirtying ~5 % of the cells); the subset rotates through all obstacles.
+MOVES_PER_STEP = {"c4": 16}
