@@ -647,6 +647,13 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.cap = cap;
     s.use_under = o.use_under ? 1 : 0;
     s.dbg_flags = std::getenv("RGG_DEBUG_FLAGS") ? std::atoi(std::getenv("RGG_DEBUG_FLAGS")) : 0;
+    {
+        // narrow operands of the whole roadmap: Box32 lines and segment records
+        const double bytes = 128.0 * Np * B + 64.0 * static_cast<double>(h->total_segs_owned);
+        int l2 = 0;
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device);
+        s.prefetch = bytes <= 0.5 * l2 && !(s.dbg_flags & 2048) ? 1 : 0;  // 2048: ablation, never
+    }
     s.aabb = h->d_aabb;
     s.sat = h->d_sat;
     s.sat32 = h->d_sat32;

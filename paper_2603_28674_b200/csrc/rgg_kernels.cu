@@ -1504,15 +1504,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
                 __syncwarp();
                 continue;
             }
-            // the narrow kernel (next launch) reads exactly these operands: stage them in L2 now
-            if (bm && w == 0) {
+            // the narrow kernel (next launch) reads exactly these operands: stage them in L2
+            // now, when the roadmap's operands fit the L2 (else the prefetches evict each other)
+            if (bm && w == 0 && s.prefetch) {
                 const size_t i0 = static_cast<size_t>(c) * s.B;
                 prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, false);
             }
-            if (sm && w == 0) {
-                prefetch_l2(s.row + c * s.B * s.S);
+            if (sm && w == 0 && s.prefetch)
                 prefetch_range(s.seg + 8 * static_cast<size_t>(seg_lo), s.seg + 8 * static_cast<size_t>(seg_hi), false);
-            }
             const int wt = rec.y + (0 * W + w) * s.cell + t, wo = rec.y + (1 * W + w) * s.cell + t,
                       wu = rec.y + (2 * W + w) * s.cell + t;
             if (valid) {

@@ -41,6 +41,7 @@ struct Store {
     int32_t cell, ncells, cap;
     int32_t use_under;
     int32_t dbg_flags;         // ablation switches (RGG_DEBUG_FLAGS): 1 = skip narrow tests, 2 = skip operand loads
+    int32_t prefetch;          // touch stages the narrow operands in L2 (they fit in half of it)
     const double2* aabb;       // 3 planes of Np double2: (minx,miny) (minz,maxx) (maxy,maxz)
     const double* sat;         // Np*B*22 (21 + pad)
     const rggd::Box32* sat32;  // Np*B fp32 filter operands of sat
