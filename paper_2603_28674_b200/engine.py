@@ -61,6 +61,7 @@ class _Report(C.Structure):
 
 
 _REPORT_DTYPE = np.dtype(_Report)
+_I32, _F64 = np.dtype(np.int32), np.dtype(np.float64)
 
 
 class _ResolveView(C.Structure):
@@ -446,6 +447,12 @@ class GpuEngine:
 
     @staticmethod
     def _moves(moves):
+        if type(moves) is tuple and len(moves) == 2:  # fast path: the arrays as they come
+            ids, rts = moves
+            if (type(ids) is np.ndarray and type(rts) is np.ndarray and ids.dtype is _I32 and rts.dtype is _F64
+                    and ids.ndim == 1 and rts.shape == (ids.shape[0], 12) and ids.flags.c_contiguous
+                    and rts.flags.c_contiguous):
+                return ids, rts
         if isinstance(moves, tuple) and len(moves) == 2 and not np.isscalar(moves[0]):
             ids, rts = moves
             if not (isinstance(ids, np.ndarray) and ids.dtype == np.int32 and ids.flags.c_contiguous):
