@@ -167,10 +167,20 @@ __global__ void super_box_kernel(const double* cell_aabb, int ncells, int nsuper
     for (int k = 0; k < 6; ++k) super_aabb[6 * static_cast<size_t>(g) + k] = box[k];
 }
 
-template <class T>
-cudaError_t alloc(T** p, size_t n) {
-    return cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(T));
-}
+// scratch allocations released on every exit of build_store
+struct Scratch {
+    void* p[16] = {};
+    int n = 0;
+    ~Scratch() {
+        for (int i = 0; i < n; ++i) cudaFree(p[i]);
+    }
+    template <class T>
+    cudaError_t alloc(T** out, size_t count) {
+        const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(out), (count ? count : 1) * sizeof(T));
+        if (e == cudaSuccess) p[n++] = *out;
+        return e;
+    }
+};
 
 #define SCK(x)                                   \
     do {                                         \
@@ -181,16 +191,17 @@ cudaError_t alloc(T** p, size_t n) {
 }  // namespace
 
 cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
+    Scratch scratch;
     const int N = in.N, B = in.B, BS = in.B * in.S, np = in.np, cell = in.cell;
     const long long nrows = static_cast<long long>(np) * BS;
     const int ncells = (np + cell - 1) / cell, nsuper = (ncells + kSuperCells - 1) / kSuperCells;
     // 1. raw inputs
     double *aabb = nullptr, *sat21 = nullptr, *segs7 = nullptr;
     int32_t* row_off = nullptr;
-    SCK(alloc(&aabb, static_cast<size_t>(N) * 6));
-    SCK(alloc(&sat21, static_cast<size_t>(N) * B * 21));
-    SCK(alloc(&row_off, static_cast<size_t>(N) * BS + 1));
-    SCK(alloc(&segs7, static_cast<size_t>(in.T) * 7));
+    SCK(scratch.alloc(&aabb, static_cast<size_t>(N) * 6));
+    SCK(scratch.alloc(&sat21, static_cast<size_t>(N) * B * 21));
+    SCK(scratch.alloc(&row_off, static_cast<size_t>(N) * BS + 1));
+    SCK(scratch.alloc(&segs7, static_cast<size_t>(in.T) * 7));
     // pageable sources: plain synchronous copies (the driver pipelines them through
     // its staging buffers; async pageable copies on a non-blocking stream were slower)
     SCK(cudaStreamSynchronize(st));
@@ -202,11 +213,11 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     // 2. Morton order
     unsigned long long *bounds = nullptr, *key = nullptr, *key2 = nullptr;
     int32_t *val = nullptr, *order = nullptr;
-    SCK(alloc(&bounds, 6));
-    SCK(alloc(&key, N));
-    SCK(alloc(&key2, N));
-    SCK(alloc(&val, N));
-    SCK(alloc(&order, N));
+    SCK(scratch.alloc(&bounds, 6));
+    SCK(scratch.alloc(&key, N));
+    SCK(scratch.alloc(&key2, N));
+    SCK(scratch.alloc(&val, N));
+    SCK(scratch.alloc(&order, N));
     const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0, 0, 0};
     SCK(cudaMemcpyAsync(bounds, init, sizeof(init), cudaMemcpyHostToDevice, st));
     const int T256 = 256;
@@ -217,10 +228,10 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     size_t tmp_bytes = 0, scan_bytes = 0;
     SCK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key, key2, val, order, N, 0, 63, st));
     int32_t *row_len = nullptr;
-    SCK(alloc(&row_len, static_cast<size_t>(nrows) + 1));
+    SCK(scratch.alloc(&row_len, static_cast<size_t>(nrows) + 1));
     SCK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, row_len, out.row, nrows + 1, st));
-    void* tmp = nullptr;
-    SCK(cudaMalloc(&tmp, std::max<size_t>(1, std::max(tmp_bytes, scan_bytes))));
+    char* tmp = nullptr;
+    SCK(scratch.alloc(&tmp, std::max(tmp_bytes, scan_bytes)));
     if (N > 0) SCK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key2, val, order, N, 0, 63, st));
     // 3. shard selection, id -> rank, gathers
     SCK(cudaMemsetAsync(out.rank, 0xFF, static_cast<size_t>(N) * 4, st));
@@ -234,7 +245,7 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     SCK(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, row_len, out.row, nrows + 1, st));
     SCK(cudaMemcpyAsync(&out.total_segs, out.row + nrows, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
-    SCK(alloc(&out.seg, static_cast<size_t>(out.total_segs) * 8));
+    SCK(cudaMalloc(reinterpret_cast<void**>(&out.seg), sizeof(double) * std::max<size_t>(1, static_cast<size_t>(out.total_segs) * 8)));
     if (nrows > 0)
         segs_kernel<<<static_cast<unsigned>((nrows + T256 - 1) / T256), T256, 0, st>>>(
             out.orig, nrows, BS, row_off, out.row, segs7, out.spline, out.seg);
@@ -244,11 +255,6 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     }
     SCK(cudaGetLastError());
     SCK(cudaStreamSynchronize(st));
-    for (void* p : {static_cast<void*>(aabb), static_cast<void*>(sat21), static_cast<void*>(row_off),
-                    static_cast<void*>(segs7), static_cast<void*>(bounds), static_cast<void*>(key),
-                    static_cast<void*>(key2), static_cast<void*>(val), static_cast<void*>(order),
-                    static_cast<void*>(row_len), tmp})
-        cudaFree(p);
     return cudaSuccess;
 }
 
