@@ -706,6 +706,9 @@ __device__ __forceinline__ void commit_grid(const Store& s, const Batch& b) {
     }
 }
 
+// the moved obstacles' operands, alone (a store without components)
+__global__ void commit_kernel(Store s, Batch b) { commit_grid(s, b); }
+
 __device__ __forceinline__ const int32_t* rec_list(int4 r) {
     return reinterpret_cast<const int32_t*>((static_cast<unsigned long long>(static_cast<uint32_t>(r.w)) << 32) |
                                             static_cast<uint32_t>(r.z));
@@ -1940,6 +1943,7 @@ cudaError_t launch_init_obstacles(const Store& s, Event*, cudaStream_t st) {
 }
 
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
+    if (s.ncells == 0) return cudaSuccess;  // no components: nothing to bin
     const int cells_per = kBinThreads / 32;  // = kSuperCells
     return launch_pdl(bin_kernel, dim3((s.ncells + cells_per - 1) / cells_per), dim3(kBinThreads), st, s, b);
 }
@@ -2041,7 +2045,11 @@ static cudaError_t launch_narrow(const Store& s, const Batch& b, int grid, cudaS
 }
 
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st) {
-    if (s.ncells == 0) return cudaSuccess;
+    if (s.ncells == 0) {  // no components: only the obstacles' operands move on
+        if (b.n == 0 || (flags & kCensus)) return cudaSuccess;
+        commit_kernel<<<(b.n + 7) / 8, 128, 0, st>>>(s, b);
+        return cudaGetLastError();
+    }
     if (pipeline() == 6) {
         static int g_touch = 0, g_touch_c = 0, g_apply = 0;
         if (!g_touch) {

@@ -219,3 +219,45 @@ def test_comparison_pipelines_stay_exact(pipeline):
                         os.path.join(here, "test_gpu_parity.py")], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_degenerate_sizes(eng_mod):
+    """Empty roadmap, no obstacles, a single component: create, update, query."""
+    from paper_2603_28674_b200.engine import LayoutView
+
+    g = load_golden("scn_quick_smoke")
+    # no components
+    lv0 = LayoutView(N=0, B=1, S=1, M=int(g["M"]), C=int(g["C"]), edge_sat=np.zeros((0, 21)),
+                     comp_aabb=np.zeros((0, 6)), row_off=np.zeros(1, np.int32), segs=np.zeros((0, 7)),
+                     spline_r=np.zeros(1), obst_he=g["obst_he"], obst_sph_local=g["obst_sph_local"],
+                     obst_sph_r=g["obst_sph_r"], obst_sph_n=g["obst_sph_n"])
+    e0 = eng_mod.GpuEngine(lv0)
+    reps = e0.batch_update((g["ids"][:5], g["rts"][:5]))
+    assert len(reps) == 5 and all(r.new_gray == 0 for r in reps)
+    assert len(e0.states()) == 0 and e0.unknown_count() == 0 and len(e0.gray_ids()) == 0
+    # one component: the first of the scenario, replayed against the reference's labels
+    lv1 = LayoutView(N=1, B=int(g["B"]), S=int(g["S"]), M=int(g["M"]), C=int(g["C"]),
+                     edge_sat=g["edge_sat"][:int(g["B"])], comp_aabb=g["comp_aabb"][:1],
+                     row_off=g["row_off"][:int(g["B"]) * int(g["S"]) + 1].astype(np.int32),
+                     segs=g["segs"][:int(g["row_off"][int(g["B"]) * int(g["S"])])], spline_r=g["spline_r"],
+                     obst_he=g["obst_he"], obst_sph_local=g["obst_sph_local"], obst_sph_r=g["obst_sph_r"],
+                     obst_sph_n=g["obst_sph_n"])
+    e1 = eng_mod.GpuEngine(lv1)
+    e1.batch_update((g["ids"], g["rts"]))
+    assert e1.states()[0] == g["snap_states"][-1][0]
+
+
+def test_no_obstacles(eng_mod):
+    """A roadmap without obstacles: every move id is unknown, labels stay GREEN."""
+    from paper_2603_28674_b200.engine import LayoutView
+
+    g = load_golden("scn_quick_smoke")
+    lv = LayoutView(N=int(g["N"]), B=int(g["B"]), S=int(g["S"]), M=0, C=1, edge_sat=g["edge_sat"],
+                    comp_aabb=g["comp_aabb"], row_off=g["row_off"].astype(np.int32), segs=g["segs"],
+                    spline_r=g["spline_r"], obst_he=np.zeros((0, 3)), obst_sph_local=np.zeros((0, 1, 3)),
+                    obst_sph_r=np.zeros(0), obst_sph_n=np.zeros(0, np.int32))
+    eng = eng_mod.GpuEngine(lv)
+    assert eng.batch_update([]) == []
+    with pytest.raises(ValueError, match="unknown obstacle id"):
+        eng.batch_update((np.zeros(1, np.int32), g["rts"][:1]))
+    assert not np.any(eng.states())
