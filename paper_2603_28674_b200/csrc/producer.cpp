@@ -8,6 +8,9 @@
 #include "../../include/rgg_build.h"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -468,6 +471,14 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                         const int32_t* edges, double eps, int32_t K, int32_t threads, int32_t flags,
                         rgg_built** out) {
     const bool keep_poses = (flags & RGG_BUILD_POSES) != 0;
+    static const bool dbg = std::getenv("RGG_DEBUG_PRODUCER") != nullptr;
+    auto t_mark = std::chrono::steady_clock::now();
+    const auto mark = [&](const char* what) {
+        if (!dbg) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[producer] %-14s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t_mark).count());
+        t_mark = t;
+    };
     const bool gpu_fit = (flags & RGG_BUILD_GPU_FIT) != 0;
     try {
         if (!out) throw std::invalid_argument("null output");
@@ -530,6 +541,7 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         work();
         for (auto& t : pool) t.join();
         if (failed) throw std::runtime_error(err);
+        mark("components");
         if (gpu_fit) {
             // obb_from_points of every component on the GPU (swept_gpu.cu), from the poses
             double cs[22];
@@ -551,16 +563,43 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
             }
         }
 
-        // ---- serialize (batch_layout.cpp:21-146)
+        mark("box fit");
+        // ---- serialize (batch_layout.cpp:21-146), components in parallel
+        const auto parallel = [&](int32_t n, auto&& fn) {  // fn(c) for c in [0, n) on the pool
+            std::atomic<int32_t> at{0};
+            std::string perr;
+            std::atomic<bool> pfail{false};
+            auto run = [&] {
+                try {
+                    for (int32_t c0; (c0 = at.fetch_add(1024)) < n && !pfail;)
+                        for (int32_t c = c0; c < std::min(n, c0 + 1024); ++c) fn(c);
+                } catch (const std::exception& ex) {
+                    if (!pfail.exchange(true)) perr = ex.what();
+                }
+            };
+            std::vector<std::thread> ts;
+            for (int i = 1; i < nt; ++i) ts.emplace_back(run);
+            run();
+            for (auto& t : ts) t.join();
+            if (pfail) throw std::logic_error(perr);
+        };
         rgg_built* L = new rgg_built();
         L->N = N;
         const int32_t nsph = static_cast<int32_t>(rb.spheres.size());
+        // splines per (component, sphere): the slots of sphere s are s*max_parts + 0, 1, ...
+        std::vector<std::atomic<int32_t>> sph_parts(std::max(nsph, 1));
+        for (auto& x : sph_parts) x = 0;
+        parallel(N, [&](int32_t c) {
+            thread_local std::vector<int32_t> parts;
+            parts.assign(std::max(nsph, 1), 0);
+            for (const Spline& sp : comps[c].under) {
+                const int32_t p = ++parts[sp.sphere];
+                for (int32_t cur = sph_parts[sp.sphere]; p > cur && !sph_parts[sp.sphere].compare_exchange_weak(cur, p);) {
+                }
+            }
+        });
         int32_t max_parts = 1;
-        std::vector<int32_t> parts(nsph);
-        for (const Comp& c : comps) {
-            std::fill(parts.begin(), parts.end(), 0);
-            for (const Spline& s : c.under) max_parts = std::max(max_parts, ++parts[s.sphere]);
-        }
+        for (int32_t k = 0; k < nsph; ++k) max_parts = std::max<int32_t>(max_parts, sph_parts[k]);
         const int32_t S = std::max(1, nsph) * max_parts;
         L->S = S;
         L->spline_r.assign(S, 0.0);
@@ -569,8 +608,11 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         L->obb15.resize(static_cast<size_t>(N) * 15);
         L->row_off.assign(static_cast<size_t>(N) * S + 1, 0);
         std::vector<int32_t> count(static_cast<size_t>(N) * S, 0);
-        std::vector<int32_t> slot_of;
-        for (int32_t c = 0; c < N; ++c) {
+        // a slot's spline radius is its sphere's (every spline of sphere s carries it, so the
+        // reference's consistency check, batch_layout.cpp:73-79, holds); unused slots stay 0
+        for (int32_t k = 0; k < nsph; ++k)
+            for (int32_t j = 0; j < sph_parts[k]; ++j) L->spline_r[k * max_parts + j] = rb.radius[k];
+        parallel(N, [&](int32_t c) {
             const Comp& cp = comps[c];
             V3 cs[8];
             corners_of(cp.over, cs);
@@ -592,14 +634,10 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                 const int32_t segc = std::max<int32_t>(1, static_cast<int32_t>(s.pts.size()) - 1);
                 if (segc > K) throw std::logic_error("spline exceeds the segment cap; the build policy should have split it");
                 const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
-                double& sr = L->spline_r[slot];
-                if (sr == 0.0)
-                    sr = s.radius;
-                else if (sr != s.radius)
-                    throw std::logic_error("inconsistent spline radius for a layout slot");
+                if (L->spline_r[slot] != s.radius) throw std::logic_error("inconsistent spline radius for a layout slot");
                 count[static_cast<size_t>(c) * S + slot] = segc;
             }
-        }
+        });
         int64_t total = 0;
         for (size_t r = 0; r < count.size(); ++r) {
             L->row_off[r] = static_cast<int32_t>(total);
@@ -607,7 +645,7 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         }
         L->row_off[count.size()] = static_cast<int32_t>(total);
         L->segs.resize(static_cast<size_t>(total) * 7);
-        for (int32_t c = 0; c < N; ++c) {
+        parallel(N, [&](int32_t c) {
             std::vector<int32_t> used(nsph, 0);
             for (const Spline& s : comps[c].under) {
                 const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
@@ -618,7 +656,7 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                     for (size_t p = 0; p + 1 < s.pts.size(); ++p) seg_prep(s.pts[p], s.pts[p + 1], dst + 7 * p);
                 }
             }
-        }
+        });
         if (keep_poses) {
             L->pose_off.assign(static_cast<size_t>(N) + 1, 0);
             for (int32_t c = 0; c < N; ++c)
@@ -632,6 +670,7 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                     d[9] = T.t.x, d[10] = T.t.y, d[11] = T.t.z;
                 }
         }
+        mark("serialize");
         *out = L;
         return 0;
     } catch (const std::exception& ex) {
