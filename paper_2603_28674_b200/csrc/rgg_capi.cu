@@ -336,7 +336,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // nodes of the graph, so a synchronous update is one graph launch and one wait
     const bool hostio = use_graph && (flags & kHostIO) != 0;
     // the apply kernel ends the update unless the gray list or an eager resolve follows:
-    // then its last CTA stores the counters into mapped host memory itself
+    // then one small kernel stores the counters into mapped host memory
     const bool out_in_kernel = hostio && !gray_list && !eager && rggk::split_pipeline();
     if (out_in_kernel) {
         b.out_mv = h->dh_mv;
@@ -372,6 +372,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[2]);
             if (e == cudaSuccess) e = rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
+            if (e == cudaSuccess && out_in_kernel) e = rggk::launch_host_out(b, h->stream);
             if (e == cudaSuccess && eager) e = resolve_hits();
             if (e == cudaSuccess) e = rec(h->ev[3]);
             if (e == cudaSuccess && gray_list)

@@ -1732,23 +1732,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
     if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
     if (full != 3 && !(s.dbg_flags & 8)) commit_grid(s, b);  // 8: ablation, no commit
-    if (b.out_ctr) {
-        // the last CTA to finish hands the counters to the host (mapped pinned memory),
-        // replacing two device-to-host copies after the kernel
-        __shared__ int s_last;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            s_last = atomicAdd(&b.ctr[11], 1) == static_cast<int>(gridDim.x) - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            for (int t = threadIdx.x; t < 4 * b.n; t += blockDim.x) b.out_mv[t] = __ldcg(b.mv + t);
-            for (int t = threadIdx.x; t < 24; t += blockDim.x) b.out_ctr[t] = __ldcg(b.ctr + t);
-        }
-    }
     tl_stop(b.tl, 4, t0);
+}
+
+// Synchronous host updates: the per-move counters and the status block straight
+// into mapped pinned host memory (one small PDL-launched kernel after apply,
+// instead of two device-to-host copies).
+__global__ void host_out_kernel(Batch b) {
+    pdl_wait();
+    for (int t = threadIdx.x; t < 4 * b.n; t += blockDim.x) b.out_mv[t] = b.mv[t];
+    for (int t = threadIdx.x; t < 24; t += blockDim.x) b.out_ctr[t] = b.ctr[t];
 }
 
 // --------------------------------------------------------------- compaction
@@ -1983,6 +1976,10 @@ static int pipeline() {
 }
 
 bool split_pipeline() { return pipeline() == 6; }
+
+cudaError_t launch_host_out(const Batch& b, cudaStream_t st) {
+    return launch_pdl(host_out_kernel, dim3(1), dim3(256), st, b);
+}
 
 // Eager batches run one single-move graph per move.  Between two graphs this
 // kernel saves move i-1's report terms (apply counters, resolved hits, resolve

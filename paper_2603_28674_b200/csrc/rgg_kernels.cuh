@@ -99,8 +99,8 @@ struct Batch {
     int32_t* unknown;      // running GRAY count, persistent across batches
     unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
     unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null
-    // host-mapped outputs (synchronous host updates): the apply kernel's last CTA
-    // stores the per-move counters (n*4) and ctr[0..23] there; null otherwise
+    // host-mapped outputs (synchronous host updates): launch_host_out stores the
+    // per-move counters (n*4) and ctr[0..23] there after the apply kernel
     int32_t* out_mv;
     int32_t* out_ctr;
 };
@@ -124,6 +124,7 @@ struct Resolver {
 };
 
 bool split_pipeline();  // RGG_PIPELINE == 6 (the default): touch / narrow / apply
+cudaError_t launch_host_out(const Batch& b, cudaStream_t st);  // counters -> b.out_mv / b.out_ctr
 // eager batches: save move i-1's report terms to rep[8(i-1)..], stage move i into slot 0
 cudaError_t launch_eager_step(const Batch& b, int32_t* ids0, double* rt0, const int32_t* st_ids, const double* st_rt,
                               int32_t* rep, int i, int k, cudaStream_t st);
