@@ -108,6 +108,7 @@ struct rgg_gpu {
     int32_t* h_mv = nullptr;   // mapped pinned (device view dh_mv)
     int32_t* h_ctr = nullptr;  // mapped pinned (device view dh_ctr)
     int32_t* dh_mv = nullptr;
+    int32_t* dh_ids = nullptr;  // device view of the mapped move staging (h_ids, then h_rt at pin_off)
     int32_t* dh_ctr = nullptr;
     // host mirrors
     std::vector<int32_t> orig;  // sorted -> id (owned)
@@ -212,7 +213,9 @@ int grow_pinned(rgg_gpu* h, int32_t n) {
     cudaFreeHost(h->h_ids);
     cudaFreeHost(h->h_mv);
     h->pin_off = ((static_cast<size_t>(cap) * 4 + 15) / 16) * 16;
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), h->pin_off + static_cast<size_t>(cap) * 96, 0));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ids), h->pin_off + static_cast<size_t>(cap) * 96,
+                     cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_ids), h->h_ids, 0));
     h->h_rt = reinterpret_cast<double*>(reinterpret_cast<char*>(h->h_ids) + h->pin_off);
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_mv), cap * 4 * sizeof(int32_t), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_mv), h->h_mv, 0));
@@ -342,6 +345,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         b.out_mv = h->dh_mv;
         b.out_ctr = h->dh_ctr;
     }
+    if (hostio) {  // the pose kernel reads the moves from the mapped staging buffer
+        b.src_ids = h->dh_ids;
+        b.src_rt = reinterpret_cast<const double*>(reinterpret_cast<const char*>(h->dh_ids) + h->pin_off);
+    }
     const int32_t key = kf | (b.census_on ? 64 : 0) | (phases ? 128 : 0) | (gray_list ? 256 : 0) | (eager ? 512 : 0) |
                         (hostio ? 1024 : 0) | ((flags & RGG_PER_MOVE) && hostio ? 2048 : 0);
     const auto resolve_hits = [&]() {
@@ -362,11 +369,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
                 return cudaEventRecordWithFlags(ev, h->stream, cudaEventRecordExternal);
             };
             CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-            cudaError_t e = cudaSuccess;
-            if (hostio)
-                e = cudaMemcpyAsync(h->d_ids, h->h_ids, h->in_off + static_cast<size_t>(n) * 96, cudaMemcpyHostToDevice,
-                                    h->stream);
-            if (e == cudaSuccess) e = rec(h->ev[0]);
+            cudaError_t e = rec(h->ev[0]);
             if (e == cudaSuccess) e = rggk::launch_pose(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[1]);
             if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);

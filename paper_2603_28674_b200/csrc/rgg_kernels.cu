@@ -165,21 +165,24 @@ __global__ void pose_kernel(Store s, Batch b) {
         if (lane == 0) *b.mtop = 0;
     }
     if (i >= b.n) return;
-    const int o = b.ids[i];
+    // moves straight from mapped host memory (synchronous host updates) or from HBM
+    const int32_t* mids = b.src_ids ? b.src_ids : b.ids;
+    const double* mrt = b.src_ids ? b.src_rt : b.rt;
+    const int o = mids[i];
     // prev / last links: the same obstacle moved earlier / later in this batch
     int p = -1;
     bool is_last = true;
     for (int base = 0; base < b.n; base += 32) {
         const int j = base + lane;
-        const bool same = j < b.n && b.ids[j] == o;
+        const bool same = j < b.n && mids[j] == o;
         const unsigned before = __ballot_sync(0xffffffffu, same && j < i);
         const unsigned after = __ballot_sync(0xffffffffu, same && j > i);
         if (before) p = base + 31 - __clz(before);
         if (after) is_last = false;
     }
     const double he[3] = {s.ohe[3 * o], s.ohe[3 * o + 1], s.ohe[3 * o + 2]};
-    const double* rt_new = b.rt + 12 * static_cast<size_t>(i);
-    const double* rt_old = p >= 0 ? b.rt + 12 * static_cast<size_t>(p) : rt_new;
+    const double* rt_new = mrt + 12 * static_cast<size_t>(i);
+    const double* rt_old = p >= 0 ? mrt + 12 * static_cast<size_t>(p) : rt_new;
     const double* rt = lane < 8 ? rt_new : (lane < 16 ? rt_old : rt_new);
     double rtl[12];
 #pragma unroll
@@ -317,7 +320,11 @@ __global__ void pose_kernel(Store s, Batch b) {
         double* et = b.evt + 24 * static_cast<size_t>(i);
         et[lane] = nu, et[6 + lane] = ol, et[12 + lane] = bn[lane], et[18 + lane] = bs[lane];
     }
-    if (lane < 12) ev.rt[lane] = b.rt[12 * static_cast<size_t>(i) + lane];
+    if (lane < 12) ev.rt[lane] = rt_new[lane];
+    if (b.src_ids) {  // the HBM copy the later kernels (and a replay) read
+        if (lane == 0) const_cast<int32_t*>(b.ids)[i] = o;
+        if (lane < 12) const_cast<double*>(b.rt)[12 * static_cast<size_t>(i) + lane] = rt_new[lane];
+    }
     if (lane >= 16 && lane - 16 < nsph) {
         ev.cen[3 * (lane - 16)] = pt[0];
         ev.cen[3 * (lane - 16) + 1] = pt[1];

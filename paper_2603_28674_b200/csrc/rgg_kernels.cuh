@@ -103,6 +103,10 @@ struct Batch {
     // per-move counters (n*4) and ctr[0..23] there after the apply kernel
     int32_t* out_mv;
     int32_t* out_ctr;
+    // host-mapped inputs (synchronous host updates): the pose kernel reads the moves
+    // there and copies them to ids / rt; null when the moves are already in HBM
+    const int32_t* src_ids;
+    const double* src_rt;
 };
 
 // Exact resolve operands (rgg_resolve.cu).
