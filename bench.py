@@ -390,6 +390,7 @@ def main():
     for it in range(args.warmup):
         step_device(it)
     torch.cuda.synchronize()
+    eng.filter_stats(reset=True)
     if dist is not None:
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -404,12 +405,16 @@ def main():
             ev[k][1].record(tstream)
         torch.cuda.synchronize()
         # keep the same load under the sampler for >= 1 s so clocks are observed under load
+        n_updates = args.steps  # updates behind the filter counters below
         while time.perf_counter() - t_clock0 < args.clock_window_s:
             step_device(args.warmup + (args.steps - 1))
             torch.cuda.synchronize()
+            n_updates += 1
     if up is not None:
         up.check()  # device-side errors of the stream-ordered updates
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    # the fp32 filters' undecided pairs (re-tested exactly) over the timed steps plus the clock window
+    fstats = eng.filter_stats(reset=True)
     # phase split (untimed): the same last steps again with per-kernel events
     eng.set_phase_timing(True)
     for k in range(min(5, args.steps)):
@@ -517,6 +522,10 @@ def main():
                           ("pose_ms", "bin_ms", "classify_ms", "compact_ms", "total_ms")},
         "dirty_cells_mean": statistics.mean(s["dirty_cells"] for s in stats),
         "roofline": roof, "clocks": clk.summary(),
+        "parity": {"mismatches_vs_reference": None, "eps_band": "none: fp32-filter-undecided pairs are re-tested with the "
+                   "reference's fp64 sequence", "filter_rechecks_per_update": {k: v / n_updates for k, v in fstats.items()},
+                   "over_pairs_per_update": census["over_pairs"],
+                   "seg_sphere_tests_per_update": census["seg_sphere_tests"]},
     }
     if world == 1 and args.extra_configs and args.config == "c2":
         line["extra"] = {}
@@ -532,9 +541,16 @@ def main():
             line["resolve"] = {"error": str(ex)[:200]}
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        n, done, spent, per_step, _ = cpu_reference_run(args.config, args.seed, iterations, args.cpu_sample_s,
-                                                        threads)
+        n, done, spent, per_step, ref_eng = cpu_reference_run(args.config, args.seed, iterations,
+                                                              args.cpu_sample_s, threads)
         cpu_v = n * done / spent
+        # label parity on the full c2 tile: a fresh engine, the same `done` updates, every label compared
+        eng_chk = E.GpuEngine(lv, device=local)
+        for it in range(done):
+            eng_chk.batch_update((ids_h[it], rts_h[it]), per_move=False)
+        line["parity"]["mismatches_vs_reference"] = int(np.sum(eng_chk.states() != ref_eng.states()))
+        line["parity"]["checked"] = f"{n} labels after {done} updates against rgg::BatchEngine"
+        del eng_chk
         line["cpu_baseline"] = {"value": cpu_v, "unit": "edges/s", "cores": threads, "kind": "reference",
                                 "sample": f"rgg::BatchEngine (AVX2, {threads} threads) on the same tile-0 roadmap "
                                           f"and moves: {done} updates x 64 moves in {spent:.1f} s",

@@ -187,6 +187,10 @@ typedef struct rgg_gpu_stats {
 int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out);
 /* Full-roadmap census against all active obstacles (one untimed launch). */
 int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out);
+/* Pairs the fp32 filters could not decide and the exact fp64 sequence re-tested
+ * (SAT, segment-sphere), summed over every handle of this process since the last
+ * reset.  The verdicts are exact either way; this is the filters' "epsilon band". */
+int rgg_gpu_filter_stats(rgg_gpu* h, int64_t* sat_rechecks, int64_t* seg_rechecks, int32_t reset);
 /* The CUDA stream the engine launches on (cudaStream_t), for event timing. */
 void* rgg_gpu_stream(rgg_gpu* h);
 /* Measured non-FMA fp64 add/mul rate of `device` in GFLOP/s (the compute roof

@@ -1048,6 +1048,17 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
     return RGG_OK;
 }
 
+int rgg_gpu_filter_stats(rgg_gpu* h, int64_t* sat_rechecks, int64_t* seg_rechecks, int32_t reset) {
+    if (!h) return RGG_EINVAL;
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    unsigned long long fs[4] = {0, 0, 0, 0};
+    rggk::filter_stats(fs, reset != 0);
+    if (sat_rechecks) *sat_rechecks = static_cast<int64_t>(fs[1]);
+    if (seg_rechecks) *seg_rechecks = static_cast<int64_t>(fs[3]);
+    return RGG_OK;
+}
+
 int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* v) {
     if (!h || !v) return RGG_EINVAL;
     clear_stale_error();

@@ -118,6 +118,7 @@ def library() -> C.CDLL:
         L.rgg_gpu_set_resolver.argtypes = [vp, C.POINTER(_ResolveView)]
         L.rgg_gpu_resolve_all.argtypes = [vp, ip]
         L.rgg_gpu_exact_check.argtypes = [vp, vp, i32, vp]
+        L.rgg_gpu_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), i32]
         _lib = L
     return _lib
 
@@ -152,7 +153,7 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
             "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
-            "rgg_gpu_exact_check"]
+            "rgg_gpu_exact_check", "rgg_gpu_filter_stats"]
 
 
 @dataclass
@@ -388,6 +389,12 @@ class GpuEngine:
         n = C.c_int32(0)
         self._check(library().rgg_gpu_resolve_all(self._h, C.byref(n)))
         return n.value
+
+    def filter_stats(self, reset: bool = False) -> dict:
+        """Pairs the fp32 filters left undecided and fp64 re-tested (process-wide)."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(library().rgg_gpu_filter_stats(self._h, C.byref(a), C.byref(b), int(reset)))
+        return {"sat_rechecks": a.value, "seg_rechecks": b.value}
 
     def exact_check(self, ids) -> np.ndarray:
         """exact_component_valid (roadmap.cpp:129-163) of ids: uint8 GREEN (free) / RED."""
