@@ -19,8 +19,12 @@
 #include <thread>
 #include <vector>
 
-extern "C" int rggp_fit_boxes_gpu(const double* poses, const int64_t* off, int32_t ncomp, const double* he3,
-                                  const double* cos_sin, int32_t device, double* out);
+extern "C" void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin,
+                                int64_t chunk_configs, int32_t device);
+extern "C" double* rggp_fit_staging(void* fs, int32_t slot);
+extern "C" int rggp_fit_push(void* fs, int32_t slot, int64_t first_config, int64_t nconfigs);
+extern "C" int rggp_fit_finish(void* fs, double* out);
+extern "C" void rggp_fit_end(void* fs);
 
 
 namespace {
@@ -499,60 +503,81 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                 *b = nodes + 6 * static_cast<size_t>(edges[2 * e + 1]);
             }
         };
-        // gpu_fit: every component's poses go straight into one buffer (pageable: pinning
-        // the ~100 B per configuration costs more than the copy it would speed up)
-        std::vector<int64_t> pose_off;
-        std::vector<double> pose_buf;
-        double* poses = nullptr;
-        if (gpu_fit) {
-            pose_off.assign(static_cast<size_t>(N) + 1, 0);
+        int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+        nt = std::max(1, std::min(nt, 256));
+        // components [c_lo, c_hi) on the pool; gpu_fit: poses into `stage` from configuration `cfg0`
+        const auto run_components = [&](int32_t c_lo, int32_t c_hi, double* stage, const int64_t* pose_off,
+                                        int64_t cfg0) {
+            std::atomic<int32_t> next{c_lo};
+            std::string err;
+            std::atomic<bool> failed{false};
+            auto work = [&] {
+                try {
+                    for (;;) {
+                        const int32_t c0 = next.fetch_add(256);
+                        if (c0 >= c_hi || failed) break;
+                        for (int32_t c = c0; c < std::min(c_hi, c0 + 256); ++c) {
+                            const double *a, *b;
+                            ends(c, &a, &b);
+                            comps[c] = build_comp(rb, a, b, eps, K, keep_poses, gpu_fit,
+                                                  stage ? stage + 12 * static_cast<size_t>(pose_off[c] - cfg0) : nullptr);
+                        }
+                    }
+                } catch (const std::exception& ex) {
+                    if (!failed.exchange(true)) err = ex.what();
+                }
+            };
+            std::vector<std::thread> pool;
+            for (int i = 1; i < nt; ++i) pool.emplace_back(work);
+            work();
+            for (auto& t : pool) t.join();
+            if (failed) throw std::runtime_error(err);
+        };
+        void* fit = nullptr;
+        if (!gpu_fit) {
+            run_components(0, N, nullptr, nullptr, 0);
+        } else {
+            // the poses stream to the GPU in chunks of <= kChunk configurations through two
+            // pinned buffers: a chunk's copy overlaps the production of the next
+            constexpr int64_t kChunk = 1 << 19;
+            std::vector<int64_t> pose_off(static_cast<size_t>(N) + 1, 0);
             for (int32_t c = 0; c < N; ++c) {
                 const double *a, *b;
                 ends(c, &a, &b);
                 pose_off[c + 1] = pose_off[c] + config_count(a, b, eps);
             }
-            pose_buf.resize(static_cast<size_t>(pose_off[N]) * 12);
-            poses = pose_buf.data();
-        }
-        int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
-        nt = std::max(1, std::min(nt, 256));
-        std::atomic<int32_t> next{0};
-        std::string err;
-        std::atomic<bool> failed{false};
-        auto work = [&] {
-            try {
-                for (;;) {
-                    const int32_t c0 = next.fetch_add(256);
-                    if (c0 >= N || failed) break;
-                    for (int32_t c = c0; c < std::min(N, c0 + 256); ++c) {
-                        const double *a, *b;
-                        ends(c, &a, &b);
-                        comps[c] = build_comp(rb, a, b, eps, K, keep_poses, gpu_fit,
-                                              gpu_fit ? poses + 12 * static_cast<size_t>(pose_off[c]) : nullptr);
-                    }
-                }
-            } catch (const std::exception& ex) {
-                failed = true;
-                err = ex.what();
-            }
-        };
-        std::vector<std::thread> pool;
-        for (int i = 1; i < nt; ++i) pool.emplace_back(work);
-        work();
-        for (auto& t : pool) t.join();
-        if (failed) throw std::runtime_error(err);
-        mark("components");
-        if (gpu_fit) {
-            // obb_from_points of every component on the GPU (swept_gpu.cu), from the poses
             double cs[22];
             constexpr double kStep = 3.0 * 3.141592653589793 / 180.0;
             for (int step = -5; step <= 5; ++step) {
                 cs[2 * (step + 5)] = std::cos(step * kStep);
                 cs[2 * (step + 5) + 1] = std::sin(step * kStep);
             }
+            int64_t max_chunk = 0;
+            for (int32_t c = 0; c < N; ++c) max_chunk = std::max(max_chunk, pose_off[c + 1] - pose_off[c]);
+            fit = rggp_fit_begin(pose_off.data(), N, he3, cs, std::max(kChunk, max_chunk), 0);
+            if (!fit) throw std::runtime_error("GPU box fit: CUDA initialisation failed");
+            try {
+                int slot = 0;
+                for (int32_t c_lo = 0; c_lo < N; slot ^= 1) {
+                    int32_t c_hi = c_lo + 1;
+                    while (c_hi < N && pose_off[c_hi + 1] - pose_off[c_lo] <= std::max(kChunk, max_chunk)) ++c_hi;
+                    double* stage = rggp_fit_staging(fit, slot);
+                    if (!stage) throw std::runtime_error("GPU box fit: staging failed");
+                    run_components(c_lo, c_hi, stage, pose_off.data(), pose_off[c_lo]);
+                    if (rggp_fit_push(fit, slot, pose_off[c_lo], pose_off[c_hi] - pose_off[c_lo]) != 0)
+                        throw std::runtime_error("GPU box fit: copy failed");
+                    c_lo = c_hi;
+                }
+            } catch (...) {
+                rggp_fit_end(fit);
+                throw;
+            }
+        }
+        mark("components");
+        if (gpu_fit) {
+            // obb_from_points of every component on the GPU (swept_gpu.cu), from the streamed poses
             std::vector<double> boxes(static_cast<size_t>(N) * 15);
-            const int rc = rggp_fit_boxes_gpu(poses, pose_off.data(), N, he3, cs, 0, boxes.data());
-            std::vector<double>().swap(pose_buf);
+            const int rc = rggp_fit_finish(fit, boxes.data());
             if (rc != 0) throw std::runtime_error("GPU box fit failed (CUDA error " + std::to_string(rc) + ")");
             for (int32_t c = 0; c < N; ++c) {
                 const double* o = &boxes[15 * static_cast<size_t>(c)];

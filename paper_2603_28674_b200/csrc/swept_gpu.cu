@@ -11,6 +11,7 @@
 // candidate angles come from the host's libm.
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -163,40 +164,101 @@ __global__ void fit_kernel(const double* poses, const int64_t* off, int ncomp, V
 
 }  // namespace
 
-// poses: total x 12 doubles (host), off: ncomp+1, cos_sin: cos/sin of step*3 deg for step = -5..5
-// (index step+5), out: ncomp x 15 doubles (host).  Returns a cudaError_t value.
-extern "C" int rggp_fit_boxes_gpu(const double* poses, const int64_t* off, int32_t ncomp, const double* he3,
-                                  const double* cos_sin, int32_t device, double* out) {
-    cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) return e;
-    const size_t total = static_cast<size_t>(off[ncomp]);
-    double *dp = nullptr, *dcs = nullptr, *dout = nullptr;
+// Streamed fit: the host produces the poses chunk by chunk into two pinned
+// staging buffers; each chunk's copy runs while the next one is produced, and one
+// fit kernel runs at the end over the poses resident on the device.
+struct FitStream {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    double* dp = nullptr;         // all poses, device
     int64_t* doff = nullptr;
-    if ((e = cudaMalloc(&dp, (total ? total : 1) * 96)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&doff, (static_cast<size_t>(ncomp) + 1) * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&dcs, 22 * 8)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&dout, (static_cast<size_t>(ncomp) + 1) * 15 * 8)) != cudaSuccess) return e;
-    e = cudaMemcpy(dp, poses, total * 96, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(doff, off, (static_cast<size_t>(ncomp) + 1) * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(dcs, cos_sin, 22 * 8, cudaMemcpyHostToDevice);
-    cudaEvent_t ev0, ev1;
-    cudaEventCreate(&ev0);
-    cudaEventCreate(&ev1);
-    cudaEventRecord(ev0);
-    if (e == cudaSuccess && ncomp > 0) {
-        fit_kernel<<<(ncomp + 127) / 128, 128>>>(dp, doff, ncomp, V3{he3[0], he3[1], he3[2]}, dcs, dout);
+    double* dcs = nullptr;
+    double* dout = nullptr;
+    double* stage[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    int32_t ncomp = 0;
+    double he[3] = {0, 0, 0};
+};
+
+extern "C" void rggp_fit_end(void* p) {
+    FitStream* f = static_cast<FitStream*>(p);
+    if (!f) return;
+    cudaSetDevice(f->device);
+    if (f->st) cudaStreamSynchronize(f->st);
+    cudaFree(f->dp), cudaFree(f->doff), cudaFree(f->dcs), cudaFree(f->dout);
+    for (int k = 0; k < 2; ++k) {
+        if (f->stage[k]) cudaFreeHost(f->stage[k]);
+        if (f->done[k]) cudaEventDestroy(f->done[k]);
+    }
+    if (f->st) cudaStreamDestroy(f->st);
+    delete f;
+}
+
+// chunk_configs: capacity of each staging buffer (configurations)
+extern "C" void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin,
+                                int64_t chunk_configs, int32_t device) {
+    FitStream* f = new FitStream();
+    f->device = device;
+    f->ncomp = ncomp;
+    for (int k = 0; k < 3; ++k) f->he[k] = he3[k];
+    const size_t total = static_cast<size_t>(off[ncomp]);
+    bool ok = cudaSetDevice(device) == cudaSuccess && cudaStreamCreateWithFlags(&f->st, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMalloc(&f->dp, (total ? total : 1) * 96) == cudaSuccess &&
+              cudaMalloc(&f->doff, (static_cast<size_t>(ncomp) + 1) * 8) == cudaSuccess &&
+              cudaMalloc(&f->dcs, 22 * 8) == cudaSuccess &&
+              cudaMalloc(&f->dout, (static_cast<size_t>(ncomp) + 1) * 15 * 8) == cudaSuccess;
+    for (int k = 0; ok && k < 2; ++k)
+        ok = cudaHostAlloc(reinterpret_cast<void**>(&f->stage[k]), static_cast<size_t>(chunk_configs) * 96, 0) == cudaSuccess &&
+             cudaEventCreateWithFlags(&f->done[k], cudaEventDisableTiming) == cudaSuccess && cudaEventRecord(f->done[k], f->st) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(f->doff, off, (static_cast<size_t>(ncomp) + 1) * 8, cudaMemcpyHostToDevice, f->st) == cudaSuccess &&
+         cudaMemcpyAsync(f->dcs, cos_sin, 22 * 8, cudaMemcpyHostToDevice, f->st) == cudaSuccess &&
+         cudaStreamSynchronize(f->st) == cudaSuccess;
+    if (!ok) {
+        rggp_fit_end(f);
+        return nullptr;
+    }
+    return f;
+}
+
+// the staging buffer of a slot, once its previous copy has drained
+extern "C" double* rggp_fit_staging(void* p, int32_t slot) {
+    FitStream* f = static_cast<FitStream*>(p);
+    return cudaEventSynchronize(f->done[slot]) == cudaSuccess ? f->stage[slot] : nullptr;
+}
+
+// queue the copy of a slot's nconfigs poses to configuration first_config
+extern "C" int rggp_fit_push(void* p, int32_t slot, int64_t first_config, int64_t nconfigs) {
+    FitStream* f = static_cast<FitStream*>(p);
+    cudaError_t e = cudaMemcpyAsync(f->dp + 12 * first_config, f->stage[slot], static_cast<size_t>(nconfigs) * 96,
+                                    cudaMemcpyHostToDevice, f->st);
+    if (e == cudaSuccess) e = cudaEventRecord(f->done[slot], f->st);
+    return e;
+}
+
+// fit every component, boxes to out (ncomp x 15), release everything
+extern "C" int rggp_fit_finish(void* p, double* out) {
+    FitStream* f = static_cast<FitStream*>(p);
+    static const bool dbg = std::getenv("RGG_DEBUG_FIT") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    const auto mark = [&](const char* what) {
+        if (!dbg) return;
+        cudaStreamSynchronize(f->st);
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[fit] %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
+    mark("copies");
+    cudaError_t e = cudaSuccess;
+    if (f->ncomp > 0) {
+        fit_kernel<<<(f->ncomp + 127) / 128, 128, 0, f->st>>>(f->dp, f->doff, f->ncomp, V3{f->he[0], f->he[1], f->he[2]},
+                                                              f->dcs, f->dout);
         e = cudaGetLastError();
     }
-    cudaEventRecord(ev1);
-    if (std::getenv("RGG_DEBUG_FIT")) {
-        float ms = 0;
-        cudaEventSynchronize(ev1);
-        cudaEventElapsedTime(&ms, ev0, ev1);
-        std::fprintf(stderr, "[fit] %d components, %zu poses: kernel %.2f ms\n", ncomp, total, ms);
-    }
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    if (e == cudaSuccess) e = cudaMemcpy(out, dout, static_cast<size_t>(ncomp) * 15 * 8, cudaMemcpyDeviceToHost);
-    cudaFree(dp), cudaFree(doff), cudaFree(dcs), cudaFree(dout);
+    mark("kernel");
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(out, f->dout, static_cast<size_t>(f->ncomp) * 15 * 8, cudaMemcpyDeviceToHost, f->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(f->st);
+    mark("boxes D2H");
+    rggp_fit_end(f);
     return e;
 }
