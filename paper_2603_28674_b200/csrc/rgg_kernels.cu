@@ -684,7 +684,6 @@ __device__ __forceinline__ void prefetch_range(const void* a, const void* e, boo
 
 constexpr int kUnderLanes = 4;  // lanes per under-approximation work item
 constexpr int kStageEv = 128;   // touch stages a whole batch of up to this many events per CTA
-constexpr int kOverLanes = 1;   // lanes per SAT work item (4 was slower: operands re-read per lane)
 
 // ------------------------------------------------------- v3: touch / narrow / apply
 //
@@ -730,22 +729,6 @@ __device__ __noinline__ bool under_inline(const Store& s, int c, const Event& ev
     return under_part<false>(s, c, ev, 0, 1, nullptr);
 }
 
-// Warp-aggregated append of n items (lane-local count) to a global queue;
-// returns this lane's first slot.
-__device__ __forceinline__ int warp_reserve(int32_t* counter, int n) {
-    const int lane = threadIdx.x & 31;
-    int x = n;
-    for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, off);
-        if (lane >= off) x += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, x, 31);
-    int base = 0;
-    if (lane == 31 && total) base = atomicAdd(counter, total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    return base + x - n;
-}
-
 __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
     __shared__ double sbox[kEvChunk][24];  // nu, old, box, sph of the chunk's events
     __shared__ int sev[kEvChunk];
@@ -761,7 +744,6 @@ __global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
     const int32_t* list = rec_list(rec);
     const int W = (count + 31) >> 5, T = s.cell;
     const int mbase = rec.y;
-    uint32_t* mb = b.mpool + mbase;
     const int c = cell * T + tid;
     const bool valid = c < s.Np;
     double aabb[6];
@@ -1386,11 +1368,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
             for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
             if (lane == 0 && x) atomicAdd(&b.census[k < 6 ? k : k + 2], static_cast<unsigned long long>(x));
         }
-        return;
+    } else {
+        // running gray count (the unknown_count of the reference)
+        for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
+        if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
     }
-    // running gray count (the unknown_count of the reference)
-    for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
-    if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
 }
 
 // ------------------------------------------------- v6: warp-slice touch / GPU-wide narrow / warp-slice apply
