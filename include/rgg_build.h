@@ -31,6 +31,9 @@ int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nod
 #define RGG_BUILD_POSES 1
 /* fit the swept-volume boxes (obb_from_points) on the GPU, bit-identical (device 0) */
 #define RGG_BUILD_GPU_FIT 2
+/* also the inner approximation (spline simplification) on the GPU, bit-identical (device 0);
+ * slower end to end than RGG_BUILD_GPU_FIT alone while serialize stays on the host */
+#define RGG_BUILD_GPU_INNER 4
 int rgg_build_layout_ex(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
                         const int32_t* edges, double eps, int32_t max_segments, int32_t threads, int32_t flags,
                         rgg_built** out);

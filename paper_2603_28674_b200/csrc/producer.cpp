@@ -19,12 +19,7 @@
 #include <thread>
 #include <vector>
 
-extern "C" void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin,
-                                int64_t chunk_configs, int32_t device);
-extern "C" double* rggp_fit_staging(void* fs, int32_t slot);
-extern "C" int rggp_fit_push(void* fs, int32_t slot, int64_t first_config, int64_t nconfigs);
-extern "C" int rggp_fit_finish(void* fs, double* out);
-extern "C" void rggp_fit_end(void* fs);
+#include "swept_gpu.h"
 
 
 namespace {
@@ -385,7 +380,7 @@ int config_count(const double* a, const double* b, double eps) {
 
 // pose_out (gpu_fit): the component's forward-kinematics poses, 12 doubles each
 Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K, bool keep_poses, bool gpu_fit,
-                double* pose_out) {
+                bool gpu_inner, double* pose_out) {
     // discretize_edge (robot.cpp:39-64)
     double len2 = 0.0;
     for (int i = 0; i < 6; ++i) {
@@ -428,6 +423,10 @@ Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, i
         cloud.insert(cloud.end(), cs, cs + 8);
     }
     comp.over = fit_box(cloud);
+    }
+    if (gpu_inner) {  // the inner approximation runs on the GPU too
+        if (keep_poses) comp.fk = std::move(fk);
+        return comp;
     }
     // build_inner_approx (swept.cpp:188-228)
     for (size_t si = 0; si < rb.spheres.size(); ++si) {
@@ -483,7 +482,8 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         std::fprintf(stderr, "[producer] %-14s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - t_mark).count());
         t_mark = t;
     };
-    const bool gpu_fit = (flags & RGG_BUILD_GPU_FIT) != 0;
+    const bool gpu_fit = (flags & (RGG_BUILD_GPU_FIT | RGG_BUILD_GPU_INNER)) != 0;
+    const bool gpu_inner = (flags & RGG_BUILD_GPU_INNER) != 0;
     try {
         if (!out) throw std::invalid_argument("null output");
         if (!(eps > 0)) throw std::invalid_argument("resolution must be positive");
@@ -505,6 +505,24 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         };
         int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
         nt = std::max(1, std::min(nt, 256));
+        const auto parallel = [&](int32_t n, auto&& fn) {  // fn(c) for c in [0, n) on the pool
+            std::atomic<int32_t> at{0};
+            std::string perr;
+            std::atomic<bool> pfail{false};
+            auto run = [&] {
+                try {
+                    for (int32_t c0; (c0 = at.fetch_add(1024)) < n && !pfail;)
+                        for (int32_t c = c0; c < std::min(n, c0 + 1024); ++c) fn(c);
+                } catch (const std::exception& ex) {
+                    if (!pfail.exchange(true)) perr = ex.what();
+                }
+            };
+            std::vector<std::thread> ts;
+            for (int i = 1; i < nt; ++i) ts.emplace_back(run);
+            run();
+            for (auto& t : ts) t.join();
+            if (pfail) throw std::logic_error(perr);
+        };
         // components [c_lo, c_hi) on the pool; gpu_fit: poses into `stage` from configuration `cfg0`
         const auto run_components = [&](int32_t c_lo, int32_t c_hi, double* stage, const int64_t* pose_off,
                                         int64_t cfg0) {
@@ -519,7 +537,7 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                         for (int32_t c = c0; c < std::min(c_hi, c0 + 256); ++c) {
                             const double *a, *b;
                             ends(c, &a, &b);
-                            comps[c] = build_comp(rb, a, b, eps, K, keep_poses, gpu_fit,
+                            comps[c] = build_comp(rb, a, b, eps, K, keep_poses, gpu_fit, gpu_inner,
                                                   stage ? stage + 12 * static_cast<size_t>(pose_off[c] - cfg0) : nullptr);
                         }
                     }
@@ -577,8 +595,42 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         if (gpu_fit) {
             // obb_from_points of every component on the GPU (swept_gpu.cu), from the streamed poses
             std::vector<double> boxes(static_cast<size_t>(N) * 15);
-            const int rc = rggp_fit_finish(fit, boxes.data());
+            InnerSpec spec;
+            spec.nsph = static_cast<int32_t>(rb.spheres.size());
+            spec.K = K;
+            for (size_t si = 0; si < rb.spheres.size(); ++si) {
+                spec.centre.insert(spec.centre.end(), {rb.spheres[si].c.x, rb.spheres[si].c.y, rb.spheres[si].c.z});
+                spec.radius.push_back(rb.radius[si]);
+                spec.step_bound.push_back(rb.lipschitz[si] * eps);
+                spec.tol.push_back(rb.tol[si]);
+            }
+            InnerOut inner;
+            const int rc = rggp_fit_finish(fit, boxes.data(), gpu_inner ? &spec : nullptr, &inner);
             if (rc != 0) throw std::runtime_error("GPU box fit failed (CUDA error " + std::to_string(rc) + ")");
+            // the splines, component by component (build_comp's order: spheres, then cap_split's)
+            const int32_t nsph = gpu_inner ? spec.nsph : 0;
+            std::vector<int64_t> so(static_cast<size_t>(N) + 1, 0), po(static_cast<size_t>(N) + 1, 0);
+            {
+                int64_t k = 0;
+                for (int32_t c = 0; c < N; ++c) {
+                    int64_t pts = 0;
+                    for (int32_t si = 0; si < nsph; ++si)
+                        for (int32_t q = 0; q < inner.nspl[static_cast<size_t>(c) * nsph + si]; ++q) pts += inner.npts[k++];
+                    so[c + 1] = k;
+                    po[c + 1] = po[c] + pts;
+                }
+            }
+            parallel(N, [&](int32_t c) {
+                int64_t k = so[c], p = po[c];
+                for (int32_t si = 0; si < nsph; ++si)
+                    for (int32_t q = 0; q < inner.nspl[static_cast<size_t>(c) * nsph + si]; ++q, ++k) {
+                        Spline sp{{}, rb.radius[si], si};
+                        sp.pts.reserve(inner.npts[k]);
+                        for (int32_t j = 0; j < inner.npts[k]; ++j, ++p)
+                            sp.pts.push_back({inner.pts[3 * p], inner.pts[3 * p + 1], inner.pts[3 * p + 2]});
+                        comps[c].under.push_back(std::move(sp));
+                    }
+            });
             for (int32_t c = 0; c < N; ++c) {
                 const double* o = &boxes[15 * static_cast<size_t>(c)];
                 Box& bx = comps[c].over;
@@ -590,24 +642,6 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
 
         mark("box fit");
         // ---- serialize (batch_layout.cpp:21-146), components in parallel
-        const auto parallel = [&](int32_t n, auto&& fn) {  // fn(c) for c in [0, n) on the pool
-            std::atomic<int32_t> at{0};
-            std::string perr;
-            std::atomic<bool> pfail{false};
-            auto run = [&] {
-                try {
-                    for (int32_t c0; (c0 = at.fetch_add(1024)) < n && !pfail;)
-                        for (int32_t c = c0; c < std::min(n, c0 + 1024); ++c) fn(c);
-                } catch (const std::exception& ex) {
-                    if (!pfail.exchange(true)) perr = ex.what();
-                }
-            };
-            std::vector<std::thread> ts;
-            for (int i = 1; i < nt; ++i) ts.emplace_back(run);
-            run();
-            for (auto& t : ts) t.join();
-            if (pfail) throw std::logic_error(perr);
-        };
         rgg_built* L = new rgg_built();
         L->N = N;
         const int32_t nsph = static_cast<int32_t>(rb.spheres.size());

@@ -11,8 +11,11 @@
 // candidate angles come from the host's libm.
 #include <cuda_runtime.h>
 
+#include "swept_gpu.h"
+
 #include <chrono>
 #include <cstdint>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 
@@ -162,6 +165,111 @@ __global__ void fit_kernel(const double* poses, const int64_t* off, int ncomp, V
     o[12] = (hi[0] - lo[0]) * 0.5, o[13] = (hi[1] - lo[1]) * 0.5, o[14] = (hi[2] - lo[2]) * 0.5;
 }
 
+// ---- inner approximation (swept.cpp:188-228: build_inner_approx + simplify :79-92
+// + cap_segments :125-162), one thread per (component, sphere), as producer.cpp
+
+__device__ inline double point_seg_dist(V3 a, V3 b, V3 c) {
+    const double s3 = b.x - a.x, s4 = b.y - a.y, s5 = b.z - a.z;
+    const double s6 = (s3 * s3 + s4 * s4) + s5 * s5;
+    const double px = c.x - a.x, py = c.y - a.y, pz = c.z - a.z;
+    double t = 0.0;
+    if (s6 > 0.0) {
+        t = ((px * s3 + py * s4) + pz * s5) / s6;
+        t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    }
+    const double qx = px - t * s3, qy = py - t * s4, qz = pz - t * s5;
+    return sqrt((qx * qx + qy * qy) + qz * qz);
+}
+
+__device__ inline bool covers(const V3* pts, int j, int p, double radius) {
+    for (int m = j + 1; m < p; ++m)
+        if (!(point_seg_dist(pts[j], pts[p], pts[m]) < radius)) return false;
+    return true;
+}
+
+struct InnerDev {
+    int nsph, K;
+    const double *centre, *radius, *step, *tol;
+};
+
+// COUNT: nspl / npts_total per (component, sphere); else write the spline sizes and points
+template <bool COUNT>
+__global__ void inner_kernel(const double* poses, const int64_t* off, int ncomp, InnerDev sp, V3* raw_scr,
+                             int32_t* kept_scr, int32_t* nspl, int32_t* npts_total, const int64_t* spl_off,
+                             const int64_t* pt_off, int32_t* spl_npts, double* pts) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<long long>(ncomp) * sp.nsph) return;
+    const int c = static_cast<int>(t / sp.nsph), si = static_cast<int>(t % sp.nsph);
+    const int n = static_cast<int>(off[c + 1] - off[c]);
+    int ns = 0, np = 0;
+    const double rad = sp.radius[si];
+    if (rad > 0.0) {
+        V3* raw = raw_scr + off[c] * sp.nsph + static_cast<long long>(si) * n;
+        int32_t* kept = kept_scr + off[c] * sp.nsph + static_cast<long long>(si) * n;
+        const V3 sc{sp.centre[3 * si], sp.centre[3 * si + 1], sp.centre[3 * si + 2]};
+        int nr = 0;
+        bool step_ok = true;
+        for (int q = 0; q < n; ++q) {
+            const double* T = poses + 12 * static_cast<size_t>(off[c] + q);
+            const V3 p{T[0] * sc.x + T[1] * sc.y + T[2] * sc.z + T[9], T[3] * sc.x + T[4] * sc.y + T[5] * sc.z + T[10],
+                       T[6] * sc.x + T[7] * sc.y + T[8] * sc.z + T[11]};
+            if (nr) {
+                const V3 d = p - raw[nr - 1];
+                if (sqrt(dotv(d, d)) > sp.step[si]) step_ok = false;
+            }
+            if (!nr || !(p.x == raw[nr - 1].x && p.y == raw[nr - 1].y && p.z == raw[nr - 1].z)) raw[nr++] = p;
+        }
+        if (step_ok) {
+            const double tol = sp.tol[si];
+            // simplify
+            int nk = 0, j = 0;
+            kept[nk++] = 0;
+            while (j < nr - 1) {
+                int p = j + 1;
+                while (p + 1 <= nr - 1 && covers(raw, j, p + 1, tol)) ++p;
+                kept[nk++] = p;
+                j = p;
+            }
+            // cap_split
+            const int q = nk - 1, K = sp.K;
+            const auto emit = [&](int cnt, auto&& idx) {  // one spline of cnt points raw[idx(0..cnt)]
+                if (!COUNT) {
+                    spl_npts[spl_off[t] + ns] = cnt;
+                    for (int k = 0; k < cnt; ++k) {
+                        const V3 v = raw[idx(k)];
+                        double* o = pts + 3 * (pt_off[t] + np + k);
+                        o[0] = v.x, o[1] = v.y, o[2] = v.z;
+                    }
+                }
+                ++ns;
+                np += cnt;
+            };
+            if (q <= K) {
+                emit(nk, [&](int k) { return kept[k]; });
+            } else {
+                bool ok = true;
+                for (int i = 0; ok && i < K; ++i) {
+                    const int a = kept[llround(static_cast<double>(i) * q / K)];
+                    const int b = kept[llround(static_cast<double>(i + 1) * q / K)];
+                    ok = covers(raw, a, b, tol);
+                }
+                if (ok) {
+                    emit(K + 1, [&](int k) { return kept[llround(static_cast<double>(k) * q / K)]; });
+                } else {
+                    for (int start = 0; start < q; start += K) {
+                        const int stop = min(start + K, q);
+                        emit(stop - start + 1, [&](int k) { return kept[start + k]; });
+                    }
+                }
+            }
+        }
+    }
+    if (COUNT) {
+        nspl[t] = ns;
+        npts_total[t] = np;
+    }
+}
+
 }  // namespace
 
 // Streamed fit: the host produces the poses chunk by chunk into two pinned
@@ -180,7 +288,7 @@ struct FitStream {
     double he[3] = {0, 0, 0};
 };
 
-extern "C" void rggp_fit_end(void* p) {
+void rggp_fit_end(void* p) {
     FitStream* f = static_cast<FitStream*>(p);
     if (!f) return;
     cudaSetDevice(f->device);
@@ -195,7 +303,7 @@ extern "C" void rggp_fit_end(void* p) {
 }
 
 // chunk_configs: capacity of each staging buffer (configurations)
-extern "C" void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin,
+void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin,
                                 int64_t chunk_configs, int32_t device) {
     FitStream* f = new FitStream();
     f->device = device;
@@ -221,13 +329,13 @@ extern "C" void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double*
 }
 
 // the staging buffer of a slot, once its previous copy has drained
-extern "C" double* rggp_fit_staging(void* p, int32_t slot) {
+double* rggp_fit_staging(void* p, int32_t slot) {
     FitStream* f = static_cast<FitStream*>(p);
     return cudaEventSynchronize(f->done[slot]) == cudaSuccess ? f->stage[slot] : nullptr;
 }
 
 // queue the copy of a slot's nconfigs poses to configuration first_config
-extern "C" int rggp_fit_push(void* p, int32_t slot, int64_t first_config, int64_t nconfigs) {
+int rggp_fit_push(void* p, int32_t slot, int64_t first_config, int64_t nconfigs) {
     FitStream* f = static_cast<FitStream*>(p);
     cudaError_t e = cudaMemcpyAsync(f->dp + 12 * first_config, f->stage[slot], static_cast<size_t>(nconfigs) * 96,
                                     cudaMemcpyHostToDevice, f->st);
@@ -236,7 +344,7 @@ extern "C" int rggp_fit_push(void* p, int32_t slot, int64_t first_config, int64_
 }
 
 // fit every component, boxes to out (ncomp x 15), release everything
-extern "C" int rggp_fit_finish(void* p, double* out) {
+int rggp_fit_finish(void* p, double* out, const InnerSpec* spec, InnerOut* inner) {
     FitStream* f = static_cast<FitStream*>(p);
     static const bool dbg = std::getenv("RGG_DEBUG_FIT") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
@@ -259,6 +367,65 @@ extern "C" int rggp_fit_finish(void* p, double* out) {
         e = cudaMemcpyAsync(out, f->dout, static_cast<size_t>(f->ncomp) * 15 * 8, cudaMemcpyDeviceToHost, f->st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(f->st);
     mark("boxes D2H");
+    if (e == cudaSuccess && spec && inner && spec->nsph > 0 && f->ncomp > 0) {
+        // the splines: count, scan on the host, write
+        const int nsph = spec->nsph;
+        const long long nt = static_cast<long long>(f->ncomp) * nsph;
+        int64_t total = 0;
+        cudaMemcpy(&total, f->doff + f->ncomp, 8, cudaMemcpyDeviceToHost);
+        double* dspec = nullptr;
+        V3* raw = nullptr;
+        int32_t *kept = nullptr, *dns = nullptr, *dnp = nullptr, *dsn = nullptr;
+        int64_t *dso = nullptr, *dpo = nullptr;
+        double* dpts = nullptr;
+        std::vector<double> hspec(6 * nsph);
+        for (int k = 0; k < 3 * nsph; ++k) hspec[k] = spec->centre[k];
+        for (int k = 0; k < nsph; ++k)
+            hspec[3 * nsph + k] = spec->radius[k], hspec[4 * nsph + k] = spec->step_bound[k], hspec[5 * nsph + k] = spec->tol[k];
+        auto ok = [&](cudaError_t x) { return e == cudaSuccess && (e = x) == cudaSuccess; };
+        ok(cudaMalloc(&dspec, hspec.size() * 8));
+        ok(cudaMalloc(&raw, static_cast<size_t>(total) * nsph * sizeof(V3) + 16));
+        ok(cudaMalloc(&kept, static_cast<size_t>(total) * nsph * 4 + 16));
+        ok(cudaMalloc(&dns, nt * 4));
+        ok(cudaMalloc(&dnp, nt * 4));
+        ok(cudaMemcpy(dspec, hspec.data(), hspec.size() * 8, cudaMemcpyHostToDevice));
+        const InnerDev sd{nsph, spec->K, dspec, dspec + 3 * nsph, dspec + 4 * nsph, dspec + 5 * nsph};
+        const unsigned grid = static_cast<unsigned>((nt + 127) / 128);
+        if (e == cudaSuccess) {
+            inner_kernel<true><<<grid, 128, 0, f->st>>>(f->dp, f->doff, f->ncomp, sd, raw, kept, dns, dnp, nullptr,
+                                                         nullptr, nullptr, nullptr);
+            ok(cudaGetLastError());
+        }
+        inner->nspl.resize(nt);
+        std::vector<int32_t> np(nt);
+        ok(cudaMemcpyAsync(inner->nspl.data(), dns, nt * 4, cudaMemcpyDeviceToHost, f->st));
+        ok(cudaMemcpyAsync(np.data(), dnp, nt * 4, cudaMemcpyDeviceToHost, f->st));
+        ok(cudaStreamSynchronize(f->st));
+        mark("splines count");
+        std::vector<int64_t> so(nt + 1, 0), po(nt + 1, 0);
+        for (long long k = 0; k < nt; ++k) so[k + 1] = so[k] + inner->nspl[k], po[k + 1] = po[k] + np[k];
+        inner->npts.resize(so[nt]);
+        inner->pts.resize(static_cast<size_t>(po[nt]) * 3);
+        ok(cudaMalloc(&dso, (nt + 1) * 8));
+        ok(cudaMalloc(&dpo, (nt + 1) * 8));
+        ok(cudaMalloc(&dsn, so[nt] * 4 + 4));
+        ok(cudaMalloc(&dpts, po[nt] * 24 + 8));
+        ok(cudaMemcpy(dso, so.data(), (nt + 1) * 8, cudaMemcpyHostToDevice));
+        ok(cudaMemcpy(dpo, po.data(), (nt + 1) * 8, cudaMemcpyHostToDevice));
+        if (e == cudaSuccess) {
+            inner_kernel<false><<<grid, 128, 0, f->st>>>(f->dp, f->doff, f->ncomp, sd, raw, kept, nullptr, nullptr, dso,
+                                                          dpo, dsn, dpts);
+            ok(cudaGetLastError());
+        }
+        ok(cudaMemcpyAsync(inner->npts.data(), dsn, so[nt] * 4, cudaMemcpyDeviceToHost, f->st));
+        ok(cudaMemcpyAsync(inner->pts.data(), dpts, po[nt] * 24, cudaMemcpyDeviceToHost, f->st));
+        ok(cudaStreamSynchronize(f->st));
+        mark("splines write");
+        for (void* q : {static_cast<void*>(dspec), static_cast<void*>(raw), static_cast<void*>(kept),
+                        static_cast<void*>(dns), static_cast<void*>(dnp), static_cast<void*>(dso),
+                        static_cast<void*>(dpo), static_cast<void*>(dsn), static_cast<void*>(dpts)})
+            cudaFree(q);
+    }
     rggp_fit_end(f);
     return e;
 }

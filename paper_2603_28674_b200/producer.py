@@ -43,7 +43,7 @@ def library():
 
 
 def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False, with_poses=False,
-                 gpu_fit=False):
+                 gpu_fit=False, gpu_inner=False):
     """Components (nodes first, then edges) of a free-flying box robot -> store arrays.
     with_poses: also a["pose_off"] (N+1) and a["poses"] (configs, 1, 12), the
     forward kinematics of every discretized configuration (GPU exact resolve)."""
@@ -54,7 +54,8 @@ def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, w
     h = C.c_void_p()
     rc = L.rgg_build_layout_ex(he.ctypes.data, len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
                                float(eps), int(max_segments), int(threads),
-                               (1 if with_poses else 0) | (2 if gpu_fit else 0), C.byref(h))
+                               (1 if with_poses else 0) | (2 if gpu_fit else 0) | (4 if gpu_inner else 0),
+                               C.byref(h))
     if rc != 0:
         raise RuntimeError(L.rgg_build_last_error().decode())
     try:

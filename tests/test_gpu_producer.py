@@ -1,5 +1,5 @@
-"""The producer's swept-volume box fit on the GPU (csrc/swept_gpu.cu, SURVEY.md §8f
-rank 3) against the host producer, which tests/test_producer.py pins bit for bit to
+"""The producer's swept-volume box fit and spline simplification on the GPU
+(csrc/swept_gpu.cu) against the host producer, which tests/test_producer.py pins bit for bit to
 the reference's build_components + serialize."""
 import numpy as np
 import pytest
@@ -13,8 +13,10 @@ pytestmark = pytest.mark.gpu
 def test_gpu_box_fit_is_bit_identical(kind, n, k, half, seed):
     rm = synth.make_roadmap(kind, n, k, half, seed)
     host = producer.build_layout(rm.robot_he, rm.nodes, rm.edges, with_obbs=True, threads=8)
-    gpu = producer.build_layout(rm.robot_he, rm.nodes, rm.edges, with_obbs=True, threads=8, gpu_fit=True)
-    assert host[:3] == gpu[:3]
-    for key in ("edge_sat", "comp_aabb", "segs", "spline_r", "obb15", "row_off"):
-        a, b = host[3][key], gpu[3][key]
-        assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), key
+    for inner in (False, True):
+        gpu = producer.build_layout(rm.robot_he, rm.nodes, rm.edges, with_obbs=True, threads=8, gpu_fit=True,
+                                    gpu_inner=inner)
+        assert host[:3] == gpu[:3]
+        for key in ("edge_sat", "comp_aabb", "segs", "spline_r", "obb15", "row_off"):
+            a, b = host[3][key], gpu[3][key]
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), (key, inner)
