@@ -10,6 +10,7 @@ Every fixture records what the reference computes on a seeded input:
   kat_seg.npz        proj/tests/test_kernels.cpp:89-121 (seed 777) — seg-sphere bytes
   kat_pairs.npz      random_obb pairs (proj/tests/oracles.hpp:98-109) + sat_margin (:62-84)
   kat_obstacle.npz   BatchLayout::update_transforms (proj/src/batch_layout.cpp:148-172)
+  prm.npz            build_prm (proj/src/roadmap.cpp:56-102) nodes + edges per scenario
   scn_*.npz          engine replays: layout + move script + BatchEngine reports after
                      every move + states/bits snapshots (proj/src/engine_batch.cpp:145-205),
                      plus batch_over/batch_under masks (:55-112)
@@ -155,6 +156,41 @@ def kat_boxes(n=1200, seed=31):
     print("kat_boxes written:", int(out.sum()), "of", n, "intersect")
 
 
+def prm():
+    """build_prm (proj/src/roadmap.cpp:56-102) of every shipped scenario's build scene,
+    proj/tests/test_roadmap.cpp:34-60's free-cube cases, and a digest of table3's
+    10,000-node roadmap (too large to store)."""
+    import glob
+    import hashlib
+    import re
+
+    d = {}
+    names = []
+
+    def put(name, text, n=-1, k=-1, seed=-1, digest=False):
+        nodes, edges, lo, hi, sec = ref.build_prm(text, n, k, seed)
+        kk = k if k >= 0 else int(re.search(r"k_neighbors\s*=\s*(\d+)", text).group(1))
+        sd = seed if seed >= 0 else int(re.search(r"roadmap_seed\s*=\s*(\d+)", text).group(1))
+        names.append(name)
+        d[f"{name}__meta"] = np.array([len(nodes), kk, sd, nodes.shape[1], len(edges)], np.int64)
+        d[f"{name}__lo"], d[f"{name}__hi"] = lo, hi
+        if digest:
+            d[f"{name}__sha_nodes"] = np.frombuffer(hashlib.sha256(nodes.tobytes()).digest(), np.uint8)
+            d[f"{name}__sha_edges"] = np.frombuffer(hashlib.sha256(edges.tobytes()).digest(), np.uint8)
+        else:
+            d[f"{name}__nodes"], d[f"{name}__edges"] = nodes, edges
+        print(f"prm {name}: {len(nodes)} nodes, {len(edges)} edges, reference {sec * 1e3:.1f} ms")
+
+    for f in sorted(glob.glob(os.path.join(REF_SCN, "*.scn"))):
+        base = os.path.basename(f)[:-4]
+        put(base, open(f).read(), digest=base.startswith("table3"))
+    cube = open(os.path.join(REF_SCN, "table2_density_10_10x2x2.scn")).read()  # env +-10, free-flying 0.5 cube
+    for n, k, seed in ((10, 16, 42), (1, 4, 7), (60, 8, 1234), (60, 8, 1235), (2, 5, 3), (300, 40, 5)):
+        put(f"cube_{n}_{k}_{seed}", cube, n, k, seed)
+    d["names"] = np.array(names)
+    np.savez_compressed(os.path.join(OUT, "prm.npz"), **d)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     if len(sys.argv) > 1:  # regenerate selected fixtures only, e.g. `gen_golden.py kat_boxes`
@@ -169,6 +205,7 @@ def main():
     scn("table5_manipulator_100", lazy=True)
     synthetic("syn_se2_m80", "se2", 800, 12, 20.0, 80, 3, 11, snap_every=40)
     synthetic("syn_3d_m20", "3d", 300, 10, 4.5, 20, 4, 21, snap_every=1)
+    prm()
 
 
 if __name__ == "__main__":

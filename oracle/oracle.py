@@ -65,6 +65,9 @@ def lib():
         L.ro_engine_pure.argtypes = [C.c_void_p, _up, _qp]
         L.ro_engine_mask.argtypes = [C.c_void_p, C.c_int, _ip, C.c_int, C.c_int32, _up]
         L.ro_engine_census.argtypes = [C.c_void_p, _lp]
+        L.ro_prm_nodes.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp, _dp, _dp]
+        L.ro_prm_knn.restype = C.c_int64
+        L.ro_prm_knn.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _ip, C.c_int64]
         _lib = L
     return _lib
 
@@ -192,3 +195,23 @@ class Engine:
         lib().ro_engine_census(self.h, out)
         keys = ["over_pairs", "sat_flops", "under_pairs", "seg_sphere_tests", "over_hits", "under_hits", "active"]
         return dict(zip(keys, out.tolist()))
+
+
+def prm_nodes(seed, n, lo, hi):
+    """build_prm's node loop (proj/src/roadmap.cpp:65-71, no active obstacles)."""
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    out = np.zeros((n, len(lo)), np.float64)
+    lib().ro_prm_nodes(int(seed), int(n), len(lo), lo, hi, out)
+    return out
+
+
+def prm_knn(nodes, k):
+    """build_prm's candidate loop (proj/src/roadmap.cpp:73-93): sorted unique (min, max) pairs."""
+    nodes = np.ascontiguousarray(nodes, np.float64)
+    n, dof = nodes.shape
+    cap = max(1, n * max(0, min(k, n - 1)))
+    out = np.zeros((cap, 2), np.int32)
+    m = lib().ro_prm_knn(nodes, n, dof, int(k), out, cap)
+    assert m >= 0
+    return out[:m].copy()

@@ -65,6 +65,8 @@ def lib():
         L.rr_sat_prep.argtypes = [C.c_int, _dp, _dp]
         L.rr_tf_euler.argtypes = [C.c_double, C.c_double, C.c_double, _dp]
         L.rr_tf_axis_angle.argtypes = [_dp, C.c_double, _dp]
+        L.rr_build_prm.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_longlong, C.POINTER(C.c_int), _dp, _dp,
+                                   C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, _lp, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -279,3 +281,22 @@ def tf_axis_angle(axis, angle):
     out = np.zeros(12)
     _check(lib().rr_tf_axis_angle(np.asarray(axis, np.float64), angle, out))
     return out
+
+
+def build_prm(scn_text: str, n_nodes: int = -1, k: int = -1, seed: int = -1):
+    """The reference's build_prm (proj/src/roadmap.cpp:56-102) over a scenario's env and robot,
+    no obstacles.  Returns (nodes n x dof, edges e x 2 int32, lo, hi, seconds)."""
+    L = lib()
+    dof = C.c_int(0)
+    lo = np.zeros(64)
+    hi = np.zeros(64)
+    counts = np.zeros(2, np.int64)
+    _check(L.rr_build_prm(scn_text.encode(), n_nodes, k, seed, C.byref(dof), lo, hi, None, 0, None, 0, counts,
+                          None))
+    D = dof.value
+    nodes = np.zeros((max(1, int(counts[0])), D), np.float64)
+    edges = np.zeros((max(1, int(counts[1])), 2), np.int32)
+    sec = C.c_double(0)
+    _check(L.rr_build_prm(scn_text.encode(), n_nodes, k, seed, C.byref(dof), lo, hi, nodes.ctypes.data,
+                          len(nodes), edges.ctypes.data, len(edges), counts, C.byref(sec)))
+    return nodes[:counts[0]].copy(), edges[:counts[1]].copy(), lo[:D].copy(), hi[:D].copy(), sec.value

@@ -612,4 +612,44 @@ int rr_tf_axis_angle(const double* axis3, double angle, double* rt12) {
     return guarded([&] { put_tf(Transform::rotation_axis_angle({axis3[0], axis3[1], axis3[2]}, angle), rt12); });
 }
 
+// build_prm (proj/src/roadmap.cpp:56-102) over the env and robot of a .scn text with
+// no obstacles (the benchmark's build scene, proj/src/bench.cpp:90-91); n_nodes, k and
+// seed override the scenario's when >= 0.  dof_bounds_for (roadmap.cpp:20-30) into lo/hi.
+int rr_build_prm(const char* text, int n_nodes, int k, long long seed, int* dof, double* lo, double* hi,
+                 double* nodes, std::int64_t node_cap, std::int32_t* edges, std::int64_t edge_cap,
+                 std::int64_t* counts, double* seconds) {
+    return guarded([&] {
+        const Scenario s = parse_scenario_text(text, "<scn>");
+        const Scene build_scene{s.env, {}, s.robot};
+        const int n = n_nodes >= 0 ? n_nodes : s.nodes;
+        const int kk = k >= 0 ? k : s.k_neighbors;
+        const std::uint64_t sd = seed >= 0 ? static_cast<std::uint64_t>(seed) : s.roadmap_seed;
+        const auto t0 = std::chrono::steady_clock::now();
+        const Roadmap r = build_prm(build_scene, n, kk, s.effective_epsilon(), sd);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        const DofBounds b = dof_bounds_for(s.robot, s.env);
+        const int D = static_cast<int>(b.lo.size());
+        if (dof) *dof = D;
+        for (int q = 0; q < D; ++q) {
+            if (lo) lo[q] = b.lo[q];
+            if (hi) hi[q] = b.hi[q];
+        }
+        counts[0] = static_cast<std::int64_t>(r.nodes.size());
+        counts[1] = static_cast<std::int64_t>(r.edges.size());
+        if (nodes) {
+            if (counts[0] > node_cap) throw std::invalid_argument("node buffer too small");
+            for (size_t i = 0; i < r.nodes.size(); ++i)
+                for (int q = 0; q < D; ++q) nodes[i * D + q] = r.nodes[i][q];
+        }
+        if (edges) {
+            if (counts[1] > edge_cap) throw std::invalid_argument("edge buffer too small");
+            for (size_t e = 0; e < r.edges.size(); ++e) {
+                edges[2 * e] = r.edges[e].first;
+                edges[2 * e + 1] = r.edges[e].second;
+            }
+        }
+    });
+}
+
 }  // extern "C"

@@ -586,3 +586,108 @@ int ro_exact_valid(int n_cfg, int n_bodies, const double* poses, const double* b
         }
     return 1;
 }
+
+/* ---- PRM construction (proj/src/roadmap.cpp:56-102), no active obstacles ---- */
+
+/* std::mt19937_64 as the C++ standard defines it (w=64, n=312, m=156, r=31,
+ * a=0xB5026F5AA96619E9, u=29 d=0x5555555555555555, s=17 b=0x71D67FFFEDA60000,
+ * t=37 c=0xFFF7EEE000000000, l=43, f=6364136223846793005). */
+typedef struct {
+    uint64_t mt[312];
+    int i;
+} ro_mt64;
+
+static void mt64_seed(ro_mt64* g, uint64_t seed) {
+    g->mt[0] = seed;
+    for (int i = 1; i < 312; ++i) g->mt[i] = 6364136223846793005ull * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+    g->i = 312;
+}
+
+static uint64_t mt64_next(ro_mt64* g) {
+    if (g->i >= 312) {
+        for (int k = 0; k < 312; ++k) {
+            const uint64_t y = (g->mt[k] & 0xFFFFFFFF80000000ull) | (g->mt[(k + 1) % 312] & 0x7FFFFFFFull);
+            g->mt[k] = g->mt[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1) ? 0xB5026F5AA96619E9ull : 0);
+        }
+        g->i = 0;
+    }
+    uint64_t x = g->mt[g->i++];
+    x ^= (x >> 29) & 0x5555555555555555ull;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+    x ^= (x << 37) & 0xFFF7EEE000000000ull;
+    x ^= x >> 43;
+    return x;
+}
+
+/* The node loop of build_prm (roadmap.cpp:65-71) with Rng::uniform (rng.hpp:17-19). */
+void ro_prm_nodes(uint64_t seed, int n, int dof, const double* lo, const double* hi, double* nodes) {
+    ro_mt64 g;
+    mt64_seed(&g, seed);
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < dof; ++k) {
+            const double u = (double)(mt64_next(&g) >> 11) * 0x1.0p-53;
+            nodes[(size_t)i * dof + k] = lo[k] + (hi[k] - lo[k]) * u;
+        }
+}
+
+typedef struct {
+    double d;
+    int32_t j;
+} ro_dj;
+
+static int dj_less(const ro_dj* a, const ro_dj* b) { return a->d < b->d || (a->d == b->d && a->j < b->j); }
+
+static int u64_cmp(const void* a, const void* b) {
+    const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+/* The candidate loop (roadmap.cpp:73-93): dof_distance2 (:36-43) to every other node, the
+ * k smallest (distance, j) pairs (partial_sort of pair<double, NodeId>), (min, max), sorted,
+ * unique.  Selection here is a bounded insertion list (same set as partial_sort).
+ * Returns the edge count (edges: cap x 2), or -(count)-1 if cap is too small. */
+int64_t ro_prm_knn(const double* nodes, int n, int dof, int k, int32_t* edges, int64_t cap) {
+    const int kk = k < n - 1 ? k : n - 1;
+    if (kk <= 0) return 0;
+    ro_dj* best = (ro_dj*)malloc(sizeof(ro_dj) * (size_t)kk);
+    uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n * kk);
+    for (int i = 0; i < n; ++i) {
+        int cnt = 0;
+        const double* a = nodes + (size_t)i * dof;
+        for (int j = 0; j < n; ++j) {
+            if (j == i) continue;
+            const double* b = nodes + (size_t)j * dof;
+            double d2 = 0.0;
+            for (int q = 0; q < dof; ++q) {
+                const double d = b[q] - a[q];
+                d2 += d * d;
+            }
+            const ro_dj c = {d2, j};
+            if (cnt == kk && !dj_less(&c, &best[kk - 1])) continue;
+            int p = cnt < kk ? cnt++ : kk - 1;
+            while (p > 0 && dj_less(&c, &best[p - 1])) {
+                best[p] = best[p - 1];
+                --p;
+            }
+            best[p] = c;
+        }
+        for (int t = 0; t < kk; ++t) {
+            const uint32_t lo = (uint32_t)(i < best[t].j ? i : best[t].j), hi = (uint32_t)(i < best[t].j ? best[t].j : i);
+            keys[(size_t)i * kk + t] = ((uint64_t)lo << 32) | hi;
+        }
+    }
+    qsort(keys, (size_t)n * kk, sizeof(uint64_t), u64_cmp);
+    int64_t m = 0;
+    for (size_t e = 0; e < (size_t)n * kk; ++e)
+        if (e == 0 || keys[e] != keys[e - 1]) keys[m++] = keys[e];
+    int64_t rc = m;
+    if (m > cap) rc = -m - 1;
+    else
+        for (int64_t e = 0; e < m; ++e) {
+            edges[2 * e] = (int32_t)(keys[e] >> 32);
+            edges[2 * e + 1] = (int32_t)(keys[e] & 0xffffffffu);
+        }
+    free(best);
+    free(keys);
+    return rc;
+}

@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 GPU_SOURCES = ["rgg_kernels.cu", "rgg_resolve.cu", "rgg_store.cu", "rgg_capi.cu"]
 GPU_DEPS = GPU_SOURCES + ["rgg_device.cuh", "rgg_kernels.cuh"]
-PRODUCER_SOURCES = ["producer.cpp", "swept_gpu.cu"]
+PRODUCER_SOURCES = ["producer.cpp", "swept_gpu.cu", "rgg_prm.cu"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -48,19 +48,20 @@ def build_producer(force: bool = False) -> str:
     os.makedirs(LIB, exist_ok=True)
     out = os.path.join(LIB, "librgg_build.so")
     srcs = [os.path.join(CSRC, f) for f in PRODUCER_SOURCES]
-    deps = srcs + [os.path.join(ROOT, "include", "rgg_build.h")]
+    deps = srcs + [os.path.join(ROOT, "include", h) for h in ("rgg_build.h", "rgg_prm.h")] + [
+        os.path.join(CSRC, "swept_gpu.h")]
     if not all(os.path.exists(s) for s in srcs):
         return ""
     if force or _stale(out, deps):
-        # host part with g++ (the reference's flags), the GPU box fit with nvcc -fmad=false
-        obj_cpp = os.path.join(LIB, "producer.o")
-        obj_cu = os.path.join(LIB, "swept_gpu.o")
+        # host part with g++ (the reference's flags); the GPU fit and PRM with nvcc -fmad=false
+        objs = [os.path.join(LIB, os.path.splitext(f)[0] + ".o") for f in PRODUCER_SOURCES]
         subprocess.check_call(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-pthread", "-c",
-                               "-I", os.path.join(ROOT, "include"), "-o", obj_cpp, srcs[0]])
-        subprocess.check_call([NVCC, *ARCH, "-O3", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-c",
-                               "-o", obj_cu, srcs[1]])
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, obj_cpp, obj_cu, "-Xcompiler", "-pthread"])
-        for o in (obj_cpp, obj_cu):
+                               "-I", os.path.join(ROOT, "include"), "-o", objs[0], srcs[0]])
+        for src, obj in zip(srcs[1:], objs[1:]):
+            subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
+                                   "-fPIC,-ffp-contract=off", "-c", "-o", obj, src])
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", out, *objs, "-Xcompiler", "-pthread"])
+        for o in objs:
             os.remove(o)
     return out
 
