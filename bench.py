@@ -325,6 +325,44 @@ def measure_resolve(config, seed, device, rounds=4, cpu=True):
     return out
 
 
+def measure_prm(cpu=True, reps=3):
+    """PRM construction: build_prm's kNN on the GPU (csrc/rgg_prm.cu)
+    through the host API (nodes H2D, edges D2H inside the wall time), at table3's 10,000
+    nodes (the reference's largest shipped roadmap, timed beside it) and at the 1M-edge
+    configs' 87,000 nodes (k=20; the reference would take minutes, so not run)."""
+
+    from paper_2603_28674_b200 import prm
+
+    out = {"what": "rgg_prm_knn_edges: k nearest nodes under dof_distance2, (min, max) pairs sorted + unique; "
+                   "host API wall time (H2D nodes, D2H edges) and device time"}
+    scn = os.path.join(ROOT, "tests", "golden", "scenarios", "table3_roadmap_10000.scn")
+    for name, n, k, half, seed in (("table3_roadmap_10000", 10000, 8, 10.0, 105),
+                                   ("n87000_k20", 87000, 20, 71.0, 12345)):
+        lo, hi = prm.dof_bounds_free_flying([-half] * 3 + [half] * 3)
+        nodes = prm.sample_nodes(seed, n, lo, hi)
+        prm.knn_edges(nodes, k)  # warm (allocations, module load)
+        wall, dev = [], []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            edges, ms = prm.knn_edges(nodes, k, return_ms=True)
+            wall.append(1e3 * (time.perf_counter() - t0))
+            dev.append(ms)
+        r = {"nodes": n, "k": k, "dof": 6, "edges": int(len(edges)), "gpu_wall_ms": statistics.median(wall),
+             "gpu_device_ms": statistics.median(dev),
+             "pairs_per_s_device": n * (n - 1) / (1e-3 * statistics.median(dev))}
+        if cpu and name.startswith("table3") and os.path.exists(scn):
+            from oracle import ref
+
+            rn, re_, _, _, sec = ref.build_prm(open(scn).read())
+            r["cpu_ref_ms"] = 1e3 * sec
+            r["cpu_ref_note"] = "rgg::build_prm (oracle/_ref), one thread as the reference runs it, kNN + sort"
+            r["speedup_wall"] = 1e3 * sec / r["gpu_wall_ms"]
+            r["edges_equal_reference"] = bool(np.array_equal(rn.view(np.uint64), nodes.view(np.uint64)) and
+                                              np.array_equal(re_, edges))
+        out[name] = r
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -539,6 +577,11 @@ def main():
             line["resolve"] = measure_resolve(args.config, args.seed, local, cpu=not args.no_cpu_baseline)
         except Exception as ex:
             line["resolve"] = {"error": str(ex)[:200]}
+    if world == 1 and args.config == "c2" and not args.no_resolve:
+        try:
+            line["prm"] = measure_prm(cpu=not args.no_cpu_baseline)
+        except Exception as ex:
+            line["prm"] = {"error": str(ex)[:200]}
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n, done, spent, per_step, ref_eng = cpu_reference_run(args.config, args.seed, iterations,

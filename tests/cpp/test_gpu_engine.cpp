@@ -9,9 +9,11 @@
 //   proj/tests/test_batch.cpp:287-295  empty move list
 //   proj/tests/test_sequential.cpp:106-126, :229-252  eager resolve semantics
 //   proj/src/bench.cpp:57-83           scenario replay with equivalence after every iteration
+//   proj/tests/test_roadmap.cpp:34-73  rgg::gpu::build_prm (include/rgg/prm_gpu.hpp) == build_prm
 // Built by `make -C oracle dropin` (needs /root/reference); run by tests/test_cpp_dropin.py on a GPU.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <fstream>
 #include <sstream>
 #include <string>
@@ -19,6 +21,7 @@
 #include "rgg/engine_batch.hpp"
 #include "rgg/engine_gpu.hpp"
 #include "rgg/engine_sequential.hpp"
+#include "rgg/prm_gpu.hpp"
 #include "rgg/rng.hpp"
 #include "rgg/scenario.hpp"
 
@@ -176,6 +179,65 @@ static void scenario_replay(const std::string& path) {
                 comps.count(), iterations);
 }
 
+static bool same_roadmap(const Roadmap& a, const Roadmap& b) {
+    if (a.nodes.size() != b.nodes.size() || a.edges != b.edges || a.adjacency != b.adjacency) return false;
+    for (size_t i = 0; i < a.nodes.size(); ++i)
+        if (std::memcmp(a.nodes[i].data(), b.nodes[i].data(), a.nodes[i].size() * sizeof(double)) != 0 ||
+            a.nodes[i].size() != b.nodes[i].size())
+            return false;
+    return true;
+}
+
+// rgg::gpu::build_prm against rgg::build_prm: the free-cube cases and the active-wall case of
+// proj/tests/test_roadmap.cpp:34-73, the argument errors, and the scenarios' build scenes.
+static void prm_matches_reference(const std::vector<std::string>& scns) {
+    auto cube = [](double half) {
+        Scene s;
+        s.bounds = {{-half, -half, -half}, {half, half, half}};
+        s.robot = make_free_flying_box({0.5, 0.5, 0.5});
+        return s;
+    };
+    const struct {
+        int n, k;
+        std::uint64_t seed;
+    } cases[] = {{10, 16, 42}, {1, 4, 7}, {60, 8, 1234}, {60, 8, 1235}, {2000, 12, 5}};
+    for (const auto& c : cases) {
+        const Scene sc = cube(10.0);
+        EXPECT(same_roadmap(rgg::gpu::build_prm(sc, c.n, c.k, 0.25, c.seed), build_prm(sc, c.n, c.k, 0.25, c.seed)),
+               "free cube n=%d k=%d", c.n, c.k);
+    }
+    {
+        Scene sc = cube(3.0);
+        ObstacleModel wall = make_box_obstacle({3.0, 3.0, 0.5}, 3);
+        wall.pose = Transform::identity();
+        wall.active = true;
+        sc.obstacles.push_back(wall);
+        const Roadmap g = rgg::gpu::build_prm(sc, 40, 6, 0.25, 99);
+        EXPECT(same_roadmap(g, build_prm(sc, 40, 6, 0.25, 99)), "active wall");
+        EXPECT(g.nodes.size() < 40, "the slab cuts out samples");
+    }
+    for (int bad = 0; bad < 2; ++bad) {
+        bool threw = false;
+        try {
+            rgg::gpu::build_prm(cube(10.0), bad == 0 ? 0 : 10, bad == 0 ? 4 : 0, 0.25, 7);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        EXPECT(threw, "invalid_argument case %d", bad);
+    }
+    for (const std::string& path : scns) {
+        std::ifstream f(path);
+        if (!f) continue;
+        std::stringstream ss;
+        ss << f.rdbuf();
+        const Scenario s = parse_scenario_text(ss.str(), path);
+        const Scene build_scene{s.env, {}, s.robot};
+        EXPECT(same_roadmap(rgg::gpu::build_prm(build_scene, s.nodes, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed),
+                            build_prm(build_scene, s.nodes, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed)),
+               "scenario %s", path.c_str());
+    }
+}
+
 int main(int argc, char** argv) {
     const std::string dir = argc > 1 ? argv[1] : "";
     equivalence_after_every_move();
@@ -186,6 +248,8 @@ int main(int argc, char** argv) {
         scenario_replay(dir + "/table4_obstacles_1000_5x.scn");
         scenario_replay(dir + "/table5_manipulator_100.scn");
     }
+    prm_matches_reference({dir + "/quick_smoke.scn", dir + "/table4_obstacles_1000_5x.scn",
+                           dir + "/table5_manipulator_100.scn"});
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
