@@ -374,16 +374,35 @@ __global__ void init_obstacles_kernel(Store s) {
 // the cell's fixed-capacity list (overflow -> pool) with warp ballots.  Work is
 // O(supercells x events + cells x candidates) instead of O(cells x events).
 
+// The per-cell test runs on fp32 boxes rounded outward (lower corners down, upper
+// corners up), a superset of the fp64 test: a listed event that touches none of
+// the cell's components is dropped by touch's exact per-component test, so the
+// lists only need to contain every overlapping event (the overflow pass below
+// applies the same two tests, so counts and lists agree).
 constexpr int kBinThreads = 512;  // 16 warps = 16 cells per CTA (one super-cell)
-constexpr int kBinChunk = 256;    // events filtered per pass (threads >= kBinChunk idle in the filter)
+constexpr int kBinChunk = 512;    // events filtered per pass
 
-__global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
+__device__ __forceinline__ void box_out32(const double* d, float* f) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        f[k] = __double2float_rd(d[k]);
+        f[3 + k] = __double2float_ru(d[3 + k]);
+    }
+}
+__device__ __forceinline__ bool overlaps32(const float* a, const float* b) {
+    return (a[0] <= b[3]) & (b[0] <= a[3]) & (a[1] <= b[4]) & (b[1] <= a[4]) & (a[2] <= b[5]) & (b[2] <= a[5]);
+}
+
+#ifndef RGG_BIN_MINB
+#define RGG_BIN_MINB 2  // two CTAs per SM (registers <= 64)
+#endif
+__global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s, Batch b) {
     const unsigned long long tw = tl_start(b.tl);
     pdl_wait();
     pdl_trigger();
     const unsigned long long t0 = tl_start(b.tl);
     tl_stop(b.tl, 5, tw);
-    __shared__ double cbox[12][kBinChunk];  // SoA: lane q reads column q, conflict-free
+    __shared__ float cbox[12][kBinChunk];  // SoA: lane q reads column q, conflict-free
     __shared__ int cidx[kBinChunk];
     __shared__ int wsum[kBinThreads / 32];
     __shared__ int s_nc;
@@ -391,10 +410,13 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
     const int cell = blockIdx.x * (kBinThreads / 32) + warp;
     const bool live = cell < s.ncells;
     double sb[6], cb[6];
+    float cbf[6];
 #pragma unroll
     for (int k = 0; k < 6; ++k) sb[k] = s.super_aabb[6 * static_cast<size_t>(blockIdx.x) + k];
-    if (live)
+    if (live) {
         for (int k = 0; k < 6; ++k) cb[k] = s.cell_aabb[6 * static_cast<size_t>(cell) + k];
+        box_out32(cb, cbf);
+    }
     int count = 0;
     int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
     for (int base = 0; base < b.n; base += kBinChunk) {
@@ -429,8 +451,11 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
         if (cand) {
             const int pos = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
             cidx[pos] = e;
+            float f[12];
+            box_out32(bx, f);
+            box_out32(bx + 6, f + 6);
 #pragma unroll
-            for (int k = 0; k < 12; ++k) cbox[k][pos] = bx[k];
+            for (int k = 0; k < 12; ++k) cbox[k][pos] = f[k];
         }
         __syncthreads();
         const int nc = s_nc;
@@ -440,10 +465,10 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
             const int q = j + lane;
             bool hit = false;
             if (q < nc) {
-                double qb[12];
+                float qb[12];
 #pragma unroll
                 for (int k = 0; k < 12; ++k) qb[k] = cbox[k][q];
-                hit = rggd::overlaps(cb, qb) | rggd::overlaps(cb, qb + 6);
+                hit = overlaps32(cbf, qb) | overlaps32(cbf, qb + 6);
             }
             const unsigned hb = __ballot_sync(0xffffffffu, hit);
             if (hit) {
@@ -470,9 +495,13 @@ __global__ void __launch_bounds__(kBinThreads) bin_kernel(Store s, Batch b) {
             for (int e0 = 0; e0 < b.n; e0 += 32) {
                 const int e = e0 + lane;
                 bool hit = false;
-                if (e < b.n) {
+                if (e < b.n) {  // the same two tests as the listing pass
                     const double* bx = b.evbox + 12 * static_cast<size_t>(e);
-                    hit = rggd::overlaps(cb, bx) || rggd::overlaps(cb, bx + 6);
+                    float f[12];
+                    box_out32(bx, f);
+                    box_out32(bx + 6, f + 6);
+                    hit = (rggd::overlaps(sb, bx) | rggd::overlaps(sb, bx + 6)) &&
+                          (overlaps32(cbf, f) | overlaps32(cbf, f + 6));
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, hit);
                 if (hit) b.pool[pbase + at + __popc(bal & ((1u << lane) - 1u))] = e;
