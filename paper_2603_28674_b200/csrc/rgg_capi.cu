@@ -34,6 +34,7 @@ struct rgg_gpu {
     rggd::Box32* d_sat32 = nullptr;
     int32_t* d_row = nullptr;
     double* d_seg = nullptr;
+    float4* d_seg32 = nullptr;
     double* d_spline = nullptr;
     int32_t* d_orig = nullptr;
     int32_t* d_rank = nullptr;
@@ -582,6 +583,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         CK(rggk::build_store(in, so, h->stream));
         mark("build_store");
         h->d_seg = so.seg;
+        h->d_seg32 = so.seg32;
         h->total_segs_owned = so.total_segs;
         h->orig.resize(Np);
         if (Np) CK(cudaMemcpy(h->orig.data(), h->d_orig, static_cast<size_t>(Np) * sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -653,7 +655,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.dbg_flags = std::getenv("RGG_DEBUG_FLAGS") ? std::atoi(std::getenv("RGG_DEBUG_FLAGS")) : 0;
     {
         // narrow operands of the whole roadmap: Box32 lines and segment records
-        const double bytes = 128.0 * Np * B + 64.0 * static_cast<double>(h->total_segs_owned);
+        const double bytes = 128.0 * Np * B + 32.0 * static_cast<double>(h->total_segs_owned);
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device);
         s.prefetch = bytes <= 0.5 * l2 && !(s.dbg_flags & 2048) ? 1 : 0;  // 2048: ablation, never
@@ -663,6 +665,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.sat32 = h->d_sat32;
     s.row = h->d_row;
     s.seg = h->d_seg;
+    s.seg32 = h->d_seg32;
     s.spline_r = h->d_spline;
     s.orig = h->d_orig;
     s.cell_aabb = h->d_cell_aabb;
@@ -695,7 +698,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_row, h->d_seg, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,

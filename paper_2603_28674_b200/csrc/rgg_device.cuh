@@ -459,6 +459,59 @@ __device__ __forceinline__ int seg_filter32_pre(const double* s, const Seg32& g,
     return g.r_ok ? f : 0;
 }
 
+// The same filter over a compact fp32 copy of the segment record (32 bytes:
+// a[3], d[3], dd, spline radius, each rounded to nearest; rgg_store.cu segs_kernel),
+// so the narrow kernel streams half the bytes and reads the fp64 record only for
+// an undecided pair.  With a and the sphere centre c rounded before the
+// subtraction, p32 = fl(c32 - a32) carries an absolute error of at most
+// E = u(|c|_1 + |a|_1) beyond the one rounding the 64u P^2 model covers; the
+// distance to a segment is 1-Lipschitz in p, so sqrt(x) moves by at most E and x
+// by at most 2 sqrt(x) E + E^2 <= 2 P E + E^2 (P >= |q|_1 >= sqrt(x)), both
+// charged with 10 % margin.  r = fl(fl(o_r) + spline32) is within 3u r of the
+// fp64 r_total, so r^2 within 7u; the band uses 16u.  A non-positive or tiny r
+// (never in a valid layout) is left to fp64, which applies the reference's sign rule.
+struct SegF {
+    float ax, ay, az, dx, dy, dz, inv_dd, dabs, aabs, r2, r2err;
+    bool dd_pos, r_fast;
+};
+
+__device__ __forceinline__ SegF segf_prep(float4 v0, float4 v1, double o_r) {
+    constexpr float u = 5.9604645e-8f;
+    SegF g;
+    g.ax = v0.x, g.ay = v0.y, g.az = v0.z;
+    g.dx = v0.w, g.dy = v1.x, g.dz = v1.y;
+    g.dd_pos = v1.z > 0.0f;
+    g.inv_dd = g.dd_pos ? __frcp_rn(v1.z) : 0.0f;
+    g.dabs = fabsf(g.dx) + fabsf(g.dy) + fabsf(g.dz);
+    g.aabs = fabsf(g.ax) + fabsf(g.ay) + fabsf(g.az);
+    const float ro = __double2float_rn(o_r);
+    const float r = ro + v1.w;
+    g.r_fast = r > 16.0f * u * (fabsf(ro) + fabsf(v1.w)) && r < 1.0e18f;
+    g.r2 = r * r;
+    g.r2err = 16.0f * u * g.r2;
+    return g;
+}
+
+// c32: the sphere centre rounded to nearest; cabs = |c32|_1 (>= |c|_1 (1 - u), the
+// 10 % margin covers the difference).  1 = hit, 0 = miss, 2 = undecided.
+__device__ __forceinline__ int segf_filter(const SegF& g, float cx, float cy, float cz, float cabs) {
+    constexpr float u = 5.9604645e-8f;
+    if (!g.r_fast) return 2;
+    const float px = cx - g.ax, py = cy - g.ay, pz = cz - g.az;
+    float t = 0.0f;
+    if (g.dd_pos) {
+        const float num = fmaf(pz, g.dz, fmaf(py, g.dy, px * g.dx));
+        t = fminf(fmaxf(num * g.inv_dd, 0.0f), 1.0f);
+    }
+    const float qx = fmaf(-t, g.dx, px), qy = fmaf(-t, g.dy, py), qz = fmaf(-t, g.dz, pz);
+    const float x = fmaf(qz, qz, fmaf(qy, qy, qx * qx));
+    const float P = ((fabsf(px) + fabsf(py)) + fabsf(pz)) + g.dabs;
+    const float E = 1.1f * u * (cabs + g.aabs);
+    const float err = 64.0f * u * P * P + 2.2f * P * E + 1.1f * E * E + 1e-30f;
+    return !(x == x) || !(P < 3.0e18f) || !(cabs < 1.0e18f) ? 2
+                                                          : (x + err < g.r2 - g.r2err ? 1 : (x - err > g.r2 + g.r2err ? 0 : 2));
+}
+
 // sat_prep, proj/src/kernels_scalar.cpp:7-30.
 __device__ __forceinline__ void sat_prep(const double* c, double* s) {
 #pragma unroll

@@ -697,6 +697,36 @@ __device__ __forceinline__ bool under_range(const Store& s, int lo, int hi, cons
     return hit;
 }
 
+// under_range over the compact fp32 records (rggd::segf_filter): the fp64 record
+// is read only when a sphere is undecided.  Verdicts are the reference's.
+__device__ __forceinline__ bool under_range32(const Store& s, int lo, int hi, const Event& ev) {
+    const int nsph = ev.nsph;
+    for (int j = lo; j < hi; ++j) {
+        const float4 v0 = s.seg32[2 * static_cast<size_t>(j)], v1 = s.seg32[2 * static_cast<size_t>(j) + 1];
+        const rggd::SegF g = rggd::segf_prep(v0, v1, ev.r);
+        bool sure = false;
+        uint32_t und = 0;
+#pragma unroll 4
+        for (int sp = 0; sp < nsph; ++sp) {
+            const float cx = __double2float_rn(ev.cen[3 * sp]), cy = __double2float_rn(ev.cen[3 * sp + 1]),
+                        cz = __double2float_rn(ev.cen[3 * sp + 2]);
+            const int f = rggd::segf_filter(g, cx, cy, cz, (fabsf(cx) + fabsf(cy)) + fabsf(cz));
+            sure |= f == 1;
+            und |= static_cast<uint32_t>(f == 2) << sp;
+        }
+        if (sure) return true;
+        if (und) {
+            const double2* p = reinterpret_cast<const double2*>(s.seg + 8 * static_cast<size_t>(j));
+            const double2 w0 = p[0], w1 = p[1], w2 = p[2], w3 = p[3];
+            const double seg[7] = {w0.x, w0.y, w1.x, w1.y, w2.x, w2.y, w3.x};
+            const double r_total = add(ev.r, w3.y);  // o_minus_r + spline_radius[row] (engine_batch.cpp:97)
+            for (; und; und &= und - 1)
+                if (seg_exact(seg, ev.cen + 3 * (__ffs(und) - 1), r_total)) return true;
+        }
+    }
+    return false;
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -909,7 +939,7 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
                 if (inext < n_over) {
                     prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
                 } else {
-                    for (int j = nx.x; j < nx.y; j += 2) prefetch_l1(s.seg + 8 * static_cast<size_t>(j));
+                    for (int j = nx.x; j < nx.y; j += 4) prefetch_l1(s.seg32 + 2 * static_cast<size_t>(j));
                 }
             }
             if (i < n_over) {
@@ -918,8 +948,7 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
                     atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
             } else if (s.dbg_flags & 256) {  // 256: ablation, no under tests
             } else {
-                for (int j = it.x; j < it.y; ++j) prefetch_l1(s.seg + 8 * static_cast<size_t>(j));
-                if (under_range<false>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, nullptr) && !(s.dbg_flags & 1024))
+                if (under_range32(s, it.x, it.y, b.ev[it.w >> 5]) && !(s.dbg_flags & 1024))
                     atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
             }
             it = nx;
@@ -1532,7 +1561,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
                 prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, false);
             }
             if (sm && w == 0 && s.prefetch)
-                prefetch_range(s.seg + 8 * static_cast<size_t>(seg_lo), s.seg + 8 * static_cast<size_t>(seg_hi), false);
+                prefetch_range(s.seg32 + 2 * static_cast<size_t>(seg_lo), s.seg32 + 2 * static_cast<size_t>(seg_hi), false);
             const int wt = rec.y + (0 * W + w) * s.cell + t, wo = rec.y + (1 * W + w) * s.cell + t,
                       wu = rec.y + (2 * W + w) * s.cell + t;
             if (valid) {

@@ -46,7 +46,8 @@ struct Store {
     const double* sat;         // Np*B*22 (21 + pad)
     const rggd::Box32* sat32;  // Np*B fp32 filter operands of sat
     const int32_t* row;        // Np*B*S+1
-    const double* seg;         // T*8 (a, d, dd, pad)
+    const double* seg;         // T*8 (a, d, dd, spline radius)
+    const float4* seg32;       // T*2: the same record rounded to fp32 (narrow's filter operand)
     const double* spline_r;    // B*S
     const int32_t* orig;       // Np: sorted -> component id
     const double* cell_aabb;   // ncells*6
@@ -149,6 +150,7 @@ struct StoreOut {
     rggd::Box32* sat32;    // np*B
     int32_t* row;          // np*B*S+1
     double* seg;           // allocated here: total_segs*8
+    float4* seg32;         // allocated here: total_segs*2
     double* spline;        // B*S
     int32_t* orig;         // np
     int32_t* rank;         // N

@@ -126,17 +126,23 @@ __global__ void gather_kernel(const int32_t* owned, int np, int B, int BS, const
 
 // one thread per row of the sorted order: its real segments + the slot's spline radius
 __global__ void segs_kernel(const int32_t* owned, long long nrows, int BS, const int32_t* row_off_src,
-                            const int32_t* row_new, const double* segs7, const double* spline, double* seg8) {
+                            const int32_t* row_new, const double* segs7, const double* spline, double* seg8,
+                            float4* seg32) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= nrows) return;
     const int i = static_cast<int>(t / BS), r = static_cast<int>(t % BS);
     const size_t src = static_cast<size_t>(owned[i]) * BS + r;
     const int k0 = row_off_src[src], k1 = row_off_src[src + 1];
     double* d = seg8 + 8 * static_cast<size_t>(row_new[t]);
-    for (int k = k0; k < k1; ++k, d += 8) {
+    float4* f = seg32 + 2 * static_cast<size_t>(row_new[t]);
+    for (int k = k0; k < k1; ++k, d += 8, f += 2) {
         const double* s = segs7 + 7 * static_cast<size_t>(k);
         for (int j = 0; j < 7; ++j) d[j] = s[j];
         d[7] = spline[r];
+        f[0] = make_float4(__double2float_rn(s[0]), __double2float_rn(s[1]), __double2float_rn(s[2]),
+                           __double2float_rn(s[3]));
+        f[1] = make_float4(__double2float_rn(s[4]), __double2float_rn(s[5]), __double2float_rn(s[6]),
+                           __double2float_rn(spline[r]));
     }
 }
 
@@ -246,9 +252,10 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     SCK(cudaMemcpyAsync(&out.total_segs, out.row + nrows, 4, cudaMemcpyDeviceToHost, st));
     SCK(cudaStreamSynchronize(st));
     SCK(cudaMalloc(reinterpret_cast<void**>(&out.seg), sizeof(double) * std::max<size_t>(1, static_cast<size_t>(out.total_segs) * 8)));
+    SCK(cudaMalloc(reinterpret_cast<void**>(&out.seg32), sizeof(float4) * std::max<size_t>(1, static_cast<size_t>(out.total_segs) * 2)));
     if (nrows > 0)
         segs_kernel<<<static_cast<unsigned>((nrows + T256 - 1) / T256), T256, 0, st>>>(
-            out.orig, nrows, BS, row_off, out.row, segs7, out.spline, out.seg);
+            out.orig, nrows, BS, row_off, out.row, segs7, out.spline, out.seg, out.seg32);
     if (ncells > 0) {
         cell_box_kernel<<<(ncells + 127) / 128, 128, 0, st>>>(out.aabb, np, cell, ncells, out.cell_aabb);
         super_box_kernel<<<(nsuper + 127) / 128, 128, 0, st>>>(out.cell_aabb, ncells, nsuper, out.super_aabb);

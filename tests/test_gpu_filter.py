@@ -112,3 +112,49 @@ def test_seg_filter_adversarial():
     exp = oracle.seg_sphere_batch(segs, np.arange(N, dtype=np.int32), centre, r)
     assert 0 < exp.sum() < N
     assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} segment-sphere verdicts differ"
+
+
+@pytest.mark.parametrize("centre,o_r", [((1.1, -2.3, 0.6), 0.0), ((71.3, -69.9, 0.6), 0.25),
+                                        ((-3.0e3, 1.5e3, 7.0), 0.5)])
+def test_seg_filter_adversarial_update_path(centre, o_r):
+    """The narrow kernel's filter over the compact fp32 segment records
+    (rggd::segf_filter, rgg_kernels.cu under_range32): the same near-contact segments,
+    far from the origin too (the absolute error term of the rounded coordinates),
+    through a real update; RED iff the reference's seg_sphere hits."""
+    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+
+    rng = np.random.default_rng(int(abs(centre[0])) + 5)
+    r_spline = 0.7
+    r = r_spline + o_r
+    centre = np.array(centre)
+    segs = []
+    for trial in range(300):
+        n = rng.normal(size=3)
+        n /= np.linalg.norm(n)
+        t = np.cross(n, rng.normal(size=3))
+        t /= np.linalg.norm(t)
+        L = rng.uniform(0.0, 2.0) if trial % 5 else 0.0
+        shift = rng.uniform(-1.0, 1.0) * L
+        for off in OFFSETS:
+            base = centre + n * r * (1 + off)
+            a = base + t * (shift - L)
+            b = base + t * (shift + L)
+            if trial % 7 == 3:
+                a = base
+                b = base + n * L
+            segs.append(oracle.seg_prep(np.concatenate([a, b])))
+    segs = np.array(segs)
+    N = len(segs)
+    pose = np.array([1, 0, 0, 0, 1, 0, 0, 0, 1, *centre])
+    lv = LayoutView(N=N, B=1, S=1, M=1, C=1, edge_sat=np.zeros((N, 21)),
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (N, 1)).astype(np.float64),
+                    row_off=np.arange(N + 1, dtype=np.int32), segs=segs, spline_r=np.array([r_spline]),
+                    obst_he=np.ones((1, 3)), obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.array([o_r]),
+                    obst_sph_n=np.ones(1, np.int32))
+    eng = GpuEngine(lv)
+    eng.update_obstacle(0, pose)
+    got = eng.states() == 1
+    r_total = o_r + r_spline
+    exp = oracle.seg_sphere_batch(segs, np.arange(N, dtype=np.int32), centre, r_total).astype(bool)
+    assert 0 < exp.sum() < N
+    assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} segment-sphere verdicts differ"
