@@ -158,3 +158,49 @@ def test_seg_filter_adversarial_update_path(centre, o_r):
     exp = oracle.seg_sphere_batch(segs, np.arange(N, dtype=np.int32), centre, r_total).astype(bool)
     assert 0 < exp.sum() < N
     assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} segment-sphere verdicts differ"
+
+
+@pytest.mark.parametrize("origin", [(0.4, -0.3, 0.2), (70.7, -69.2, 0.2), (-2.5e3, 4.0e3, 15.0)])
+def test_sat_filter_adversarial_update_path(origin):
+    """The narrow kernel's over filter on the 64-byte heads with an fp32 centre
+    (rggd::sat_filter32h): near-contact boxes around an obstacle far from the origin too,
+    through a real update; GRAY iff the reference's sat_boxes intersects."""
+    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+
+    rng = np.random.default_rng(int(abs(origin[0])) + 17)
+    he_o = np.array([1.3, 0.7, 0.9])
+    Ro = rot(rng)
+    pose = np.concatenate([Ro.reshape(-1), origin])
+    osat, _, _, _ = oracle.obstacle_operands(he_o, np.zeros((1, 3)), 1, 0.1, pose)
+    boxes = []
+    for trial in range(150):
+        R = rot(rng) if trial % 3 else np.eye(3)
+        he = rng.uniform(0.05, 2.0, 3)
+        n = rng.normal(size=3)
+        n /= np.linalg.norm(n)
+        if trial % 3 == 0:
+            R = Ro.copy()
+            n = Ro[:, trial % 3]
+        lo, hi = 0.0, 20.0
+        for _ in range(80):
+            mid = 0.5 * (lo + hi)
+            s = oracle.sat_prep(corners(pose[9:] + mid * n, R, he))
+            lo, hi = (mid, hi) if oracle.sat_boxes(s, osat) else (lo, mid)
+        for off in OFFSETS:
+            t = lo * (1 + off) + off
+            boxes.append(oracle.sat_prep(corners(pose[9:] + t * n, R, he)))
+        boxes.append(oracle.sat_prep(corners(pose[9:] + np.nextafter(lo, 0) * n, R, he)))
+        boxes.append(oracle.sat_prep(corners(pose[9:] + np.nextafter(hi, 30) * n, R, he)))
+    boxes = np.array(boxes)
+    N = len(boxes)
+    lv = LayoutView(N=N, B=1, S=1, M=1, C=1, edge_sat=boxes,
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (N, 1)).astype(np.float64),
+                    row_off=np.zeros(N + 1, np.int32), segs=np.zeros((0, 7)), spline_r=np.zeros(1),
+                    obst_he=he_o[None, :], obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.array([0.1]),
+                    obst_sph_n=np.ones(1, np.int32))
+    eng = GpuEngine(lv)
+    eng.update_obstacle(0, pose)
+    got = eng.states() == 2
+    exp = oracle.sat_batch(boxes, np.arange(N, dtype=np.int32), osat).astype(bool)
+    assert 0 < exp.sum() < N
+    assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
