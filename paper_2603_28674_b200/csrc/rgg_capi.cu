@@ -91,6 +91,7 @@ struct rgg_gpu {
     uint8_t* d_last = nullptr;
     int32_t* d_unknown = nullptr;
     unsigned long long* d_dbg = nullptr;
+    int32_t* d_evready = nullptr;         // Batch::evready (split pipeline)
     unsigned long long* d_tl = nullptr;  // RGG_DEBUG_TIMELINE: 16 x 8 words (rgg_kernels.cu tl_stop)
     Event* d_ev = nullptr;
     int32_t* d_mv = nullptr;
@@ -265,6 +266,11 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     static const bool timeline = std::getenv("RGG_DEBUG_TIMELINE") != nullptr;
     if (timeline && !h->d_tl) cudaMalloc(reinterpret_cast<void**>(&h->d_tl), 128 * 8);
     b.tl = h->d_tl;
+    if (rggk::split_pipeline() && !h->d_evready) {
+        cudaMalloc(reinterpret_cast<void**>(&h->d_evready), sizeof(int32_t));
+        cudaMemset(h->d_evready, 0, sizeof(int32_t));
+    }
+    b.evready = rggk::split_pipeline() && !std::getenv("RGG_NO_EARLY_BIN") ? h->d_evready : nullptr;
     return b;
 }
 
@@ -702,7 +708,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
-                   h->d_mv, h->d_pool, h->d_tl, h->d_dbg, h->d_hits_prev,
+                   h->d_mv, h->d_pool, h->d_tl, h->d_dbg, h->d_hits_prev, h->d_evready,
                    h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_ids, h->d_res_cnt, h->d_res_out,
                    h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};
     for (void* p : dev)

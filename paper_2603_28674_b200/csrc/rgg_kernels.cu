@@ -226,6 +226,61 @@ __global__ void pose_kernel(Store s, Batch b) {
             }
         }
     }
+    // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
+    double bn[6], bo[6], bs[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        bn[k] = shfl(lo[k], 0), bn[3 + k] = shfl(hi[k], 0);
+        bo[k] = shfl(lo[k], 8), bo[3 + k] = shfl(hi[k], 8);
+        bs[k] = shfl(lo[k], 16), bs[3 + k] = shfl(hi[k], 16);
+    }
+    // the old spheres' box: recompute on lanes 16.. only when the obstacle moved earlier in this batch
+    double os[6];
+    if (p >= 0) {
+        double olo[3], ohi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            olo[k] = __longlong_as_double(0x7ff0000000000000ll);
+            ohi[k] = __longlong_as_double(0xfff0000000000000ll);
+        }
+        if (lane >= 16 && lane - 16 < nsph) {
+            const double* l = s.osl + (static_cast<size_t>(o) * s.C + (lane - 16)) * 3;
+            double q[3];
+            rggd::tf_apply(rt_old, l[0], l[1], l[2], q);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                olo[k] = sub(q[k], r);
+                ohi[k] = add(q[k], r);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                olo[k] = fmin(olo[k], __shfl_xor_sync(0xffffffffu, olo[k], off));
+                ohi[k] = fmax(ohi[k], __shfl_xor_sync(0xffffffffu, ohi[k], off));
+            }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            os[k] = fmin(bo[k], olo[k]);
+            os[3 + k] = fmax(bo[3 + k], ohi[k]);
+        }
+    }
+    // the binning boxes first: the bin kernel starts on them (Batch::evready)
+    double nu6 = 0.0, ol6 = 0.0;
+    if (lane < 6) {
+        nu6 = lane < 3 ? fmin(bn[lane], bs[lane]) : fmax(bn[lane], bs[lane]);
+        ol6 = p >= 0 ? os[lane] : s.cur_union[6 * o + lane];
+        b.evbox[12 * static_cast<size_t>(i) + lane] = nu6;  // compact copy for the binning
+        b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol6;
+    }
+    if (b.evready) {  // release: the warp's stores (evbox, and the counter resets of warp 0), then the count
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(b.evready, 1);
+        }
+    }
     // sat_prep (kernels_scalar.cpp:7-30): lane k < 3 derives axis k
     const int src = lane < 3 ? (1 << lane) : 0;
     double c0[3], ch[3], e[3], u[3];
@@ -268,57 +323,13 @@ __global__ void pose_kernel(Store s, Batch b) {
         rggd::box32_terms(ev.sat, ev.b32);
         for (int k = 0; k < 3; ++k) ev.b32.c[k] = ev.sat[k];
     }
-    // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
-    double bn[6], bo[6], bs[6];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        bn[k] = shfl(lo[k], 0), bn[3 + k] = shfl(hi[k], 0);
-        bo[k] = shfl(lo[k], 8), bo[3 + k] = shfl(hi[k], 8);
-        bs[k] = shfl(lo[k], 16), bs[3 + k] = shfl(hi[k], 16);
-    }
-    // the old spheres' box: recompute on lanes 16.. only when the obstacle moved earlier in this batch
-    double os[6];
-    if (p >= 0) {
-        double olo[3], ohi[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            olo[k] = __longlong_as_double(0x7ff0000000000000ll);
-            ohi[k] = __longlong_as_double(0xfff0000000000000ll);
-        }
-        if (lane >= 16 && lane - 16 < nsph) {
-            const double* l = s.osl + (static_cast<size_t>(o) * s.C + (lane - 16)) * 3;
-            double q[3];
-            rggd::tf_apply(rt_old, l[0], l[1], l[2], q);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                olo[k] = sub(q[k], r);
-                ohi[k] = add(q[k], r);
-            }
-        }
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                olo[k] = fmin(olo[k], __shfl_xor_sync(0xffffffffu, olo[k], off));
-                ohi[k] = fmax(ohi[k], __shfl_xor_sync(0xffffffffu, ohi[k], off));
-            }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            os[k] = fmin(bo[k], olo[k]);
-            os[3 + k] = fmax(bo[3 + k], ohi[k]);
-        }
-    }
     if (lane < 6) {
         ev.box[lane] = bn[lane];
         ev.sph[lane] = bs[lane];
-        const double nu = lane < 3 ? fmin(bn[lane], bs[lane]) : fmax(bn[lane], bs[lane]);
-        const double ol = p >= 0 ? os[lane] : s.cur_union[6 * o + lane];
-        ev.nu[lane] = nu;
-        ev.old[lane] = ol;
-        b.evbox[12 * static_cast<size_t>(i) + lane] = nu;  // compact copy for the binning
-        b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol;
+        ev.nu[lane] = nu6;
+        ev.old[lane] = ol6;
         double* et = b.evt + 24 * static_cast<size_t>(i);
-        et[lane] = nu, et[6 + lane] = ol, et[12 + lane] = bn[lane], et[18 + lane] = bs[lane];
+        et[lane] = nu6, et[6 + lane] = ol6, et[12 + lane] = bn[lane], et[18 + lane] = bs[lane];
     }
     if (lane < 12) ev.rt[lane] = rt_new[lane];
     if (b.src_ids) {  // the HBM copy the later kernels (and a replay) read
@@ -398,8 +409,21 @@ __device__ __forceinline__ bool overlaps32(const float* a, const float* b) {
 #endif
 __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s, Batch b) {
     const unsigned long long tw = tl_start(b.tl);
-    pdl_wait();
-    pdl_trigger();
+    if (b.evready) {
+        // the pose warps publish their binning boxes first (release: fence + count);
+        // the rest of the pose kernel overlaps this kernel, whose end waits for it
+        pdl_trigger();
+        if (threadIdx.x == 0) {
+            int r;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready) : "memory");
+            } while (r < b.n);
+        }
+        __syncthreads();
+    } else {
+        pdl_wait();
+        pdl_trigger();
+    }
     const unsigned long long t0 = tl_start(b.tl);
     tl_stop(b.tl, 5, tw);
     __shared__ float cbox[12][kBinChunk];  // SoA: lane q reads column q, conflict-free
@@ -478,7 +502,10 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
             count += __popc(hb);
         }
     }
-    if (!live) return;
+    if (!live) {
+        if (b.evready) pdl_wait();  // the grid ends after the pose kernel (touch waits on this grid only)
+        return;
+    }
     if (count > s.cap) {
         // Overflow: the full ordered list goes to the pool (second pass over the events).
         int pbase = 0;
@@ -533,6 +560,7 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
         b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
     }
     tl_stop(b.tl, 1, t0);
+    if (b.evready) pdl_wait();
 }
 
 // ----------------------------------------------------------------- classify
@@ -1639,6 +1667,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
     const bool staged = b.n <= kStageIds;
+    if (b.evready && blockIdx.x == 0 && threadIdx.x == 0) *b.evready = 0;  // for the next update's bin kernel
     if (staged) {
         for (int t = threadIdx.x; t < b.n; t += blockDim.x) s_ids[t] = b.ids[t];
         __syncthreads();

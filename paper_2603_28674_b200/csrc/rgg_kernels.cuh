@@ -108,6 +108,10 @@ struct Batch {
     // there and copies them to ids / rt; null when the moves are already in HBM
     const int32_t* src_ids;
     const double* src_rt;
+    // split pipeline: the pose warps count the events whose binning boxes (evbox) are
+    // stored, so the bin kernel starts before the pose kernel's remaining work ends;
+    // the apply kernel resets it.  Null: bin waits for the whole pose kernel.
+    int32_t* evready;
 };
 
 // Exact resolve operands (rgg_resolve.cu).
