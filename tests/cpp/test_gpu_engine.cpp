@@ -179,6 +179,105 @@ static void scenario_replay(const std::string& path) {
                 comps.count(), iterations);
 }
 
+// The semantic cases of proj/tests/test_sequential.cpp:83-184 on rgg::GpuEngine: one straight
+// edge along x (nodes 0 and 1 at x = 0 and 4, the edge is component 2) and box obstacles.
+struct Straight {
+    Scene scene;
+    Roadmap roadmap;
+    ComponentSet components;
+    explicit Straight(std::vector<ObstacleModel> obstacles) {
+        scene.bounds = {{-10, -10, -10}, {10, 10, 10}};
+        scene.robot = make_free_flying_box({0.5, 0.5, 0.5});
+        scene.obstacles = std::move(obstacles);
+        roadmap.nodes = {{0.0, 0, 0, 0, 0, 0}, {4.0, 0, 0, 0, 0, 0}};
+        roadmap.edges = {{0, 1}};
+        roadmap.rebuild_adjacency();
+        components = build_components(roadmap, scene.robot, default_body_spheres(scene.robot), 0.25, 16);
+    }
+};
+
+static void sequential_semantics() {
+    {  // far obstacle changes nothing (:83-96), eager
+        Straight fx({make_box_obstacle({1, 1, 1}, 1)});
+        GpuEngine g(fx.components, fx.scene, {});
+        const UpdateReport r = g.update_obstacle(0, Transform::translation({8, 8, 8}), false);
+        EXPECT(r.new_green + r.new_red + r.new_gray == 0 && g.unknown_count() == 0, "far obstacle");
+        bool all_valid = true;
+        for (ValidityState v : g.states()) all_valid &= v == ValidityState::Valid;
+        EXPECT(all_valid, "far obstacle leaves every label valid");
+    }
+    {  // an obstacle on a node's centre is red through the inner hit, lazily (:98-104)
+        Straight fx({make_box_obstacle({1, 1, 1}, 1)});
+        GpuEngine g(fx.components, fx.scene, {});
+        g.update_obstacle(0, Transform::translation({0, 0, 0}), true);
+        EXPECT(g.states()[0] == ValidityState::Invalid && g.states()[2] == ValidityState::Invalid, "inner hit");
+    }
+    for (bool lazy : {true, false}) {  // grazing overlap: gray when lazy, resolved red when eager (:106-126)
+        Straight fx({make_box_obstacle({0.5, 0.5, 0.5}, 1)});
+        GpuEngine g(fx.components, fx.scene, {});
+        const Transform graze = Transform::translation({2.0, 0.99, 0});
+        g.update_obstacle(0, graze, lazy);
+        EXPECT(g.states()[2] == (lazy ? ValidityState::Unknown : ValidityState::Invalid), "graze lazy=%d", lazy);
+    }
+    {  // departure restores green; a second obstacle keeps gray; bits 0b11 -> 0b10 -> 0 (:128-149)
+        Straight fx({make_box_obstacle({0.5, 0.5, 0.5}, 1), make_box_obstacle({0.5, 0.5, 0.5}, 1)});
+        GpuEngine g(fx.components, fx.scene, {});
+        g.update_obstacle(0, Transform::translation({2.0, 0, 0}), true);
+        EXPECT(g.states()[2] == ValidityState::Invalid, "revalidation step 1");
+        g.update_obstacle(1, Transform::translation({2.0, 0.99, 0}), true);
+        EXPECT(g.states()[2] == ValidityState::Invalid && g.obstacle_bits()[2] == 0b11, "revalidation step 2");
+        g.update_obstacle(0, Transform::translation({8, 8, 8}), true);
+        EXPECT(g.states()[2] == ValidityState::Unknown && g.obstacle_bits()[2] == 0b10, "revalidation step 3");
+        g.update_obstacle(1, Transform::translation({-8, 8, 8}), true);
+        EXPECT(g.states()[2] == ValidityState::Valid && g.obstacle_bits()[2] == 0, "revalidation step 4");
+    }
+    {  // red restored when the remaining obstacle still under-hits (:151-162)
+        Straight fx({make_box_obstacle({0.5, 0.5, 0.5}, 1), make_box_obstacle({0.5, 0.5, 0.5}, 1)});
+        GpuEngine g(fx.components, fx.scene, {});
+        g.update_obstacle(0, Transform::translation({1.0, 0, 0}), true);
+        g.update_obstacle(1, Transform::translation({3.0, 0, 0}), true);
+        EXPECT(g.states()[2] == ValidityState::Invalid, "red restored step 1");
+        g.update_obstacle(0, Transform::translation({8, 8, 8}), true);
+        EXPECT(g.states()[2] == ValidityState::Invalid && g.obstacle_bits()[2] == 0b10, "red restored step 2");
+    }
+    for (bool lazy : {true, false}) {  // idempotence: the same pose twice changes nothing (:164-184)
+        Scene scene;
+        scene.bounds = {{-6, -6, -6}, {6, 6, 6}};
+        scene.robot = make_free_flying_box({0.5, 0.5, 0.5});
+        scene.obstacles = {make_box_obstacle({1, 0.6, 0.6}, 2)};
+        const Roadmap roadmap = build_prm(scene, 40, 6, 0.25, 11);
+        const ComponentSet set = build_components(roadmap, scene.robot, default_body_spheres(scene.robot), 0.25, 16);
+        GpuEngine g(set, scene, {});
+        const Transform pose = Transform::translation({0.5, -0.3, 0.2});
+        g.update_obstacle(0, pose, lazy);
+        const auto states = g.states();
+        const auto bits = g.obstacle_bits();
+        g.update_obstacle(0, pose, lazy);
+        EXPECT(g.states() == states && g.obstacle_bits() == bits, "idempotence lazy=%d", lazy);
+    }
+}
+
+// proj/tests/test_batch.cpp:236-258: garbage in the layout's masked (padding) slots never
+// changes a mask.  The GPU never stores padding; the host layout stays the reference's own.
+static void padding_neutrality() {
+    Scenelet fx(40, 1, 54);
+    GpuEngine engine(fx.components, fx.scene, {});
+    engine.update_obstacle(0, Transform::translation({0.5, 0.5, 0}), true);
+    std::vector<ComponentId> all;
+    for (ComponentId c = 0; c < fx.components.count(); ++c) all.push_back(c);
+    std::vector<std::uint8_t> before, after;
+    engine.batch_under(all, 0, before);
+    BatchLayout& l = const_cast<BatchLayout&>(engine.layout());
+    Rng rng(1);
+    for (size_t slot = 0; slot < l.seg_mask.size(); ++slot) {
+        if (l.seg_mask[slot]) continue;
+        for (int j = 0; j < 6; ++j) l.e_minus[slot * 6 + j] = rng.uniform(-50, 50);
+    }
+    l.rebuild_segment_operands();
+    engine.batch_under(all, 0, after);
+    EXPECT(before == after, "padding neutrality");
+}
+
 static bool same_roadmap(const Roadmap& a, const Roadmap& b) {
     if (a.nodes.size() != b.nodes.size() || a.edges != b.edges || a.adjacency != b.adjacency) return false;
     for (size_t i = 0; i < a.nodes.size(); ++i)
@@ -243,6 +342,8 @@ int main(int argc, char** argv) {
     equivalence_after_every_move();
     narrow_masks_match_sequential();
     batch_update_matches_batch_engine();
+    padding_neutrality();
+    sequential_semantics();
     if (!dir.empty()) {
         scenario_replay(dir + "/quick_smoke.scn");
         scenario_replay(dir + "/table4_obstacles_1000_5x.scn");
