@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <limits>
+#include <atomic>
 #include <cstring>
 #include <chrono>
 #include <numeric>
@@ -841,6 +842,7 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
         // synchronous update with matching staging layouts: the copies are graph nodes
         const bool hostio = !(flags & RGG_ASYNC) && !bad && h->pin_off == h->in_off && graphs_enabled(h);
         if (hostio) {
+            reinterpret_cast<volatile int32_t*>(h->h_ctr)[31] = 0;
             rc = enqueue(h, k, flags | kHostIO);
             if (rc) return rc;
         } else if (h->pin_off == h->in_off) {  // same layout on both sides: one copy
@@ -860,7 +862,22 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
                                                 cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
             }
-            CK(cudaStreamSynchronize(h->stream));
+            if (hostio) {
+                // poll the flag the last kernel stores into mapped memory (lower wake-up latency
+                // than a stream sync); the stream is queried now and then so that a failed
+                // launch cannot hang the caller
+                volatile int32_t* flag = reinterpret_cast<volatile int32_t*>(h->h_ctr) + 31;
+                for (unsigned spins = 1; *flag == 0; ++spins) {
+                    if ((spins & 1023) == 0) {
+                        const cudaError_t q = cudaStreamQuery(h->stream);
+                        if (q == cudaSuccess) break;  // stream idle: the flag must be visible now
+                        if (q != cudaErrorNotReady) CK(q);
+                    }
+                }
+                std::atomic_thread_fence(std::memory_order_acquire);
+            } else {
+                CK(cudaStreamSynchronize(h->stream));
+            }
             dump_timeline(h);
             for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {
                 // the update was not applied (apply kernel skipped): grow the queue and replay it

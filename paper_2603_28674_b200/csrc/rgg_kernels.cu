@@ -1818,6 +1818,12 @@ __global__ void host_out_kernel(Batch b) {
     pdl_wait();
     for (int t = threadIdx.x; t < 4 * b.n; t += blockDim.x) b.out_mv[t] = b.mv[t];
     for (int t = threadIdx.x; t < 24; t += blockDim.x) b.out_ctr[t] = b.ctr[t];
+    // out_ctr[31]: "results stored", released to the host (it polls instead of a stream sync)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        reinterpret_cast<volatile int32_t*>(b.out_ctr)[31] = 1;
+    }
 }
 
 // --------------------------------------------------------------- compaction
