@@ -44,6 +44,7 @@ struct rgg_gpu {
     double* d_evbox = nullptr;
     double* d_evt = nullptr;
     int4* d_units = nullptr;
+    int32_t* d_unit_ready = nullptr;  // Batch::unit_ready: units_cap generation stamps
     int32_t units_cap = 0;
     double* d_ohe = nullptr;
     double* d_osl = nullptr;
@@ -92,7 +93,7 @@ struct rgg_gpu {
     uint8_t* d_last = nullptr;
     int32_t* d_unknown = nullptr;
     unsigned long long* d_dbg = nullptr;
-    int32_t* d_evready = nullptr;         // Batch::evready (split pipeline)
+    int32_t* d_evready = nullptr;         // Batch::evready[8] (split pipeline)
     unsigned long long* d_tl = nullptr;  // RGG_DEBUG_TIMELINE: 16 x 8 words (rgg_kernels.cu tl_stop)
     Event* d_ev = nullptr;
     int32_t* d_mv = nullptr;
@@ -167,6 +168,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     cudaFree(h->d_evbox);
     cudaFree(h->d_evt);
     cudaFree(h->d_units);
+    cudaFree(h->d_unit_ready);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
     cudaFree(h->d_mpool);
@@ -183,6 +185,8 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     if (units > INT32_MAX) return fail(h, RGG_ENOMEM, "batch too large for the touch work list; split it");
     h->units_cap = static_cast<int32_t>(units);
     CK(dalloc(&h->d_units, static_cast<size_t>(units)));
+    CK(dalloc(&h->d_unit_ready, static_cast<size_t>(units)));
+    CK(cudaMemset(h->d_unit_ready, 0, static_cast<size_t>(units) * sizeof(int32_t)));
     CK(dalloc(&h->d_mv, static_cast<size_t>(cap) * 4));
     // every (cell, event) pair fits: the overflow pool can never run out
     h->pool_cap = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * cap);
@@ -268,10 +272,18 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     if (timeline && !h->d_tl) cudaMalloc(reinterpret_cast<void**>(&h->d_tl), 128 * 8);
     b.tl = h->d_tl;
     if (rggk::split_pipeline() && !h->d_evready) {
-        cudaMalloc(reinterpret_cast<void**>(&h->d_evready), sizeof(int32_t));
-        cudaMemset(h->d_evready, 0, sizeof(int32_t));
+        cudaMalloc(reinterpret_cast<void**>(&h->d_evready), 8 * sizeof(int32_t));
+        cudaMemset(h->d_evready, 0, 8 * sizeof(int32_t));
     }
     b.evready = rggk::split_pipeline() && !std::getenv("RGG_NO_EARLY_BIN") ? h->d_evready : nullptr;
+    // touch on published units pays for large batches (c5: -6 %, c3: -2 %); for small ones
+    // its spinning warps slow the bin kernel they share SMs with (c2: +8 %, c4: +19 %)
+    static const int early_touch_min = [] {
+        const char* e = std::getenv("RGG_EARLY_TOUCH_MIN");
+        return e ? std::atoi(e) : 256;
+    }();
+    b.unit_ready = b.evready && n >= early_touch_min ? h->d_unit_ready : nullptr;
+    b.bin_warps = (h->s.ncells + rggk::kSuperCells - 1) / rggk::kSuperCells * rggk::kSuperCells;
     return b;
 }
 
@@ -705,7 +717,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,

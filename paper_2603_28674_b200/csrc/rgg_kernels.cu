@@ -163,6 +163,7 @@ __global__ void pose_kernel(Store s, Batch b) {
         b.census[lane] = 0;
         if (lane < 4) b.ctr[20 + lane] = 0;  // eager resolve report deltas
         if (lane == 0) *b.mtop = 0;
+        if (lane == 0 && b.unit_ready) b.evready[4] += 1;  // this update's generation (released below)
     }
     if (i >= b.n) return;
     // moves straight from mapped host memory (synchronous host updates) or from HBM
@@ -349,6 +350,13 @@ __global__ void pose_kernel(Store s, Batch b) {
         b.last[i] = is_last ? 1 : 0;
         reinterpret_cast<int4*>(b.mv)[i] = make_int4(0, 0, 0, 0);
     }
+    if (b.unit_ready) {  // release this event's operands to the touch kernel
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(b.evready + 1, 1);
+        }
+    }
     tl_stop(b.tl, 0, t0);
 }
 
@@ -402,6 +410,16 @@ __device__ __forceinline__ void box_out32(const double* d, float* f) {
 }
 __device__ __forceinline__ bool overlaps32(const float* a, const float* b) {
     return (a[0] <= b[3]) & (b[0] <= a[3]) & (a[1] <= b[4]) & (b[1] <= a[4]) & (a[2] <= b[5]) & (b[2] <= a[5]);
+}
+
+// a bin warp has released all its units (touch on published units counts them)
+__device__ __forceinline__ void bin_warp_done(const Batch& b, int lane) {
+    if (!b.unit_ready) return;
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        atomicAdd(b.evready + 2, 1);
+    }
 }
 
 #ifndef RGG_BIN_MINB
@@ -503,6 +521,7 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
         }
     }
     if (!live) {
+        bin_warp_done(b, lane);
         if (b.evready) pdl_wait();  // the grid ends after the pose kernel (touch waits on this grid only)
         return;
     }
@@ -537,9 +556,10 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
             if (lane == 0) b.cell_ovf[cell] = pbase;
         }
     }
+    __syncwarp();  // every lane's list entries precede the unit stamps below
     if (lane == 0) {
         b.cell_count[cell] = count;
-        int mbase = 0;
+        int mbase = 0, ub = 0, W = 0;
         if (count > 0) {
             b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
             // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
@@ -550,16 +570,22 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
             mbase = base + need > b.mpool_cap ? 0 : static_cast<int>(base);
             // one touch work unit per chunk of 32 listed events, carrying what the
             // touch kernel needs of the cell record
-            const int W = (count + 31) >> 5;
-            const int ub = atomicAdd(&b.ctr[10], W);
+            W = (count + 31) >> 5;
+            ub = atomicAdd(&b.ctr[10], W);
             for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int4(cell, w, count, mbase);
         }
         // one 16-byte record per cell: count, mask base, list address
         const int32_t* list = count <= s.cap ? inl : b.pool + b.cell_ovf[cell];
         const unsigned long long a = reinterpret_cast<unsigned long long>(list);
         b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
+        if (b.unit_ready && count > 0) {  // release the cell's units (record, list, mask base) to touch
+            const int gen = reinterpret_cast<volatile int32_t*>(b.evready)[4];
+            __threadfence();
+            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.unit_ready[ub + w] = gen;
+        }
     }
     tl_stop(b.tl, 1, t0);
+    bin_warp_done(b, lane);
     if (b.evready) pdl_wait();
 }
 
@@ -1473,8 +1499,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store 
 template <bool CENSUS>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, Batch b) {
     const unsigned long long tw = CENSUS ? 0 : tl_start(b.tl);
-    pdl_wait();
-    pdl_trigger();
+    // touch on published units (Batch::unit_ready): the event operands once every pose
+    // warp released them, then each unit once bin stamped it; otherwise the whole bin kernel
+    const bool flow = !CENSUS && b.unit_ready != nullptr;
+    if (flow) {
+        pdl_trigger();
+        if (threadIdx.x == 0) {
+            int r;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready + 1) : "memory");
+            } while (r < b.n);
+        }
+        __syncthreads();
+    } else {
+        pdl_wait();
+        pdl_trigger();
+    }
     const unsigned long long t0 = CENSUS ? 0 : tl_start(b.tl);
     if (!CENSUS) tl_stop(b.tl, 6, tw);
     // event operands: for small batches (n <= kStageEv) the whole batch is staged
@@ -1519,7 +1559,42 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     // walks every slice with all its chunks.
     const int spc = s.cell >> 5;  // slices per cell
     const int n_units = CENSUS ? nslices : min(b.ctr[10], b.units_cap) * spc;
-    for (int u = blockIdx.x * kWarpsPerCta + wi; u < n_units; u += gridDim.x * kWarpsPerCta) {
+    const int gen = flow ? reinterpret_cast<volatile int32_t*>(b.evready)[4] : 0;
+    // flow: slice-units are taken one at a time from a counter, and a unit is used once
+    // its stamp is this update's generation; the list ends when every bin warp is done
+    // and the index is past the final unit count
+    auto take = [&]() {
+        int v = 0;
+        if (lane == 0) v = atomicAdd(b.evready + 3, 1);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto available = [&](int u) {
+        if (!flow) return u < n_units;
+        const int unit = u / spc;
+        for (;;) {
+            int st = 0;
+            if (lane == 0) {
+                int r;
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.unit_ready + min(unit, b.units_cap - 1)) : "memory");
+                if (unit < b.units_cap && r == gen) {
+                    st = 1;
+                } else {
+                    int d;
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(d) : "l"(b.evready + 2) : "memory");
+                    if (d >= b.bin_warps) {
+                        const int cnt = min(reinterpret_cast<volatile int32_t*>(b.ctr)[10], b.units_cap);
+                        if (unit >= cnt) st = 2;  // past the end
+                    }
+                }
+            }
+            st = __shfl_sync(0xffffffffu, st, 0);
+            if (st == 1) return true;
+            if (st == 2) return false;
+            __nanosleep(64);
+        }
+    };
+    for (int u = flow ? take() : blockIdx.x * kWarpsPerCta + wi; available(u);
+         u = flow ? take() : u + gridDim.x * kWarpsPerCta) {
         int q = u, w_first = 0, w_last = 1 << 30;
         int4 rec;
         if (!CENSUS) {
@@ -1642,6 +1717,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
         if (lane == 0) dbgw[1] = gtimer(), dbgw[2] = dbg_slices, dbgw[3] = 0;
     }
     if (!CENSUS) tl_stop(b.tl, 2, t0);
+    if (flow) pdl_wait();  // the grid ends after bin's (narrow waits on this grid only)
     if (CENSUS) {
         unsigned long long v[5] = {c_dirty, c_box, c_sph, c_segs, c_touch};
 #pragma unroll
@@ -1667,7 +1743,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
     const bool staged = b.n <= kStageIds;
-    if (b.evready && blockIdx.x == 0 && threadIdx.x == 0) *b.evready = 0;  // for the next update's bin kernel
+    if (b.evready && blockIdx.x == 0 && threadIdx.x < 4) b.evready[threadIdx.x] = 0;  // for the next update
     if (staged) {
         for (int t = threadIdx.x; t < b.n; t += blockDim.x) s_ids[t] = b.ids[t];
         __syncthreads();

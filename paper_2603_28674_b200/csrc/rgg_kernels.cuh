@@ -112,6 +112,12 @@ struct Batch {
     // stored, so the bin kernel starts before the pose kernel's remaining work ends;
     // the apply kernel resets it.  Null: bin waits for the whole pose kernel.
     int32_t* evready;
+    // split pipeline, touch on published units: evready[1] = pose warps done,
+    // evready[2] = bin warps done, evready[3] = next touch slice-unit, evready[4] =
+    // update generation (never reset); bin stamps unit_ready[u] with the generation
+    // once unit u and its cell list are stored.  Null: touch waits for the whole bin kernel.
+    int32_t* unit_ready;
+    int32_t bin_warps;
 };
 
 // Exact resolve operands (rgg_resolve.cu).

@@ -221,6 +221,24 @@ def test_comparison_pipelines_stay_exact(pipeline):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}])
+def test_kernel_handoffs(env):
+    """The split pipeline's in-kernel handoffs, forced on or off for every batch size
+    (rgg_kernels.cu: bin on the pose warps' published boxes, touch on bin's published
+    units; by default touch waits for the whole bin kernel below 256 moves)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k",
+                        "replay or chunked or overflow or eager or resolve",
+                        os.path.join(here, "test_gpu_parity.py"), os.path.join(here, "test_gpu_resolve.py")],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 def test_degenerate_sizes(eng_mod):
     """Empty roadmap, no obstacles, a single component: create, update, query."""
     from paper_2603_28674_b200.engine import LayoutView
