@@ -93,6 +93,7 @@ struct rgg_gpu {
     uint8_t* d_last = nullptr;
     int32_t* d_unknown = nullptr;
     unsigned long long* d_dbg = nullptr;
+    cudaEvent_t done_ev = nullptr;        // stream_wait
     int32_t* d_evready = nullptr;         // Batch::evready[8] (split pipeline)
     unsigned long long* d_tl = nullptr;  // RGG_DEBUG_TIMELINE: 16 x 8 words (rgg_kernels.cu tl_stop)
     Event* d_ev = nullptr;
@@ -153,6 +154,20 @@ inline void clear_stale_error() { (void)cudaGetLastError(); }
         cudaError_t e_ = (expr);                                                                 \
         if (e_ != cudaSuccess) return fail(h, RGG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
+
+// Wait for the handle's stream by polling an event: cudaStreamSynchronize costs about
+// 11 us of wake-up per call on the B200 boxes, a poll about 1 us.
+cudaError_t stream_wait(rgg_gpu* h) {
+    if (!h->done_ev) {
+        const cudaError_t e = cudaEventCreateWithFlags(&h->done_ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(h->done_ev, h->stream);
+    if (e != cudaSuccess) return e;
+    while ((e = cudaEventQuery(h->done_ev)) == cudaErrorNotReady) {
+    }
+    return e;
+}
 
 template <class T>
 cudaError_t dalloc(T** p, size_t n) {
@@ -344,7 +359,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     static const bool debug = std::getenv("RGG_DEBUG_PHASES") != nullptr;
     auto phase = [&](const char* name) -> int {
         if (!debug) return RGG_OK;
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
         std::fprintf(stderr, "[rgg] %s done\n", name);
         return RGG_OK;
     };
@@ -438,7 +453,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         const size_t nw = region == 0 ? static_cast<size_t>(h->grid_classify) * 4 : ns;
         std::vector<unsigned long long> t(nw * 4);
         CK(cudaMemcpyAsync(t.data(), b.dbg + (region ? 8 * ns : 0), t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
         std::fprintf(stderr, "[rgg] %s ", region == 0 ? "narrow" : "touch ");
         unsigned long long lo = ~0ull, hi = 0;
         std::vector<double> st, du;
@@ -472,7 +487,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         const size_t ns = static_cast<size_t>((h->s.Np + 31) / 32);
         std::vector<unsigned long long> t(ns * 16);
         CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
         // sections: comp loads, staging, masks, worklist, narrow, transitions+, writes
         double acc[2][7] = {}, cnt[2] = {0, 0}, lo = 1e300, hi = 0;
         for (size_t q = 0; q < ns; ++q) {
@@ -513,7 +528,7 @@ int refresh_unknown(rgg_gpu* h) {
     if (!h->unknown_stale) return RGG_OK;
     int32_t v = 0;
     CK(cudaMemcpyAsync(&v, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     h->unknown = v;
     h->unknown_stale = false;
     return RGG_OK;
@@ -651,7 +666,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
         std::vector<uint8_t> st(static_cast<size_t>(N), 0xFF);
         for (int32_t c : h->orig) st[c] = 0;
         CK(cudaMemcpyAsync(h->d_state, st.data(), st.size(), cudaMemcpyHostToDevice, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
     }
     CK(cudaMemsetAsync(h->d_state_c, 0, static_cast<size_t>(Np) + 16, h->stream));
     CK(cudaMemsetAsync(h->d_cnt, 0, static_cast<size_t>(Np) * sizeof(uint32_t), h->stream));
@@ -706,7 +721,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     h->grid_classify = std::max(1, std::min(ncells, h->sms * rggk::classify_occupancy(cell, rggk::kPerMove)));
     const int rc = grow_batch(h, 64);
     if (rc) return rc;
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     mark("batch");
     h->unknown = 0;
     h->unknown_stale = false;
@@ -717,6 +732,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->done_ev) cudaEventDestroy(h->done_ev);
     void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
@@ -806,7 +822,7 @@ static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int3
         CK(cudaMemcpyAsync(h->h_eg_rep, h->d_eg_rep, static_cast<size_t>(k) * 8 * sizeof(int32_t),
                            cudaMemcpyDeviceToHost, h->stream));
         CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
         if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, "eager update: device pool overflow");
         int32_t u = h->unknown;
         for (int32_t i = 0; i < k; ++i) {
@@ -888,7 +904,7 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
                 }
                 std::atomic_thread_fence(std::memory_order_acquire);
             } else {
-                CK(cudaStreamSynchronize(h->stream));
+                CK(stream_wait(h));
             }
             dump_timeline(h);
             for (int attempt = 0; h->h_ctr[6] == 3 && attempt < 4; ++attempt) {
@@ -900,7 +916,7 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
                 if (reports) CK(cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(k) * 4 * sizeof(int32_t),
                                                 cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaStreamSynchronize(h->stream));
+                CK(stream_wait(h));
             }
             if (h->h_ctr[6])
                 return fail(h, RGG_ELOGIC, h->h_ctr[6] == 1   ? "overflow pool exhausted"
@@ -969,7 +985,7 @@ int rgg_gpu_sync(rgg_gpu* h) {
     CK(cudaSetDevice(h->device));
     int32_t err = 0;
     CK(cudaMemcpyAsync(&err, h->d_ctr + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     dump_timeline(h);
     if (err == 3) {
         int32_t need[2] = {0, 0};
@@ -996,7 +1012,7 @@ int rgg_gpu_read_states(rgg_gpu* h, uint8_t* out) {
     if (!h || !out) return RGG_EINVAL;
     CK(cudaSetDevice(h->device));
     CK(cudaMemcpyAsync(out, h->d_state, h->s.N, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     return RGG_OK;
 }
 
@@ -1008,7 +1024,7 @@ int rgg_gpu_read_bits(rgg_gpu* h, uint64_t* out, int32_t words_per_comp) {
     std::vector<uint64_t> w(static_cast<size_t>(h->words) * Np);
     if (!w.empty()) {
         CK(cudaMemcpyAsync(w.data(), h->d_over, w.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
     }
     std::memset(out, 0, static_cast<size_t>(h->s.N) * words_per_comp * 8);
     for (int32_t i = 0; i < Np; ++i)
@@ -1039,7 +1055,7 @@ int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
     if (out && cap > 0 && h->unknown > 0) {
         CK(cudaMemcpyAsync(out, h->d_gray, std::min(cap, h->unknown) * sizeof(int32_t), cudaMemcpyDeviceToHost,
                            h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
     }
     return RGG_OK;
 }
@@ -1050,11 +1066,11 @@ int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
     CK(cudaSetDevice(h->device));
     int32_t cnt = 0;
     CK(cudaMemcpyAsync(&cnt, h->d_ctr + 5, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     *n = cnt;
     if (out && cap > 0 && cnt > 0) {
         CK(cudaMemcpyAsync(out, h->d_hits, std::min(cap, cnt) * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
         std::sort(out, out + std::min(cap, cnt));
     }
     return RGG_OK;
@@ -1077,7 +1093,7 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
     CK(rggk::launch_write_states(h->s, d_ids, d_st, n, h->stream));
     CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
     CK(cudaMemcpyAsync(h->d_unknown, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     h->gray_fresh = true;
     cudaFree(d_ids);
     cudaFree(d_st);
@@ -1089,7 +1105,7 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
 int rgg_gpu_filter_stats(rgg_gpu* h, int64_t* sat_rechecks, int64_t* seg_rechecks, int32_t reset) {
     if (!h) return RGG_EINVAL;
     CK(cudaSetDevice(h->device));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     unsigned long long fs[4] = {0, 0, 0, 0};
     rggk::filter_stats(fs, reset != 0);
     if (sat_rechecks) *sat_rechecks = static_cast<int64_t>(fs[1]);
@@ -1146,7 +1162,7 @@ int rgg_gpu_resolve_all(rgg_gpu* h, int32_t* resolved) {
         const Batch b = batch_of(h, 1);
         CK(rggk::launch_resolve(h->s, resolver_of(h), b, h->d_gray, h->d_ctr + 4, n, rggk::kResolve, nullptr,
                                 h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        CK(stream_wait(h));
     }
     h->gray_fresh = false;
     h->unknown_stale = true;
@@ -1172,7 +1188,7 @@ int rgg_gpu_exact_check(rgg_gpu* h, const int32_t* ids, int32_t n, uint8_t* out)
     CK(rggk::launch_resolve(h->s, resolver_of(h), b, h->d_res_ids, h->d_res_cnt, n, rggk::kCheck, h->d_res_out,
                             h->stream));
     CK(cudaMemcpyAsync(out, h->d_res_out, n, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     return RGG_OK;
 }
 
@@ -1191,7 +1207,7 @@ int rgg_gpu_pair_masks(rgg_gpu* h, int32_t kind, const int32_t* cand, int32_t n,
     CK(cudaMemcpyAsync(d_c, cand, n * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
     CK(rggk::launch_pair_masks(h->s, h->d_rank, kind, d_c, n, o, d_m, h->stream));
     CK(cudaMemcpyAsync(mask, d_m, n, cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     cudaFree(d_c);
     cudaFree(d_m);
     return RGG_OK;
@@ -1202,7 +1218,7 @@ int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out) {
     std::memset(out, 0, sizeof(*out));
     if (!h->timed) return RGG_OK;
     CK(cudaSetDevice(h->device));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     float t[5] = {0, 0, 0, 0, 0};
     if (h->phase_timing)
         for (int p = 0; p < 4; ++p) CK(cudaEventElapsedTime(&t[p], h->ev[p], h->ev[p + 1]));
@@ -1233,7 +1249,7 @@ int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
     CK(rggk::launch_classify(h->s, b, rggk::kCensus, h->grid_classify, h->stream));
     unsigned long long c[16];
     CK(cudaMemcpyAsync(c, h->d_census, sizeof(c), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    CK(stream_wait(h));
     out->over_pairs = static_cast<int64_t>(c[0]);
     out->sat_flops = static_cast<int64_t>(c[1]);
     out->under_pairs = static_cast<int64_t>(c[2]);
