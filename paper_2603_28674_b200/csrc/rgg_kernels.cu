@@ -1752,8 +1752,24 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     // a full narrow-item queue left some verdicts uncomputed: apply nothing, so the
     // engine stays at its pre-update state and the host can grow the queue and replay
     const int full = b.ctr[6];
-    for (int q = blockIdx.x * kWarpsPerCta + wi; q < nslices; q += gridDim.x * kWarpsPerCta) {
+    // Work list: when fewer than half the cells are dirty, the dirty slices only, from
+    // touch's work units (a cell's first chunk stands for the cell: {cell, 0, count,
+    // mask base}); otherwise every slice, with its state loads issued before the cell
+    // record's (one round trip less on the chain).  c4: -14 %; c5 would lose 2.5 %.
+    // RGG_DEBUG_FLAGS 16384 forces the every-slice walk.
+    const bool dirty_only = (s.dbg_flags & 16384) == 0 && 2 * b.ctr[0] < s.ncells;
+    const int spc = s.cell >> 5;
+    const int n_work = dirty_only ? min(b.ctr[10], b.units_cap) * spc : nslices;
+    for (int wq = blockIdx.x * kWarpsPerCta + wi; wq < n_work; wq += gridDim.x * kWarpsPerCta) {
+        int q = wq;
+        int4 un = make_int4(0, 0, 0, 0);
+        if (dirty_only) {
+            un = b.units[wq / spc];
+            if (un.y != 0) continue;  // warp-uniform: a later chunk of a listed cell
+            q = un.x * spc + wq % spc;
+        }
         const int c0 = q << 5;
+        if (c0 >= s.Np) continue;
         const int cell = c0 / s.cell;
         const int c = c0 + lane, t = c - cell * s.cell;
         const bool valid = c < s.Np;
@@ -1771,7 +1787,14 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
             }
             label = s.state_c[c];
         }
-        const int4 rec = b.crec[cell];
+        int4 rec;
+        if (dirty_only) {
+            const int32_t* lst = un.z <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap : b.pool + b.cell_ovf[cell];
+            const unsigned long long la = reinterpret_cast<unsigned long long>(lst);
+            rec = make_int4(un.z, un.w, static_cast<int>(la & 0xffffffffu), static_cast<int>(la >> 32));
+        } else {
+            rec = b.crec[cell];
+        }
         const int count = rec.x;
         if (full == 3) break;  // warp-uniform
         if (count == 0) continue;
