@@ -298,7 +298,7 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
         return e ? std::atoi(e) : 256;
     }();
     b.unit_ready = b.evready && n >= early_touch_min ? h->d_unit_ready : nullptr;
-    b.bin_warps = (h->s.ncells + rggk::kSuperCells - 1) / rggk::kSuperCells * rggk::kSuperCells;
+    b.bin_warps = h->s.ncells;  // one counted warp per cell, whichever bin kernel runs
     return b;
 }
 

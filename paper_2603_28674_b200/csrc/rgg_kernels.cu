@@ -412,7 +412,43 @@ __device__ __forceinline__ bool overlaps32(const float* a, const float* b) {
     return (a[0] <= b[3]) & (b[0] <= a[3]) & (a[1] <= b[4]) & (b[1] <= a[4]) & (a[2] <= b[5]) & (b[2] <= a[5]);
 }
 
-// a bin warp has released all its units (touch on published units counts them)
+// The per-cell record of a listed cell (lane 0 after the warp's list stores): count,
+// dirty list, mask block, touch work units, the 16-byte cell record, and the unit
+// stamps of the early-touch handoff.
+__device__ __forceinline__ void bin_cell_tail(const Store& s, const Batch& b, int cell, int count,
+                                              const int32_t* inl, int lane) {
+    __syncwarp();  // every lane's list entries precede the unit stamps below
+    if (lane == 0) {
+        b.cell_count[cell] = count;
+        int mbase = 0, ub = 0, W = 0;
+        if (count > 0) {
+            b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
+            // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
+            const long long need = 3ll * ((count + 31) >> 5) * s.cell;
+            const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
+                                             static_cast<unsigned long long>(need));
+            if (base + need > b.mpool_cap) atomicExch(&b.ctr[6], 2);
+            mbase = base + need > b.mpool_cap ? 0 : static_cast<int>(base);
+            // one touch work unit per chunk of 32 listed events, carrying what the
+            // touch kernel needs of the cell record
+            W = (count + 31) >> 5;
+            ub = atomicAdd(&b.ctr[10], W);
+            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int4(cell, w, count, mbase);
+        }
+        // one 16-byte record per cell: count, mask base, list address
+        const int32_t* list = count <= s.cap ? inl : b.pool + b.cell_ovf[cell];
+        const unsigned long long a = reinterpret_cast<unsigned long long>(list);
+        b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
+        if (b.unit_ready && count > 0) {  // release the cell's units (record, list, mask base) to touch
+            const int gen = reinterpret_cast<volatile int32_t*>(b.evready)[4];
+            __threadfence();
+            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.unit_ready[ub + w] = gen;
+        }
+    }
+}
+
+// a cell's warp has released all its units (touch on published units waits for
+// every cell: Batch::bin_warps = ncells)
 __device__ __forceinline__ void bin_warp_done(const Batch& b, int lane) {
     if (!b.unit_ready) return;
     __syncwarp();
@@ -521,7 +557,6 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
         }
     }
     if (!live) {
-        bin_warp_done(b, lane);
         if (b.evready) pdl_wait();  // the grid ends after the pose kernel (touch waits on this grid only)
         return;
     }
@@ -556,34 +591,81 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
             if (lane == 0) b.cell_ovf[cell] = pbase;
         }
     }
-    __syncwarp();  // every lane's list entries precede the unit stamps below
-    if (lane == 0) {
-        b.cell_count[cell] = count;
-        int mbase = 0, ub = 0, W = 0;
-        if (count > 0) {
-            b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
-            // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
-            const long long need = 3ll * ((count + 31) >> 5) * s.cell;
-            const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
-                                             static_cast<unsigned long long>(need));
-            if (base + need > b.mpool_cap) atomicExch(&b.ctr[6], 2);
-            mbase = base + need > b.mpool_cap ? 0 : static_cast<int>(base);
-            // one touch work unit per chunk of 32 listed events, carrying what the
-            // touch kernel needs of the cell record
-            W = (count + 31) >> 5;
-            ub = atomicAdd(&b.ctr[10], W);
-            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int4(cell, w, count, mbase);
+    bin_cell_tail(s, b, cell, count, inl, lane);
+    tl_stop(b.tl, 1, t0);
+    bin_warp_done(b, lane);
+    if (b.evready) pdl_wait();
+}
+
+// Small batches (n <= 64 moves): one warp per cell, no super-cell stage.  Lane l
+// tests events l and l + 32 (exact fp64 closed-box tests of the new and old
+// boxes), two ordered ballots build the list.  Small warps-per-CTA so every cell's
+// warp is resident in one wave even for a million components (c4: 8400 cells).
+constexpr int kBinSmallMax = 64;
+constexpr int kBinSmallWarps = 8;
+
+__global__ void __launch_bounds__(32 * kBinSmallWarps) bin_small_kernel(Store s, Batch b) {
+    const unsigned long long tw = tl_start(b.tl);
+    if (b.evready) {
+        pdl_trigger();
+        if (threadIdx.x == 0) {
+            int r;
+            do {
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready) : "memory");
+            } while (r < b.n);
         }
-        // one 16-byte record per cell: count, mask base, list address
-        const int32_t* list = count <= s.cap ? inl : b.pool + b.cell_ovf[cell];
-        const unsigned long long a = reinterpret_cast<unsigned long long>(list);
-        b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
-        if (b.unit_ready && count > 0) {  // release the cell's units (record, list, mask base) to touch
-            const int gen = reinterpret_cast<volatile int32_t*>(b.evready)[4];
-            __threadfence();
-            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.unit_ready[ub + w] = gen;
+        __syncthreads();
+    } else {
+        pdl_wait();
+        pdl_trigger();
+    }
+    const unsigned long long t0 = tl_start(b.tl);
+    tl_stop(b.tl, 5, tw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cell = blockIdx.x * kBinSmallWarps + warp;
+    if (cell >= s.ncells) {
+        if (b.evready) pdl_wait();
+        return;
+    }
+    double cb[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) cb[k] = s.cell_aabb[6 * static_cast<size_t>(cell) + k];
+    unsigned bal[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int e = 32 * h + lane;
+        bool hit = false;
+        if (e < b.n) {
+            const double* bx = b.evbox + 12 * static_cast<size_t>(e);
+            hit = rggd::overlaps(cb, bx) | rggd::overlaps(cb, bx + 6);
+        }
+        bal[h] = __ballot_sync(0xffffffffu, hit);
+    }
+    int count = __popc(bal[0]) + __popc(bal[1]);
+    int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
+    int32_t* dst = inl;
+    if (count > s.cap) {  // the ordered list goes to the pool
+        int pbase = 0;
+        if (lane == 0) {
+            pbase = atomicAdd(&b.ctr[1], count);
+            atomicAdd(&b.ctr[3], 1);
+        }
+        pbase = __shfl_sync(0xffffffffu, pbase, 0);
+        if (pbase + count > b.pool_cap) {
+            if (lane == 0) atomicExch(&b.ctr[6], 1);
+            count = s.cap;  // truncated: reported as an error by the host
+        } else {
+            dst = b.pool + pbase;
+            if (lane == 0) b.cell_ovf[cell] = pbase;
         }
     }
+    const int lim = count;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int pos = (h ? __popc(bal[0]) : 0) + __popc(bal[h] & ((1u << lane) - 1u));
+        if (((bal[h] >> lane) & 1u) && pos < lim) dst[pos] = 32 * h + lane;
+    }
+    bin_cell_tail(s, b, cell, count, inl, lane);
     tl_stop(b.tl, 1, t0);
     bin_warp_done(b, lane);
     if (b.evready) pdl_wait();
@@ -2119,6 +2201,10 @@ cudaError_t launch_init_obstacles(const Store& s, Event*, cudaStream_t st) {
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
     if (s.ncells == 0) return cudaSuccess;  // no components: nothing to bin
     const int cells_per = kBinThreads / 32;  // = kSuperCells
+    static const bool no_small = std::getenv("RGG_NO_SMALL_BIN") != nullptr;
+    if (b.n <= kBinSmallMax && !no_small)
+        return launch_pdl(bin_small_kernel, dim3((s.ncells + kBinSmallWarps - 1) / kBinSmallWarps),
+                          dim3(32 * kBinSmallWarps), st, s, b);
     return launch_pdl(bin_kernel, dim3((s.ncells + cells_per - 1) / cells_per), dim3(kBinThreads), st, s, b);
 }
 

@@ -113,7 +113,7 @@ struct Batch {
     // the apply kernel resets it.  Null: bin waits for the whole pose kernel.
     int32_t* evready;
     // split pipeline, touch on published units: evready[1] = pose warps done,
-    // evready[2] = bin warps done, evready[3] = next touch slice-unit, evready[4] =
+    // evready[2] = cells binned (one count per cell's warp), evready[3] = next touch slice-unit, evready[4] =
     // update generation (never reset); bin stamps unit_ready[u] with the generation
     // once unit u and its cell list are stored.  Null: touch waits for the whole bin kernel.
     int32_t* unit_ready;
