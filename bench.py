@@ -530,16 +530,16 @@ def main():
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     # dram__bytes_read.sum + dram__bytes_write.sum of the classify kernel from the committed
-    # `ncu --set full` capture (profiles/r1e_classify_ncu.json); null when absent
+    # `ncu --set full` capture (profiles/r1f_classify_ncu.json); null when absent
     roof["traffic"] = None
-    pf = os.path.join(ROOT, "profiles", "r1e_classify_ncu.json")
+    pf = os.path.join(ROOT, "profiles", "r1f_classify_ncu.json")
     if os.path.exists(pf):
         try:
             p = json.load(open(pf))
             unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             rd, wr = p["dram__bytes_read.sum"], p["dram__bytes_write.sum"]
             roof["traffic"] = float(rd[0]) * unit[rd[1]] + float(wr[0]) * unit[wr[1]]
-            roof["traffic_source"] = "profiles/r1e_classify_ncu.json (ncu --set full, one c2 update, 3 kernels)"
+            roof["traffic_source"] = "profiles/r1f_classify_ncu.json (ncu --set full, one c2 update, 3 kernels)"
         except (KeyError, ValueError):
             pass
     roof["kernel"] = ("classify stage = touch_warp_kernel + narrow_kernel + apply_warp_kernel "
