@@ -77,9 +77,11 @@ def test_replay_one_batch(eng_mod, name):
 
 
 @pytest.mark.parametrize("name", ["scn_table4_obstacles_1000_5x", "syn_se2_m80"])
-@pytest.mark.parametrize("chunk", [7, 64])
+@pytest.mark.parametrize("chunk", [7, 64, 100, 300])
 def test_replay_chunked_lazy(eng_mod, name, chunk):
-    """Lazy batches without per-move reports (the bench path); final state is the reference's."""
+    """Lazy batches without per-move reports (the bench path); final state is the reference's.
+    Chunks of <= 64 moves use bin_small_kernel, larger ones bin_kernel, >= 256 also touch on
+    published units; a cell capacity of 4 puts the overflow pool in use in all of them."""
     g = load_golden(name)
     eng = eng_mod.GpuEngine(_layout(g), cell_size=64, cell_capacity=4)  # tiny capacity: overflow pool in use
     ids, rts = g["ids"], g["rts"]
