@@ -921,6 +921,7 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
             if (h->h_ctr[6])
                 return fail(h, RGG_ELOGIC, h->h_ctr[6] == 1   ? "overflow pool exhausted"
                                            : h->h_ctr[6] == 2 ? "mask pool exhausted"
+                                           : h->h_ctr[6] == 4 ? "device handoff timed out"
                                                               : "narrow item queue full (split the batch)");
             h->unknown = h->h_ctr[16];
             h->unknown_stale = false;

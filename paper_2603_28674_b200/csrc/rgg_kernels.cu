@@ -34,6 +34,15 @@ namespace {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// In-kernel handoffs (Batch::evready, unit_ready) spin on counters another kernel
+// raises; a spin that outlasts ~1 s (2^23 polls with back-off) gives up with status 4
+// (ctr[6]) instead of hanging the GPU, and the host fails the update.
+__device__ __forceinline__ bool handoff_timeout(const Batch& b, unsigned spins) {
+    if (spins < (1u << 23)) return false;
+    atomicExch(&b.ctr[6], 4);
+    return true;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -468,10 +477,12 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
         // the rest of the pose kernel overlaps this kernel, whose end waits for it
         pdl_trigger();
         if (threadIdx.x == 0) {
-            int r;
-            do {
+            for (unsigned spins = 0;; ++spins) {
+                int r;
                 asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready) : "memory");
-            } while (r < b.n);
+                if (r >= b.n || handoff_timeout(b, spins)) break;
+                __nanosleep(32);
+            }
         }
         __syncthreads();
     } else {
@@ -609,10 +620,12 @@ __global__ void __launch_bounds__(32 * kBinSmallWarps) bin_small_kernel(Store s,
     if (b.evready) {
         pdl_trigger();
         if (threadIdx.x == 0) {
-            int r;
-            do {
+            for (unsigned spins = 0;; ++spins) {
+                int r;
                 asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready) : "memory");
-            } while (r < b.n);
+                if (r >= b.n || handoff_timeout(b, spins)) break;
+                __nanosleep(32);
+            }
         }
         __syncthreads();
     } else {
@@ -1587,10 +1600,12 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     if (flow) {
         pdl_trigger();
         if (threadIdx.x == 0) {
-            int r;
-            do {
+            for (unsigned spins = 0;; ++spins) {
+                int r;
                 asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready + 1) : "memory");
-            } while (r < b.n);
+                if (r >= b.n || handoff_timeout(b, spins)) break;
+                __nanosleep(32);
+            }
         }
         __syncthreads();
     } else {
@@ -1653,7 +1668,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     auto available = [&](int u) {
         if (!flow) return u < n_units;
         const int unit = u / spc;
-        for (;;) {
+        for (unsigned spins = 0;; ++spins) {
             int st = 0;
             if (lane == 0) {
                 int r;
@@ -1668,6 +1683,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
                         if (unit >= cnt) st = 2;  // past the end
                     }
                 }
+                if (st == 0 && handoff_timeout(b, spins)) st = 2;
             }
             st = __shfl_sync(0xffffffffu, st, 0);
             if (st == 1) return true;
