@@ -9,6 +9,8 @@
  *                      (min, max) pairs — the roadmap's edges when no obstacle is active (:95-101).
  * dof_bounds_for (roadmap.cpp:20-30) gives lo/hi: env then [-pi, pi]^3 for a free-flying robot,
  * [-pi, pi] per joint for a serial chain.  Lives in lib/librgg_build.so (device 0).
+ * Not reentrant: one call at a time per process (the device buffers are a grow-only arena
+ * reused across calls).
  */
 #ifndef RGG_PRM_H
 #define RGG_PRM_H
