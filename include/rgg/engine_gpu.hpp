@@ -18,8 +18,9 @@
 //    every body at every discretized configuration: on first use the wrapper
 //    evaluates the reference's own forward_kinematics (robot.cpp:66-84) over
 //    components.cfgs once and uploads it (rgg_gpu_set_resolver).  The GPU checks
-//    against the obstacles this engine has moved, so a Scene whose obstacles are
-//    active before the engine moves them is rejected with std::logic_error.
+//    against the obstacles this engine has moved at their engine poses, and
+//    against the Scene's other active obstacles at their scene poses (listed
+//    before every exact resolve, rgg_gpu_set_active_obstacles).
 // Not provided: grid() (the GPU engine has no SpatialGrid; its cells are the
 // cell-sorted component blocks of rgg_gpu_create).
 #pragma once
@@ -212,9 +213,21 @@ private:
     // The exact resolve's inputs, once: forward_kinematics of every configuration
     // (body-major per configuration) and the body half extents.
     void ensure_resolver() {
+        // obstacles active in the Scene that this engine has not moved: checked at their scene pose
+        std::vector<std::int32_t> sid;
+        std::vector<double> srt;
         for (size_t o = 0; o < scene_.obstacles.size(); ++o)
-            if (scene_.obstacles[o].active && !moved_[o])
-                throw std::logic_error("GPU exact resolve: obstacle active before this engine moved it");
+            if (scene_.obstacles[o].active && !moved_[o]) {
+                const Transform& p = scene_.obstacles[o].pose;
+                sid.push_back(static_cast<std::int32_t>(o));
+                for (double r : p.r) srt.push_back(r);
+                srt.push_back(p.t.x), srt.push_back(p.t.y), srt.push_back(p.t.z);
+            }
+        if (sid != static_ids_ || srt != static_rt_) {
+            check(rgg_gpu_set_active_obstacles(h_, sid.data(), srt.data(), static_cast<std::int32_t>(sid.size())));
+            static_ids_ = std::move(sid);
+            static_rt_ = std::move(srt);
+        }
         if (resolver_ready_) return;
         const RobotModel& m = scene_.robot;
         const int B = static_cast<int>(m.bodies.size());
@@ -251,6 +264,8 @@ private:
     std::int32_t words_ = 1;
     mutable bool stale_ = false;
     bool resolver_ready_ = false;
+    std::vector<std::int32_t> static_ids_;  // the scene-active list last uploaded
+    std::vector<double> static_rt_;
     std::vector<std::uint8_t> moved_ = std::vector<std::uint8_t>(scene_.obstacles.size(), 0);
     mutable std::vector<ValidityState> states_;
     mutable std::vector<std::uint64_t> bits_;

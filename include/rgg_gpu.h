@@ -155,8 +155,8 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
  * configurations are [pose_off[c], pose_off[c+1]), and configuration k's body b
  * has the world pose poses[(k*B + b)*12 ..] (row-major rotation r[9], then t[3]),
  * i.e. forward_kinematics(robot, cfgs[c][j])[b].  Obstacles are exact-checked at
- * the poses this engine's moves gave them (active after their first move, like
- * the reference's Scene when it starts with inactive obstacles). */
+ * the poses this engine's moves gave them (active after their first move), plus
+ * those rgg_gpu_set_active_obstacles lists (active in the Scene before). */
 typedef struct rgg_resolve_view {
     int32_t n_components;           /* N */
     int32_t n_bodies;               /* B (the layout's) */
@@ -165,6 +165,14 @@ typedef struct rgg_resolve_view {
     const double* poses;            /* pose_off[N]*B*12 */
 } rgg_resolve_view;
 int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* view);
+/* The Scene's obstacles that are active before this engine moves them
+ * (ObstacleModel::active + pose, proj/include/rgg/swept.hpp:43, read by
+ * exact_component_valid at proj/src/roadmap.cpp:135-139).  Replaces the previous
+ * list; rt = n poses of 12 doubles (r[9] row-major, t[3]); a repeated id keeps its
+ * last pose.  An obstacle's own moves supersede its listed pose.  Only the exact
+ * resolve reads the list: the reference's BatchEngine labels and bits do not
+ * depend on obstacles it has not moved (engine_batch.cpp:145-215). */
+int rgg_gpu_set_active_obstacles(rgg_gpu* h, const int32_t* ids, const double* rt, int32_t n);
 /* resolve_all_unknown (engine_batch.cpp:217-227): every GRAY component becomes
  * GREEN (free) or RED; *resolved = how many were GRAY. */
 int rgg_gpu_resolve_all(rgg_gpu* h, int32_t* resolved);

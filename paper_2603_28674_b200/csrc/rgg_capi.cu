@@ -70,6 +70,8 @@ struct rgg_gpu {
     long long* d_res_off = nullptr;
     double* d_res_pose = nullptr;
     rggk::ObsPoly* d_opoly = nullptr;
+    double* d_res_spose = nullptr;  // M*12 scene poses of pre-active obstacles
+    uint8_t* d_res_sact = nullptr;  // M
     int32_t* d_res_ids = nullptr;  // N: scratch id list (rgg_gpu_exact_check)
     int32_t* d_res_cnt = nullptr;
     uint8_t* d_res_out = nullptr;  // N
@@ -343,6 +345,8 @@ rggk::Resolver resolver_of(rgg_gpu* h) {
     r.off = h->d_res_off;
     r.pose = h->d_res_pose;
     r.opoly = h->d_opoly;
+    r.spose = h->d_res_spose;
+    r.sact = h->d_res_sact;
     return r;
 }
 
@@ -738,7 +742,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
                    h->d_mv, h->d_pool, h->d_tl, h->d_dbg, h->d_hits_prev, h->d_evready,
-                   h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_ids, h->d_res_cnt, h->d_res_out,
+                   h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_spose, h->d_res_sact, h->d_res_ids, h->d_res_cnt, h->d_res_out,
                    h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};
     for (void* p : dev)
         if (p) cudaFree(p);
@@ -1148,6 +1152,32 @@ int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* v) {
                       cudaMemcpyHostToDevice));
     h->res_B = B;
     h->res_ready = true;
+    ++h->gen;  // captured eager graphs hold the old resolver pointers
+    return RGG_OK;
+}
+
+int rgg_gpu_set_active_obstacles(rgg_gpu* h, const int32_t* ids, const double* rt, int32_t n) {
+    if (!h) return RGG_EINVAL;
+    clear_stale_error();
+    if (n < 0 || (n > 0 && (!ids || !rt))) return fail(h, RGG_EINVAL, "bad obstacle list");
+    for (int32_t i = 0; i < n; ++i)
+        if (ids[i] < 0 || ids[i] >= h->s.M) return fail(h, RGG_EINVAL, "unknown obstacle id");
+    const int32_t M = std::max(1, h->s.M);
+    std::vector<uint8_t> act(static_cast<size_t>(M), 0);
+    std::vector<double> pose(static_cast<size_t>(M) * 12, 0.0);
+    for (int32_t i = 0; i < n; ++i) {  // a repeated id: the last pose wins
+        act[ids[i]] = 1;
+        std::copy(rt + 12 * static_cast<size_t>(i), rt + 12 * static_cast<size_t>(i) + 12, pose.begin() + 12 * ids[i]);
+    }
+    CK(cudaSetDevice(h->device));
+    if (!h->d_res_sact) {
+        CK(dalloc(&h->d_res_spose, static_cast<size_t>(M) * 12));
+        CK(dalloc(&h->d_res_sact, static_cast<size_t>(M)));
+        ++h->gen;  // captured eager graphs were built without these pointers
+    }
+    CK(cudaStreamSynchronize(h->stream));  // a queued resolve may still read the old list
+    CK(cudaMemcpy(h->d_res_spose, pose.data(), pose.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_res_sact, act.data(), act.size(), cudaMemcpyHostToDevice));
     return RGG_OK;
 }
 

@@ -136,6 +136,8 @@ struct Resolver {
     const long long* off;    // N+1: configurations of component c are [off[c], off[c+1])
     const double* pose;      // off[N]*B*12: world pose of each body box per configuration
     ObsPoly* opoly;          // M
+    const double* spose;     // M*12: scene pose of obstacles active before this engine moved them
+    const uint8_t* sact;     // M: 1 = scene-active at spose (null: none)
 };
 
 bool split_pipeline();  // RGG_PIPELINE == 6 (the default): touch / narrow / apply

@@ -128,15 +128,20 @@ __device__ __forceinline__ bool box_overlap(const double* a, const double* b) {
     return a[0] <= b[3] && b[0] <= a[3] && a[1] <= b[4] && b[1] <= a[4] && a[2] <= b[5] && b[2] <= a[5];
 }
 
-// The active obstacles' polytopes at their current poses (Event::rt).
+// The active obstacles' polytopes at their current poses (Event::rt).  An
+// obstacle this engine has not moved yet is active at its scene pose when the
+// host listed it (rgg_gpu_set_active_obstacles: ObstacleModel::active before the
+// engine's first move, the `if (!o.active) continue;` of roadmap.cpp:135-136).
 __global__ void resolve_prep_kernel(Store s, Resolver r) {
     const int o = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (o >= s.M) return;
     __shared__ PolyS sp[4];
     PolyS& P = sp[threadIdx.x >> 5];
     const double* un = s.cur_union + 6 * o;
-    const bool active = un[0] <= un[3];  // inactive obstacles keep an empty union box
-    build_poly(P, s.cur[o].rt, s.ohe + 3 * o, lane);
+    const bool moved = un[0] <= un[3];  // inactive obstacles keep an empty union box
+    const bool scene = !moved && r.sact && r.sact[o];
+    const bool active = moved || scene;
+    build_poly(P, scene ? r.spose + 12 * static_cast<size_t>(o) : s.cur[o].rt, s.ohe + 3 * o, lane);
     ObsPoly& out = r.opoly[o];
     for (int t = lane; t < 24; t += 32) out.v[t] = P.v[t];
     for (int t = lane; t < 9; t += 32) out.ax[t] = P.ax[t];

@@ -118,6 +118,7 @@ def library() -> C.CDLL:
         L.rgg_gpu_set_resolver.argtypes = [vp, C.POINTER(_ResolveView)]
         L.rgg_gpu_resolve_all.argtypes = [vp, ip]
         L.rgg_gpu_exact_check.argtypes = [vp, vp, i32, vp]
+        L.rgg_gpu_set_active_obstacles.argtypes = [vp, vp, vp, i32]
         L.rgg_gpu_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), i32]
         _lib = L
     return _lib
@@ -153,7 +154,7 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
             "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
-            "rgg_gpu_exact_check", "rgg_gpu_filter_stats"]
+            "rgg_gpu_exact_check", "rgg_gpu_filter_stats", "rgg_gpu_set_active_obstacles"]
 
 
 @dataclass
@@ -377,6 +378,16 @@ class GpuEngine:
         v = _ResolveView(self.n_components, he.shape[0], he.ctypes.data, off.ctypes.data, ps.ctypes.data)
         self._check(library().rgg_gpu_set_resolver(self._h, C.byref(v)))
         self._resolver = (off, he)
+
+    def set_active_obstacles(self, ids, rts):
+        """The Scene's obstacles active before this engine moves them (ObstacleModel::active
+        and pose; exact_component_valid reads them, roadmap.cpp:135-139): ids int[n],
+        rts float64 (n, 12). Replaces the previous list; the exact resolve only."""
+        ids = np.ascontiguousarray(ids, np.int32).reshape(-1)
+        rts = np.ascontiguousarray(rts, np.float64).reshape(-1, 12)
+        if rts.shape[0] != ids.shape[0]:
+            raise ValueError("one 12-double pose per obstacle id")
+        self._check(library().rgg_gpu_set_active_obstacles(self._h, ids.ctypes.data, rts.ctypes.data, len(ids)))
 
     def resolve_all_unknown(self, resolve: Callable[[np.ndarray], np.ndarray] | None = None) -> int:
         """BatchEngine::resolve_all_unknown (engine_batch.cpp:217-227): on the GPU after

@@ -145,6 +145,43 @@ static void batch_update_matches_batch_engine() {
     EXPECT(gpu.unknown_count() == 0, "gray left after resolve_all_unknown");
 }
 
+// Obstacles active in the Scene before the engine moves them (static walls): the reference's
+// exact_component_valid checks every active obstacle (roadmap.cpp:135-139), so eager updates and
+// resolve_all_unknown must see them at their scene poses until the engine first moves them.
+static void scene_active_obstacles() {
+    for (int trial = 0; trial < 4; ++trial) {
+        Scenelet fx(70 + 20 * trial, 3, 810 + trial, 5.0);
+        Rng rng(4200 + trial);
+        Scene base = fx.scene;
+        for (int o = 1; o < 3; ++o) {  // obstacles 1 and 2 start active at random poses
+            Transform pose = Transform::from_euler_xyz(rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(-3, 3));
+            pose.t = {rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(-3, 3)};
+            base.obstacles[o].pose = pose;
+            base.obstacles[o].active = true;
+        }
+        Scene bat_scene = base, gpu_scene = base;
+        BatchEngine bat(fx.components, bat_scene, {});
+        GpuEngine gpu(fx.components, gpu_scene, {});
+        const bool lazy = trial % 2 == 1;
+        for (int move = 0; move < 24; ++move) {
+            // obstacle 0 moves throughout; obstacle 1 first moves at move 12; obstacle 2 never moves
+            const ObstacleId o = move >= 12 && move % 3 == 0 ? 1 : 0;
+            Transform pose = Transform::from_euler_xyz(rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(-3, 3));
+            pose.t = {rng.uniform(-4, 4), rng.uniform(-4, 4), rng.uniform(-4, 4)};
+            const UpdateReport rb = bat.update_obstacle(o, pose, lazy);
+            const UpdateReport rg = gpu.update_obstacle(o, pose, lazy);
+            EXPECT(same_reports(rb, rg) && rb.resolve_checks == rg.resolve_checks,
+                   "scene-active trial %d move %d: reports bat(%d,%d,%d,%d,%d) gpu(%d,%d,%d,%d,%d)", trial, move,
+                   rb.new_green, rb.new_red, rb.new_gray, rb.unknown_after_heuristic, rb.residual_unknown, rg.new_green,
+                   rg.new_red, rg.new_gray, rg.unknown_after_heuristic, rg.residual_unknown);
+            EXPECT(bat.states() == gpu.states(), "scene-active trial %d move %d: states", trial, move);
+        }
+        const int nb = bat.resolve_all_unknown(), ng = gpu.resolve_all_unknown();
+        EXPECT(nb == ng, "scene-active trial %d: resolve_all_unknown %d vs %d", trial, nb, ng);
+        EXPECT(bat.states() == gpu.states(), "scene-active trial %d: states after resolve_all_unknown", trial);
+    }
+}
+
 static void scenario_replay(const std::string& path) {
     std::ifstream f(path);
     if (!f) {
@@ -344,6 +381,7 @@ int main(int argc, char** argv) {
     batch_update_matches_batch_engine();
     padding_neutrality();
     sequential_semantics();
+    scene_active_obstacles();
     if (!dir.empty()) {
         scenario_replay(dir + "/quick_smoke.scn");
         scenario_replay(dir + "/table4_obstacles_1000_5x.scn");

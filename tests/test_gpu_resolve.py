@@ -155,3 +155,52 @@ def test_box_pairs_kat_through_engine(mods):
         eng.batch_update((np.arange(lo, min(n, lo + 256), dtype=np.int32), g["rt_b"][lo:lo + 256]), per_move=False)
     got = eng.exact_check(np.arange(n, dtype=np.int32))
     assert np.array_equal(got, g["out"]), f"{int(np.sum(got != g['out']))} of {n} pair verdicts differ"
+
+
+def test_scene_active_obstacles(mods):
+    """Obstacles active in the Scene before the engine moves them (rgg_gpu_set_active_obstacles):
+    exact_component_valid checks every active obstacle at its pose (roadmap.cpp:135-139); an
+    obstacle's own move supersedes its listed pose.  Checked against the C oracle's ro_exact_valid."""
+    from oracle import oracle as O
+
+    ref, engine = mods
+    w = _world(ref, "quick_smoke")
+    ids, rts = w.moves()
+    lay = w.layout()
+    ohe = np.asarray(lay.obst_he, np.float64).reshape(-1, 3)
+    M = ohe.shape[0]
+    assert M >= 2
+    eng = _gpu(engine, w)
+    off, poses = w.poses()
+    he = np.asarray(w.body_half_extents(), np.float64).reshape(-1)
+    B = len(he) // 3
+    poses = np.asarray(poses, np.float64).reshape(-1, B, 12)
+    N = w.counts()["N"]
+    rng = np.random.default_rng(11)
+    sample = np.sort(rng.choice(N, min(N, 400), replace=False)).astype(np.int32)
+
+    def expect(active, obst_rt):
+        return np.array([0 if O.exact_valid(poses[off[c]:off[c + 1]], he, active, obst_rt, ohe) else 1
+                         for c in sample], np.uint8)
+
+    # two obstacles active at the poses of the script's first moves for them, none moved yet
+    pick = [int(np.flatnonzero(ids == o)[0]) for o in (0, 1)]
+    obst_rt = np.zeros((M, 12))
+    active = np.zeros(M, np.uint8)
+    for o, i in zip((0, 1), pick):
+        obst_rt[o], active[o] = rts[i], 1
+    eng.set_active_obstacles([0, 1], obst_rt[[0, 1]])
+    exp = expect(active, obst_rt)
+    assert 0 < int(exp.sum()) < len(sample), "the sample should straddle the scene obstacles"
+    assert np.array_equal(eng.exact_check(sample), exp)
+    # obstacle 0 moves: its engine pose wins over the listed one; obstacle 1 stays at its scene pose
+    j = int(np.flatnonzero(ids == 0)[1])
+    eng.update_obstacle(0, rts[j])
+    obst_rt[0] = rts[j]
+    assert np.array_equal(eng.exact_check(sample), expect(active, obst_rt))
+    # an empty list leaves only the moved obstacle
+    eng.set_active_obstacles([], np.zeros((0, 12)))
+    active[1] = 0
+    assert np.array_equal(eng.exact_check(sample), expect(active, obst_rt))
+    with pytest.raises(ValueError, match="unknown obstacle id"):
+        eng.set_active_obstacles([M], np.zeros((1, 12)))
