@@ -173,6 +173,16 @@ int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* view);
  * resolve reads the list: the reference's BatchEngine labels and bits do not
  * depend on obstacles it has not moved (engine_batch.cpp:145-215). */
 int rgg_gpu_set_active_obstacles(rgg_gpu* h, const int32_t* ids, const double* rt, int32_t n);
+/* exact_component_valid (proj/src/roadmap.cpp:129-163) of n_sets independent
+ * configuration sets, without an engine: the node and edge checks of build_prm
+ * (roadmap.cpp:69, :95-99; proj/src/roadmap.cpp:47-52 component_collides is its
+ * negation).  Set i's configurations are [cfg_off[i], cfg_off[i+1]); poses holds
+ * per configuration, per body, 12 doubles (r[9], t[3]) = forward_kinematics; the
+ * n_obst obstacles are the Scene's active ones (half extents, pose rt[12]).
+ * free_out[i] = 1 if set i is free.  Stateless; runs on `device`. */
+int rgg_exact_valid_sets(int32_t device, int32_t n_sets, const int64_t* cfg_off, int32_t n_bodies,
+                         const double* body_he, const double* poses, int32_t n_obst, const double* obst_he,
+                         const double* obst_rt, uint8_t* free_out);
 /* resolve_all_unknown (engine_batch.cpp:217-227): every GRAY component becomes
  * GREEN (free) or RED; *resolved = how many were GRAY. */
 int rgg_gpu_resolve_all(rgg_gpu* h, int32_t* resolved);

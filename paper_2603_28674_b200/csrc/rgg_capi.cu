@@ -1335,6 +1335,87 @@ int rgg_gpu_fp64_peak(int device, double* gflops) {
     return RGG_OK;
 }
 
+// exact_component_valid (roadmap.cpp:129-163) of independent configuration sets against
+// a fixed obstacle list, without an engine: build_prm's node and edge checks (:69, :95-99).
+int rgg_exact_valid_sets(int32_t device, int32_t n_sets, const int64_t* cfg_off, int32_t n_bodies,
+                         const double* body_he, const double* poses, int32_t n_obst, const double* obst_he,
+                         const double* obst_rt, uint8_t* free_out) {
+    rgg_gpu* h = nullptr;
+    clear_stale_error();
+    if (n_sets < 0 || n_bodies < 1 || n_obst < 0) return RGG_EINVAL;
+    if (n_sets == 0) return RGG_OK;
+    if (!cfg_off || !body_he || !free_out || (n_obst > 0 && (!obst_he || !obst_rt))) return RGG_EINVAL;
+    if (cfg_off[0] != 0) return RGG_EINVAL;
+    for (int32_t c = 0; c < n_sets; ++c)
+        if (cfg_off[c + 1] < cfg_off[c]) return RGG_EINVAL;
+    const int64_t total = cfg_off[n_sets];
+    if (total > 0 && !poses) return RGG_EINVAL;
+    if (n_obst == 0) {  // exact_component_valid: no active obstacle, every set is free
+        std::fill(free_out, free_out + n_sets, uint8_t{1});
+        return RGG_OK;
+    }
+    for (int k = 0; k < 3 * n_bodies; ++k)
+        if (!(body_he[k] > 0.0)) return RGG_EINVAL;  // ConvexPolytope::box: degenerate polytope
+    for (int k = 0; k < 3 * n_obst; ++k)
+        if (!(obst_he[k] > 0.0)) return RGG_EINVAL;
+    CK(cudaSetDevice(device));
+    struct Bufs {
+        std::vector<void*> p;
+        ~Bufs() {
+            for (void* q : p) cudaFree(q);
+        }
+    } bufs;
+    auto take = [&](auto** q, size_t n) {
+        const cudaError_t e = dalloc(q, n);
+        if (e == cudaSuccess) bufs.p.push_back(*q);
+        return e;
+    };
+    double *d_bhe, *d_pose, *d_ohe, *d_spose, *d_union;
+    long long* d_off;
+    uint8_t *d_sact, *d_out;
+    int32_t *d_ids, *d_cnt;
+    rggk::ObsPoly* d_opoly;
+    CK(take(&d_bhe, static_cast<size_t>(n_bodies) * 3));
+    CK(take(&d_pose, static_cast<size_t>(total) * n_bodies * 12));
+    CK(take(&d_off, static_cast<size_t>(n_sets) + 1));
+    CK(take(&d_ohe, static_cast<size_t>(n_obst) * 3));
+    CK(take(&d_spose, static_cast<size_t>(n_obst) * 12));
+    CK(take(&d_union, static_cast<size_t>(n_obst) * 6));
+    CK(take(&d_sact, static_cast<size_t>(n_obst)));
+    CK(take(&d_opoly, static_cast<size_t>(n_obst)));
+    CK(take(&d_out, static_cast<size_t>(n_sets)));
+    CK(take(&d_ids, static_cast<size_t>(n_sets)));
+    CK(take(&d_cnt, 1));
+    std::vector<int32_t> ids(static_cast<size_t>(n_sets));
+    for (int32_t i = 0; i < n_sets; ++i) ids[i] = i;
+    std::vector<double> empty(static_cast<size_t>(n_obst) * 6);
+    for (int32_t o = 0; o < n_obst; ++o)  // no engine moves: every obstacle is active at its listed pose
+        for (int k = 0; k < 3; ++k) empty[6 * o + k] = 1.0, empty[6 * o + 3 + k] = 0.0;
+    std::vector<uint8_t> act(static_cast<size_t>(n_obst), 1);
+    static_assert(sizeof(long long) == sizeof(int64_t), "int64 offsets");
+    CK(cudaMemcpy(d_bhe, body_he, static_cast<size_t>(n_bodies) * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    if (total > 0)
+        CK(cudaMemcpy(d_pose, poses, static_cast<size_t>(total) * n_bodies * 12 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_off, cfg_off, (static_cast<size_t>(n_sets) + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ohe, obst_he, static_cast<size_t>(n_obst) * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_spose, obst_rt, static_cast<size_t>(n_obst) * 12 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_union, empty.data(), empty.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sact, act.data(), act.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_ids, ids.data(), ids.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_cnt, &n_sets, sizeof(int32_t), cudaMemcpyHostToDevice));
+    rggk::Store st{};
+    st.M = n_obst;
+    st.ohe = d_ohe;
+    st.cur_union = d_union;
+    rggk::Resolver r{};
+    r.B = n_bodies, r.he = d_bhe, r.off = d_off, r.pose = d_pose, r.opoly = d_opoly, r.spose = d_spose, r.sact = d_sact;
+    rggk::Batch b{};
+    CK(rggk::launch_resolve(st, r, b, d_ids, d_cnt, n_sets, rggk::kCheck, d_out, nullptr));
+    CK(cudaMemcpy(free_out, d_out, static_cast<size_t>(n_sets), cudaMemcpyDeviceToHost));
+    for (int32_t i = 0; i < n_sets; ++i) free_out[i] = free_out[i] ? 0 : 1;  // kCheck writes 1 = RED
+    return RGG_OK;
+}
+
 }  // extern "C"
 
 extern "C" int rgg_gpu_set_phase_timing(rgg_gpu* h, int32_t on) {

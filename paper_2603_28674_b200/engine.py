@@ -119,6 +119,7 @@ def library() -> C.CDLL:
         L.rgg_gpu_resolve_all.argtypes = [vp, ip]
         L.rgg_gpu_exact_check.argtypes = [vp, vp, i32, vp]
         L.rgg_gpu_set_active_obstacles.argtypes = [vp, vp, vp, i32]
+        L.rgg_exact_valid_sets.argtypes = [i32, i32, vp, i32, vp, vp, i32, vp, vp, vp]
         L.rgg_gpu_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), i32]
         _lib = L
     return _lib
@@ -154,7 +155,8 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
             "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
-            "rgg_gpu_exact_check", "rgg_gpu_filter_stats", "rgg_gpu_set_active_obstacles"]
+            "rgg_gpu_exact_check", "rgg_gpu_filter_stats", "rgg_gpu_set_active_obstacles",
+            "rgg_exact_valid_sets"]
 
 
 @dataclass

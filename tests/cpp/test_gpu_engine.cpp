@@ -11,6 +11,7 @@
 //   proj/src/bench.cpp:57-83           scenario replay with equivalence after every iteration
 //   proj/tests/test_roadmap.cpp:34-73  rgg::gpu::build_prm (include/rgg/prm_gpu.hpp) == build_prm
 // Built by `make -C oracle dropin` (needs /root/reference); run by tests/test_cpp_dropin.py on a GPU.
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -371,10 +372,46 @@ static void prm_matches_reference(const std::vector<std::string>& scns) {
         EXPECT(same_roadmap(rgg::gpu::build_prm(build_scene, s.nodes, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed),
                             build_prm(build_scene, s.nodes, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed)),
                "scenario %s", path.c_str());
+        // the same robot among the scenario's obstacles, active at their first scripted poses:
+        // node and edge checks through rgg_exact_valid_sets (incl. the serial-chain manipulator)
+        Scene obst_scene{s.env, s.make_obstacles(), s.robot};
+        const auto moves = s.make_moves();
+        for (const auto& [o, pose] : moves)
+            if (!obst_scene.obstacles[o].active) {
+                obst_scene.obstacles[o].pose = pose;
+                obst_scene.obstacles[o].active = true;
+            }
+        const int n = std::min(s.nodes, 600);
+        const auto t0 = std::chrono::steady_clock::now();
+        const Roadmap g = rgg::gpu::build_prm(obst_scene, n, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed);
+        const auto t1 = std::chrono::steady_clock::now();
+        const Roadmap want = build_prm(obst_scene, n, s.k_neighbors, s.effective_epsilon(), s.roadmap_seed);
+        const auto t2 = std::chrono::steady_clock::now();
+        EXPECT(same_roadmap(g, want), "scenario %s with active obstacles", path.c_str());
+        std::printf("prm %s with %zu active obstacles: %zu of %d nodes, %zu edges; gpu %.1f ms, reference %.1f ms\n",
+                    s.name.c_str(), obst_scene.obstacles.size(), want.nodes.size(), n, want.edges.size(),
+                    std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                    std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
+    for (int trial = 0; trial < 3; ++trial) {  // random active boxes in a small cube
+        Scene sc = cube(4.0);
+        Rng rng(77 + trial);
+        for (int i = 0; i < 4; ++i) {
+            ObstacleModel ob = make_box_obstacle({rng.uniform(0.3, 1.5), rng.uniform(0.3, 1.5), rng.uniform(0.3, 1.5)}, 2);
+            ob.pose = Transform::from_euler_xyz(rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(-3, 3));
+            ob.pose.t = {rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(-3, 3)};
+            ob.active = true;
+            sc.obstacles.push_back(ob);
+        }
+        const Roadmap g = rgg::gpu::build_prm(sc, 300, 8, 0.25, 500 + trial);
+        const Roadmap want = build_prm(sc, 300, 8, 0.25, 500 + trial);
+        EXPECT(same_roadmap(g, want), "random active boxes trial %d", trial);
+        EXPECT(want.nodes.size() < 300, "trial %d: the boxes cut out samples", trial);
     }
 }
 
 int main(int argc, char** argv) {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);  // progress survives a crash
     const std::string dir = argc > 1 ? argv[1] : "";
     equivalence_after_every_move();
     narrow_masks_match_sequential();

@@ -204,3 +204,44 @@ def test_scene_active_obstacles(mods):
     assert np.array_equal(eng.exact_check(sample), expect(active, obst_rt))
     with pytest.raises(ValueError, match="unknown obstacle id"):
         eng.set_active_obstacles([M], np.zeros((1, 12)))
+
+
+@pytest.mark.parametrize("name", ["quick_smoke", "table5_manipulator_100"])
+def test_exact_valid_sets_stateless(mods, name):
+    """rgg_exact_valid_sets (build_prm's node/edge checks, roadmap.cpp:69, :95-99) against the
+    C oracle's ro_exact_valid, with every obstacle active at its first scripted pose."""
+    import ctypes as C
+
+    from oracle import oracle as O
+
+    ref, engine = mods
+    w = _world(ref, name)
+    ids, rts = w.moves()
+    ohe = np.ascontiguousarray(np.asarray(w.layout().obst_he, np.float64).reshape(-1, 3))
+    M = ohe.shape[0]
+    ort = np.zeros((M, 12))
+    for o in range(M):
+        ort[o] = rts[int(np.flatnonzero(ids == o)[0])]
+    off, poses = w.poses()
+    he = np.ascontiguousarray(np.asarray(w.body_half_extents(), np.float64).reshape(-1))
+    B = len(he) // 3
+    poses = np.ascontiguousarray(np.asarray(poses, np.float64).reshape(-1, B, 12))
+    off = np.ascontiguousarray(off, np.int64)
+    n = min(len(off) - 1, 500)
+    got = np.zeros(n, np.uint8)
+    L = engine.library()
+    rc = L.rgg_exact_valid_sets(0, n, off.ctypes.data, B, he.ctypes.data, poses.ctypes.data, M, ohe.ctypes.data,
+                                ort.ctypes.data, got.ctypes.data)
+    assert rc == 0
+    exp = np.array([1 if O.exact_valid(poses[off[c]:off[c + 1]], he, np.ones(M, np.uint8), ort, ohe) else 0
+                    for c in range(n)], np.uint8)
+    assert 0 < int(exp.sum()) < n
+    assert np.array_equal(got, exp)
+    # no obstacles: every set is free; bad offsets: EINVAL
+    rc = L.rgg_exact_valid_sets(0, n, off.ctypes.data, B, he.ctypes.data, poses.ctypes.data, 0, None, None,
+                                got.ctypes.data)
+    assert rc == 0 and got.all()
+    bad = off.copy()
+    bad[0] = 1
+    assert L.rgg_exact_valid_sets(0, n, bad.ctypes.data, B, he.ctypes.data, poses.ctypes.data, M, ohe.ctypes.data,
+                                  ort.ctypes.data, got.ctypes.data) != 0
