@@ -351,7 +351,7 @@ rggk::Resolver resolver_of(rgg_gpu* h) {
 }
 
 // grid bound of the eager resolve (a move's gray over-hits; the kernel strides)
-constexpr int kEagerResolveGrid = 2048;
+constexpr int kEagerResolveGrid = 592;  // 4 x 148 SMs: one CTA per gray over-hit, strided beyond
 
 // Enqueue the whole pipeline for n moves already in d_ids/d_rt.
 int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {

@@ -152,27 +152,49 @@ __global__ void resolve_prep_kernel(Store s, Resolver r) {
 
 constexpr int kResolveWarps = 4;
 
-// One warp per listed component.  MODE kResolve: the listed (GRAY) components
-// become GREEN or RED.  kEager (one-move eager update): the list is the move's
-// gray over-hits with their pre-move labels, and the report deltas of
-// finish_counts (engine_batch.cpp:41-53) go to ctr[20..23].  kCheck: verdicts
-// to out[], no label changes.
-template <int MODE>
+// SPLIT (eager moves: a few hundred gray over-hits, too few warps to fill the GPU):
+// one CTA per listed component; its warps split the component's configurations
+// (warp w takes configurations c0 + w, c0 + w + kResolveWarps, ...) and stop as soon
+// as any warp finds an intersection (a shared flag).  Otherwise (resolve_all_unknown,
+// exact checks: thousands of components) one warp per component.  The verdict is the
+// OR over (configuration, body, obstacle) of polytopes_intersect, so the mapping
+// does not change it.  MODE kResolve: the listed (GRAY) components become GREEN or RED.
+// kEager (one-move eager update): the list is the move's gray over-hits with their
+// pre-move labels, and the report deltas of finish_counts (engine_batch.cpp:41-53)
+// go to ctr[20..23].  kCheck: verdicts to out[], no label changes.
+template <int MODE, bool SPLIT>
 __global__ void __launch_bounds__(32 * kResolveWarps) resolve_kernel(Store s, Resolver r, Batch b, const int32_t* ids,
                                                                      const int32_t* count_ptr, uint8_t* out) {
     constexpr bool EAGER = MODE == kEager;
     __shared__ PolyS sa[kResolveWarps], sb[kResolveWarps];
+    __shared__ int hits[kResolveWarps];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    volatile int* hit = hits + (SPLIT ? 0 : wi);
+    const bool leader = SPLIT ? threadIdx.x == 0 : lane == 0;
+    const int unit0 = SPLIT ? blockIdx.x : blockIdx.x * kResolveWarps + wi;
+    const int ustride = SPLIT ? gridDim.x : gridDim.x * kResolveWarps;
+    const int cfg0 = SPLIT ? wi : 0, cstride = SPLIT ? kResolveWarps : 1;
+    auto sync = [&]() {
+        if (SPLIT)
+            __syncthreads();
+        else
+            __syncwarp();
+    };
     PolyS& A = sa[wi];
     PolyS& Bo = sb[wi];
     const int count = *count_ptr;
     int d[4] = {0, 0, 0, 0};
-    for (int k = blockIdx.x * kResolveWarps + wi; k < count; k += gridDim.x * kResolveWarps) {
+    for (int k = unit0; k < count; k += ustride) {
         const int id = ids[k];
-        bool free = true;
+        if (leader) *hit = 0;
+        sync();
         const long long c0 = r.off[id], c1 = r.off[id + 1];
-        for (long long cfg = c0; cfg < c1 && free; ++cfg) {
+        bool free = true;
+        for (long long cfg = c0 + cfg0; cfg < c1 && free; cfg += cstride) {
             for (int body = 0; body < r.B && free; ++body) {
+                // another warp found an intersection: stop (warp-uniform)
+                if (SPLIT && __any_sync(0xffffffffu, *hit != 0)) free = false;
+                if (!free) break;
                 const double* pose = r.pose + (cfg * r.B + body) * 12;
                 __syncwarp();
                 build_poly(A, pose, r.he + 3 * body, lane);
@@ -190,14 +212,19 @@ __global__ void __launch_bounds__(32 * kResolveWarps) resolve_kernel(Store s, Re
                         for (int t = lane; t < 9; t += 32) Bo.ax[t] = op.ax[t];
                         for (int t = lane; t < 36; t += 32) Bo.ed[t] = op.ed[t];
                         __syncwarp();
-                        if (boxes_intersect(A, Bo, lane)) free = false;
+                        if (boxes_intersect(A, Bo, lane)) {
+                            free = false;
+                            if (lane == 0) *hit = 1;
+                        }
                     }
                 }
             }
         }
-        if (lane == 0 && MODE == kCheck) out[k] = free ? 0 : 1;
-        if (lane == 0 && MODE != kCheck) {
-            const uint8_t fin = free ? 0 : 1;  // GREEN : RED
+        sync();
+        const bool is_free = *hit == 0;
+        if (leader && MODE == kCheck) out[k] = is_free ? 0 : 1;
+        if (leader && MODE != kCheck) {
+            const uint8_t fin = is_free ? 0 : 1;  // GREEN : RED
             s.state[id] = fin;
             const int c = s.rank[id];
             if (c >= 0) s.state_c[c] = fin;
@@ -209,10 +236,11 @@ __global__ void __launch_bounds__(32 * kResolveWarps) resolve_kernel(Store s, Re
                 d[3] += (prev == 2);
             }
         }
+        sync();  // the flag is reset for the next component only after every thread read it
     }
-    if (lane == 0 && MODE != kCheck) {
+    if (leader && MODE != kCheck) {
         int n = 0;
-        for (int k = blockIdx.x * kResolveWarps + wi; k < count; k += gridDim.x * kResolveWarps) ++n;
+        for (int k = unit0; k < count; k += ustride) ++n;
         if (n) atomicAdd(b.unknown, -n);  // every listed component was GRAY
         if (EAGER)
             for (int q = 0; q < 4; ++q)
@@ -232,14 +260,15 @@ cudaError_t launch_resolve(const Store& s, const Resolver& r, const Batch& b, co
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int need = (max_count + kResolveWarps - 1) / kResolveWarps;
+    // eager: one CTA per component (max_count bounds the grid); otherwise one warp per component
+    const int need = mode == kEager ? max_count : (max_count + kResolveWarps - 1) / kResolveWarps;
     const int grid = need < 1 ? 1 : (need < 8 * sms ? need : 8 * sms);
     if (mode == kEager)
-        resolve_kernel<kEager><<<grid, 32 * kResolveWarps, 0, st>>>(s, r, b, ids, count_dev, out);
+        resolve_kernel<kEager, true><<<grid, 32 * kResolveWarps, 0, st>>>(s, r, b, ids, count_dev, out);
     else if (mode == kCheck)
-        resolve_kernel<kCheck><<<grid, 32 * kResolveWarps, 0, st>>>(s, r, b, ids, count_dev, out);
+        resolve_kernel<kCheck, false><<<grid, 32 * kResolveWarps, 0, st>>>(s, r, b, ids, count_dev, out);
     else
-        resolve_kernel<kResolve><<<grid, 32 * kResolveWarps, 0, st>>>(s, r, b, ids, count_dev, out);
+        resolve_kernel<kResolve, false><<<grid, 32 * kResolveWarps, 0, st>>>(s, r, b, ids, count_dev, out);
     return cudaGetLastError();
 }
 
