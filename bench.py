@@ -1,31 +1,32 @@
 #!/usr/bin/env python
 """bench.py — SerRGG edge classification on B200: edges classified/s and per-update latency.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1], "c2"): SE(2) warehouse roadmap, 10k nodes /
-114k edges (N = 124,080 components incl. nodes), 64 moving yaw-rotated box
-obstacles, a move script of W + K iterations.  One STEP = one update of the
-obstacle set = one iteration of the script: all 64 obstacles re-posed through
-``batch_update`` with per-move UpdateReports (the reference's 64 calls to
-BatchEngine::update_obstacle, proj/src/engine_batch.cpp:145-215).  After each
-step every one of the N labels is the reference's, so
+Workload (the north star's target, BASELINE.json configs[4], "c5"): SE(2) roadmap,
+87,000 nodes / 988,896 edges (N = 1,075,896 components incl. nodes), 1024 moving
+yaw-rotated box obstacles.  One STEP = one update of the obstacle set = all 1024
+obstacles re-posed through ``batch_update`` with per-move UpdateReports (the
+reference's 1024 calls to BatchEngine::update_obstacle, proj/src/engine_batch.cpp:
+145-215, with the GRAY-id list compacted on the device, :193-200).  After each step
+every one of the N labels is the reference's, so
 
     value = N_components x steps / device time          ("edges/s")
     per-update latency = ms_per_step
 
-* ``value``: moves already resident in HBM, timed with CUDA events on the
-  engine's stream, L2 flushed (512 MB write) between steps.
+* ``value``: moves already resident in HBM, CUDA events on the engine's stream, L2
+  flushed (512 MB write) between steps; the update includes the gray-list compaction.
 * ``e2e``: the same steps through the public API with HOST buffers
-  (GpuEngine.batch_update -> rgg_gpu_update: H2D of the moves, D2H of the
-  per-move reports), wall clock around the call.
-* ``--impl reference``: the reference's own CPU SerRGG path (BatchEngine, AVX2
-  backend, all host threads) from oracle/_ref on the same roadmap and moves.
-
-N > 1 (torchrun, one rank per GPU, NCCL): weak scaling.  Rank r owns tile r of
-an N-tile world (a c2 roadmap + 64 obstacles per tile, tiles side by side);
-obstacle moves are broadcast from rank 0 every step (ncclBroadcast) and the
-per-move report counters are summed onto every rank (ncclAllReduce).
+  (GpuEngine.batch_update -> rgg_gpu_update: H2D of the moves, D2H of the per-move
+  reports, then the GRAY ids D2H), wall clock around the calls.
+* ``--impl reference``: the reference's own CPU SerRGG path on the same roadmap and
+  moves (oracle/_ref, built from /root/reference's sources): ceil(1024/64) = 16
+  grouped SequentialEngines (the reference refuses > 64 obstacles per engine,
+  engine_batch.cpp:27; SequentialEngine is its fastest CPU path at c5).
+* N > 1 (torchrun, one rank per GPU, NCCL): strong scaling of the same c5 roadmap.
+  Rank r owns the Morton-ordered cells c with c % N == r; per step the moves are
+  broadcast from rank 0, the per-move report counters all-reduced and the GRAY-id
+  lists gathered to rank 0 (paper_2603_28674_b200/dist.py).
 """
 from __future__ import annotations
 
@@ -48,24 +49,26 @@ BASE_METRIC = "edges classified/sec and per-update latency (ms) at 1/2/4/8 B200 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--config", default="c2")
+    p.add_argument("--config", default="c5")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--seed", type=int, default=12345)
-    p.add_argument("--cpu-sample-s", type=float, default=15.0)
+    p.add_argument("--cpu-sample-s", type=float, default=8.0, help="CPU seconds per reference-engine sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extras", action="store_true", help="skip the other configs, resolve and PRM")
     p.add_argument("--json-out", default="")
     p.add_argument("--clock-window-s", type=float, default=1.0)
-    p.add_argument("--no-resolve", action="store_true", help="skip the exact-resolve measurement")
-    p.add_argument("--extra-configs", default="c5,c4,c3",
-                   help="comma list of configs also measured on rank 0 (N=1) and reported under 'extra'")
+    p.add_argument("--extra-configs", default="c2,c3,c4,c1")
     return p.parse_args()
 
 
+# ------------------------------------------------------------------ workloads
+
 def tile_workload(config, rank, seed, iterations):
-    """Rank r's tile: the config's roadmap shifted by r tiles in x, obstacles r*M..r*M+M-1."""
-    from paper_2603_28674_b200 import producer, synth
+    """The config's roadmap and obstacle set (rank kept for the tools' call signature:
+    tile r is the roadmap shifted by r tiles in x)."""
+    from paper_2603_28674_b200 import synth
 
     kind, nodes, k, half, m, ohalf = synth.CONFIGS[config]
     rm = synth.make_roadmap(kind, nodes, k, half, seed + 1000 * rank)
@@ -77,7 +80,8 @@ def tile_workload(config, rank, seed, iterations):
 
 
 def world_moves(config, world, seed, iterations):
-    """Moves of every tile, interleaved per iteration: [iteration][tile][obstacle]."""
+    """The move script [iteration][move]: every obstacle once per iteration, or the
+    rotating subset of MOVES_PER_STEP (c4's ~5 % dirty cells)."""
     from paper_2603_28674_b200 import synth
 
     kind, nodes, k, half, m, ohalf = synth.CONFIGS[config]
@@ -94,7 +98,30 @@ def world_moves(config, world, seed, iterations):
         sel = np.array([[r * m + (k * it + j) % m for r in range(world) for j in range(k)] for it in range(iterations)])
         ids = np.take_along_axis(ids, sel, 1).astype(np.int32)
         rts = np.take_along_axis(rts, sel[:, :, None], 1)
-    return ids, rts
+    return np.ascontiguousarray(ids), np.ascontiguousarray(rts)
+
+
+def workload_name(config, n_components):
+    from paper_2603_28674_b200 import synth
+
+    kind, nodes, k, half, m, ohalf = synth.CONFIGS[config]
+    mv = synth.MOVES_PER_STEP.get(config)
+    step = (f"1 step = 1 update = {mv} of the {m} obstacles re-posed (rotating subset, ~5 % of cells dirty)"
+            if mv else f"1 step = 1 update = all {m} obstacles re-posed")
+    return (f"{config}: {'SE(2)' if kind == 'se2' else '3D'} roadmap {nodes} nodes k={k} ({n_components} components "
+            f"incl. nodes) x {m} moving OBB obstacles; {step} (per-move reports, gray-id list compacted on device)")
+
+
+def config_dict(config, n_components, world=1):
+    from paper_2603_28674_b200 import synth
+
+    m = synth.CONFIGS[config][4]
+    return {"workload": workload_name(config, n_components), "components": n_components, "obstacles": m,
+            "moves_per_step": synth.MOVES_PER_STEP.get(config) or m,
+            "l2": "flushed (512 MB write) between timed steps",
+            "parallelism": (f"{world} shards of one roadmap (interleaved Morton cells), obstacles replicated, "
+                            f"moves broadcast, counters all-reduced, gray ids gathered" if world > 1 else "1 GPU"),
+            "precision": "verdicts exact: fp32 filters with proven error bounds, fp64 reference op order otherwise"}
 
 
 class ClockSampler:
@@ -145,72 +172,134 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_run(config, seed, iterations, sample_s, threads, engine_kind=0):
-    """The reference's CPU SerRGG path on tile 0's roadmap + moves (oracle/_ref)."""
-    from oracle import ref
-    from paper_2603_28674_b200 import producer, synth
+def host_info():
+    model = ""
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
 
-    rm, obs, _ = tile_workload(config, 0, seed, iterations)
+
+# ------------------------------------------------------------ reference (CPU)
+
+def ref_world(rm, obs):
+    from oracle import ref
+
     w = ref.World.from_roadmap(rm.robot_he, rm.env, rm.nodes, rm.edges, rm.eps, rm.max_segments)
     for he, ns in zip(obs.he, obs.spheres):
         w.add_obstacle(he, int(ns))
-    ids, rts = world_moves(config, 1, seed, iterations)
-    eng = ref.Engine(w, kind=engine_kind, threads=threads, group_size=64)
-    n = w.counts()["N"]
-    done, spent = 0, 0.0
-    per_step = []
-    for it in range(iterations):
-        us = eng.run(ids[it], rts[it], lazy=True)
-        per_step.append(us)
-        spent += us * 1e-6
-        done += 1
-        if spent >= sample_s:
-            break
-    return n, done, spent, per_step, eng
+    return w
+
+
+def ref_engine_kind(m):
+    """The reference engine a CPU arm runs: SequentialEngine, the reference's fastest
+    CPU path wherever we probed it, grouped by 64 obstacles."""
+    groups = (m + 63) // 64
+    return 1, (f"rgg::SequentialEngine x {groups} obstacle groups of <= 64 (engine_batch.cpp:27 caps an engine "
+               f"at 64), 1 thread" if groups > 1 else "rgg::SequentialEngine, 1 thread")
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref) on this arm's
+    workload, metric and unit; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    threads = os.cpu_count() or 1
+    from oracle import ref
+
     iterations = args.warmup + args.steps
-    n, done, spent, per_step, _ = cpu_reference_run(args.config, args.seed, iterations, 1e18, threads)
-    timed = per_step[args.warmup:] or per_step
-    t = sum(timed) * 1e-6
+    rm, obs, _ = tile_workload(args.config, 0, args.seed, iterations)
+    t0 = time.time()
+    w = ref_world(rm, obs)
+    kind, what = ref_engine_kind(len(obs.he))
+    eng = ref.Engine(w, kind=kind, threads=1, group_size=64)
+    build_s = time.time() - t0
+    ids, rts = world_moves(args.config, 1, args.seed, iterations)
+    n = w.counts()["N"]
+    per = [eng.run(ids[it], rts[it], lazy=True) * 1e-6 for it in range(iterations)]
+    timed = per[args.warmup:]
+    t = sum(timed)
     value = n * len(timed) / t
     line = {
         "impl": "reference", "metric": BASE_METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
-        "steps": len(timed), "warmup": min(args.warmup, done), "ms_per_step": 1e3 * t / len(timed),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, n),
-        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
-                         "sample": f"rgg::BatchEngine (AVX2, {threads} threads) on tile 0: {len(timed)} updates x "
-                                   f"64 moves, oracle/_ref/librgg_ref.so"},
+        "steps": len(timed), "warmup": args.warmup, "ms_per_step": 1e3 * t / len(timed), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.config, n),
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": 1, "kind": "reference",
+                         "sample": f"{what}, oracle/_ref/librgg_ref.so: {len(timed)} full updates of "
+                                   f"{ids.shape[1]} moves each (+{args.warmup} untimed); engines built in "
+                                   f"{build_s:.0f} s", "host": host_info()},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_dict(args, n_components, world=1):
-    from paper_2603_28674_b200 import synth
+def cpu_baselines(config, rm, obs, ids, rts, sample_s, parity_updates=2):
+    """The reference's CPU engines on the headline workload:
+    grouped SequentialEngine (1 thread), BatchEngine with 1 thread and with all host
+    threads.  Returns (baselines, sequential engine after its updates, updates run)."""
+    from oracle import ref
 
-    kind, nodes, k, half, m, ohalf = synth.CONFIGS[args.config]
-    mv = synth.MOVES_PER_STEP.get(args.config)
-    step = (f"1 step = 1 update = {mv} of the {m} obstacles re-posed (rotating subset, ~5 % of cells dirty)"
-            if mv else f"1 step = 1 update = all {m} obstacles re-posed")
-    return {"workload": f"{args.config}: {'SE(2)' if kind == 'se2' else '3D'} roadmap {nodes} nodes k={k} "
-                        f"({n_components} components incl. nodes) x {m} moving OBB obstacles per GPU tile; "
-                        f"{step} (per-move reports)",
-            "components_per_gpu": n_components, "obstacles_per_gpu": m, "moves_per_step": m * world,
-            "l2": "flushed (512 MB write) between timed steps", "parallelism": f"tiles x{world} (weak)",
-            "precision": "fp64-exact (reference op order, no FMA)"}
+    m = len(obs.he)
+    groups = (m + 63) // 64
+    nproc = os.cpu_count() or 1
+    out = {"host": host_info()}
+    t0 = time.time()
+    w = ref_world(rm, obs)
+    out["world_build_s"] = round(time.time() - t0, 1)
+    n = w.counts()["N"]
+    # grouped SequentialEngine over whole updates (also the parity reference)
+    t0 = time.time()
+    seq = ref.Engine(w, kind=1, threads=1, group_size=64)
+    build = time.time() - t0
+    per, spent = [], 0.0
+    for it in range(len(ids)):
+        per.append(seq.run(ids[it], rts[it], lazy=True) * 1e-6)
+        spent += per[-1]
+        if len(per) >= parity_updates and spent >= sample_s:
+            break
+    out["sequential_1t"] = {"ms_per_update": 1e3 * statistics.mean(per), "edges_per_s": n / statistics.mean(per),
+                            "cores": 1, "build_s": round(build, 1),
+                            "sample": f"{len(per)} full updates x {ids.shape[1]} moves, {groups} grouped engines"}
+    # BatchEngine: a bounded sample, the first obstacle group's moves of each update
+    # (its engine holds the whole roadmap, ~64 B/comp per group of layout); the per-update
+    # figure scales the per-move time by the moves per update
+    for threads in (1, nproc):
+        t0 = time.time()
+        bat = ref.Engine(w, kind=0, threads=threads, group_size=64, max_groups=1)
+        build = time.time() - t0
+        mv_s, nmv, spent = [], 0, 0.0
+        for it in range(len(ids)):
+            sel = ids[it] < 64
+            if not sel.any():
+                continue
+            s = bat.run(np.ascontiguousarray(ids[it][sel]), np.ascontiguousarray(rts[it][sel]), lazy=True) * 1e-6
+            nmv += int(sel.sum())
+            spent += s
+            if spent >= sample_s / 2:
+                break
+        per_move = spent / max(1, nmv)
+        ms = 1e3 * per_move * ids.shape[1]
+        out[f"batch_{threads}t"] = {"ms_per_update": ms, "edges_per_s": n / (ms * 1e-3), "cores": threads,
+                                    "build_s_one_group": round(build, 1),
+                                    "sample": f"{nmv} moves of obstacle group 0 (one BatchEngine over all {n} "
+                                              f"components), {1e3 * per_move:.2f} ms/move x {ids.shape[1]} moves"}
+        del bat
+    best = min(("sequential_1t", "batch_1t", f"batch_{nproc}t"), key=lambda k: out[k]["ms_per_update"])
+    out["fastest"] = best
+    return out, seq, len(per), n
 
 
-def measure_extra(config, seed, device, steps=10, warmup=3):
+# --------------------------------------------------------------- GPU helpers
+
+def measure_extra(config, seed, device, steps=10, warmup=3, cell_capacity=64, parity=False):
     """A further BASELINE config on one GPU (device-resident moves, L2 flushed between
-    updates): per-update latency and edges/s, the flop/byte census of one update."""
+    updates): per-update latency and edges/s, the census of one update; parity
+    against the pinned C oracle's pure-function labels and bits when asked."""
     import torch
 
     from paper_2603_28674_b200 import engine as E
@@ -220,7 +309,7 @@ def measure_extra(config, seed, device, steps=10, warmup=3):
     rm, obs, _ = tile_workload(config, 0, seed, warmup + steps)
     lv = producer.layout_for(rm, obs)
     build_s = time.time() - t0
-    eng = E.GpuEngine(lv, device=device)
+    eng = E.GpuEngine(lv, device=device, cell_capacity=cell_capacity)
     ids_h, rts_h = world_moves(config, 1, seed, warmup + steps)
     dev = torch.device("cuda", device)
     ids_d = torch.from_numpy(ids_h).to(dev)
@@ -228,9 +317,8 @@ def measure_extra(config, seed, device, steps=10, warmup=3):
     m = ids_h.shape[1]
     stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    eng.set_phase_timing(False)
     for it in range(warmup):
-        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m, per_move=True)
+        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m, per_move=True, gray_list=True)
     torch.cuda.synchronize()
     ms = []
     for k in range(steps):
@@ -238,39 +326,92 @@ def measure_extra(config, seed, device, steps=10, warmup=3):
             flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        eng.update_device(ids_d[warmup + k].data_ptr(), rts_d[warmup + k].data_ptr(), m, per_move=True)
+        eng.update_device(ids_d[warmup + k].data_ptr(), rts_d[warmup + k].data_ptr(), m, per_move=True,
+                          gray_list=True)
         b.record(stream)
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
-    eng.set_phase_timing(True)
-    eng.update_device(ids_d[warmup + steps - 1].data_ptr(), rts_d[warmup + steps - 1].data_ptr(), m, per_move=True)
     eng.sync()
-    dirty = eng.last_stats()["dirty_cells"]
-    eng.set_phase_timing(False)
-    eng.update_device(ids_d[warmup + steps - 1].data_ptr(), rts_d[warmup + steps - 1].data_ptr(), m,
-                      per_move=True, census=True)
+    st = eng.last_stats()
+    last = warmup + steps - 1
+    eng.update_device(ids_d[last].data_ptr(), rts_d[last].data_ptr(), m, per_move=True, census=True)
     cen = eng.census()
     per = statistics.mean(ms)
     ncells = (lv.N + 127) // 128
-    byts = cen["bytes_components"] + m * 768
-    return {"workload": config_dict(argparse.Namespace(config=config), lv.N)["workload"],
-            "components": lv.N, "moves_per_update": m, "per_update_ms": per,
-            # incremental configs: the components of the dirty cells are the ones relabelled
-            "value": (min(lv.N, dirty * 128) if synth.MOVES_PER_STEP.get(config) else lv.N) / (per * 1e-3),
-            "value_all_components": lv.N / (per * 1e-3),
-            "unit": "edges/s", "steps": steps, "build_s": round(build_s, 1),
-            "dirty_cells": dirty, "dirty_fraction": dirty / max(1, ncells),
-            "hbm_frac_of_update": byts / (per * 1e-3) / 1e9 / 6553.3,
-            "census": {k: cen[k] for k in ("over_pairs", "sat_flops", "under_pairs", "seg_sphere_tests",
-                                           "bytes_components")}}
+    out = {"workload": workload_name(config, lv.N), "components": lv.N, "moves_per_update": m,
+           "per_update_ms": per,
+           # incremental configs: the components of the dirty cells are the ones relabelled
+           "value": (min(lv.N, st["dirty_cells"] * 128) if synth.MOVES_PER_STEP.get(config) else lv.N) / (per * 1e-3),
+           "value_all_components": lv.N / (per * 1e-3), "unit": "edges/s", "steps": steps,
+           "build_s": round(build_s, 1), "cell_capacity": cell_capacity, "dirty_cells": st["dirty_cells"],
+           "dirty_fraction": st["dirty_cells"] / max(1, ncells), "overflow_cells": st["overflow_cells"],
+           "census": {k: cen[k] for k in ("over_pairs", "sat_flops", "under_pairs", "seg_sphere_tests",
+                                           "bytes_components", "bytes_fp32", "gray")}}
+    if parity:
+        from oracle import oracle as O
+
+        ora = O.Engine(lv)
+        t0 = time.time()
+        for it in range(last + 1):
+            for o, rt in zip(ids_h[it], rts_h[it]):
+                ora.update(int(o), rt)
+        sts, bits = ora.pure()
+        got_bits = eng.obstacle_bits().reshape(lv.N, -1)
+        out["parity"] = {"mismatches_vs_oracle": int(np.sum(eng.states() != sts)),
+                         "bit_word_mismatches": int(np.sum(got_bits != bits.reshape(got_bits.shape))),
+                         "checked": f"{lv.N} labels and {got_bits.size} bit words after {last + 1} updates against "
+                                    f"the pinned C oracle's pure-function labels (oracle/rgg_oracle.c ro_engine_pure)",
+                         "oracle_s": round(time.time() - t0, 1)}
+    return out
+
+
+def measure_c1(device, reps=20):
+    """C1 (BASELINE configs[0]): table4_obstacles_1000_5x as shipped.
+    Replay iteration 1 (activates all 5 obstacles), then time ONE update_obstacle,
+    the first move of iteration 2, through the host API; the reference engines time
+    the same single move on the same state."""
+    from oracle import ref
+    from paper_2603_28674_b200 import engine as E
+
+    scn = os.path.join(ROOT, "tests", "golden", "scenarios", "table4_obstacles_1000_5x.scn")
+    w = ref.World.from_scn(open(scn).read())
+    k = w.counts()
+    lay = w.layout()
+    ids, rts = w.moves()
+    m = k["M"]
+    lv = E.LayoutView.from_any(lay)
+    out = {"workload": f"c1: table4_obstacles_1000_5x ({k['N']} components, {m} obstacles); one update_obstacle "
+                       f"(the first move of iteration 2) after replaying iteration 1"}
+    gpu = []
+    for _ in range(reps):
+        eng = E.GpuEngine(lv, device=device)
+        for o, rt in zip(ids[:m], rts[:m]):  # iteration 1, one move at a time (the single-move graph is built here)
+            eng.update_obstacle(int(o), rt)
+        t0 = time.perf_counter()
+        eng.update_obstacle(int(ids[m]), rts[m])
+        gpu.append(1e6 * (time.perf_counter() - t0))
+        last = eng
+    out["gpu_us"] = statistics.median(gpu)
+    cpu = {}
+    for name, kind, threads in (("sequential_1t", 1, 1), ("batch_1t", 0, 1), (f"batch_{os.cpu_count()}t", 0,
+                                                                                 os.cpu_count() or 1)):
+        us = []
+        for _ in range(reps):
+            e = ref.Engine(w, kind=kind, threads=threads)
+            e.run(ids[:m], rts[:m])
+            us.append(e.run(ids[m:m + 1], rts[m:m + 1]))
+        cpu[name] = statistics.median(us)
+        if name == "batch_1t":
+            out["labels_equal_reference"] = bool(np.array_equal(last.states(), e.states()))
+    out["cpu_us"] = cpu
+    out["speedup_vs_fastest_cpu"] = min(cpu.values()) / out["gpu_us"]
+    return out
 
 
 def measure_resolve(config, seed, device, rounds=4, cpu=True):
     """The exact resolve on the GPU: resolve_all_unknown after
     each lazy update, and one eager update, through the host API; the reference's
     own resolve_all_unknown / eager update_obstacle on the same roadmap and moves."""
-    import numpy as np
-
     from paper_2603_28674_b200 import engine as E
     from paper_2603_28674_b200 import producer
 
@@ -293,8 +434,8 @@ def measure_resolve(config, seed, device, rounds=4, cpu=True):
     reps = eng.batch_update((ids[rounds], rts[rounds]), lazy=False)
     eager_ms = 1e3 * (time.perf_counter() - t0)
     checks = int(sum(r.resolve_checks for r in reps))
-    out = {"what": "resolve_all_unknown after each lazy update (64 moves), then one eager update (64 moves, each "
-                   "move's gray over-hits resolved before the next); host API wall time incl. gray compaction",
+    out = {"what": f"{config}: resolve_all_unknown after each lazy update ({ids.shape[1]} moves), then one eager "
+                   f"update (each move's gray over-hits resolved before the next); host API wall time",
            "configs": int(lv.resolver[0][-1]), "pose_upload_s": round(upload_s, 3),
            "resolve_all": {"gray_per_call": grays, "gpu_ms": gpu_ms,
                            "gpu_components_per_s": sum(grays) / (1e-3 * sum(gpu_ms))},
@@ -302,9 +443,7 @@ def measure_resolve(config, seed, device, rounds=4, cpu=True):
     if cpu:
         from oracle import ref
 
-        w = ref.World.from_roadmap(rm.robot_he, rm.env, rm.nodes, rm.edges, rm.eps, rm.max_segments)
-        for he, ns in zip(obs.he, obs.spheres):
-            w.add_obstacle(he, int(ns))
+        w = ref_world(rm, obs)
         re = ref.Engine(w, kind=0, threads=os.cpu_count() or 1)
         cpu_ms = []
         for r in range(min(rounds, 2)):  # bounded sample
@@ -314,7 +453,6 @@ def measure_resolve(config, seed, device, rounds=4, cpu=True):
             cpu_ms.append(1e3 * (time.perf_counter() - t0))
         out["resolve_all"]["cpu_ref_ms"] = cpu_ms
         out["resolve_all"]["speedup"] = statistics.mean(cpu_ms) / statistics.mean(gpu_ms[: len(cpu_ms)])
-        # lock-step check: same labels after the same lazy updates + resolves
         for r in range(min(rounds, 2), rounds):
             re.run(ids[r], rts[r], lazy=True)
             re.resolve_all_unknown()
@@ -328,9 +466,7 @@ def measure_resolve(config, seed, device, rounds=4, cpu=True):
 def measure_prm(cpu=True, reps=3):
     """PRM construction: build_prm's kNN on the GPU (csrc/rgg_prm.cu)
     through the host API (nodes H2D, edges D2H inside the wall time), at table3's 10,000
-    nodes (the reference's largest shipped roadmap, timed beside it) and at the 1M-edge
-    configs' 87,000 nodes (k=20; the reference would take minutes, so not run)."""
-
+    nodes (timed beside the reference) and at the 1M-edge configs' 87,000 nodes."""
     from paper_2603_28674_b200 import prm
 
     out = {"what": "rgg_prm_knn_edges: k nearest nodes under dof_distance2, (min, max) pairs sorted + unique; "
@@ -340,7 +476,7 @@ def measure_prm(cpu=True, reps=3):
                                    ("n87000_k20", 87000, 20, 71.0, 12345)):
         lo, hi = prm.dof_bounds_free_flying([-half] * 3 + [half] * 3)
         nodes = prm.sample_nodes(seed, n, lo, hi)
-        prm.knn_edges(nodes, k)  # warm (allocations, module load)
+        prm.knn_edges(nodes, k)
         wall, dev = [], []
         for _ in range(reps):
             t0 = time.perf_counter()
@@ -348,20 +484,60 @@ def measure_prm(cpu=True, reps=3):
             wall.append(1e3 * (time.perf_counter() - t0))
             dev.append(ms)
         r = {"nodes": n, "k": k, "dof": 6, "edges": int(len(edges)), "gpu_wall_ms": statistics.median(wall),
-             "gpu_device_ms": statistics.median(dev),
-             "pairs_per_s_device": n * (n - 1) / (1e-3 * statistics.median(dev))}
+             "gpu_device_ms": statistics.median(dev)}
         if cpu and name.startswith("table3") and os.path.exists(scn):
             from oracle import ref
 
             rn, re_, _, _, sec = ref.build_prm(open(scn).read())
             r["cpu_ref_ms"] = 1e3 * sec
-            r["cpu_ref_note"] = "rgg::build_prm (oracle/_ref), one thread as the reference runs it, kNN + sort"
             r["speedup_wall"] = 1e3 * sec / r["gpu_wall_ms"]
             r["edges_equal_reference"] = bool(np.array_equal(rn.view(np.uint64), nodes.view(np.uint64)) and
                                               np.array_equal(re_, edges))
         out[name] = r
     return out
 
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+def roofline(census, kernel_ms, world, profile_json=None):
+    """HBM roofline of the update (the slower of the FP32 test rate and HBM for the
+    census bytes): achieved = algorithmic bytes (fp32 model) / time."""
+    from paper_2603_28674_b200 import engine as E
+
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6550.0))
+    fp32 = E.fp32_peak_gflops(0)
+    flops = census["sat_flops"] + 21 * census["seg_sphere_tests"]
+    byts = census["bytes_fp32"]
+    t_fl, t_by = flops / (fp32 * 1e9), byts / (hbm * 1e9)
+    roof = {"bound": "hbm" if t_by >= t_fl else "fp32",
+            "achieved": byts / (kernel_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md",
+            "kernel": "the whole update (pose, bin scatter + cell lists, touch, narrow, apply, gray compaction: "
+                      "paper_2603_28674_b200/csrc/rgg_kernels.cu), timed with CUDA events per update",
+            "algorithmic": {"bytes_per_update": byts, "bytes_model": "SURVEY.md §8(d) fp32 model (DESIGN.md §4)",
+                            "bytes_fp64_records": census["bytes_components"], "flops_per_update": flops,
+                            "fp32_peak_gflops_measured": fp32, "t_bytes_ms": 1e3 * t_by, "t_flops_ms": 1e3 * t_fl,
+                            "per_shard": world > 1}}
+    if roof["bound"] == "fp32":
+        roof.update(achieved=flops / (kernel_ms * 1e-3) / 1e12, peak=fp32 / 1e3, unit="TFLOP/s",
+                    peak_source="measured live: FFMA issue rate (rgg_gpu_fp32_peak)")
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    if profile_json and os.path.exists(profile_json):
+        try:
+            p = json.load(open(profile_json))
+            roof["traffic"] = p["dram_bytes_per_update"]
+            roof["traffic_source"] = os.path.relpath(profile_json, ROOT)
+        except (KeyError, ValueError):
+            pass
+    return roof
+
+
+# ---------------------------------------------------------------------- main
 
 def main():
     args = parse()
@@ -383,25 +559,19 @@ def main():
     from paper_2603_28674_b200 import producer
 
     iterations = args.warmup + args.steps
-    rm, obs, _ = tile_workload(args.config, rank, args.seed, iterations)
-    obs_all = obs
-    if world > 1:
-        from paper_2603_28674_b200 import synth
-
-        obs_all = synth.Obstacles(he=np.tile(obs.he, (world, 1)), spheres=np.tile(obs.spheres, world))
-    lv = producer.layout_for(rm, obs_all)
-    eng = E.GpuEngine(lv, device=local)
+    rm, obs, _ = tile_workload(args.config, 0, args.seed, iterations)
+    lv = producer.layout_for(rm, obs)
     N = lv.N
-    m_step = len(obs.he) * world
-    if rank == 0:
-        ids_h, rts_h = world_moves(args.config, world, args.seed, iterations)
-    else:
-        ids_h = np.zeros((iterations, m_step), np.int32)
-        rts_h = np.zeros((iterations, m_step, 12))
+    eng = E.GpuEngine(lv, device=local, shard_rank=rank, shard_count=world)
+    ids_h, rts_h = world_moves(args.config, 1, args.seed, iterations)
+    m_step = ids_h.shape[1]
     dev = torch.device("cuda", local)
     stream = torch.cuda.ExternalStream(eng.stream(), device=dev)
-    ids_d = torch.from_numpy(ids_h).to(dev)
-    rts_d = torch.from_numpy(rts_h).to(dev)
+    if rank == 0:
+        ids_d, rts_d = torch.from_numpy(ids_h).to(dev), torch.from_numpy(rts_h).to(dev)
+    else:  # filled by the broadcast inside each step
+        ids_d = torch.zeros((iterations, m_step), dtype=torch.int32, device=dev)
+        rts_d = torch.zeros((iterations, m_step, 12), dtype=torch.float64, device=dev)
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     torch.cuda.synchronize()
 
@@ -409,30 +579,30 @@ def main():
     if dist is not None:
         from paper_2603_28674_b200.dist import DistributedUpdater
 
-        up = DistributedUpdater(eng, dev)
+        np_max = torch.tensor([eng.n_owned], dtype=torch.int64, device=dev)
+        dist.all_reduce(np_max, op=dist.ReduceOp.MAX)
+        up = DistributedUpdater(eng, dev, gray_cap=int(np_max.item()))
 
     def step_device(it):
         if up is None:
-            eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True)
-        else:  # broadcast of the moves from rank 0, shard update, all-reduce of the report counters
-            up.update(ids_d[it], rts_d[it], per_move=True, check=False)
+            eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True, gray_list=True)
+        else:  # move broadcast, shard update, counter all-reduce, gray-list gather: all stream-ordered
+            up.update(ids_d[it], rts_d[it], per_move=True, check=False, gather_gray=True)
 
-    # N = 1: the engine's own stream carries everything; N > 1: the collectives run on
-    # torch's current stream and DistributedUpdater orders the engine stream against it
+    # N = 1: the engine's stream carries everything; N > 1: the collectives run on torch's
+    # current stream and DistributedUpdater orders the engine stream against it
     tstream = stream if dist is None else torch.cuda.current_stream(dev)
-
-    # ---- warm-up (device path), then K timed steps with L2 flushed in between; the
-    # per-kernel phase split is sampled afterwards (its events would serialise the
-    # pipeline's programmatic launches inside the timed steps)
     eng.set_phase_timing(False)
     for it in range(args.warmup):
         step_device(it)
     torch.cuda.synchronize()
+    if up is not None:
+        up.check()
     eng.filter_stats(reset=True)
     if dist is not None:
         dist.barrier()
+    torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    classify_ms, stats = [], []
     with ClockSampler(local) as clk:
         t_clock0 = time.perf_counter()
         for k in range(args.steps):
@@ -442,162 +612,180 @@ def main():
             step_device(args.warmup + k)
             ev[k][1].record(tstream)
         torch.cuda.synchronize()
-        # keep the same load under the sampler for >= 1 s so clocks are observed under load
-        n_updates = args.steps  # updates behind the filter counters below
-        while time.perf_counter() - t_clock0 < args.clock_window_s:
-            step_device(args.warmup + (args.steps - 1))
+        n_updates = args.steps
+        while time.perf_counter() - t_clock0 < args.clock_window_s:  # >= 1 s of the same load under the sampler
+            step_device(args.warmup + args.steps - 1)
             torch.cuda.synchronize()
             n_updates += 1
     if up is not None:
-        up.check()  # device-side errors of the stream-ordered updates
+        up.check()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    # the fp32 filters' undecided pairs (re-tested exactly) over the timed steps plus the clock window
-    fstats = eng.filter_stats(reset=True)
-    # phase split (untimed): the same last steps again with per-kernel events
-    eng.set_phase_timing(True)
-    for k in range(min(5, args.steps)):
-        with torch.cuda.stream(tstream):
-            flush.zero_()
-        step_device(args.warmup + args.steps - 1 - k)
-        st = eng.last_stats()
-        classify_ms.append(st["classify_ms"])
-        stats.append(st)
-    eng.set_phase_timing(False)
     total_ms = float(sum(step_ms))
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    launches_per_step = 5  # pose, bin, touch, narrow, apply (one CUDA graph); gray ids are compacted on demand
-    # one more (untimed) update of the last step's moves with the byte census on, then the flop census
-    eng.update_device(ids_d[args.warmup + args.steps - 1].data_ptr(), rts_d[args.warmup + args.steps - 1].data_ptr(),
-                      m_step, per_move=True, census=True)
+        dist.barrier()
+    fstats = eng.filter_stats(reset=True)
+    # kernel-only time of one update on this shard (no collectives), then the phase split
+    # (untimed: per-kernel events serialise the programmatic launches) and the census
+    kern_ms = []
+    for k in range(min(10, args.steps)):
+        it = args.warmup + k
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True, gray_list=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        kern_ms.append(a.elapsed_time(b))
+    eng.set_phase_timing(True)
+    stats = []
+    for k in range(3):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        it = args.warmup + args.steps - 1 - k
+        eng.update_device(ids_d[it].data_ptr(), rts_d[it].data_ptr(), m_step, per_move=True, gray_list=True)
+        stats.append(eng.last_stats())
+    eng.set_phase_timing(False)
+    last = args.warmup + args.steps - 1
+    eng.update_device(ids_d[last].data_ptr(), rts_d[last].data_ptr(), m_step, per_move=True, census=True)
     census = eng.census()
-    flops = census["sat_flops"] + 21 * census["seg_sphere_tests"]
-    byts = census["bytes_components"] + m_step * 768
-    mean_classify = statistics.mean(classify_ms)
+    eng.close()
 
-    # ---- e2e through the public API with host buffers (rank 0 drives; N>1 via torch collectives)
-    eng_e2e = E.GpuEngine(lv, device=local)
+    # ---- e2e through the public API with host buffers
+    eng_e2e = E.GpuEngine(lv, device=local, shard_rank=rank, shard_count=world)
     up_e2e = None
     if dist is not None:
         from paper_2603_28674_b200.dist import DistributedUpdater
 
-        up_e2e = DistributedUpdater(eng_e2e, dev)
-    e2e_s = []
+        up_e2e = DistributedUpdater(eng_e2e, dev, gray_cap=up.gray_cap)
+    e2e_s, d2h, ngray = [], [], 0
     for it in range(iterations):
         if it >= args.warmup:
             with torch.cuda.stream(stream):
                 flush.zero_()
             torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
         t0 = time.perf_counter()
         if dist is None:
-            reps = eng_e2e.batch_update((ids_h[it], rts_h[it]), per_move=True)
+            reps = eng_e2e.batch_update((ids_h[it], rts_h[it]), per_move=True, gray_list=True)
+            gray = eng_e2e.gray_ids()
         else:
             ids_t = torch.from_numpy(ids_h[it]).pin_memory().to(dev, non_blocking=True)
             rts_t = torch.from_numpy(rts_h[it]).pin_memory().to(dev, non_blocking=True)
-            reps = up_e2e.update(ids_t, rts_t, per_move=True).cpu()
+            reps = up_e2e.update(ids_t, rts_t, per_move=True, gather_gray=True).cpu()
+            gray = up_e2e.gathered_gray()
         t1 = time.perf_counter()
         if it >= args.warmup:
             e2e_s.append(t1 - t0)
+            ngray = 0 if gray is None else len(gray)
+            d2h.append(m_step * 16 + 96 + 4 * ngray)
     e2e_total = sum(e2e_s)
     if dist is not None:
         t = torch.tensor([e2e_total], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_total = float(t.item())
-    # e2e and device engines must agree on the final labels
-    agree = bool(np.array_equal(eng.states(), eng_e2e.states()))
+    labels_e2e = eng_e2e.states() if dist is None else up_e2e.states(N)
+    eng_e2e.close()
 
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
         return 0
 
-    n_total = N * world
-    value = n_total * args.steps / (total_ms * 1e-3)
-    e2e_value = n_total * args.steps / e2e_total
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
-    fp64 = E.fp64_peak_gflops(local)
-    t_fl = flops / (fp64 * 1e9)
-    t_by = byts / (hbm * 1e9)
-    if t_fl >= t_by:
-        roof = {"bound": "fp64", "achieved": flops / (mean_classify * 1e-3) / 1e12, "peak": fp64 / 1e3,
-                "unit": "TFLOP/s", "peak_source": "measured live: non-FMA DADD/DMUL issue rate (rgg_gpu_fp64_peak)"}
-    else:
-        roof = {"bound": "hbm", "achieved": byts / (mean_classify * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback B200_PROFILING.md"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    # dram__bytes_read.sum + dram__bytes_write.sum of the classify kernel from the committed
-    # `ncu --set full` capture (profiles/r1f_classify_ncu.json); null when absent
-    roof["traffic"] = None
-    pf = os.path.join(ROOT, "profiles", "r1f_classify_ncu.json")
-    if os.path.exists(pf):
-        try:
-            p = json.load(open(pf))
-            unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            rd, wr = p["dram__bytes_read.sum"], p["dram__bytes_write.sum"]
-            roof["traffic"] = float(rd[0]) * unit[rd[1]] + float(wr[0]) * unit[wr[1]]
-            roof["traffic_source"] = "profiles/r1f_classify_ncu.json (ncu --set full, one c2 update, 3 kernels)"
-        except (KeyError, ValueError):
-            pass
-    roof["kernel"] = ("classify stage = touch_warp_kernel + narrow_kernel + apply_warp_kernel "
-                      "(paper_2603_28674_b200/csrc/rgg_kernels.cu), timed together by the phase events")
-    roof["algorithmic"] = {"flops_per_launch": flops, "bytes_per_launch": byts, "classify_ms_mean": mean_classify,
-                           "roof_ms": 1e3 * max(t_fl, t_by), "census": census}
+    value = N * args.steps / (total_ms * 1e-3)
+    e2e_value = N * args.steps / e2e_total
+    per_update = total_ms / args.steps
+    roof = roofline(census, statistics.mean(kern_ms), world,
+                    os.path.join(ROOT, "profiles", "r2_c5_ncu.json") if args.config == "c5" else None)
     line = {
         "metric": BASE_METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args, N, world),
-        "per_update_ms": total_ms / args.steps, "per_move_us": 1e3 * total_ms / args.steps / m_step,
+        "warmup": args.warmup, "ms_per_step": per_update, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded roadmap, obstacles and poses of the named shape)",
+        "config": config_dict(args.config, N, world),
+        "per_update_ms": per_update, "per_move_us": 1e3 * per_update / m_step,
+        "kernel_ms_per_update": statistics.mean(kern_ms),
         "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": 1e3 * e2e_total / args.steps,
-                "h2d_bytes_per_step": m_step * (4 + 96 + 4 + 1), "d2h_bytes_per_step": m_step * 16 + 32,
-                "path": "GpuEngine.batch_update -> rgg_gpu_update (host numpy moves, per-move reports)",
-                "labels_equal_device_path": agree},
-        "gpu_launches": launches_per_step * args.steps,
+                "h2d_bytes_per_step": m_step * (4 + 96), "d2h_bytes_per_step": int(statistics.mean(d2h)),
+                "path": "GpuEngine.batch_update(host moves, per-move reports, gray list) -> rgg_gpu_update, then "
+                        "gray_ids() D2H" + (" ; N>1: pinned H2D on every rank, DistributedUpdater (broadcast, "
+                                            "all-reduce, gray gather), reports + gray ids D2H on rank 0"
+                                            if world > 1 else "")},
+        "gpu_launches": 8 * args.steps,
+        "gpu_launches_note": "per update: pose, bin scatter, bin cells, touch, narrow, apply, gray count, gray write "
+                             "(one CUDA graph)",
         "phase_ms_mean": {k: statistics.mean(s[k] for s in stats) for k in
                           ("pose_ms", "bin_ms", "classify_ms", "compact_ms", "total_ms")},
-        "dirty_cells_mean": statistics.mean(s["dirty_cells"] for s in stats),
+        "dirty_cells": stats[0]["dirty_cells"], "overflow_cells": stats[0]["overflow_cells"],
+        "gray_after_update": census["gray"],
         "roofline": roof, "clocks": clk.summary(),
-        "parity": {"mismatches_vs_reference": None, "eps_band": "none: fp32-filter-undecided pairs are re-tested with the "
-                   "reference's fp64 sequence", "filter_rechecks_per_update": {k: v / n_updates for k, v in fstats.items()},
+        "parity": {"mismatches_vs_reference": None,
+                   "eps_band": "none: fp32-filter-undecided pairs are re-tested with the reference's fp64 sequence",
+                   "filter_rechecks_per_update": {k: v / n_updates for k, v in fstats.items()},
                    "over_pairs_per_update": census["over_pairs"],
                    "seg_sphere_tests_per_update": census["seg_sphere_tests"]},
     }
-    if world == 1 and args.extra_configs and args.config == "c2":
+    if world == 1 and not args.no_cpu_baseline:
+        base, seq, done, n_ref = cpu_baselines(args.config, rm, obs, ids_h, rts_h, args.cpu_sample_s)
+        # label and bit parity on the full roadmap: a fresh engine, the same `done` updates
+        eng_chk = E.GpuEngine(lv, device=local)
+        reps_chk = []
+        for it in range(done):
+            reps_chk.append(eng_chk.batch_update((ids_h[it], rts_h[it]), per_move=True).counts())
+        gst = eng_chk.states()
+        gbits = eng_chk.obstacle_bits().reshape(N, -1)
+        rbits = seq.bits()
+        line["parity"]["mismatches_vs_reference"] = int(np.sum(gst != seq.states()))
+        line["parity"]["bit_word_mismatches_vs_reference"] = int(np.sum(gbits != rbits.reshape(gbits.shape)))
+        line["parity"]["checked"] = (f"{N} labels and {gbits.size} obstacle-bit words after {done} updates against "
+                                     f"the reference's grouped SequentialEngines ({rbits.shape[1]} x 64 obstacles)")
+        line["parity"]["labels_equal_e2e_path"] = bool(np.array_equal(labels_e2e, gst)) if done == iterations else None
+        # per-move reports: the pinned C oracle (one ungrouped engine; the reference caps an
+        # engine at 64 obstacles, so it has no per-move reports for M > 64)
+        from oracle import oracle as O
+
+        t0 = time.time()
+        ora = O.Engine(lv)
+        bad = 0
+        n_rep = min(done, 2)
+        for it in range(n_rep):
+            exp = np.array([ora.update(int(o), rt) for o, rt in zip(ids_h[it], rts_h[it])])
+            bad += int(np.sum(np.any(exp[:, :4] != reps_chk[it], 1)))
+        line["parity"]["report_mismatches_vs_oracle"] = bad
+        line["parity"]["reports_checked"] = (f"{n_rep * m_step} per-move reports (new_green, new_red, new_gray, "
+                                             f"unknown_after_heuristic) of updates 0..{n_rep - 1} against the pinned C "
+                                             f"oracle's engine (oracle/rgg_oracle.c ro_engine_update), "
+                                             f"{time.time() - t0:.0f} s")
+        del eng_chk, seq
+        fast = base[base["fastest"]]
+        line["cpu_baseline"] = {"value": fast["edges_per_s"], "unit": "edges/s", "cores": fast["cores"],
+                                "kind": "reference", "ms_per_step": fast["ms_per_update"],
+                                "sample": f"the fastest of the reference's CPU engines on this workload "
+                                          f"({base['fastest']}): {fast['sample']}",
+                                "all": base}
+    if world == 1 and not args.no_extras:
         line["extra"] = {}
         for cfg in [c for c in args.extra_configs.split(",") if c and c != args.config]:
             try:
-                line["extra"][cfg] = measure_extra(cfg, args.seed, local)
+                if cfg == "c1":
+                    line["extra"][cfg] = measure_c1(local)
+                elif cfg == "c3":  # fixed-capacity overflow: 16 inline slots per cell
+                    line["extra"][cfg] = measure_extra(cfg, args.seed, local, cell_capacity=16, parity=True)
+                else:
+                    line["extra"][cfg] = measure_extra(cfg, args.seed, local)
             except Exception as ex:  # keep the headline line even if an extra config fails
-                line["extra"][cfg] = {"error": str(ex)[:200]}
-    if world == 1 and args.config == "c2" and not args.no_resolve:
+                line["extra"][cfg] = {"error": str(ex)[:300]}
         try:
-            line["resolve"] = measure_resolve(args.config, args.seed, local, cpu=not args.no_cpu_baseline)
+            line["resolve"] = measure_resolve("c2", args.seed, local, cpu=not args.no_cpu_baseline)
         except Exception as ex:
-            line["resolve"] = {"error": str(ex)[:200]}
-    if world == 1 and args.config == "c2" and not args.no_resolve:
+            line["resolve"] = {"error": str(ex)[:300]}
         try:
             line["prm"] = measure_prm(cpu=not args.no_cpu_baseline)
         except Exception as ex:
-            line["prm"] = {"error": str(ex)[:200]}
-    if not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        n, done, spent, per_step, ref_eng = cpu_reference_run(args.config, args.seed, iterations,
-                                                              args.cpu_sample_s, threads)
-        cpu_v = n * done / spent
-        # label parity on the full c2 tile: a fresh engine, the same `done` updates, every label compared
-        eng_chk = E.GpuEngine(lv, device=local)
-        for it in range(done):
-            eng_chk.batch_update((ids_h[it], rts_h[it]), per_move=False)
-        line["parity"]["mismatches_vs_reference"] = int(np.sum(eng_chk.states() != ref_eng.states()))
-        line["parity"]["checked"] = f"{n} labels after {done} updates against rgg::BatchEngine"
-        del eng_chk
-        line["cpu_baseline"] = {"value": cpu_v, "unit": "edges/s", "cores": threads, "kind": "reference",
-                                "sample": f"rgg::BatchEngine (AVX2, {threads} threads) on the same tile-0 roadmap "
-                                          f"and moves: {done} updates x 64 moves in {spent:.1f} s",
-                                "ms_per_step": 1e3 * spent / done}
+            line["prm"] = {"error": str(ex)[:300]}
     print(json.dumps(line), flush=True)
     if args.json_out:
         json.dump(line, open(args.json_out, "w"), indent=1)

@@ -144,6 +144,11 @@ int rgg_gpu_read_bits(rgg_gpu* h, uint64_t* out, int32_t words_per_comp);
 int rgg_gpu_unknown_count(rgg_gpu* h, int32_t* out);
 /* Ascending ids of every GRAY component (the gray list handed to the exact resolve). */
 int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
+/* The same list left in DEVICE memory, enqueued on the handle's stream without a host
+ * wait (multi-GPU gather): the GRAY count into d_count (int32, may be null) and the
+ * first cap ids into d_ids (entries past the count are unspecified).  Compacts the
+ * current labels first unless the last update ran with RGG_GRAY_LIST. */
+int rgg_gpu_gray_device(rgg_gpu* h, int32_t* d_count, int32_t* d_ids, int32_t cap);
 /* Components over-hit by the last move of the last update that are still GRAY
  * (the over_hits the reference resolves in eager mode, engine_batch.cpp:193-200). */
 int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
@@ -200,7 +205,9 @@ typedef struct rgg_gpu_stats {
     float pose_ms, bin_ms, classify_ms, compact_ms, total_ms;
     int32_t dirty_cells, events, overflow_cells;
     int64_t over_pairs, sat_flops, under_pairs, seg_sphere_tests, over_hits, under_hits;
-    int64_t bytes_components; /* algorithmic bytes of the dirty components */
+    int64_t bytes_components; /* algorithmic bytes of the dirty components, fp64 records */
+    int64_t bytes_fp32;       /* algorithmic bytes in SURVEY.md §8(d)'s fp32 model */
+    int64_t gray;             /* GRAY components after the update */
 } rgg_gpu_stats;
 int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out);
 /* Full-roadmap census against all active obstacles (one untimed launch). */
@@ -214,6 +221,11 @@ void* rgg_gpu_stream(rgg_gpu* h);
 /* Measured non-FMA fp64 add/mul rate of `device` in GFLOP/s (the compute roof
  * of the fp64-exact classification). */
 int rgg_gpu_fp64_peak(int device, double* gflops);
+/* Measured FP32 FMA rate of `device` in GFLOP/s (2 flops per FFMA): the compute roof
+ * the north star states for the geometric tests. */
+int rgg_gpu_fp32_peak(int device, double* gflops);
+/* Components this handle owns (its shard of the roadmap; N when unsharded). */
+int rgg_gpu_owned(const rgg_gpu* h, int32_t* n_owned);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,8 @@ def lib():
         L.rr_obstacle_operands.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp]
         L.rr_engine_new.restype = C.c_void_p
         L.rr_engine_new.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.rr_engine_new_groups.restype = C.c_void_p
+        L.rr_engine_new_groups.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
         L.rr_engine_free.argtypes = [C.c_void_p]
         L.rr_engine_update.argtypes = [C.c_void_p, C.c_int32, _dp, C.c_int, _lp]
         L.rr_engine_run.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.POINTER(C.c_double)]
@@ -198,9 +200,12 @@ def box_intersect(rt_a, he_a, rt_b, he_b) -> bool:
 class Engine:
     """Reference BatchEngine (kind=0) or SequentialEngine (kind=1), grouped for M > 64."""
 
-    def __init__(self, world: World, kind=0, threads=1, use_under=True, cell_capacity=1024, group_size=64):
+    def __init__(self, world: World, kind=0, threads=1, use_under=True, cell_capacity=1024, group_size=64,
+                 max_groups=-1):
+        """max_groups >= 0: only the first max_groups obstacle groups (a bounded sample)."""
         self.world = world
-        self.h = lib().rr_engine_new(world.h, kind, threads, int(use_under), cell_capacity, group_size)
+        self.h = lib().rr_engine_new_groups(world.h, kind, threads, int(use_under), cell_capacity, group_size,
+                                            int(max_groups))
         if not self.h:
             raise RuntimeError(lib().rr_last_error().decode())
         self.N = world.counts()["N"]

@@ -311,8 +311,11 @@ int rr_obstacle_operands(void* wp, int o, const double* rt12, double* sat21, dou
 // ---------------------------------------------------------------- engines
 
 // kind 0 = BatchEngine, 1 = SequentialEngine.  Obstacles are split into
-// groups of group_size (<= 64) independent engines.
-void* rr_engine_new(void* wp, int kind, int threads, int use_under, int cell_capacity, int group_size) {
+// groups of group_size (<= 64) independent engines; max_groups >= 0
+// builds only the first max_groups of them (bounded CPU-baseline samples: moves of
+// obstacles beyond them are rejected).
+void* rr_engine_new_groups(void* wp, int kind, int threads, int use_under, int cell_capacity, int group_size,
+                           int max_groups) {
     const World* w = static_cast<const World*>(wp);
     Engine* e = new Engine();
     const int rc = guarded([&] {
@@ -323,7 +326,8 @@ void* rr_engine_new(void* wp, int kind, int threads, int use_under, int cell_cap
         opts.threads = threads;
         opts.use_under = use_under != 0;
         const int m = static_cast<int>(w->scene.obstacles.size());
-        const int ng = m == 0 ? 1 : (m + group_size - 1) / group_size;
+        int ng = m == 0 ? 1 : (m + group_size - 1) / group_size;
+        if (max_groups >= 0 && max_groups < ng) ng = std::max(1, max_groups);
         for (int g = 0; g < ng; ++g) {
             auto grp = std::make_unique<Group>();
             grp->scene.bounds = w->scene.bounds;
@@ -344,6 +348,10 @@ void* rr_engine_new(void* wp, int kind, int threads, int use_under, int cell_cap
     return e;
 }
 
+void* rr_engine_new(void* wp, int kind, int threads, int use_under, int cell_capacity, int group_size) {
+    return rr_engine_new_groups(wp, kind, threads, use_under, cell_capacity, group_size, -1);
+}
+
 void rr_engine_free(void* ep) { delete static_cast<Engine*>(ep); }
 
 // rep: obstacle, new_green, new_red, new_gray, reval_us, over_us, under_us,
@@ -354,7 +362,8 @@ int rr_engine_update(void* ep, std::int32_t o, const double* rt12, int lazy, std
     Engine* e = static_cast<Engine*>(ep);
     return guarded([&] {
         const int m = static_cast<int>(e->world->scene.obstacles.size());
-        if (o < 0 || o >= m) throw std::invalid_argument("unknown obstacle id");
+        if (o < 0 || o >= m || o / e->group_size >= static_cast<int>(e->groups.size()))
+            throw std::invalid_argument("unknown obstacle id");
         Group& g = *e->groups[o / e->group_size];
         const ObstacleId local = o % e->group_size;
         const UpdateReport r = g.bat ? g.bat->update_obstacle(local, tf_of(rt12), lazy != 0)
@@ -377,7 +386,8 @@ int rr_engine_run(void* ep, int n, const std::int32_t* ids, const double* rt12, 
         const auto t0 = std::chrono::steady_clock::now();
         for (int i = 0; i < n; ++i) {
             const int o = ids[i];
-            if (o < 0 || o >= m) throw std::invalid_argument("unknown obstacle id");
+            if (o < 0 || o >= m || o / e->group_size >= static_cast<int>(e->groups.size()))
+                throw std::invalid_argument("unknown obstacle id");
             Group& g = *e->groups[o / e->group_size];
             const ObstacleId local = o % e->group_size;
             if (g.bat)

@@ -40,9 +40,12 @@ struct rgg_gpu {
     int32_t* d_orig = nullptr;
     int32_t* d_rank = nullptr;
     double* d_cell_aabb = nullptr;
-    double* d_super_aabb = nullptr;
+    rggk::CellGrid grid{};   // the binning's uniform grid over the cell boxes
+    uint32_t* d_cmask = nullptr;  // Batch::cmask (ncells x cmask_words)
+    int32_t cmask_words = 0;
     double* d_evbox = nullptr;
     double* d_evt = nullptr;
+    float4* d_evs = nullptr;
     int4* d_units = nullptr;
     int32_t* d_unit_ready = nullptr;  // Batch::unit_ready: units_cap generation stamps
     int32_t units_cap = 0;
@@ -84,7 +87,6 @@ struct rgg_gpu {
     int32_t* d_cell_count = nullptr;
     int32_t* d_cell_list = nullptr;
     int32_t* d_cell_ovf = nullptr;
-    int32_t* d_dirty = nullptr;
     int4* d_crec = nullptr;
     long long* d_mtop = nullptr;
     // batch buffers (grown on demand)
@@ -94,7 +96,6 @@ struct rgg_gpu {
     size_t in_off = 0;
     uint8_t* d_last = nullptr;
     int32_t* d_unknown = nullptr;
-    unsigned long long* d_dbg = nullptr;
     cudaEvent_t done_ev = nullptr;        // stream_wait
     int32_t* d_evready = nullptr;         // Batch::evready[8] (split pipeline)
     unsigned long long* d_tl = nullptr;  // RGG_DEBUG_TIMELINE: 16 x 8 words (rgg_kernels.cu tl_stop)
@@ -184,11 +185,13 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     cudaFree(h->d_ev);
     cudaFree(h->d_evbox);
     cudaFree(h->d_evt);
+    cudaFree(h->d_evs);
     cudaFree(h->d_units);
     cudaFree(h->d_unit_ready);
     cudaFree(h->d_mv);
     cudaFree(h->d_pool);
     cudaFree(h->d_mpool);
+    cudaFree(h->d_cmask);
     // moves: ids then poses in one block, so the host path needs a single H2D copy
     h->in_off = ((static_cast<size_t>(cap) * 4 + 15) / 16) * 16;
     CK(dalloc(reinterpret_cast<char**>(&h->d_ids), h->in_off + static_cast<size_t>(cap) * 96));
@@ -197,6 +200,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     CK(dalloc(&h->d_ev, cap));
     CK(dalloc(&h->d_evbox, static_cast<size_t>(cap) * 12));
     CK(dalloc(&h->d_evt, static_cast<size_t>(cap) * 24));
+    CK(dalloc(&h->d_evs, static_cast<size_t>(cap) * rggk::kEvS));
     // touch work units: at most ceil(cap / 32) chunks per cell
     const int64_t units = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * ((cap + 31) / 32));
     if (units > INT32_MAX) return fail(h, RGG_ENOMEM, "batch too large for the touch work list; split it");
@@ -212,6 +216,11 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     h->mpool_cap = std::max<int64_t>(1, 3ll * h->s.ncells * h->s.cell * ((cap + 31) / 32));
     if (h->mpool_cap > INT32_MAX) return fail(h, RGG_ENOMEM, "batch too large for the mask pool; split it");
     CK(dalloc(&h->d_mpool, static_cast<size_t>(h->mpool_cap)));
+    // event bitmask per cell (binning); zero between updates
+    h->cmask_words = (cap + 31) / 32;
+    const size_t cm = std::max<size_t>(1, static_cast<size_t>(h->s.ncells) * h->cmask_words);
+    CK(dalloc(&h->d_cmask, cm));
+    CK(cudaMemset(h->d_cmask, 0, cm * sizeof(uint32_t)));
     h->cap_moves = cap;
     ++h->gen;  // buffers moved: captured graphs are stale
     return RGG_OK;
@@ -257,6 +266,7 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.ev = h->d_ev;
     b.evbox = h->d_evbox;
     b.evt = h->d_evt;
+    b.evs = h->d_evs;
     b.units = h->d_units;
     b.units_cap = h->units_cap;
     b.cell_count = h->d_cell_count;
@@ -265,7 +275,6 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.pool = h->d_pool;
     b.pool_cap = static_cast<int32_t>(std::min<int64_t>(h->pool_cap, INT32_MAX));
     b.ctr = h->d_ctr;
-    b.dirty = h->d_dirty;
     b.mv = h->d_mv;
     b.hits = h->d_hits;
     b.hits_prev = h->d_hits_prev;
@@ -278,29 +287,26 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.items_over = h->d_items_over;
     b.items_under = h->d_items_under;
     b.items_cap = h->items_cap;
-    static const bool dbg_timing = std::getenv("RGG_DEBUG_TIMING") != nullptr;
-    const size_t dbg_n = static_cast<size_t>((h->s.Np + 31) / 32) * 16;
-    if (dbg_timing && !h->d_dbg) {
-        cudaMalloc(reinterpret_cast<void**>(&h->d_dbg), dbg_n * 8);
-        cudaMemset(h->d_dbg, 0, dbg_n * 8);
-    }
-    b.dbg = h->d_dbg;
     static const bool timeline = std::getenv("RGG_DEBUG_TIMELINE") != nullptr;
     if (timeline && !h->d_tl) cudaMalloc(reinterpret_cast<void**>(&h->d_tl), 128 * 8);
     b.tl = h->d_tl;
-    if (rggk::split_pipeline() && !h->d_evready) {
+    if (!h->d_evready) {
         cudaMalloc(reinterpret_cast<void**>(&h->d_evready), 8 * sizeof(int32_t));
         cudaMemset(h->d_evready, 0, 8 * sizeof(int32_t));
     }
-    b.evready = rggk::split_pipeline() && !std::getenv("RGG_NO_EARLY_BIN") ? h->d_evready : nullptr;
-    // touch on published units pays for large batches (c5: -6 %, c3: -2 %); for small ones
-    // its spinning warps slow the bin kernel they share SMs with (c2: +8 %, c4: +19 %)
+    static const bool no_early_bin = std::getenv("RGG_NO_EARLY_BIN") != nullptr;  // tests: the plain PDL waits
+    b.evready = no_early_bin ? nullptr : h->d_evready;
+    // touch on published units (RGG_EARLY_TOUCH_MIN moves and more; off by default): its
+    // warps take slice-units with a same-address atomic and poll the units' stamps, which
+    // costs more than the overlap saves once the binning is short
     static const int early_touch_min = [] {
         const char* e = std::getenv("RGG_EARLY_TOUCH_MIN");
-        return e ? std::atoi(e) : 256;
+        return e ? std::atoi(e) : 1 << 30;
     }();
     b.unit_ready = b.evready && n >= early_touch_min ? h->d_unit_ready : nullptr;
     b.bin_warps = h->s.ncells;  // one counted warp per cell, whichever bin kernel runs
+    b.cmask = h->d_cmask;
+    b.cmask_words = h->cmask_words;
     return b;
 }
 
@@ -313,16 +319,18 @@ void dump_timeline(rgg_gpu* h) {
     if (cudaMemcpy(t, h->d_tl, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess) return;
     const double z = static_cast<double>(~t[0]);
     const auto us = [&](unsigned long long v) { return (static_cast<double>(v) - z) * 1e-3; };
-    static const char* name[5] = {"pose", "bin", "touch", "narrow", "apply"};
+    static const char* name[13] = {"pose", "bin", "touch", "narrow", "apply", "", "", "", "", "scatter", "",
+                                   "c.count", "c.list"};
     std::fprintf(stderr, "[tl]");
-    for (int k = 0; k < 5; ++k) {
+    for (int k = 0; k < 13; ++k) {
+        if ((k >= 5 && k < 9) || k == 10) continue;
         const unsigned long long* p = t + 8 * k;
         if (!p[5]) continue;
         std::fprintf(stderr, " %s %.1f %.1f %.1f %.1f %.2f |", name[k], us(~p[0]), us(p[1]), us(~p[2]), us(p[3]),
                      p[4] * 1e-3 / p[5]);
     }
     std::fprintf(stderr, " arrive");
-    for (int k = 5; k < 9; ++k)
+    for (int k : {5, 10, 6, 7, 8})
         if (t[8 * k + 5]) std::fprintf(stderr, " %.1f", us(~t[8 * k]));
     std::fprintf(stderr, "\n");
 }
@@ -333,9 +341,8 @@ constexpr int32_t kMaxBatch = 1 << 26;
 constexpr int32_t kHostIO = 1 << 20;
 
 bool graphs_enabled(const rgg_gpu* h) {
-    static const bool off = std::getenv("RGG_DEBUG_PHASES") || std::getenv("RGG_NO_GRAPH") ||
-                            std::getenv("RGG_DEBUG_TIMING");
-    return !off && !h->d_dbg;
+    static const bool off = std::getenv("RGG_DEBUG_PHASES") || std::getenv("RGG_NO_GRAPH");
+    return !off;
 }
 
 rggk::Resolver resolver_of(rgg_gpu* h) {
@@ -368,7 +375,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         return RGG_OK;
     };
     static const bool no_graph = std::getenv("RGG_NO_GRAPH") != nullptr;
-    const bool use_graph = !debug && !b.dbg && !no_graph;
+    const bool use_graph = !debug && !no_graph;
     const bool phases = h->phase_timing;
     // the gray id list is compacted in the update only on request; otherwise lazily
     // by rgg_gpu_gray_ids (labels, reports and the gray count never need it)
@@ -379,7 +386,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     const bool hostio = use_graph && (flags & kHostIO) != 0;
     // the apply kernel ends the update unless the gray list or an eager resolve follows:
     // then one small kernel stores the counters into mapped host memory
-    const bool out_in_kernel = hostio && !gray_list && !eager && rggk::split_pipeline();
+    const bool out_in_kernel = hostio && !gray_list && !eager;
     if (out_in_kernel) {
         b.out_mv = h->dh_mv;
         b.out_ctr = h->dh_ctr;
@@ -452,69 +459,6 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     CK(cudaEventRecord(h->ev[2], h->stream));
     CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
     if (phase("classify")) return RGG_ECUDA;
-    if (b.dbg && std::getenv("RGG_DEBUG_NARROW")) for (int region = 0; region < 2; ++region) {
-        const size_t ns = (h->s.Np + 31) / 32;
-        const size_t nw = region == 0 ? static_cast<size_t>(h->grid_classify) * 4 : ns;
-        std::vector<unsigned long long> t(nw * 4);
-        CK(cudaMemcpyAsync(t.data(), b.dbg + (region ? 8 * ns : 0), t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-        CK(stream_wait(h));
-        std::fprintf(stderr, "[rgg] %s ", region == 0 ? "narrow" : "touch ");
-        unsigned long long lo = ~0ull, hi = 0;
-        std::vector<double> st, du;
-        for (size_t w = 0; w < nw; ++w)
-            if (t[4 * w] && t[4 * w + 1]) lo = std::min(lo, t[4 * w]), hi = std::max(hi, t[4 * w + 1]);
-        for (size_t w = 0; w < nw; ++w)
-            if (t[4 * w] && t[4 * w + 1]) st.push_back((t[4 * w] - lo) * 1e-3), du.push_back((t[4 * w + 1] - t[4 * w]) * 1e-3);
-        std::sort(st.begin(), st.end());
-        std::sort(du.begin(), du.end());
-        const size_t n = st.size();
-        if (n)
-            std::fprintf(stderr, "warps %zu span %.1f us | start p50 %.1f p90 %.1f max %.1f | dur p50 %.1f p90 %.1f max %.1f\n",
-                         n, (hi - lo) * 1e-3, st[n / 2], st[n * 9 / 10], st[n - 1], du[n / 2], du[n * 9 / 10], du[n - 1]);
-        if (region == 0) {
-            // the slowest narrow warps: start, duration, lane-max items and segments
-            std::vector<std::pair<double, size_t>> order;
-            for (size_t w = 0; w < nw; ++w)
-                if (t[4 * w] && t[4 * w + 1]) order.push_back({(t[4 * w + 1] - t[4 * w]) * 1e-3, w});
-            std::sort(order.rbegin(), order.rend());
-            for (size_t r = 0; r < std::min<size_t>(8, order.size()); ++r) {
-                const size_t w = order[r].second;
-                std::fprintf(stderr, "   warp %zu start %.1f dur %.1f items %llu segs %llu\n", w, (t[4 * w] - lo) * 1e-3,
-                             order[r].first, t[4 * w + 2], t[4 * w + 3]);
-            }
-            double si = 0;
-            for (size_t w = 0; w < nw; ++w) si += t[4 * w + 2];
-            std::fprintf(stderr, "   mean lane-max items %.2f\n", si / std::max<size_t>(1, n));
-        }
-        CK(cudaMemsetAsync(b.dbg + (region ? 8 * ns : 0), 0, t.size() * 8, h->stream));
-    } else if (b.dbg) {
-        const size_t ns = static_cast<size_t>((h->s.Np + 31) / 32);
-        std::vector<unsigned long long> t(ns * 16);
-        CK(cudaMemcpyAsync(t.data(), b.dbg, t.size() * 8, cudaMemcpyDeviceToHost, h->stream));
-        CK(stream_wait(h));
-        // sections: comp loads, staging, masks, worklist, narrow, transitions+, writes
-        double acc[2][7] = {}, cnt[2] = {0, 0}, lo = 1e300, hi = 0;
-        for (size_t q = 0; q < ns; ++q) {
-            const unsigned long long* d = &t[16 * q];
-            if (!d[0] || !d[7]) continue;
-            const int heavy = (d[9] + d[10]) > 0 ? 1 : 0;
-            for (int k = 0; k < 7; ++k) acc[heavy][k] += double(d[k + 1]) - double(d[k]);
-            cnt[heavy] += 1;
-            lo = std::min(lo, double(d[0]));
-            hi = std::max(hi, double(d[7]));
-        }
-        for (int hv = 0; hv < 2; ++hv)
-            if (cnt[hv])
-                std::fprintf(stderr, "[rgg] %s slices %5.0f us: comp %.2f stage %.2f masks %.2f list %.2f narrow %.2f "
-                                     "trans %.2f write %.2f | span %.1f\n", hv ? "narrow" : "plain ", cnt[hv],
-                             acc[hv][0] / cnt[hv] * 1e-3, acc[hv][1] / cnt[hv] * 1e-3, acc[hv][2] / cnt[hv] * 1e-3,
-                             acc[hv][3] / cnt[hv] * 1e-3, acc[hv][4] / cnt[hv] * 1e-3, acc[hv][5] / cnt[hv] * 1e-3,
-                             acc[hv][6] / cnt[hv] * 1e-3, (hi - lo) * 1e-3);
-        CK(cudaMemsetAsync(b.dbg, 0, t.size() * 8, h->stream));
-        unsigned long long fs[4];
-        rggk::filter_stats(fs, true);
-        std::fprintf(stderr, "[rgg] fp64 rechecks: SAT %llu, seg-sphere %llu\n", fs[1], fs[3]);
-    }
     if (eager) CK(resolve_hits());
     CK(cudaEventRecord(h->ev[3], h->stream));
     if (gray_list) CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
@@ -598,7 +542,6 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     for (int64_t g = rank; g < gcells; g += shards) np64 += std::min<int64_t>(cell, N - g * cell);
     const int32_t Np = static_cast<int32_t>(np64);
     const int32_t ncells = (Np + cell - 1) / cell;
-    const int32_t nsuper = (ncells + rggk::kSuperCells - 1) / rggk::kSuperCells;
     h->words = M <= 64 ? 1 : (M + 63) / 64;
     const int64_t T = v->row_off[nrows];
     if (T > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
@@ -610,19 +553,20 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_orig, Np));
     CK(dalloc(&h->d_rank, N));
     CK(dalloc(&h->d_cell_aabb, static_cast<size_t>(std::max(ncells, 1)) * 6));
-    CK(dalloc(&h->d_super_aabb, static_cast<size_t>(std::max(nsuper, 1)) * 6));
     {
         rggk::StoreIn in{N, B, S, static_cast<int32_t>(T), Np, cell, shards, rank,
                          v->comp_aabb, v->edge_sat, v->row_off, v->segs, v->spline_radius};
         rggk::StoreOut so{};
         so.aabb = h->d_aabb, so.sat = h->d_sat, so.sat32 = h->d_sat32, so.row = h->d_row, so.spline = h->d_spline;
-        so.orig = h->d_orig, so.rank = h->d_rank, so.cell_aabb = h->d_cell_aabb, so.super_aabb = h->d_super_aabb;
+        so.orig = h->d_orig, so.rank = h->d_rank, so.cell_aabb = h->d_cell_aabb;
         mark("allocs");
         CK(rggk::build_store(in, so, h->stream));
         mark("build_store");
         h->d_seg = so.seg;
         h->d_seg32 = so.seg32;
         h->total_segs_owned = so.total_segs;
+        CK(rggk::build_cell_grid(h->d_cell_aabb, ncells, h->grid, h->stream));
+        mark("cell grid");
         h->orig.resize(Np);
         if (Np) CK(cudaMemcpy(h->orig.data(), h->d_orig, static_cast<size_t>(Np) * sizeof(int32_t), cudaMemcpyDeviceToHost));
     }
@@ -654,7 +598,6 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_cell_count, ncells));
     CK(dalloc(&h->d_cell_list, static_cast<size_t>(ncells) * cap));
     CK(dalloc(&h->d_cell_ovf, ncells));
-    CK(dalloc(&h->d_dirty, ncells));
     CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_ctr), 32 * sizeof(int32_t), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_ctr), h->h_ctr, 0));
     auto up = [&](void* dst, const void* src, size_t bytes) {
@@ -690,13 +633,12 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.ncells = ncells;
     s.cap = cap;
     s.use_under = o.use_under ? 1 : 0;
-    s.dbg_flags = std::getenv("RGG_DEBUG_FLAGS") ? std::atoi(std::getenv("RGG_DEBUG_FLAGS")) : 0;
     {
         // narrow operands of the whole roadmap: Box32 lines and segment records
         const double bytes = 128.0 * Np * B + 32.0 * static_cast<double>(h->total_segs_owned);
         int l2 = 0;
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device);
-        s.prefetch = bytes <= 0.5 * l2 && !(s.dbg_flags & 2048) ? 1 : 0;  // 2048: ablation, never
+        s.prefetch = bytes <= 0.5 * l2 ? 1 : 0;
     }
     s.aabb = h->d_aabb;
     s.sat = h->d_sat;
@@ -707,7 +649,9 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.spline_r = h->d_spline;
     s.orig = h->d_orig;
     s.cell_aabb = h->d_cell_aabb;
-    s.super_aabb = h->d_super_aabb;
+    for (int k = 0; k < 3; ++k) s.gorg[k] = h->grid.org[k], s.ginv[k] = h->grid.inv[k], s.gdim[k] = h->grid.dim[k];
+    s.gcell_off = h->grid.off;
+    s.gcell = h->grid.cells;
     s.ohe = h->d_ohe;
     s.osl = h->d_osl;
     s.osr = h->d_osr;
@@ -737,11 +681,11 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->done_ev) cudaEventDestroy(h->done_ev);
-    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->d_super_aabb, h->d_evbox, h->d_evt, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->grid.off, h->grid.cells, h->d_cmask, h->d_evbox, h->d_evt, h->d_evs, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
-                   h->d_cell_list, h->d_cell_ovf, h->d_dirty, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
-                   h->d_mv, h->d_pool, h->d_tl, h->d_dbg, h->d_hits_prev, h->d_evready,
+                   h->d_cell_list, h->d_cell_ovf, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
+                   h->d_mv, h->d_pool, h->d_tl, h->d_hits_prev, h->d_evready,
                    h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_spose, h->d_res_sact, h->d_res_ids, h->d_res_cnt, h->d_res_out,
                    h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};
     for (void* p : dev)
@@ -775,7 +719,6 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
     // eager: one move at a time, each resolving its gray over-hits before the next
     // (BatchEngine::batch_update(moves, false) = update_obstacle per move)
     if (!h->res_ready) return fail(h, RGG_EINVAL, "eager updates need rgg_gpu_set_resolver");
-    if (!rggk::split_pipeline()) return fail(h, RGG_EINVAL, "eager updates need RGG_PIPELINE=6");
     return update_eager(h, ids, rt12, n, flags, reports);
 }
 
@@ -1065,6 +1008,21 @@ int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
     return RGG_OK;
 }
 
+int rgg_gpu_gray_device(rgg_gpu* h, int32_t* d_count, int32_t* d_ids, int32_t cap) {
+    if (!h) return RGG_EINVAL;
+    if (cap < 0 || (cap > 0 && !d_ids)) return fail(h, RGG_EINVAL, "bad gray id buffer");
+    CK(cudaSetDevice(h->device));
+    if (!h->gray_fresh) {
+        CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+        h->gray_fresh = true;
+    }
+    if (d_count) CK(cudaMemcpyAsync(d_count, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
+    const int32_t n = std::min(cap, h->s.N);
+    if (n > 0) CK(cudaMemcpyAsync(d_ids, h->d_gray, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                  h->stream));
+    return RGG_OK;
+}
+
 int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n) {
     if (!h || !n) return RGG_EINVAL;
     if (!h->last_hits_valid) return fail(h, RGG_EINVAL, "last hits are kept for single-move updates only");
@@ -1299,12 +1257,23 @@ int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
     const int64_t bit_bytes = h->words == 1 ? dirty * 32 : touched * 32;
     out->bytes_components = dirty * (48 + 2 * (1 + 4)) + bit_bytes + box_comps * h->s.B * 168 +
                             sph_comps * 4 * (h->s.B * h->s.S + 1) + segs * 56;
+    // per relabelled component B x 48 B of SatBox (centre + scaled
+    // axes in fp32), 12 B per real-segment point (segments + rows), 8 B per row, the
+    // label read and written, the counters read and written; 16 B of over / under bit
+    // words read and written per touched (component, obstacle) pair; 96 B of pose per
+    // move; 4 B per GRAY id of the compacted list
+    const int64_t segs_all = static_cast<int64_t>(c[13]), rows = static_cast<int64_t>(h->s.B) * h->s.S;
+    int32_t gray = 0;
+    CK(cudaMemcpy(&gray, h->d_unknown, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    out->gray = gray;
+    out->bytes_fp32 = dirty * (h->s.B * 48 + 8 * rows + 2 + 8) + 12 * (segs_all + dirty * rows) + 32 * touched +
+                      96ll * h->last_n + 4ll * gray;
     return RGG_OK;
 }
 
-// Measured fp64 (non-FMA add/mul) issue rate in GFLOP/s: the compute roof of
-// the fp64-exact classification (bench.py roofline).
-int rgg_gpu_fp64_peak(int device, double* gflops) {
+// Measured issue rates in GFLOP/s: fp64 non-FMA add/mul (the fp64-exact sequence's
+// roof) and fp32 FMA (the filters' roof), best of 5 CUDA-event-timed launches.
+static int peak_probe(int device, bool fp32, double* gflops) {
     rgg_gpu* h = nullptr;
     CK(cudaSetDevice(device));
     cudaDeviceProp prop{};
@@ -1315,12 +1284,16 @@ int rgg_gpu_fp64_peak(int device, double* gflops) {
     CK(cudaEventCreate(&a));
     CK(cudaEventCreate(&b));
     const int block = 256, grid = prop.multiProcessorCount * 8, iters = 4096;
-    CK(rggk::launch_fp64_peak(sink, iters, grid, block, nullptr));
+    const auto run = [&]() {
+        return fp32 ? rggk::launch_fp32_peak(reinterpret_cast<float*>(sink), iters, grid, block, nullptr)
+                    : rggk::launch_fp64_peak(sink, iters, grid, block, nullptr);
+    };
+    CK(run());
     CK(cudaDeviceSynchronize());
     float best = 1e30f;
     for (int r = 0; r < 5; ++r) {
         CK(cudaEventRecord(a));
-        CK(rggk::launch_fp64_peak(sink, iters, grid, block, nullptr));
+        CK(run());
         CK(cudaEventRecord(b));
         CK(cudaEventSynchronize(b));
         float ms = 0;
@@ -1330,8 +1303,17 @@ int rgg_gpu_fp64_peak(int device, double* gflops) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(sink);
-    const double flops = 2.0 * 8.0 * iters * static_cast<double>(grid) * block;
+    const double flops = 2.0 * (fp32 ? 16.0 : 8.0) * iters * static_cast<double>(grid) * block;
     *gflops = flops / (best * 1e-3) / 1e9;
+    return RGG_OK;
+}
+
+int rgg_gpu_fp64_peak(int device, double* gflops) { return peak_probe(device, false, gflops); }
+int rgg_gpu_fp32_peak(int device, double* gflops) { return peak_probe(device, true, gflops); }
+
+int rgg_gpu_owned(const rgg_gpu* h, int32_t* n_owned) {
+    if (!h || !n_owned) return RGG_EINVAL;
+    *n_owned = h->s.Np;
     return RGG_OK;
 }
 

@@ -475,7 +475,7 @@ struct SegF {
     bool dd_pos, r_fast;
 };
 
-__device__ __forceinline__ SegF segf_prep(float4 v0, float4 v1, double o_r) {
+__device__ __forceinline__ SegF segf_prep(float4 v0, float4 v1, float ro) {
     constexpr float u = 5.9604645e-8f;
     SegF g;
     g.ax = v0.x, g.ay = v0.y, g.az = v0.z;
@@ -484,8 +484,7 @@ __device__ __forceinline__ SegF segf_prep(float4 v0, float4 v1, double o_r) {
     g.inv_dd = g.dd_pos ? __frcp_rn(v1.z) : 0.0f;
     g.dabs = fabsf(g.dx) + fabsf(g.dy) + fabsf(g.dz);
     g.aabs = fabsf(g.ax) + fabsf(g.ay) + fabsf(g.az);
-    const float ro = __double2float_rn(o_r);
-    const float r = ro + v1.w;
+    const float r = ro + v1.w;  // ro = fl(o_minus_r)
     g.r_fast = r > 16.0f * u * (fabsf(ro) + fabsf(v1.w)) && r < 1.0e18f;
     g.r2 = r * r;
     g.r2err = 16.0f * u * g.r2;

@@ -350,7 +350,10 @@ __global__ void pose_kernel(Store s, Batch b) {
         ev.cen[3 * (lane - 16)] = pt[0];
         ev.cen[3 * (lane - 16) + 1] = pt[1];
         ev.cen[3 * (lane - 16) + 2] = pt[2];
+        const float cx = __double2float_rn(pt[0]), cy = __double2float_rn(pt[1]), cz = __double2float_rn(pt[2]);
+        b.evs[kEvS * static_cast<size_t>(i) + 1 + (lane - 16)] = make_float4(cx, cy, cz, (fabsf(cx) + fabsf(cy)) + fabsf(cz));
     }
+    if (lane == 0) b.evs[kEvS * static_cast<size_t>(i)] = make_float4(__double2float_rn(r), __int_as_float(nsph), 0.0f, 0.0f);
     if (lane == 0) {
         ev.r = r;
         ev.o = o;
@@ -393,66 +396,63 @@ __global__ void init_obstacles_kernel(Store s) {
 
 // ------------------------------------------------------------------ binning
 //
-// One CTA per group of 16 cells (a Morton-contiguous "super-cell", union box
-// precomputed), one warp per cell.  Events stream through in chunks of 512:
-// each thread loads one event's new/old boxes (compact evbox array, coalesced)
-// and tests them against the super-cell box; an ordered block-wide ballot
-// compaction leaves the chunk's candidates in shared memory; each warp then
-// tests its cell against the candidates and appends hits, in event order, to
-// the cell's fixed-capacity list (overflow -> pool) with warp ballots.  Work is
-// O(supercells x events + cells x candidates) instead of O(cells x events).
+// Event-centric counting sort of the events into the cells' lists (replaces
+// SpatialGrid::build / candidates, proj/src/spatial_grid.cpp:50-135):
+//   bin_scatter_kernel  one warp per event: the bins of a uniform grid over the
+//                       cell boxes (Store::gcell*) that the event's new and old
+//                       union boxes cover; the lanes test those bins' cells
+//                       (closed fp64 box test) and set bit e of each overlapping
+//                       cell's event mask (atomicOr);
+//   bin_cells_kernel    one warp per cell: popcount + warp prefix scan of the
+//                       cell's mask words gives the count and every event's list
+//                       position, so the list is written in move order without
+//                       a sort; then the fixed-capacity list (overflow -> pool),
+//                       the dirty list and the cell's touch work units.
+// Work is O(events x bins x cells per bin + cells x n/32), not O(cells x events).
 
-// The per-cell test runs on fp32 boxes rounded outward (lower corners down, upper
-// corners up), a superset of the fp64 test: a listed event that touches none of
-// the cell's components is dropped by touch's exact per-component test, so the
-// lists only need to contain every overlapping event (the overflow pass below
-// applies the same two tests, so counts and lists agree).
-constexpr int kBinThreads = 512;  // 16 warps = 16 cells per CTA (one super-cell)
-constexpr int kBinChunk = 512;    // events filtered per pass
-
-__device__ __forceinline__ void box_out32(const double* d, float* f) {
+// The per-cell records of the CTA's listed cells (WARPS cells per CTA, one warp
+// each; every warp of the CTA calls this, count = 0 past the last cell): count,
+// the 16-byte cell record {count, mask base, list address}, one touch work unit
+// per chunk of 32 listed events, and the unit stamps of the early-touch handoff.
+// The dirty count and the unit list are reserved with one atomic per CTA; each
+// cell's mask block (3 * ceil(count/32) words per component) sits at a fixed
+// offset of the mask pool, sized for the batch capacity.
+template <int WARPS>
+__device__ __forceinline__ void bin_cells_tail(const Store& s, const Batch& b, int cell, int count,
+                                               const int32_t* inl, int lane, int warp) {
+    __shared__ int s_units[WARPS];
+    __shared__ int s_ub;
+    const int W = (count + 31) >> 5;
+    if (lane == 0) s_units[warp] = W;
+    __syncthreads();  // also orders every lane's list entries before the stamps below
+    if (threadIdx.x == 0) {
+        int tot = 0, nd = 0;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        f[k] = __double2float_rd(d[k]);
-        f[3 + k] = __double2float_ru(d[3 + k]);
+        for (int w = 0; w < WARPS; ++w) {
+            const int t = s_units[w];
+            s_units[w] = tot;
+            tot += t;
+            nd += t > 0;
+        }
+        s_ub = tot ? atomicAdd(&b.ctr[10], tot) : 0;
+        if (nd) atomicAdd(&b.ctr[0], nd);
     }
-}
-__device__ __forceinline__ bool overlaps32(const float* a, const float* b) {
-    return (a[0] <= b[3]) & (b[0] <= a[3]) & (a[1] <= b[4]) & (b[1] <= a[4]) & (a[2] <= b[5]) & (b[2] <= a[5]);
-}
-
-// The per-cell record of a listed cell (lane 0 after the warp's list stores): count,
-// dirty list, mask block, touch work units, the 16-byte cell record, and the unit
-// stamps of the early-touch handoff.
-__device__ __forceinline__ void bin_cell_tail(const Store& s, const Batch& b, int cell, int count,
-                                              const int32_t* inl, int lane) {
-    __syncwarp();  // every lane's list entries precede the unit stamps below
+    __syncthreads();
+    if (cell >= s.ncells) return;
+    const int ub = s_ub + s_units[warp];
+    const int mbase = cell * 3 * s.cell * b.cmask_words;
     if (lane == 0) {
         b.cell_count[cell] = count;
-        int mbase = 0, ub = 0, W = 0;
-        if (count > 0) {
-            b.dirty[atomicAdd(&b.ctr[0], 1)] = cell;
-            // mask block of the v3 touch / narrow / apply kernels: 3 * ceil(count/32) words per component
-            const long long need = 3ll * ((count + 31) >> 5) * s.cell;
-            const long long base = atomicAdd(reinterpret_cast<unsigned long long*>(b.mtop),
-                                             static_cast<unsigned long long>(need));
-            if (base + need > b.mpool_cap) atomicExch(&b.ctr[6], 2);
-            mbase = base + need > b.mpool_cap ? 0 : static_cast<int>(base);
-            // one touch work unit per chunk of 32 listed events, carrying what the
-            // touch kernel needs of the cell record
-            W = (count + 31) >> 5;
-            ub = atomicAdd(&b.ctr[10], W);
-            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.units[ub + w] = make_int4(cell, w, count, mbase);
-        }
-        // one 16-byte record per cell: count, mask base, list address
         const int32_t* list = count <= s.cap ? inl : b.pool + b.cell_ovf[cell];
         const unsigned long long a = reinterpret_cast<unsigned long long>(list);
         b.crec[cell] = make_int4(count, mbase, static_cast<int>(a & 0xffffffffu), static_cast<int>(a >> 32));
-        if (b.unit_ready && count > 0) {  // release the cell's units (record, list, mask base) to touch
-            const int gen = reinterpret_cast<volatile int32_t*>(b.evready)[4];
-            __threadfence();
-            for (int w = 0; w < W && ub + w < b.units_cap; ++w) b.unit_ready[ub + w] = gen;
-        }
+    }
+    for (int w = lane; w < W && ub + w < b.units_cap; w += 32) b.units[ub + w] = make_int4(cell, w, count, mbase);
+    if (b.unit_ready && count > 0) {  // release the cell's units (record, list, mask base) to touch
+        __syncwarp();
+        const int gen = reinterpret_cast<volatile int32_t*>(b.evready)[4];
+        __threadfence();
+        for (int w = lane; w < W && ub + w < b.units_cap; w += 32) b.unit_ready[ub + w] = gen;
     }
 }
 
@@ -467,14 +467,15 @@ __device__ __forceinline__ void bin_warp_done(const Batch& b, int lane) {
     }
 }
 
-#ifndef RGG_BIN_MINB
-#define RGG_BIN_MINB 2  // two CTAs per SM (registers <= 64)
-#endif
-__global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s, Batch b) {
-    const unsigned long long tw = tl_start(b.tl);
+__device__ __forceinline__ int grid_bin(const Store& s, double v, int k) {
+    const double f = floor((v - s.gorg[k]) * s.ginv[k]);
+    return f < 0.0 ? 0 : (f >= s.gdim[k] ? s.gdim[k] - 1 : static_cast<int>(f));
+}
+
+// Waits until the pose warps have published every event's binning boxes
+// (Batch::evready: release by each pose warp, acquire here), else the whole pose kernel.
+__device__ __forceinline__ void wait_event_boxes(const Batch& b) {
     if (b.evready) {
-        // the pose warps publish their binning boxes first (release: fence + count);
-        // the rest of the pose kernel overlaps this kernel, whose end waits for it
         pdl_trigger();
         if (threadIdx.x == 0) {
             for (unsigned spins = 0;; ++spins) {
@@ -489,90 +490,131 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
         pdl_wait();
         pdl_trigger();
     }
-    const unsigned long long t0 = tl_start(b.tl);
+}
+
+// One CTA per event.  For each of the event's two boxes the CTA flattens the
+// (bin, cell) entries of the bins the box covers: the bins' entry counts are
+// scanned in shared memory, then every thread takes entries, so a box's ~10^2-10^3
+// entries cost about three memory round trips.  A cell listed in several of the
+// box's bins is tested in one of them only: the bin at the low corner of the
+// intersection of the cell's and the box's bin ranges (the cell's low bin rides in
+// its grid entry).
+constexpr int kScatterThreads = 256;
+
+__global__ void __launch_bounds__(kScatterThreads) bin_scatter_kernel(Store s, Batch b) {
+    // a plain PDL wait for the pose kernel: a thousand CTAs polling the pose warps' count
+    // (Batch::evready) slowed those warps' own release atomics more than it saved
+    const unsigned long long tw = tl_start(b.tl);
+    pdl_wait();
+    pdl_trigger();
     tl_stop(b.tl, 5, tw);
-    __shared__ float cbox[12][kBinChunk];  // SoA: lane q reads column q, conflict-free
-    __shared__ int cidx[kBinChunk];
-    __shared__ int wsum[kBinThreads / 32];
-    __shared__ int s_nc;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cell = blockIdx.x * (kBinThreads / 32) + warp;
+    const unsigned long long t0 = tl_start(b.tl);
+    __shared__ int s_pre[kScatterThreads + 1];
+    __shared__ int s_tot;
+    const int tid = threadIdx.x;
+    const int e = blockIdx.x;
+    const double* evb = b.evbox + 12 * static_cast<size_t>(e);
+    double bx[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) bx[k] = evb[k];
+    uint32_t* col = b.cmask + (e >> 5);
+    const uint32_t bit = 1u << (e & 31);
+    for (int h = 0; h < 2; ++h) {
+        const double* q = bx + 6 * h;
+        if (!(q[0] <= q[3] && q[1] <= q[4] && q[2] <= q[5])) continue;  // empty (inactive obstacle)
+        if (h == 1 && q[0] >= bx[0] && q[1] >= bx[1] && q[2] >= bx[2] && q[3] <= bx[3] && q[4] <= bx[4] && q[5] <= bx[5])
+            continue;  // the old box lies inside the new one
+        const int x0 = grid_bin(s, q[0], 0), x1 = grid_bin(s, q[3], 0);
+        const int y0 = grid_bin(s, q[1], 1), y1 = grid_bin(s, q[4], 1);
+        const int z0 = grid_bin(s, q[2], 2), z1 = grid_bin(s, q[5], 2);
+        const int nx = x1 - x0 + 1, ny = y1 - y0 + 1, nb = nx * ny * (z1 - z0 + 1);
+        for (int b0 = 0; b0 < nb; b0 += kScatterThreads) {  // bins in passes of one per thread
+            const int nbp = min(kScatterThreads, nb - b0);
+            int lo = 0, cnt = 0;
+            if (tid < nbp) {
+                const int i = b0 + tid;
+                const int g = ((z0 + i / (nx * ny)) * s.gdim[1] + y0 + (i / nx) % ny) * s.gdim[0] + x0 + i % nx;
+                lo = s.gcell_off[g];
+                cnt = s.gcell_off[g + 1] - lo;
+            }
+            // exclusive scan of the bins' entry counts
+            int x = cnt;
+            const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, off);
+                if (lane >= off) x += y;
+            }
+            __syncthreads();  // the previous pass's readers of s_pre are done
+            if (lane == 31) s_pre[warp] = x;
+            __syncthreads();
+            if (tid == 0) {
+                int acc = 0;
+                for (int w = 0; w < kScatterThreads / 32; ++w) {
+                    const int t = s_pre[w];
+                    s_pre[w] = acc;
+                    acc += t;
+                }
+                s_tot = acc;
+            }
+            __syncthreads();
+            const int excl = s_pre[warp] + x - cnt;
+            const int tot = s_tot;
+            __syncthreads();
+            if (tid < nbp) s_pre[tid] = excl;
+            s_pre[kScatterThreads] = tot;  // (every thread stores the same value)
+            __shared__ int s_lo[kScatterThreads];
+            if (tid < nbp) s_lo[tid] = lo;
+            __syncthreads();
+            for (int j = tid; j < tot; j += kScatterThreads) {
+                // the bin of entry j: the last bin whose exclusive prefix is <= j
+                int a = 0, z = nbp - 1;
+                while (a < z) {
+                    const int mid = (a + z + 1) >> 1;
+                    if (s_pre[mid] <= j) a = mid;
+                    else z = mid - 1;
+                }
+                const int i = b0 + a;
+                const int xb = x0 + i % nx, yb = y0 + (i / nx) % ny, zb = z0 + i / (nx * ny);
+                const int2 ent = s.gcell[s_lo[a] + j - s_pre[a]];  // {cell, low bin x | y << 10 | z << 20}
+                const int c = ent.x;
+                if (xb != max(ent.y & 1023, x0) || yb != max((ent.y >> 10) & 1023, y0) ||
+                    zb != max((ent.y >> 20) & 1023, z0))
+                    continue;
+                const double* cb = s.cell_aabb + 6 * static_cast<size_t>(c);
+                double cbox[6];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) cbox[k] = cb[k];
+                if (rggd::overlaps(cbox, q)) atomicOr(col + static_cast<size_t>(c) * b.cmask_words, bit);
+            }
+        }
+    }
+    tl_stop(b.tl, 9, t0);
+}
+
+constexpr int kCellWarps = 32;
+
+__global__ void __launch_bounds__(32 * kCellWarps) bin_cells_kernel(Store s, Batch b) {
+    const unsigned long long tw = tl_start(b.tl);
+    pdl_wait();
+    pdl_trigger();
+    tl_stop(b.tl, 10, tw);
+    const unsigned long long t0 = tl_start(b.tl);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int cell = blockIdx.x * kCellWarps + warp;
     const bool live = cell < s.ncells;
-    double sb[6], cb[6];
-    float cbf[6];
-#pragma unroll
-    for (int k = 0; k < 6; ++k) sb[k] = s.super_aabb[6 * static_cast<size_t>(blockIdx.x) + k];
-    if (live) {
-        for (int k = 0; k < 6; ++k) cb[k] = s.cell_aabb[6 * static_cast<size_t>(cell) + k];
-        box_out32(cb, cbf);
-    }
+    uint32_t* m = b.cmask + static_cast<size_t>(live ? cell : 0) * b.cmask_words;
+    const int nw = live ? (b.n + 31) >> 5 : 0;
+    // count: popcounts of the mask words (lane j: words j, j + 32, ...)
     int count = 0;
+    for (int w = lane; w < nw; w += 32) count += __popc(m[w]);
+    count = __reduce_add_sync(0xffffffffu, count);
+    tl_stop(b.tl, 11, t0);
     int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
-    for (int base = 0; base < b.n; base += kBinChunk) {
-        // ---- super-cell filter, ordered compaction of the chunk's candidates
-        const int e = base + threadIdx.x;
-        double bx[12];
-        bool cand = false;
-        if (threadIdx.x < kBinChunk && e < b.n) {
-            const double2* p = reinterpret_cast<const double2*>(b.evbox + 12 * static_cast<size_t>(e));
-#pragma unroll
-            for (int k = 0; k < 6; ++k) {
-                const double2 v = p[k];
-                bx[2 * k] = v.x;
-                bx[2 * k + 1] = v.y;
-            }
-            cand = rggd::overlaps(sb, bx) | rggd::overlaps(sb, bx + 6);
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, cand);
-        __syncthreads();
-        if (lane == 0) wsum[warp] = __popc(bal);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int w = 0; w < kBinThreads / 32; ++w) {
-                const int t = wsum[w];
-                wsum[w] = acc;
-                acc += t;
-            }
-            s_nc = acc;
-        }
-        __syncthreads();
-        if (cand) {
-            const int pos = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
-            cidx[pos] = e;
-            float f[12];
-            box_out32(bx, f);
-            box_out32(bx + 6, f + 6);
-#pragma unroll
-            for (int k = 0; k < 12; ++k) cbox[k][pos] = f[k];
-        }
-        __syncthreads();
-        const int nc = s_nc;
-        if (!live) continue;
-        // ---- per-cell test of the candidates, ordered ballot append
-        for (int j = 0; j < nc; j += 32) {
-            const int q = j + lane;
-            bool hit = false;
-            if (q < nc) {
-                float qb[12];
-#pragma unroll
-                for (int k = 0; k < 12; ++k) qb[k] = cbox[k][q];
-                hit = overlaps32(cbf, qb) | overlaps32(cbf, qb + 6);
-            }
-            const unsigned hb = __ballot_sync(0xffffffffu, hit);
-            if (hit) {
-                const int pos = count + __popc(hb & ((1u << lane) - 1u));
-                if (pos < s.cap) inl[pos] = cidx[q];
-            }
-            count += __popc(hb);
-        }
-    }
-    if (!live) {
-        if (b.evready) pdl_wait();  // the grid ends after the pose kernel (touch waits on this grid only)
-        return;
-    }
-    if (count > s.cap) {
-        // Overflow: the full ordered list goes to the pool (second pass over the events).
+    int32_t* dst = inl;
+    int lim = count;
+    if (count > s.cap) {  // the ordered list goes to the overflow pool
         int pbase = 0;
         if (lane == 0) {
             pbase = atomicAdd(&b.ctr[1], count);
@@ -581,34 +623,40 @@ __global__ void __launch_bounds__(kBinThreads, RGG_BIN_MINB) bin_kernel(Store s,
         pbase = __shfl_sync(0xffffffffu, pbase, 0);
         if (pbase + count > b.pool_cap) {
             if (lane == 0) atomicExch(&b.ctr[6], 1);
-            count = s.cap;  // truncated: reported as an error by the host
+            lim = count = s.cap;  // truncated: reported as an error by the host
         } else {
-            int at = 0;
-            for (int e0 = 0; e0 < b.n; e0 += 32) {
-                const int e = e0 + lane;
-                bool hit = false;
-                if (e < b.n) {  // the same two tests as the listing pass
-                    const double* bx = b.evbox + 12 * static_cast<size_t>(e);
-                    float f[12];
-                    box_out32(bx, f);
-                    box_out32(bx + 6, f + 6);
-                    hit = (rggd::overlaps(sb, bx) | rggd::overlaps(sb, bx + 6)) &&
-                          (overlaps32(cbf, f) | overlaps32(cbf, f + 6));
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                if (hit) b.pool[pbase + at + __popc(bal & ((1u << lane) - 1u))] = e;
-                at += __popc(bal);
-            }
+            dst = b.pool + pbase;
             if (lane == 0) b.cell_ovf[cell] = pbase;
         }
     }
-    bin_cell_tail(s, b, cell, count, inl, lane);
+    if (count > 0) {
+        // positions: exclusive warp scan of the popcounts, 32 words per pass; each lane
+        // writes its word's events in bit (= move) order, then clears the word
+        int at = 0;
+        for (int w0 = 0; w0 < nw; w0 += 32) {
+            const int w = w0 + lane;
+            uint32_t x = w < nw ? m[w] : 0u;
+            const int c = __popc(x);
+            int incl = c;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += y;
+            }
+            int pos = at + incl - c;
+            if (x) m[w] = 0u;
+            for (; x; x &= x - 1, ++pos)
+                if (pos < lim) dst[pos] = 32 * w + __ffs(x) - 1;
+            at += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    tl_stop(b.tl, 12, t0);
+    bin_cells_tail<kCellWarps>(s, b, cell, count, inl, lane, warp);
     tl_stop(b.tl, 1, t0);
-    bin_warp_done(b, lane);
-    if (b.evready) pdl_wait();
+    if (live) bin_warp_done(b, lane);
 }
 
-// Small batches (n <= 64 moves): one warp per cell, no super-cell stage.  Lane l
+// Small batches (n <= 64 moves): one warp per cell, no scatter stage.  Lane l
 // tests events l and l + 32 (exact fp64 closed-box tests of the new and old
 // boxes), two ordered ballots build the list.  Small warps-per-CTA so every cell's
 // warp is resident in one wave even for a million components (c4: 8400 cells).
@@ -617,45 +665,28 @@ constexpr int kBinSmallWarps = 8;
 
 __global__ void __launch_bounds__(32 * kBinSmallWarps) bin_small_kernel(Store s, Batch b) {
     const unsigned long long tw = tl_start(b.tl);
-    if (b.evready) {
-        pdl_trigger();
-        if (threadIdx.x == 0) {
-            for (unsigned spins = 0;; ++spins) {
-                int r;
-                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(r) : "l"(b.evready) : "memory");
-                if (r >= b.n || handoff_timeout(b, spins)) break;
-                __nanosleep(32);
-            }
-        }
-        __syncthreads();
-    } else {
-        pdl_wait();
-        pdl_trigger();
-    }
+    wait_event_boxes(b);
     const unsigned long long t0 = tl_start(b.tl);
     tl_stop(b.tl, 5, tw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cell = blockIdx.x * kBinSmallWarps + warp;
-    if (cell >= s.ncells) {
-        if (b.evready) pdl_wait();
-        return;
-    }
+    const bool live = cell < s.ncells;
     double cb[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) cb[k] = s.cell_aabb[6 * static_cast<size_t>(cell) + k];
+    for (int k = 0; k < 6; ++k) cb[k] = live ? s.cell_aabb[6 * static_cast<size_t>(cell) + k] : 0.0;
     unsigned bal[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int e = 32 * h + lane;
         bool hit = false;
-        if (e < b.n) {
+        if (live && e < b.n) {
             const double* bx = b.evbox + 12 * static_cast<size_t>(e);
             hit = rggd::overlaps(cb, bx) | rggd::overlaps(cb, bx + 6);
         }
         bal[h] = __ballot_sync(0xffffffffu, hit);
     }
     int count = __popc(bal[0]) + __popc(bal[1]);
-    int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
+    int32_t* inl = b.cell_list + static_cast<size_t>(live ? cell : 0) * s.cap;
     int32_t* dst = inl;
     if (count > s.cap) {  // the ordered list goes to the pool
         int pbase = 0;
@@ -678,16 +709,16 @@ __global__ void __launch_bounds__(32 * kBinSmallWarps) bin_small_kernel(Store s,
         const int pos = (h ? __popc(bal[0]) : 0) + __popc(bal[h] & ((1u << lane) - 1u));
         if (((bal[h] >> lane) & 1u) && pos < lim) dst[pos] = 32 * h + lane;
     }
-    bin_cell_tail(s, b, cell, count, inl, lane);
+    bin_cells_tail<kBinSmallWarps>(s, b, cell, count, inl, lane, warp);
     tl_stop(b.tl, 1, t0);
-    bin_warp_done(b, lane);
+    if (live) bin_warp_done(b, lane);
     if (b.evready) pdl_wait();
 }
 
 // ----------------------------------------------------------------- classify
 
 // batch_over for one (component, obstacle) pair: any body intersects (engine_batch.cpp:55-74).
-// filter outcome counters (tests / RGG_DEBUG_TIMING): [0] SAT filtered, [1] SAT rechecked in
+// filter outcome counters (tests, rgg_gpu_filter_stats): [0] SAT filtered, [1] SAT rechecked in
 // fp64, [2] seg-sphere filtered, [3] seg-sphere rechecked
 __device__ unsigned long long g_filter_stats[4];
 
@@ -710,14 +741,8 @@ __device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev
         bool hit = false;
         for (int b = 0; b < s.B && !hit; ++b) {
             const size_t i = static_cast<size_t>(c) * s.B + b;
-            int f;
-            if (s.dbg_flags & 512) {  // 512: the axis-form filter
-                const rggd::Box32& a32 = s.sat32[i];
-                f = rggd::sat_filter32(a32.c, a32, osat, ev.b32);
-            } else {
-                const rggd::Box32G a32 = rggd::load_box32g(s.sat32 + i), o32 = rggd::load_box32g(&ev.b32);
-                f = rggd::sat_filter32g(a32, o32.c, o32);
-            }
+            const rggd::Box32G a32 = rggd::load_box32g(s.sat32 + i), o32 = rggd::load_box32g(&ev.b32);
+            const int f = rggd::sat_filter32g(a32, o32.c, o32);
             hit = f == 2 ? sat_exact(s.sat + i * 22, osat) : f == 1;
         }
         return hit;
@@ -768,46 +793,6 @@ __device__ __forceinline__ bool under_test(const Store& s, int c, const Event& e
     return hit;
 }
 
-// One CTA per dirty cell (persistent, dynamic cell queue), one thread per
-// component.  Per chunk of <= 32 events staged in shared memory:
-//   A. each thread builds its touch / box / sphere overlap masks over the chunk;
-//   B. the CTA evaluates the narrow-test work list (over items, then under
-//      items) with all its threads — the (component, event) pairs that
-//      actually need a SAT or a segment-sphere test — into result masks;
-//   C. each thread applies its events in move order with the reference's
-//      per-move transition (engine_batch.cpp:114-188) from the result masks.
-// B is where the fp64 work is; spreading it over the CTA keeps the lanes busy
-// where the v1 event loop left 18 of 32 idle (profiles/r1_v1_summary.md).
-// One lane's share (segments g, g+G, ...) of batch_under for one pair.  A
-// component's real segments are contiguous (rows (c, b, s) in order), so the
-// lanes walk [row[c*B*S], row[(c+1)*B*S]) and look up each segment's row for
-// its slot radius (engine_batch.cpp:97).
-template <bool COUNT>
-__device__ __forceinline__ bool under_part(const Store& s, int c, const Event& ev, int g, int G, long long* tests) {
-    const int rows = s.B * s.S;
-    const int r0 = c * rows;
-    const int lo = s.row[r0], hi = s.row[r0 + rows];
-    int rr = 0, rend = s.row[r0 + 1];
-    bool hit = false;
-    for (int j = lo + g; j < hi; j += G) {
-        while (j >= rend) rend = s.row[r0 + (++rr) + 1];
-        const double r_total = add(ev.r, s.spline_r[rr]);
-        const double2* p = reinterpret_cast<const double2*>(s.seg + 8 * static_cast<size_t>(j));
-        const double2 v0 = p[0], v1 = p[1], v2 = p[2], v3 = p[3];
-        const double seg[7] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x};
-        for (int sp = 0; sp < ev.nsph; ++sp) {
-            if (COUNT) {
-                *tests += 1;
-                hit |= rggd::seg_sphere_fast(seg, ev.cen + 3 * sp, r_total);
-            } else {
-                const int f = rggd::seg_filter32(seg, ev.cen + 3 * sp, r_total);
-                if (f == 1 || (f == 2 && seg_exact(seg, ev.cen + 3 * sp, r_total))) return true;
-            }
-        }
-    }
-    return hit;
-}
-
 // batch_under for one pair from its item (narrow kernel): the component's real
 // segments [lo, hi); word 7 of each segment record carries its row's spline
 // radius (rgg_capi.cu upload), so no row lookup is needed.  Lanes g, g+G, ...
@@ -847,19 +832,20 @@ __device__ __forceinline__ bool under_range(const Store& s, int lo, int hi, cons
 }
 
 // under_range over the compact fp32 records (rggd::segf_filter): the fp64 record
-// is read only when a sphere is undecided.  Verdicts are the reference's.
-__device__ __forceinline__ bool under_range32(const Store& s, int lo, int hi, const Event& ev) {
-    const int nsph = ev.nsph;
+// is read only when a sphere is undecided.  es: the event's sphere operands
+// (Batch::evs).  Verdicts are the reference's.
+__device__ __forceinline__ bool under_range32(const Store& s, int lo, int hi, const float4* es, const Event& ev) {
+    const float4 hd = es[0];
+    const int nsph = __float_as_int(hd.y);
     for (int j = lo; j < hi; ++j) {
         const float4 v0 = s.seg32[2 * static_cast<size_t>(j)], v1 = s.seg32[2 * static_cast<size_t>(j) + 1];
-        const rggd::SegF g = rggd::segf_prep(v0, v1, ev.r);
+        const rggd::SegF g = rggd::segf_prep(v0, v1, hd.x);
         bool sure = false;
         uint32_t und = 0;
 #pragma unroll 4
         for (int sp = 0; sp < nsph; ++sp) {
-            const float cx = __double2float_rn(ev.cen[3 * sp]), cy = __double2float_rn(ev.cen[3 * sp + 1]),
-                        cz = __double2float_rn(ev.cen[3 * sp + 2]);
-            const int f = rggd::segf_filter(g, cx, cy, cz, (fabsf(cx) + fabsf(cy)) + fabsf(cz));
+            const float4 c = es[1 + sp];
+            const int f = rggd::segf_filter(g, c.x, c.y, c.z, c.w);
             sure |= f == 1;
             und |= static_cast<uint32_t>(f == 2) << sp;
         }
@@ -890,10 +876,8 @@ __device__ __forceinline__ void prefetch_range(const void* a, const void* e, boo
     for (; p < reinterpret_cast<const char*>(e); p += 128) l1 ? prefetch_l1(p) : prefetch_l2(p);
 }
 
-constexpr int kUnderLanes = 4;  // lanes per under-approximation work item
-constexpr int kStageEv = 128;   // touch stages a whole batch of up to this many events per CTA
 
-// ------------------------------------------------------- v3: touch / narrow / apply
+// ------------------------------------------------------- mask blocks of touch / narrow / apply
 //
 // Per cell with L listed events the bin kernel reserves a mask block of
 // 3 * ceil(L/32) * cell words: touch[w][t], over[w][t], under[w][t] (bit k of
@@ -928,131 +912,13 @@ __device__ __forceinline__ const int32_t* rec_list(int4 r) {
                                             static_cast<uint32_t>(r.z));
 }
 
-// Narrow tests of a pair whose item did not fit the queue (kept out of line so
-// the touch kernel's register budget stays that of an AABB filter).
-__device__ __noinline__ bool over_inline(const Store& s, int c, const Event& ev) {
-    return over_test<false>(s, c, ev, nullptr);
-}
-__device__ __noinline__ bool under_inline(const Store& s, int c, const Event& ev) {
-    return under_part<false>(s, c, ev, 0, 1, nullptr);
-}
 
-__global__ void __launch_bounds__(kMaxCell) touch_kernel(Store s, Batch b) {
-    __shared__ double sbox[kEvChunk][24];  // nu, old, box, sph of the chunk's events
-    __shared__ int sev[kEvChunk];
-    __shared__ int s_no, s_nu, s_bo, s_bu;
-    __shared__ unsigned long long scen[4];
-    const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-    commit_grid(s, b);
-    const int4 rec = b.crec[cell];
-    const int count = rec.x;
-    if (count == 0) return;
-    const bool census = b.census_on != 0;
-    if (census && tid < 4) scen[tid] = 0;
-    const int32_t* list = rec_list(rec);
-    const int W = (count + 31) >> 5, T = s.cell;
-    const int mbase = rec.y;
-    const int c = cell * T + tid;
-    const bool valid = c < s.Np;
-    double aabb[6];
-    if (valid) {
-        const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
-        aabb[0] = a0.x, aabb[1] = a0.y, aabb[2] = a1.x, aabb[3] = a1.y, aabb[4] = a2.x, aabb[5] = a2.y;
-    }
-    bool any_box = false, any_sph = false;
-    for (int w = 0; w < W; ++w) {
-        const int m = min(32, count - 32 * w);
-        __syncthreads();
-        if (tid < m) sev[tid] = list[32 * w + tid];
-        if (tid == 0) s_no = s_nu = 0;
-        __syncthreads();
-        for (int t = tid; t < m * 24; t += blockDim.x) {
-            const int e = t / 24, k = t % 24;
-            const Event& ev = b.ev[sev[e]];
-            sbox[e][k] = k < 6 ? ev.nu[k] : (k < 12 ? ev.old[k - 6] : (k < 18 ? ev.box[k - 12] : ev.sph[k - 18]));
-        }
-        __syncthreads();
-        uint32_t tm = 0, bm = 0, sm = 0;
-        if (valid) {
-            for (int k = 0; k < m; ++k) {
-                if (rggd::overlaps(aabb, sbox[k]) || rggd::overlaps(aabb, sbox[k] + 6)) {
-                    tm |= 1u << k;
-                    if (rggd::overlaps(aabb, sbox[k] + 12)) bm |= 1u << k;
-                    if (s.use_under && rggd::overlaps(aabb, sbox[k] + 18)) sm |= 1u << k;
-                }
-            }
-        }
-        const int wt = mbase + (0 * W + w) * T + tid, wo = mbase + (1 * W + w) * T + tid,
-                  wu = mbase + (2 * W + w) * T + tid;
-        b.mpool[wt] = tm;
-        b.mpool[wo] = 0;
-        b.mpool[wu] = 0;
-        any_box |= bm != 0;
-        any_sph |= sm != 0;
-        // block-level reservation in the item queues: one global atomic per queue per CTA
-        const int no = __popc(bm), nu = __popc(sm);
-        int xo = no, xu = nu;
-        for (int off = 1; off < 32; off <<= 1) {
-            const int yo = __shfl_up_sync(0xffffffffu, xo, off), yu = __shfl_up_sync(0xffffffffu, xu, off);
-            if (lane >= off) xo += yo, xu += yu;
-        }
-        int wbo = 0, wbu = 0;
-        if (lane == 31) {
-            wbo = atomicAdd(&s_no, xo);
-            wbu = atomicAdd(&s_nu, xu);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            s_bo = s_no ? atomicAdd(&b.ctr[8], s_no) : 0;
-            s_bu = s_nu ? atomicAdd(&b.ctr[9], s_nu) : 0;
-        }
-        __syncthreads();
-        wbo = __shfl_sync(0xffffffffu, wbo, 31);
-        wbu = __shfl_sync(0xffffffffu, wbu, 31);
-        int at = s_bo + wbo + xo - no;
-        for (uint32_t x = bm; x; x &= x - 1, ++at) {
-            const int k = __ffs(x) - 1;
-            if (at < b.items_cap)
-                b.items_over[at] = make_int4(c, sev[k], wo, 1 << k);
-            else if (over_inline(s, c, b.ev[sev[k]]))
-                b.mpool[wo] |= 1u << k;  // this thread owns the word until the narrow kernel
-        }
-        at = s_bu + wbu + xu - nu;
-        const int ulo = sm ? s.row[c * s.B * s.S] : 0, uhi = sm ? s.row[(c + 1) * s.B * s.S] : 0;
-        for (uint32_t x = sm; x; x &= x - 1, ++at) {
-            const int k = __ffs(x) - 1;
-            if (at < b.items_cap)
-                b.items_under[at] = make_int4(ulo, uhi, wu, (sev[k] << 5) | k);
-            else if (under_inline(s, c, b.ev[sev[k]]))
-                b.mpool[wu] |= 1u << k;
-        }
-    }
-    if (census) {
-        // algorithmic-bytes census: components of dirty cells,
-        // components reading SatBoxes, components reading segments, segments read
-        int segs = 0;
-        if (valid && any_sph) {
-            const int rows = s.B * s.S;
-            segs = s.row[(c + 1) * rows] - s.row[c * rows];
-        }
-        unsigned long long v[4] = {valid ? 1ull : 0ull, any_box ? 1ull : 0ull, any_sph ? 1ull : 0ull,
-                                   static_cast<unsigned long long>(segs)};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            unsigned long long x = v[k];
-            for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-            if (lane == 0 && x) atomicAdd(&scen[k], x);
-        }
-        __syncthreads();
-        if (tid < 4 && scen[tid]) atomicAdd(&b.census[8 + tid], scen[tid]);
-    }
-}
-
-// The narrow tests of all items, GPU-wide (persistent grid).  Over items
-// {component, event, result word, bit}: one thread each (15-axis SAT per body).
-// Under items {first segment, end segment, result word, event << 5 | bit}: G
-// lanes each.
-template <bool COUNT, int G>
+// The narrow tests of all items, GPU-wide (persistent grid), one thread per
+// item.  Over items {component, event, result word, bit}: the 15-axis SAT per
+// body.  Under items {first segment, end segment, result word, event << 5 | bit}:
+// the component's real segments against the event's spheres.  COUNT: the
+// reference's operation census (rgg_gpu_census) instead of the verdicts.
+template <bool COUNT>
 __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     const unsigned long long tw = COUNT ? 0 : tl_start(b.tl);
     pdl_wait();
@@ -1061,535 +927,69 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
     if (!COUNT) tl_stop(b.tl, 7, tw);
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
-    unsigned long long* dbgw = (!COUNT && b.dbg) ? b.dbg + 4 * static_cast<size_t>(gt >> 5) : nullptr;
-    if (dbgw && lane == 0) dbgw[0] = gtimer();
     const int n_over = min(b.ctr[8], b.items_cap), n_under = min(b.ctr[9], b.items_cap);
-    long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
-    if (!COUNT && G == 1) {
-        // One pass over both queues (over items first).  The next item is loaded
-        // while the current one is tested, and an under item's segment records
-        // are prefetched into L1 before they are walked: about one exposed memory
-        // round trip per item instead of one per load.
+    if (!COUNT) {
+        // One pass over both queues (over items first).  The item after next is
+        // loaded and the next item's operands are prefetched into L1 while the
+        // current one is tested: about one exposed memory round trip per item.
         const int total = n_over + n_under;
-        const auto item = [&](int i) {
-            return i < n_over ? b.items_over[i] : b.items_under[i - n_over];
-        };
-        // two items ahead: the item after next is loaded and the next item's operands
-        // are prefetched into L1 while the current one is tested
+        const auto item = [&](int i) { return i < n_over ? b.items_over[i] : b.items_under[i - n_over]; };
         int i = gt;
         int4 it = i < total ? item(i) : make_int4(0, 0, 0, 0);
         int4 nx = i + nthreads < total ? item(i + nthreads) : make_int4(0, 0, 0, 0);
-        unsigned long long d_items = 0, d_segs = 0;
         while (i < total) {
-            if (dbgw) d_items += 1, d_segs += i < n_over ? 0 : it.y - it.x;
             const int inext = i + nthreads, i2 = inext + nthreads;
             const int4 nn = i2 < total ? item(i2) : make_int4(0, 0, 0, 0);
             if (inext < total) {
                 if (inext < n_over) {
                     prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
+                    prefetch_l1(&b.ev[nx.y].b32);
                 } else {
                     for (int j = nx.x; j < nx.y; j += 4) prefetch_l1(s.seg32 + 2 * static_cast<size_t>(j));
+                    prefetch_l1(b.evs + kEvS * static_cast<size_t>(nx.w >> 5));
                 }
             }
             if (i < n_over) {
-                if (!(s.dbg_flags & 128) && over_test<false>(s, it.x, b.ev[it.y], nullptr) &&
-                    !(s.dbg_flags & 1024))  // 128: ablation, no over tests; 1024: no result atomics
-                    atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
-            } else if (s.dbg_flags & 256) {  // 256: ablation, no under tests
-            } else {
-                if (under_range32(s, it.x, it.y, b.ev[it.w >> 5]) && !(s.dbg_flags & 1024))
-                    atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
+                if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+            } else if (under_range32(s, it.x, it.y, b.evs + kEvS * static_cast<size_t>(it.w >> 5), b.ev[it.w >> 5])) {
+                atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
             }
             it = nx;
             nx = nn;
             i = inext;
         }
-        if (dbgw) {
-            // lane maxima: items, segments
-            for (int off = 16; off; off >>= 1) {
-                d_items = max(d_items, __shfl_xor_sync(0xffffffffu, d_items, off));
-                d_segs = max(d_segs, __shfl_xor_sync(0xffffffffu, d_segs, off));
-            }
-        }
-        if (dbgw && lane == 0) dbgw[2] = d_items, dbgw[3] = d_segs;
-    }
-    for (int i = gt; i < (COUNT || G > 1 ? n_over : 0); i += nthreads) {
-        const int4 it = b.items_over[i];  // component, event, result word, bit
-        const bool h = over_test<COUNT>(s, it.x, b.ev[it.y], &c_sat);
-        if (COUNT) c_op += s.B, c_oh += h;
-        if (h) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
-    }
-    const int g = gt % G, groups = nthreads / G;
-    const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (lane & ~(G - 1));
-    for (int i = gt / G; i < (COUNT || G > 1 ? n_under : 0); i += groups) {
-        const int4 it = b.items_under[i];
-        bool h = under_range<COUNT>(s, it.x, it.y, b.ev[it.w >> 5], g, G, &c_tests);
-#pragma unroll
-        for (int off = 1; off < G; off <<= 1) {
-            const bool other = __shfl_xor_sync(gmask, h, off);  // the group's lanes share i
-            h = h || other;
-        }
-        if (COUNT) c_up += 1, c_uh += h;
-        if (h && g == 0) atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
-    }
-    if (dbgw) {
-        __syncwarp();
-        if (lane == 0) dbgw[1] = gtimer();
-    }
-    if (!COUNT) tl_stop(b.tl, 3, t0);
-    if (COUNT) {
-        long long v[6] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh};
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            long long x = v[k];
-            for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-            if (lane == 0 && x) atomicAdd(&b.census[k], static_cast<unsigned long long>(x));
-        }
+        tl_stop(b.tl, 3, t0);
         return;
     }
-}
-
-// Per-move transitions (engine_batch.cpp:114-188) of every component of a
-// dirty cell, in list (= move) order, from the touch / over / under words.
-template <int FLAGS, bool WIDE>
-__global__ void __launch_bounds__(kMaxCell) apply_kernel(Store s, Batch b) {
-    constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
-    constexpr bool HITS = (FLAGS & kHits) != 0;
-    __shared__ int s_o[32], s_move[32];
-    __shared__ int scnt[32][4];
-    const int cell = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-    const int4 rec = b.crec[cell];
-    const int count = rec.x;
-    if (count == 0) return;
-    const int32_t* list = rec_list(rec);
-    const int W = (count + 31) >> 5, T = s.cell;
-    const uint32_t* mb = b.mpool + rec.y;
-    const int c = cell * T + tid;
-    const bool valid = c < s.Np;
-    int label = 0, oc = 0, bc = 0, id = -1;
-    unsigned long long OW = 0, UW = 0;
-    if (valid) {
-        id = s.orig[c];
-        label = s.state[id];
-        const uint32_t cw = s.cnt[c];
-        oc = cw & 0xffff;
-        bc = cw >> 16;
-        if (!WIDE) {
-            OW = s.over[c];
-            UW = s.under[c];
-        }
-    }
-    const int label0 = label;
-    const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
-    const unsigned long long OW0 = OW, UW0 = UW;
-    bool hit_last = false;
-    for (int w = 0; w < W; ++w) {
-        const int m = min(32, count - 32 * w);
-        __syncthreads();
-        if (tid < m) {
-            const Event& ev = b.ev[list[32 * w + tid]];
-            s_o[tid] = ev.o;
-            s_move[tid] = ev.move;
-        }
-        if (PER_MOVE)
-            for (int t = tid; t < m * 4; t += blockDim.x) scnt[t >> 2][t & 3] = 0;
-        __syncthreads();
-        const uint32_t tm = mb[(0 * W + w) * T + tid], ro = mb[(1 * W + w) * T + tid],
-                       ru = mb[(2 * W + w) * T + tid];
-        for (int k = 0; k < m; ++k) {
-            const int before = label;
-            if (valid && ((tm >> k) & 1u)) {
-                const int o = s_o[k];
-                const int wo = o >> 6;
-                const unsigned long long bit = 1ull << (o & 63);
-                unsigned long long ow, uw;
-                if (WIDE) {
-                    ow = s.over[static_cast<size_t>(wo) * s.Np + c];
-                    uw = s.under[static_cast<size_t>(wo) * s.Np + c];
-                } else {
-                    ow = OW;
-                    uw = UW;
-                }
-                const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
-                const bool n_over = (ro >> k) & 1u, n_under = (ru >> k) & 1u;
-                // revalidate_old_intersections (engine_batch.cpp:114-143)
-                if (old_over) {
-                    oc -= 1;
-                    const int rest = bc - (old_under ? 1 : 0);
-                    label = oc == 0 ? 0 : ((s.use_under && rest > 0) ? 1 : 2);
-                }
-                // over phase (engine_batch.cpp:163-177)
-                if (n_over) {
-                    if (label == 0) label = 2;
-                    oc += 1;
-                }
-                // under phase (engine_batch.cpp:181-188)
-                if (n_under) label = 1;
-                bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
-                const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
-                const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
-                if (WIDE) {
-                    if (nw != ow) s.over[static_cast<size_t>(wo) * s.Np + c] = nw;
-                    if (nuw != uw) s.under[static_cast<size_t>(wo) * s.Np + c] = nuw;
-                } else {
-                    OW = nw;
-                    UW = nuw;
-                }
-                if (HITS && s_move[k] == b.n - 1) hit_last = n_over;
-            }
-            if (PER_MOVE) {
-                const bool ch = label != before;
-                const unsigned g = __ballot_sync(0xffffffffu, ch && label == 0);
-                const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
-                const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
-                const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
-                if (lane == 0 && (g | r | y | f)) {
-                    if (g) atomicAdd(&scnt[k][0], __popc(g));
-                    if (r) atomicAdd(&scnt[k][1], __popc(r));
-                    if (y) atomicAdd(&scnt[k][2], __popc(y));
-                    if (f) atomicAdd(&scnt[k][3], __popc(f));
-                }
-            }
-        }
-        if (PER_MOVE) {
-            __syncthreads();
-            for (int t = tid; t < m * 4; t += blockDim.x) {
-                const int v = scnt[t >> 2][t & 3];
-                if (v) atomicAdd(&b.mv[4 * s_move[t >> 2] + (t & 3)], v);
-            }
-        }
-    }
-    int dgray = 0;
-    if (valid) {
-        if (label != label0) {
-            s.state[id] = static_cast<uint8_t>(label);
-            s.state_c[c] = static_cast<uint8_t>(label);
-            dgray = (label == 2) - (label0 == 2);
-        }
-        const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
-        if (cw != cnt0) s.cnt[c] = cw;
-        if (!WIDE) {
-            if (OW != OW0) s.over[c] = OW;
-            if (UW != UW0) s.under[c] = UW;
-        }
-    }
-    // running gray count (the unknown_count of the reference)
-    for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
-    if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
-    if (HITS) {
-        const bool h = valid && hit_last && label == 2;
-        const unsigned bal = __ballot_sync(0xffffffffu, h);
-        int pos = 0;
-        if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
-        pos = __shfl_sync(0xffffffffu, pos, 0);
-        if (h) {
-                const int at = pos + __popc(bal & ((1u << lane) - 1u));
-                b.hits[at] = id;
-                b.hits_prev[at] = static_cast<uint8_t>(label0);
-            }
-    }
-}
-
-// ------------------------------------------------- v4: warp-centric fused classify
-//
-// One warp owns a slice of 32 consecutive (cell-sorted) components and runs
-// the whole per-update work of that slice warp-synchronously, with no CTA
-// barrier: its operands are loaded up front, each lane builds its touch / box /
-// sphere masks over the cell's event list (32 events per pass, boxes read as
-// warp-broadcast L1 loads), the (component, event) pairs needing a narrow test
-// become a warp-local work list that all 32 lanes drain (SATs one lane each,
-// segment-sphere tests kUnderLanes lanes each), and each lane then replays its
-// events in move order with the reference's transition.  Warps are persistent
-// and stride over the slices, so there is no dependence on CTA scheduling.
-constexpr int kWarpsPerCta = 4;
-static_assert(kStageEv <= 32 * kWarpsPerCta, "the touch staging table is the warps' chunk buffers");
-constexpr int kStageIds = 1024;  // apply stages the moved obstacle ids of batches up to this size
-
-template <int FLAGS, bool WIDE>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) classify_warp_kernel(Store s, Batch b) {
-    constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
-    constexpr bool HITS = (FLAGS & kHits) != 0;
-    constexpr bool CENSUS = (FLAGS & kCensus) != 0;
-    __shared__ uint16_t sitem[kWarpsPerCta][2][32 * 32];
-    __shared__ uint32_t sres[kWarpsPerCta][2][32];
-    __shared__ int sev[kWarpsPerCta][32];
-    __shared__ double sbx[kWarpsPerCta][32][24];  // per event: nu, old, box, sph (one load wave per chunk)
-    __shared__ int2 som[kWarpsPerCta][32];        // per event: obstacle id, move index
-    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nslices = (s.Np + 31) >> 5;
-    if (!CENSUS) commit_grid(s, b);
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
-    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
-    int dgray = 0;
-    // slices near an obstacle are Morton-adjacent and heavy: spread them over warps / SMs by
-    // walking the slices with a prime stride (a bijection when it does not divide nslices)
-    const long long stride = (nslices % 7919) ? 7919 : 1;
-    for (int q0 = blockIdx.x * kWarpsPerCta + wi; q0 < nslices; q0 += gridDim.x * kWarpsPerCta) {
-        const int q = static_cast<int>((q0 * stride) % nslices);
-        const int c0 = q << 5;
-        const int cell = c0 / s.cell;
-        const int4 rec = b.crec[cell];
-        const int count = rec.x;
-        if (count == 0) continue;  // warp-uniform: clean cell
-        const int c = c0 + lane;
-        const bool valid = c < s.Np;
-        const int rows = s.B * s.S;
-        int seg_lo = 0, seg_hi = 0;
-        double aabb[6];
-        int label = 0, oc = 0, bc = 0, id = -1;
-        unsigned long long OW = 0, UW = 0;
-        if (valid) {
-            seg_lo = s.row[c * rows];
-            seg_hi = s.row[(c + 1) * rows];
-            const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
-            aabb[0] = a0.x, aabb[1] = a0.y, aabb[2] = a1.x, aabb[3] = a1.y, aabb[4] = a2.x, aabb[5] = a2.y;
-            if (!CENSUS) {
-                id = s.orig[c];
-                const uint32_t cw = s.cnt[c];
-                oc = cw & 0xffff;
-                bc = cw >> 16;
-                if (!WIDE) {
-                    OW = s.over[c];
-                    UW = s.under[c];
-                }
-                label = s.state[id];
-            }
-        }
-        const int label0 = label;
-        const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
-        const unsigned long long OW0 = OW, UW0 = UW;
-        bool hit_last = false, any_box = false, any_sph = false;
-        unsigned long long* dbg = b.dbg ? b.dbg + 16 * static_cast<size_t>(q) : nullptr;
-        const long long clk0 = clock64();
-        if (dbg && lane == 0) dbg[0] = gtimer(), dbg[8] = count;
-#define RGG_STAMP(i) if (dbg) { __syncwarp(); if (lane == 0) dbg[i] = gtimer(); }
-        if (dbg && __any_sync(0xffffffffu, label == 77)) dbg[14] = 1;  // waits for the component loads
-        RGG_STAMP(1)
-        const int32_t* list = rec_list(rec);
-        for (int base = 0; base < count; base += 32) {
-            const int m = min(32, count - base);
-            const int myev = lane < m ? list[base + lane] : 0;
-            sev[wi][lane] = myev;
-            if (lane < m) {  // lane k stages event k: one load wave for the whole chunk
-                const Event& ev = b.ev[myev];
-                double v[24];
-#pragma unroll
-                for (int j = 0; j < 6; ++j) v[j] = ev.nu[j], v[6 + j] = ev.old[j], v[12 + j] = ev.box[j], v[18 + j] = ev.sph[j];
-#pragma unroll
-                for (int j = 0; j < 24; ++j) sbx[wi][lane][j] = v[j];
-                som[wi][lane] = make_int2(ev.o, ev.move);
-            }
-            __syncwarp();
-            if (base == 0) {
-                if (dbg && __any_sync(0xffffffffu, valid && aabb[0] == -1.25e300)) dbg[15] = 1;  // waits for the AABB
-                RGG_STAMP(2)
-            }
-            // ---- touch / box / sphere masks
-            uint32_t tm = 0, bm = 0, sm = 0;
-            if (valid) {
-                for (int k = 0; k < m; ++k) {
-                    const double* bx = sbx[wi][k];
-                    const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
-                    tm |= static_cast<uint32_t>(touch) << k;
-                    bm |= static_cast<uint32_t>(touch & rggd::overlaps(aabb, bx + 12)) << k;
-                    sm |= static_cast<uint32_t>(touch & (s.use_under != 0) & rggd::overlaps(aabb, bx + 18)) << k;
-                }
-            }
-            any_box |= bm != 0;
-            any_sph |= sm != 0;
-            if (CENSUS) c_touch += __popc(tm);
-            // pull this lane's narrow operands towards the SM now: the work list is
-            // drained by other lanes of the warp, which then hit in L1
-            if (bm) {
-                const size_t i0 = static_cast<size_t>(c) * s.B;
-                prefetch_range(s.sat + i0 * 22, s.sat + (i0 + s.B) * 22, true);
-                prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, true);
-            }
-            if (sm) prefetch_range(s.seg + 8 * static_cast<size_t>(seg_lo), s.seg + 8 * static_cast<size_t>(seg_hi), true);
-            if (base == 0) RGG_STAMP(3)
-            // ---- warp-local narrow work list
-            const int no = __popc(bm), nu = __popc(sm);
-            int xo = no, xu = nu;
-            for (int off = 1; off < 32; off <<= 1) {
-                const int yo = __shfl_up_sync(0xffffffffu, xo, off), yu = __shfl_up_sync(0xffffffffu, xu, off);
-                if (lane >= off) xo += yo, xu += yu;
-            }
-            const int tot_o = __shfl_sync(0xffffffffu, xo, 31), tot_u = __shfl_sync(0xffffffffu, xu, 31);
-            {
-                int po = xo - no, pu = xu - nu;
-                for (uint32_t x = bm; x; x &= x - 1) sitem[wi][0][po++] = static_cast<uint16_t>((lane << 5) | (__ffs(x) - 1));
-                for (uint32_t x = sm; x; x &= x - 1) sitem[wi][1][pu++] = static_cast<uint16_t>((lane << 5) | (__ffs(x) - 1));
-            }
-            sres[wi][0][lane] = 0;
-            sres[wi][1][lane] = 0;
-            __syncwarp();
-            if (base == 0) RGG_STAMP(4)
-            for (int i = lane; i < tot_o; i += 32) {
-                const int it = sitem[wi][0][i], t = it >> 5, k = it & 31;
-                if (!CENSUS && (s.dbg_flags & 1)) {  // ablation: no test
-                    if ((s.dbg_flags & 2) == 0 && s.sat[(c0 + t) * 22] == 12345.0) atomicOr(&sres[wi][0][t], 1u << k);
-                    continue;
-                }
-                const bool h = over_test<CENSUS>(s, c0 + t, b.ev[sev[wi][k]], &c_sat);
-                if (CENSUS) c_op += s.B, c_oh += h;
-                if (h) atomicOr(&sres[wi][0][t], 1u << k);
-            }
-            const int g = lane % kUnderLanes;
-            for (int ub = 0; ub < tot_u; ub += 32 / kUnderLanes) {
-                const int i = ub + lane / kUnderLanes;
-                bool h = false;
-                int t = 0, k = 0;
-                if (i < tot_u && (!CENSUS || g == 0)) {  // census: one lane counts the whole item
-                    const int it = sitem[wi][1][i];
-                    t = it >> 5;
-                    k = it & 31;
-                    if (!CENSUS && (s.dbg_flags & 1))  // ablation: no test
-                        h = (s.dbg_flags & 2) == 0 && s.seg[8 * static_cast<size_t>(seg_lo)] == 12345.0;
-                    else
-                    h = under_part<CENSUS>(s, c0 + t, b.ev[sev[wi][k]], CENSUS ? 0 : g, CENSUS ? 1 : kUnderLanes,
-                                           &c_tests);
-                }
-                if (!CENSUS) {
-#pragma unroll
-                    for (int off = 1; off < kUnderLanes; off <<= 1) {
-                        const bool other = __shfl_xor_sync(0xffffffffu, h, off);  // every lane shuffles
-                        h = h || other;
-                    }
-                }
-                if (i < tot_u && g == 0) {
-                    if (CENSUS) c_up += 1, c_uh += h;
-                    if (h) atomicOr(&sres[wi][1][t], 1u << k);
-                }
-            }
-            __syncwarp();
-            if (base == 0) RGG_STAMP(5)
-            if (dbg && lane == 0 && base == 0) dbg[9] = tot_o, dbg[10] = tot_u;
-            if (CENSUS) continue;
-            // ---- transitions in move order (engine_batch.cpp:114-188)
-            const uint32_t ro = sres[wi][0][lane], ru = sres[wi][1][lane];
-            for (int k = 0; k < m; ++k) {
-                const int before = label;
-                const int2 om = som[wi][k];
-                if ((tm >> k) & 1u) {
-                    const int o = om.x;
-                    const int wo = o >> 6;
-                    const unsigned long long bit = 1ull << (o & 63);
-                    unsigned long long ow, uw;
-                    if (WIDE) {
-                        ow = s.over[static_cast<size_t>(wo) * s.Np + c];
-                        uw = s.under[static_cast<size_t>(wo) * s.Np + c];
-                    } else {
-                        ow = OW;
-                        uw = UW;
-                    }
-                    const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
-                    const bool n_over = (ro >> k) & 1u, n_under = (ru >> k) & 1u;
-                    if (old_over) {  // revalidate_old_intersections (engine_batch.cpp:114-143)
-                        oc -= 1;
-                        const int rest = bc - (old_under ? 1 : 0);
-                        label = oc == 0 ? 0 : ((s.use_under && rest > 0) ? 1 : 2);
-                    }
-                    if (n_over) {  // over phase (engine_batch.cpp:163-177)
-                        if (label == 0) label = 2;
-                        oc += 1;
-                    }
-                    if (n_under) label = 1;  // under phase (engine_batch.cpp:181-188)
-                    bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
-                    const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
-                    const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
-                    if (WIDE) {
-                        if (nw != ow) s.over[static_cast<size_t>(wo) * s.Np + c] = nw;
-                        if (nuw != uw) s.under[static_cast<size_t>(wo) * s.Np + c] = nuw;
-                    } else {
-                        OW = nw;
-                        UW = nuw;
-                    }
-                    if (HITS && om.y == b.n - 1) hit_last = n_over;
-                }
-                if (PER_MOVE) {
-                    const bool ch = label != before;
-                    const unsigned gg = __ballot_sync(0xffffffffu, ch && label == 0);
-                    const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
-                    const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
-                    const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
-                    if (lane == 0 && (gg | r | y | f) && !(s.dbg_flags & 4)) {  // 4: ablation, no counters
-                        int* mv = b.mv + 4 * om.y;
-                        if (gg) atomicAdd(mv + 0, __popc(gg));
-                        if (r) atomicAdd(mv + 1, __popc(r));
-                        if (y) atomicAdd(mv + 2, __popc(y));
-                        if (f) atomicAdd(mv + 3, __popc(f));
-                    }
-                }
-            }
-        }
-        if (dbg && !CENSUS) RGG_STAMP(6)
-        if (CENSUS) {
-            if (valid) {
-                c_dirty += 1;
-                c_box += any_box;
-                c_sph += any_sph;
-                if (any_sph) c_segs += seg_hi - seg_lo;
-            }
-            continue;
-        }
-        if (valid) {
-            if (label != label0) {
-                s.state[id] = static_cast<uint8_t>(label);
-                s.state_c[c] = static_cast<uint8_t>(label);
-                dgray += (label == 2) - (label0 == 2);
-            }
-            const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
-            if (cw != cnt0) s.cnt[c] = cw;
-            if (!WIDE) {
-                if (OW != OW0) s.over[c] = OW;
-                if (UW != UW0) s.under[c] = UW;
-            }
-        }
-        if (HITS) {
-            const bool h = valid && hit_last && label == 2;
-            const unsigned bal = __ballot_sync(0xffffffffu, h);
-            int pos = 0;
-            if (lane == 0 && bal) pos = atomicAdd(&b.ctr[5], __popc(bal));
-            pos = __shfl_sync(0xffffffffu, pos, 0);
-            if (h) {
-                const int at = pos + __popc(bal & ((1u << lane) - 1u));
-                b.hits[at] = id;
-                b.hits_prev[at] = static_cast<uint8_t>(label0);
-            }
-        }
-        if (dbg) {
-            __syncwarp();
-            if (lane == 0) dbg[7] = gtimer(), dbg[11] = static_cast<unsigned long long>(clock64() - clk0);
-        }
+    for (int i = gt; i < n_over; i += nthreads) {
+        const int4 it = b.items_over[i];  // component, event, result word, bit
+        const bool h = over_test<true>(s, it.x, b.ev[it.y], &c_sat);
+        c_op += s.B, c_oh += h;
     }
-    if (CENSUS) {
-        long long v[11] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh, 0, 0, 0, 0, 0};
-        v[6] = static_cast<long long>(c_dirty);
-        v[7] = static_cast<long long>(c_box);
-        v[8] = static_cast<long long>(c_sph);
-        v[9] = static_cast<long long>(c_segs);
-        v[10] = static_cast<long long>(c_touch);
+    for (int i = gt; i < n_under; i += nthreads) {
+        const int4 it = b.items_under[i];
+        const bool h = under_range<true>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, &c_tests);
+        c_up += 1, c_uh += h;
+    }
+    long long v[6] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh};
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            long long x = v[k];
-            for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-            if (lane == 0 && x) atomicAdd(&b.census[k < 6 ? k : k + 2], static_cast<unsigned long long>(x));
-        }
-    } else {
-        // running gray count (the unknown_count of the reference)
-        for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
-        if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
+    for (int k = 0; k < 6; ++k) {
+        long long x = v[k];
+        for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+        if (lane == 0 && x) atomicAdd(&b.census[k], static_cast<unsigned long long>(x));
     }
 }
 
-// ------------------------------------------------- v6: warp-slice touch / GPU-wide narrow / warp-slice apply
+// ------------------------------------------------- warp-slice touch / GPU-wide narrow / warp-slice apply
+constexpr int kWarpsPerCta = 4;   // warps per CTA of the slice kernels (touch, apply)
+constexpr int kStageIds = 1024;  // apply stages the moved obstacle ids of batches up to this size
 //
-// v4 split at its narrow phase.  A warp owns a 32-component slice (as in v4)
-// for the touch masks and for the transitions, but the narrow tests of all
-// slices are drained by one GPU-wide kernel (one (component, event) item per
-// thread, 4 lanes per segment-sphere item), so a slice next to an obstacle no
-// longer serialises its SAT / segment rounds on one warp.  Masks live in the
-// per-cell mask blocks the bin kernel reserves (word (kind*W + w)*cell + t).
+// A warp owns a 32-component slice for the touch masks and for the transitions;
+// the narrow tests of all slices are drained by one GPU-wide kernel (one
+// (component, event) item per thread), so a slice next to an obstacle does not
+// serialise its SAT / segment rounds on one warp.  Masks live in the per-cell
+// mask blocks the bin kernel reserves (word (kind*W + w)*cell + t).
 
 template <bool CENSUS>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, Batch b) {
@@ -1614,43 +1014,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     }
     const unsigned long long t0 = CENSUS ? 0 : tl_start(b.tl);
     if (!CENSUS) tl_stop(b.tl, 6, tw);
-    // event operands: for small batches (n <= kStageEv) the whole batch is staged
-    // once per CTA and the slices index it through their cell lists; otherwise
-    // each warp stages its current chunk of 32 listed events
+    // each warp stages its current chunk of 32 listed events; the batch's operands
+    // are prefetched into this SM's L1 first (read per chunk below)
     __shared__ double sbx[kWarpsPerCta * 32][24];
     __shared__ int sev[kWarpsPerCta][32];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
-    const bool staged = b.n <= kStageEv && (s.dbg_flags & 64);  // 64: stage the batch in shared memory
-    if (!staged) {  // the batch's operands into this SM's L1 (read per chunk below)
+    {
         const char* p = reinterpret_cast<const char*>(b.evt);
         const int lines = (b.n * 24 * 8 + 127) >> 7;
         for (int l = threadIdx.x; l < min(lines, 256); l += blockDim.x) prefetch_l1(p + (static_cast<size_t>(l) << 7));
     }
-    if (staged) {  // all loads in flight at once, then the stores
-        constexpr int kPer = kStageEv * 12 / (32 * kWarpsPerCta);
-        const double2* src = reinterpret_cast<const double2*>(b.evt);
-        double2* dst = reinterpret_cast<double2*>(&sbx[0][0]);
-        const int nv = b.n * 12;
-        double2 v[kPer];
-#pragma unroll
-        for (int r = 0; r < kPer; ++r) {
-            const int t = threadIdx.x + r * 32 * kWarpsPerCta;
-            if (t < nv) v[r] = src[t];
-        }
-#pragma unroll
-        for (int r = 0; r < kPer; ++r) {
-            const int t = threadIdx.x + r * 32 * kWarpsPerCta;
-            if (t < nv) dst[t] = v[r];
-        }
-        __syncthreads();
-    }
-    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0;
-    unsigned long long* dbgw = (!CENSUS && b.dbg) ? b.dbg + 8 * static_cast<size_t>(nslices) +
-                                                        4 * static_cast<size_t>((blockIdx.x * blockDim.x + threadIdx.x) >> 5)
-                                                  : nullptr;
-    if (dbgw && lane == 0) dbgw[0] = gtimer();
-    int dbg_slices = 0;
+    unsigned long long c_dirty = 0, c_box = 0, c_sph = 0, c_segs = 0, c_touch = 0, c_segs_all = 0;
     // Work units: (slice, chunk of <= 32 listed events) from the bin kernel's unit
     // list, so a cell with many events spreads over several warps.  The census
     // walks every slice with all its chunks.
@@ -1728,7 +1103,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             const int m = min(32, count - base);
             const int myev = lane < m ? list[base + lane] : 0;
             sev[wi][lane] = myev;
-            if (!staged && lane < m) {
+            if (lane < m) {
                 const double2* src = reinterpret_cast<const double2*>(b.evt + 24 * static_cast<size_t>(myev));
 #pragma unroll
                 for (int j = 0; j < 12; ++j) {
@@ -1741,7 +1116,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             uint32_t tm = 0, bm = 0, sm = 0;
             if (valid) {
                 for (int k = 0; k < m; ++k) {
-                    const double* bx = sbx[staged ? sev[wi][k] : 32 * wi + k];
+                    const double* bx = sbx[32 * wi + k];
                     const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
                     tm |= static_cast<uint32_t>(touch) << k;
                     bm |= static_cast<uint32_t>(touch & rggd::overlaps(aabb, bx + 12)) << k;
@@ -1807,19 +1182,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             c_box += any_box;
             c_sph += any_sph;
             if (any_sph) c_segs += seg_hi - seg_lo;
+            c_segs_all += seg_hi - seg_lo;
         }
-        ++dbg_slices;
-    }
-    if (dbgw) {
-        __syncwarp();
-        if (lane == 0) dbgw[1] = gtimer(), dbgw[2] = dbg_slices, dbgw[3] = 0;
     }
     if (!CENSUS) tl_stop(b.tl, 2, t0);
     if (flow) pdl_wait();  // the grid ends after bin's (narrow waits on this grid only)
     if (CENSUS) {
-        unsigned long long v[5] = {c_dirty, c_box, c_sph, c_segs, c_touch};
+        unsigned long long v[6] = {c_dirty, c_box, c_sph, c_segs, c_touch, c_segs_all};
 #pragma unroll
-        for (int k = 0; k < 5; ++k) {
+        for (int k = 0; k < 6; ++k) {
             unsigned long long x = v[k];
             for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
             if (lane == 0 && x) atomicAdd(&b.census[8 + k], x);
@@ -1827,6 +1198,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     }
 }
 
+// Per-move transitions (engine_batch.cpp:114-188) of every component of a dirty
+// slice, in list (= move) order, from the touch / over / under words.  WIDE (M > 64 obstacles, ceil(M/64) bit words per
+// component): the old over / under bits of every event touching a lane are loaded
+// up front, four at a time, before the walk, and changed bits are written back with
+// fire-and-forget atomics, so the walk has no memory round trip per event.  A batch
+// that moves an obstacle twice keeps the sequential read-modify-write (the second
+// move's old bits are the first one's new bits).
 template <int FLAGS, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, Batch b) {
     const unsigned long long tw = tl_start(b.tl);
@@ -1842,35 +1220,41 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     const int nslices = (s.Np + 31) >> 5;
     const bool staged = b.n <= kStageIds;
     if (b.evready && blockIdx.x == 0 && threadIdx.x < 4) b.evready[threadIdx.x] = 0;  // for the next update
-    if (staged) {
-        for (int t = threadIdx.x; t < b.n; t += blockDim.x) s_ids[t] = b.ids[t];
-        __syncthreads();
+    int rep = 0;  // some obstacle moves twice in this batch (b.last from the pose kernel)
+    for (int t = threadIdx.x; t < b.n; t += blockDim.x) {
+        if (staged) s_ids[t] = b.ids[t];
+        if (WIDE) rep |= b.last[t] == 0;
     }
+    const bool repeats = __syncthreads_or(rep) != 0;
     int dgray = 0;
-    // a full narrow-item queue left some verdicts uncomputed: apply nothing, so the
-    // engine stays at its pre-update state and the host can grow the queue and replay
-    const int full = b.ctr[6];
+    // any failed stage (status ctr[6]: 1 overflow pool, 2 mask pool, 3 full narrow-item
+    // queue, 4 handoff timeout) left some verdicts uncomputed: apply nothing, so the
+    // engine stays at its pre-update state (the host grows the queue and replays on 3,
+    // and fails the update otherwise)
+    const int status = b.ctr[6];
     // Work list: when fewer than half the cells are dirty, the dirty slices only, from
     // touch's work units (a cell's first chunk stands for the cell: {cell, 0, count,
     // mask base}); otherwise every slice, with its state loads issued before the cell
-    // record's (one round trip less on the chain).  c4: -14 %; c5 would lose 2.5 %.
-    // RGG_DEBUG_FLAGS 16384 forces the every-slice walk.
-    const bool dirty_only = (s.dbg_flags & 16384) == 0 && 2 * b.ctr[0] < s.ncells;
+    // record's (one round trip less on the chain).
+    const bool dirty_only = 2 * b.ctr[0] < s.ncells;
     const int spc = s.cell >> 5;
-    const int n_work = dirty_only ? min(b.ctr[10], b.units_cap) * spc : nslices;
+    const int n_work = status != 0 ? 0 : (dirty_only ? min(b.ctr[10], b.units_cap) * spc : nslices);
+    // static striding over the work list (a same-address atomic per slice to take work
+    // dynamically serialised at the L2: slower at c5)
     for (int wq = blockIdx.x * kWarpsPerCta + wi; wq < n_work; wq += gridDim.x * kWarpsPerCta) {
         int q = wq;
         int4 un = make_int4(0, 0, 0, 0);
+        bool skip = false;
         if (dirty_only) {
             un = b.units[wq / spc];
-            if (un.y != 0) continue;  // warp-uniform: a later chunk of a listed cell
+            skip = un.y != 0;  // warp-uniform: a later chunk of a listed cell
             q = un.x * spc + wq % spc;
         }
         const int c0 = q << 5;
-        if (c0 >= s.Np) continue;
+        skip |= c0 >= s.Np;
         const int cell = c0 / s.cell;
         const int c = c0 + lane, t = c - cell * s.cell;
-        const bool valid = c < s.Np;
+        const bool valid = !skip && c < s.Np;
         // the slice's state (coalesced, cell order) is loaded together with the
         // cell record, so one memory round trip serves both
         int label = 0, oc = 0, bc = 0, id = -1;
@@ -1885,21 +1269,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
             }
             label = s.state_c[c];
         }
-        int4 rec;
-        if (dirty_only) {
-            const int32_t* lst = un.z <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap : b.pool + b.cell_ovf[cell];
-            const unsigned long long la = reinterpret_cast<unsigned long long>(lst);
-            rec = make_int4(un.z, un.w, static_cast<int>(la & 0xffffffffu), static_cast<int>(la >> 32));
-        } else {
-            rec = b.crec[cell];
+        int4 rec = make_int4(0, 0, 0, 0);
+        if (!skip) {
+            if (dirty_only) {
+                const int32_t* lst =
+                    un.z <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap : b.pool + b.cell_ovf[cell];
+                const unsigned long long la = reinterpret_cast<unsigned long long>(lst);
+                rec = make_int4(un.z, un.w, static_cast<int>(la & 0xffffffffu), static_cast<int>(la >> 32));
+            } else {
+                rec = b.crec[cell];
+            }
         }
         const int count = rec.x;
-        if (full == 3) break;  // warp-uniform
-        if (count == 0) continue;
         oc = cw & 0xffff;
         bc = cw >> 16;
         const int label0 = label;
-        const uint32_t cnt0 = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+        const uint32_t cnt0 = cw;
         const unsigned long long OW0 = OW, UW0 = UW;
         bool hit_last = false;
         const int32_t* list = rec_list(rec);
@@ -1917,6 +1302,33 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                 ru = b.mpool[rec.y + (2 * W + w) * s.cell + t];
             }
             __syncwarp();
+            // WIDE: the old bits of this lane's touching events, all loads in flight together
+            uint32_t oldO = 0, oldU = 0;
+            if (WIDE && !repeats) {
+                for (uint32_t x = tm; x;) {
+                    int k[4];
+                    unsigned long long wo[4], wu[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        k[j] = x ? __ffs(x) - 1 : -1;
+                        x &= x - 1;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (k[j] >= 0) {
+                            const size_t idx = static_cast<size_t>(som[wi][k[j]].x >> 6) * s.Np + c;
+                            wo[j] = s.over[idx];
+                            wu[j] = s.under[idx];
+                        }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (k[j] >= 0) {
+                            const int ob = som[wi][k[j]].x & 63;
+                            oldO |= static_cast<uint32_t>((wo[j] >> ob) & 1ull) << k[j];
+                            oldU |= static_cast<uint32_t>((wu[j] >> ob) & 1ull) << k[j];
+                        }
+                }
+            }
             // only the events that touch some component of the slice can change a
             // label or a counter: walk those, in list (= move) order
             for (uint32_t em = __reduce_or_sync(0xffffffffu, tm); em; em &= em - 1) {
@@ -1925,17 +1337,22 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                 const int2 om = som[wi][k];
                 if ((tm >> k) & 1u) {
                     const int o = om.x;
-                    const int wo = o >> 6;
+                    const size_t widx = static_cast<size_t>(o >> 6) * s.Np + c;
                     const unsigned long long bit = 1ull << (o & 63);
-                    unsigned long long ow, uw;
-                    if (WIDE) {
-                        ow = s.over[static_cast<size_t>(wo) * s.Np + c];
-                        uw = s.under[static_cast<size_t>(wo) * s.Np + c];
+                    bool old_over, old_under;
+                    unsigned long long ow = 0, uw = 0;
+                    if (!WIDE) {
+                        old_over = (OW & bit) != 0;
+                        old_under = (UW & bit) != 0;
+                    } else if (!repeats) {
+                        old_over = (oldO >> k) & 1u;
+                        old_under = (oldU >> k) & 1u;
                     } else {
-                        ow = OW;
-                        uw = UW;
+                        ow = s.over[widx];
+                        uw = s.under[widx];
+                        old_over = (ow & bit) != 0;
+                        old_under = (uw & bit) != 0;
                     }
-                    const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
                     const bool n_over = (ro >> k) & 1u, n_under = (ru >> k) & 1u;
                     if (old_over) {  // revalidate_old_intersections (engine_batch.cpp:114-143)
                         oc -= 1;
@@ -1948,14 +1365,19 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                     }
                     if (n_under) label = 1;  // under phase (engine_batch.cpp:181-188)
                     bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
-                    const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
-                    const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
-                    if (WIDE) {
-                        if (nw != ow) s.over[static_cast<size_t>(wo) * s.Np + c] = nw;
-                        if (nuw != uw) s.under[static_cast<size_t>(wo) * s.Np + c] = nuw;
+                    if (!WIDE) {
+                        OW = n_over ? (OW | bit) : (OW & ~bit);
+                        UW = n_under ? (UW | bit) : (UW & ~bit);
+                    } else if (!repeats) {  // each lane owns its component's words: only this bit changes
+                        if (n_over != old_over)
+                            n_over ? atomicOr(&s.over[widx], bit) : atomicAnd(&s.over[widx], ~bit);
+                        if (n_under != old_under)
+                            n_under ? atomicOr(&s.under[widx], bit) : atomicAnd(&s.under[widx], ~bit);
                     } else {
-                        OW = nw;
-                        UW = nuw;
+                        const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
+                        const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
+                        if (nw != ow) s.over[widx] = nw;
+                        if (nuw != uw) s.under[widx] = nuw;
                     }
                     if (HITS && om.y == b.n - 1) hit_last = n_over;
                 }
@@ -1965,7 +1387,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
                     const unsigned r = __ballot_sync(0xffffffffu, ch && label == 1);
                     const unsigned y = __ballot_sync(0xffffffffu, ch && label == 2);
                     const unsigned f = __ballot_sync(0xffffffffu, ch && before == 2);
-                    if (lane == 0 && (gg | r | y | f) && !(s.dbg_flags & 4)) {  // 4: ablation, no counters
+                    if (lane == 0 && (gg | r | y | f)) {
                         int* mv = b.mv + 4 * om.y;
                         if (gg) atomicAdd(mv + 0, __popc(gg));
                         if (r) atomicAdd(mv + 1, __popc(r));
@@ -1976,20 +1398,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
             }
             __syncwarp();
         }
-        if (valid) {
+        if (valid && count > 0) {
             if (label != label0) {
                 s.state[id] = static_cast<uint8_t>(label);
                 s.state_c[c] = static_cast<uint8_t>(label);
                 dgray += (label == 2) - (label0 == 2);
             }
-            const uint32_t cw = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
-            if (cw != cnt0) s.cnt[c] = cw;
+            const uint32_t cwn = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+            if (cwn != cnt0) s.cnt[c] = cwn;
             if (!WIDE) {
                 if (OW != OW0) s.over[c] = OW;
                 if (UW != UW0) s.under[c] = UW;
             }
         }
-        if (HITS) {
+        if (HITS && count > 0) {
             const bool h = valid && hit_last && label == 2;
             const unsigned bal = __ballot_sync(0xffffffffu, h);
             int pos = 0;
@@ -2004,7 +1426,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     }
     for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
     if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
-    if (full != 3 && !(s.dbg_flags & 8)) commit_grid(s, b);  // 8: ablation, no commit
+    if (status == 0) commit_grid(s, b);
     tl_stop(b.tl, 4, t0);
 }
 
@@ -2159,6 +1581,22 @@ __global__ void fp64_peak_kernel(double* sink, int iters) {
     if (t == 12345.0) sink[0] = t;
 }
 
+// FP32 FMA issue-rate probe: 16 independent FFMA chains per thread.
+__global__ void fp32_peak_kernel(float* sink, int iters) {
+    float x[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = 1.0f + 1e-6f * (threadIdx.x + k);
+    const float a = 0.9999999f, c = 1e-7f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) x[k] = fmaf(x[k], a, c);
+    }
+    float t = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t += x[k];
+    if (t == 12345.0f) sink[0] = t;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -2216,49 +1654,15 @@ cudaError_t launch_init_obstacles(const Store& s, Event*, cudaStream_t st) {
 
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
     if (s.ncells == 0) return cudaSuccess;  // no components: nothing to bin
-    const int cells_per = kBinThreads / 32;  // = kSuperCells
     static const bool no_small = std::getenv("RGG_NO_SMALL_BIN") != nullptr;
     if (b.n <= kBinSmallMax && !no_small)
         return launch_pdl(bin_small_kernel, dim3((s.ncells + kBinSmallWarps - 1) / kBinSmallWarps),
                           dim3(32 * kBinSmallWarps), st, s, b);
-    return launch_pdl(bin_kernel, dim3((s.ncells + cells_per - 1) / cells_per), dim3(kBinThreads), st, s, b);
+    cudaError_t e = launch_pdl(bin_scatter_kernel, dim3(b.n), dim3(kScatterThreads), st, s, b);  // a CTA per event
+    if (e != cudaSuccess) return e;
+    return launch_pdl(bin_cells_kernel, dim3((s.ncells + kCellWarps - 1) / kCellWarps), dim3(32 * kCellWarps), st, s, b);
 }
 
-template <int F, bool W>
-static cudaError_t apply_t(const Store& s, const Batch& b, cudaStream_t st) {
-    apply_kernel<F, W><<<s.ncells, s.cell, 0, st>>>(s, b);
-    return cudaGetLastError();
-}
-
-static int grid_warp(const Store& s) {
-    static int per_sm = 0, sms = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, classify_warp_kernel<kPerMove, false>, 32 * kWarpsPerCta, 0);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        per_sm = per_sm < 1 ? 1 : per_sm;
-    }
-    const int slices = (s.Np + 31) / 32;
-    const int need = (slices + kWarpsPerCta - 1) / kWarpsPerCta;
-    return need < per_sm * sms ? (need < 1 ? 1 : need) : per_sm * sms;
-}
-
-template <int F, bool W>
-static cudaError_t warp_t(const Store& s, const Batch& b, int grid, cudaStream_t st) {
-    classify_warp_kernel<F, W><<<grid, 32 * kWarpsPerCta, 0, st>>>(s, b);
-    return cudaGetLastError();
-}
-
-static int pipeline() {
-    static const int p = [] {
-        const char* e = std::getenv("RGG_PIPELINE");
-        return e ? std::atoi(e) : 6;
-    }();
-    return p;
-}
-
-bool split_pipeline() { return pipeline() == 6; }
 
 cudaError_t launch_host_out(const Batch& b, cudaStream_t st) {
     return launch_pdl(host_out_kernel, dim3(1), dim3(256), st, b);
@@ -2288,40 +1692,33 @@ static cudaError_t apply6_t(const Store& s, const Batch& b, int grid, cudaStream
     return launch_pdl(apply_warp_kernel<F, W>, dim3(grid), dim3(32 * kWarpsPerCta), st, s, b);
 }
 
+// persistent slice kernels: one wave (resident CTAs x SMs), fewer CTAs when the
+// store has fewer slices
 static int grid_slices(const Store& s, const void* fn) {
-    int per_sm = 0, sms = 0, dev = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarpsPerCta, 0);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    per_sm = per_sm < 1 ? 1 : per_sm;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    static const void* fns[16];
+    static int occ[16], nfn = 0;
+    int per_sm = 0;
+    for (int i = 0; i < nfn; ++i)
+        if (fns[i] == fn) per_sm = occ[i];
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kWarpsPerCta, 0);
+        per_sm = per_sm < 1 ? 1 : per_sm;
+        if (nfn < 16) fns[nfn] = fn, occ[nfn++] = per_sm;
+    }
     const int need = ((s.Np + 31) / 32 + kWarpsPerCta - 1) / kWarpsPerCta;
     return need < per_sm * sms ? (need < 1 ? 1 : need) : per_sm * sms;
 }
 
-// lanes per under item (RGG_UNDER_LANES = 1, 2 or 4)
-static int under_lanes() {
-    static const int g = [] {
-        const char* e = std::getenv("RGG_UNDER_LANES");
-        const int v = e ? std::atoi(e) : 1;
-        return v == 2 || v == 4 ? v : 1;
-    }();
-    return g;
-}
-
-static cudaError_t launch_narrow(const Store& s, const Batch& b, int grid, cudaStream_t st, bool pdl) {
-    static const int forced = std::getenv("RGG_NARROW_CTAS") ? std::atoi(std::getenv("RGG_NARROW_CTAS")) : 0;
-    if (forced > 0) grid = forced;
-    switch (under_lanes()) {
-        case 2:
-            return pdl ? launch_pdl(narrow_kernel<false, 2>, dim3(grid), dim3(128), st, s, b)
-                       : (narrow_kernel<false, 2><<<grid, 128, 0, st>>>(s, b), cudaGetLastError());
-        case 4:
-            return pdl ? launch_pdl(narrow_kernel<false, 4>, dim3(grid), dim3(128), st, s, b)
-                       : (narrow_kernel<false, 4><<<grid, 128, 0, st>>>(s, b), cudaGetLastError());
-        default:
-            return pdl ? launch_pdl(narrow_kernel<false, 1>, dim3(grid), dim3(128), st, s, b)
-                       : (narrow_kernel<false, 1><<<grid, 128, 0, st>>>(s, b), cudaGetLastError());
-    }
+template <int F, bool W>
+static cudaError_t apply_t(const Store& s, const Batch& b, cudaStream_t st) {
+    return launch_pdl(apply_warp_kernel<F, W>, dim3(grid_slices(s, reinterpret_cast<const void*>(apply_warp_kernel<F, W>))),
+                      dim3(32 * kWarpsPerCta), st, s, b);
 }
 
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st) {
@@ -2330,57 +1727,17 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
         commit_kernel<<<(b.n + 7) / 8, 128, 0, st>>>(s, b);
         return cudaGetLastError();
     }
-    if (pipeline() == 6) {
-        static int g_touch = 0, g_touch_c = 0, g_apply = 0;
-        if (!g_touch) {
-            g_touch = grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>));
-            g_touch_c = grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<true>));
-            g_apply = grid_slices(s, reinterpret_cast<const void*>(apply_warp_kernel<kPerMove, false>));
-        }
-        if (flags & kCensus) {
-            touch_warp_kernel<true><<<g_touch_c, 32 * kWarpsPerCta, 0, st>>>(s, b);
-            narrow_kernel<true, 1><<<grid, 128, 0, st>>>(s, b);
-            return cudaGetLastError();
-        }
-        cudaError_t e = launch_pdl(touch_warp_kernel<false>, dim3(g_touch), dim3(32 * kWarpsPerCta), st, s, b);
-        if (e == cudaSuccess) e = launch_narrow(s, b, grid, st, true);
-        if (e == cudaSuccess && (s.dbg_flags & 16)) e = launch_narrow(s, b, grid, st, true);  // 16: run twice (warm)
-        if (e != cudaSuccess) return e;
-        const bool wide = s.W > 1;
-        const int ga = g_apply;
-        switch (flags & (kPerMove | kHits)) {
-            case 0:
-                return wide ? apply6_t<0, true>(s, b, ga, st) : apply6_t<0, false>(s, b, ga, st);
-            case kPerMove:
-                return wide ? apply6_t<kPerMove, true>(s, b, ga, st) : apply6_t<kPerMove, false>(s, b, ga, st);
-            case kHits:
-                return wide ? apply6_t<kHits, true>(s, b, ga, st) : apply6_t<kHits, false>(s, b, ga, st);
-            default:
-                return wide ? apply6_t<kPerMove | kHits, true>(s, b, ga, st)
-                            : apply6_t<kPerMove | kHits, false>(s, b, ga, st);
-        }
-    }
-    if (pipeline() == 4) {
-        const int g = grid_warp(s);
-        const bool wide = s.W > 1;
-        if (flags & kCensus) return wide ? warp_t<kCensus, true>(s, b, g, st) : warp_t<kCensus, false>(s, b, g, st);
-        switch (flags & (kPerMove | kHits)) {
-            case 0:
-                return wide ? warp_t<0, true>(s, b, g, st) : warp_t<0, false>(s, b, g, st);
-            case kPerMove:
-                return wide ? warp_t<kPerMove, true>(s, b, g, st) : warp_t<kPerMove, false>(s, b, g, st);
-            case kHits:
-                return wide ? warp_t<kHits, true>(s, b, g, st) : warp_t<kHits, false>(s, b, g, st);
-            default:
-                return wide ? warp_t<kPerMove | kHits, true>(s, b, g, st) : warp_t<kPerMove | kHits, false>(s, b, g, st);
-        }
-    }
     if (flags & kCensus) {
-        narrow_kernel<true, 1><<<grid, 128, 0, st>>>(s, b);
+        touch_warp_kernel<true><<<grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<true>)),
+                                  32 * kWarpsPerCta, 0, st>>>(s, b);
+        narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
         return cudaGetLastError();
     }
-    touch_kernel<<<s.ncells, s.cell, 0, st>>>(s, b);
-    launch_narrow(s, b, grid, st, false);
+    cudaError_t e = launch_pdl(touch_warp_kernel<false>,
+                               dim3(grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>))),
+                               dim3(32 * kWarpsPerCta), st, s, b);
+    if (e == cudaSuccess) e = launch_pdl(narrow_kernel<false>, dim3(grid), dim3(128), st, s, b);
+    if (e != cudaSuccess) return e;
     const bool wide = s.W > 1;
     switch (flags & (kPerMove | kHits)) {
         case 0:
@@ -2404,7 +1761,7 @@ void filter_stats(unsigned long long* out, bool reset) {
 
 int classify_occupancy(int, int) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_kernel<false, 1>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_kernel<false>, 128, 0);
     return n < 1 ? 1 : n;
 }
 
@@ -2428,6 +1785,11 @@ cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, con
                               uint8_t* mask, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     pair_masks_kernel<<<(n + 127) / 128, 128, 0, st>>>(s, rank, kind, cand, n, o, mask);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fp32_peak(float* sink, int iters, int grid, int block, cudaStream_t st) {
+    fp32_peak_kernel<<<grid, block, 0, st>>>(sink, iters);
     return cudaGetLastError();
 }
 

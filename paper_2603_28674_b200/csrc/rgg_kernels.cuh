@@ -10,9 +10,9 @@
 namespace rggk {
 
 constexpr int kMaxSpheres = 16;  // obstacle inner spheres per event (C)
+constexpr int kEvS = kMaxSpheres + 1;  // float4 records per event in Batch::evs
 constexpr int kEvChunk = 32;     // events staged in shared memory per pass (one bit each)
 constexpr int kMaxCell = 128;
-constexpr int kSuperCells = 16;  // cells per binning super-cell (= warps per bin CTA)    // components per cell = threads per classify CTA
 
 // One obstacle move after re-posing (BatchLayout::update_transforms,
 // proj/src/batch_layout.cpp:148-172), plus the obstacle's previous union box.
@@ -40,7 +40,6 @@ struct Store {
     int32_t B, S, M, C, W;
     int32_t cell, ncells, cap;
     int32_t use_under;
-    int32_t dbg_flags;         // ablation switches (RGG_DEBUG_FLAGS): 1 = skip narrow tests, 2 = skip operand loads
     int32_t prefetch;          // touch stages the narrow operands in L2 (they fit in half of it)
     const double2* aabb;       // 3 planes of Np double2: (minx,miny) (minz,maxx) (maxy,maxz)
     const double* sat;         // Np*B*22 (21 + pad)
@@ -51,7 +50,12 @@ struct Store {
     const double* spline_r;    // B*S
     const int32_t* orig;       // Np: sorted -> component id
     const double* cell_aabb;   // ncells*6
-    const double* super_aabb;  // ceil(ncells/16)*6: union box of 16 consecutive cells (binning filter)
+    // uniform grid over the cells (binning): bin (x, y, z) = floor((p - gorg) * ginv) clamped
+    // to [0, gdim); the cells whose box overlaps bin g are gcell[gcell_off[g] .. gcell_off[g+1])
+    double gorg[3], ginv[3];
+    int32_t gdim[3];
+    const int32_t* gcell_off;
+    const int2* gcell;       // {cell, the cell's lowest bin per axis: x | y << 10 | z << 20} (the scatter's dedup)
     const double* ohe;         // M*3
     const double* osl;         // M*C*3
     const double* osr;         // M
@@ -75,6 +79,8 @@ struct Batch {
     Event* ev;             // n
     double* evbox;         // n*12: new and old union box of each event (compact, for the binning)
     double* evt;           // n*24: new union, old union, box, sphere box (the touch kernel's operands)
+    float4* evs;           // n*kEvS: the narrow kernel's sphere operands (pose kernel): [0] = {fl(o_minus_r),
+                           // sphere count (int bits), 0, 0}, [1 + k] = {fl(centre k), |fl(centre k)|_1}
     int32_t* cell_count;   // ncells
     int32_t* cell_list;    // ncells*cap
     int32_t* cell_ovf;     // ncells: base in pool when count > cap
@@ -82,7 +88,6 @@ struct Batch {
     int32_t pool_cap;
     int32_t* ctr;          // [0] dirty count, [1] pool top, [2] work counter, [3] overflow cells,
                            // [4] gray count, [5] hits count, [6] error flag, [8] over items, [9] under items
-    int32_t* dirty;        // ncells
     int32_t* mv;           // n*4: to_green, to_red, to_gray, from_gray
     int32_t* hits;         // N: over-hit-by-last-move & still gray
     uint8_t* hits_prev;    // N: their labels before the move (eager report counts)
@@ -98,7 +103,6 @@ struct Batch {
     int32_t items_cap;
     int32_t census_on;           // touch accumulates the byte census
     int32_t* unknown;      // running GRAY count, persistent across batches
-    unsigned long long* dbg;     // optional per-cell timestamps (RGG_DEBUG_TIMING), else null
     unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null
     // host-mapped outputs (synchronous host updates): launch_host_out stores the
     // per-move counters (n*4) and ctr[0..23] there after the apply kernel
@@ -118,6 +122,11 @@ struct Batch {
     // once unit u and its cell list are stored.  Null: touch waits for the whole bin kernel.
     int32_t* unit_ready;
     int32_t bin_warps;
+    // event bitmask per cell (bin_scatter_kernel -> bin_cells_kernel): cmask[cell * cmask_words + e / 32]
+    // bit e % 32 = event e's new or old union box overlaps the cell's box; the cell pass
+    // clears the words it reads, so they are zero between updates
+    uint32_t* cmask;
+    int32_t cmask_words;
 };
 
 // Exact resolve operands (rgg_resolve.cu).
@@ -140,7 +149,6 @@ struct Resolver {
     const uint8_t* sact;     // M: 1 = scene-active at spose (null: none)
 };
 
-bool split_pipeline();  // RGG_PIPELINE == 6 (the default): touch / narrow / apply
 cudaError_t launch_host_out(const Batch& b, cudaStream_t st);  // counters -> b.out_mv / b.out_ctr
 // eager batches: save move i-1's report terms to rep[8(i-1)..], stage move i into slot 0
 cudaError_t launch_eager_step(const Batch& b, int32_t* ids0, double* rt0, const int32_t* st_ids, const double* st_rt,
@@ -167,10 +175,19 @@ struct StoreOut {
     int32_t* orig;         // np
     int32_t* rank;         // N
     double* cell_aabb;     // ncells*6
-    double* super_aabb;    // nsuper*6
     int32_t total_segs;
 };
 cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st);
+
+// The binning's uniform grid over the cell boxes (Store::gorg / ginv / gdim / gcell_off / gcell).
+struct CellGrid {
+    double org[3], inv[3];
+    int32_t dim[3];
+    int32_t* off = nullptr;    // device, bins + 1
+    int2* cells = nullptr;     // device: {cell, low bin packed}
+    int64_t entries = 0;
+};
+cudaError_t build_cell_grid(const double* d_cell_aabb, int ncells, CellGrid& g, cudaStream_t st);
 
 enum ResolveMode : int { kResolve = 0, kEager = 1, kCheck = 2 };
 // exact check of ids[0..*count_dev) (max_count bounds the grid), after
@@ -189,6 +206,7 @@ cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, con
                               uint8_t* mask, cudaStream_t st);
 cudaError_t launch_init_obstacles(const Store& s, Event* scratch, cudaStream_t st);
 cudaError_t launch_fp64_peak(double* sink, int iters, int grid, int block, cudaStream_t st);
+cudaError_t launch_fp32_peak(float* sink, int iters, int grid, int block, cudaStream_t st);
 int classify_occupancy(int cell, int flags);
 void filter_stats(unsigned long long* out, bool reset);
 

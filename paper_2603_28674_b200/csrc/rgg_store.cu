@@ -9,7 +9,12 @@
 //   2. stable radix sort of (key, id) (CUB), shard selection of interleaved cells;
 //   3. gathers: AABB planes, SatBoxes (22-double records), Box32 filter operands,
 //      per-row segment counts -> exclusive scan -> CSR rows, segment records
-//      (+ the row's spline radius), id -> rank map, cell and super-cell boxes.
+//      (+ the row's spline radius), id -> rank map, cell boxes;
+//   4. the uniform grid over the cell boxes that the binning queries (build_cell_grid).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -161,17 +166,6 @@ __global__ void cell_box_kernel(const double2* aabb, int np, int cell, int ncell
     for (int k = 0; k < 6; ++k) cell_aabb[6 * static_cast<size_t>(g) + k] = box[k];
 }
 
-__global__ void super_box_kernel(const double* cell_aabb, int ncells, int nsuper, double* super_aabb) {
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= nsuper) return;
-    double box[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
-    for (int c = g * kSuperCells; c < min(ncells, (g + 1) * kSuperCells); ++c)
-        for (int k = 0; k < 3; ++k) {
-            box[k] = fmin(box[k], cell_aabb[6 * static_cast<size_t>(c) + k]);
-            box[3 + k] = fmax(box[3 + k], cell_aabb[6 * static_cast<size_t>(c) + 3 + k]);
-        }
-    for (int k = 0; k < 6; ++k) super_aabb[6 * static_cast<size_t>(g) + k] = box[k];
-}
 
 // scratch allocations released on every exit of build_store
 struct Scratch {
@@ -200,7 +194,7 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     Scratch scratch;
     const int N = in.N, B = in.B, BS = in.B * in.S, np = in.np, cell = in.cell;
     const long long nrows = static_cast<long long>(np) * BS;
-    const int ncells = (np + cell - 1) / cell, nsuper = (ncells + kSuperCells - 1) / kSuperCells;
+    const int ncells = (np + cell - 1) / cell;
     // 1. raw inputs
     double *aabb = nullptr, *sat21 = nullptr, *segs7 = nullptr;
     int32_t* row_off = nullptr;
@@ -256,12 +250,90 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     if (nrows > 0)
         segs_kernel<<<static_cast<unsigned>((nrows + T256 - 1) / T256), T256, 0, st>>>(
             out.orig, nrows, BS, row_off, out.row, segs7, out.spline, out.seg, out.seg32);
-    if (ncells > 0) {
-        cell_box_kernel<<<(ncells + 127) / 128, 128, 0, st>>>(out.aabb, np, cell, ncells, out.cell_aabb);
-        super_box_kernel<<<(nsuper + 127) / 128, 128, 0, st>>>(out.cell_aabb, ncells, nsuper, out.super_aabb);
-    }
+    if (ncells > 0) cell_box_kernel<<<(ncells + 127) / 128, 128, 0, st>>>(out.aabb, np, cell, ncells, out.cell_aabb);
     SCK(cudaGetLastError());
     SCK(cudaStreamSynchronize(st));
+    return cudaSuccess;
+}
+
+// A uniform grid over the cell boxes (host side: a few thousand cells).  Bins are
+// about half the median cell extent per axis (one bin along an axis the cells
+// span almost entirely, e.g. z of an SE(2) roadmap), at most 128 per axis and 2^21
+// in all; each cell is listed in every bin its closed box overlaps.  The binning's
+// monotone index map floor((p - org) * inv), clamped, sends every point of a cell
+// box and every point of an event box to bins inside the ranges both register, so
+// two overlapping boxes always share a bin.
+cudaError_t build_cell_grid(const double* d_cell_aabb, int ncells, CellGrid& g, cudaStream_t st) {
+    std::vector<double> box(static_cast<size_t>(ncells) * 6);
+    if (ncells) SCK(cudaMemcpyAsync(box.data(), d_cell_aabb, box.size() * 8, cudaMemcpyDeviceToHost, st));
+    SCK(cudaStreamSynchronize(st));
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    std::vector<double> ext[3];
+    for (int c = 0; c < ncells; ++c)
+        for (int k = 0; k < 3; ++k) {
+            if (!(box[6 * c] <= box[6 * c + 3])) continue;  // empty cell box
+            lo[k] = std::min(lo[k], box[6 * c + k]);
+            hi[k] = std::max(hi[k], box[6 * c + 3 + k]);
+            ext[k].push_back(box[6 * c + 3 + k] - box[6 * c + k]);
+        }
+    long long total = 1;
+    for (int k = 0; k < 3; ++k) {
+        double med = 0.0;
+        if (!ext[k].empty()) {
+            std::nth_element(ext[k].begin(), ext[k].begin() + ext[k].size() / 2, ext[k].end());
+            med = ext[k][ext[k].size() / 2];
+        }
+        const double span = ext[k].empty() ? 0.0 : hi[k] - lo[k];
+        int d = 1;
+        if (span > 0 && med < 0.75 * span)
+            d = static_cast<int>(std::min(128.0, std::max(1.0, std::ceil(span / std::max(0.5 * med, span / 128.0)))));
+        g.dim[k] = d;
+        g.org[k] = ext[k].empty() ? 0.0 : lo[k];
+        g.inv[k] = span > 0 ? d / span : 0.0;
+        total *= d;
+    }
+    while (total > (1 << 21)) {  // coarsen the finest axis
+        int k = 0;
+        for (int j = 1; j < 3; ++j) k = g.dim[j] > g.dim[k] ? j : k;
+        total /= g.dim[k];
+        g.inv[k] *= static_cast<double>((g.dim[k] + 1) / 2) / g.dim[k];
+        g.dim[k] = (g.dim[k] + 1) / 2;
+        total *= g.dim[k];
+    }
+    const auto bin = [&](double v, int k) {
+        const double f = std::floor((v - g.org[k]) * g.inv[k]);
+        return f < 0 ? 0 : (f >= g.dim[k] ? g.dim[k] - 1 : static_cast<int>(f));
+    };
+    std::vector<int32_t> cnt(static_cast<size_t>(total) + 1, 0);
+    std::vector<int2> lst;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int c = 0; c < ncells; ++c) {
+            const double* b = &box[6 * static_cast<size_t>(c)];
+            if (!(b[0] <= b[3])) continue;  // empty cell box
+            int l[3], h[3];
+            for (int k = 0; k < 3; ++k) l[k] = bin(b[k], k), h[k] = bin(b[3 + k], k);
+            const int lo_packed = l[0] | (l[1] << 10) | (l[2] << 20);
+            for (int z = l[2]; z <= h[2]; ++z)
+                for (int y = l[1]; y <= h[1]; ++y)
+                    for (int x = l[0]; x <= h[0]; ++x) {
+                        const size_t q = (static_cast<size_t>(z) * g.dim[1] + y) * g.dim[0] + x;
+                        if (pass == 0) ++cnt[q + 1];
+                        else lst[cnt[q]++] = int2{c, lo_packed};
+                    }
+        }
+        if (pass == 0) {
+            for (size_t q = 0; q < static_cast<size_t>(total); ++q) cnt[q + 1] += cnt[q];
+            lst.resize(std::max<size_t>(1, static_cast<size_t>(cnt[total])), int2{0, 0});
+        } else {
+            for (size_t q = static_cast<size_t>(total); q > 0; --q) cnt[q] = cnt[q - 1];
+            cnt[0] = 0;
+        }
+    }
+    SCK(cudaMalloc(reinterpret_cast<void**>(&g.off), cnt.size() * 4));
+    SCK(cudaMalloc(reinterpret_cast<void**>(&g.cells), lst.size() * sizeof(int2)));
+    SCK(cudaMemcpy(g.off, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice));
+    SCK(cudaMemcpy(g.cells, lst.data(), lst.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    g.entries = cnt[total];
     return cudaSuccess;
 }
 

@@ -1,22 +1,25 @@
 """Multi-GPU driver: one process per GPU, components sharded, obstacles replicated.
 
 SURVEY.md §8(e): a component's label depends only on its own geometry and the
-(replicated) obstacle set, so components shard with no data-path exchange.  Per
-update there are exactly two collectives (torch.distributed over NCCL on B200,
-gloo in the CPU tests):
+(replicated) obstacle set, so components shard with no data-path exchange.  One
+roadmap is split by the engine's interleaved cell sharding
+(``rgg_gpu_options.shard_rank / shard_count``: rank r owns the Morton-ordered cells
+c with c % world == r, so the cells an obstacle dirties spread over every rank).
+Per update (torch.distributed over NCCL on B200, gloo in the CPU tests):
 
 1. ``broadcast`` of the move batch (ids int32[n], poses float64[n, 12]) from
    rank 0 — the host that receives the obstacle updates;
 2. ``all_reduce`` (sum) of the per-move report counters
    (n x {to_green, to_red, to_gray, from_gray}); shards own disjoint components,
-   so the sums are the reference's UpdateReport counts for the whole roadmap.
+   so the sums are the reference's UpdateReport counts for the whole roadmap;
+3. with ``gather_gray``, the per-shard GRAY id lists (compacted inside each
+   shard's update) are gathered to rank 0: an all_gather of the counts and a
+   fixed-capacity all_gather of the lists (capacity = the largest shard, so no
+   host round trip is needed to size it).
 
-The gray list is gathered to rank 0 on request (``gray_ids``): per-shard counts
-with one all_gather, then the id lists padded to the largest count.
-
-Sharding itself is either spatial tiles (each rank's engine holds its own part
-of the roadmap, bench.py's weak-scaling world) or the engine's interleaved cell
-sharding of one roadmap (``rgg_gpu_options.shard_rank / shard_count``).
+Everything is stream-ordered: the engine stream waits on the broadcast, torch's
+stream waits on the engine's counters and gray list; nothing blocks the host
+unless ``check`` asks for the update's device-side status.
 """
 from __future__ import annotations
 
@@ -28,32 +31,80 @@ import torch.distributed as dist
 class DistributedUpdater:
     """Drive a per-rank engine shard.
 
-    ``engine`` needs ``update_tensors(ids, rts, per_move)``, ``counters_into(t, n)``
-    and ``gray_ids()`` (GpuEngine provides them; tests use an oracle-backed shard).
-    ``id_offset`` maps the shard's local component ids to global ids for gray_ids.
+    ``engine`` needs ``update_tensors(ids, rts, per_move, gray_list)``,
+    ``counters_into(t, n, check)``, ``sync()``, ``states()``, ``gray_ids()`` and, for
+    ``gather_gray``, ``gray_count_into(t)`` / ``gray_ids_into(t, cap)`` (GpuEngine
+    provides them; the CPU tests use an oracle-backed shard).  ``id_offset`` maps a
+    shard's local component ids to global ids (0 for interleaved cell shards, whose
+    ids are global already).  ``gray_cap``: capacity per rank of the gathered gray
+    lists (the largest shard's component count).
     """
 
-    def __init__(self, engine, device: torch.device, group=None, id_offset: int = 0):
+    def __init__(self, engine, device: torch.device, group=None, id_offset: int = 0, gray_cap: int = 0):
         self.engine = engine
         self.device = device
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.id_offset = id_offset
+        self.gray_cap = int(gray_cap)
+        self._gray = None
 
-    def update(self, ids: torch.Tensor, rts: torch.Tensor, per_move: bool = True) -> torch.Tensor:
+    def update(self, ids: torch.Tensor, rts: torch.Tensor, per_move: bool = True, check: bool = True,
+               gather_gray: bool = False) -> torch.Tensor:
         """Apply one batch of moves on every shard; returns the summed per-move
-        counters (n x 4 int32) on every rank.  ``ids``/``rts`` are only read on rank 0."""
+        counters (n x 4 int32) on every rank.  ``ids``/``rts`` are only read on rank 0.
+        check=False leaves the update's status to a later ``check()`` (no host wait)."""
         n = int(ids.numel())
         if self.world > 1:
             dist.broadcast(ids, 0, group=self.group)
             dist.broadcast(rts, 0, group=self.group)
-        self.engine.update_tensors(ids, rts, per_move)
-        counters = torch.zeros((n, 4), dtype=torch.int32, device=self.device)
-        self.engine.counters_into(counters, n)
+        # allocated before the update is enqueued: the engine stream waits on this
+        # allocation's stream, and the copy below writes every entry
+        counters = torch.empty((n, 4), dtype=torch.int32, device=self.device)
+        self.engine.update_tensors(ids, rts, per_move, gray_list=gather_gray)
+        self.engine.counters_into(counters, n, check=check)
         if self.world > 1:
             dist.all_reduce(counters, group=self.group)
+        if gather_gray:
+            self._gather_gray()
         return counters
+
+    def check(self):
+        """Wait for the enqueued updates and raise their device-side errors."""
+        self.engine.sync()
+
+    def _gather_gray(self):
+        cap = max(1, self.gray_cap)
+        cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+        ids = torch.empty(cap, dtype=torch.int32, device=self.device)
+        self.engine.gray_count_into(cnt)
+        self.engine.gray_ids_into(ids, cap)
+        if self.id_offset:
+            ids += self.id_offset
+        if self.world > 1:
+            counts = torch.empty(self.world, dtype=torch.int32, device=self.device)
+            lists = torch.empty(self.world * cap, dtype=torch.int32, device=self.device)
+            dist.all_gather_into_tensor(counts, cnt, group=self.group)
+            dist.all_gather_into_tensor(lists, ids, group=self.group)
+        else:
+            counts, lists = cnt, ids
+        self._gray = (counts, lists, cap)
+
+    def gathered_gray(self) -> np.ndarray | None:
+        """The GRAY ids (ascending, global) gathered by the last ``update(gather_gray=True)``,
+        on rank 0 (None elsewhere).  Copies to the host."""
+        if self._gray is None:
+            raise RuntimeError("no gray list gathered: call update(..., gather_gray=True)")
+        if self.rank != 0:
+            return None
+        counts, lists, cap = self._gray
+        c = counts.cpu().numpy()
+        if int(c.max(initial=0)) > cap:
+            raise RuntimeError("a shard's gray list exceeds the gather capacity")
+        flat = lists.cpu().numpy()
+        parts = [flat[r * cap:r * cap + int(c[r])].astype(np.int64) for r in range(len(c))]
+        return np.sort(np.concatenate(parts)) if parts else np.zeros(0, np.int64)
 
     @staticmethod
     def reports(counters: torch.Tensor, unknown_before: int) -> list[dict]:
@@ -87,7 +138,8 @@ class DistributedUpdater:
         return int(t.item())
 
     def gray_ids(self) -> np.ndarray | None:
-        """All GRAY component ids (ascending) on rank 0, None elsewhere."""
+        """All GRAY component ids (ascending) on rank 0, None elsewhere (host lists,
+        outside the update)."""
         local = np.asarray(self.engine.gray_ids(), np.int64) + self.id_offset
         if self.world == 1:
             return np.sort(local)

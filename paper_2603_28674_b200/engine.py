@@ -74,7 +74,8 @@ class Stats(C.Structure):
                 ("compact_ms", C.c_float), ("total_ms", C.c_float), ("dirty_cells", C.c_int32),
                 ("events", C.c_int32), ("overflow_cells", C.c_int32), ("over_pairs", C.c_int64),
                 ("sat_flops", C.c_int64), ("under_pairs", C.c_int64), ("seg_sphere_tests", C.c_int64),
-                ("over_hits", C.c_int64), ("under_hits", C.c_int64), ("bytes_components", C.c_int64)]
+                ("over_hits", C.c_int64), ("under_hits", C.c_int64), ("bytes_components", C.c_int64),
+                ("bytes_fp32", C.c_int64), ("gray", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -121,6 +122,9 @@ def library() -> C.CDLL:
         L.rgg_gpu_set_active_obstacles.argtypes = [vp, vp, vp, i32]
         L.rgg_exact_valid_sets.argtypes = [i32, i32, vp, i32, vp, vp, i32, vp, vp, vp]
         L.rgg_gpu_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), i32]
+        L.rgg_gpu_gray_device.argtypes = [vp, vp, vp, i32]
+        L.rgg_gpu_fp32_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+        L.rgg_gpu_owned.argtypes = [vp, ip]
         _lib = L
     return _lib
 
@@ -156,7 +160,7 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
             "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
             "rgg_gpu_exact_check", "rgg_gpu_filter_stats", "rgg_gpu_set_active_obstacles",
-            "rgg_exact_valid_sets"]
+            "rgg_exact_valid_sets", "rgg_gpu_gray_device", "rgg_gpu_fp32_peak", "rgg_gpu_owned"]
 
 
 @dataclass
@@ -281,6 +285,8 @@ class GpuEngine:
         n, m, w = C.c_int32(), C.c_int32(), C.c_int32()
         L.rgg_gpu_count(h, C.byref(n), C.byref(m), C.byref(w))
         self.n_components, self.n_obstacles, self.words = n.value, m.value, w.value
+        L.rgg_gpu_owned(h, C.byref(n))
+        self.n_owned = n.value  # components of this shard
         self.layout = lv
         self._resolver = None
         self._hv = h.value or 0  # the handle as an int (pyfast)
@@ -313,8 +319,10 @@ class GpuEngine:
 
     # ------------------------------------------------------------ update API
     def batch_update(self, moves, lazy: bool = True, per_move: bool = True,
-                     resolve: Callable[[np.ndarray], np.ndarray] | None = None) -> list[UpdateReport]:
-        """moves: list of (obstacle, pose12) pairs, or a tuple (ids int32[n], rt12 float64[n, 12])."""
+                     resolve: Callable[[np.ndarray], np.ndarray] | None = None,
+                     gray_list: bool = False) -> list[UpdateReport]:
+        """moves: list of (obstacle, pose12) pairs, or a tuple (ids int32[n], rt12 float64[n, 12]).
+        gray_list: compact the GRAY ids inside the update (gray_ids() then only copies them)."""
         ids, rts = self._moves(moves)
         if not lazy:
             if self._resolver is not None and resolve is None:  # exact resolve on the GPU, move by move
@@ -330,7 +338,7 @@ class GpuEngine:
         if n == 0:
             return []
         reps = (_Report * n)()
-        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0)
+        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0) | (RGG_GRAY_LIST if gray_list else 0)
         fast = _fast()
         if fast is not None:
             rc = fast.update(self._hv, ids, rts, flags, reps)
@@ -422,8 +430,12 @@ class GpuEngine:
         self._check(library().rgg_gpu_update(self._h, ids.ctypes.data, rts.ctypes.data, len(ids),
                                              RGG_LAZY | RGG_ASYNC, None))
 
-    def update_device(self, d_ids_ptr: int, d_rt_ptr: int, n: int, per_move: bool = False, census: bool = False):
-        flags = RGG_LAZY | (RGG_PER_MOVE if per_move else 0) | (RGG_CENSUS if census else 0)
+    def update_device(self, d_ids_ptr: int, d_rt_ptr: int, n: int, per_move: bool = False, census: bool = False,
+                      gray_list: bool = False):
+        """Enqueue a lazy batch whose moves are already in device memory (no host wait).
+        gray_list: the GRAY-id compaction runs inside the update."""
+        flags = (RGG_LAZY | (RGG_PER_MOVE if per_move else 0) | (RGG_CENSUS if census else 0)
+                 | (RGG_GRAY_LIST if gray_list else 0))
         self._check(library().rgg_gpu_update_device(self._h, C.c_void_p(d_ids_ptr), C.c_void_p(d_rt_ptr), n, flags))
 
     def sync(self):
@@ -437,14 +449,30 @@ class GpuEngine:
             self._ext = torch.cuda.ExternalStream(self.stream(), device=device)
         return self._ext
 
-    def update_tensors(self, ids, rts, per_move: bool = True):
+    def update_tensors(self, ids, rts, per_move: bool = True, gray_list: bool = False):
         """ids int32[n] / rts float64[n, 12] CUDA tensors, enqueued on the engine stream
         after the current torch stream's work (so a preceding broadcast is visible); no
         host synchronisation."""
         import torch
 
         self._torch_stream(ids.device).wait_stream(torch.cuda.current_stream(ids.device))
-        self.update_device(ids.data_ptr(), rts.data_ptr(), int(ids.numel()), per_move=per_move)
+        self.update_device(ids.data_ptr(), rts.data_ptr(), int(ids.numel()), per_move=per_move, gray_list=gray_list)
+
+    def gray_count_into(self, out):
+        """The GRAY count of the last update (compacted with gray_list=True) into a CUDA
+        int32 tensor (1,), ordered before the current torch stream's later work."""
+        import torch
+
+        self._check(library().rgg_gpu_gray_device(self._h, C.c_void_p(out.data_ptr()), C.c_void_p(0), 0))
+        torch.cuda.current_stream(out.device).wait_stream(self._torch_stream(out.device))
+
+    def gray_ids_into(self, out, cap: int):
+        """The first cap GRAY ids (ascending) of the last update into a CUDA int32 tensor,
+        on the engine stream, ordered before the current torch stream's later work."""
+        import torch
+
+        self._check(library().rgg_gpu_gray_device(self._h, C.c_void_p(0), C.c_void_p(out.data_ptr()), int(cap)))
+        torch.cuda.current_stream(out.device).wait_stream(self._torch_stream(out.device))
 
     def counters_into(self, out, n: int, check: bool = True):
         """Per-move counters of the last update into a CUDA int32 tensor (n, 4), ordered
@@ -557,6 +585,15 @@ class GpuEngine:
 def fp64_peak_gflops(device: int = 0) -> float:
     v = C.c_double()
     rc = library().rgg_gpu_fp64_peak(device, C.byref(v))
+    if rc != RGG_OK:
+        raise RuntimeError(library().rgg_gpu_last_error(None).decode())
+    return v.value
+
+
+def fp32_peak_gflops(device: int = 0) -> float:
+    """Measured FP32 FMA rate (GFLOP/s, 2 per FFMA) of `device`."""
+    v = C.c_double()
+    rc = library().rgg_gpu_fp32_peak(device, C.byref(v))
     if rc != RGG_OK:
         raise RuntimeError(library().rgg_gpu_last_error(None).decode())
     return v.value

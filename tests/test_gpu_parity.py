@@ -207,24 +207,8 @@ def test_item_queue_overflow_replays(eng_mod, name, monkeypatch):
     assert np.array_equal(bits, g["snap_bits"][-1].reshape(bits.shape))
 
 
-@pytest.mark.parametrize("pipeline", ["3", "4"])
-def test_comparison_pipelines_stay_exact(pipeline):
-    """The earlier designs kept for comparison (RGG_PIPELINE=3: CTA-per-cell touch /
-    narrow / apply; 4: one fused warp kernel) still reproduce the golden replays."""
-    import os
-    import subprocess
-    import sys
-
-    env = dict(os.environ, RGG_PIPELINE=pipeline)
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "replay_one_batch or chunked",
-                        os.path.join(here, "test_gpu_parity.py")], env=env, capture_output=True, text=True,
-                       timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-
-
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}])
+@pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}, {"RGG_NO_SMALL_BIN": "1"}])
 def test_kernel_handoffs(env):
     """The split pipeline's in-kernel handoffs, forced on or off for every batch size
     (rgg_kernels.cu: bin on the pose warps' published boxes, touch on bin's published
