@@ -29,6 +29,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <cstring>
 #include <vector>
 
 #include "rgg/batch_layout.hpp"
@@ -127,13 +128,17 @@ public:
         // eager: move by move on the device, each move's gray over-hits resolved exactly
         const int rc = rgg_gpu_update(h_, ids.data(), rt.data(), static_cast<std::int32_t>(ids.size()),
                                       (lazy ? RGG_LAZY : RGG_EAGER) | RGG_PER_MOVE, rep.data());
-        // the moves the device applied (all, or those before an unknown id) mutate the scene
+        // the moves the device applied mutate the scene: all of them, those before the first
+        // unknown id (the reference's sequential loop throws there, engine_batch.cpp:146-148),
+        // or none when the call was rejected before the device ran or the update failed
         size_t applied = moves.size();
-        if (rc == RGG_EINVAL)
-            for (applied = 0; applied < moves.size() && moves[applied].first >= 0 &&
-                              moves[applied].first < static_cast<ObstacleId>(scene_.obstacles.size());
-                 ++applied) {
-            }
+        if (rc != RGG_OK) {
+            applied = 0;
+            if (rc == RGG_EINVAL && std::strcmp(rgg_gpu_last_error(h_), "unknown obstacle id") == 0)
+                while (applied < moves.size() && moves[applied].first >= 0 &&
+                       moves[applied].first < static_cast<ObstacleId>(scene_.obstacles.size()))
+                    ++applied;
+        }
         for (size_t i = 0; i < applied; ++i) {
             scene_.obstacles[moves[i].first].pose = moves[i].second;
             scene_.obstacles[moves[i].first].active = true;

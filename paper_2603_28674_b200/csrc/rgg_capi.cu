@@ -139,6 +139,7 @@ struct rgg_gpu {
     bool timed = false;
     int grid_classify = 1;
     int64_t total_segs_owned = 0;
+    bool poisoned = false;  // a failed eager batch left a partial state (rgg_gpu_update fails from then on)
 };
 
 namespace {
@@ -319,11 +320,10 @@ void dump_timeline(rgg_gpu* h) {
     if (cudaMemcpy(t, h->d_tl, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess) return;
     const double z = static_cast<double>(~t[0]);
     const auto us = [&](unsigned long long v) { return (static_cast<double>(v) - z) * 1e-3; };
-    static const char* name[13] = {"pose", "bin", "touch", "narrow", "apply", "", "", "", "", "scatter", "",
-                                   "c.count", "c.list"};
+    static const char* name[10] = {"pose", "bin", "touch", "narrow", "apply", "", "", "", "", "scatter"};
     std::fprintf(stderr, "[tl]");
-    for (int k = 0; k < 13; ++k) {
-        if ((k >= 5 && k < 9) || k == 10) continue;
+    for (int k = 0; k < 10; ++k) {
+        if (k >= 5 && k < 9) continue;
         const unsigned long long* p = t + 8 * k;
         if (!p[5]) continue;
         std::fprintf(stderr, " %s %.1f %.1f %.1f %.1f %.2f |", name[k], us(~p[0]), us(p[1]), us(~p[2]), us(p[3]),
@@ -339,6 +339,8 @@ void dump_timeline(rgg_gpu* h) {
 constexpr int32_t kMaxBatch = 1 << 26;
 // internal enqueue flag: host copies inside the update's graph
 constexpr int32_t kHostIO = 1 << 20;
+// host updates of at most this many moves read them from mapped memory in the pose kernel
+constexpr int32_t kMappedMovesMax = 128;
 
 bool graphs_enabled(const rgg_gpu* h) {
     static const bool off = std::getenv("RGG_DEBUG_PHASES") || std::getenv("RGG_NO_GRAPH");
@@ -391,7 +393,11 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         b.out_mv = h->dh_mv;
         b.out_ctr = h->dh_ctr;
     }
-    if (hostio) {  // the pose kernel reads the moves from the mapped staging buffer
+    // small batches: the pose kernel reads the moves straight from the mapped staging
+    // buffer (no copy node); large ones (a 1024-move batch is 100 KB, read by every pose
+    // warp over PCIe) get one H2D copy node into HBM before the pose kernel
+    const bool mapped_moves = hostio && n <= kMappedMovesMax;
+    if (mapped_moves) {
         b.src_ids = h->dh_ids;
         b.src_rt = reinterpret_cast<const double*>(reinterpret_cast<const char*>(h->dh_ids) + h->pin_off);
     }
@@ -416,6 +422,9 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             };
             CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
             cudaError_t e = rec(h->ev[0]);
+            if (e == cudaSuccess && hostio && !mapped_moves)
+                e = cudaMemcpyAsync(h->d_ids, h->h_ids, h->in_off + static_cast<size_t>(n) * 96, cudaMemcpyHostToDevice,
+                                    h->stream);
             if (e == cudaSuccess) e = rggk::launch_pose(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[1]);
             if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);
@@ -501,7 +510,11 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     if (M > 64 && !o.allow_wide) return fail(h, RGG_EINVAL, "obstacle bitsets support at most 64 obstacles");
     if (C > rggk::kMaxSpheres) return fail(h, RGG_EINVAL, "too many spheres per obstacle (max 16)");
     if (M > 0xfffe) return fail(h, RGG_EINVAL, "too many obstacles");
-    const int cell = o.cell_size > 0 ? o.cell_size : 128;
+    static const int cell_default = [] {  // RGG_CELL_SIZE: experiments only
+        const char* e = std::getenv("RGG_CELL_SIZE");
+        return e ? std::atoi(e) : 128;
+    }();
+    const int cell = o.cell_size > 0 ? o.cell_size : cell_default;
     if (cell % 32 != 0 || cell > rggk::kMaxCell) return fail(h, RGG_EINVAL, "cell_size must be a multiple of 32, <= 128");
     const int cap = o.cell_capacity > 0 ? o.cell_capacity : 64;
     const int shards = o.shard_count > 1 ? o.shard_count : 1;
@@ -709,6 +722,7 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
                    rgg_update_report* reports) {
     if (!h) return RGG_EINVAL;
     clear_stale_error();
+    if (h->poisoned) return fail(h, RGG_ELOGIC, "engine state lost after a failed eager update");
     if (n < 0 || (n > 0 && (!ids || !rt12))) return fail(h, RGG_EINVAL, "bad move list");
     if (n >= kMaxBatch) return fail(h, RGG_EINVAL, "at most 2^26 - 1 moves per batch (split it)");
     if (!(flags & (RGG_LAZY | RGG_EAGER)))
@@ -755,6 +769,7 @@ static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int3
         }
         std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
         std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 96);
+        CK(cudaMemsetAsync(h->d_ctr + 18, 0, sizeof(int32_t), h->stream));  // the batch's sticky status
         CK(cudaMemcpyAsync(h->d_eg_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
         CK(cudaMemcpyAsync(h->d_eg_rt, h->h_rt, static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice, h->stream));
         const Batch b = batch_of(h, 1);
@@ -770,7 +785,12 @@ static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int3
                            cudaMemcpyDeviceToHost, h->stream));
         CK(cudaMemcpyAsync(h->h_ctr, h->d_ctr, 24 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
         CK(stream_wait(h));
-        if (h->h_ctr[6]) return fail(h, RGG_ELOGIC, "eager update: device pool overflow");
+        if (h->h_ctr[6] | h->h_ctr[18]) {
+            // some move failed on the device and the moves after it were applied: the
+            // engine's state is no longer the reference's, so every later call fails
+            h->poisoned = true;
+            return fail(h, RGG_ELOGIC, "eager update failed on the device (engine state lost)");
+        }
         int32_t u = h->unknown;
         for (int32_t i = 0; i < k; ++i) {
             const int32_t* q = h->h_eg_rep + 8 * i;  // mv[4], hits, resolve deltas [3]

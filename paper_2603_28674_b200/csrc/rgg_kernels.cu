@@ -610,7 +610,6 @@ __global__ void __launch_bounds__(32 * kCellWarps) bin_cells_kernel(Store s, Bat
     int count = 0;
     for (int w = lane; w < nw; w += 32) count += __popc(m[w]);
     count = __reduce_add_sync(0xffffffffu, count);
-    tl_stop(b.tl, 11, t0);
     int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
     int32_t* dst = inl;
     int lim = count;
@@ -650,7 +649,6 @@ __global__ void __launch_bounds__(32 * kCellWarps) bin_cells_kernel(Store s, Bat
             at += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
-    tl_stop(b.tl, 12, t0);
     bin_cells_tail<kCellWarps>(s, b, cell, count, inl, lane, warp);
     tl_stop(b.tl, 1, t0);
     if (live) bin_warp_done(b, lane);
@@ -1675,6 +1673,7 @@ __global__ void eager_step_kernel(Batch b, int32_t* ids0, double* rt0, const int
                                   int32_t* rep, int i, int k) {
     const int t = threadIdx.x;
     if (i > 0 && t < 8) rep[8 * (i - 1) + t] = t < 4 ? b.mv[t] : (t == 4 ? b.ctr[5] : b.ctr[20 + t - 5]);
+    if (i > 0 && t == 0 && b.ctr[6]) b.ctr[18] |= b.ctr[6];  // sticky status of the batch (pose resets ctr[6])
     if (i < k) {
         if (t == 0) ids0[0] = st_ids[i];
         if (t < 12) rt0[t] = st_rt[12 * static_cast<size_t>(i) + t];

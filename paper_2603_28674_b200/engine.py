@@ -257,7 +257,7 @@ def _pose12(pose) -> np.ndarray:
 
 
 class GpuEngine:
-    def __init__(self, layout, use_under: bool = True, cell_size: int = 128, cell_capacity: int = 64,
+    def __init__(self, layout, use_under: bool = True, cell_size: int = 0, cell_capacity: int = 64,
                  allow_wide: bool | None = None, device: int = 0, shard_rank: int = 0, shard_count: int = 1):
         L = library()
         lv = layout if isinstance(layout, LayoutView) else LayoutView.from_any(layout)
