@@ -78,6 +78,28 @@ typedef struct rgg_layout_view {
     const int32_t* obst_sph_n;
 } rgg_layout_view;
 
+/* The same store from the components themselves, without the serialized layout:
+ * the engine runs the serialize step (BatchLayout::serialize, batch_layout.cpp:55-146:
+ * sat_prep of the corners, component AABBs, seg_prep of the real segments) on the
+ * device.  A caller that never needs the padded host layout (12x the real segments
+ * at c2) never builds it.
+ *   obb_corners     N*B*24   obb_corners(components.geometry[c].over[b]) (batch_layout.cpp:10-17)
+ *   row_off         N*B*S+1  real segments of row (c, b, s), as in rgg_layout_view
+ *   seg_points      T*6      each real segment's end points (a, b); a single-point spline is
+ *                            one degenerate segment (a, a) (batch_layout.cpp:84-90)
+ *   spline_radius .. obst_sph_n: as in rgg_layout_view */
+typedef struct rgg_component_view {
+    int32_t n_components, n_bodies, n_slots, n_obstacles, max_spheres;
+    const double* obb_corners;
+    const int32_t* row_off;
+    const double* seg_points;
+    const double* spline_radius;
+    const double* obst_he;
+    const double* obst_sph_local;
+    const double* obst_sph_r;
+    const int32_t* obst_sph_n;
+} rgg_component_view;
+
 typedef struct rgg_gpu_options {
     int32_t device;        /* CUDA ordinal (one process per GPU) */
     int32_t use_under;     /* EngineOptions::use_under (update_report.hpp:43-46) */
@@ -113,6 +135,8 @@ typedef struct rgg_gpu rgg_gpu;
 /* BatchEngine::BatchEngine (engine_batch.cpp:20-31): uploads the store into
  * HBM (cell-sorted SoA), builds the cells, all labels GREEN, bits 0. */
 int rgg_gpu_create(const rgg_layout_view* view, const rgg_gpu_options* opts, rgg_gpu** out);
+/* rgg_gpu_create from raw components (rgg_component_view): same engine, same results. */
+int rgg_gpu_create_from_components(const rgg_component_view* view, const rgg_gpu_options* opts, rgg_gpu** out);
 void rgg_gpu_destroy(rgg_gpu* h);
 const char* rgg_gpu_last_error(const rgg_gpu* h);
 

@@ -52,6 +52,7 @@ def lib():
         L.rr_engine_free.argtypes = [C.c_void_p]
         L.rr_engine_update.argtypes = [C.c_void_p, C.c_int32, _dp, C.c_int, _lp]
         L.rr_engine_run.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.POINTER(C.c_double)]
+        L.rr_engine_run_parallel.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.rr_world_poses.argtypes = [C.c_void_p, _lp, C.c_void_p]
         L.rr_world_body_he.argtypes = [C.c_void_p, _dp]
         L.rr_box_intersect.argtypes = [_dp, _dp, _dp, _dp, C.POINTER(C.c_int)]
@@ -238,6 +239,14 @@ class Engine:
         rts = np.ascontiguousarray(rts, np.float64).reshape(-1)
         us = C.c_double(0)
         _check(lib().rr_engine_run(self.h, len(ids), ids, rts, int(lazy), C.byref(us)))
+        return us.value
+
+    def run_parallel(self, ids, rts, threads, lazy=True) -> float:
+        """run() with the obstacle groups' engines on up to `threads` host threads."""
+        ids = np.ascontiguousarray(ids, np.int32)
+        rts = np.ascontiguousarray(rts, np.float64).reshape(-1)
+        us = C.c_double(0)
+        _check(lib().rr_engine_run_parallel(self.h, len(ids), ids, rts, int(lazy), int(threads), C.byref(us)))
         return us.value
 
     def states(self):

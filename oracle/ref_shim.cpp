@@ -20,6 +20,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "oracles.hpp"
@@ -396,6 +397,52 @@ int rr_engine_run(void* ep, int n, const std::int32_t* ids, const double* rt12, 
                 g.seq->update_obstacle(local, tf_of(rt12 + 12 * i), lazy != 0);
         }
         const auto t1 = std::chrono::steady_clock::now();
+        if (elapsed_us) *elapsed_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
+    });
+}
+
+// The same moves with the obstacle groups' engines run concurrently, one host thread
+// per group (at most `threads` at a time): the groups are independent engines over
+// the same components, and each group's moves keep their order, so the combined
+// states and bits equal rr_engine_run's.  The grouped reference's use of all host
+// threads (a single SequentialEngine is single-threaded).
+int rr_engine_run_parallel(void* ep, int n, const std::int32_t* ids, const double* rt12, int lazy, int threads,
+                           double* elapsed_us) {
+    Engine* e = static_cast<Engine*>(ep);
+    return guarded([&] {
+        const int m = static_cast<int>(e->world->scene.obstacles.size());
+        const int ng = static_cast<int>(e->groups.size());
+        std::vector<std::vector<int>> per(ng);
+        for (int i = 0; i < n; ++i) {
+            const int o = ids[i];
+            if (o < 0 || o >= m || o / e->group_size >= ng) throw std::invalid_argument("unknown obstacle id");
+            per[o / e->group_size].push_back(i);
+        }
+        const int nt = std::max(1, std::min(threads, ng));
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(nt);
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    for (int g = t; g < ng; g += nt) {
+                        Group& grp = *e->groups[g];
+                        for (int i : per[g]) {
+                            const ObstacleId local = ids[i] % e->group_size;
+                            if (grp.bat)
+                                grp.bat->update_obstacle(local, tf_of(rt12 + 12 * i), lazy != 0);
+                            else
+                                grp.seq->update_obstacle(local, tf_of(rt12 + 12 * i), lazy != 0);
+                        }
+                    }
+                } catch (const std::exception& ex) {
+                    errs[t] = ex.what();
+                }
+            });
+        for (auto& th : pool) th.join();
+        const auto t1 = std::chrono::steady_clock::now();
+        for (const auto& er : errs)
+            if (!er.empty()) throw std::runtime_error(er);
         if (elapsed_us) *elapsed_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
     });
 }

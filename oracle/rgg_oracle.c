@@ -151,6 +151,21 @@ static int aabb_overlaps(const double* a, const double* b) {
     return a[0] <= b[3] && b[0] <= a[3] && a[1] <= b[4] && b[1] <= a[4] && a[2] <= b[5] && b[2] <= a[5];
 }
 
+/* The candidate filter of a (component, obstacle) pair.  The reference tests every
+ * spatial-grid candidate (engine_batch.cpp:55-74, spatial_grid.cpp:114-135); a pair
+ * whose exact AABBs miss by an ulp can still be an fp64 SAT / segment-sphere hit
+ * (tests/test_gpu_filter.py finds such pairs), so the obstacle box b is widened by a
+ * relative 2^-40 on every face, as the GPU's pose kernel does (rgg_kernels.cu widen_*). */
+static double widen(double v, int up) {
+    if (!isfinite(v)) return v;
+    return up ? v + (fabs(v) + 1.0) * 0x1p-40 : v - (fabs(v) + 1.0) * 0x1p-40;
+}
+static int candidate_overlaps(const double* comp, const double* b) {
+    double w[6];
+    for (int k = 0; k < 6; ++k) w[k] = widen(b[k], k >= 3);
+    return aabb_overlaps(comp, w);
+}
+
 /* Transform::apply (vec3.hpp:72-76): ((r0 x + r1 y) + r2 z) + t. */
 static void tf_apply(const double* rt, const double* p, double* out) {
     for (int i = 0; i < 3; ++i)
@@ -356,7 +371,7 @@ int ro_engine_update(ro_engine* e, int32_t o, const double* rt, int64_t* rep) {
     e->active[o] = 1;
     /* over phase (engine_batch.cpp:163-177); candidates = closed AABB overlap */
     for (int32_t c = 0; c < N; ++c) {
-        if (!aabb_overlaps(e->v.comp_aabb + 6 * (size_t)c, e->oaabb + 6 * (size_t)o)) continue;
+        if (!candidate_overlaps(e->v.comp_aabb + 6 * (size_t)c, e->oaabb + 6 * (size_t)o)) continue;
         if (!over_pair(e, c, o)) continue;
         if (e->states[c] == 0) set_state(e, c, 2);
         uint64_t* bc = e->bits + (size_t)c * W + w;
@@ -368,7 +383,7 @@ int ro_engine_update(ro_engine* e, int32_t o, const double* rt, int64_t* rep) {
     /* under phase (engine_batch.cpp:181-188) */
     if (e->use_under) {
         for (int32_t c = 0; c < N; ++c) {
-            if (!aabb_overlaps(e->v.comp_aabb + 6 * (size_t)c, e->osaabb + 6 * (size_t)o)) continue;
+            if (!candidate_overlaps(e->v.comp_aabb + 6 * (size_t)c, e->osaabb + 6 * (size_t)o)) continue;
             if (under_pair(e, c, o)) set_state(e, c, 1);
         }
     }
@@ -412,11 +427,11 @@ void ro_engine_pure(const ro_engine* e, uint8_t* states, uint64_t* bits) {
         for (int32_t o = 0; o < e->v.n_obstacles; ++o) {
             if (!e->active[o]) continue;
             const double* ca = e->v.comp_aabb + 6 * (size_t)c;
-            if (aabb_overlaps(ca, e->oaabb + 6 * (size_t)o) && over_pair(e, c, o)) {
+            if (candidate_overlaps(ca, e->oaabb + 6 * (size_t)o) && over_pair(e, c, o)) {
                 over = 1;
                 bc[o >> 6] |= 1ull << (o & 63);
             }
-            if (e->use_under && aabb_overlaps(ca, e->osaabb + 6 * (size_t)o) && under_pair(e, c, o)) under = 1;
+            if (e->use_under && candidate_overlaps(ca, e->osaabb + 6 * (size_t)o) && under_pair(e, c, o)) under = 1;
         }
         states[c] = under ? 1 : (over ? 2 : 0);
     }
@@ -435,7 +450,7 @@ void ro_engine_census(const ro_engine* e, int64_t* out) {
         const int64_t segs = e->v.row_off[((size_t)c + 1) * nb * ns] - e->v.row_off[(size_t)c * nb * ns];
         for (int32_t o = 0; o < e->v.n_obstacles; ++o) {
             if (!e->active[o]) continue;
-            if (aabb_overlaps(ca, e->oaabb + 6 * (size_t)o)) {
+            if (candidate_overlaps(ca, e->oaabb + 6 * (size_t)o)) {
                 int hit = 0;
                 for (int b = 0; b < nb; ++b) {
                     const double* a = e->v.edge_sat + 21 * ((size_t)c * nb + b);
@@ -445,7 +460,7 @@ void ro_engine_census(const ro_engine* e, int64_t* out) {
                 }
                 out[4] += hit;
             }
-            if (e->use_under && aabb_overlaps(ca, e->osaabb + 6 * (size_t)o)) {
+            if (e->use_under && candidate_overlaps(ca, e->osaabb + 6 * (size_t)o)) {
                 out[2] += 1;
                 out[3] += segs * e->v.obst_sph_n[o];
                 out[5] += under_pair(e, c, o);

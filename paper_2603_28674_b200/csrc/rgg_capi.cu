@@ -40,6 +40,7 @@ struct rgg_gpu {
     int32_t* d_orig = nullptr;
     int32_t* d_rank = nullptr;
     double* d_cell_aabb = nullptr;
+    double* d_slice_aabb = nullptr;
     rggk::CellGrid grid{};   // the binning's uniform grid over the cell boxes
     uint32_t* d_cmask = nullptr;  // Batch::cmask (ncells x cmask_words)
     int32_t cmask_words = 0;
@@ -497,12 +498,81 @@ extern "C" {
 
 const char* rgg_gpu_last_error(const rgg_gpu* h) { return h ? h->err.c_str() : "null handle"; }
 
-int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gpu** out) {
+}  // extern "C"
+
+namespace {
+// Device-resident inputs of rgg_gpu_create_from_components (sat_prep / seg_prep done on
+// the device); null: the view's host arrays are uploaded.
+struct DeviceInputs {
+    const double* comp_aabb = nullptr;
+    const double* edge_sat = nullptr;
+    const double* segs = nullptr;
+    const int32_t* row_off = nullptr;
+};
+int create_impl(rgg_gpu* h, const rgg_layout_view* v, const rgg_gpu_options* opts, const DeviceInputs* dev);
+}  // namespace
+
+extern "C" int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gpu** out) {
     if (!out) return RGG_EINVAL;
     *out = nullptr;
     rgg_gpu* h = new rgg_gpu();
     *out = h;
     if (!v) return fail(h, RGG_EINVAL, "null layout view");
+    return create_impl(h, v, opts, nullptr);
+}
+
+extern "C" int rgg_gpu_create_from_components(const rgg_component_view* cv, const rgg_gpu_options* opts,
+                                              rgg_gpu** out) {
+    if (!out) return RGG_EINVAL;
+    *out = nullptr;
+    rgg_gpu* h = new rgg_gpu();
+    *out = h;
+    if (!cv) return fail(h, RGG_EINVAL, "null component view");
+    const int32_t N = cv->n_components, B = cv->n_bodies, S = cv->n_slots;
+    if (N < 0 || B < 1 || S < 1) return fail(h, RGG_EINVAL, "malformed component view");
+    const int64_t nrows = static_cast<int64_t>(N) * B * S;
+    if (cv->row_off[0] != 0) return fail(h, RGG_ELOGIC, "row_off must start at 0");
+    for (int64_t r = 0; r < nrows; ++r)
+        if (cv->row_off[r + 1] < cv->row_off[r]) return fail(h, RGG_ELOGIC, "row_off must be non-decreasing");
+    const int64_t T = cv->row_off[nrows];
+    if (T > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
+    rgg_gpu_options o{};
+    if (opts) o = *opts;
+    clear_stale_error();
+    CK(cudaSetDevice(o.device));
+    // upload the raw geometry, then sat_prep / AABBs / seg_prep on the device
+    struct Bufs {
+        std::vector<void*> p;
+        ~Bufs() {
+            for (void* q : p) cudaFree(q);
+        }
+    } bufs;
+    const auto take = [&](auto** q, size_t n) {
+        const cudaError_t e = dalloc(q, n);
+        if (e == cudaSuccess) bufs.p.push_back(*q);
+        return e;
+    };
+    double *d_corners, *d_pts, *d_aabb, *d_sat, *d_segs;
+    int32_t* d_row;
+    CK(take(&d_corners, static_cast<size_t>(N) * B * 24));
+    CK(take(&d_pts, static_cast<size_t>(T) * 6));
+    CK(take(&d_aabb, static_cast<size_t>(N) * 6));
+    CK(take(&d_sat, static_cast<size_t>(N) * B * 21));
+    CK(take(&d_segs, static_cast<size_t>(T) * 7));
+    CK(take(&d_row, static_cast<size_t>(nrows) + 1));
+    CK(cudaMemcpy(d_corners, cv->obb_corners, static_cast<size_t>(N) * B * 24 * 8, cudaMemcpyHostToDevice));
+    if (T) CK(cudaMemcpy(d_pts, cv->seg_points, static_cast<size_t>(T) * 6 * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_row, cv->row_off, (static_cast<size_t>(nrows) + 1) * 4, cudaMemcpyHostToDevice));
+    CK(rggk::prep_components(d_corners, N, B, d_pts, static_cast<int>(T), d_sat, d_aabb, d_segs, nullptr));
+    CK(cudaDeviceSynchronize());
+    rgg_layout_view v{N, B, S, cv->n_obstacles, cv->max_spheres, nullptr, nullptr, cv->row_off, nullptr,
+                      cv->spline_radius, cv->obst_he, cv->obst_sph_local, cv->obst_sph_r, cv->obst_sph_n};
+    const DeviceInputs dev{d_aabb, d_sat, d_segs, d_row};
+    return create_impl(h, &v, opts, &dev);
+}
+
+namespace {
+int create_impl(rgg_gpu* h, const rgg_layout_view* v, const rgg_gpu_options* opts, const DeviceInputs* dev) {
     rgg_gpu_options o{};
     if (opts) o = *opts;
     const int32_t N = v->n_components, B = v->n_bodies, S = v->n_slots, M = v->n_obstacles, C = v->max_spheres;
@@ -566,12 +636,18 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     CK(dalloc(&h->d_orig, Np));
     CK(dalloc(&h->d_rank, N));
     CK(dalloc(&h->d_cell_aabb, static_cast<size_t>(std::max(ncells, 1)) * 6));
+    CK(dalloc(&h->d_slice_aabb, static_cast<size_t>(std::max((Np + 31) / 32, 1)) * 6));
     {
         rggk::StoreIn in{N, B, S, static_cast<int32_t>(T), Np, cell, shards, rank,
                          v->comp_aabb, v->edge_sat, v->row_off, v->segs, v->spline_radius};
+        if (dev) {
+            in.comp_aabb = dev->comp_aabb, in.edge_sat = dev->edge_sat, in.segs = dev->segs;
+            in.device = true;
+            in.row_off_dev = dev->row_off;
+        }
         rggk::StoreOut so{};
         so.aabb = h->d_aabb, so.sat = h->d_sat, so.sat32 = h->d_sat32, so.row = h->d_row, so.spline = h->d_spline;
-        so.orig = h->d_orig, so.rank = h->d_rank, so.cell_aabb = h->d_cell_aabb;
+        so.orig = h->d_orig, so.rank = h->d_rank, so.cell_aabb = h->d_cell_aabb, so.slice_aabb = h->d_slice_aabb;
         mark("allocs");
         CK(rggk::build_store(in, so, h->stream));
         mark("build_store");
@@ -662,6 +738,7 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     s.spline_r = h->d_spline;
     s.orig = h->d_orig;
     s.cell_aabb = h->d_cell_aabb;
+    s.slice_aabb = h->d_slice_aabb;
     for (int k = 0; k < 3; ++k) s.gorg[k] = h->grid.org[k], s.ginv[k] = h->grid.inv[k], s.gdim[k] = h->grid.dim[k];
     s.gcell_off = h->grid.off;
     s.gcell = h->grid.cells;
@@ -689,12 +766,16 @@ int rgg_gpu_create(const rgg_layout_view* v, const rgg_gpu_options* opts, rgg_gp
     return RGG_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 void rgg_gpu_destroy(rgg_gpu* h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->done_ev) cudaEventDestroy(h->done_ev);
-    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->grid.off, h->grid.cells, h->d_cmask, h->d_evbox, h->d_evt, h->d_evs, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb,
+    void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->grid.off, h->grid.cells, h->d_cmask, h->d_evbox, h->d_evt, h->d_evs, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb, h->d_slice_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
                    h->d_cell_list, h->d_cell_ovf, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,

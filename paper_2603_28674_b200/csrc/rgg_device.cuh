@@ -296,6 +296,21 @@ __host__ __device__ inline void box32_terms(const double* sat, Box32& x) {
         x.h[k] = static_cast<float>(sqrt(n2));
         degen |= !(u2 > 0.5);
     }
+    // sat_filter32g's margins equal the reference's for orthonormal frames with e_k = |e_k| u_k
+    // (what sat_prep produces, kernels_scalar.cpp:18-28): a caller's SatBox outside that
+    // (|u_i.u_j|, ||u_k|^2 - 1| or the e/u misalignment above 1e-9) is decided in fp64
+    for (int i = 0; i < 3 && !degen; ++i) {
+        const double* ui = sat + 12 + 3 * i;
+        const double* ei = sat + 3 + 3 * i;
+        const double uu = ui[0] * ui[0] + ui[1] * ui[1] + ui[2] * ui[2];
+        degen |= !(fabs(uu - 1.0) <= 1e-9);
+        const double h = sqrt(ei[0] * ei[0] + ei[1] * ei[1] + ei[2] * ei[2]);
+        for (int k = 0; k < 3; ++k) degen |= !(fabs(ei[k] - h * ui[k]) <= 1e-9 * (h + 1e-300));
+        for (int j = i + 1; j < 3; ++j) {
+            const double* uj = sat + 12 + 3 * j;
+            degen |= !(fabs(ui[0] * uj[0] + ui[1] * uj[1] + ui[2] * uj[2]) <= 1e-9);
+        }
+    }
     x.degen = degen ? 1u : 0u;
     // rounded up: nextafter of the nearest float of a value inflated by 1e-15
     const float lf = static_cast<float>(l1 * (1.0 + 1e-15));

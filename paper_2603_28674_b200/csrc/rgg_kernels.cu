@@ -79,6 +79,13 @@ __device__ __forceinline__ void aabb_expand(double* a, double x, double y, doubl
     a[5] = fmax(a[5], z);
 }
 
+// The candidate filter's widening of an obstacle box face: 2^-40 relative (plus 2^-40
+// absolute near zero), far above the fp64 rounding of the SAT margins and the AABB
+// corners (~1e-16 relative) and far below any geometric scale.  +-inf (empty boxes)
+// stay as they are.
+__device__ __forceinline__ double widen_lo(double v) { return isfinite(v) ? v - (fabs(v) + 1.0) * 0x1p-40 : v; }
+__device__ __forceinline__ double widen_hi(double v) { return isfinite(v) ? v + (fabs(v) + 1.0) * 0x1p-40 : v; }
+
 __device__ __forceinline__ void aabb_union(const double* a, const double* b, double* out) {
     for (int k = 0; k < 3; ++k) out[k] = fmin(a[k], b[k]);
     for (int k = 3; k < 6; ++k) out[k] = fmax(a[k], b[k]);
@@ -236,13 +243,16 @@ __global__ void pose_kernel(Store s, Batch b) {
             }
         }
     }
-    // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16
+    // boxes: new corners on lane 0, old corners on lane 8, spheres on lane 16, each
+    // widened by a relative 2^-40 (candidate_widen): the reference tests every grid
+    // candidate, and the fp64 SAT / segment-sphere test can report contact for a pair
+    // whose exact AABBs miss by an ulp, so the AABB filter keeps those pairs too
     double bn[6], bo[6], bs[6];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        bn[k] = shfl(lo[k], 0), bn[3 + k] = shfl(hi[k], 0);
-        bo[k] = shfl(lo[k], 8), bo[3 + k] = shfl(hi[k], 8);
-        bs[k] = shfl(lo[k], 16), bs[3 + k] = shfl(hi[k], 16);
+        bn[k] = widen_lo(shfl(lo[k], 0)), bn[3 + k] = widen_hi(shfl(hi[k], 0));
+        bo[k] = widen_lo(shfl(lo[k], 8)), bo[3 + k] = widen_hi(shfl(hi[k], 8));
+        bs[k] = widen_lo(shfl(lo[k], 16)), bs[3 + k] = widen_hi(shfl(hi[k], 16));
     }
     // the old spheres' box: recompute on lanes 16.. only when the obstacle moved earlier in this batch
     double os[6];
@@ -272,8 +282,8 @@ __global__ void pose_kernel(Store s, Batch b) {
             }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            os[k] = fmin(bo[k], olo[k]);
-            os[3 + k] = fmax(bo[3 + k], ohi[k]);
+            os[k] = fmin(bo[k], widen_lo(olo[k]));
+            os[3 + k] = fmax(bo[3 + k], widen_hi(ohi[k]));
         }
     }
     // the binning boxes first: the bin kernel starts on them (Batch::evready)
@@ -1083,7 +1093,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
         if (count == 0) continue;  // warp-uniform: clean cell
         const int c = c0 + lane, t = c - cell * s.cell;
         const bool valid = c < s.Np;
-        double aabb[6];
+        double aabb[6], sbox[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) sbox[j] = s.slice_aabb[6 * static_cast<size_t>(q) + j];
         int seg_lo = 0, seg_hi = 0;
         if (valid) {
             const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
@@ -1111,9 +1123,18 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
                 }
             }
             __syncwarp();
+            // the chunk's events whose new or old box meets the slice's box: the cell's list
+            // is coarser than a slice, and the other events touch none of its components
+            bool near = false;
+            if (lane < m) {
+                const double* bx = sbx[32 * wi + lane];
+                near = rggd::overlaps(sbox, bx) | rggd::overlaps(sbox, bx + 6);
+            }
+            const uint32_t smask = __ballot_sync(0xffffffffu, near);
             uint32_t tm = 0, bm = 0, sm = 0;
             if (valid) {
-                for (int k = 0; k < m; ++k) {
+                for (uint32_t x = smask; x; x &= x - 1) {
+                    const int k = __ffs(x) - 1;
                     const double* bx = sbx[32 * wi + k];
                     const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
                     tm |= static_cast<uint32_t>(touch) << k;

@@ -50,6 +50,7 @@ struct Store {
     const double* spline_r;    // B*S
     const int32_t* orig;       // Np: sorted -> component id
     const double* cell_aabb;   // ncells*6
+    const double* slice_aabb;  // ceil(Np/32)*6: union box of each 32-component slice (touch's event filter)
     // uniform grid over the cells (binning): bin (x, y, z) = floor((p - gorg) * ginv) clamped
     // to [0, gdim); the cells whose box overlaps bin g are gcell[gcell_off[g] .. gcell_off[g+1])
     double gorg[3], ginv[3];
@@ -158,12 +159,17 @@ cudaError_t launch_eager_step(const Batch& b, int32_t* ids0, double* rt0, const 
 // arrays of rgg_layout_view; outputs are preallocated except `seg`.
 struct StoreIn {
     int32_t N, B, S, T, np, cell, shards, shard_rank;
-    const double* comp_aabb;  // host N*6
-    const double* edge_sat;   // host N*B*21
+    const double* comp_aabb;  // N*6 (device when `device`, else host)
+    const double* edge_sat;   // N*B*21 (idem)
     const int32_t* row_off;   // host N*B*S+1
-    const double* segs;       // host T*7
+    const double* segs;       // T*7 (idem)
     const double* spline;     // host B*S
+    bool device = false;               // comp_aabb, edge_sat, segs are device arrays
+    const int32_t* row_off_dev = nullptr;  // device copy of row_off when `device`
 };
+// sat_prep / component AABBs / seg_prep of raw components on the device (rgg_store.cu)
+cudaError_t prep_components(const double* corners, int N, int B, const double* pts, int T, double* sat21,
+                            double* aabb, double* segs7, cudaStream_t st);
 struct StoreOut {
     double2* aabb;         // 3*np
     double* sat;           // np*B*22
@@ -175,6 +181,7 @@ struct StoreOut {
     int32_t* orig;         // np
     int32_t* rank;         // N
     double* cell_aabb;     // ncells*6
+    double* slice_aabb;    // ceil(np/32)*6
     int32_t total_segs;
 };
 cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st);

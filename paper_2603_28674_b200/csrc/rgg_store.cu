@@ -195,20 +195,28 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
     const int N = in.N, B = in.B, BS = in.B * in.S, np = in.np, cell = in.cell;
     const long long nrows = static_cast<long long>(np) * BS;
     const int ncells = (np + cell - 1) / cell;
-    // 1. raw inputs
+    // 1. raw inputs (host arrays uploaded here, or device arrays the caller prepared:
+    // rgg_gpu_create_from_components runs sat_prep / seg_prep on the device)
     double *aabb = nullptr, *sat21 = nullptr, *segs7 = nullptr;
     int32_t* row_off = nullptr;
-    SCK(scratch.alloc(&aabb, static_cast<size_t>(N) * 6));
-    SCK(scratch.alloc(&sat21, static_cast<size_t>(N) * B * 21));
-    SCK(scratch.alloc(&row_off, static_cast<size_t>(N) * BS + 1));
-    SCK(scratch.alloc(&segs7, static_cast<size_t>(in.T) * 7));
-    // pageable sources: plain synchronous copies (the driver pipelines them through
-    // its staging buffers; async pageable copies on a non-blocking stream were slower)
     SCK(cudaStreamSynchronize(st));
-    SCK(cudaMemcpy(aabb, in.comp_aabb, static_cast<size_t>(N) * 6 * 8, cudaMemcpyHostToDevice));
-    SCK(cudaMemcpy(sat21, in.edge_sat, static_cast<size_t>(N) * B * 21 * 8, cudaMemcpyHostToDevice));
-    SCK(cudaMemcpy(row_off, in.row_off, (static_cast<size_t>(N) * BS + 1) * 4, cudaMemcpyHostToDevice));
-    if (in.T) SCK(cudaMemcpy(segs7, in.segs, static_cast<size_t>(in.T) * 7 * 8, cudaMemcpyHostToDevice));
+    if (in.device) {
+        aabb = const_cast<double*>(in.comp_aabb);
+        sat21 = const_cast<double*>(in.edge_sat);
+        row_off = const_cast<int32_t*>(in.row_off_dev);
+        segs7 = const_cast<double*>(in.segs);
+    } else {
+        SCK(scratch.alloc(&aabb, static_cast<size_t>(N) * 6));
+        SCK(scratch.alloc(&sat21, static_cast<size_t>(N) * B * 21));
+        SCK(scratch.alloc(&row_off, static_cast<size_t>(N) * BS + 1));
+        SCK(scratch.alloc(&segs7, static_cast<size_t>(in.T) * 7));
+        // pageable sources: plain synchronous copies (the driver pipelines them through
+        // its staging buffers; async pageable copies on a non-blocking stream were slower)
+        SCK(cudaMemcpy(aabb, in.comp_aabb, static_cast<size_t>(N) * 6 * 8, cudaMemcpyHostToDevice));
+        SCK(cudaMemcpy(sat21, in.edge_sat, static_cast<size_t>(N) * B * 21 * 8, cudaMemcpyHostToDevice));
+        SCK(cudaMemcpy(row_off, in.row_off, (static_cast<size_t>(N) * BS + 1) * 4, cudaMemcpyHostToDevice));
+        if (in.T) SCK(cudaMemcpy(segs7, in.segs, static_cast<size_t>(in.T) * 7 * 8, cudaMemcpyHostToDevice));
+    }
     SCK(cudaMemcpy(out.spline, in.spline, static_cast<size_t>(BS) * 8, cudaMemcpyHostToDevice));
     // 2. Morton order
     unsigned long long *bounds = nullptr, *key = nullptr, *key2 = nullptr;
@@ -251,9 +259,54 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
         segs_kernel<<<static_cast<unsigned>((nrows + T256 - 1) / T256), T256, 0, st>>>(
             out.orig, nrows, BS, row_off, out.row, segs7, out.spline, out.seg, out.seg32);
     if (ncells > 0) cell_box_kernel<<<(ncells + 127) / 128, 128, 0, st>>>(out.aabb, np, cell, ncells, out.cell_aabb);
+    const int nslices = (np + 31) / 32;
+    if (nslices > 0) cell_box_kernel<<<(nslices + 127) / 128, 128, 0, st>>>(out.aabb, np, 32, nslices, out.slice_aabb);
     SCK(cudaGetLastError());
     SCK(cudaStreamSynchronize(st));
     return cudaSuccess;
+}
+
+// The serialize step on the device (batch_layout.cpp:55-62, 80-105, 132-146): per
+// (component, body) sat_prep of the OBB corners (kernels_scalar.cpp:7-30) and the
+// component AABB as the union of the bodies' corner boxes (aabb_of_obb,
+// geometry.cpp:205-213); per real segment seg_prep (kernels_scalar.cpp:71-79).
+__global__ void prep_boxes_kernel(const double* corners, int N, int B, double* sat21, double* aabb) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    double box[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int b = 0; b < B; ++b) {
+        const double* p = corners + (static_cast<size_t>(c) * B + b) * 24;
+        double cs[24];
+        for (int k = 0; k < 24; ++k) cs[k] = p[k];
+        rggd::sat_prep(cs, sat21 + (static_cast<size_t>(c) * B + b) * 21);
+        for (int i = 0; i < 8; ++i)
+            for (int k = 0; k < 3; ++k) {
+                box[k] = fmin(box[k], cs[3 * i + k]);
+                box[3 + k] = fmax(box[3 + k], cs[3 * i + k]);
+            }
+    }
+    for (int k = 0; k < 6; ++k) aabb[6 * static_cast<size_t>(c) + k] = box[k];
+}
+
+__global__ void prep_segs_kernel(const double* pts, int T, double* segs7) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const double* p = pts + 6 * static_cast<size_t>(t);
+    double* q = segs7 + 7 * static_cast<size_t>(t);
+    double d[3];
+    for (int j = 0; j < 3; ++j) {
+        q[j] = p[j];
+        d[j] = __dsub_rn(p[3 + j], p[j]);
+        q[3 + j] = d[j];
+    }
+    q[6] = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
+}
+
+cudaError_t prep_components(const double* corners, int N, int B, const double* pts, int T, double* sat21,
+                            double* aabb, double* segs7, cudaStream_t st) {
+    if (N > 0) prep_boxes_kernel<<<(N + 127) / 128, 128, 0, st>>>(corners, N, B, sat21, aabb);
+    if (T > 0) prep_segs_kernel<<<(T + 255) / 256, 256, 0, st>>>(pts, T, segs7);
+    return cudaGetLastError();
 }
 
 // A uniform grid over the cell boxes (host side: a few thousand cells).  Bins are

@@ -47,6 +47,14 @@ class _View(C.Structure):
                 ("obst_sph_local", C.c_void_p), ("obst_sph_r", C.c_void_p), ("obst_sph_n", C.c_void_p)]
 
 
+class _CompView(C.Structure):
+    _fields_ = [("n_components", C.c_int32), ("n_bodies", C.c_int32), ("n_slots", C.c_int32),
+                ("n_obstacles", C.c_int32), ("max_spheres", C.c_int32), ("obb_corners", C.c_void_p),
+                ("row_off", C.c_void_p), ("seg_points", C.c_void_p), ("spline_radius", C.c_void_p),
+                ("obst_he", C.c_void_p), ("obst_sph_local", C.c_void_p), ("obst_sph_r", C.c_void_p),
+                ("obst_sph_n", C.c_void_p)]
+
+
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int32), ("use_under", C.c_int32), ("cell_size", C.c_int32),
                 ("cell_capacity", C.c_int32), ("allow_wide", C.c_int32), ("shard_rank", C.c_int32),
@@ -94,6 +102,7 @@ def library() -> C.CDLL:
         L = C.CDLL(LIB_PATH)
         vp, ip, i32 = C.c_void_p, C.POINTER(C.c_int32), C.c_int32
         L.rgg_gpu_create.argtypes = [C.POINTER(_View), C.POINTER(_Options), C.POINTER(vp)]
+        L.rgg_gpu_create_from_components.argtypes = [C.POINTER(_CompView), C.POINTER(_Options), C.POINTER(vp)]
         L.rgg_gpu_destroy.argtypes = [vp]
         L.rgg_gpu_destroy.restype = None
         L.rgg_gpu_last_error.argtypes = [vp]
@@ -154,7 +163,7 @@ def _fast():
     return _fastmod
 
 
-EXPORTED = ["rgg_gpu_create", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_update", "rgg_gpu_update_device",
+EXPORTED = ["rgg_gpu_create", "rgg_gpu_create_from_components", "rgg_gpu_destroy", "rgg_gpu_last_error", "rgg_gpu_update", "rgg_gpu_update_device",
             "rgg_gpu_sync", "rgg_gpu_count", "rgg_gpu_read_states", "rgg_gpu_read_bits", "rgg_gpu_unknown_count",
             "rgg_gpu_gray_ids", "rgg_gpu_last_hits", "rgg_gpu_write_states", "rgg_gpu_pair_masks",
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
@@ -258,9 +267,15 @@ def _pose12(pose) -> np.ndarray:
 
 class GpuEngine:
     def __init__(self, layout, use_under: bool = True, cell_size: int = 0, cell_capacity: int = 64,
-                 allow_wide: bool | None = None, device: int = 0, shard_rank: int = 0, shard_count: int = 1):
+                 allow_wide: bool | None = None, device: int = 0, shard_rank: int = 0, shard_count: int = 1,
+                 components: bool = False):
+        """layout: the serialized store (LayoutView, or anything with its names).  With
+        components=True it is the raw components instead (attributes N, B, S, M, C,
+        e_plus = OBB corners N*B x 24, row_off, seg_pts = real segment end points T x 6,
+        spline_r and the obstacle arrays): rgg_gpu_create_from_components runs the
+        serialize step on the device."""
         L = library()
-        lv = layout if isinstance(layout, LayoutView) else LayoutView.from_any(layout)
+        lv = layout if components or isinstance(layout, LayoutView) else LayoutView.from_any(layout)
         keep = {}
 
         def arr(name, dt, shape=None):
@@ -268,14 +283,21 @@ class GpuEngine:
             keep[name] = a
             return a.ctypes.data
 
-        view = _View(lv.N, lv.B, lv.S, lv.M, lv.C, arr("edge_sat", np.float64), arr("comp_aabb", np.float64),
-                     arr("row_off", np.int32), arr("segs", np.float64), arr("spline_r", np.float64),
-                     arr("obst_he", np.float64), arr("obst_sph_local", np.float64), arr("obst_sph_r", np.float64),
-                     arr("obst_sph_n", np.int32))
         wide = lv.M > 64 if allow_wide is None else allow_wide
         opts = _Options(device, int(use_under), cell_size, cell_capacity, int(wide), shard_rank, shard_count)
         h = C.c_void_p()
-        rc = L.rgg_gpu_create(C.byref(view), C.byref(opts), C.byref(h))
+        if components:
+            cview = _CompView(lv.N, lv.B, lv.S, lv.M, lv.C, arr("e_plus", np.float64), arr("row_off", np.int32),
+                              arr("seg_pts", np.float64), arr("spline_r", np.float64), arr("obst_he", np.float64),
+                              arr("obst_sph_local", np.float64), arr("obst_sph_r", np.float64),
+                              arr("obst_sph_n", np.int32))
+            rc = L.rgg_gpu_create_from_components(C.byref(cview), C.byref(opts), C.byref(h))
+        else:
+            view = _View(lv.N, lv.B, lv.S, lv.M, lv.C, arr("edge_sat", np.float64), arr("comp_aabb", np.float64),
+                         arr("row_off", np.int32), arr("segs", np.float64), arr("spline_r", np.float64),
+                         arr("obst_he", np.float64), arr("obst_sph_local", np.float64),
+                         arr("obst_sph_r", np.float64), arr("obst_sph_n", np.int32))
+            rc = L.rgg_gpu_create(C.byref(view), C.byref(opts), C.byref(h))
         self._h = h
         if rc != RGG_OK:
             msg = L.rgg_gpu_last_error(h).decode()

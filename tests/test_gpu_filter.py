@@ -204,3 +204,125 @@ def test_sat_filter_adversarial_update_path(origin):
     exp = oracle.sat_batch(boxes, np.arange(N, dtype=np.int32), osat).astype(bool)
     assert 0 < exp.sum() < N
     assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
+
+
+def _aabb_of(cs):
+    p = cs.reshape(8, 3)
+    return np.concatenate([p.min(0), p.max(0)])
+
+
+def test_aabb_near_contact_through_update():
+    """Candidate semantics at rounding level.  The reference tests
+    every grid candidate with the fp64 SAT (engine_batch.cpp:55-74); the GPU tests the
+    pairs whose closed AABBs overlap after widening the obstacle's boxes by a relative
+    2^-40 (rgg_kernels.cu pose_kernel).  Boxes are placed at the fp64 SAT contact
+    distance and a few ulps either side, along world axes (face contact: the AABB gap
+    and the SAT margin round independently), so some pairs have disjoint AABBs while the
+    fp64 SAT still reports an intersection.  Through the whole update path the labels
+    must equal the all-pairs fp64 SAT verdicts (everything in one reference grid cell)."""
+    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+
+    rng = np.random.default_rng(11)
+    boxes, aabbs, exp = [], [], []
+    disjoint_hits = 0
+    for trial in range(400):
+        he_o = rng.uniform(0.2, 2.0, 3)
+        Ro = np.eye(3) if trial % 2 else rot(rng)
+        c_o = rng.uniform(-50, 50, 3)
+        pose = np.concatenate([Ro.reshape(-1), c_o])
+        osat, oaabb, _, _ = oracle.obstacle_operands(he_o, np.zeros((1, 3)), 1, 1e-3, pose)
+        he = rng.uniform(0.05, 2.0, 3)
+        k = trial % 3
+        n = np.zeros(3)
+        n[k] = 1.0 if trial % 4 < 2 else -1.0
+        R = np.eye(3)
+        lo, hi = 0.0, 20.0
+        for _ in range(100):
+            mid = 0.5 * (lo + hi)
+            s = oracle.sat_prep(corners(c_o + mid * n, R, he))
+            lo, hi = (mid, hi) if oracle.sat_boxes(s, osat) else (lo, mid)
+        t = lo
+        for step in range(-3, 4):
+            cs = corners(c_o + t * n, R, he)
+            s = oracle.sat_prep(cs)
+            a = _aabb_of(cs)
+            hit = bool(oracle.sat_boxes(s, osat))
+            ov = bool(np.all(a[:3] <= oaabb[3:]) and np.all(oaabb[:3] <= a[3:]))
+            disjoint_hits += hit and not ov
+            boxes.append((s, a, pose, he_o, hit))
+            t = np.nextafter(t, 100.0) if step >= 0 else t
+        for _ in range(3):
+            t = np.nextafter(t, 100.0)
+            cs = corners(c_o + t * n, R, he)
+            s = oracle.sat_prep(cs)
+            boxes.append((s, _aabb_of(cs), pose, he_o, bool(oracle.sat_boxes(s, osat))))
+    # one engine per obstacle pose: every component against obstacle 0
+    by_pose = {}
+    for s, a, pose, he_o, hit in boxes:
+        by_pose.setdefault(pose.tobytes(), (pose, he_o, []))[2].append((s, a, hit))
+    bad = 0
+    for pose, he_o, items in by_pose.values():
+        N = len(items)
+        lv = LayoutView(N=N, B=1, S=1, M=1, C=1, edge_sat=np.array([s for s, _, _ in items]),
+                        comp_aabb=np.array([a for _, a, _ in items]), row_off=np.zeros(N + 1, np.int32),
+                        segs=np.zeros((0, 7)), spline_r=np.zeros(1), obst_he=he_o[None, :],
+                        obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.array([1e-3]),
+                        obst_sph_n=np.ones(1, np.int32))
+        eng = GpuEngine(lv, use_under=False)
+        eng.update_obstacle(0, pose)
+        got = eng.states()
+        want = np.array([2 if hit else 0 for _, _, hit in items], np.uint8)
+        bad += int(np.sum(got != want))
+    print(f"pairs {len(boxes)}, AABB-disjoint fp64-SAT hits {disjoint_hits}")
+    assert bad == 0, f"{bad} labels differ from the all-pairs fp64 SAT ({disjoint_hits} AABB-disjoint hits)"
+
+
+def test_non_orthonormal_satboxes_take_the_exact_path():
+    """the fp32 SAT filter's form equals the reference's margins only
+    for orthonormal frames with e_k = |e_k| u_k.  Caller-supplied SatBoxes that are
+    sheared, have non-unit axes or axes misaligned with their extents are flagged at
+    rgg_gpu_create (Box32::degen) and decided by the fp64 reference sequence: the verdicts
+    equal the oracle's on every pair, near contact included."""
+    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+
+    rng = np.random.default_rng(5)
+    he_o = np.array([1.1, 0.6, 0.8])
+    pose = np.concatenate([rot(rng).reshape(-1), [0.2, 0.1, -0.3]])
+    osat, _, _, _ = oracle.obstacle_operands(he_o, np.zeros((1, 3)), 1, 0.1, pose)
+    boxes = []
+    for trial in range(400):
+        R = rot(rng)
+        he = rng.uniform(0.1, 1.5, 3)
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        lo, hi = 0.0, 10.0
+        for _ in range(60):
+            mid = 0.5 * (lo + hi)
+            s = oracle.sat_prep(corners(pose[9:] + mid * d, R, he))
+            lo, hi = (mid, hi) if oracle.sat_boxes(s, osat) else (lo, mid)
+        s = oracle.sat_prep(corners(pose[9:] + lo * (1 + rng.uniform(-1e-6, 1e-6)) * d, R, he)).copy()
+        kind = trial % 3
+        if kind == 0:  # sheared frame: u_1 tilted towards u_0, e_1 along it
+            u1 = s[15:18] + 1e-4 * s[12:15]
+            s[15:18] = u1 / np.linalg.norm(u1)
+            s[6:9] = s[15:18] * np.linalg.norm(s[6:9])
+        elif kind == 1:  # axis not unit length
+            s[12:15] *= 1 + 1e-6
+        else:  # extent not along its axis
+            s[3:6] += 1e-7 * s[15:18]
+        boxes.append(s)
+    boxes = np.array(boxes)
+    N = len(boxes)
+    lv = LayoutView(N=N, B=1, S=1, M=1, C=1, edge_sat=boxes,
+                    comp_aabb=np.tile([-1e9, -1e9, -1e9, 1e9, 1e9, 1e9], (N, 1)).astype(np.float64),
+                    row_off=np.zeros(N + 1, np.int32), segs=np.zeros((0, 7)), spline_r=np.zeros(1),
+                    obst_he=he_o[None, :], obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.array([0.1]),
+                    obst_sph_n=np.ones(1, np.int32))
+    eng = GpuEngine(lv)
+    eng.filter_stats(reset=True)
+    eng.update_obstacle(0, pose)
+    got = eng.batch_over(np.arange(N, dtype=np.int32), 0)
+    exp = oracle.sat_batch(boxes, np.arange(N, dtype=np.int32), osat)
+    assert 0 < exp.sum() < N
+    assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
+    assert eng.filter_stats()["sat_rechecks"] >= N, "flagged boxes must take the fp64 path"

@@ -265,3 +265,29 @@ def test_no_obstacles(eng_mod):
     with pytest.raises(ValueError, match="unknown obstacle id"):
         eng.batch_update((np.zeros(1, np.int32), g["rts"][:1]))
     assert not np.any(eng.states())
+
+
+@pytest.mark.parametrize("scn", ["quick_smoke", "table4_obstacles_1000_5x", "table5_manipulator_100"])
+def test_create_from_components_equals_layout(eng_mod, scn):
+    """rgg_gpu_create_from_components (serialize on the device: sat_prep, AABBs, seg_prep
+    from the OBB corners and real spline points) builds the same engine as
+    rgg_gpu_create from the reference's serialized layout: every report, label and bit
+    word equal after the scenario's moves."""
+    import os
+
+    from conftest import GOLDEN
+    from oracle import ref
+
+    w = ref.World.from_scn(open(os.path.join(GOLDEN, "scenarios", scn + ".scn")).read())
+    lay = w.layout()
+    ids, rts = w.moves()
+    a = eng_mod.GpuEngine(eng_mod.LayoutView.from_any(lay), allow_wide=True)
+    b = eng_mod.GpuEngine(lay, components=True, allow_wide=True)
+    ra = a.batch_update((ids, rts)).counts()
+    rb = b.batch_update((ids, rts)).counts()
+    assert np.array_equal(ra, rb)
+    assert np.array_equal(a.states(), b.states())
+    assert np.array_equal(a.obstacle_bits(), b.obstacle_bits())
+    ref_eng = ref.Engine(w, kind=0, threads=1)
+    ref_eng.run(ids, rts)
+    assert np.array_equal(b.states(), ref_eng.states())
