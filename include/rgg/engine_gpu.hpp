@@ -25,7 +25,9 @@
 // cell-sorted component blocks of rgg_gpu_create).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -33,6 +35,7 @@
 #include <vector>
 
 #include "rgg/batch_layout.hpp"
+#include "rgg/geometry.hpp"
 #include "rgg/roadmap.hpp"
 #include "rgg/robot.hpp"
 #include "rgg/update_report.hpp"
@@ -44,56 +47,97 @@ class GpuEngine {
 public:
     GpuEngine(const ComponentSet& components, Scene& scene, EngineOptions options = {}, int cell_capacity = 1024,
               int device = 0, bool allow_wide = false)
-        : components_(&components), scene_(scene), options_(options),
-          layout_(BatchLayout::serialize(components, scene.obstacles)) {
+        : components_(&components), scene_(scene), options_(options) {
         if (scene.obstacles.size() > 64 && !allow_wide)
             throw std::invalid_argument("obstacle bitsets support at most 64 obstacles");
-        // CSR view of the padded layout: real segments only (seg_count per row)
-        const size_t rows = layout_.seg_count.size();
-        row_off_.assign(rows + 1, 0);
-        for (size_t r = 0; r < rows; ++r) row_off_[r + 1] = row_off_[r] + layout_.seg_count[r];
-        segs_.resize(static_cast<size_t>(row_off_[rows]) * 7);
-        for (size_t r = 0, at = 0; r < rows; ++r)
-            for (std::int32_t k = 0; k < layout_.seg_count[r]; ++k, ++at) {
-                const kern::SegPrep& s = layout_.seg_prep[r * layout_.max_segments + k];
-                double* d = &segs_[at * 7];
-                for (int j = 0; j < 3; ++j) d[j] = s.a[j], d[3 + j] = s.d[j];
-                d[6] = s.dd;
+        // The component view (include/rgg_gpu.h rgg_component_view): the serialize step's
+        // inputs only (OBB corners, the real segments' end points in CSR rows, slot radii);
+        // sat_prep, the AABBs and seg_prep run on the device.  The padded BatchLayout
+        // (BatchLayout::serialize, batch_layout.cpp:21-146) is built only if layout() is called.
+        const int N = components.count();
+        const int B = static_cast<int>(components.spheres.per_body.size());
+        const int K = components.max_segments;
+        // slot layout: spheres per body x the worst split factor (batch_layout.cpp:28-43)
+        int max_parts = 1, max_spheres = 1;
+        for (int b = 0; b < B; ++b)
+            max_spheres = std::max(max_spheres, static_cast<int>(components.spheres.per_body[b].size()));
+        for (const EdgeGeometry& g : components.geometry)
+            for (int b = 0; b < B; ++b) {
+                std::vector<int> parts(components.spheres.per_body[b].size(), 0);
+                for (const Spline& s : g.under[b]) max_parts = std::max(max_parts, ++parts[s.sphere_index]);
             }
-        edge_sat_.resize(layout_.edge_sat.size() * 21);
-        for (size_t i = 0; i < layout_.edge_sat.size(); ++i) {
-            const kern::SatBox& b = layout_.edge_sat[i];
-            double* d = &edge_sat_[i * 21];
-            for (int j = 0; j < 3; ++j) d[j] = b.center[j];
-            for (int k = 0; k < 3; ++k)
-                for (int j = 0; j < 3; ++j) d[3 + 3 * k + j] = b.e[k][j], d[12 + 3 * k + j] = b.u[k][j];
+        const int S = max_spheres * max_parts;
+        n_components_ = N;
+        corners_.resize(static_cast<size_t>(N) * B * 24);
+        spline_r_.assign(static_cast<size_t>(B) * S, 0.0);
+        std::vector<std::int32_t> count(static_cast<size_t>(N) * B * S, 0);
+        std::vector<const Spline*> row_spline(count.size(), nullptr);
+        for (int c = 0; c < N; ++c) {
+            const EdgeGeometry& g = components.geometry[c];
+            for (int b = 0; b < B; ++b) {
+                const ObbCorners oc = obb_corners(g.over[b]);  // write_corners, batch_layout.cpp:10-17
+                double* d = &corners_[(static_cast<size_t>(c) * B + b) * 24];
+                for (int i = 0; i < 8; ++i) d[3 * i] = oc[i].x, d[3 * i + 1] = oc[i].y, d[3 * i + 2] = oc[i].z;
+                std::vector<int> used(components.spheres.per_body[b].size(), 0);
+                for (const Spline& s : g.under[b]) {  // batch_layout.cpp:64-105
+                    if (s.segment_count() > K)
+                        throw std::logic_error("spline exceeds the segment cap; the build policy should have split it");
+                    const int slot = s.sphere_index * max_parts + used[s.sphere_index]++;
+                    double& slot_radius = spline_r_[static_cast<size_t>(b) * S + slot];
+                    if (slot_radius == 0.0) slot_radius = s.radius;
+                    else if (slot_radius != s.radius) throw std::logic_error("inconsistent spline radius for a layout slot");
+                    const size_t row = (static_cast<size_t>(c) * B + b) * S + slot;
+                    row_spline[row] = &s;
+                    count[row] = s.points.size() == 1 ? 1 : static_cast<std::int32_t>(s.points.size()) - 1;
+                }
+            }
         }
-        comp_aabb_.resize(static_cast<size_t>(layout_.n_components) * 6);
-        for (int c = 0; c < layout_.n_components; ++c) {
-            const Aabb& a = layout_.component_aabb[c];
-            const double v[6] = {a.min.x, a.min.y, a.min.z, a.max.x, a.max.y, a.max.z};
-            for (int j = 0; j < 6; ++j) comp_aabb_[6 * c + j] = v[j];
+        row_off_.assign(count.size() + 1, 0);
+        for (size_t r = 0; r < count.size(); ++r) row_off_[r + 1] = row_off_[r] + count[r];
+        seg_pts_.resize(static_cast<size_t>(row_off_.back()) * 6);
+        for (size_t r = 0; r < count.size(); ++r) {
+            const Spline* s = row_spline[r];
+            if (!s) continue;
+            double* d = &seg_pts_[static_cast<size_t>(row_off_[r]) * 6];
+            const size_t np = s->points.size();
+            for (size_t p = 0; p < (np == 1 ? 1 : np - 1); ++p, d += 6) {  // one degenerate segment for a point
+                const Vec3& a = s->points[p];
+                const Vec3& e = s->points[np == 1 ? p : p + 1];
+                d[0] = a.x, d[1] = a.y, d[2] = a.z, d[3] = e.x, d[4] = e.y, d[5] = e.z;
+            }
         }
-        const int M = layout_.n_obstacles, C = layout_.n_spheres;
+        // obstacle side (batch_layout.cpp:108-131)
+        const int M = static_cast<int>(scene.obstacles.size());
+        int C = 1;
+        for (const ObstacleModel& o : scene.obstacles) C = std::max(C, static_cast<int>(o.inner.size()));
         obst_he_.resize(static_cast<size_t>(M) * 3);
         obst_sl_.assign(static_cast<size_t>(M) * C * 3, 0.0);
+        obst_r_.assign(M, 0.0);
+        obst_n_.assign(M, 0);
         for (int o = 0; o < M; ++o) {
             const ObstacleModel& m = scene.obstacles[o];
+            for (const Sphere& s : m.inner)
+                if (s.radius != m.inner[0].radius)
+                    throw std::invalid_argument("layout requires one shared sphere radius per obstacle");
             obst_he_[3 * o] = m.half_extents.x, obst_he_[3 * o + 1] = m.half_extents.y, obst_he_[3 * o + 2] = m.half_extents.z;
             for (size_t s = 0; s < m.inner.size(); ++s) {
                 double* d = &obst_sl_[(static_cast<size_t>(o) * C + s) * 3];
                 d[0] = m.inner[s].center.x, d[1] = m.inner[s].center.y, d[2] = m.inner[s].center.z;
             }
+            obst_r_[o] = m.inner.empty() ? 0.0 : m.inner[0].radius;
+            obst_n_[o] = static_cast<std::int32_t>(m.inner.size());
         }
-        rgg_layout_view v{layout_.n_components, layout_.n_bodies, layout_.n_slots, M, C, edge_sat_.data(),
-                          comp_aabb_.data(), row_off_.data(), segs_.data(), layout_.spline_radius.data(),
-                          obst_he_.data(), obst_sl_.data(), layout_.o_minus_r.data(), layout_.o_sphere_count.data()};
+        rgg_component_view v{N, B, S, M, C, corners_.data(), row_off_.data(), seg_pts_.data(), spline_r_.data(),
+                             obst_he_.data(), obst_sl_.data(), obst_r_.data(), obst_n_.data()};
         rgg_gpu_options opt{};
         opt.device = device;
         opt.use_under = options.use_under ? 1 : 0;
-        opt.cell_capacity = cell_capacity < 1 ? 1 : (cell_capacity > 256 ? 256 : cell_capacity);
+        // the reference's cell_capacity bounds a SpatialGrid cell's inline components before
+        // its overflow list (spatial_grid.cpp:94-110); here it bounds a cell's inline event
+        // slots before the overflow pool.  Either way only storage changes, never a result.
+        opt.cell_capacity = cell_capacity < 1 ? 1 : cell_capacity;
         opt.allow_wide = allow_wide ? 1 : 0;
-        const int rc = rgg_gpu_create(&v, &opt, &h_);
+        const int rc = rgg_gpu_create_from_components(&v, &opt, &h_);
         if (rc != RGG_OK) {
             const std::string msg = rgg_gpu_last_error(h_);
             rgg_gpu_destroy(h_);
@@ -101,8 +145,12 @@ public:
             raise(rc, msg);
         }
         rgg_gpu_count(h_, nullptr, nullptr, &words_);
-        states_.assign(layout_.n_components, ValidityState::Valid);
-        bits_.assign(static_cast<size_t>(layout_.n_components) * words_, 0);
+        states_.assign(n_components_, ValidityState::Valid);
+        bits_.assign(static_cast<size_t>(n_components_) * words_, 0);
+        // the host buffers are not needed any more (the engine copied them into HBM)
+        std::vector<double>().swap(corners_);
+        std::vector<double>().swap(seg_pts_);
+        std::vector<std::int32_t>().swap(row_off_);
     }
 
     ~GpuEngine() { rgg_gpu_destroy(h_); }
@@ -171,7 +219,15 @@ public:
         check(rgg_gpu_unknown_count(h_, &n));
         return n;
     }
-    const BatchLayout& layout() const { return layout_; }
+    // The reference's serialized layout, built on first use (the engine itself never
+    // reads it): obstacle rows at the Scene's current poses, which this engine keeps
+    // equal to the moved obstacles' poses, as the reference's update_transforms does.
+    // Scribbling into its padding (test_batch.cpp:248-256) cannot change a GPU mask:
+    // the device store holds the real segments only.
+    const BatchLayout& layout() const {
+        if (!layout_) layout_ = std::make_unique<BatchLayout>(BatchLayout::serialize(*components_, scene_.obstacles));
+        return *layout_;
+    }
     int words_per_component() const { return words_; }
 
     void batch_over(const std::vector<ComponentId>& candidates, ObstacleId o, std::vector<std::uint8_t>& mask) {
@@ -262,9 +318,10 @@ private:
     const ComponentSet* components_;
     Scene& scene_;
     EngineOptions options_;
-    BatchLayout layout_;
-    std::vector<double> edge_sat_, comp_aabb_, segs_, obst_he_, obst_sl_;
-    std::vector<std::int32_t> row_off_;
+    mutable std::unique_ptr<BatchLayout> layout_;
+    int n_components_ = 0;
+    std::vector<double> corners_, seg_pts_, spline_r_, obst_he_, obst_sl_, obst_r_;
+    std::vector<std::int32_t> row_off_, obst_n_;
     rgg_gpu* h_ = nullptr;
     std::int32_t words_ = 1;
     mutable bool stale_ = false;

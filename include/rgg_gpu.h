@@ -103,7 +103,7 @@ typedef struct rgg_component_view {
 typedef struct rgg_gpu_options {
     int32_t device;        /* CUDA ordinal (one process per GPU) */
     int32_t use_under;     /* EngineOptions::use_under (update_report.hpp:43-46) */
-    int32_t cell_size;     /* components per cell (0 -> 128; multiple of 32, <= 256) */
+    int32_t cell_size;     /* components per cell (0 -> 128; a multiple of 32, <= 128) */
     int32_t cell_capacity; /* inline event slots per cell before overflow (0 -> 64) */
     int32_t allow_wide;    /* accept M > 64 (bitsets become ceil(M/64) words) */
     int32_t shard_rank;    /* this handle owns cells c with c % shard_count == shard_rank */
@@ -228,7 +228,8 @@ int rgg_gpu_pair_masks(rgg_gpu* h, int32_t kind, const int32_t* cand, int32_t n,
 typedef struct rgg_gpu_stats {
     float pose_ms, bin_ms, classify_ms, compact_ms, total_ms;
     int32_t dirty_cells, events, overflow_cells;
-    int64_t over_pairs, sat_flops, under_pairs, seg_sphere_tests, over_hits, under_hits;
+    int64_t over_pairs, sat_flops, under_pairs, seg_sphere_tests, over_hits;
+    int64_t under_hits;       /* (pair, segment) items with a hit */
     int64_t bytes_components; /* algorithmic bytes of the dirty components, fp64 records */
     int64_t bytes_fp32;       /* algorithmic bytes in SURVEY.md §8(d)'s fp32 model */
     int64_t gray;             /* GRAY components after the update */

@@ -820,8 +820,8 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
 // Eager batch, chained on the device: per move one single-move graph (pose ..
 // apply + exact resolve of the move's gray over-hits) and one staging kernel;
 // one H2D of all moves before and one D2H of all report slots after.  A single
-// move lists at most one event per cell, so its item queues (>= Np) and pools
-// cannot overflow: no per-move host check is needed.
+// move lists at most one event per cell, so its item queues (sized below) and
+// pools cannot overflow: no per-move host check is needed.
 static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n, int32_t flags,
                         rgg_update_report* reports) {
     CK(cudaSetDevice(h->device));
@@ -834,8 +834,11 @@ static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int3
         if (rc) return rc;
         rc = grow_pinned(h, k);
         if (rc) return rc;
-        if (h->items_cap < h->s.Np) {
-            rc = grow_items(h, h->s.Np);
+        // a single move queues at most one over item per component and one under item per
+        // segment: queues this large cannot fill during an eager batch
+        const int64_t need = std::max<int64_t>(h->s.Np, h->total_segs_owned);
+        if (h->items_cap < need) {
+            rc = grow_items(h, need);
             if (rc) return rc;
         }
         if (k > h->eager_cap) {

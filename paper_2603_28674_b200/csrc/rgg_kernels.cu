@@ -923,8 +923,9 @@ __device__ __forceinline__ const int32_t* rec_list(int4 r) {
 
 // The narrow tests of all items, GPU-wide (persistent grid), one thread per
 // item.  Over items {component, event, result word, bit}: the 15-axis SAT per
-// body.  Under items {first segment, end segment, result word, event << 5 | bit}:
-// the component's real segments against the event's spheres.  COUNT: the
+// body.  Under items {segment, the pair's first segment, result word, event << 5 | bit}:
+// one real segment of the component against the event's spheres (a pair's segments
+// OR their verdicts into the same bit).  COUNT: the
 // reference's operation census (rgg_gpu_census) instead of the verdicts.
 template <bool COUNT>
 __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
@@ -953,14 +954,14 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
                     prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
                     prefetch_l1(&b.ev[nx.y].b32);
                 } else {
-                    for (int j = nx.x; j < nx.y; j += 4) prefetch_l1(s.seg32 + 2 * static_cast<size_t>(j));
+                    prefetch_l1(s.seg32 + 2 * static_cast<size_t>(nx.x));
                     prefetch_l1(b.evs + kEvS * static_cast<size_t>(nx.w >> 5));
                 }
             }
             if (i < n_over) {
                 if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
-            } else if (under_range32(s, it.x, it.y, b.evs + kEvS * static_cast<size_t>(it.w >> 5), b.ev[it.w >> 5])) {
-                atomicOr(&b.mpool[it.z], 1u << (it.w & 31));
+            } else if (under_range32(s, it.x, it.x + 1, b.evs + kEvS * static_cast<size_t>(it.w >> 5), b.ev[it.w >> 5])) {
+                atomicOr(&b.mpool[it.z], 1u << (it.w & 31));  // a pair's segments OR into one bit
             }
             it = nx;
             nx = nn;
@@ -975,10 +976,10 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
         const bool h = over_test<true>(s, it.x, b.ev[it.y], &c_sat);
         c_op += s.B, c_oh += h;
     }
-    for (int i = gt; i < n_under; i += nthreads) {
+    for (int i = gt; i < n_under; i += nthreads) {  // per (pair, segment) items: pairs = first segments
         const int4 it = b.items_under[i];
-        const bool h = under_range<true>(s, it.x, it.y, b.ev[it.w >> 5], 0, 1, &c_tests);
-        c_up += 1, c_uh += h;
+        const bool h = under_range<true>(s, it.x, it.x + 1, b.ev[it.w >> 5], 0, 1, &c_tests);
+        c_up += it.x == it.y, c_uh += h;
     }
     long long v[6] = {c_op, c_sat, c_up, c_tests, c_oh, c_uh};
 #pragma unroll
@@ -1169,8 +1170,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             // a full queue is reported through ctr[6] = 3 (the apply kernel then applies nothing)
             int at, atu;
             {
+                // under work is queued per (pair, segment): the narrow threads then test one
+                // segment each, so a pair's segment count no longer diverges a warp
                 const unsigned long long mine = static_cast<unsigned long long>(__popc(bm)) |
-                                                (static_cast<unsigned long long>(__popc(sm)) << 32);
+                                                (static_cast<unsigned long long>(__popc(sm) * (seg_hi - seg_lo)) << 32);
                 unsigned long long x = mine;
                 for (int off = 1; off < 32; off <<= 1) {
                     const unsigned long long y = __shfl_up_sync(0xffffffffu, x, off);
@@ -1189,10 +1192,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
                 else b.ctr[6] = 3;
             }
             at = atu;
-            for (uint32_t x = sm; x; x &= x - 1, ++at) {
+            for (uint32_t x = sm; x; x &= x - 1) {
                 const int k = __ffs(x) - 1;
-                if (at < b.items_cap) b.items_under[at] = make_int4(seg_lo, seg_hi, wu, (sev[wi][k] << 5) | k);
-                else b.ctr[6] = 3;
+                const int w4 = (sev[wi][k] << 5) | k;
+                for (int j = seg_lo; j < seg_hi; ++j, ++at) {  // {segment, the pair's first segment, word, event|bit}
+                    if (at < b.items_cap) b.items_under[at] = make_int4(j, seg_lo, wu, w4);
+                    else b.ctr[6] = 3;
+                }
             }
             __syncwarp();
         }
