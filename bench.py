@@ -714,8 +714,10 @@ def main():
     value = N * args.steps / (total_ms * 1e-3)
     e2e_value = N * args.steps / e2e_total
     per_update = total_ms / args.steps
-    roof = roofline(census, statistics.mean(kern_ms), world,
-                    os.path.join(ROOT, "profiles", "r2_c5_ncu.json") if args.config == "c5" else None)
+    import glob
+
+    prof = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r2*_{args.config}_ncu.json")))
+    roof = roofline(census, statistics.mean(kern_ms), world, prof[-1] if prof else None)
     line = {
         "metric": BASE_METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": per_update, "higher_is_better": True, "scaling": "strong",

@@ -48,6 +48,9 @@ int rgg_built_export(const rgg_built* b, double* edge_sat, double* comp_aabb, in
                      double* spline_r, double* obb15);
 void rgg_built_free(rgg_built* b);
 const char* rgg_build_last_error(void);
+/* CUDA devices visible to the producer (0 without a GPU): the GPU box fit
+ * (RGG_BUILD_GPU_FIT) is the Python producer's default when this is positive. */
+int rgg_build_gpu_count(void);
 /* obstacle_inner_spheres (proj/src/swept.cpp:23-49): count centres (count*3) and the radius. */
 int rgg_obstacle_spheres(const double* he3, int32_t count, double* centres, double* radius);
 

@@ -429,3 +429,12 @@ int rggp_fit_finish(void* p, double* out, const InnerSpec* spec, InnerOut* inner
     rggp_fit_end(f);
     return e;
 }
+
+extern "C" int rgg_build_gpu_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
