@@ -1039,11 +1039,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
     // list, so a cell with many events spreads over several warps.  The census
     // walks every slice with all its chunks.
     const int spc = s.cell >> 5;  // slices per cell
-    // a dense update (at least half the cells listed) walks every slice with all its chunks:
-    // the slice's cell record, its operands and (speculatively, for lists of at most 32
-    // inline events) its list entries then come in one round trip, without a unit record
-    const bool dense = CENSUS || (!flow && 2 * b.ctr[0] >= s.ncells);
-    const int n_units = dense ? nslices : min(b.ctr[10], b.units_cap) * spc;
+    const int n_units = CENSUS ? nslices : min(b.ctr[10], b.units_cap) * spc;
     const int gen = flow ? reinterpret_cast<volatile int32_t*>(b.evready)[4] : 0;
     // flow: slice-units are taken one at a time from a counter, and a unit is used once
     // its stamp is this update's generation; the list ends when every bin warp is done
@@ -1083,7 +1079,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
          u = flow ? take() : u + gridDim.x * kWarpsPerCta) {
         int q = u, w_first = 0, w_last = 1 << 30;
         int4 rec;
-        if (!dense) {
+        if (!CENSUS) {
             const int4 un = b.units[u / spc];  // {cell, chunk, count, mask base}
             q = un.x * spc + u % spc;
             w_first = un.y;
@@ -1093,11 +1089,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
         const int c0 = q << 5;
         if (c0 >= s.Np) continue;
         const int cell = c0 / s.cell;
-        int spec_e = 0;
-        if (dense) {
-            rec = b.crec[cell];
-            if (!CENSUS && lane < min(32, s.cap)) spec_e = b.cell_list[static_cast<size_t>(cell) * s.cap + lane];
-        }
+        if (CENSUS) rec = b.crec[cell];
         const int count = rec.x;
         if (count == 0) continue;  // warp-uniform: clean cell
         const int c = c0 + lane, t = c - cell * s.cell;
@@ -1120,7 +1112,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
         for (int w = w_first; w < min(W, w_last); ++w) {
             const int base = 32 * w;
             const int m = min(32, count - base);
-            const int myev = lane < m ? (dense && !CENSUS && count <= 32 && count <= s.cap ? spec_e : list[base + lane]) : 0;
+            const int myev = lane < m ? list[base + lane] : 0;
             sev[wi][lane] = myev;
             if (lane < m) {
                 const double2* src = reinterpret_cast<const double2*>(b.evt + 24 * static_cast<size_t>(myev));
@@ -1303,28 +1295,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
             label = s.state_c[c];
         }
         int4 rec = make_int4(0, 0, 0, 0);
-        // speculative first chunk, in the same round trip as the cell record: a cell of at
-        // most 32 (and at most cap) listed events keeps its list in its inline slots and its
-        // masks at the start of its fixed mask block (W = 1); longer lists load again below
-        const int32_t* inl = b.cell_list + static_cast<size_t>(cell) * s.cap;
-        const int mb1 = cell * 3 * s.cell * b.cmask_words;
-        int spec_e = 0;
-        uint32_t spec_m[3] = {0u, 0u, 0u};
         if (!skip) {
             if (dirty_only) {
-                const int32_t* lst = un.z <= s.cap ? inl : b.pool + b.cell_ovf[cell];
+                const int32_t* lst =
+                    un.z <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap : b.pool + b.cell_ovf[cell];
                 const unsigned long long la = reinterpret_cast<unsigned long long>(lst);
                 rec = make_int4(un.z, un.w, static_cast<int>(la & 0xffffffffu), static_cast<int>(la >> 32));
             } else {
                 rec = b.crec[cell];
             }
-            if (lane < min(32, s.cap)) spec_e = inl[lane];
-            if (valid)
-#pragma unroll
-                for (int j = 0; j < 3; ++j) spec_m[j] = b.mpool[mb1 + j * s.cell + t];
         }
         const int count = rec.x;
-        const bool spec = count <= 32 && count <= s.cap;
         oc = cw & 0xffff;
         bc = cw >> 16;
         const int label0 = label;
@@ -1336,11 +1317,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
         for (int base = 0, w = 0; base < count; base += 32, ++w) {
             const int m = min(32, count - base);
             if (lane < m) {  // list entries are move indices; the event of move e moves obstacle ids[e]
-                const int e = spec ? spec_e : list[base + lane];
+                const int e = list[base + lane];
                 som[wi][lane] = make_int2(staged ? s_ids[e] : b.ids[e], e);
             }
-            uint32_t tm = spec_m[0], ro = spec_m[1], ru = spec_m[2];
-            if (valid && !spec) {
+            uint32_t tm = 0, ro = 0, ru = 0;
+            if (valid) {
                 tm = b.mpool[rec.y + (0 * W + w) * s.cell + t];
                 ro = b.mpool[rec.y + (1 * W + w) * s.cell + t];
                 ru = b.mpool[rec.y + (2 * W + w) * s.cell + t];
