@@ -687,7 +687,7 @@ def main():
         t0 = time.perf_counter()
         if dist is None:
             reps = eng_e2e.batch_update((ids_h[it], rts_h[it]), per_move=True, gray_list=True)
-            gray = eng_e2e.gray_ids()
+            gray = eng_e2e.gray_ids_view()  # one DMA into the engine's pinned host buffer
         else:
             ids_t = torch.from_numpy(ids_h[it]).pin_memory().to(dev, non_blocking=True)
             rts_t = torch.from_numpy(rts_h[it]).pin_memory().to(dev, non_blocking=True)
@@ -728,7 +728,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": 1e3 * e2e_total / args.steps,
                 "h2d_bytes_per_step": m_step * (4 + 96), "d2h_bytes_per_step": int(statistics.mean(d2h)),
                 "path": "GpuEngine.batch_update(host moves, per-move reports, gray list) -> rgg_gpu_update, then "
-                        "gray_ids() D2H" + (" ; N>1: pinned H2D on every rank, DistributedUpdater (broadcast, "
+                        "gray_ids_view() (rgg_gpu_gray_view: the gray ids DMA'd into pinned host memory)" + (" ; N>1: pinned H2D on every rank, DistributedUpdater (broadcast, "
                                             "all-reduce, gray gather), reports + gray ids D2H on rank 0"
                                             if world > 1 else "")},
         "gpu_launches": 8 * args.steps,

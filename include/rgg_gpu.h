@@ -173,6 +173,9 @@ int rgg_gpu_gray_ids(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);
  * first cap ids into d_ids (entries past the count are unspecified).  Compacts the
  * current labels first unless the last update ran with RGG_GRAY_LIST. */
 int rgg_gpu_gray_device(rgg_gpu* h, int32_t* d_count, int32_t* d_ids, int32_t cap);
+/* The same list copied into a handle-owned pinned host buffer (one DMA, no staging):
+ * *ids points at n ascending ids, valid until the next call on this handle. */
+int rgg_gpu_gray_view(rgg_gpu* h, const int32_t** ids, int32_t* n);
 /* Components over-hit by the last move of the last update that are still GRAY
  * (the over_hits the reference resolves in eager mode, engine_batch.cpp:193-200). */
 int rgg_gpu_last_hits(rgg_gpu* h, int32_t* out, int32_t cap, int32_t* n);

@@ -141,6 +141,8 @@ struct rgg_gpu {
     int grid_classify = 1;
     int64_t total_segs_owned = 0;
     bool poisoned = false;  // a failed eager batch left a partial state (rgg_gpu_update fails from then on)
+    int32_t* h_gray = nullptr;  // pinned host copy of the gray list (rgg_gpu_gray_view)
+    int32_t gray_pin_cap = 0;
 };
 
 namespace {
@@ -784,7 +786,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr, h->h_eg_rep};
+    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr, h->h_eg_rep, h->h_gray};
     for (void* p : pin)
         if (p) cudaFreeHost(p);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
@@ -1124,6 +1126,34 @@ int rgg_gpu_gray_device(rgg_gpu* h, int32_t* d_count, int32_t* d_ids, int32_t ca
     const int32_t n = std::min(cap, h->s.N);
     if (n > 0) CK(cudaMemcpyAsync(d_ids, h->d_gray, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                   h->stream));
+    return RGG_OK;
+}
+
+int rgg_gpu_gray_view(rgg_gpu* h, const int32_t** ids, int32_t* n) {
+    if (!h || !ids || !n) return RGG_EINVAL;
+    CK(cudaSetDevice(h->device));
+    if (!h->gray_fresh) {
+        CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
+        h->gray_fresh = true;
+    }
+    const int rc = refresh_unknown(h);
+    if (rc) return rc;
+    const int32_t cnt = h->unknown;
+    if (cnt > h->gray_pin_cap) {
+        cudaFreeHost(h->h_gray);
+        h->h_gray = nullptr;
+        h->gray_pin_cap = 0;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_gray), static_cast<size_t>(std::max(cnt, 1)) * sizeof(int32_t),
+                         cudaHostAllocDefault));
+        h->gray_pin_cap = std::max(cnt, 1);
+    }
+    if (cnt > 0) {
+        CK(cudaMemcpyAsync(h->h_gray, h->d_gray, static_cast<size_t>(cnt) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                           h->stream));
+        CK(stream_wait(h));
+    }
+    *ids = h->h_gray;
+    *n = cnt;
     return RGG_OK;
 }
 

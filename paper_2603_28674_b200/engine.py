@@ -132,6 +132,7 @@ def library() -> C.CDLL:
         L.rgg_exact_valid_sets.argtypes = [i32, i32, vp, i32, vp, vp, i32, vp, vp, vp]
         L.rgg_gpu_filter_stats.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), i32]
         L.rgg_gpu_gray_device.argtypes = [vp, vp, vp, i32]
+        L.rgg_gpu_gray_view.argtypes = [vp, C.POINTER(C.POINTER(C.c_int32)), ip]
         L.rgg_gpu_fp32_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
         L.rgg_gpu_owned.argtypes = [vp, ip]
         _lib = L
@@ -169,7 +170,7 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_create_from_components", "rgg_gpu_destroy
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
             "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
             "rgg_gpu_exact_check", "rgg_gpu_filter_stats", "rgg_gpu_set_active_obstacles",
-            "rgg_exact_valid_sets", "rgg_gpu_gray_device", "rgg_gpu_fp32_peak", "rgg_gpu_owned"]
+            "rgg_exact_valid_sets", "rgg_gpu_gray_device", "rgg_gpu_fp32_peak", "rgg_gpu_owned", "rgg_gpu_gray_view"]
 
 
 @dataclass
@@ -485,6 +486,8 @@ class GpuEngine:
         int32 tensor (1,), ordered before the current torch stream's later work."""
         import torch
 
+        # the engine stream writes `out`: order it after the current stream's use of that memory
+        self._torch_stream(out.device).wait_stream(torch.cuda.current_stream(out.device))
         self._check(library().rgg_gpu_gray_device(self._h, C.c_void_p(out.data_ptr()), C.c_void_p(0), 0))
         torch.cuda.current_stream(out.device).wait_stream(self._torch_stream(out.device))
 
@@ -493,6 +496,7 @@ class GpuEngine:
         on the engine stream, ordered before the current torch stream's later work."""
         import torch
 
+        self._torch_stream(out.device).wait_stream(torch.cuda.current_stream(out.device))
         self._check(library().rgg_gpu_gray_device(self._h, C.c_void_p(0), C.c_void_p(out.data_ptr()), int(cap)))
         torch.cuda.current_stream(out.device).wait_stream(self._torch_stream(out.device))
 
@@ -560,6 +564,18 @@ class GpuEngine:
         if n.value:
             self._check(library().rgg_gpu_gray_ids(self._h, out.ctypes.data, n.value, C.byref(n)))
         return out
+
+    def gray_ids_view(self) -> np.ndarray:
+        """The GRAY ids (ascending) as a read-only view of the engine's pinned host buffer:
+        one DMA, no copy; valid until the next call on this engine."""
+        p = C.POINTER(C.c_int32)()
+        n = C.c_int32()
+        self._check(library().rgg_gpu_gray_view(self._h, C.byref(p), C.byref(n)))
+        if n.value == 0:
+            return np.zeros(0, np.int32)
+        v = np.ctypeslib.as_array(p, shape=(n.value,))
+        v.flags.writeable = False
+        return v
 
     def last_hits(self) -> np.ndarray:
         n = C.c_int32()

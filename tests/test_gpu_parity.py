@@ -70,6 +70,7 @@ def test_replay_one_batch(eng_mod, name):
     st = g["snap_states"][-1]
     assert eng.unknown_count() == int(np.sum(st == 2))
     assert np.array_equal(eng.gray_ids(), np.nonzero(st == 2)[0].astype(np.int32))
+    assert np.array_equal(eng.gray_ids_view(), np.nonzero(st == 2)[0].astype(np.int32))
     allc = np.arange(int(g["N"]), dtype=np.int32)
     o = int(g["mask_obstacle"])
     assert np.array_equal(eng.batch_over(allc, o), g["masks"][0])
