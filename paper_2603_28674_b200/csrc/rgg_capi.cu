@@ -532,12 +532,16 @@ extern "C" int rgg_gpu_create_from_components(const rgg_component_view* cv, cons
     if (!cv) return fail(h, RGG_EINVAL, "null component view");
     const int32_t N = cv->n_components, B = cv->n_bodies, S = cv->n_slots;
     if (N < 0 || B < 1 || S < 1) return fail(h, RGG_EINVAL, "malformed component view");
+    if (!cv->row_off || !cv->spline_radius || (N > 0 && !cv->obb_corners) ||
+        (cv->n_obstacles > 0 && (!cv->obst_he || !cv->obst_sph_r || !cv->obst_sph_n)))
+        return fail(h, RGG_EINVAL, "null array in the component view");
     const int64_t nrows = static_cast<int64_t>(N) * B * S;
     if (cv->row_off[0] != 0) return fail(h, RGG_ELOGIC, "row_off must start at 0");
     for (int64_t r = 0; r < nrows; ++r)
         if (cv->row_off[r + 1] < cv->row_off[r]) return fail(h, RGG_ELOGIC, "row_off must be non-decreasing");
     const int64_t T = cv->row_off[nrows];
     if (T > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
+    if (T > 0 && !cv->seg_points) return fail(h, RGG_EINVAL, "null array in the component view");
     rgg_gpu_options o{};
     if (opts) o = *opts;
     clear_stale_error();
@@ -579,6 +583,9 @@ int create_impl(rgg_gpu* h, const rgg_layout_view* v, const rgg_gpu_options* opt
     if (opts) o = *opts;
     const int32_t N = v->n_components, B = v->n_bodies, S = v->n_slots, M = v->n_obstacles, C = v->max_spheres;
     if (N < 0 || B < 1 || S < 1 || M < 0 || C < 0) return fail(h, RGG_EINVAL, "malformed layout view");
+    if (!v->row_off || !v->spline_radius || (!dev && N > 0 && (!v->edge_sat || !v->comp_aabb)) ||
+        (M > 0 && (!v->obst_he || !v->obst_sph_r || !v->obst_sph_n || (C > 0 && !v->obst_sph_local))))
+        return fail(h, RGG_EINVAL, "null array in the layout view");
     if (M > 64 && !o.allow_wide) return fail(h, RGG_EINVAL, "obstacle bitsets support at most 64 obstacles");
     if (C > rggk::kMaxSpheres) return fail(h, RGG_EINVAL, "too many spheres per obstacle (max 16)");
     if (M > 0xfffe) return fail(h, RGG_EINVAL, "too many obstacles");
@@ -630,6 +637,7 @@ int create_impl(rgg_gpu* h, const rgg_layout_view* v, const rgg_gpu_options* opt
     h->words = M <= 64 ? 1 : (M + 63) / 64;
     const int64_t T = v->row_off[nrows];
     if (T > INT32_MAX) return fail(h, RGG_ELOGIC, "too many segments");
+    if (!dev && T > 0 && !v->segs) return fail(h, RGG_EINVAL, "null array in the layout view");
     CK(dalloc(&h->d_aabb, static_cast<size_t>(Np) * 3));
     CK(dalloc(&h->d_sat, static_cast<size_t>(Np) * B * 22));
     CK(dalloc(&h->d_sat32, static_cast<size_t>(Np) * B));

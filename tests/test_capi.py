@@ -50,3 +50,21 @@ def test_create_without_gpu_fails_loudly():
                            obst_sph_n=np.ones(1, np.int32))
     with pytest.raises(RuntimeError):
         engine.GpuEngine(lv)
+
+
+def test_null_views_are_rejected_before_any_device_work():
+    """Argument errors come back as RGG_EINVAL with a message on any host (no GPU needed)."""
+    import ctypes as C
+
+    from paper_2603_28674_b200 import engine
+
+    L = engine.library()
+    h = C.c_void_p()
+    cv = engine._CompView(4, 1, 1, 0, 1)  # every array null
+    assert L.rgg_gpu_create_from_components(C.byref(cv), None, C.byref(h)) == engine.RGG_EINVAL
+    assert b"null array" in L.rgg_gpu_last_error(h)
+    L.rgg_gpu_destroy(h)
+    v = engine._View(4, 1, 1, 0, 1)
+    assert L.rgg_gpu_create(C.byref(v), None, C.byref(h)) == engine.RGG_EINVAL
+    assert b"null array" in L.rgg_gpu_last_error(h)
+    L.rgg_gpu_destroy(h)
