@@ -791,8 +791,8 @@ def main():
                     line["extra"][cfg] = measure_c1(local)
                 elif cfg == "c3":  # fixed-capacity overflow: 16 inline slots per cell
                     line["extra"][cfg] = measure_extra(cfg, args.seed, local, cell_capacity=16, parity=True)
-                else:
-                    line["extra"][cfg] = measure_extra(cfg, args.seed, local)
+                else:  # c2, c4: parity against the oracle too
+                    line["extra"][cfg] = measure_extra(cfg, args.seed, local, parity=True)
             except Exception as ex:  # keep the headline line even if an extra config fails
                 line["extra"][cfg] = {"error": str(ex)[:300]}
         try:
