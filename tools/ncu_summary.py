@@ -53,7 +53,7 @@ out = {"source": f"ncu --set full --clock-control none, {src}, {rep.split('/')[-
        "note": "ncu flushes caches before each kernel and serialises them: durations are cold-cache, and "
                "operands a kernel reads that its predecessor left in L2 are re-read from DRAM here"}
 json.dump(out, open(f"profiles/{name}_ncu.json", "w"), indent=1)
-if len(sys.argv) > 3:
+if len(sys.argv) > 3 and sys.argv[3]:
     shutil.copy(sys.argv[3], f"profiles/{name}_launches.csv")
 for k in kernels:
     print(f"{k['kernel'][:40]:40s} {k.get('duration_us', 0):7.2f} us  dram {k.get('dram_read_bytes', 0) / 1e6:6.2f} MB  "
