@@ -124,6 +124,7 @@ struct rgg_gpu {
     int32_t words = 1;
     int32_t last_n = 0;
     int32_t last_flags = 0;
+    bool last_single = false;  // the last update took the single-move path (no cell lists)
     bool last_hits_valid = false;
     int32_t unknown = 0;
     bool unknown_stale = false;
@@ -372,6 +373,15 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     int kf = 0;
     if (flags & RGG_PER_MOVE) kf |= rggk::kPerMove;
     if (n == 1) kf |= rggk::kHits;
+    // single moves (update_obstacle, eager): dirty cells straight from the move's boxes and
+    // one fused touch + narrow + transition kernel (rggk::launch_single); the census keeps
+    // the batched path, whose cell lists and item queues it counts
+    static const bool no_single = std::getenv("RGG_NO_SINGLE") != nullptr;
+    const bool single = n == 1 && !b.census_on && !no_single;
+    const auto classify = [&]() {
+        return single ? rggk::launch_single(h->s, b, kf, h->stream)
+                      : rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
+    };
     static const bool debug = std::getenv("RGG_DEBUG_PHASES") != nullptr;
     auto phase = [&](const char* name) -> int {
         if (!debug) return RGG_OK;
@@ -430,9 +440,9 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
                                     h->stream);
             if (e == cudaSuccess) e = rggk::launch_pose(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[1]);
-            if (e == cudaSuccess) e = rggk::launch_bin(h->s, b, h->stream);
+            if (e == cudaSuccess && !single) e = rggk::launch_bin(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[2]);
-            if (e == cudaSuccess) e = rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
+            if (e == cudaSuccess) e = classify();
             if (e == cudaSuccess && out_in_kernel) e = rggk::launch_host_out(b, h->stream);
             if (e == cudaSuccess && eager) e = resolve_hits();
             if (e == cudaSuccess) e = rec(h->ev[3]);
@@ -457,6 +467,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         h->gray_fresh = gray_list;
         h->last_n = n;
         h->last_flags = flags;
+        h->last_single = single;
         h->last_hits_valid = n == 1 && !eager;
         h->timed = true;
         h->unknown_stale = true;
@@ -466,10 +477,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     CK(rggk::launch_pose(h->s, b, h->stream));
     if (phase("pose")) return RGG_ECUDA;
     CK(cudaEventRecord(h->ev[1], h->stream));
-    CK(rggk::launch_bin(h->s, b, h->stream));
+    if (!single) CK(rggk::launch_bin(h->s, b, h->stream));
     if (phase("bin")) return RGG_ECUDA;
     CK(cudaEventRecord(h->ev[2], h->stream));
-    CK(rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream));
+    CK(classify());
     if (phase("classify")) return RGG_ECUDA;
     if (eager) CK(resolve_hits());
     CK(cudaEventRecord(h->ev[3], h->stream));
@@ -478,6 +489,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     h->gray_fresh = gray_list;
     h->last_n = n;
     h->last_flags = flags;
+    h->last_single = single;
     h->last_hits_valid = n == 1 && !eager;
     h->timed = true;
     h->unknown_stale = true;
@@ -1372,6 +1384,8 @@ int rgg_gpu_last_stats(rgg_gpu* h, rgg_gpu_stats* out) {
 int rgg_gpu_census(rgg_gpu* h, rgg_gpu_stats* out) {
     if (!h || !out) return RGG_EINVAL;
     if (h->last_n <= 0) return fail(h, RGG_EINVAL, "no update to count");
+    if (h->last_single)
+        return fail(h, RGG_EINVAL, "a single-move update keeps no cell lists to count: update with RGG_CENSUS");
     CK(cudaSetDevice(h->device));
     int rc = rgg_gpu_last_stats(h, out);
     if (rc) return rc;

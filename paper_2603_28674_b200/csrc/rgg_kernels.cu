@@ -185,6 +185,10 @@ __global__ void pose_kernel(Store s, Batch b) {
     // moves straight from mapped host memory (synchronous host updates) or from HBM
     const int32_t* mids = b.src_ids ? b.src_ids : b.ids;
     const double* mrt = b.src_ids ? b.src_rt : b.rt;
+    const double* rt_new = mrt + 12 * static_cast<size_t>(i);
+    double rtl[12];  // the move's pose does not depend on its id: both loads in flight together
+#pragma unroll
+    for (int k = 0; k < 12; ++k) rtl[k] = rt_new[k];
     const int o = mids[i];
     // prev / last links: the same obstacle moved earlier / later in this batch
     int p = -1;
@@ -198,12 +202,11 @@ __global__ void pose_kernel(Store s, Batch b) {
         if (after) is_last = false;
     }
     const double he[3] = {s.ohe[3 * o], s.ohe[3 * o + 1], s.ohe[3 * o + 2]};
-    const double* rt_new = mrt + 12 * static_cast<size_t>(i);
+    const double cu = lane < 6 ? s.cur_union[6 * o + lane] : 0.0;  // the old union box when p < 0
     const double* rt_old = p >= 0 ? mrt + 12 * static_cast<size_t>(p) : rt_new;
-    const double* rt = lane < 8 ? rt_new : (lane < 16 ? rt_old : rt_new);
-    double rtl[12];
+    if (p >= 0 && lane >= 8 && lane < 16)  // lanes 8-15 place the old corners
 #pragma unroll
-    for (int k = 0; k < 12; ++k) rtl[k] = rt[k];
+        for (int k = 0; k < 12; ++k) rtl[k] = rt_old[k];
     // corners (lanes 0-15) and sphere centres (lanes 16-31)
     const int nsph = s.osn[o];
     const double r = s.osr[o];
@@ -290,7 +293,7 @@ __global__ void pose_kernel(Store s, Batch b) {
     double nu6 = 0.0, ol6 = 0.0;
     if (lane < 6) {
         nu6 = lane < 3 ? fmin(bn[lane], bs[lane]) : fmax(bn[lane], bs[lane]);
-        ol6 = p >= 0 ? os[lane] : s.cur_union[6 * o + lane];
+        ol6 = p >= 0 ? os[lane] : cu;
         b.evbox[12 * static_cast<size_t>(i) + lane] = nu6;  // compact copy for the binning
         b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol6;
     }
@@ -351,10 +354,16 @@ __global__ void pose_kernel(Store s, Batch b) {
         double* et = b.evt + 24 * static_cast<size_t>(i);
         et[lane] = nu6, et[6 + lane] = ol6, et[12 + lane] = bn[lane], et[18 + lane] = bs[lane];
     }
-    if (lane < 12) ev.rt[lane] = rt_new[lane];
+    double rtk = 0.0;  // the new pose's element k on lane k (lane 0 holds it in registers)
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const double v = shfl(rtl[k], 0);
+        if (lane == k) rtk = v;
+    }
+    if (lane < 12) ev.rt[lane] = rtk;
     if (b.src_ids) {  // the HBM copy the later kernels (and a replay) read
         if (lane == 0) const_cast<int32_t*>(b.ids)[i] = o;
-        if (lane < 12) const_cast<double*>(b.rt)[12 * static_cast<size_t>(i) + lane] = rt_new[lane];
+        if (lane < 12) const_cast<double*>(b.rt)[12 * static_cast<size_t>(i) + lane] = rtk;
     }
     if (lane >= 16 && lane - 16 < nsph) {
         ev.cen[3 * (lane - 16)] = pt[0];
@@ -402,6 +411,23 @@ __global__ void init_obstacles_kernel(Store s) {
     aabb_union(e.box, e.sph, e.nu);
     aabb_empty(e.old);
     aabb_empty(s.cur_union + 6 * o);
+}
+
+// Commit the moved obstacles' operands for the next batch (s.cur, s.cur_union):
+// one 16-byte word per thread over the whole grid.  Nothing between the pose
+// kernel and the end of the update reads s.cur / s.cur_union.
+__device__ __forceinline__ void commit_grid(const Store& s, const Batch& b) {
+    constexpr int kVec = sizeof(Event) / 16 + 1;  // + the 6-double union box
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int w = gt; w < b.n * kVec; w += gridDim.x * blockDim.x) {
+        const int i = w / kVec, k = w % kVec;
+        if (!b.last[i]) continue;
+        const int o = b.ids[i];
+        if (k < kVec - 1)
+            reinterpret_cast<int4*>(&s.cur[o])[k] = reinterpret_cast<const int4*>(&b.ev[i])[k];
+        else
+            for (int j = 0; j < 6; ++j) s.cur_union[6 * o + j] = b.ev[i].nu[j];
+    }
 }
 
 // ------------------------------------------------------------------ binning
@@ -894,23 +920,6 @@ __device__ __forceinline__ void prefetch_range(const void* a, const void* e, boo
 // event) pair whose boxes overlap; narrow evaluates every item with the whole
 // GPU and ORs the verdicts into the result words; apply replays each
 // component's events in move order from the three words.
-
-// Commit the moved obstacles' operands for the next batch (s.cur, s.cur_union):
-// one 16-byte word per thread over the whole grid.  Nothing between the pose
-// kernel and the end of the update reads s.cur / s.cur_union.
-__device__ __forceinline__ void commit_grid(const Store& s, const Batch& b) {
-    constexpr int kVec = sizeof(Event) / 16 + 1;  // + the 6-double union box
-    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-    for (int w = gt; w < b.n * kVec; w += gridDim.x * blockDim.x) {
-        const int i = w / kVec, k = w % kVec;
-        if (!b.last[i]) continue;
-        const int o = b.ids[i];
-        if (k < kVec - 1)
-            reinterpret_cast<int4*>(&s.cur[o])[k] = reinterpret_cast<const int4*>(&b.ev[i])[k];
-        else
-            for (int j = 0; j < 6; ++j) s.cur_union[6 * o + j] = b.ev[i].nu[j];
-    }
-}
 
 // the moved obstacles' operands, alone (a store without components)
 __global__ void commit_kernel(Store s, Batch b) { commit_grid(s, b); }
@@ -1455,6 +1464,114 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) apply_warp_kernel(Store s, 
     tl_stop(b.tl, 4, t0);
 }
 
+// Single-move updates (n == 1: update_obstacle and every eager move): one kernel after
+// the pose kernel, no binning, cell lists, work units or item queues.  CTA b tests the
+// cells b, b + G, b + 2G, ... (one per thread; a move's dirty cells are neighbours in
+// Morton order, so the stride spreads them over the CTAs) against the move's new and old
+// union boxes, then runs every hit cell with one thread per component: touch, both
+// narrow tests and the reference's transition for the one event (engine_batch.cpp:114-188).
+// The per-move counters gather in shared memory; the gray over-hits are listed for the
+// eager resolve.
+template <int FLAGS, bool WIDE>
+__global__ void __launch_bounds__(kMaxCell) single_cells_kernel(Store s, Batch b) {
+    constexpr bool HITS = (FLAGS & kHits) != 0;
+    constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
+    const int tid = threadIdx.x, lane = tid & 31, T = blockDim.x;
+    // the first round's cell boxes are static: loaded while the pose kernel runs
+    double q0[6];
+    {
+        const long long k = blockIdx.x + static_cast<long long>(gridDim.x) * tid;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) q0[j] = k < s.ncells ? s.cell_aabb[6 * k + j] : 0.0;
+    }
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double sbx[24];  // the event's new union, old union, box, sphere box
+    __shared__ int s_mv[4], s_cells[kMaxCell], s_n;
+    if (tid < 24) sbx[tid] = b.evt[tid];
+    if (tid < 4) s_mv[tid] = 0;
+    if (tid == 0) s_n = 0;
+    if (b.evready && blockIdx.x == 0 && tid < 4) b.evready[tid] = 0;  // for the next update
+    commit_grid(s, b);  // s.cur / s.cur_union: read by the next update's pose kernel only
+    __syncthreads();
+    const Event& ev = b.ev[0];
+    const int o = ev.o;
+    const unsigned long long bit = 1ull << (o & 63);
+    int dgray = 0;
+    for (int r0 = 0; blockIdx.x + static_cast<long long>(gridDim.x) * r0 < s.ncells; r0 += T) {
+        const long long k = blockIdx.x + static_cast<long long>(gridDim.x) * (r0 + tid);
+        if (k < s.ncells) {
+            double q[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) q[j] = r0 == 0 ? q0[j] : s.cell_aabb[6 * k + j];
+            if (rggd::overlaps(q, sbx) | rggd::overlaps(q, sbx + 6)) s_cells[atomicAdd(&s_n, 1)] = static_cast<int>(k);
+        }
+        __syncthreads();
+        const int nh = s_n;
+        for (int h = 0; h < nh; ++h) {
+            const int c = s_cells[h] * s.cell + tid;
+            if (c >= s.Np) continue;
+            const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
+            const double aabb[6] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y};
+            const bool touch = rggd::overlaps(aabb, sbx) | rggd::overlaps(aabb, sbx + 6);
+            if (!touch) continue;
+            const bool box = rggd::overlaps(aabb, sbx + 12);
+            const bool sph = s.use_under && rggd::overlaps(aabb, sbx + 18);
+            const size_t widx = WIDE ? static_cast<size_t>(o >> 6) * s.Np + c : static_cast<size_t>(c);
+            const int id = s.orig[c];
+            const uint32_t cw = s.cnt[c];
+            const int label0 = s.state_c[c];
+            const unsigned long long ow = s.over[widx], uw = s.under[widx];
+            const bool n_over = box && over_test<false>(s, c, ev, nullptr);
+            bool n_under = false;
+            if (sph) {
+                const int rows = s.B * s.S;
+                n_under = under_range32(s, s.row[c * rows], s.row[(c + 1) * rows], b.evs, ev);
+            }
+            int oc = cw & 0xffff, bc = cw >> 16, label = label0;
+            const bool old_over = (ow & bit) != 0, old_under = (uw & bit) != 0;
+            if (old_over) {  // revalidate_old_intersections (engine_batch.cpp:114-143)
+                oc -= 1;
+                const int rest = bc - (old_under ? 1 : 0);
+                label = oc == 0 ? 0 : ((s.use_under && rest > 0) ? 1 : 2);
+            }
+            if (n_over) {  // over phase (engine_batch.cpp:163-177)
+                if (label == 0) label = 2;
+                oc += 1;
+            }
+            if (n_under) label = 1;  // under phase (engine_batch.cpp:181-188)
+            bc += (n_over && n_under ? 1 : 0) - (old_over && old_under ? 1 : 0);
+            const unsigned long long nw = n_over ? (ow | bit) : (ow & ~bit);
+            const unsigned long long nuw = n_under ? (uw | bit) : (uw & ~bit);
+            if (nw != ow) s.over[widx] = nw;
+            if (nuw != uw) s.under[widx] = nuw;
+            const uint32_t cwn = static_cast<uint32_t>(oc) | (static_cast<uint32_t>(bc) << 16);
+            if (cwn != cw) s.cnt[c] = cwn;
+            if (label != label0) {  // finish_counts (engine_batch.cpp:41-53)
+                s.state[id] = static_cast<uint8_t>(label);
+                s.state_c[c] = static_cast<uint8_t>(label);
+                dgray += (label == 2) - (label0 == 2);
+                if (PER_MOVE) {
+                    atomicAdd(&s_mv[label], 1);
+                    if (label0 == 2) atomicAdd(&s_mv[3], 1);
+                }
+            }
+            if (HITS && n_over && label == 2) {
+                const int at = atomicAdd(&b.ctr[5], 1);
+                b.hits[at] = id;
+                b.hits_prev[at] = static_cast<uint8_t>(label0);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) s_n = 0;
+        __syncthreads();
+    }
+    for (int off = 16; off; off >>= 1) dgray += __shfl_down_sync(0xffffffffu, dgray, off);
+    if (lane == 0 && dgray) atomicAdd(b.unknown, dgray);
+    __syncthreads();
+    if (PER_MOVE && tid < 4 && s_mv[tid]) atomicAdd(&b.mv[tid], s_mv[tid]);
+}
+
 // Synchronous host updates: the per-move counters and the status block straight
 // into mapped pinned host memory (one small PDL-launched kernel after apply,
 // instead of two device-to-host copies).
@@ -1745,6 +1862,34 @@ template <int F, bool W>
 static cudaError_t apply_t(const Store& s, const Batch& b, cudaStream_t st) {
     return launch_pdl(apply_warp_kernel<F, W>, dim3(grid_slices(s, reinterpret_cast<const void*>(apply_warp_kernel<F, W>))),
                       dim3(32 * kWarpsPerCta), st, s, b);
+}
+
+template <int F, bool W>
+static cudaError_t single_t(const Store& s, const Batch& b, cudaStream_t st) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // one round of cell tests per CTA when the cells allow, at least 2 CTAs per SM otherwise
+    const int grid = std::max(std::min(s.ncells, 2 * sms), (s.ncells + s.cell - 1) / s.cell);
+    return launch_pdl(single_cells_kernel<F, W>, dim3(std::max(1, grid)), dim3(s.cell), st, s, b);
+}
+
+cudaError_t launch_single(const Store& s, const Batch& b, int flags, cudaStream_t st) {
+    if (s.ncells == 0) {
+        commit_kernel<<<1, 128, 0, st>>>(s, b);
+        return cudaGetLastError();
+    }
+    const bool wide = s.W > 1;
+    constexpr int H = kHits, P = kPerMove;
+    switch (flags & (kHits | kPerMove)) {
+        case H | P: return wide ? single_t<H | P, true>(s, b, st) : single_t<H | P, false>(s, b, st);
+        case H: return wide ? single_t<H, true>(s, b, st) : single_t<H, false>(s, b, st);
+        case P: return wide ? single_t<P, true>(s, b, st) : single_t<P, false>(s, b, st);
+        default: return wide ? single_t<0, true>(s, b, st) : single_t<0, false>(s, b, st);
+    }
 }
 
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st) {

@@ -207,6 +207,9 @@ enum Flags : int32_t { kPerMove = 2, kHits = 8, kCensus = 16 };
 cudaError_t launch_pose(const Store& s, const Batch& b, cudaStream_t st);
 cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st);
 cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid, cudaStream_t st);
+// single-move updates: one kernel tests the cells against the move's boxes, then runs touch,
+// narrow and the transition per component of every hit cell
+cudaError_t launch_single(const Store& s, const Batch& b, int flags, cudaStream_t st);
 cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st);
 cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st);
 cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, const int32_t* cand, int n, int o,

@@ -313,6 +313,7 @@ class GpuEngine:
         self.layout = lv
         self._resolver = None
         self._hv = h.value or 0  # the handle as an int (pyfast)
+        self._one = (np.zeros(1, np.int32), (_Report * 1)())  # update_obstacle's move / report buffers
 
     # ------------------------------------------------------------- plumbing
     @staticmethod
@@ -376,7 +377,18 @@ class GpuEngine:
         ``resolve(ids) -> uint8 states``: the exact per-component check of
         exact_component_valid (proj/src/roadmap.cpp:129-163), which stays on the host."""
         if lazy:
-            return self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=True)[0]
+            fast = _fast()
+            if fast is None:
+                return self.batch_update(([int(o)], _pose12(pose)[None, :]), lazy=True)[0]
+            # one move: reused one-element buffers, the report built from its fields
+            p = pose if (type(pose) is np.ndarray and pose.dtype is _F64 and pose.size == 12
+                         and pose.flags.c_contiguous) else _pose12(pose)
+            ids, rep = self._one
+            ids[0] = o
+            self._check(fast.update(self._hv, ids, p, RGG_LAZY | RGG_PER_MOVE, rep))
+            r = rep[0]
+            return UpdateReport(r.obstacle, r.new_green, r.new_red, r.new_gray, r.reval_us, r.over_us, r.under_us,
+                                r.resolve_us, r.unknown_after_heuristic, r.residual_unknown, r.resolve_checks)
         if resolve is None:
             if self._resolver is None:
                 raise ValueError("eager updates need set_resolver() (GPU exact resolve) or a resolve callable")

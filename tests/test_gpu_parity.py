@@ -209,11 +209,13 @@ def test_item_queue_overflow_replays(eng_mod, name, monkeypatch):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}, {"RGG_NO_SMALL_BIN": "1"}])
+@pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}, {"RGG_NO_SMALL_BIN": "1"},
+                                 {"RGG_NO_SINGLE": "1"}])
 def test_kernel_handoffs(env):
     """The split pipeline's in-kernel handoffs, forced on or off for every batch size
     (rgg_kernels.cu: bin on the pose warps' published boxes, touch on bin's published
-    units; by default touch waits for the whole bin kernel below 256 moves)."""
+    units; by default touch waits for the whole bin kernel below 256 moves; single moves
+    through the batched pipeline instead of the single-move kernel)."""
     import os
     import subprocess
     import sys
@@ -292,3 +294,28 @@ def test_create_from_components_equals_layout(eng_mod, scn):
     ref_eng = ref.Engine(w, kind=0, threads=1)
     ref_eng.run(ids, rts)
     assert np.array_equal(b.states(), ref_eng.states())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SCENARIOS)
+def test_single_move_kernel_equals_batched_path(eng_mod, name):
+    """Single-move updates take the fused single-move kernel (rggk::launch_single); an
+    update with census=True keeps the batched pipeline.  Move by move, both engines give
+    the same report, labels, bit words and (as a set) gray over-hits."""
+    import torch
+
+    g = load_golden(name)
+    a = eng_mod.GpuEngine(_layout(g))
+    b = eng_mod.GpuEngine(_layout(g))
+    ids = torch.tensor(np.asarray(g["ids"], np.int32), device="cuda")
+    rts = torch.tensor(np.asarray(g["rts"], np.float64).reshape(len(g["ids"]), 12), device="cuda")
+    cnt = torch.empty((1, 4), dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    for i, (o, rt) in enumerate(zip(g["ids"], g["rts"])):
+        ra = a.update_obstacle(int(o), rt)
+        b.update_device(ids[i:].data_ptr(), rts[i:].data_ptr(), 1, per_move=True, census=True)
+        b.counters_into(cnt, 1)
+        assert [ra.new_green, ra.new_red, ra.new_gray] == cnt[0, :3].tolist(), i
+        assert np.array_equal(np.sort(a.last_hits()), np.sort(b.last_hits())), i
+    assert np.array_equal(a.states(), b.states())
+    assert np.array_equal(a.obstacle_bits(), b.obstacle_bits())
