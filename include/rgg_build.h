@@ -1,10 +1,10 @@
 /* rgg_build.h — C-ABI of the host-side roadmap producer (CPU, multithreaded).
  *
  * Produces the serialized store consumed by rgg_gpu_create (include/rgg_gpu.h)
- * from a roadmap of a free-flying box robot, following the reference's
+ * from a roadmap of a free-flying box robot or a serial chain, following the reference's
  * preprocessing so the inputs have the reference's shapes:
  *   discretize_edge        proj/src/robot.cpp:39-64
- *   forward_kinematics     proj/src/robot.cpp:66-84 (free-flying branch)
+ *   forward_kinematics     proj/src/robot.cpp:66-84 (free-flying and serial-chain branches)
  *   build_outer_approx     proj/src/swept.cpp:100-118 + obb_from_points geometry.cpp:134-195
  *   build_inner_approx     proj/src/swept.cpp:188-228 (+ simplify :79-92, cap_segments :125-162)
  *   build_components       proj/src/roadmap.cpp:104-127 (nodes first, then edges)
@@ -37,7 +37,29 @@ int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nod
 int rgg_build_layout_ex(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
                         const int32_t* edges, double eps, int32_t max_segments, int32_t threads, int32_t flags,
                         rgg_built** out);
-/* The kept poses: *n_configs = pose_off[N]; pose_off N+1; poses n_configs*12 (r[9], t[3]).
+/* Any robot of the reference (RobotModel, proj/include/rgg/robot.hpp:13-58): free flying
+ * (6 DOFs: x, y, z, rx, ry, rz; every body rides the one world frame) or a serial chain
+ * (one revolute joint per body: DOF j is joint j's angle).  Its inner spheres are
+ * default_body_spheres (proj/src/swept.cpp:52-65), as in the reference's scenarios. */
+#define RGG_ROBOT_FREE_FLYING 0
+#define RGG_ROBOT_SERIAL_CHAIN 1
+typedef struct {
+    int32_t kinematics;          /* RGG_ROBOT_FREE_FLYING or RGG_ROBOT_SERIAL_CHAIN */
+    int32_t n_bodies;            /* >= 1 (<= 64 for a chain) */
+    const double* half_extents;  /* n_bodies x 3, positive */
+    const double* local;         /* n_bodies x 12 (r[9] row-major, t[3]) body frames; NULL = identity */
+    const double* joint_axis;    /* serial chain: n_bodies x 3, nonzero */
+    const double* joint_offset;  /* serial chain: n_bodies x 3, translation from the parent joint frame */
+} rgg_robot_view;
+/* rgg_build_layout_ex for any robot: nodes n_nodes x dof (6, or n_bodies for a chain).
+ * The layout has B = n_bodies SatBoxes per component (body-minor) and B*S slots.
+ * RGG_BUILD_GPU_FIT fits every (component, body) box on the GPU; RGG_BUILD_GPU_INNER
+ * takes single-body robots only. */
+int rgg_build_layout_robot(const rgg_robot_view* robot, int32_t n_nodes, const double* nodes, int32_t n_edges,
+                           const int32_t* edges, double eps, int32_t max_segments, int32_t threads, int32_t flags,
+                           rgg_built** out);
+/* The kept poses: *n_configs = pose_off[N]; pose_off N+1; poses n_configs*B*12 (r[9], t[3];
+ * body-minor per configuration).
  * Any pointer may be null. */
 int rgg_built_poses(const rgg_built* b, int64_t* n_configs, int64_t* pose_off, double* poses);
 /* out[0..3] = N, B, S, T (real segments) */

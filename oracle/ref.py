@@ -55,6 +55,11 @@ def lib():
         L.rr_engine_run_parallel.argtypes = [C.c_void_p, C.c_int, _ip, _dp, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.rr_world_poses.argtypes = [C.c_void_p, _lp, C.c_void_p]
         L.rr_world_body_he.argtypes = [C.c_void_p, _dp]
+        L.rr_world_from_robot.restype = C.c_void_p
+        L.rr_world_from_robot.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_int, _dp, C.c_int, _ip,
+                                          C.c_double, C.c_int]
+        L.rr_world_robot.argtypes = [C.c_void_p, _ip] + [C.c_void_p] * 5
+        L.rr_world_roadmap.argtypes = [C.c_void_p, _dp, _ip]
         L.rr_box_intersect.argtypes = [_dp, _dp, _dp, _dp, C.POINTER(C.c_int)]
         L.rr_engine_exact.argtypes = [C.c_void_p, C.c_int, _ip, _up]
         L.rr_engine_resolve_all.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
@@ -127,6 +132,41 @@ class World:
                                         nodes.shape[0], nodes.reshape(-1), edges.shape[0], edges.reshape(-1),
                                         float(eps), int(max_segments))
         return cls(h)
+
+    @classmethod
+    def from_robot(cls, robot: dict, env, nodes, edges, eps, max_segments=16) -> "World":
+        """Any robot (robot.hpp:13-58) over an explicit roadmap: robot = {"kinematics":
+        0 free flying / 1 serial chain, "he" (B, 3), "local" (B, 12), "axis" / "offset" (B, 3)}."""
+        he = np.ascontiguousarray(robot["he"], np.float64).reshape(-1, 3)
+        B = he.shape[0]
+        loc = np.ascontiguousarray(robot["local"], np.float64).reshape(B, 12)
+        ax = np.ascontiguousarray(robot.get("axis", np.zeros((B, 3))), np.float64).reshape(B, 3)
+        off = np.ascontiguousarray(robot.get("offset", np.zeros((B, 3))), np.float64).reshape(B, 3)
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        edges = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+        h = lib().rr_world_from_robot(int(robot["kinematics"]), B, he.reshape(-1), loc.reshape(-1), ax.reshape(-1),
+                                      off.reshape(-1), np.asarray(env, np.float64), nodes.shape[0], nodes.reshape(-1),
+                                      edges.shape[0], edges.reshape(-1), float(eps), int(max_segments))
+        return cls(h)
+
+    def robot(self) -> dict:
+        """The world's robot (the from_robot dict) plus its components' eps and max_segments."""
+        meta = np.zeros(3, np.int32)
+        _check(lib().rr_world_robot(self.h, meta, None, None, None, None, None))
+        B = int(meta[1])
+        he, loc, ax, off, ek = np.zeros((B, 3)), np.zeros((B, 12)), np.zeros((B, 3)), np.zeros((B, 3)), np.zeros(2)
+        _check(lib().rr_world_robot(self.h, meta, *[a.ctypes.data for a in (he, loc, ax, off, ek)]))
+        return dict(kinematics=int(meta[0]), dof=int(meta[2]), he=he, local=loc, axis=ax, offset=off,
+                    eps=float(ek[0]), max_segments=int(ek[1]))
+
+    def roadmap(self):
+        """(nodes (n, dof), edges (e, 2))."""
+        k = self.counts()
+        dof = self.robot()["dof"]
+        nodes = np.zeros((k["n_nodes"], dof))
+        edges = np.zeros((k["n_edges"], 2), np.int32)
+        _check(lib().rr_world_roadmap(self.h, nodes.reshape(-1), edges.reshape(-1)))
+        return nodes, edges
 
     def add_obstacle(self, he, spheres=0):
         _check(lib().rr_world_add_obstacle(self.h, np.asarray(he, np.float64), int(spheres)))

@@ -158,6 +158,89 @@ void* rr_world_from_roadmap(const double* robot_he3, const double* env6, int n_n
     return w;
 }
 
+// Any robot (free-flying or serial chain, robot.hpp:13-58) over an explicit roadmap
+// (nodes n x dof, edges e x 2): kin 0 free flying / 1 serial chain; per body its half
+// extents (3) and local frame (12: r[9], t[3]); per joint (chains) axis (3), offset (3).
+void* rr_world_from_robot(int kin, int n_bodies, const double* he, const double* local12, const double* axis,
+                          const double* offset, const double* env6, int n_nodes, const double* nodes, int n_edges,
+                          const std::int32_t* edges, double eps, int max_segments) {
+    World* w = new World();
+    const int rc = guarded([&] {
+        w->scene.bounds = {{env6[0], env6[1], env6[2]}, {env6[3], env6[4], env6[5]}};
+        RobotModel m;
+        m.kinematics = kin == 1 ? KinematicsType::SerialChain : KinematicsType::FreeFlying;
+        for (int b = 0; b < n_bodies; ++b) {
+            m.bodies.push_back({{he[3 * b], he[3 * b + 1], he[3 * b + 2]}, tf_of(local12 + 12 * b)});
+            if (kin == 1) {
+                Joint j;
+                j.axis = {axis[3 * b], axis[3 * b + 1], axis[3 * b + 2]};
+                j.offset = {offset[3 * b], offset[3 * b + 1], offset[3 * b + 2]};
+                m.joints.push_back(j);
+            }
+        }
+        m.validate();
+        w->scene.robot = m;
+        const int dof = m.dof_count();
+        w->roadmap.nodes.resize(n_nodes);
+        for (int i = 0; i < n_nodes; ++i) w->roadmap.nodes[i].assign(nodes + i * dof, nodes + (i + 1) * dof);
+        w->roadmap.edges.resize(n_edges);
+        for (int e = 0; e < n_edges; ++e) w->roadmap.edges[e] = {edges[2 * e], edges[2 * e + 1]};
+        w->roadmap.rebuild_adjacency();
+        w->comps = build_components(w->roadmap, m, default_body_spheres(m), eps, max_segments);
+    });
+    if (rc != 0) {
+        delete w;
+        return nullptr;
+    }
+    return w;
+}
+
+// The world's robot: meta = {kinematics (0 free flying, 1 serial chain), bodies, dof};
+// he B*3, local B*12, axis / offset B*3 (zero for free flying); eps_k = {epsilon,
+// max_segments} of its components.  Null arrays are skipped.
+int rr_world_robot(void* wp, std::int32_t* meta, double* he, double* local12, double* axis, double* offset,
+                   double* eps_k) {
+    const World* w = static_cast<const World*>(wp);
+    return guarded([&] {
+        const RobotModel& m = w->scene.robot;
+        const int B = static_cast<int>(m.bodies.size());
+        meta[0] = m.kinematics == KinematicsType::SerialChain ? 1 : 0;
+        meta[1] = B;
+        meta[2] = m.dof_count();
+        for (int b = 0; b < B; ++b) {
+            const Vec3& v = m.bodies[b].half_extents;
+            if (he) he[3 * b] = v.x, he[3 * b + 1] = v.y, he[3 * b + 2] = v.z;
+            if (local12) put_tf(m.bodies[b].local, local12 + 12 * b);
+            const bool j = b < static_cast<int>(m.joints.size());
+            if (axis) {
+                axis[3 * b] = j ? m.joints[b].axis.x : 0.0;
+                axis[3 * b + 1] = j ? m.joints[b].axis.y : 0.0;
+                axis[3 * b + 2] = j ? m.joints[b].axis.z : 0.0;
+            }
+            if (offset) {
+                offset[3 * b] = j ? m.joints[b].offset.x : 0.0;
+                offset[3 * b + 1] = j ? m.joints[b].offset.y : 0.0;
+                offset[3 * b + 2] = j ? m.joints[b].offset.z : 0.0;
+            }
+        }
+        if (eps_k) eps_k[0] = w->comps.epsilon, eps_k[1] = w->comps.max_segments;
+    });
+}
+
+// The world's roadmap: nodes n x dof, edges e x 2 (counts from rr_world_counts).
+int rr_world_roadmap(void* wp, double* nodes, std::int32_t* edges) {
+    const World* w = static_cast<const World*>(wp);
+    return guarded([&] {
+        size_t k = 0;
+        for (const Configuration& c : w->roadmap.nodes)
+            for (double v : c) nodes[k++] = v;
+        for (size_t e = 0; e < w->roadmap.edges.size(); ++e) {
+            edges[2 * e] = w->roadmap.edges[e].first;
+            edges[2 * e + 1] = w->roadmap.edges[e].second;
+        }
+    });
+}
+
 int rr_world_add_obstacle(void* wp, const double* he3, int spheres) {
     World* w = static_cast<World*>(wp);
     return guarded([&] {

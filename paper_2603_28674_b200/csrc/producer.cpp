@@ -1,8 +1,8 @@
 // producer.cpp — host roadmap producer: swept-volume approximations + serialized store.
 //
-// Free-flying box robot (one body).  Every floating-point expression keeps the
-// association of the reference's preprocessing (built, like the reference, with
-// -ffp-contract=off) so the store it emits is the one the reference would
+// Free-flying robots and serial chains (robot.hpp:13-58), one box per body.  Every
+// floating-point expression keeps the association of the reference's preprocessing
+// (built, like the reference, with -ffp-contract=off) so the store it emits is the one the reference would
 // serialize for the same roadmap; tests/test_producer.py checks that bit for bit.
 // Components are independent, so they are built on a pool of std::threads.
 #include "../../include/rgg_build.h"
@@ -16,6 +16,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <thread>
 #include <vector>
 
@@ -329,123 +330,206 @@ void cap_split(const std::vector<V3>& raw, const std::vector<int>& kept, double 
 }
 
 struct Comp {
-    Box over;
-    std::vector<Spline> under;
-    std::vector<Tf> fk;  // forward_kinematics per configuration (kept for the exact resolve)
+    std::vector<Box> over;                   // per body
+    std::vector<std::vector<Spline>> under;  // per body
+    std::vector<Tf> fk;  // forward_kinematics per configuration, body-minor (kept for the exact resolve)
 };
 
-struct Robot {
+// RobotModel (robot.hpp:13-58) with its default inner spheres (default_body_spheres,
+// swept.cpp:52-65) and their certified spline radii.
+struct Body {
     V3 he;
+    Tf local;
     std::vector<Sph> spheres;
     std::vector<double> lipschitz, radius, tol;
 };
 
-Robot make_robot(V3 he, double eps) {
+struct Robot {
+    bool chain = false;  // KinematicsType::SerialChain
+    int dof = 6;
+    std::vector<Body> bodies;
+    std::vector<V3> axis, offset;  // joints (serial chain)
+};
+
+bool finite3(V3 v) { return std::isfinite(v.x) && std::isfinite(v.y) && std::isfinite(v.z); }
+
+// Transform::rotation_valid (geometry.cpp:36-48)
+bool rotation_valid(const Tf& t, double tol) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double v = 0.0;
+            for (int q = 0; q < 3; ++q) v += t.r[q * 3 + i] * t.r[q * 3 + j];
+            if (std::fabs(v - (i == j ? 1.0 : 0.0)) > tol) return false;
+        }
+    const double* r = t.r;
+    const double det = r[0] * (r[4] * r[8] - r[5] * r[7]) - r[1] * (r[3] * r[8] - r[5] * r[6]) +
+                       r[2] * (r[3] * r[7] - r[4] * r[6]);
+    return std::fabs(det - 1.0) <= tol;
+}
+
+// RobotModel::validate (robot.cpp:17-37), BodySpheres::validate (swept.cpp:9-21),
+// center_lipschitz (swept.cpp:164-178), certified_spline_radius (:180-186)
+Robot make_robot(const rgg_robot_view& v, double eps) {
+    if (v.kinematics != RGG_ROBOT_FREE_FLYING && v.kinematics != RGG_ROBOT_SERIAL_CHAIN)
+        throw std::invalid_argument("robot kinematics must be free flying or serial chain");
+    if (v.n_bodies < 1 || !v.half_extents) throw std::invalid_argument("robot needs at least one body");
     Robot r;
-    r.he = he;
-    r.spheres = inner_spheres(he, sphere_count(he));
-    for (const Sph& s : r.spheres) {
-        // center_lipschitz (swept.cpp:166-178), body.local = identity
-        const Tf local;
-        const V3 p = local.apply(s.c);
-        const double L = std::sqrt(1.0 + 3.0 * dotv(p, p));
-        // certified_spline_radius (swept.cpp:180-186)
-        const double half_step = 0.5 * L * eps;
-        const double r2 = s.r * s.r - half_step * half_step;
-        double rad = 0.0;
-        if (r2 > 0.0) rad = std::sqrt(r2) * (1.0 - 0.1) - 1e-9;
-        r.lipschitz.push_back(L);
-        r.radius.push_back(rad);
-        r.tol.push_back(std::sqrt(s.r * s.r - 0.25 * L * eps * L * eps) - rad - 1e-9);
+    r.chain = v.kinematics == RGG_ROBOT_SERIAL_CHAIN;
+    for (int32_t b = 0; b < v.n_bodies; ++b) {
+        Body bd;
+        bd.he = {v.half_extents[3 * b], v.half_extents[3 * b + 1], v.half_extents[3 * b + 2]};
+        if (!(bd.he.x > 0 && bd.he.y > 0 && bd.he.z > 0)) throw std::invalid_argument("body half extents must be positive");
+        if (v.local) {
+            std::memcpy(bd.local.r, v.local + 12 * b, 9 * sizeof(double));
+            bd.local.t = {v.local[12 * b + 9], v.local[12 * b + 10], v.local[12 * b + 11]};
+        }
+        if (!finite3(bd.local.t) || !rotation_valid(bd.local, 1e-9)) throw std::invalid_argument("body local frame invalid");
+        r.bodies.push_back(bd);
+    }
+    if (r.chain) {
+        if (!v.joint_axis || !v.joint_offset) throw std::invalid_argument("serial chain needs one joint per body");
+        for (int32_t j = 0; j < v.n_bodies; ++j) {
+            const V3 ax{v.joint_axis[3 * j], v.joint_axis[3 * j + 1], v.joint_axis[3 * j + 2]};
+            const V3 of{v.joint_offset[3 * j], v.joint_offset[3 * j + 1], v.joint_offset[3 * j + 2]};
+            if (!finite3(of) || !(std::sqrt(dotv(ax, ax)) > 0)) throw std::invalid_argument("joint axis/offset invalid");
+            r.axis.push_back(ax);
+            r.offset.push_back(of);
+        }
+        if (v.n_bodies > 64) throw std::invalid_argument("serial chain: at most 64 joints");
+        r.dof = v.n_bodies;
+    }
+    for (size_t b = 0; b < r.bodies.size(); ++b) {
+        Body& bd = r.bodies[b];
+        bd.spheres = inner_spheres(bd.he, sphere_count(bd.he));
+        for (const Sph& s : bd.spheres) {
+            if (!(s.r > 0)) throw std::invalid_argument("body sphere radius must be positive");
+            if (std::fabs(s.c.x) + s.r > bd.he.x || std::fabs(s.c.y) + s.r > bd.he.y || std::fabs(s.c.z) + s.r > bd.he.z)
+                throw std::invalid_argument("body sphere escapes its box");
+            const V3 p = bd.local.apply(s.c);
+            double L;
+            if (!r.chain) {
+                L = std::sqrt(1.0 + 3.0 * dotv(p, p));
+            } else {
+                double span = std::sqrt(dotv(p, p));
+                for (size_t j = 0; j <= b; ++j) span += std::sqrt(dotv(r.offset[j], r.offset[j]));
+                L = span * std::sqrt(static_cast<double>(b + 1));
+            }
+            const double half_step = 0.5 * L * eps;
+            const double r2 = s.r * s.r - half_step * half_step;
+            double rad = 0.0;
+            if (r2 > 0.0) rad = std::sqrt(r2) * (1.0 - 0.1) - 1e-9;
+            bd.lipschitz.push_back(L);
+            bd.radius.push_back(rad);
+            bd.tol.push_back(std::sqrt(s.r * s.r - 0.25 * L * eps * L * eps) - rad - 1e-9);
+        }
     }
     return r;
 }
 
-// forward_kinematics, free-flying branch (robot.cpp:71-74).
-Tf body_pose(const double* c) {
-    Tf world = axis_angle({0, 0, 1}, c[5]).compose(axis_angle({0, 1, 0}, c[4])).compose(axis_angle({1, 0, 0}, c[3]));
-    world.t = {c[0], c[1], c[2]};
-    return world.compose(Tf{});
+// forward_kinematics (robot.cpp:66-84): one pose per body
+void forward_kinematics(const Robot& r, const double* c, Tf* out) {
+    if (!r.chain) {
+        Tf world = axis_angle({0, 0, 1}, c[5]).compose(axis_angle({0, 1, 0}, c[4])).compose(axis_angle({1, 0, 0}, c[3]));
+        world.t = {c[0], c[1], c[2]};
+        for (size_t b = 0; b < r.bodies.size(); ++b) out[b] = world.compose(r.bodies[b].local);
+        return;
+    }
+    Tf acc;
+    for (size_t j = 0; j < r.axis.size(); ++j) {
+        Tf tr;
+        tr.t = r.offset[j];
+        const Tf jt = tr.compose(axis_angle(r.axis[j], c[j]));
+        acc = acc.compose(jt);
+        out[j] = acc.compose(r.bodies[j].local);
+    }
 }
 
 // discretize_edge's configuration count (robot.cpp:39-64)
-int config_count(const double* a, const double* b, double eps) {
+int config_count(const double* a, const double* b, int dof, double eps) {
     double len2 = 0.0;
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < dof; ++i) {
         const double d = b[i] - a[i];
         len2 += d * d;
     }
     return std::max(2, static_cast<int>(std::ceil(std::sqrt(len2) / eps)) + 1);
 }
 
-// pose_out (gpu_fit): the component's forward-kinematics poses, 12 doubles each
+// pose_out (gpu_fit): the component's forward-kinematics poses, 12 doubles each,
+// body-major (body b's n poses at pose_out + 12 * n * b)
 Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, int K, bool keep_poses, bool gpu_fit,
                 bool gpu_inner, double* pose_out) {
+    const int dof = rb.dof, B = static_cast<int>(rb.bodies.size());
     // discretize_edge (robot.cpp:39-64)
-    double len2 = 0.0;
-    for (int i = 0; i < 6; ++i) {
-        const double d = b[i] - a[i];
-        len2 += d * d;
-    }
-    const double len = std::sqrt(len2);
-    const int n = std::max(2, static_cast<int>(std::ceil(len / eps)) + 1);
-    std::vector<Tf> fk(n);
-    double cfg[6];
+    const int n = config_count(a, b, dof, eps);
+    std::vector<Tf> fk(static_cast<size_t>(n) * B);
+    double cfg[64];
     for (int i = 0; i < n; ++i) {
         if (i == 0) {
-            std::memcpy(cfg, a, sizeof(cfg));
+            std::memcpy(cfg, a, dof * sizeof(double));
         } else if (i == n - 1) {
-            std::memcpy(cfg, b, sizeof(cfg));
+            std::memcpy(cfg, b, dof * sizeof(double));
         } else {
             const double t = static_cast<double>(i) / static_cast<double>(n - 1);
-            for (int k = 0; k < 6; ++k) cfg[k] = a[k] + (b[k] - a[k]) * t;
+            for (int q = 0; q < dof; ++q) cfg[q] = a[q] + (b[q] - a[q]) * t;
         }
-        fk[i] = body_pose(cfg);
-        if (pose_out) {
-            std::memcpy(pose_out + 12 * i, fk[i].r, 9 * sizeof(double));
-            pose_out[12 * i + 9] = fk[i].t.x, pose_out[12 * i + 10] = fk[i].t.y, pose_out[12 * i + 11] = fk[i].t.z;
-        }
+        Tf* T = &fk[static_cast<size_t>(i) * B];
+        forward_kinematics(rb, cfg, T);
+        if (pose_out)
+            for (int bd = 0; bd < B; ++bd) {
+                double* d = pose_out + 12 * (static_cast<size_t>(bd) * n + i);
+                std::memcpy(d, T[bd].r, 9 * sizeof(double));
+                d[9] = T[bd].t.x, d[10] = T[bd].t.y, d[11] = T[bd].t.z;
+            }
     }
     Comp comp;
-    // build_outer_approx (swept.cpp:100-118); with gpu_fit the box is fitted later on the GPU
-    std::vector<V3> cloud;
+    comp.over.resize(B);
+    comp.under.resize(B);
+    // build_outer_approx (swept.cpp:100-118); with gpu_fit the boxes are fitted later on the GPU
     if (!gpu_fit) {
-    cloud.reserve(static_cast<size_t>(n) * 8);
-    for (const Tf& T : fk) {
-        Box w;
-        w.c = T.apply({0, 0, 0});
-        w.ax[0] = T.rotate({1, 0, 0});
-        w.ax[1] = T.rotate({0, 1, 0});
-        w.ax[2] = T.rotate({0, 0, 1});
-        w.he = rb.he;
-        V3 cs[8];
-        corners_of(w, cs);
-        cloud.insert(cloud.end(), cs, cs + 8);
-    }
-    comp.over = fit_box(cloud);
+        std::vector<V3> cloud;
+        cloud.reserve(static_cast<size_t>(n) * 8);
+        for (int bd = 0; bd < B; ++bd) {
+            cloud.clear();
+            for (int i = 0; i < n; ++i) {
+                const Tf& T = fk[static_cast<size_t>(i) * B + bd];
+                Box w;
+                w.c = T.apply({0, 0, 0});
+                w.ax[0] = T.rotate({1, 0, 0});
+                w.ax[1] = T.rotate({0, 1, 0});
+                w.ax[2] = T.rotate({0, 0, 1});
+                w.he = rb.bodies[bd].he;
+                V3 cs[8];
+                corners_of(w, cs);
+                cloud.insert(cloud.end(), cs, cs + 8);
+            }
+            comp.over[bd] = fit_box(cloud);
+        }
     }
     if (gpu_inner) {  // the inner approximation runs on the GPU too
         if (keep_poses) comp.fk = std::move(fk);
         return comp;
     }
     // build_inner_approx (swept.cpp:188-228)
-    for (size_t si = 0; si < rb.spheres.size(); ++si) {
-        const double rad = rb.radius[si];
-        if (rad <= 0.0) continue;
-        const double step_bound = rb.lipschitz[si] * eps;
-        std::vector<V3> raw;
-        bool step_ok = true;
-        for (const Tf& T : fk) {
-            const V3 c = T.apply(rb.spheres[si].c);
-            if (!raw.empty()) {
-                const V3 d = c - raw.back();
-                if (std::sqrt(dotv(d, d)) > step_bound) step_ok = false;
+    for (int bd = 0; bd < B; ++bd) {
+        const Body& body = rb.bodies[bd];
+        for (size_t si = 0; si < body.spheres.size(); ++si) {
+            const double rad = body.radius[si];
+            if (rad <= 0.0) continue;
+            const double step_bound = body.lipschitz[si] * eps;
+            std::vector<V3> raw;
+            bool step_ok = true;
+            for (int i = 0; i < n; ++i) {
+                const V3 c = fk[static_cast<size_t>(i) * B + bd].apply(body.spheres[si].c);
+                if (!raw.empty()) {
+                    const V3 d = c - raw.back();
+                    if (std::sqrt(dotv(d, d)) > step_bound) step_ok = false;
+                }
+                if (raw.empty() || !same(c, raw.back())) raw.push_back(c);
             }
-            if (raw.empty() || !same(c, raw.back())) raw.push_back(c);
+            if (!step_ok) continue;
+            const std::vector<int> kept = simplify(raw, body.tol[si]);
+            cap_split(raw, kept, rad, body.tol[si], K, static_cast<int>(si), comp.under[bd]);
         }
-        if (!step_ok) continue;
-        const std::vector<int> kept = simplify(raw, rb.tol[si]);
-        cap_split(raw, kept, rad, rb.tol[si], K, static_cast<int>(si), comp.under);
     }
     if (keep_poses) comp.fk = std::move(fk);
     return comp;
@@ -458,7 +542,7 @@ struct rgg_built {
     std::vector<double> edge_sat, comp_aabb, segs, spline_r, obb15;
     std::vector<int32_t> row_off;
     std::vector<int64_t> pose_off;  // RGG_BUILD_POSES: N+1
-    std::vector<double> poses;      // pose_off[N] * 12 (one body)
+    std::vector<double> poses;      // pose_off[N] * B * 12 (body-minor per configuration)
 };
 
 extern "C" {
@@ -473,6 +557,20 @@ int rgg_build_layout(const double* he3, int32_t n_nodes, const double* nodes, in
 int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
                         const int32_t* edges, double eps, int32_t K, int32_t threads, int32_t flags,
                         rgg_built** out) {
+    if (!he3) {
+        g_err = "null robot half extents";
+        return -1;
+    }
+    rgg_robot_view v{};
+    v.kinematics = RGG_ROBOT_FREE_FLYING;
+    v.n_bodies = 1;
+    v.half_extents = he3;  // make_free_flying_box (robot.cpp:86-92): one body, identity local frame
+    return rgg_build_layout_robot(&v, n_nodes, nodes, n_edges, edges, eps, K, threads, flags, out);
+}
+
+int rgg_build_layout_robot(const rgg_robot_view* robot, int32_t n_nodes, const double* nodes, int32_t n_edges,
+                           const int32_t* edges, double eps, int32_t K, int32_t threads, int32_t flags,
+                           rgg_built** out) {
     const bool keep_poses = (flags & RGG_BUILD_POSES) != 0;
     static const bool dbg = std::getenv("RGG_DEBUG_PRODUCER") != nullptr;
     auto t_mark = std::chrono::steady_clock::now();
@@ -485,22 +583,27 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
     const bool gpu_fit = (flags & (RGG_BUILD_GPU_FIT | RGG_BUILD_GPU_INNER)) != 0;
     const bool gpu_inner = (flags & RGG_BUILD_GPU_INNER) != 0;
     try {
-        if (!out) throw std::invalid_argument("null output");
+        if (!out || !robot) throw std::invalid_argument("null robot or output");
         if (!(eps > 0)) throw std::invalid_argument("resolution must be positive");
         if (K < 1) throw std::invalid_argument("segment cap must be >= 1");
+        if (n_nodes < 0 || n_edges < 0 || (n_nodes > 0 && !nodes) || (n_edges > 0 && !edges))
+            throw std::invalid_argument("bad roadmap arrays");
         for (int32_t e = 0; e < n_edges; ++e)
             if (edges[2 * e] < 0 || edges[2 * e] >= n_nodes || edges[2 * e + 1] < 0 || edges[2 * e + 1] >= n_nodes)
                 throw std::invalid_argument("edge endpoint out of range");
-        const Robot rb = make_robot({he3[0], he3[1], he3[2]}, eps);
+        const Robot rb = make_robot(*robot, eps);
+        const int dof = rb.dof;
+        const int32_t B = static_cast<int32_t>(rb.bodies.size());
+        if (gpu_inner && B != 1) throw std::invalid_argument("the GPU inner approximation takes single-body robots");
         const int32_t N = n_nodes + n_edges;
         std::vector<Comp> comps(static_cast<size_t>(N));
         const auto ends = [&](int32_t c, const double** a, const double** b) {
             if (c < n_nodes) {
-                *a = *b = nodes + 6 * static_cast<size_t>(c);
+                *a = *b = nodes + dof * static_cast<size_t>(c);
             } else {
                 const int32_t e = c - n_nodes;
-                *a = nodes + 6 * static_cast<size_t>(edges[2 * e]);
-                *b = nodes + 6 * static_cast<size_t>(edges[2 * e + 1]);
+                *a = nodes + dof * static_cast<size_t>(edges[2 * e]);
+                *b = nodes + dof * static_cast<size_t>(edges[2 * e + 1]);
             }
         };
         int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
@@ -538,7 +641,8 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
                             const double *a, *b;
                             ends(c, &a, &b);
                             comps[c] = build_comp(rb, a, b, eps, K, keep_poses, gpu_fit, gpu_inner,
-                                                  stage ? stage + 12 * static_cast<size_t>(pose_off[c] - cfg0) : nullptr);
+                                                  stage ? stage + 12 * static_cast<size_t>(pose_off[c] - cfg0) * B
+                                                        : nullptr);
                         }
                     }
                 } catch (const std::exception& ex) {
@@ -555,34 +659,44 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         if (!gpu_fit) {
             run_components(0, N, nullptr, nullptr, 0);
         } else {
-            // the poses stream to the GPU in chunks of <= kChunk configurations through two
-            // pinned buffers: a chunk's copy overlaps the production of the next
+            // the poses stream to the GPU in chunks of <= kChunk poses through two pinned
+            // buffers: a chunk's copy overlaps the production of the next.  One fit unit per
+            // (component, body), its poses contiguous (build_comp's body-major pose_out)
             constexpr int64_t kChunk = 1 << 19;
             std::vector<int64_t> pose_off(static_cast<size_t>(N) + 1, 0);
             for (int32_t c = 0; c < N; ++c) {
                 const double *a, *b;
                 ends(c, &a, &b);
-                pose_off[c + 1] = pose_off[c] + config_count(a, b, eps);
+                pose_off[c + 1] = pose_off[c] + config_count(a, b, dof, eps);
             }
+            std::vector<int64_t> unit_off(static_cast<size_t>(N) * B + 1, 0);
+            for (int32_t c = 0; c < N; ++c)
+                for (int32_t bd = 0; bd < B; ++bd)
+                    unit_off[static_cast<size_t>(c) * B + bd] = pose_off[c] * B + bd * (pose_off[c + 1] - pose_off[c]);
+            unit_off[static_cast<size_t>(N) * B] = pose_off[N] * B;
             double cs[22];
             constexpr double kStep = 3.0 * 3.141592653589793 / 180.0;
             for (int step = -5; step <= 5; ++step) {
                 cs[2 * (step + 5)] = std::cos(step * kStep);
                 cs[2 * (step + 5) + 1] = std::sin(step * kStep);
             }
+            std::vector<double> he(static_cast<size_t>(B) * 3);
+            for (int32_t bd = 0; bd < B; ++bd)
+                he[3 * bd] = rb.bodies[bd].he.x, he[3 * bd + 1] = rb.bodies[bd].he.y, he[3 * bd + 2] = rb.bodies[bd].he.z;
             int64_t max_chunk = 0;
             for (int32_t c = 0; c < N; ++c) max_chunk = std::max(max_chunk, pose_off[c + 1] - pose_off[c]);
-            fit = rggp_fit_begin(pose_off.data(), N, he3, cs, std::max(kChunk, max_chunk), 0);
+            const int64_t chunk = std::max(kChunk / B, max_chunk);  // configurations per staging buffer
+            fit = rggp_fit_begin(unit_off.data(), N * B, he.data(), B, cs, chunk * B, 0);
             if (!fit) throw std::runtime_error("GPU box fit: CUDA initialisation failed");
             try {
                 int slot = 0;
                 for (int32_t c_lo = 0; c_lo < N; slot ^= 1) {
                     int32_t c_hi = c_lo + 1;
-                    while (c_hi < N && pose_off[c_hi + 1] - pose_off[c_lo] <= std::max(kChunk, max_chunk)) ++c_hi;
+                    while (c_hi < N && pose_off[c_hi + 1] - pose_off[c_lo] <= chunk) ++c_hi;
                     double* stage = rggp_fit_staging(fit, slot);
                     if (!stage) throw std::runtime_error("GPU box fit: staging failed");
                     run_components(c_lo, c_hi, stage, pose_off.data(), pose_off[c_lo]);
-                    if (rggp_fit_push(fit, slot, pose_off[c_lo], pose_off[c_hi] - pose_off[c_lo]) != 0)
+                    if (rggp_fit_push(fit, slot, pose_off[c_lo] * B, (pose_off[c_hi] - pose_off[c_lo]) * B) != 0)
                         throw std::runtime_error("GPU box fit: copy failed");
                     c_lo = c_hi;
                 }
@@ -593,16 +707,17 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
         }
         mark("components");
         if (gpu_fit) {
-            // obb_from_points of every component on the GPU (swept_gpu.cu), from the streamed poses
-            std::vector<double> boxes(static_cast<size_t>(N) * 15);
+            // obb_from_points of every (component, body) on the GPU (swept_gpu.cu), from the streamed poses
+            std::vector<double> boxes(static_cast<size_t>(N) * B * 15);
             InnerSpec spec;
-            spec.nsph = static_cast<int32_t>(rb.spheres.size());
+            const Body& b0 = rb.bodies[0];
+            spec.nsph = static_cast<int32_t>(b0.spheres.size());
             spec.K = K;
-            for (size_t si = 0; si < rb.spheres.size(); ++si) {
-                spec.centre.insert(spec.centre.end(), {rb.spheres[si].c.x, rb.spheres[si].c.y, rb.spheres[si].c.z});
-                spec.radius.push_back(rb.radius[si]);
-                spec.step_bound.push_back(rb.lipschitz[si] * eps);
-                spec.tol.push_back(rb.tol[si]);
+            for (size_t si = 0; si < b0.spheres.size(); ++si) {
+                spec.centre.insert(spec.centre.end(), {b0.spheres[si].c.x, b0.spheres[si].c.y, b0.spheres[si].c.z});
+                spec.radius.push_back(b0.radius[si]);
+                spec.step_bound.push_back(b0.lipschitz[si] * eps);
+                spec.tol.push_back(b0.tol[si]);
             }
             InnerOut inner;
             const int rc = rggp_fit_finish(fit, boxes.data(), gpu_inner ? &spec : nullptr, &inner);
@@ -611,126 +726,150 @@ int rgg_build_layout_ex(const double* he3, int32_t n_nodes, const double* nodes,
             const int32_t nsph = gpu_inner ? spec.nsph : 0;
             std::vector<int64_t> so(static_cast<size_t>(N) + 1, 0), po(static_cast<size_t>(N) + 1, 0);
             {
-                int64_t k = 0;
+                int64_t q = 0;
                 for (int32_t c = 0; c < N; ++c) {
                     int64_t pts = 0;
                     for (int32_t si = 0; si < nsph; ++si)
-                        for (int32_t q = 0; q < inner.nspl[static_cast<size_t>(c) * nsph + si]; ++q) pts += inner.npts[k++];
-                    so[c + 1] = k;
+                        for (int32_t s = 0; s < inner.nspl[static_cast<size_t>(c) * nsph + si]; ++s) pts += inner.npts[q++];
+                    so[c + 1] = q;
                     po[c + 1] = po[c] + pts;
                 }
             }
             parallel(N, [&](int32_t c) {
-                int64_t k = so[c], p = po[c];
+                int64_t q = so[c], p = po[c];
                 for (int32_t si = 0; si < nsph; ++si)
-                    for (int32_t q = 0; q < inner.nspl[static_cast<size_t>(c) * nsph + si]; ++q, ++k) {
-                        Spline sp{{}, rb.radius[si], si};
-                        sp.pts.reserve(inner.npts[k]);
-                        for (int32_t j = 0; j < inner.npts[k]; ++j, ++p)
+                    for (int32_t s = 0; s < inner.nspl[static_cast<size_t>(c) * nsph + si]; ++s, ++q) {
+                        Spline sp{{}, b0.radius[si], si};
+                        sp.pts.reserve(inner.npts[q]);
+                        for (int32_t j = 0; j < inner.npts[q]; ++j, ++p)
                             sp.pts.push_back({inner.pts[3 * p], inner.pts[3 * p + 1], inner.pts[3 * p + 2]});
-                        comps[c].under.push_back(std::move(sp));
+                        comps[c].under[0].push_back(std::move(sp));
                     }
             });
-            for (int32_t c = 0; c < N; ++c) {
-                const double* o = &boxes[15 * static_cast<size_t>(c)];
-                Box& bx = comps[c].over;
-                bx.c = {o[0], o[1], o[2]};
-                for (int k = 0; k < 3; ++k) bx.ax[k] = {o[3 + 3 * k], o[4 + 3 * k], o[5 + 3 * k]};
-                bx.he = {o[12], o[13], o[14]};
-            }
+            for (int32_t c = 0; c < N; ++c)
+                for (int32_t bd = 0; bd < B; ++bd) {
+                    const double* o = &boxes[15 * (static_cast<size_t>(c) * B + bd)];
+                    Box& bx = comps[c].over[bd];
+                    bx.c = {o[0], o[1], o[2]};
+                    for (int q = 0; q < 3; ++q) bx.ax[q] = {o[3 + 3 * q], o[4 + 3 * q], o[5 + 3 * q]};
+                    bx.he = {o[12], o[13], o[14]};
+                }
         }
 
         mark("box fit");
         // ---- serialize (batch_layout.cpp:21-146), components in parallel
         rgg_built* L = new rgg_built();
+        std::unique_ptr<rgg_built> own(L);
         L->N = N;
-        const int32_t nsph = static_cast<int32_t>(rb.spheres.size());
-        // splines per (component, sphere): the slots of sphere s are s*max_parts + 0, 1, ...
-        std::vector<std::atomic<int32_t>> sph_parts(std::max(nsph, 1));
+        L->B = B;
+        // slots: spheres-per-body x the worst split factor; the splines of (body b, sphere s)
+        // take slots s*max_parts + 0, 1, ... of body b
+        int32_t max_spheres = 1;
+        std::vector<int32_t> sph_base(B + 1, 0);  // (body, sphere) index base
+        for (int32_t bd = 0; bd < B; ++bd) {
+            const int32_t ns = static_cast<int32_t>(rb.bodies[bd].spheres.size());
+            max_spheres = std::max(max_spheres, ns);
+            sph_base[bd + 1] = sph_base[bd] + ns;
+        }
+        const int32_t nbs = sph_base[B];
+        std::vector<std::atomic<int32_t>> sph_parts(std::max(nbs, 1));
         for (auto& x : sph_parts) x = 0;
         parallel(N, [&](int32_t c) {
             thread_local std::vector<int32_t> parts;
-            parts.assign(std::max(nsph, 1), 0);
-            for (const Spline& sp : comps[c].under) {
-                const int32_t p = ++parts[sp.sphere];
-                for (int32_t cur = sph_parts[sp.sphere]; p > cur && !sph_parts[sp.sphere].compare_exchange_weak(cur, p);) {
+            parts.assign(std::max(nbs, 1), 0);
+            for (int32_t bd = 0; bd < B; ++bd)
+                for (const Spline& sp : comps[c].under[bd]) {
+                    const int32_t x = sph_base[bd] + sp.sphere;
+                    const int32_t p = ++parts[x];
+                    for (int32_t cur = sph_parts[x]; p > cur && !sph_parts[x].compare_exchange_weak(cur, p);) {
+                    }
                 }
-            }
         });
         int32_t max_parts = 1;
-        for (int32_t k = 0; k < nsph; ++k) max_parts = std::max<int32_t>(max_parts, sph_parts[k]);
-        const int32_t S = std::max(1, nsph) * max_parts;
+        for (int32_t x = 0; x < nbs; ++x) max_parts = std::max<int32_t>(max_parts, sph_parts[x]);
+        const int32_t S = max_spheres * max_parts;
         L->S = S;
-        L->spline_r.assign(S, 0.0);
-        L->edge_sat.resize(static_cast<size_t>(N) * 21);
+        const size_t NB = static_cast<size_t>(N) * B;
+        L->spline_r.assign(static_cast<size_t>(B) * S, 0.0);
+        L->edge_sat.resize(NB * 21);
         L->comp_aabb.resize(static_cast<size_t>(N) * 6);
-        L->obb15.resize(static_cast<size_t>(N) * 15);
-        L->row_off.assign(static_cast<size_t>(N) * S + 1, 0);
-        std::vector<int32_t> count(static_cast<size_t>(N) * S, 0);
+        L->obb15.resize(NB * 15);
+        L->row_off.assign(NB * S + 1, 0);
+        std::vector<int32_t> count(NB * S, 0);
         // a slot's spline radius is its sphere's (every spline of sphere s carries it, so the
         // reference's consistency check, batch_layout.cpp:73-79, holds); unused slots stay 0
-        for (int32_t k = 0; k < nsph; ++k)
-            for (int32_t j = 0; j < sph_parts[k]; ++j) L->spline_r[k * max_parts + j] = rb.radius[k];
+        for (int32_t bd = 0; bd < B; ++bd)
+            for (int32_t s = 0; s < sph_base[bd + 1] - sph_base[bd]; ++s)
+                for (int32_t j = 0; j < sph_parts[sph_base[bd] + s]; ++j)
+                    L->spline_r[static_cast<size_t>(bd) * S + s * max_parts + j] = rb.bodies[bd].radius[s];
         parallel(N, [&](int32_t c) {
             const Comp& cp = comps[c];
-            V3 cs[8];
-            corners_of(cp.over, cs);
-            sat_prep(&cs[0].x, &L->edge_sat[21 * static_cast<size_t>(c)]);
+            // component_aabb = Aabb::empty() expanded by every body box's corners (aabb_of_obb)
             double box[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-            for (const V3& p : cs) {
-                box[0] = std::fmin(box[0], p.x), box[1] = std::fmin(box[1], p.y), box[2] = std::fmin(box[2], p.z);
-                box[3] = std::fmax(box[3], p.x), box[4] = std::fmax(box[4], p.y), box[5] = std::fmax(box[5], p.z);
+            for (int32_t bd = 0; bd < B; ++bd) {
+                const size_t u = static_cast<size_t>(c) * B + bd;
+                V3 cs[8];
+                corners_of(cp.over[bd], cs);
+                sat_prep(&cs[0].x, &L->edge_sat[21 * u]);
+                for (const V3& p : cs) {
+                    box[0] = std::fmin(box[0], p.x), box[1] = std::fmin(box[1], p.y), box[2] = std::fmin(box[2], p.z);
+                    box[3] = std::fmax(box[3], p.x), box[4] = std::fmax(box[4], p.y), box[5] = std::fmax(box[5], p.z);
+                }
+                double* o = &L->obb15[15 * u];
+                const Box& ob = cp.over[bd];
+                o[0] = ob.c.x, o[1] = ob.c.y, o[2] = ob.c.z;
+                for (int q = 0; q < 3; ++q) o[3 + 3 * q] = ob.ax[q].x, o[4 + 3 * q] = ob.ax[q].y, o[5 + 3 * q] = ob.ax[q].z;
+                o[12] = ob.he.x, o[13] = ob.he.y, o[14] = ob.he.z;
+                std::vector<int32_t> used(rb.bodies[bd].spheres.size(), 0);
+                for (const Spline& s : cp.under[bd]) {
+                    const int32_t segc = std::max<int32_t>(1, static_cast<int32_t>(s.pts.size()) - 1);
+                    if (segc > K) throw std::logic_error("spline exceeds the segment cap; the build policy should have split it");
+                    const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
+                    if (L->spline_r[static_cast<size_t>(bd) * S + slot] != s.radius)
+                        throw std::logic_error("inconsistent spline radius for a layout slot");
+                    count[u * S + slot] = segc;
+                }
             }
-            // component_aabb = union of the body boxes (one body): Aabb::empty().expand(box)
             std::memcpy(&L->comp_aabb[6 * static_cast<size_t>(c)], box, sizeof(box));
-            double* o = &L->obb15[15 * static_cast<size_t>(c)];
-            o[0] = cp.over.c.x, o[1] = cp.over.c.y, o[2] = cp.over.c.z;
-            for (int k = 0; k < 3; ++k) o[3 + 3 * k] = cp.over.ax[k].x, o[4 + 3 * k] = cp.over.ax[k].y,
-                                        o[5 + 3 * k] = cp.over.ax[k].z;
-            o[12] = cp.over.he.x, o[13] = cp.over.he.y, o[14] = cp.over.he.z;
-            std::vector<int32_t> used(nsph, 0);
-            for (const Spline& s : cp.under) {
-                const int32_t segc = std::max<int32_t>(1, static_cast<int32_t>(s.pts.size()) - 1);
-                if (segc > K) throw std::logic_error("spline exceeds the segment cap; the build policy should have split it");
-                const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
-                if (L->spline_r[slot] != s.radius) throw std::logic_error("inconsistent spline radius for a layout slot");
-                count[static_cast<size_t>(c) * S + slot] = segc;
-            }
         });
         int64_t total = 0;
         for (size_t r = 0; r < count.size(); ++r) {
             L->row_off[r] = static_cast<int32_t>(total);
             total += count[r];
+            if (total > INT32_MAX) throw std::invalid_argument("more than 2^31 - 1 real segments");
         }
         L->row_off[count.size()] = static_cast<int32_t>(total);
         L->segs.resize(static_cast<size_t>(total) * 7);
         parallel(N, [&](int32_t c) {
-            std::vector<int32_t> used(nsph, 0);
-            for (const Spline& s : comps[c].under) {
-                const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
-                double* dst = &L->segs[7 * static_cast<size_t>(L->row_off[static_cast<size_t>(c) * S + slot])];
-                if (s.pts.size() == 1) {
-                    seg_prep(s.pts[0], s.pts[0], dst);
-                } else {
-                    for (size_t p = 0; p + 1 < s.pts.size(); ++p) seg_prep(s.pts[p], s.pts[p + 1], dst + 7 * p);
+            for (int32_t bd = 0; bd < B; ++bd) {
+                std::vector<int32_t> used(rb.bodies[bd].spheres.size(), 0);
+                for (const Spline& s : comps[c].under[bd]) {
+                    const int32_t slot = s.sphere * max_parts + used[s.sphere]++;
+                    double* dst = &L->segs[7 * static_cast<size_t>(L->row_off[(static_cast<size_t>(c) * B + bd) * S + slot])];
+                    if (s.pts.size() == 1) {
+                        seg_prep(s.pts[0], s.pts[0], dst);
+                    } else {
+                        for (size_t p = 0; p + 1 < s.pts.size(); ++p) seg_prep(s.pts[p], s.pts[p + 1], dst + 7 * p);
+                    }
                 }
             }
         });
         if (keep_poses) {
             L->pose_off.assign(static_cast<size_t>(N) + 1, 0);
             for (int32_t c = 0; c < N; ++c)
-                L->pose_off[c + 1] = L->pose_off[c] + static_cast<int64_t>(comps[c].fk.size());
-            L->poses.resize(static_cast<size_t>(L->pose_off[N]) * 12);
-            for (int32_t c = 0; c < N; ++c)
-                for (size_t k = 0; k < comps[c].fk.size(); ++k) {
-                    double* d = &L->poses[(static_cast<size_t>(L->pose_off[c]) + k) * 12];
-                    const Tf& T = comps[c].fk[k];
+                L->pose_off[c + 1] = L->pose_off[c] + static_cast<int64_t>(comps[c].fk.size() / B);
+            L->poses.resize(static_cast<size_t>(L->pose_off[N]) * B * 12);
+            parallel(N, [&](int32_t c) {
+                for (size_t q = 0; q < comps[c].fk.size(); ++q) {
+                    double* d = &L->poses[(static_cast<size_t>(L->pose_off[c]) * B + q) * 12];
+                    const Tf& T = comps[c].fk[q];
                     std::memcpy(d, T.r, 9 * sizeof(double));
                     d[9] = T.t.x, d[10] = T.t.y, d[11] = T.t.z;
                 }
+            });
         }
         mark("serialize");
-        *out = L;
+        *out = own.release();
         return 0;
     } catch (const std::exception& ex) {
         g_err = ex.what();

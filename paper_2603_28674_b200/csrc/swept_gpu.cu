@@ -100,10 +100,13 @@ __device__ void jacobi3(double m[3][3], double vals[3], V3 vecs[3]) {
 }
 
 // fit_box (producer.cpp) of the corners of n poses; out = centre, axes[3], half extents
-__global__ void fit_kernel(const double* poses, const int64_t* off, int ncomp, V3 he, const double* cs,
-                           double* out) {
+// one thread per fit unit c (a (component, body) pair; body c % nb, half extents he3[body])
+__global__ void fit_kernel(const double* poses, const int64_t* off, int ncomp, const double* he3, int nb,
+                           const double* cs, double* out) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= ncomp) return;
+    const int body = c % nb;
+    const V3 he{he3[3 * body], he3[3 * body + 1], he3[3 * body + 2]};
     const double* P = poses + 12 * static_cast<size_t>(off[c]);
     const int n = static_cast<int>(off[c + 1] - off[c]);
     const double npts = static_cast<double>(8 * n);
@@ -284,8 +287,9 @@ struct FitStream {
     double* dout = nullptr;
     double* stage[2] = {nullptr, nullptr};
     cudaEvent_t done[2] = {nullptr, nullptr};
-    int32_t ncomp = 0;
-    double he[3] = {0, 0, 0};
+    int32_t ncomp = 0;  // fit units
+    int32_t nb = 1;     // bodies: unit c fits body c % nb
+    double* dhe = nullptr;
 };
 
 void rggp_fit_end(void* p) {
@@ -293,7 +297,7 @@ void rggp_fit_end(void* p) {
     if (!f) return;
     cudaSetDevice(f->device);
     if (f->st) cudaStreamSynchronize(f->st);
-    cudaFree(f->dp), cudaFree(f->doff), cudaFree(f->dcs), cudaFree(f->dout);
+    cudaFree(f->dp), cudaFree(f->doff), cudaFree(f->dcs), cudaFree(f->dout), cudaFree(f->dhe);
     for (int k = 0; k < 2; ++k) {
         if (f->stage[k]) cudaFreeHost(f->stage[k]);
         if (f->done[k]) cudaEventDestroy(f->done[k]);
@@ -303,23 +307,25 @@ void rggp_fit_end(void* p) {
 }
 
 // chunk_configs: capacity of each staging buffer (configurations)
-void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin,
-                                int64_t chunk_configs, int32_t device) {
+void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, int32_t nbodies, const double* cos_sin,
+                     int64_t chunk_configs, int32_t device) {
     FitStream* f = new FitStream();
     f->device = device;
     f->ncomp = ncomp;
-    for (int k = 0; k < 3; ++k) f->he[k] = he3[k];
+    f->nb = nbodies;
     const size_t total = static_cast<size_t>(off[ncomp]);
     bool ok = cudaSetDevice(device) == cudaSuccess && cudaStreamCreateWithFlags(&f->st, cudaStreamNonBlocking) == cudaSuccess &&
               cudaMalloc(&f->dp, (total ? total : 1) * 96) == cudaSuccess &&
               cudaMalloc(&f->doff, (static_cast<size_t>(ncomp) + 1) * 8) == cudaSuccess &&
               cudaMalloc(&f->dcs, 22 * 8) == cudaSuccess &&
+              cudaMalloc(&f->dhe, static_cast<size_t>(nbodies) * 24) == cudaSuccess &&
               cudaMalloc(&f->dout, (static_cast<size_t>(ncomp) + 1) * 15 * 8) == cudaSuccess;
     for (int k = 0; ok && k < 2; ++k)
         ok = cudaHostAlloc(reinterpret_cast<void**>(&f->stage[k]), static_cast<size_t>(chunk_configs) * 96, 0) == cudaSuccess &&
              cudaEventCreateWithFlags(&f->done[k], cudaEventDisableTiming) == cudaSuccess && cudaEventRecord(f->done[k], f->st) == cudaSuccess;
     ok = ok && cudaMemcpyAsync(f->doff, off, (static_cast<size_t>(ncomp) + 1) * 8, cudaMemcpyHostToDevice, f->st) == cudaSuccess &&
          cudaMemcpyAsync(f->dcs, cos_sin, 22 * 8, cudaMemcpyHostToDevice, f->st) == cudaSuccess &&
+         cudaMemcpyAsync(f->dhe, he3, static_cast<size_t>(nbodies) * 24, cudaMemcpyHostToDevice, f->st) == cudaSuccess &&
          cudaStreamSynchronize(f->st) == cudaSuccess;
     if (!ok) {
         rggp_fit_end(f);
@@ -358,8 +364,7 @@ int rggp_fit_finish(void* p, double* out, const InnerSpec* spec, InnerOut* inner
     mark("copies");
     cudaError_t e = cudaSuccess;
     if (f->ncomp > 0) {
-        fit_kernel<<<(f->ncomp + 127) / 128, 128, 0, f->st>>>(f->dp, f->doff, f->ncomp, V3{f->he[0], f->he[1], f->he[2]},
-                                                              f->dcs, f->dout);
+        fit_kernel<<<(f->ncomp + 127) / 128, 128, 0, f->st>>>(f->dp, f->doff, f->ncomp, f->dhe, f->nb, f->dcs, f->dout);
         e = cudaGetLastError();
     }
     mark("kernel");

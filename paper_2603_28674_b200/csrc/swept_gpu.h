@@ -22,8 +22,10 @@ struct InnerOut {
     std::vector<double> pts;
 };
 
-void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, const double* cos_sin, int64_t chunk_configs,
-                     int32_t device);
+// ncomp fit units (one per (component, body)), unit c with the poses [off[c], off[c+1])
+// of body c % nbodies (half extents he3[3 * body]); chunk_configs = staging capacity (poses)
+void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, int32_t nbodies, const double* cos_sin,
+                     int64_t chunk_configs, int32_t device);
 double* rggp_fit_staging(void* fs, int32_t slot);
 int rggp_fit_push(void* fs, int32_t slot, int64_t first_config, int64_t nconfigs);
 // fit every component's box (ncomp x 15 doubles to out); with spec, also the splines

@@ -31,6 +31,8 @@ def library():
                                        C.POINTER(vp)]
         L.rgg_build_layout_ex.argtypes = [vp, C.c_int32, vp, C.c_int32, vp, C.c_double, C.c_int32, C.c_int32,
                                           C.c_int32, C.POINTER(vp)]
+        L.rgg_build_layout_robot.argtypes = [C.POINTER(_RobotView), C.c_int32, vp, C.c_int32, vp, C.c_double,
+                                             C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
         L.rgg_built_poses.argtypes = [vp, vp, vp, vp]
         L.rgg_built_counts.argtypes = [vp, vp]
         L.rgg_built_export.argtypes = [vp] * 7
@@ -43,29 +45,75 @@ def library():
     return _lib
 
 
+class _RobotView(C.Structure):
+    _fields_ = [("kinematics", C.c_int32), ("n_bodies", C.c_int32), ("half_extents", C.c_void_p),
+                ("local", C.c_void_p), ("joint_axis", C.c_void_p), ("joint_offset", C.c_void_p)]
+
+
+FREE_FLYING, SERIAL_CHAIN = 0, 1
+
+
+def free_flying(he) -> dict:
+    """make_free_flying_box (proj/src/robot.cpp:86-92): one box body, identity local frame."""
+    return dict(kinematics=FREE_FLYING, he=np.asarray(he, np.float64).reshape(1, 3))
+
+
+def serial_chain(links) -> dict:
+    """A serial chain as the scenario format's ``link`` lines (proj/src/scenario.cpp:144-157):
+    per link (axis[3], offset[3], half extents[3], local translation[3])."""
+    a = np.asarray(links, np.float64).reshape(-1, 12)
+    loc = np.zeros((len(a), 12))
+    loc[:, [0, 4, 8]] = 1.0
+    loc[:, 9:] = a[:, 9:12]
+    return dict(kinematics=SERIAL_CHAIN, axis=a[:, 0:3].copy(), offset=a[:, 3:6].copy(), he=a[:, 6:9].copy(), local=loc)
+
+
+def robot_dof(robot: dict) -> int:
+    return 6 if int(robot["kinematics"]) == FREE_FLYING else int(np.asarray(robot["he"]).reshape(-1, 3).shape[0])
+
+
 def gpu_available() -> bool:
     return library().rgg_build_gpu_count() > 0
 
 
 def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False, with_poses=False,
                  gpu_fit=None, gpu_inner=False):
-    """Components (nodes first, then edges) of a free-flying box robot -> store arrays.
-    with_poses: also a["pose_off"] (N+1) and a["poses"] (configs, 1, 12), the
+    """Components (nodes first, then edges) of a free-flying box robot -> store arrays
+    (build_layout_robot with free_flying(robot_he))."""
+    return build_layout_robot(free_flying(robot_he), nodes, edges, eps, max_segments, threads, with_obbs, with_poses,
+                              gpu_fit, gpu_inner)
+
+
+def build_layout_robot(robot: dict, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False,
+                       with_poses=False, gpu_fit=None, gpu_inner=False):
+    """build_components (proj/src/roadmap.cpp:104-127) + BatchLayout::serialize for any
+    robot: ``robot`` = {"kinematics": FREE_FLYING | SERIAL_CHAIN, "he" (B, 3), optional
+    "local" (B, 12), and for chains "axis" / "offset" (B, 3)}; nodes (n, dof).
+    with_poses: also a["pose_off"] (N+1) and a["poses"] (configs, B, 12), the
     forward kinematics of every discretized configuration (GPU exact resolve).
-    gpu_fit: the swept-volume box fit (obb_from_points, geometry.cpp:134-195) on the
-    GPU, bit-identical to the host fit (tests/test_gpu_producer.py) and faster end to
-    end at c5 (0.69 s against 1.20 s); None (the default) = when a GPU is present."""
+    gpu_fit: the swept-volume box fit (obb_from_points, geometry.cpp:134-195) of every
+    (component, body) on the GPU, bit-identical to the host fit (tests/test_gpu_producer.py);
+    None (the default) = when a GPU is present."""
     L = library()
     if gpu_fit is None:
         gpu_fit = gpu_available()
-    he = np.ascontiguousarray(robot_he, np.float64)
-    nodes = np.ascontiguousarray(nodes, np.float64)
+    he = np.ascontiguousarray(robot["he"], np.float64).reshape(-1, 3)
+    B = he.shape[0]
+    arrs = [he]
+    view = _RobotView(int(robot["kinematics"]), B, he.ctypes.data, None, None, None)
+    for key, field, width in (("local", "local", 12), ("axis", "joint_axis", 3), ("offset", "joint_offset", 3)):
+        if robot.get(key) is not None:
+            a = np.ascontiguousarray(robot[key], np.float64).reshape(B, width)
+            arrs.append(a)
+            setattr(view, field, a.ctypes.data)
+    dof = robot_dof(robot)
+    nodes = np.ascontiguousarray(nodes, np.float64).reshape(-1, dof)
     edges = np.ascontiguousarray(edges, np.int32).reshape(-1, 2)
     h = C.c_void_p()
-    rc = L.rgg_build_layout_ex(he.ctypes.data, len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
-                               float(eps), int(max_segments), int(threads),
-                               (1 if with_poses else 0) | (2 if gpu_fit else 0) | (4 if gpu_inner else 0),
-                               C.byref(h))
+    rc = L.rgg_build_layout_robot(C.byref(view), len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
+                                  float(eps), int(max_segments), int(threads),
+                                  (1 if with_poses else 0) | (2 if gpu_fit else 0) | (4 if gpu_inner else 0),
+                                  C.byref(h))
     if rc != 0:
         raise RuntimeError(L.rgg_build_last_error().decode())
     try:
@@ -80,7 +128,7 @@ def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, w
             if L.rgg_built_poses(h, C.byref(nc), None, None) != 0:
                 raise RuntimeError(L.rgg_build_last_error().decode())
             a["pose_off"] = np.empty(N + 1, np.int64)
-            a["poses"] = np.empty((nc.value, 1, 12))
+            a["poses"] = np.empty((nc.value, B, 12))
             L.rgg_built_poses(h, None, a["pose_off"].ctypes.data, a["poses"].ctypes.data)
     finally:
         L.rgg_built_free(h)

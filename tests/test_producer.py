@@ -42,3 +42,98 @@ def test_producer_poses_match_reference_fk(kind, n, k, half, seed):
     assert np.array_equal(a["pose_off"], off)
     assert np.array_equal(a["poses"].view(np.uint64), poses.view(np.uint64))
     assert np.array_equal(w.body_half_extents(), np.asarray(rm.robot_he).reshape(1, 3))
+
+
+def _chain_case(seed, n=60, k=5):
+    """A 4-link chain with a rotated body frame, over uniform joint angles."""
+    from paper_2603_28674_b200 import synth
+
+    links = [[0, 0, 1, 0, 0, 0, 0.4, 0.12, 0.1, 0.4, 0, 0],
+             [0, 1, 0, 0.8, 0, 0, 0.35, 0.1, 0.1, 0.35, 0, 0],
+             [1, 1, 0, 0.7, 0, 0.1, 0.3, 0.09, 0.12, 0.3, 0, 0],
+             [0, 0, 1, 0.6, 0, 0, 0.2, 0.1, 0.1, 0.2, 0, 0.05]]
+    robot = producer.serial_chain(links)
+    c, s = np.cos(0.3), np.sin(0.3)
+    robot["local"][2, :9] = [c, -s, 0, s, c, 0, 0, 0, 1]  # a rotated body frame (robot.hpp BoxBody::local)
+    rng = np.random.default_rng(seed)
+    nodes = rng.uniform(-np.pi, np.pi, (n, 4))
+    return robot, nodes, synth.knn_edges(nodes, k)
+
+
+def _compare(a, L, w):
+    for key in ("edge_sat", "comp_aabb", "segs", "spline_r"):
+        assert np.array_equal(a[key].view(np.uint64), getattr(L, key).view(np.uint64)), key
+    assert np.array_equal(a["row_off"], L.row_off)
+    assert np.array_equal(a["obb15"], w.obbs())
+    off, poses = w.poses()
+    assert np.array_equal(a["pose_off"], off)
+    assert np.array_equal(a["poses"].view(np.uint64), poses.view(np.uint64))
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_serial_chain_producer_matches_reference_manipulator():
+    """table5_manipulator_100's six-link chain (its own PRM roadmap, eps 0.02): every
+    SatBox, AABB, real segment, slot radius, fitted OBB and forward-kinematics pose equals
+    the reference's build_components + serialize (robot.cpp:66-84 serial branch,
+    swept.cpp:100-228, center_lipschitz's chain bound, batch_layout.cpp:21-146 with B = 6)."""
+    import os
+
+    from conftest import GOLDEN
+
+    w = ref.World.from_scn(open(os.path.join(GOLDEN, "scenarios", "table5_manipulator_100.scn")).read())
+    r = w.robot()
+    nodes, edges = w.roadmap()
+    N, B, S, a = producer.build_layout_robot(r, nodes, edges, r["eps"], r["max_segments"], threads=4,
+                                             with_obbs=True, with_poses=True, gpu_fit=False)
+    L = w.layout()
+    assert (N, B, S) == (L.N, L.B, L.S) and B == 6
+    _compare(a, L, w)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed,eps", [(3, 0.05), (4, 0.11)])
+def test_serial_chain_producer_matches_reference_random(seed, eps):
+    """A synthetic 4-link chain (a tilted joint axis, a rotated body frame, a body offset
+    along z) over random joint angles: the layout equals the reference's."""
+    robot, nodes, edges = _chain_case(seed)
+    env = np.array([-4, -4, -4, 4, 4, 4.0])
+    w = ref.World.from_robot(robot, env, nodes, edges, eps)
+    N, B, S, a = producer.build_layout_robot(robot, nodes, edges, eps, 16, threads=3, with_obbs=True,
+                                             with_poses=True, gpu_fit=False)
+    L = w.layout()
+    assert (N, B, S) == (L.N, L.B, L.S)
+    _compare(a, L, w)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_free_flying_multibody_matches_reference():
+    """A free-flying robot of two bodies (robot.cpp:71-74: every body rides the world frame
+    through its own local frame)."""
+    from paper_2603_28674_b200 import synth
+
+    loc = np.zeros((2, 12))
+    loc[:, [0, 4, 8]] = 1.0
+    loc[1, 9:] = [0.9, 0.0, 0.2]
+    robot = dict(kinematics=producer.FREE_FLYING, he=np.array([[0.5, 0.2, 0.2], [0.3, 0.3, 0.1]]), local=loc)
+    rm = synth.make_roadmap("3d", 80, 6, 4.0, 12)
+    w = ref.World.from_robot(robot, rm.env, rm.nodes, rm.edges, 0.25)
+    N, B, S, a = producer.build_layout_robot(robot, rm.nodes, rm.edges, 0.25, 16, threads=2, with_obbs=True,
+                                             with_poses=True, gpu_fit=False)
+    assert B == 2
+    _compare(a, w.layout(), w)
+
+
+def test_robot_validation_errors():
+    """RobotModel::validate's errors (robot.cpp:17-37) surface as the producer's."""
+    nodes = np.zeros((2, 2))
+    edges = np.array([[0, 1]])
+    bad_axis = producer.serial_chain([[0, 0, 0, 0, 0, 0, 0.3, 0.1, 0.1, 0, 0, 0]] * 2)
+    with pytest.raises(RuntimeError, match="joint axis/offset invalid"):
+        producer.build_layout_robot(bad_axis, nodes, edges, 0.1, gpu_fit=False)
+    bad_he = producer.serial_chain([[0, 0, 1, 0, 0, 0, 0.0, 0.1, 0.1, 0, 0, 0]] * 2)
+    with pytest.raises(RuntimeError, match="half extents must be positive"):
+        producer.build_layout_robot(bad_he, nodes, edges, 0.1, gpu_fit=False)
+    skew = producer.serial_chain([[0, 0, 1, 0, 0, 0, 0.3, 0.1, 0.1, 0, 0, 0]] * 2)
+    skew["local"][0, 1] = 0.5
+    with pytest.raises(RuntimeError, match="local frame invalid"):
+        producer.build_layout_robot(skew, nodes, edges, 0.1, gpu_fit=False)
