@@ -106,7 +106,8 @@ def workload_name(config, n_components):
 
     kind, nodes, k, half, m, ohalf = synth.CONFIGS[config]
     mv = synth.MOVES_PER_STEP.get(config)
-    step = (f"1 step = 1 update = {mv} of the {m} obstacles re-posed (rotating subset, ~5 % of cells dirty)"
+    step = (f"1 step = 1 update = {mv} of the {m} obstacles re-posed (rotating subset, ~5 % of cells dirty: "
+            f"see dirty_fraction)"
             if mv else f"1 step = 1 update = all {m} obstacles re-posed")
     return (f"{config}: {'SE(2)' if kind == 'se2' else '3D'} roadmap {nodes} nodes k={k} ({n_components} components "
             f"incl. nodes) x {m} moving OBB obstacles; {step} (per-move reports, gray-id list compacted on device)")

@@ -1,4 +1,5 @@
-"""Replay a few c2 updates through the engine (profiling driver: launch lists / ncu)."""
+"""Replay a few updates of a config through the engine (profiling driver: launch lists / ncu):
+python tools/step_once.py STEPS CONFIG [gray]."""
 import sys
 sys.path.insert(0, '.')
 from paper_2603_28674_b200 import engine as E, producer
@@ -10,5 +11,5 @@ lv = producer.layout_for(rm, obs)
 ids, rts = bench.world_moves(cfg, 1, 12345, steps)
 eng = E.GpuEngine(lv)
 for it in range(steps):
-    eng.batch_update((ids[it], rts[it]), per_move=True)
+    eng.batch_update((ids[it], rts[it]), per_move=True, gray_list=len(sys.argv) > 3 and sys.argv[3] == "gray")
 print("done", eng.last_stats())
