@@ -212,7 +212,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     h->units_cap = static_cast<int32_t>(units);
     CK(dalloc(&h->d_units, static_cast<size_t>(units)));
     CK(dalloc(&h->d_unit_ready, static_cast<size_t>(units)));
-    CK(cudaMemset(h->d_unit_ready, 0, static_cast<size_t>(units) * sizeof(int32_t)));
+    CK(cudaMemsetAsync(h->d_unit_ready, 0, static_cast<size_t>(units) * sizeof(int32_t), h->stream));
     CK(dalloc(&h->d_mv, static_cast<size_t>(cap) * 4));
     // every (cell, event) pair fits: the overflow pool can never run out
     h->pool_cap = std::max<int64_t>(1, static_cast<int64_t>(h->s.ncells) * cap);
@@ -225,7 +225,7 @@ int grow_batch(rgg_gpu* h, int32_t n) {
     h->cmask_words = (cap + 31) / 32;
     const size_t cm = std::max<size_t>(1, static_cast<size_t>(h->s.ncells) * h->cmask_words);
     CK(dalloc(&h->d_cmask, cm));
-    CK(cudaMemset(h->d_cmask, 0, cm * sizeof(uint32_t)));
+    CK(cudaMemsetAsync(h->d_cmask, 0, cm * sizeof(uint32_t), h->stream));
     h->cap_moves = cap;
     ++h->gen;  // buffers moved: captured graphs are stale
     return RGG_OK;
@@ -297,7 +297,7 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.tl = h->d_tl;
     if (!h->d_evready) {
         cudaMalloc(reinterpret_cast<void**>(&h->d_evready), 8 * sizeof(int32_t));
-        cudaMemset(h->d_evready, 0, 8 * sizeof(int32_t));
+        cudaMemsetAsync(h->d_evready, 0, 8 * sizeof(int32_t), h->stream);
     }
     static const bool no_early_bin = std::getenv("RGG_NO_EARLY_BIN") != nullptr;  // tests: the plain PDL waits
     b.evready = no_early_bin ? nullptr : h->d_evready;
@@ -1256,12 +1256,17 @@ int rgg_gpu_set_resolver(rgg_gpu* h, const rgg_resolve_view* v) {
     if (!h->d_res_ids) CK(dalloc(&h->d_res_ids, static_cast<size_t>(N) + 1));
     if (!h->d_res_out) CK(dalloc(&h->d_res_out, static_cast<size_t>(N) + 1));
     if (!h->d_res_cnt) CK(dalloc(&h->d_res_cnt, 1));
-    CK(cudaMemcpy(h->d_res_he, v->body_half_extents, static_cast<size_t>(B) * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    // stream-ordered copies: a synchronous cudaMemcpy from pageable memory runs on the
+    // legacy stream and may return before its DMA lands, unordered with h->stream's kernels
+    CK(cudaMemcpyAsync(h->d_res_he, v->body_half_extents, static_cast<size_t>(B) * 3 * sizeof(double),
+                       cudaMemcpyHostToDevice, h->stream));
     static_assert(sizeof(long long) == sizeof(int64_t), "int64 offsets");
-    CK(cudaMemcpy(h->d_res_off, v->pose_off, (static_cast<size_t>(N) + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(h->d_res_off, v->pose_off, (static_cast<size_t>(N) + 1) * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, h->stream));
     if (total > 0)
-        CK(cudaMemcpy(h->d_res_pose, v->poses, static_cast<size_t>(total) * B * 12 * sizeof(double),
-                      cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(h->d_res_pose, v->poses, static_cast<size_t>(total) * B * 12 * sizeof(double),
+                           cudaMemcpyHostToDevice, h->stream));
+    CK(stream_wait(h));  // the caller's arrays may go away on return
     h->res_B = B;
     h->res_ready = true;
     ++h->gen;  // captured eager graphs hold the old resolver pointers
@@ -1287,9 +1292,12 @@ int rgg_gpu_set_active_obstacles(rgg_gpu* h, const int32_t* ids, const double* r
         CK(dalloc(&h->d_res_sact, static_cast<size_t>(M)));
         ++h->gen;  // captured eager graphs were built without these pointers
     }
-    CK(cudaStreamSynchronize(h->stream));  // a queued resolve may still read the old list
-    CK(cudaMemcpy(h->d_res_spose, pose.data(), pose.size() * sizeof(double), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_res_sact, act.data(), act.size(), cudaMemcpyHostToDevice));
+    // stream-ordered after any queued resolve that still reads the old list, and before the
+    // next update's (a synchronous pageable cudaMemcpy is neither: it runs on the legacy
+    // stream and may return before its DMA lands)
+    CK(cudaMemcpyAsync(h->d_res_spose, pose.data(), pose.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_res_sact, act.data(), act.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(stream_wait(h));
     return RGG_OK;
 }
 

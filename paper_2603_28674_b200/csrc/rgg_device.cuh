@@ -21,6 +21,10 @@ namespace rggd {
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+// x / len for a positive len (sat_prep's unit axes): a zero numerator returns x itself,
+// which is the IEEE quotient (a zero with x's sign); __ddiv_rn sends a zero numerator to
+// its out-of-line slow path (~100 instructions), and axis-aligned boxes have many
+__device__ __forceinline__ double div_pos(double x, double len) { return x == 0.0 ? x : __ddiv_rn(x, len); }
 
 // dot3 of kernels_scalar.cpp:35: (x0 y0 + x1 y1) + x2 y2
 __device__ __forceinline__ double dot3(const double* x, const double* y) {
@@ -281,7 +285,7 @@ __device__ __forceinline__ int sat_filter32(const double* ca, const Box32& a, co
 
 // The Box32 terms of one SatBox (fp64 e[9], u[9] at sat + 3, sat + 12).
 __host__ __device__ inline void box32_terms(const double* sat, Box32& x) {
-    double l1 = 0.0;
+    double l1 = 0.0, hd[3];
     bool degen = false;
     for (int k = 0; k < 3; ++k) {
         double n2 = 0.0, u2 = 0.0;
@@ -293,7 +297,8 @@ __host__ __device__ inline void box32_terms(const double* sat, Box32& x) {
             n2 += e * e;
             u2 += uu * uu;
         }
-        x.h[k] = static_cast<float>(sqrt(n2));
+        hd[k] = sqrt(n2);
+        x.h[k] = static_cast<float>(hd[k]);
         degen |= !(u2 > 0.5);
     }
     // sat_filter32g's margins equal the reference's for orthonormal frames with e_k = |e_k| u_k
@@ -304,7 +309,7 @@ __host__ __device__ inline void box32_terms(const double* sat, Box32& x) {
         const double* ei = sat + 3 + 3 * i;
         const double uu = ui[0] * ui[0] + ui[1] * ui[1] + ui[2] * ui[2];
         degen |= !(fabs(uu - 1.0) <= 1e-9);
-        const double h = sqrt(ei[0] * ei[0] + ei[1] * ei[1] + ei[2] * ei[2]);
+        const double h = hd[i];
         for (int k = 0; k < 3; ++k) degen |= !(fabs(ei[k] - h * ui[k]) <= 1e-9 * (h + 1e-300));
         for (int j = i + 1; j < 3; ++j) {
             const double* uj = sat + 12 + 3 * j;
@@ -543,7 +548,7 @@ __device__ __forceinline__ void sat_prep(const double* c, double* s) {
         if (n2 > 0.0) {
             const double len = __dsqrt_rn(n2);
 #pragma unroll
-            for (int j = 0; j < 3; ++j) s[12 + 3 * k + j] = __ddiv_rn(ek[j], len);
+            for (int j = 0; j < 3; ++j) s[12 + 3 * k + j] = div_pos(ek[j], len);
         } else {
             s[12 + 3 * k + 0] = s[12 + 3 * k + 1] = s[12 + 3 * k + 2] = 0.0;
         }

@@ -319,7 +319,7 @@ __global__ void pose_kernel(Store s, Batch b) {
         if (n2 > 0.0) {
             const double len = __dsqrt_rn(n2);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) u[k] = __ddiv_rn(e[k], len);
+            for (int k = 0; k < 3; ++k) u[k] = rggd::div_pos(e[k], len);
         } else {
             u[0] = u[1] = u[2] = 0.0;
         }

@@ -210,14 +210,14 @@ cudaError_t build_store(const StoreIn& in, StoreOut& out, cudaStream_t st) {
         SCK(scratch.alloc(&sat21, static_cast<size_t>(N) * B * 21));
         SCK(scratch.alloc(&row_off, static_cast<size_t>(N) * BS + 1));
         SCK(scratch.alloc(&segs7, static_cast<size_t>(in.T) * 7));
-        // pageable sources: plain synchronous copies (the driver pipelines them through
-        // its staging buffers; async pageable copies on a non-blocking stream were slower)
-        SCK(cudaMemcpy(aabb, in.comp_aabb, static_cast<size_t>(N) * 6 * 8, cudaMemcpyHostToDevice));
-        SCK(cudaMemcpy(sat21, in.edge_sat, static_cast<size_t>(N) * B * 21 * 8, cudaMemcpyHostToDevice));
-        SCK(cudaMemcpy(row_off, in.row_off, (static_cast<size_t>(N) * BS + 1) * 4, cudaMemcpyHostToDevice));
-        if (in.T) SCK(cudaMemcpy(segs7, in.segs, static_cast<size_t>(in.T) * 7 * 8, cudaMemcpyHostToDevice));
+        // pageable sources, copied in stream order: a synchronous cudaMemcpy runs on the
+        // legacy stream and may return before its DMA lands, unordered with st's kernels
+        SCK(cudaMemcpyAsync(aabb, in.comp_aabb, static_cast<size_t>(N) * 6 * 8, cudaMemcpyHostToDevice, st));
+        SCK(cudaMemcpyAsync(sat21, in.edge_sat, static_cast<size_t>(N) * B * 21 * 8, cudaMemcpyHostToDevice, st));
+        SCK(cudaMemcpyAsync(row_off, in.row_off, (static_cast<size_t>(N) * BS + 1) * 4, cudaMemcpyHostToDevice, st));
+        if (in.T) SCK(cudaMemcpyAsync(segs7, in.segs, static_cast<size_t>(in.T) * 7 * 8, cudaMemcpyHostToDevice, st));
     }
-    SCK(cudaMemcpy(out.spline, in.spline, static_cast<size_t>(BS) * 8, cudaMemcpyHostToDevice));
+    SCK(cudaMemcpyAsync(out.spline, in.spline, static_cast<size_t>(BS) * 8, cudaMemcpyHostToDevice, st));
     // 2. Morton order
     unsigned long long *bounds = nullptr, *key = nullptr, *key2 = nullptr;
     int32_t *val = nullptr, *order = nullptr;
@@ -384,8 +384,9 @@ cudaError_t build_cell_grid(const double* d_cell_aabb, int ncells, CellGrid& g, 
     }
     SCK(cudaMalloc(reinterpret_cast<void**>(&g.off), cnt.size() * 4));
     SCK(cudaMalloc(reinterpret_cast<void**>(&g.cells), lst.size() * sizeof(int2)));
-    SCK(cudaMemcpy(g.off, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice));
-    SCK(cudaMemcpy(g.cells, lst.data(), lst.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    SCK(cudaMemcpyAsync(g.off, cnt.data(), cnt.size() * 4, cudaMemcpyHostToDevice, st));
+    SCK(cudaMemcpyAsync(g.cells, lst.data(), lst.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    SCK(cudaStreamSynchronize(st));
     g.entries = cnt[total];
     return cudaSuccess;
 }

@@ -377,7 +377,8 @@ int rggp_fit_finish(void* p, double* out, const InnerSpec* spec, InnerOut* inner
         const int nsph = spec->nsph;
         const long long nt = static_cast<long long>(f->ncomp) * nsph;
         int64_t total = 0;
-        cudaMemcpy(&total, f->doff + f->ncomp, 8, cudaMemcpyDeviceToHost);
+        cudaMemcpyAsync(&total, f->doff + f->ncomp, 8, cudaMemcpyDeviceToHost, f->st);
+        cudaStreamSynchronize(f->st);
         double* dspec = nullptr;
         V3* raw = nullptr;
         int32_t *kept = nullptr, *dns = nullptr, *dnp = nullptr, *dsn = nullptr;
@@ -393,7 +394,7 @@ int rggp_fit_finish(void* p, double* out, const InnerSpec* spec, InnerOut* inner
         ok(cudaMalloc(&kept, static_cast<size_t>(total) * nsph * 4 + 16));
         ok(cudaMalloc(&dns, nt * 4));
         ok(cudaMalloc(&dnp, nt * 4));
-        ok(cudaMemcpy(dspec, hspec.data(), hspec.size() * 8, cudaMemcpyHostToDevice));
+        ok(cudaMemcpyAsync(dspec, hspec.data(), hspec.size() * 8, cudaMemcpyHostToDevice, f->st));
         const InnerDev sd{nsph, spec->K, dspec, dspec + 3 * nsph, dspec + 4 * nsph, dspec + 5 * nsph};
         const unsigned grid = static_cast<unsigned>((nt + 127) / 128);
         if (e == cudaSuccess) {
@@ -415,8 +416,8 @@ int rggp_fit_finish(void* p, double* out, const InnerSpec* spec, InnerOut* inner
         ok(cudaMalloc(&dpo, (nt + 1) * 8));
         ok(cudaMalloc(&dsn, so[nt] * 4 + 4));
         ok(cudaMalloc(&dpts, po[nt] * 24 + 8));
-        ok(cudaMemcpy(dso, so.data(), (nt + 1) * 8, cudaMemcpyHostToDevice));
-        ok(cudaMemcpy(dpo, po.data(), (nt + 1) * 8, cudaMemcpyHostToDevice));
+        ok(cudaMemcpyAsync(dso, so.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, f->st));
+        ok(cudaMemcpyAsync(dpo, po.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, f->st));
         if (e == cudaSuccess) {
             inner_kernel<false><<<grid, 128, 0, f->st>>>(f->dp, f->doff, f->ncomp, sd, raw, kept, nullptr, nullptr, dso,
                                                           dpo, dsn, dpts);
