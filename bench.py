@@ -565,7 +565,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # RGG_BENCH_DIST=1 (tests, under torchrun): the N > 1 path (NCCL collectives) at any N
+    if world > 1 or os.environ.get("RGG_BENCH_DIST") == "1":
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -678,6 +679,9 @@ def main():
 
         up_e2e = DistributedUpdater(eng_e2e, dev, gray_cap=up.gray_cap)
     e2e_s, d2h, ngray = [], [], 0
+    if dist is not None:  # the moves' pinned staging buffers, reused by every step
+        pin_ids = torch.empty((m_step,), dtype=torch.int32, pin_memory=True)
+        pin_rts = torch.empty((m_step, 12), dtype=torch.float64, pin_memory=True)
     for it in range(iterations):
         if it >= args.warmup:
             with torch.cuda.stream(stream):
@@ -690,8 +694,10 @@ def main():
             reps = eng_e2e.batch_update((ids_h[it], rts_h[it]), per_move=True, gray_list=True)
             gray = eng_e2e.gray_ids_view()  # one DMA into the engine's pinned host buffer
         else:
-            ids_t = torch.from_numpy(ids_h[it]).pin_memory().to(dev, non_blocking=True)
-            rts_t = torch.from_numpy(rts_h[it]).pin_memory().to(dev, non_blocking=True)
+            pin_ids.numpy()[:] = ids_h[it]
+            pin_rts.numpy()[:] = rts_h[it]
+            ids_t = pin_ids.to(dev, non_blocking=True)
+            rts_t = pin_rts.to(dev, non_blocking=True)
             reps = up_e2e.update(ids_t, rts_t, per_move=True, gather_gray=True).cpu()
             gray = up_e2e.gathered_gray()
         t1 = time.perf_counter()

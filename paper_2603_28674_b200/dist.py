@@ -49,6 +49,7 @@ class DistributedUpdater:
         self.id_offset = id_offset
         self.gray_cap = int(gray_cap)
         self._gray = None
+        self._pin = None  # pinned host buffer of gathered_gray
 
     def update(self, ids: torch.Tensor, rts: torch.Tensor, per_move: bool = True, check: bool = True,
                gather_gray: bool = False) -> torch.Tensor:
@@ -102,9 +103,23 @@ class DistributedUpdater:
         c = counts.cpu().numpy()
         if int(c.max(initial=0)) > cap:
             raise RuntimeError("a shard's gray list exceeds the gather capacity")
-        flat = lists.cpu().numpy()
-        parts = [flat[r * cap:r * cap + int(c[r])].astype(np.int64) for r in range(len(c))]
-        return np.sort(np.concatenate(parts)) if parts else np.zeros(0, np.int64)
+        # merge on the device (each shard's list is ascending; interleaved shards interleave
+        # their ids), then one copy of just the ids into a reused pinned buffer
+        total = int(c.sum())
+        if total == 0:
+            return np.zeros(0, np.int64)
+        if len(c) == 1:
+            merged = lists[:total]
+        else:
+            keep = torch.arange(cap, device=lists.device)[None, :] < counts.to(torch.int64)[:, None]
+            merged = torch.sort(lists.view(len(c), cap)[keep]).values
+        if not merged.is_cuda:
+            return merged.numpy().astype(np.int64)
+        if self._pin is None or self._pin.numel() < total:
+            self._pin = torch.empty(max(total, 1 << 16), dtype=torch.int32, pin_memory=True)
+        out = self._pin[:total]
+        out.copy_(merged)
+        return out.numpy().astype(np.int64)
 
     @staticmethod
     def reports(counters: torch.Tensor, unknown_before: int) -> list[dict]:
