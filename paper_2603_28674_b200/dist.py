@@ -93,8 +93,9 @@ class DistributedUpdater:
         self._gray = (counts, lists, cap)
 
     def gathered_gray(self) -> np.ndarray | None:
-        """The GRAY ids (ascending, global) gathered by the last ``update(gather_gray=True)``,
-        on rank 0 (None elsewhere).  Copies to the host."""
+        """The GRAY ids (ascending, global, int32) gathered by the last
+        ``update(gather_gray=True)``, on rank 0 (None elsewhere): one copy into a pinned
+        host buffer, returned as a view that the next call overwrites."""
         if self._gray is None:
             raise RuntimeError("no gray list gathered: call update(..., gather_gray=True)")
         if self.rank != 0:
@@ -107,19 +108,19 @@ class DistributedUpdater:
         # their ids), then one copy of just the ids into a reused pinned buffer
         total = int(c.sum())
         if total == 0:
-            return np.zeros(0, np.int64)
+            return np.zeros(0, np.int32)
         if len(c) == 1:
             merged = lists[:total]
         else:
             keep = torch.arange(cap, device=lists.device)[None, :] < counts.to(torch.int64)[:, None]
             merged = torch.sort(lists.view(len(c), cap)[keep]).values
         if not merged.is_cuda:
-            return merged.numpy().astype(np.int64)
+            return merged.numpy().copy()
         if self._pin is None or self._pin.numel() < total:
             self._pin = torch.empty(max(total, 1 << 16), dtype=torch.int32, pin_memory=True)
         out = self._pin[:total]
         out.copy_(merged)
-        return out.numpy().astype(np.int64)
+        return out.numpy()  # int32 view of the pinned buffer: valid until the next call
 
     @staticmethod
     def reports(counters: torch.Tensor, unknown_before: int) -> list[dict]:
