@@ -531,7 +531,7 @@ def roofline(census, kernel_ms, world, profile_json=None):
     roof = {"bound": "hbm" if t_by >= t_fl else "fp32",
             "achieved": byts / (kernel_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback B200_PROFILING.md",
-            "kernel": "the whole update (pose, bin scatter + cell lists, touch, narrow, apply, gray compaction: "
+            "kernel": "the whole update (pose, bin scatter + cell lists, touch, narrow over + under, apply, gray compaction: "
                       "paper_2603_28674_b200/csrc/rgg_kernels.cu), timed with CUDA events per update",
             "algorithmic": {"bytes_per_update": byts, "bytes_model": "SURVEY.md §8(d) fp32 model (DESIGN.md §4)",
                             "bytes_fp64_records": census["bytes_components"], "flops_per_update": flops,
@@ -738,8 +738,9 @@ def main():
                         "gray_ids_view() (rgg_gpu_gray_view: the gray ids DMA'd into pinned host memory)" + (" ; N>1: pinned H2D on every rank, DistributedUpdater (broadcast, "
                                             "all-reduce, gray gather), reports + gray ids D2H on rank 0"
                                             if world > 1 else "")},
-        "gpu_launches": 8 * args.steps,
-        "gpu_launches_note": "per update: pose, bin scatter, bin cells, touch, narrow, apply, gray count, gray write "
+        "gpu_launches": 9 * args.steps,
+        "gpu_launches_note": "per update: pose, bin scatter, bin cells, touch, narrow over, narrow under, apply, gray "
+                             "count, gray write "
                              "(one CUDA graph)",
         "phase_ms_mean": {k: statistics.mean(s[k] for s in stats) for k in
                           ("pose_ms", "bin_ms", "classify_ms", "compact_ms", "total_ms")},

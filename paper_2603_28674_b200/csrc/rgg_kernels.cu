@@ -930,55 +930,16 @@ __device__ __forceinline__ const int32_t* rec_list(int4 r) {
 }
 
 
-// The narrow tests of all items, GPU-wide (persistent grid), one thread per
-// item.  Over items {component, event, result word, bit}: the 15-axis SAT per
-// body.  Under items {segment, the pair's first segment, result word, event << 5 | bit}:
-// one real segment of the component against the event's spheres (a pair's segments
-// OR their verdicts into the same bit).  COUNT: the
-// reference's operation census (rgg_gpu_census) instead of the verdicts.
-template <bool COUNT>
-__global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
-    const unsigned long long tw = COUNT ? 0 : tl_start(b.tl);
-    pdl_wait();
-    pdl_trigger();
-    const unsigned long long t0 = COUNT ? 0 : tl_start(b.tl);
-    if (!COUNT) tl_stop(b.tl, 7, tw);
+// The reference's operation census of the last update's narrow items (rgg_gpu_census),
+// GPU-wide, one thread per item.  Over items {component, event, result word, bit}: the
+// 15-axis SAT per body.  Under items {segment, the pair's first segment, result word,
+// event << 5 | bit}: one real segment of the component against the event's spheres.
+// The verdicts themselves come from narrow_over_kernel / narrow_under_kernel below.
+__global__ void __launch_bounds__(128) narrow_census_kernel(Store s, Batch b) {
+    constexpr bool COUNT = true;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     const int n_over = min(b.ctr[8], b.items_cap), n_under = min(b.ctr[9], b.items_cap);
-    if (!COUNT) {
-        // One pass over both queues (over items first).  The item after next is
-        // loaded and the next item's operands are prefetched into L1 while the
-        // current one is tested: about one exposed memory round trip per item.
-        const int total = n_over + n_under;
-        const auto item = [&](int i) { return i < n_over ? b.items_over[i] : b.items_under[i - n_over]; };
-        int i = gt;
-        int4 it = i < total ? item(i) : make_int4(0, 0, 0, 0);
-        int4 nx = i + nthreads < total ? item(i + nthreads) : make_int4(0, 0, 0, 0);
-        while (i < total) {
-            const int inext = i + nthreads, i2 = inext + nthreads;
-            const int4 nn = i2 < total ? item(i2) : make_int4(0, 0, 0, 0);
-            if (inext < total) {
-                if (inext < n_over) {
-                    prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
-                    prefetch_l1(&b.ev[nx.y].b32);
-                } else {
-                    prefetch_l1(s.seg32 + 2 * static_cast<size_t>(nx.x));
-                    prefetch_l1(b.evs + kEvS * static_cast<size_t>(nx.w >> 5));
-                }
-            }
-            if (i < n_over) {
-                if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
-            } else if (under_range32(s, it.x, it.x + 1, b.evs + kEvS * static_cast<size_t>(it.w >> 5), b.ev[it.w >> 5])) {
-                atomicOr(&b.mpool[it.z], 1u << (it.w & 31));  // a pair's segments OR into one bit
-            }
-            it = nx;
-            nx = nn;
-            i = inext;
-        }
-        tl_stop(b.tl, 3, t0);
-        return;
-    }
     long long c_sat = 0, c_tests = 0, c_op = 0, c_up = 0, c_oh = 0, c_uh = 0;
     for (int i = gt; i < n_over; i += nthreads) {
         const int4 it = b.items_over[i];  // component, event, result word, bit
@@ -997,6 +958,58 @@ __global__ void __launch_bounds__(128) narrow_kernel(Store s, Batch b) {
         for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
         if (lane == 0 && x) atomicAdd(&b.census[k], static_cast<unsigned long long>(x));
     }
+}
+
+// The narrow tests split by item kind, so each kernel gets the registers (and hence the
+// occupancy) its own test needs: the SAT filter of the over items, the segment-sphere
+// filter of the under items.  narrow_over_kernel waits for touch (PDL) and triggers
+// right away; narrow_under_kernel's CTAs therefore start only after every over CTA is
+// past its wait (touch complete, its items visible), run without a wait of their own,
+// and wait for narrow_over_kernel before they exit, so the apply kernel's wait on
+// narrow_under_kernel covers both.
+__global__ void __launch_bounds__(128) narrow_over_kernel(Store s, Batch b) {
+    pdl_wait();
+    pdl_trigger();
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+    const int total = min(b.ctr[8], b.items_cap);
+    int i = gt;
+    int4 it = i < total ? b.items_over[i] : make_int4(0, 0, 0, 0);
+    int4 nx = i + nthreads < total ? b.items_over[i + nthreads] : make_int4(0, 0, 0, 0);
+    while (i < total) {
+        const int inext = i + nthreads, i2 = inext + nthreads;
+        const int4 nn = i2 < total ? b.items_over[i2] : make_int4(0, 0, 0, 0);
+        if (inext < total) {
+            prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
+            prefetch_l1(&b.ev[nx.y].b32);
+        }
+        if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+        it = nx;
+        nx = nn;
+        i = inext;
+    }
+}
+
+__global__ void __launch_bounds__(128) narrow_under_kernel(Store s, Batch b) {
+    pdl_trigger();
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+    const int total = min(b.ctr[9], b.items_cap);
+    int i = gt;
+    int4 it = i < total ? b.items_under[i] : make_int4(0, 0, 0, 0);
+    int4 nx = i + nthreads < total ? b.items_under[i + nthreads] : make_int4(0, 0, 0, 0);
+    while (i < total) {
+        const int inext = i + nthreads, i2 = inext + nthreads;
+        const int4 nn = i2 < total ? b.items_under[i2] : make_int4(0, 0, 0, 0);
+        if (inext < total) {
+            prefetch_l1(s.seg32 + 2 * static_cast<size_t>(nx.x));
+            prefetch_l1(b.evs + kEvS * static_cast<size_t>(nx.w >> 5));
+        }
+        if (under_range32(s, it.x, it.x + 1, b.evs + kEvS * static_cast<size_t>(it.w >> 5), b.ev[it.w >> 5]))
+            atomicOr(&b.mpool[it.z], 1u << (it.w & 31));  // a pair's segments OR into one bit
+        it = nx;
+        nx = nn;
+        i = inext;
+    }
+    pdl_wait();  // narrow_over_kernel is complete before this grid is
 }
 
 // ------------------------------------------------- warp-slice touch / GPU-wide narrow / warp-slice apply
@@ -1901,13 +1914,26 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
     if (flags & kCensus) {
         touch_warp_kernel<true><<<grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<true>)),
                                   32 * kWarpsPerCta, 0, st>>>(s, b);
-        narrow_kernel<true><<<grid, 128, 0, st>>>(s, b);
+        narrow_census_kernel<<<grid, 128, 0, st>>>(s, b);
         return cudaGetLastError();
     }
     cudaError_t e = launch_pdl(touch_warp_kernel<false>,
                                dim3(grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>))),
                                dim3(32 * kWarpsPerCta), st, s, b);
-    if (e == cudaSuccess) e = launch_pdl(narrow_kernel<false>, dim3(grid), dim3(128), st, s, b);
+    {
+        static int g_over = 0, g_under = 0;
+        if (!g_over) {
+            int sms = 148, dev = 0, n = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_over_kernel, 128, 0);
+            g_over = sms * std::max(1, n);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_under_kernel, 128, 0);
+            g_under = sms * std::max(1, n);
+        }
+        if (e == cudaSuccess) e = launch_pdl(narrow_over_kernel, dim3(g_over), dim3(128), st, s, b);
+        if (e == cudaSuccess) e = launch_pdl(narrow_under_kernel, dim3(g_under), dim3(128), st, s, b);
+    }
     if (e != cudaSuccess) return e;
     const bool wide = s.W > 1;
     switch (flags & (kPerMove | kHits)) {
@@ -1932,7 +1958,7 @@ void filter_stats(unsigned long long* out, bool reset) {
 
 int classify_occupancy(int, int) {
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_kernel<false>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_census_kernel, 128, 0);
     return n < 1 ? 1 : n;
 }
 
