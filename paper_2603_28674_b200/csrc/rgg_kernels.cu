@@ -936,7 +936,6 @@ __device__ __forceinline__ const int32_t* rec_list(int4 r) {
 // event << 5 | bit}: one real segment of the component against the event's spheres.
 // The verdicts themselves come from narrow_over_kernel / narrow_under_kernel below.
 __global__ void __launch_bounds__(128) narrow_census_kernel(Store s, Batch b) {
-    constexpr bool COUNT = true;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31;
     const int n_over = min(b.ctr[8], b.items_cap), n_under = min(b.ctr[9], b.items_cap);
@@ -1242,6 +1241,128 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
             for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
             if (lane == 0 && x) atomicAdd(&b.census[8 + k], x);
         }
+    }
+}
+
+// touch, one CTA per work unit (a cell's chunk of <= 32 listed events): warp w takes the
+// cell's slice w (kWarpsPerCta == slices per cell at 128-component cells), so the chunk's
+// event boxes are staged once per CTA (all 128 threads load them) instead of once per
+// slice, and the CTA reserves its narrow items with one atomic instead of four.  The
+// tests and items are touch_warp_kernel's; that kernel remains for the census and for the
+// published-unit handoff (Batch::unit_ready).
+__global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, Batch b) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ double sbx[32][24];
+    __shared__ int sev[32];
+    __shared__ unsigned long long s_res[kWarpsPerCta], s_base;
+    const int tid = threadIdx.x, wi = tid >> 5, lane = tid & 31;
+    {
+        const char* p = reinterpret_cast<const char*>(b.evt);
+        const int lines = (b.n * 24 * 8 + 127) >> 7;
+        for (int l = tid; l < min(lines, 256); l += blockDim.x) prefetch_l1(p + (static_cast<size_t>(l) << 7));
+    }
+    const int spc = s.cell >> 5;  // slices per cell (<= kWarpsPerCta)
+    const int n_rec = min(b.ctr[10], b.units_cap);
+    for (int r = blockIdx.x; r < n_rec; r += gridDim.x) {
+        const int4 un = b.units[r];  // {cell, chunk, count, mask base}
+        const int cell = un.x, w = un.y, count = un.z;
+        const int q = cell * spc + wi, c0 = q << 5;
+        const bool has_slice = wi < spc && c0 < s.Np;
+        const int c = c0 + lane, t = c - cell * s.cell;
+        const bool valid = has_slice && c < s.Np;
+        // this warp's slice operands (independent of the staging below)
+        double aabb[6], sbox[6];
+        int seg_lo = 0, seg_hi = 0;
+        if (has_slice) {
+#pragma unroll
+            for (int j = 0; j < 6; ++j) sbox[j] = s.slice_aabb[6 * static_cast<size_t>(q) + j];
+        }
+        if (valid) {
+            const double2 a0 = s.aabb[c], a1 = s.aabb[s.Np + c], a2 = s.aabb[2 * s.Np + c];
+            aabb[0] = a0.x, aabb[1] = a0.y, aabb[2] = a1.x, aabb[3] = a1.y, aabb[4] = a2.x, aabb[5] = a2.y;
+            seg_lo = s.row[c * s.B * s.S];
+            seg_hi = s.row[(c + 1) * s.B * s.S];
+        }
+        // stage the chunk's event boxes: 12 double2 per event over the CTA's threads
+        const int32_t* list = count <= s.cap ? b.cell_list + static_cast<size_t>(cell) * s.cap : b.pool + b.cell_ovf[cell];
+        const int W = (count + 31) >> 5, base = 32 * w, m = min(32, count - base);
+        for (int x = tid; x < m * 12; x += blockDim.x) {
+            const int e = x / 12, j = x - 12 * e;
+            const int ev = list[base + e];
+            const double2 v = reinterpret_cast<const double2*>(b.evt + 24 * static_cast<size_t>(ev))[j];
+            sbx[e][2 * j] = v.x;
+            sbx[e][2 * j + 1] = v.y;
+            if (j == 0) sev[e] = ev;
+        }
+        __syncthreads();
+        uint32_t tm = 0, bm = 0, sm = 0;
+        if (has_slice) {
+            // the chunk's events whose new or old box meets the slice's box
+            bool near = false;
+            if (lane < m) near = rggd::overlaps(sbox, sbx[lane]) | rggd::overlaps(sbox, sbx[lane] + 6);
+            const uint32_t smask = __ballot_sync(0xffffffffu, near);
+            if (valid) {
+                for (uint32_t x = smask; x; x &= x - 1) {
+                    const int kk = __ffs(x) - 1;
+                    const double* bx = sbx[kk];
+                    const bool touch = rggd::overlaps(aabb, bx) | rggd::overlaps(aabb, bx + 6);
+                    tm |= static_cast<uint32_t>(touch) << kk;
+                    bm |= static_cast<uint32_t>(touch & rggd::overlaps(aabb, bx + 12)) << kk;
+                    sm |= static_cast<uint32_t>(touch & (s.use_under != 0) & rggd::overlaps(aabb, bx + 18)) << kk;
+                }
+            }
+            // the narrow kernels (next launches) read exactly these operands: stage them in L2
+            if (bm && w == 0 && s.prefetch) {
+                const size_t i0 = static_cast<size_t>(c) * s.B;
+                prefetch_range(s.sat32 + i0, s.sat32 + i0 + s.B, false);
+            }
+            if (sm && w == 0 && s.prefetch)
+                prefetch_range(s.seg32 + 2 * static_cast<size_t>(seg_lo), s.seg32 + 2 * static_cast<size_t>(seg_hi), false);
+        }
+        const int wt = un.w + (0 * W + w) * s.cell + t, wo = un.w + (1 * W + w) * s.cell + t,
+                  wu = un.w + (2 * W + w) * s.cell + t;
+        if (valid) {
+            b.mpool[wt] = tm;
+            b.mpool[wo] = 0;
+            b.mpool[wu] = 0;
+        }
+        // one packed reservation per CTA for both queues (ctr[8] over items, ctr[9] under
+        // items per (pair, segment)); a full queue is reported through ctr[6] = 3
+        const unsigned long long mine = static_cast<unsigned long long>(__popc(bm)) |
+                                        (static_cast<unsigned long long>(__popc(sm) * (seg_hi - seg_lo)) << 32);
+        unsigned long long x = mine;
+        for (int off = 1; off < 32; off <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, off);
+            if (lane >= off) x += y;
+        }
+        if (lane == 31) s_res[wi] = x;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long tot = 0;
+            for (int v = 0; v < kWarpsPerCta; ++v) tot += s_res[v];
+            s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(&b.ctr[8]), tot) : 0ull;
+        }
+        __syncthreads();
+        unsigned long long wbase = s_base;
+        for (int v = 0; v < wi; ++v) wbase += s_res[v];
+        const unsigned long long at64 = wbase + x - mine;
+        int at = static_cast<int>(at64 & 0xffffffffu);
+        for (uint32_t y = bm; y; y &= y - 1, ++at) {
+            const int kk = __ffs(y) - 1;
+            if (at < b.items_cap) b.items_over[at] = make_int4(c, sev[kk], wo, 1 << kk);
+            else b.ctr[6] = 3;
+        }
+        at = static_cast<int>(at64 >> 32);
+        for (uint32_t y = sm; y; y &= y - 1) {
+            const int kk = __ffs(y) - 1;
+            const int w4 = (sev[kk] << 5) | kk;
+            for (int j = seg_lo; j < seg_hi; ++j, ++at) {  // {segment, the pair's first segment, word, event|bit}
+                if (at < b.items_cap) b.items_under[at] = make_int4(j, seg_lo, wu, w4);
+                else b.ctr[6] = 3;
+            }
+        }
+        __syncthreads();  // sbx / sev / s_res are restaged by the next unit
     }
 }
 
@@ -1919,9 +2040,15 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
         narrow_census_kernel<<<grid, 128, 0, st>>>(s, b);
         return cudaGetLastError();
     }
-    cudaError_t e = launch_pdl(touch_warp_kernel<false>,
-                               dim3(grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>))),
-                               dim3(32 * kWarpsPerCta), st, s, b);
+    // touch: one CTA per work unit when a cell's slices fill the CTA's warps (128-component
+    // cells), else (and for the published-unit handoff) one warp per (slice, unit)
+    static const bool warp_touch = std::getenv("RGG_WARP_TOUCH") != nullptr;
+    const bool cta = !warp_touch && !b.unit_ready && (s.cell >> 5) == kWarpsPerCta;
+    cudaError_t e = cta ? launch_pdl(touch_cta_kernel, dim3(grid_slices(s, reinterpret_cast<const void*>(touch_cta_kernel))),
+                                     dim3(32 * kWarpsPerCta), st, s, b)
+                        : launch_pdl(touch_warp_kernel<false>,
+                                     dim3(grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>))),
+                                     dim3(32 * kWarpsPerCta), st, s, b);
     {
         static int g_over = 0, g_under = 0;
         if (!g_over) {
