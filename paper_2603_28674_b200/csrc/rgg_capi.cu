@@ -144,6 +144,11 @@ struct rgg_gpu {
     bool poisoned = false;  // a failed eager batch left a partial state (rgg_gpu_update fails from then on)
     int32_t* h_gray = nullptr;  // pinned host copy of the gray list (rgg_gpu_gray_view)
     int32_t gray_pin_cap = 0;
+    // mapped pinned gray list (capacity N) that a synchronous host update with RGG_GRAY_LIST
+    // writes inside the update; gray_host_fresh: it holds the current labels' list
+    int32_t* h_gray_map = nullptr;
+    int32_t* dh_gray_map = nullptr;
+    bool gray_host_fresh = false;
 };
 
 namespace {
@@ -410,6 +415,13 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // buffer (no copy node); large ones (a 1024-move batch is 100 KB, read by every pose
     // warp over PCIe) get one H2D copy node into HBM before the pose kernel
     const bool mapped_moves = hostio && n <= kMappedMovesMax;
+    // the gray list of a synchronous host update goes straight to mapped host memory
+    const bool gray_host = hostio && gray_list && h->s.N > 0;
+    if (gray_host && !h->h_gray_map) {
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_gray_map), static_cast<size_t>(h->s.N) * sizeof(int32_t),
+                         cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->dh_gray_map), h->h_gray_map, 0));
+    }
     if (mapped_moves) {
         b.src_ids = h->dh_ids;
         b.src_rt = reinterpret_cast<const double*>(reinterpret_cast<const char*>(h->dh_ids) + h->pin_off);
@@ -447,7 +459,8 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess && eager) e = resolve_hits();
             if (e == cudaSuccess) e = rec(h->ev[3]);
             if (e == cudaSuccess && gray_list)
-                e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream);
+                e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream,
+                                         gray_host ? h->dh_gray_map : nullptr);
             if (e == cudaSuccess) e = rec(h->ev[4]);
             if (e == cudaSuccess && hostio && !out_in_kernel && (flags & RGG_PER_MOVE))
                 e = cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(n) * 4 * sizeof(int32_t),
@@ -465,6 +478,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
         if (h->d_tl) CK(cudaMemsetAsync(h->d_tl, 0, 128 * 8, h->stream));
         CK(cudaGraphLaunch(exec, h->stream));
         h->gray_fresh = gray_list;
+        h->gray_host_fresh = gray_host;
         h->last_n = n;
         h->last_flags = flags;
         h->last_single = single;
@@ -487,6 +501,7 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     if (gray_list) CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
     CK(cudaEventRecord(h->ev[4], h->stream));
     h->gray_fresh = gray_list;
+    h->gray_host_fresh = false;
     h->last_n = n;
     h->last_flags = flags;
     h->last_single = single;
@@ -806,7 +821,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
                    h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr, h->h_eg_rep, h->h_gray};
+    void* pin[] = {h->h_ids, h->h_mv, h->h_ctr, h->h_eg_rep, h->h_gray, h->h_gray_map};
     for (void* p : pin)
         if (p) cudaFreeHost(p);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
@@ -1152,6 +1167,11 @@ int rgg_gpu_gray_device(rgg_gpu* h, int32_t* d_count, int32_t* d_ids, int32_t ca
 int rgg_gpu_gray_view(rgg_gpu* h, const int32_t** ids, int32_t* n) {
     if (!h || !ids || !n) return RGG_EINVAL;
     CK(cudaSetDevice(h->device));
+    if (h->gray_host_fresh) {  // written by the last update itself (synchronous, RGG_GRAY_LIST);
+        *ids = h->h_gray_map;    // its count came back with the update's counters (ctr[4])
+        *n = h->h_ctr[4];
+        return RGG_OK;
+    }
     if (!h->gray_fresh) {
         CK(rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream));
         h->gray_fresh = true;
@@ -1212,6 +1232,7 @@ int rgg_gpu_write_states(rgg_gpu* h, const int32_t* ids, const uint8_t* st, int3
     CK(cudaMemcpyAsync(h->d_unknown, h->d_ctr + 4, sizeof(int32_t), cudaMemcpyDeviceToDevice, h->stream));
     CK(stream_wait(h));
     h->gray_fresh = true;
+    h->gray_host_fresh = false;
     cudaFree(d_ids);
     cudaFree(d_st);
     h->unknown_stale = true;
@@ -1316,6 +1337,7 @@ int rgg_gpu_resolve_all(rgg_gpu* h, int32_t* resolved) {
         CK(stream_wait(h));
     }
     h->gray_fresh = false;
+    h->gray_host_fresh = false;
     h->unknown_stale = true;
     h->last_hits_valid = false;
     rc = refresh_unknown(h);

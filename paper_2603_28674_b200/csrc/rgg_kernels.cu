@@ -1767,12 +1767,17 @@ __global__ void __launch_bounds__(kCompactThreads) gray_count_kernel(const uint8
     }
 }
 
+// host_out (synchronous host updates with the gray list): the same ids, also written into
+// mapped pinned host memory, through shared memory so each tile's contiguous output range
+// goes over PCIe in 16-byte stores (the host reads the list when the update returns)
 __global__ void __launch_bounds__(kCompactThreads) gray_write_kernel(const uint8_t* st, int N, const int32_t* tile_cnt,
-                                                                     int ntiles, int32_t* out, int32_t* gray_n) {
+                                                                     int ntiles, int32_t* out, int32_t* gray_n,
+                                                                     int32_t* host_out) {
     pdl_wait();
     pdl_trigger();
     __shared__ int ws[kCompactThreads / 32];
     __shared__ int s_base;
+    __shared__ __align__(16) int32_t s_ids[kTile + 4];
     // tile base = sum of earlier tiles
     int acc = 0;
     for (int t = threadIdx.x; t < blockIdx.x; t += kCompactThreads) acc += tile_cnt[t];
@@ -1809,10 +1814,35 @@ __global__ void __launch_bounds__(kCompactThreads) gray_write_kernel(const uint8
     }
     __syncthreads();
     int pos = s_base + x - n + (warp > 0 ? ws[warp - 1] : 0);
+    if (!host_out) {
+        if (n) {
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+            for (int i = 0; i < 16; ++i)
+                if (b[i] == 2) out[pos++] = base + i;
+        }
+        return;
+    }
+    // the tile's ids in shared memory at their offset from the 16-byte-aligned start of
+    // its output range, then copied out as int4 (host and device)
+    const int lo = s_base & ~3, head = s_base - lo;
+    const int total = ws[kCompactThreads / 32 - 1];
     if (n) {
         const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+        int q = pos - lo;
         for (int i = 0; i < 16; ++i)
-            if (b[i] == 2) out[pos++] = base + i;
+            if (b[i] == 2) s_ids[q++] = base + i;
+    }
+    __syncthreads();
+    const int end = head + total;  // entries [head, end) of s_ids are this tile's
+    for (int j = 4 * threadIdx.x; j < end; j += 4 * kCompactThreads) {
+        if (j >= head && j + 4 <= end) {
+            const int4 q4 = *reinterpret_cast<const int4*>(&s_ids[j]);
+            *reinterpret_cast<int4*>(out + lo + j) = q4;
+            *reinterpret_cast<int4*>(host_out + lo + j) = q4;
+        } else {  // the partial words at either end of the range (a neighbour tile owns the rest)
+            for (int u = j; u < j + 4 && u < end; ++u)
+                if (u >= head) out[lo + u] = s_ids[u], host_out[lo + u] = s_ids[u];
+        }
     }
 }
 
@@ -2091,14 +2121,15 @@ int classify_occupancy(int, int) {
     return n < 1 ? 1 : n;
 }
 
-cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st) {
+cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st,
+                           int32_t* host_out) {
     const int ntiles = (s.N + kTile - 1) / kTile;
     if (ntiles == 0) return cudaMemsetAsync(gray_n, 0, sizeof(int32_t), st);
     cudaError_t e = launch_pdl(gray_count_kernel, dim3(ntiles), dim3(kCompactThreads), st,
                                static_cast<const uint8_t*>(s.state), s.N, tile_cnt);
     if (e != cudaSuccess) return e;
     return launch_pdl(gray_write_kernel, dim3(ntiles), dim3(kCompactThreads), st, static_cast<const uint8_t*>(s.state),
-                      s.N, static_cast<const int32_t*>(tile_cnt), ntiles, out_ids, gray_n);
+                      s.N, static_cast<const int32_t*>(tile_cnt), ntiles, out_ids, gray_n, host_out);
 }
 
 cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st) {

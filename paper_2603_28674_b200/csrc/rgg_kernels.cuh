@@ -210,7 +210,9 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
 // single-move updates: one kernel tests the cells against the move's boxes, then runs touch,
 // narrow and the transition per component of every hit cell
 cudaError_t launch_single(const Store& s, const Batch& b, int flags, cudaStream_t st);
-cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st);
+// host_out: also write the ids into mapped pinned host memory (capacity N)
+cudaError_t launch_compact(const Store& s, int32_t* out_ids, int32_t* tile_cnt, int32_t* gray_n, cudaStream_t st,
+                           int32_t* host_out = nullptr);
 cudaError_t launch_write_states(const Store& s, const int32_t* ids, const uint8_t* st_in, int n, cudaStream_t st);
 cudaError_t launch_pair_masks(const Store& s, const int32_t* rank, int kind, const int32_t* cand, int n, int o,
                               uint8_t* mask, cudaStream_t st);

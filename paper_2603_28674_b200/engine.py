@@ -259,6 +259,15 @@ class Reports:
         return np.stack([a["new_green"], a["new_red"], a["new_gray"], a["unknown_after_heuristic"]], 1)
 
 
+class _ArrayView:
+    """A read-only int32 array interface over host memory the engine owns."""
+
+    __slots__ = ("__array_interface__",)
+
+    def __init__(self, addr: int, n: int):
+        self.__array_interface__ = {"data": (addr, True), "shape": (n,), "typestr": "<i4", "version": 3}
+
+
 def _pose12(pose) -> np.ndarray:
     p = np.ascontiguousarray(pose, dtype=np.float64).reshape(-1)
     if p.size != 12:
@@ -314,6 +323,7 @@ class GpuEngine:
         self._resolver = None
         self._hv = h.value or 0  # the handle as an int (pyfast)
         self._one = (np.zeros(1, np.int32), (_Report * 1)())  # update_obstacle's move / report buffers
+        self._gv_p, self._gv_n = C.POINTER(C.c_int32)(), C.c_int32()  # gray_ids_view's out-parameters
 
     # ------------------------------------------------------------- plumbing
     @staticmethod
@@ -580,14 +590,13 @@ class GpuEngine:
     def gray_ids_view(self) -> np.ndarray:
         """The GRAY ids (ascending) as a read-only view of the engine's pinned host buffer:
         one DMA, no copy; valid until the next call on this engine."""
-        p = C.POINTER(C.c_int32)()
-        n = C.c_int32()
+        p = self._gv_p
+        n = self._gv_n
         self._check(library().rgg_gpu_gray_view(self._h, C.byref(p), C.byref(n)))
         if n.value == 0:
             return np.zeros(0, np.int32)
-        v = np.ctypeslib.as_array(p, shape=(n.value,))
-        v.flags.writeable = False
-        return v
+        # a read-only array over the pointer (np.ctypeslib.as_array builds a ctypes type per call)
+        return np.asarray(_ArrayView(C.cast(p, C.c_void_p).value, n.value))
 
     def last_hits(self) -> np.ndarray:
         n = C.c_int32()

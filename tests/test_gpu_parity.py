@@ -320,3 +320,26 @@ def test_single_move_kernel_equals_batched_path(eng_mod, name):
         assert np.array_equal(np.sort(a.last_hits()), np.sort(b.last_hits())), i
     assert np.array_equal(a.states(), b.states())
     assert np.array_equal(a.obstacle_bits(), b.obstacle_bits())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SCENARIOS)
+def test_gray_list_written_inside_the_host_update(eng_mod, name):
+    """A synchronous batch_update with gray_list=True writes the GRAY ids into mapped host
+    memory inside the update (gray_write_kernel's host_out): gray_ids_view() then returns
+    them without a copy.  Chunked updates exercise tile boundaries at several counts; the
+    list equals the device compaction and the labels, and a later label change (write_states,
+    resolve) falls back to the device list."""
+    g = load_golden(name)
+    eng = eng_mod.GpuEngine(_layout(g))
+    ids, rts = np.asarray(g["ids"], np.int32), np.asarray(g["rts"], np.float64).reshape(-1, 12)
+    for a in range(0, len(ids), 7):
+        eng.batch_update((ids[a:a + 7], rts[a:a + 7]), gray_list=True)
+        view = eng.gray_ids_view().copy()
+        st = eng.states()
+        assert np.array_equal(view, np.nonzero(st == 2)[0].astype(np.int32)), a
+        assert np.array_equal(eng.gray_ids(), view), a
+    gray = np.nonzero(eng.states() == 2)[0].astype(np.int32)
+    if len(gray):
+        eng.write_states(gray[:1], np.zeros(1, np.uint8))
+        assert np.array_equal(eng.gray_ids_view(), gray[1:])
