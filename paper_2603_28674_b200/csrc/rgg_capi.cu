@@ -404,9 +404,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // kHostIO (rgg_gpu_update): the moves' H2D copy and the counters' D2H copies are
     // nodes of the graph, so a synchronous update is one graph launch and one wait
     const bool hostio = use_graph && (flags & kHostIO) != 0;
-    // the apply kernel ends the update unless the gray list or an eager resolve follows:
-    // then one small kernel stores the counters into mapped host memory
-    const bool out_in_kernel = hostio && !gray_list && !eager;
+    // synchronous host updates end with one small kernel that stores the counters into
+    // mapped host memory and raises the flag the host polls: after apply, or after the
+    // gray-list compaction when the update compacts it (eager updates copy them instead)
+    const bool out_in_kernel = hostio && !eager;
     if (out_in_kernel) {
         b.out_mv = h->dh_mv;
         b.out_ctr = h->dh_ctr;
@@ -455,12 +456,13 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
             if (e == cudaSuccess && !single) e = rggk::launch_bin(h->s, b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[2]);
             if (e == cudaSuccess) e = classify();
-            if (e == cudaSuccess && out_in_kernel) e = rggk::launch_host_out(b, h->stream);
+            if (e == cudaSuccess && out_in_kernel && !gray_list) e = rggk::launch_host_out(b, h->stream);
             if (e == cudaSuccess && eager) e = resolve_hits();
             if (e == cudaSuccess) e = rec(h->ev[3]);
             if (e == cudaSuccess && gray_list)
                 e = rggk::launch_compact(h->s, h->d_gray, h->d_tiles, h->d_ctr + 4, h->stream,
                                          gray_host ? h->dh_gray_map : nullptr);
+            if (e == cudaSuccess && out_in_kernel && gray_list) e = rggk::launch_host_out(b, h->stream);
             if (e == cudaSuccess) e = rec(h->ev[4]);
             if (e == cudaSuccess && hostio && !out_in_kernel && (flags & RGG_PER_MOVE))
                 e = cudaMemcpyAsync(h->h_mv, h->d_mv, static_cast<size_t>(n) * 4 * sizeof(int32_t),

@@ -1844,6 +1844,10 @@ __global__ void __launch_bounds__(kCompactThreads) gray_write_kernel(const uint8
                 if (u >= head) out[lo + u] = s_ids[u], host_out[lo + u] = s_ids[u];
         }
     }
+    // the host reads the list once host_out_kernel raises its flag: release this CTA's
+    // host stores at system scope first
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
 }
 
 __global__ void write_states_kernel(Store s, const int32_t* ids, const uint8_t* st, int n) {
