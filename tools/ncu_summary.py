@@ -36,7 +36,7 @@ for row in rows[2:]:
             k[out] = v
     kernels.append(k)
 upd = ("pose_kernel", "bin_scatter", "bin_cells", "bin_small", "cells_touch", "touch_warp_kernel<0", "touch_warp_kernel<false", "narrow_kernel<0",
-       "narrow_kernel<false", "narrow_over", "narrow_under", "single_cells", "apply_warp", "gray_count", "gray_write")
+       "narrow_kernel<false", "touch_cta", "narrow_over", "narrow_under", "single_cells", "apply_warp", "gray_count", "gray_write")
 seen, cls = set(), []
 for k in kernels:  # one launch of each update kernel
     tag = next((t for t in upd if t in k["kernel"]), None)
