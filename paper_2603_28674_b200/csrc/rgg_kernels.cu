@@ -1247,15 +1247,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
 // touch, one CTA per work unit (a cell's chunk of <= 32 listed events): warp w takes the
 // cell's slice w (kWarpsPerCta == slices per cell at 128-component cells), so the chunk's
 // event boxes are staged once per CTA (all 128 threads load them) instead of once per
-// slice, and the CTA reserves its narrow items with one atomic instead of four.  The
-// tests and items are touch_warp_kernel's; that kernel remains for the census and for the
-// published-unit handoff (Batch::unit_ready).
+// slice.  The tests and items are touch_warp_kernel's; that kernel remains for the census
+// and for the published-unit handoff (Batch::unit_ready).
 __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, Batch b) {
     pdl_wait();
     pdl_trigger();
     __shared__ double sbx[32][24];
     __shared__ int sev[32];
-    __shared__ unsigned long long s_res[kWarpsPerCta], s_base;
     const int tid = threadIdx.x, wi = tid >> 5, lane = tid & 31;
     {
         const char* p = reinterpret_cast<const char*>(b.evt);
@@ -1327,8 +1325,9 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, B
             b.mpool[wo] = 0;
             b.mpool[wu] = 0;
         }
-        // one packed reservation per CTA for both queues (ctr[8] over items, ctr[9] under
-        // items per (pair, segment)); a full queue is reported through ctr[6] = 3
+        // one packed reservation per warp for both queues (ctr[8] over items, ctr[9] under
+        // items per (pair, segment)); a full queue is reported through ctr[6] = 3.  (One per
+        // CTA, by thread 0 between two barriers, was slower.)
         const unsigned long long mine = static_cast<unsigned long long>(__popc(bm)) |
                                         (static_cast<unsigned long long>(__popc(sm) * (seg_hi - seg_lo)) << 32);
         unsigned long long x = mine;
@@ -1336,16 +1335,10 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, B
             const unsigned long long y = __shfl_up_sync(0xffffffffu, x, off);
             if (lane >= off) x += y;
         }
-        if (lane == 31) s_res[wi] = x;
-        __syncthreads();
-        if (tid == 0) {
-            unsigned long long tot = 0;
-            for (int v = 0; v < kWarpsPerCta; ++v) tot += s_res[v];
-            s_base = tot ? atomicAdd(reinterpret_cast<unsigned long long*>(&b.ctr[8]), tot) : 0ull;
-        }
-        __syncthreads();
-        unsigned long long wbase = s_base;
-        for (int v = 0; v < wi; ++v) wbase += s_res[v];
+        const unsigned long long wtot = __shfl_sync(0xffffffffu, x, 31);
+        unsigned long long wbase = 0;
+        if (lane == 31 && wtot) wbase = atomicAdd(reinterpret_cast<unsigned long long*>(&b.ctr[8]), wtot);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
         const unsigned long long at64 = wbase + x - mine;
         int at = static_cast<int>(at64 & 0xffffffffu);
         for (uint32_t y = bm; y; y &= y - 1, ++at) {
@@ -1362,7 +1355,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, B
                 else b.ctr[6] = 3;
             }
         }
-        __syncthreads();  // sbx / sev / s_res are restaged by the next unit
+        __syncthreads();  // sbx / sev are restaged by the next unit
     }
 }
 
