@@ -1386,7 +1386,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 9) apply_warp_kernel(Store 
     int rep = 0;  // some obstacle moves twice in this batch (b.last from the pose kernel)
     for (int t = threadIdx.x; t < b.n; t += blockDim.x) {
         if (staged) s_ids[t] = b.ids[t];
-        if (WIDE) rep |= b.last[t] == 0;
+        rep |= b.last[t] == 0;
     }
     const bool repeats = __syncthreads_or(rep) != 0;
     int dgray = 0;
@@ -1492,13 +1492,26 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 9) apply_warp_kernel(Store 
                         }
                 }
             }
-            // only the events that touch some component of the slice can change a
-            // label or a counter: walk those, in list (= move) order
-            for (uint32_t em = __reduce_or_sync(0xffffffffu, tm); em; em &= em - 1) {
+            // a touching event changes nothing for a component that neither held its bits
+            // nor is hit now: walk only the events some lane of the slice is active for, in
+            // list (= move) order (with an obstacle moved twice in the batch, its second
+            // move's old bits are the first one's new bits: then every touching event)
+            uint32_t act = tm;
+            if (!repeats) {
+                if (!WIDE)
+                    for (uint32_t x = tm; x; x &= x - 1) {
+                        const int kk = __ffs(x) - 1;
+                        const int ob = som[wi][kk].x & 63;
+                        oldO |= static_cast<uint32_t>((OW >> ob) & 1ull) << kk;
+                        oldU |= static_cast<uint32_t>((UW >> ob) & 1ull) << kk;
+                    }
+                act = tm & (ro | ru | oldO | oldU);
+            }
+            for (uint32_t em = __reduce_or_sync(0xffffffffu, act); em; em &= em - 1) {
                 const int k = __ffs(em) - 1;
                 const int before = label;
                 const int2 om = som[wi][k];
-                if ((tm >> k) & 1u) {
+                if ((act >> k) & 1u) {
                     const int o = om.x;
                     const size_t widx = static_cast<size_t>(o >> 6) * s.Np + c;
                     const unsigned long long bit = 1ull << (o & 63);
