@@ -383,6 +383,10 @@ int enqueue(rgg_gpu* h, int32_t n, int32_t flags) {
     // the batched path, whose cell lists and item queues it counts
     static const bool no_single = std::getenv("RGG_NO_SINGLE") != nullptr;
     const bool single = n == 1 && !b.census_on && !no_single;
+    if (single) {  // no bin kernel waits on the pose warps' published boxes
+        b.evready = nullptr;
+        b.unit_ready = nullptr;
+    }
     const auto classify = [&]() {
         return single ? rggk::launch_single(h->s, b, kf, h->stream)
                       : rggk::launch_classify(h->s, b, kf, h->grid_classify, h->stream);
