@@ -309,6 +309,16 @@ def cpu_baselines(config, rm, obs, ids, rts, sample_s, parity_updates=2):
     return out, seq, done, n
 
 
+def cpu_reference_run(config, seed, iterations, sample_s, out_path):
+    """cpu_baselines on the headline workload, rebuilt from its seed (run_isolated's child);
+    the grouped SequentialEngines' labels and bits after the updates they ran go to out_path."""
+    rm, obs, _ = tile_workload(config, 0, seed, iterations)
+    ids, rts = world_moves(config, 1, seed, iterations)
+    base, seq, done, _ = cpu_baselines(config, rm, obs, ids, rts, sample_s)
+    np.savez(out_path, states=np.asarray(seq.states()), bits=np.asarray(seq.bits()))
+    return {"baselines": base, "done": done}
+
+
 # --------------------------------------------------------------- GPU helpers
 
 def measure_extra(config, seed, device, steps=10, warmup=3, cell_capacity=64, parity=False):
@@ -554,7 +564,29 @@ def roofline(census, kernel_ms, world, profile_json=None):
 
 # ---------------------------------------------------------------------- main
 
+def run_isolated(fn: str, *args, **kwargs) -> dict:
+    """bench.<fn>(*args, **kwargs) in a child process (its JSON result), or {"error": ...}."""
+    code = ("import json, sys; sys.path.insert(0, %r); import bench; "
+            "a = json.loads(sys.argv[1]); print(json.dumps(getattr(bench, %r)(*a['args'], **a['kwargs'])))"
+            % (ROOT, fn))
+    try:
+        r = subprocess.run([sys.executable, "-X", "faulthandler", "-c", code,
+                            json.dumps({"args": list(args), "kwargs": kwargs})],
+                           capture_output=True, text=True, timeout=1800, cwd=ROOT)
+    except subprocess.TimeoutExpired:
+        return {"error": f"{fn}: timed out"}
+    if r.returncode != 0:
+        return {"error": f"{fn}: exit {r.returncode}: " + (r.stderr or "")[-400:]}
+    try:
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except (ValueError, IndexError):
+        return {"error": f"{fn}: no JSON result: " + (r.stdout or "")[-200:]}
+
+
 def main():
+    import faulthandler
+
+    faulthandler.enable()  # a native crash prints the Python stacks to stderr
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
@@ -754,7 +786,18 @@ def main():
                    "seg_sphere_tests_per_update": census["seg_sphere_tests"]},
     }
     if world == 1 and not args.no_cpu_baseline:
-        base, seq, done, n_ref = cpu_baselines(args.config, rm, obs, ids_h, rts_h, args.cpu_sample_s)
+        # the reference's CPU engines in a child process (it saves its labels and bits after
+        # `done` updates), so a failure there cannot take the headline line with it
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as tmp:
+            res = run_isolated("cpu_reference_run", args.config, args.seed, iterations, args.cpu_sample_s,
+                               os.path.join(tmp, "ref.npz"))
+            if "error" in res:
+                raise RuntimeError("reference CPU run failed: " + res["error"])
+            with np.load(os.path.join(tmp, "ref.npz")) as z:
+                ref_states, ref_bits = z["states"], z["bits"]
+        base, done = res["baselines"], res["done"]
         # label and bit parity on the full roadmap: a fresh engine, the same `done` updates
         eng_chk = E.GpuEngine(lv, device=local)
         reps_chk = []
@@ -762,8 +805,8 @@ def main():
             reps_chk.append(eng_chk.batch_update((ids_h[it], rts_h[it]), per_move=True).counts())
         gst = eng_chk.states()
         gbits = eng_chk.obstacle_bits().reshape(N, -1)
-        rbits = seq.bits()
-        line["parity"]["mismatches_vs_reference"] = int(np.sum(gst != seq.states()))
+        rbits = ref_bits
+        line["parity"]["mismatches_vs_reference"] = int(np.sum(gst != ref_states))
         line["parity"]["bit_word_mismatches_vs_reference"] = int(np.sum(gbits != rbits.reshape(gbits.shape)))
         line["parity"]["checked"] = (f"{N} labels and {gbits.size} obstacle-bit words after {done} updates against "
                                      f"the reference's grouped SequentialEngines ({rbits.shape[1]} x 64 obstacles)")
@@ -784,7 +827,7 @@ def main():
                                              f"unknown_after_heuristic) of updates 0..{n_rep - 1} against the pinned C "
                                              f"oracle's engine (oracle/rgg_oracle.c ro_engine_update), "
                                              f"{time.time() - t0:.0f} s")
-        del eng_chk, seq
+        del eng_chk
         fast = base[base["fastest"]]
         line["cpu_baseline"] = {"value": fast["edges_per_s"], "unit": "edges/s", "cores": fast["cores"],
                                 "kind": "reference", "ms_per_step": fast["ms_per_update"],
@@ -792,25 +835,18 @@ def main():
                                           f"({base['fastest']}): {fast['sample']}",
                                 "all": base}
     if world == 1 and not args.no_extras:
+        # each extra measurement in its own process: a failure there (even a native one)
+        # cannot take the headline line with it
         line["extra"] = {}
         for cfg in [c for c in args.extra_configs.split(",") if c and c != args.config]:
-            try:
-                if cfg == "c1":
-                    line["extra"][cfg] = measure_c1(local)
-                elif cfg == "c3":  # fixed-capacity overflow: 16 inline slots per cell
-                    line["extra"][cfg] = measure_extra(cfg, args.seed, local, cell_capacity=16, parity=True)
-                else:  # c2, c4: parity against the oracle too
-                    line["extra"][cfg] = measure_extra(cfg, args.seed, local, parity=True)
-            except Exception as ex:  # keep the headline line even if an extra config fails
-                line["extra"][cfg] = {"error": str(ex)[:300]}
-        try:
-            line["resolve"] = measure_resolve("c2", args.seed, local, cpu=not args.no_cpu_baseline)
-        except Exception as ex:
-            line["resolve"] = {"error": str(ex)[:300]}
-        try:
-            line["prm"] = measure_prm(cpu=not args.no_cpu_baseline)
-        except Exception as ex:
-            line["prm"] = {"error": str(ex)[:300]}
+            if cfg == "c1":
+                line["extra"][cfg] = run_isolated("measure_c1", local)
+            elif cfg == "c3":  # fixed-capacity overflow: 16 inline slots per cell
+                line["extra"][cfg] = run_isolated("measure_extra", cfg, args.seed, local, cell_capacity=16, parity=True)
+            else:  # c2, c4: parity against the oracle too
+                line["extra"][cfg] = run_isolated("measure_extra", cfg, args.seed, local, parity=True)
+        line["resolve"] = run_isolated("measure_resolve", "c2", args.seed, local, cpu=not args.no_cpu_baseline)
+        line["prm"] = run_isolated("measure_prm", cpu=not args.no_cpu_baseline)
     print(json.dumps(line), flush=True)
     if args.json_out:
         json.dump(line, open(args.json_out, "w"), indent=1)
