@@ -29,9 +29,10 @@ int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nod
 /* Same, with flags: RGG_BUILD_POSES keeps forward_kinematics of every discretized
  * configuration for the GPU exact resolve (rgg_gpu_set_resolver, include/rgg_gpu.h). */
 #define RGG_BUILD_POSES 1
-/* fit the swept-volume boxes (obb_from_points) on the GPU, bit-identical (device 0) */
+/* fit the swept-volume boxes (obb_from_points) on the GPU, bit-identical (the calling thread's
+ * current CUDA device) */
 #define RGG_BUILD_GPU_FIT 2
-/* also the inner approximation (spline simplification) on the GPU, bit-identical (device 0);
+/* also the inner approximation (spline simplification) on the GPU, bit-identical (same device);
  * slower end to end than RGG_BUILD_GPU_FIT alone while serialize stays on the host */
 #define RGG_BUILD_GPU_INNER 4
 int rgg_build_layout_ex(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,

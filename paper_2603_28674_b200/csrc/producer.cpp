@@ -686,7 +686,7 @@ int rgg_build_layout_robot(const rgg_robot_view* robot, int32_t n_nodes, const d
             int64_t max_chunk = 0;
             for (int32_t c = 0; c < N; ++c) max_chunk = std::max(max_chunk, pose_off[c + 1] - pose_off[c]);
             const int64_t chunk = std::max(kChunk / B, max_chunk);  // configurations per staging buffer
-            fit = rggp_fit_begin(unit_off.data(), N * B, he.data(), B, cs, chunk * B, 0);
+            fit = rggp_fit_begin(unit_off.data(), N * B, he.data(), B, cs, chunk * B, -1);  // current device
             if (!fit) throw std::runtime_error("GPU box fit: CUDA initialisation failed");
             try {
                 int slot = 0;

@@ -310,6 +310,7 @@ void rggp_fit_end(void* p) {
 void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, int32_t nbodies, const double* cos_sin,
                      int64_t chunk_configs, int32_t device) {
     FitStream* f = new FitStream();
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) device = 0;  // the caller's current device
     f->device = device;
     f->ncomp = ncomp;
     f->nb = nbodies;

@@ -23,7 +23,8 @@ struct InnerOut {
 };
 
 // ncomp fit units (one per (component, body)), unit c with the poses [off[c], off[c+1])
-// of body c % nbodies (half extents he3[3 * body]); chunk_configs = staging capacity (poses)
+// of body c % nbodies (half extents he3[3 * body]); chunk_configs = staging capacity (poses);
+// device < 0: the calling thread's current CUDA device
 void* rggp_fit_begin(const int64_t* off, int32_t ncomp, const double* he3, int32_t nbodies, const double* cos_sin,
                      int64_t chunk_configs, int32_t device);
 double* rggp_fit_staging(void* fs, int32_t slot);
