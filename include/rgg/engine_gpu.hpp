@@ -21,8 +21,8 @@
 //    against the obstacles this engine has moved at their engine poses, and
 //    against the Scene's other active obstacles at their scene poses (listed
 //    before every exact resolve, rgg_gpu_set_active_obstacles).
-// Not provided: grid() (the GPU engine has no SpatialGrid; its cells are the
-// cell-sorted component blocks of rgg_gpu_create).
+// grid() is the reference's own SpatialGrid over the component AABBs, built on first
+// call (the GPU engine bins on its own cells and never reads it).
 #pragma once
 
 #include <algorithm>
@@ -38,6 +38,7 @@
 #include "rgg/geometry.hpp"
 #include "rgg/roadmap.hpp"
 #include "rgg/robot.hpp"
+#include "rgg/spatial_grid.hpp"
 #include "rgg/update_report.hpp"
 #include "rgg_gpu.h"
 
@@ -47,7 +48,8 @@ class GpuEngine {
 public:
     GpuEngine(const ComponentSet& components, Scene& scene, EngineOptions options = {}, int cell_capacity = 1024,
               int device = 0, bool allow_wide = false)
-        : components_(&components), scene_(scene), options_(options) {
+        : components_(&components), scene_(scene), options_(options), bounds_(scene.bounds),
+          cell_capacity_(cell_capacity) {
         if (scene.obstacles.size() > 64 && !allow_wide)
             throw std::invalid_argument("obstacle bitsets support at most 64 obstacles");
         // The component view (include/rgg_gpu.h rgg_component_view): the serialize step's
@@ -228,6 +230,12 @@ public:
         if (!layout_) layout_ = std::make_unique<BatchLayout>(BatchLayout::serialize(*components_, scene_.obstacles));
         return *layout_;
     }
+    // BatchEngine::grid() (engine_batch.hpp:32): SpatialGrid::build over the layout's component
+    // AABBs, the construction-time scene bounds and cell capacity (engine_batch.cpp:26)
+    const SpatialGrid& grid() const {
+        if (!grid_) grid_ = std::make_unique<SpatialGrid>(SpatialGrid::build(layout().component_aabb, bounds_, cell_capacity_));
+        return *grid_;
+    }
     int words_per_component() const { return words_; }
 
     void batch_over(const std::vector<ComponentId>& candidates, ObstacleId o, std::vector<std::uint8_t>& mask) {
@@ -318,7 +326,10 @@ private:
     const ComponentSet* components_;
     Scene& scene_;
     EngineOptions options_;
+    Aabb bounds_;
+    int cell_capacity_;
     mutable std::unique_ptr<BatchLayout> layout_;
+    mutable std::unique_ptr<SpatialGrid> grid_;
     int n_components_ = 0;
     std::vector<double> corners_, seg_pts_, spline_r_, obst_he_, obst_sl_, obst_r_;
     std::vector<std::int32_t> row_off_, obst_n_;

@@ -131,6 +131,21 @@ static void batch_update_matches_batch_engine() {
         EXPECT(bat.unknown_count() == gpu.unknown_count(), "iteration %d unknown count", it);
     }
     EXPECT(gpu.batch_update({}, true).empty(), "empty move list");
+    // grid(): the reference's SpatialGrid over the same component AABBs
+    const SpatialGrid& gb = bat.grid();
+    const SpatialGrid& gg = gpu.grid();
+    EXPECT(gb.cell_count() == gg.cell_count() && gb.capacity() == gg.capacity() &&
+               gb.overflow_total() == gg.overflow_total(),
+           "grid(): %d cells vs %d", gb.cell_count(), gg.cell_count());
+    for (int q = 0; q < 20; ++q) {
+        const Vec3 c{rng.uniform(-5, 5), rng.uniform(-5, 5), rng.uniform(-5, 5)};
+        const double r = rng.uniform(0.2, 2.0);
+        const Aabb box{{c.x - r, c.y - r, c.z - r}, {c.x + r, c.y + r, c.z + r}};
+        std::vector<std::int32_t> cb, cg;
+        gb.candidates(box, cb);
+        gg.candidates(box, cg);
+        EXPECT(cb == cg, "grid() candidates differ for query %d", q);
+    }
     bool threw = false;
     try {
         gpu.update_obstacle(99, Transform::identity(), true);
