@@ -3,7 +3,7 @@
 // Same public surface as the reference's update API
 //   class rgg::BatchEngine    proj/include/rgg/engine_batch.hpp:17-63
 // (constructor over ComponentSet + Scene&, update_obstacle, batch_update,
-// resolve_all_unknown, states, obstacle_bits, unknown_count, layout,
+// resolve_all_unknown, states, obstacle_bits, unknown_count, layout, grid,
 // batch_over, batch_under), header-only over the C-ABI of include/rgg_gpu.h
 // (link paper_2603_28674_b200/lib/librgg_gpu.so).  A maintainer compiles it
 // against the reference's own headers; see INTEGRATION.md.
