@@ -1250,16 +1250,17 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_warp_kernel(Store s, 
 // slice.  The tests and items are touch_warp_kernel's; that kernel remains for the census
 // and for the published-unit handoff (Batch::unit_ready).
 __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, Batch b) {
-    pdl_wait();
-    pdl_trigger();
     __shared__ double sbx[32][24];
     __shared__ int sev[32];
     const int tid = threadIdx.x, wi = tid >> 5, lane = tid & 31;
-    {
+    {  // the pose kernel's event boxes are complete once this grid's CTAs run (every kernel
+       // since waited on its predecessor): into this SM's L1 before the wait
         const char* p = reinterpret_cast<const char*>(b.evt);
         const int lines = (b.n * 24 * 8 + 127) >> 7;
         for (int l = tid; l < min(lines, 256); l += blockDim.x) prefetch_l1(p + (static_cast<size_t>(l) << 7));
     }
+    pdl_wait();
+    pdl_trigger();
     const int spc = s.cell >> 5;  // slices per cell (<= kWarpsPerCta)
     const int n_rec = min(b.ctr[10], b.units_cap);
     for (int r = blockIdx.x; r < n_rec; r += gridDim.x) {
@@ -1371,10 +1372,6 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) touch_cta_kernel(Store s, B
 template <int FLAGS, bool WIDE>
 __global__ void __launch_bounds__(32 * kWarpsPerCta, 9) apply_warp_kernel(Store s, Batch b) {
     const unsigned long long tw = tl_start(b.tl);
-    pdl_wait();
-    pdl_trigger();
-    const unsigned long long t0 = tl_start(b.tl);
-    tl_stop(b.tl, 8, tw);
     constexpr bool PER_MOVE = (FLAGS & kPerMove) != 0;
     constexpr bool HITS = (FLAGS & kHits) != 0;
     __shared__ int2 som[kWarpsPerCta][32];
@@ -1382,13 +1379,20 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta, 9) apply_warp_kernel(Store 
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = (s.Np + 31) >> 5;
     const bool staged = b.n <= kStageIds;
-    if (b.evready && blockIdx.x == 0 && threadIdx.x < 4) b.evready[threadIdx.x] = 0;  // for the next update
+    // the pose kernel's outputs (ids, last) are complete once this grid's CTAs run: every
+    // kernel since has waited on its predecessor, so stage them before the wait, while
+    // the narrow kernels drain
     int rep = 0;  // some obstacle moves twice in this batch (b.last from the pose kernel)
     for (int t = threadIdx.x; t < b.n; t += blockDim.x) {
         if (staged) s_ids[t] = b.ids[t];
         rep |= b.last[t] == 0;
     }
     const bool repeats = __syncthreads_or(rep) != 0;
+    pdl_wait();
+    pdl_trigger();
+    const unsigned long long t0 = tl_start(b.tl);
+    tl_stop(b.tl, 8, tw);
+    if (b.evready && blockIdx.x == 0 && threadIdx.x < 4) b.evready[threadIdx.x] = 0;  // for the next update
     int dgray = 0;
     // any failed stage (status ctr[6]: 1 overflow pool, 2 mask pool, 3 full narrow-item
     // queue, 4 handoff timeout) left some verdicts uncomputed: apply nothing, so the
