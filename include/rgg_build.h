@@ -74,6 +74,32 @@ const char* rgg_build_last_error(void);
 /* CUDA devices visible to the producer (0 without a GPU): the GPU box fit
  * (RGG_BUILD_GPU_FIT) is the Python producer's default when this is positive. */
 int rgg_build_gpu_count(void);
+/* The reference's binary roadmap file (save_roadmap / load_roadmap, proj/src/roadmap_io.cpp:150-301:
+ * magic "RGGRDMP1", version 1, little-endian sections, a CRC-32 of the whole file), read and fully
+ * verified before anything is built, straight into the component view of
+ * rgg_gpu_create_from_components (include/rgg_gpu.h): no ComponentSet and no padded layout.
+ * Returns 0, one of the error kinds below (RoadmapIoError, roadmap_io.hpp:10-16), or -1 (an
+ * inconsistent file, e.g. an inconsistent slot radius); rgg_build_last_error has the text. */
+#define RGG_ROADMAP_BAD_MAGIC 1
+#define RGG_ROADMAP_BAD_VERSION 2
+#define RGG_ROADMAP_TRUNCATED 3
+#define RGG_ROADMAP_CHECKSUM 4
+typedef struct rgg_roadmap_file rgg_roadmap_file;
+int rgg_roadmap_load(const char* path, rgg_roadmap_file** out);
+/* out[0..8] = n_nodes, n_edges, dof, N (components), B, S, T (real segments), kinematics, max_segments */
+int rgg_roadmap_counts(const rgg_roadmap_file* f, int64_t* out);
+/* the component view's arrays: obb_corners N*B*24, row_off N*B*S+1, seg_points T*6, spline_radius B*S
+ * (any pointer may be null) */
+int rgg_roadmap_components(const rgg_roadmap_file* f, double* obb_corners, int32_t* row_off, double* seg_points,
+                           double* spline_radius);
+/* the roadmap: nodes n_nodes*dof, edges n_edges*2, and the discretization resolution */
+int rgg_roadmap_graph(const rgg_roadmap_file* f, double* nodes, int32_t* edges, double* eps);
+/* the robot (rgg_robot_view's arrays): half extents B*3, local frames B*12, joint axes / offsets B*3 (chains) */
+int rgg_roadmap_robot(const rgg_roadmap_file* f, double* he, double* local12, double* axis, double* offset);
+/* the exact resolve's inputs (rgg_resolve_view): *n_configs, pose_off N+1, poses n_configs*B*12 (pass
+ * poses = NULL to size them) */
+int rgg_roadmap_poses(const rgg_roadmap_file* f, int64_t* n_configs, int64_t* pose_off, double* poses);
+void rgg_roadmap_free(rgg_roadmap_file* f);
 /* obstacle_inner_spheres (proj/src/swept.cpp:23-49): count centres (count*3) and the radius. */
 int rgg_obstacle_spheres(const double* he3, int32_t count, double* centres, double* radius);
 

@@ -60,6 +60,7 @@ def lib():
                                           C.c_double, C.c_int]
         L.rr_world_robot.argtypes = [C.c_void_p, _ip] + [C.c_void_p] * 5
         L.rr_world_roadmap.argtypes = [C.c_void_p, _dp, _ip]
+        L.rr_world_save.argtypes = [C.c_void_p, C.c_char_p]
         L.rr_box_intersect.argtypes = [_dp, _dp, _dp, _dp, C.POINTER(C.c_int)]
         L.rr_engine_exact.argtypes = [C.c_void_p, C.c_int, _ip, _up]
         L.rr_engine_resolve_all.argtypes = [C.c_void_p, C.POINTER(C.c_int32)]
@@ -167,6 +168,10 @@ class World:
         edges = np.zeros((k["n_edges"], 2), np.int32)
         _check(lib().rr_world_roadmap(self.h, nodes.reshape(-1), edges.reshape(-1)))
         return nodes, edges
+
+    def save(self, path: str):
+        """save_roadmap (roadmap_io.cpp:150-203): the world's robot, roadmap and components."""
+        _check(lib().rr_world_save(self.h, str(path).encode()))
 
     def add_obstacle(self, he, spheres=0):
         _check(lib().rr_world_add_obstacle(self.h, np.asarray(he, np.float64), int(spheres)))

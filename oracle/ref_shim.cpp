@@ -29,6 +29,7 @@
 #include "rgg/engine_sequential.hpp"
 #include "rgg/kernels.hpp"
 #include "rgg/rng.hpp"
+#include "rgg/roadmap_io.hpp"
 #include "rgg/scenario.hpp"
 
 using namespace rgg;
@@ -225,6 +226,12 @@ int rr_world_robot(void* wp, std::int32_t* meta, double* he, double* local12, do
         }
         if (eps_k) eps_k[0] = w->comps.epsilon, eps_k[1] = w->comps.max_segments;
     });
+}
+
+// save_roadmap (roadmap_io.cpp:150-203) of the world's robot, roadmap and components.
+int rr_world_save(void* wp, const char* path) {
+    const World* w = static_cast<const World*>(wp);
+    return guarded([&] { save_roadmap(path, w->scene.robot, w->roadmap, w->comps); });
 }
 
 // The world's roadmap: nodes n x dof, edges e x 2 (counts from rr_world_counts).

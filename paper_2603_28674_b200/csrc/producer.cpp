@@ -535,6 +535,73 @@ Comp build_comp(const Robot& rb, const double* a, const double* b, double eps, i
     return comp;
 }
 
+// ---- the reference's binary roadmap file (save_roadmap / load_roadmap,
+// roadmap_io.cpp:150-301): "RGGRDMP1", u32 version 1, then little-endian sections
+// (robot; sphere sets per body; epsilon, segment cap; nodes; edges; per component the
+// body OBBs and the body splines) and a CRC-32 of everything before it.
+
+// CRC-32 (reflected, polynomial 0xEDB88320, initial and final xor 0xFFFFFFFF), the
+// checksum of roadmap_io.cpp:125-138
+uint32_t crc32_of(const uint8_t* p, size_t n) {
+    static uint32_t table[256];
+    static const bool ready = [] {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int k = 0; k < 8; ++k) c = (c >> 1) ^ ((c & 1u) ? 0xEDB88320u : 0u);
+            table[i] = c;
+        }
+        return true;
+    }();
+    (void)ready;
+    uint32_t c = 0xFFFFFFFFu;
+    for (size_t i = 0; i < n; ++i) c = table[(c ^ p[i]) & 0xFFu] ^ (c >> 8);
+    return ~c;
+}
+
+// load_roadmap's error kinds (roadmap_io.hpp:10-16)
+struct FileError : std::runtime_error {
+    int kind;
+    FileError(int k, const std::string& m) : std::runtime_error(m), kind(k) {}
+};
+
+struct ByteReader {
+    const uint8_t* p;
+    size_t n, at = 0;
+    void need(size_t k) const {
+        if (at + k > n) throw FileError(RGG_ROADMAP_TRUNCATED, "roadmap file truncated");
+    }
+    uint8_t u8() {
+        need(1);
+        return p[at++];
+    }
+    uint32_t u32() {
+        need(4);
+        uint32_t v = 0;
+        for (int i = 0; i < 4; ++i) v |= static_cast<uint32_t>(p[at + i]) << (8 * i);
+        at += 4;
+        return v;
+    }
+    double f64() {
+        need(8);
+        uint64_t v = 0;
+        for (int i = 0; i < 8; ++i) v |= static_cast<uint64_t>(p[at + i]) << (8 * i);
+        at += 8;
+        double d;
+        std::memcpy(&d, &v, 8);
+        return d;
+    }
+    V3 v3() {
+        const double x = f64(), y = f64(), z = f64();
+        return {x, y, z};
+    }
+    // a count bounded like the reference's sanity_count (roadmap_io.cpp:90-93)
+    uint32_t count(uint32_t limit, const char* what) {
+        const uint32_t v = u32();
+        if (v > limit) throw FileError(RGG_ROADMAP_TRUNCATED, std::string("implausible count for ") + what);
+        return v;
+    }
+};
+
 }  // namespace
 
 struct rgg_built {
@@ -914,6 +981,286 @@ int rgg_built_poses(const rgg_built* b, int64_t* n_configs, int64_t* pose_off, d
 }
 
 void rgg_built_free(rgg_built* b) { delete b; }
+
+struct rgg_roadmap_file {
+    int32_t kinematics = 0, B = 0, S = 1, dof = 0, n_nodes = 0, n_edges = 0, K = 16;
+    double eps = 0.0;
+    std::vector<double> he, local, axis, offset;  // the robot
+    std::vector<double> nodes;
+    std::vector<int32_t> edges;
+    std::vector<double> corners, seg_pts, spline_r;  // the component view
+    std::vector<int32_t> row_off;
+};
+
+int rgg_roadmap_load(const char* path, rgg_roadmap_file** out) {
+    try {
+        if (!path || !out) throw FileError(RGG_ROADMAP_TRUNCATED, "null path or output");
+        std::vector<uint8_t> buf;
+        {
+            std::FILE* f = std::fopen(path, "rb");
+            if (!f) throw FileError(RGG_ROADMAP_TRUNCATED, std::string("cannot open ") + path);
+            uint8_t chunk[1 << 16];
+            for (size_t got; (got = std::fread(chunk, 1, sizeof(chunk), f)) > 0;) buf.insert(buf.end(), chunk, chunk + got);
+            std::fclose(f);
+        }
+        static const char kMagic[8] = {'R', 'G', 'G', 'R', 'D', 'M', 'P', '1'};
+        if (buf.size() < sizeof(kMagic) + 8) throw FileError(RGG_ROADMAP_TRUNCATED, "file too small");
+        if (std::memcmp(buf.data(), kMagic, sizeof(kMagic)) != 0) throw FileError(RGG_ROADMAP_BAD_MAGIC, "not a roadmap file");
+        const size_t body = buf.size() - 4;
+        const uint32_t stored = static_cast<uint32_t>(buf[body]) | static_cast<uint32_t>(buf[body + 1]) << 8 |
+                                static_cast<uint32_t>(buf[body + 2]) << 16 | static_cast<uint32_t>(buf[body + 3]) << 24;
+        if (crc32_of(buf.data(), body) != stored) throw FileError(RGG_ROADMAP_CHECKSUM, "checksum mismatch");
+        ByteReader rd{buf.data(), body, sizeof(kMagic)};
+        if (rd.u32() != 1) throw FileError(RGG_ROADMAP_BAD_VERSION, "unsupported roadmap file version");
+        std::unique_ptr<rgg_roadmap_file> F(new rgg_roadmap_file());
+        // robot (write_robot, roadmap_io.cpp:95-107)
+        F->kinematics = rd.u8();
+        F->B = static_cast<int32_t>(rd.count(1u << 16, "bodies"));
+        for (int32_t b = 0; b < F->B; ++b) {
+            const V3 he = rd.v3();
+            F->he.insert(F->he.end(), {he.x, he.y, he.z});
+            for (int q = 0; q < 12; ++q) F->local.push_back(rd.f64());
+        }
+        const uint32_t nj = rd.count(1u << 16, "joints");
+        for (uint32_t j = 0; j < nj; ++j) {
+            const V3 ax = rd.v3(), of = rd.v3();
+            F->axis.insert(F->axis.end(), {ax.x, ax.y, ax.z});
+            F->offset.insert(F->offset.end(), {of.x, of.y, of.z});
+        }
+        // sphere sets: only their counts shape the slot layout (batch_layout.cpp:28-43)
+        const uint32_t nsb = rd.count(1u << 16, "sphere bodies");
+        int32_t max_spheres = 1;
+        std::vector<int32_t> nsph(nsb);
+        for (uint32_t b = 0; b < nsb; ++b) {
+            nsph[b] = static_cast<int32_t>(rd.count(1u << 20, "spheres"));
+            max_spheres = std::max(max_spheres, nsph[b]);
+            for (int32_t s = 0; s < nsph[b]; ++s) rd.v3(), rd.f64();
+        }
+        F->eps = rd.f64();
+        F->K = static_cast<int32_t>(rd.u32());
+        F->n_nodes = static_cast<int32_t>(rd.count(1u << 24, "nodes"));
+        F->dof = static_cast<int32_t>(rd.count(1u << 10, "dof"));
+        F->nodes.resize(static_cast<size_t>(F->n_nodes) * F->dof);
+        for (double& v : F->nodes) v = rd.f64();
+        F->n_edges = static_cast<int32_t>(rd.count(1u << 26, "edges"));
+        F->edges.resize(2 * static_cast<size_t>(F->n_edges));
+        for (int32_t& v : F->edges) v = static_cast<int32_t>(rd.u32());
+        const uint32_t ng = rd.count(1u << 26, "geometry");
+        if (ng != static_cast<uint32_t>(F->n_nodes) + static_cast<uint32_t>(F->n_edges))
+            throw FileError(RGG_ROADMAP_TRUNCATED, "geometry count mismatch");
+        const int32_t N = static_cast<int32_t>(ng), B = F->B;
+        if (static_cast<int32_t>(nsb) != B) throw std::invalid_argument("sphere set / body count mismatch");
+        // per component: body OBBs, then per body its splines {radius, sphere index, points}
+        struct Spl {
+            double r;
+            int32_t sphere;
+            uint32_t first, npts;  // into pts
+        };
+        std::vector<Box> boxes(static_cast<size_t>(N) * B);
+        std::vector<std::vector<Spl>> spl(static_cast<size_t>(N) * B);
+        std::vector<V3> pts;
+        for (int32_t c = 0; c < N; ++c) {
+            const uint32_t nover = rd.count(1u << 16, "over boxes");
+            if (static_cast<int32_t>(nover) != B) throw std::invalid_argument("component body count mismatch");
+            for (int32_t b = 0; b < B; ++b) {
+                Box& o = boxes[static_cast<size_t>(c) * B + b];
+                o.c = rd.v3();
+                for (int q = 0; q < 3; ++q) o.ax[q] = rd.v3();
+                o.he = rd.v3();
+            }
+            for (int32_t b = 0; b < B; ++b) {
+                const uint32_t ns = rd.count(1u << 20, "splines");
+                for (uint32_t s = 0; s < ns; ++s) {
+                    Spl sp;
+                    sp.r = rd.f64();
+                    sp.sphere = static_cast<int32_t>(rd.u32());
+                    sp.npts = rd.count(1u << 24, "spline points");
+                    sp.first = static_cast<uint32_t>(pts.size());
+                    for (uint32_t q = 0; q < sp.npts; ++q) pts.push_back(rd.v3());
+                    if (sp.sphere < 0 || sp.sphere >= nsph[b]) throw std::invalid_argument("spline sphere index out of range");
+                    spl[static_cast<size_t>(c) * B + b].push_back(sp);
+                }
+            }
+        }
+        // the component view (rgg_component_view, include/rgg_gpu.h): OBB corners in
+        // obb_corners order, real segments per (component, body, slot) row with the slot
+        // layout of BatchLayout::serialize (batch_layout.cpp:28-105)
+        int32_t max_parts = 1;
+        for (int32_t u = 0; u < N * B; ++u) {
+            std::vector<int32_t> parts(nsph[u % B], 0);
+            for (const Spl& sp : spl[u]) max_parts = std::max(max_parts, ++parts[sp.sphere]);
+        }
+        const int32_t S = max_spheres * max_parts;
+        F->S = S;
+        F->spline_r.assign(static_cast<size_t>(B) * S, 0.0);
+        F->corners.resize(static_cast<size_t>(N) * B * 24);
+        std::vector<int32_t> count(static_cast<size_t>(N) * B * S, 0);
+        std::vector<std::vector<std::pair<int32_t, const Spl*>>> rows(static_cast<size_t>(N) * B);
+        for (int32_t u = 0; u < N * B; ++u) {
+            V3 cs[8];
+            corners_of(boxes[u], cs);
+            for (int i = 0; i < 8; ++i)
+                F->corners[24 * static_cast<size_t>(u) + 3 * i] = cs[i].x, F->corners[24 * static_cast<size_t>(u) + 3 * i + 1] = cs[i].y,
+                                                      F->corners[24 * static_cast<size_t>(u) + 3 * i + 2] = cs[i].z;
+            const int32_t b = u % B;
+            std::vector<int32_t> used(nsph[b], 0);
+            for (const Spl& sp : spl[u]) {
+                const int32_t segc = std::max<int32_t>(1, static_cast<int32_t>(sp.npts) - 1);
+                if (segc > F->K) throw std::logic_error("spline exceeds the segment cap; the build policy should have split it");
+                const int32_t slot = sp.sphere * max_parts + used[sp.sphere]++;
+                double& rad = F->spline_r[static_cast<size_t>(b) * S + slot];
+                if (rad == 0.0) rad = sp.r;
+                else if (rad != sp.r) throw std::logic_error("inconsistent spline radius for a layout slot");
+                count[static_cast<size_t>(u) * S + slot] = segc;
+                rows[u].push_back({slot, &sp});
+            }
+        }
+        F->row_off.assign(count.size() + 1, 0);
+        int64_t total = 0;
+        for (size_t r = 0; r < count.size(); ++r) {
+            F->row_off[r] = static_cast<int32_t>(total);
+            total += count[r];
+            if (total > INT32_MAX) throw std::invalid_argument("more than 2^31 - 1 real segments");
+        }
+        F->row_off[count.size()] = static_cast<int32_t>(total);
+        F->seg_pts.resize(static_cast<size_t>(total) * 6);
+        for (int32_t u = 0; u < N * B; ++u)
+            for (const auto& [slot, sp] : rows[u]) {
+                double* d = &F->seg_pts[6 * static_cast<size_t>(F->row_off[static_cast<size_t>(u) * S + slot])];
+                const V3* q = &pts[sp->first];
+                if (sp->npts == 1) {  // a single-point spline is a degenerate segment (batch_layout.cpp:84-90)
+                    const double s6[6] = {q[0].x, q[0].y, q[0].z, q[0].x, q[0].y, q[0].z};
+                    std::memcpy(d, s6, sizeof(s6));
+                } else {
+                    for (uint32_t k = 0; k + 1 < sp->npts; ++k, d += 6) {
+                        const double s6[6] = {q[k].x, q[k].y, q[k].z, q[k + 1].x, q[k + 1].y, q[k + 1].z};
+                        std::memcpy(d, s6, sizeof(s6));
+                    }
+                }
+            }
+        *out = F.release();
+        return 0;
+    } catch (const FileError& ex) {
+        g_err = ex.what();
+        return ex.kind;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
+    }
+}
+
+int rgg_roadmap_counts(const rgg_roadmap_file* f, int64_t* out) {
+    if (!f || !out) return -1;
+    out[0] = f->n_nodes;
+    out[1] = f->n_edges;
+    out[2] = f->dof;
+    out[3] = static_cast<int64_t>(f->n_nodes) + f->n_edges;
+    out[4] = f->B;
+    out[5] = f->S;
+    out[6] = static_cast<int64_t>(f->seg_pts.size() / 6);
+    out[7] = f->kinematics;
+    out[8] = f->K;
+    return 0;
+}
+
+int rgg_roadmap_components(const rgg_roadmap_file* f, double* obb_corners, int32_t* row_off, double* seg_points,
+                           double* spline_radius) {
+    if (!f) return -1;
+    auto cp = [](void* dst, const auto& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(obb_corners, f->corners);
+    cp(row_off, f->row_off);
+    cp(seg_points, f->seg_pts);
+    cp(spline_radius, f->spline_r);
+    return 0;
+}
+
+int rgg_roadmap_graph(const rgg_roadmap_file* f, double* nodes, int32_t* edges, double* eps) {
+    if (!f) return -1;
+    if (nodes && !f->nodes.empty()) std::memcpy(nodes, f->nodes.data(), f->nodes.size() * sizeof(double));
+    if (edges && !f->edges.empty()) std::memcpy(edges, f->edges.data(), f->edges.size() * sizeof(int32_t));
+    if (eps) *eps = f->eps;
+    return 0;
+}
+
+int rgg_roadmap_robot(const rgg_roadmap_file* f, double* he, double* local12, double* axis, double* offset) {
+    if (!f) return -1;
+    auto cp = [](double* dst, const std::vector<double>& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    };
+    cp(he, f->he);
+    cp(local12, f->local);
+    cp(axis, f->axis);
+    cp(offset, f->offset);
+    return 0;
+}
+
+int rgg_roadmap_poses(const rgg_roadmap_file* f, int64_t* n_configs, int64_t* pose_off, double* poses) {
+    // the exact resolve's inputs: forward_kinematics (robot.cpp:66-84) of every configuration
+    // of discretize_edge (robot.cpp:39-64), which load_roadmap rebuilds (roadmap_io.cpp:294-298)
+    try {
+        if (!f) throw std::invalid_argument("null roadmap file");
+        rgg_robot_view v{};
+        v.kinematics = f->kinematics;
+        v.n_bodies = f->B;
+        v.half_extents = f->he.data();
+        v.local = f->local.data();
+        v.joint_axis = f->axis.empty() ? nullptr : f->axis.data();
+        v.joint_offset = f->offset.empty() ? nullptr : f->offset.data();
+        const Robot rb = make_robot(v, f->eps);
+        if (rb.dof != f->dof) throw std::invalid_argument("configuration DOF mismatch");
+        const int32_t N = f->n_nodes + f->n_edges, B = f->B, dof = f->dof;
+        const auto ends = [&](int32_t c, const double** a, const double** b) {
+            if (c < f->n_nodes) {
+                *a = *b = f->nodes.data() + static_cast<size_t>(dof) * c;
+            } else {
+                *a = f->nodes.data() + static_cast<size_t>(dof) * f->edges[2 * (c - f->n_nodes)];
+                *b = f->nodes.data() + static_cast<size_t>(dof) * f->edges[2 * (c - f->n_nodes) + 1];
+            }
+        };
+        int64_t total = 0;
+        for (int32_t c = 0; c < N; ++c) {
+            const double *a, *b;
+            ends(c, &a, &b);
+            if (pose_off) pose_off[c] = total;
+            total += config_count(a, b, dof, f->eps);
+        }
+        if (pose_off) pose_off[N] = total;
+        if (n_configs) *n_configs = total;
+        if (!poses) return 0;
+        std::vector<Tf> fk(B);
+        double cfg[64];
+        int64_t q = 0;
+        for (int32_t c = 0; c < N; ++c) {
+            const double *a, *b;
+            ends(c, &a, &b);
+            const int n = config_count(a, b, dof, f->eps);
+            for (int i = 0; i < n; ++i, ++q) {
+                if (i == 0) {
+                    std::memcpy(cfg, a, dof * sizeof(double));
+                } else if (i == n - 1) {
+                    std::memcpy(cfg, b, dof * sizeof(double));
+                } else {
+                    const double t = static_cast<double>(i) / static_cast<double>(n - 1);
+                    for (int k = 0; k < dof; ++k) cfg[k] = a[k] + (b[k] - a[k]) * t;
+                }
+                forward_kinematics(rb, cfg, fk.data());
+                for (int32_t bd = 0; bd < B; ++bd) {
+                    double* d = poses + 12 * (static_cast<size_t>(q) * B + bd);
+                    std::memcpy(d, fk[bd].r, 9 * sizeof(double));
+                    d[9] = fk[bd].t.x, d[10] = fk[bd].t.y, d[11] = fk[bd].t.z;
+                }
+            }
+        }
+        return 0;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
+    }
+}
+
+void rgg_roadmap_free(rgg_roadmap_file* f) { delete f; }
 
 int rgg_obstacle_spheres(const double* he3, int32_t count, double* centres, double* radius) {
     if (count < 1 || !(he3[0] > 0 && he3[1] > 0 && he3[2] > 0)) {

@@ -41,6 +41,14 @@ def library():
         L.rgg_build_last_error.restype = C.c_char_p
         L.rgg_obstacle_spheres.argtypes = [vp, C.c_int32, vp, vp]
         L.rgg_build_gpu_count.restype = C.c_int
+        L.rgg_roadmap_load.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.rgg_roadmap_counts.argtypes = [vp, vp]
+        L.rgg_roadmap_components.argtypes = [vp] * 5
+        L.rgg_roadmap_graph.argtypes = [vp] * 4
+        L.rgg_roadmap_robot.argtypes = [vp] * 5
+        L.rgg_roadmap_poses.argtypes = [vp] * 4
+        L.rgg_roadmap_free.argtypes = [vp]
+        L.rgg_roadmap_free.restype = None
         _lib = L
     return _lib
 
@@ -133,6 +141,77 @@ def build_layout_robot(robot: dict, nodes, edges, eps=0.25, max_segments=16, thr
     finally:
         L.rgg_built_free(h)
     return N, B, S, a
+
+
+class RoadmapFileError(RuntimeError):
+    """load_roadmap's RoadmapIoError (proj/include/rgg/roadmap_io.hpp:10-26): ``kind`` is one of
+    "bad_magic", "bad_version", "truncated", "checksum", or "invalid" (an inconsistent file)."""
+
+    def __init__(self, kind, msg):
+        super().__init__(msg)
+        self.kind = kind
+
+
+def load_roadmap(path, with_poses=False) -> dict:
+    """The reference's binary roadmap file (load_roadmap, proj/src/roadmap_io.cpp:205-301), read
+    and verified by ``rgg_roadmap_load`` straight into the component view of
+    ``rgg_gpu_create_from_components``: keys N, B, S, e_plus (obb corners, N*B x 24), row_off,
+    seg_pts (T x 6), spline_r, nodes (n, dof), edges (e, 2), eps, max_segments, robot (the
+    ``build_layout_robot`` dict); with_poses: pose_off, poses (configs, B, 12) for the resolver."""
+    L = library()
+    h = C.c_void_p()
+    rc = L.rgg_roadmap_load(str(path).encode(), C.byref(h))
+    if rc != 0:
+        kinds = {1: "bad_magic", 2: "bad_version", 3: "truncated", 4: "checksum"}
+        raise RoadmapFileError(kinds.get(rc, "invalid"), L.rgg_build_last_error().decode())
+    try:
+        cnt = np.zeros(9, np.int64)
+        L.rgg_roadmap_counts(h, cnt.ctypes.data)
+        n_nodes, n_edges, dof, N, B, S, T, kin, K = (int(x) for x in cnt)
+        out = dict(N=N, B=B, S=S, max_segments=K, e_plus=np.empty((N * B, 24)),
+                   row_off=np.empty(N * B * S + 1, np.int32), seg_pts=np.empty((T, 6)), spline_r=np.empty(B * S),
+                   nodes=np.empty((n_nodes, dof)), edges=np.empty((n_edges, 2), np.int32))
+        L.rgg_roadmap_components(h, out["e_plus"].ctypes.data, out["row_off"].ctypes.data,
+                                 out["seg_pts"].ctypes.data, out["spline_r"].ctypes.data)
+        eps = C.c_double()
+        L.rgg_roadmap_graph(h, out["nodes"].ctypes.data, out["edges"].ctypes.data, C.byref(eps))
+        out["eps"] = eps.value
+        robot = dict(kinematics=kin, he=np.empty((B, 3)), local=np.empty((B, 12)),
+                     axis=np.zeros((B, 3)), offset=np.zeros((B, 3)))
+        L.rgg_roadmap_robot(h, robot["he"].ctypes.data, robot["local"].ctypes.data,
+                            robot["axis"].ctypes.data if kin == SERIAL_CHAIN else None,
+                            robot["offset"].ctypes.data if kin == SERIAL_CHAIN else None)
+        out["robot"] = robot
+        if with_poses:
+            nc = C.c_int64()
+            off = np.empty(N + 1, np.int64)
+            if L.rgg_roadmap_poses(h, C.byref(nc), off.ctypes.data, None) != 0:
+                raise RoadmapFileError("invalid", L.rgg_build_last_error().decode())
+            poses = np.empty((nc.value, B, 12))
+            L.rgg_roadmap_poses(h, None, off.ctypes.data, poses.ctypes.data)
+            out["pose_off"], out["poses"] = off, poses
+    finally:
+        L.rgg_roadmap_free(h)
+    return out
+
+
+def component_view(rf: dict, obstacles: synth.Obstacles):
+    """A loaded roadmap file plus obstacles (box half extents and default sphere counts, as
+    make_box_obstacle builds them) -> the view ``GpuEngine(view, components=True)`` takes."""
+    from types import SimpleNamespace
+
+    M = len(obstacles.he)
+    Cmax = int(obstacles.spheres.max()) if M else 1
+    sl = np.zeros((M, Cmax, 3))
+    sr = np.zeros(M)
+    for o in range(M):
+        cen, r = obstacle_spheres(obstacles.he[o], obstacles.spheres[o])
+        sl[o, : len(cen)] = cen
+        sr[o] = r
+    return SimpleNamespace(N=rf["N"], B=rf["B"], S=rf["S"], M=M, C=Cmax, e_plus=rf["e_plus"], row_off=rf["row_off"],
+                           seg_pts=rf["seg_pts"], spline_r=rf["spline_r"],
+                           obst_he=np.ascontiguousarray(obstacles.he, np.float64), obst_sph_local=sl, obst_sph_r=sr,
+                           obst_sph_n=np.ascontiguousarray(obstacles.spheres, np.int32))
 
 
 def obstacle_spheres(he, count):

@@ -94,3 +94,37 @@ def test_manipulator_end_to_end_from_own_producer():
         assert np.array_equal(eng.states(), re.states()), i
         checks += rep.resolve_checks
     assert checks > 0
+
+
+@pytest.mark.parametrize("scn", ["table4_obstacles_1000_5x", "table5_manipulator_100"])
+def test_engine_from_roadmap_file_matches_reference(scn, tmp_path):
+    """A roadmap file saved by the reference (save_roadmap) straight to the GPU engine:
+    rgg_roadmap_load -> rgg_gpu_create_from_components, the scenario's obstacles, its moves
+    (lazy) and the exact resolve from the file's poses; labels, bits and resolve_all_unknown
+    equal the reference engine's."""
+    import os
+
+    from conftest import GOLDEN
+    from oracle import ref
+    from paper_2603_28674_b200 import engine as E
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    w = ref.World.from_scn(open(os.path.join(GOLDEN, "scenarios", scn + ".scn")).read())
+    path = tmp_path / "r.rgg"
+    w.save(str(path))
+    rf = producer.load_roadmap(path, with_poses=True)
+    L = w.layout()
+    obs = synth.Obstacles(he=np.asarray(L.obst_he).reshape(-1, 3), spheres=np.asarray(L.obst_sph_n, np.int32))
+    view = producer.component_view(rf, obs)
+    eng = E.GpuEngine(view, components=True, allow_wide=True)
+    eng.set_resolver(rf["pose_off"], rf["poses"], rf["robot"]["he"])
+    re = ref.Engine(w, kind=0)
+    ids, rts = w.moves()
+    for i in range(len(ids)):
+        re.update(ids[i], rts[i], lazy=True)
+    eng.batch_update((ids, rts))
+    assert np.array_equal(eng.states(), re.states())
+    assert np.array_equal(eng.obstacle_bits().reshape(-1), re.bits().reshape(-1))
+    assert eng.resolve_all_unknown() == re.resolve_all_unknown()
+    assert np.array_equal(eng.states(), re.states())

@@ -137,3 +137,65 @@ def test_robot_validation_errors():
     skew["local"][0, 1] = 0.5
     with pytest.raises(RuntimeError, match="local frame invalid"):
         producer.build_layout_robot(skew, nodes, edges, 0.1, gpu_fit=False)
+
+
+def _saved(w, tmp_path, name="r.rgg"):
+    path = tmp_path / name
+    w.save(str(path))
+    return path
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("scn", ["quick_smoke", "table5_manipulator_100"])
+def test_roadmap_file_loads_into_the_component_view(scn, tmp_path):
+    """rgg_roadmap_load reads the reference's own save_roadmap file (roadmap_io.cpp:150-203) into the
+    component view: the OBB corners, CSR rows, real segment points and slot radii equal the
+    reference's BatchLayout::serialize of the same components (e_plus, row_off, seg_pts, spline_r),
+    and the resolver poses equal forward_kinematics over the rebuilt discretization."""
+    import os
+
+    from conftest import GOLDEN
+
+    w = ref.World.from_scn(open(os.path.join(GOLDEN, "scenarios", scn + ".scn")).read())
+    rf = producer.load_roadmap(_saved(w, tmp_path), with_poses=True)
+    L = w.layout()
+    assert (rf["N"], rf["B"], rf["S"]) == (L.N, L.B, L.S)
+    for key in ("e_plus", "seg_pts", "spline_r"):
+        assert np.array_equal(rf[key].view(np.uint64), getattr(L, key).view(np.uint64)), key
+    assert np.array_equal(rf["row_off"], L.row_off)
+    nodes, edges = w.roadmap()
+    assert np.array_equal(rf["nodes"], nodes) and np.array_equal(rf["edges"], edges)
+    off, poses = w.poses()
+    assert np.array_equal(rf["pose_off"], off)
+    assert np.array_equal(rf["poses"].view(np.uint64), poses.view(np.uint64))
+    r = w.robot()
+    assert rf["robot"]["kinematics"] == r["kinematics"] and np.array_equal(rf["robot"]["he"], r["he"])
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_roadmap_file_errors(tmp_path):
+    """load_roadmap's error kinds (roadmap_io.hpp:10-16, checked in its order: size, magic, CRC,
+    version), and a file is verified before anything is built."""
+    import os
+    import struct
+    import zlib
+
+    from conftest import GOLDEN
+
+    w = ref.World.from_scn(open(os.path.join(GOLDEN, "scenarios", "quick_smoke.scn")).read())
+    raw = _saved(w, tmp_path).read_bytes()
+
+    def kind(data):
+        p = tmp_path / "bad.rgg"
+        p.write_bytes(data)
+        with pytest.raises(producer.RoadmapFileError) as e:
+            producer.load_roadmap(p)
+        return e.value.kind
+
+    assert kind(b"XXXXXXXX" + raw[8:]) == "bad_magic"
+    assert kind(raw[:9]) == "truncated"
+    assert kind(raw[:200] + bytes([raw[200] ^ 1]) + raw[201:]) == "checksum"
+    body = raw[:8] + struct.pack("<I", 2) + raw[12:-4]
+    assert kind(body + struct.pack("<I", zlib.crc32(body))) == "bad_version"
+    cut = raw[:-40]  # a consistent checksum over a truncated body
+    assert kind(cut + struct.pack("<I", zlib.crc32(cut))) == "truncated"
