@@ -35,6 +35,8 @@ int rgg_build_layout(const double* robot_he3, int32_t n_nodes, const double* nod
 /* also the inner approximation (spline simplification) on the GPU, bit-identical (same device);
  * slower end to end than RGG_BUILD_GPU_FIT alone while serialize stays on the host */
 #define RGG_BUILD_GPU_INNER 4
+/* keep the robot, the roadmap and the swept-volume geometry for rgg_built_save_roadmap */
+#define RGG_BUILD_KEEP_GEOMETRY 8
 int rgg_build_layout_ex(const double* robot_he3, int32_t n_nodes, const double* nodes, int32_t n_edges,
                         const int32_t* edges, double eps, int32_t max_segments, int32_t threads, int32_t flags,
                         rgg_built** out);
@@ -70,6 +72,9 @@ int rgg_built_counts(const rgg_built* b, int64_t* out);
 int rgg_built_export(const rgg_built* b, double* edge_sat, double* comp_aabb, int32_t* row_off, double* segs,
                      double* spline_r, double* obb15);
 void rgg_built_free(rgg_built* b);
+/* save_roadmap (proj/src/roadmap_io.cpp:150-203) of a build made with RGG_BUILD_KEEP_GEOMETRY:
+ * the reference's binary roadmap file, which its load_roadmap reads (and rgg_roadmap_load). */
+int rgg_built_save_roadmap(const rgg_built* b, const char* path);
 const char* rgg_build_last_error(void);
 /* CUDA devices visible to the producer (0 without a GPU): the GPU box fit
  * (RGG_BUILD_GPU_FIT) is the Python producer's default when this is positive. */

@@ -610,6 +610,16 @@ struct rgg_built {
     std::vector<int32_t> row_off;
     std::vector<int64_t> pose_off;  // RGG_BUILD_POSES: N+1
     std::vector<double> poses;      // pose_off[N] * B * 12 (body-minor per configuration)
+    // RGG_BUILD_KEEP_GEOMETRY: what save_roadmap writes (the robot, the roadmap and the
+    // ComponentSet's spheres, resolution, cap and geometry)
+    bool kept = false;
+    Robot robot;
+    std::vector<double> rb_he, rb_local, rb_axis, rb_offset;
+    int32_t kinematics = 0, dof = 0, K = 16;
+    double eps = 0.0;
+    std::vector<double> nodes;
+    std::vector<int32_t> edges;
+    std::vector<Comp> comps;
 };
 
 extern "C" {
@@ -936,7 +946,104 @@ int rgg_build_layout_robot(const rgg_robot_view* robot, int32_t n_nodes, const d
             });
         }
         mark("serialize");
+        if (flags & RGG_BUILD_KEEP_GEOMETRY) {
+            L->kept = true;
+            L->robot = rb;
+            L->kinematics = robot->kinematics;
+            L->dof = dof;
+            L->K = K;
+            L->eps = eps;
+            L->rb_he.assign(robot->half_extents, robot->half_extents + 3 * static_cast<size_t>(B));
+            if (robot->local) L->rb_local.assign(robot->local, robot->local + 12 * static_cast<size_t>(B));
+            if (rb.chain) {
+                L->rb_axis.assign(robot->joint_axis, robot->joint_axis + 3 * static_cast<size_t>(B));
+                L->rb_offset.assign(robot->joint_offset, robot->joint_offset + 3 * static_cast<size_t>(B));
+            }
+            L->nodes.assign(nodes, nodes + static_cast<size_t>(n_nodes) * dof);
+            L->edges.assign(edges, edges + 2 * static_cast<size_t>(n_edges));
+            L->comps = std::move(comps);
+        }
         *out = own.release();
+        return 0;
+    } catch (const std::exception& ex) {
+        g_err = ex.what();
+        return -1;
+    }
+}
+
+// save_roadmap (roadmap_io.cpp:150-203) of a producer build kept with RGG_BUILD_KEEP_GEOMETRY:
+// the same sections, so the reference's load_roadmap reads it (and a build bit-identical to
+// the reference's gives the same file byte for byte)
+int rgg_built_save_roadmap(const rgg_built* b, const char* path) {
+    try {
+        if (!b || !path) throw std::invalid_argument("null build or path");
+        if (!b->kept) throw std::invalid_argument("layout was built without RGG_BUILD_KEEP_GEOMETRY");
+        std::vector<uint8_t> w;
+        const auto u8 = [&](uint8_t v) { w.push_back(v); };
+        const auto u32 = [&](uint32_t v) {
+            for (int i = 0; i < 4; ++i) w.push_back(static_cast<uint8_t>(v >> (8 * i)));
+        };
+        const auto f64 = [&](double d) {
+            uint64_t v;
+            std::memcpy(&v, &d, 8);
+            for (int i = 0; i < 8; ++i) w.push_back(static_cast<uint8_t>(v >> (8 * i)));
+        };
+        const auto v3 = [&](V3 p) { f64(p.x), f64(p.y), f64(p.z); };
+        static const char kMagic[8] = {'R', 'G', 'G', 'R', 'D', 'M', 'P', '1'};
+        w.insert(w.end(), kMagic, kMagic + 8);
+        u32(1);
+        // robot: kinematics, bodies {half extents, local frame}, joints {axis, offset}
+        const int32_t B = b->B;
+        u8(static_cast<uint8_t>(b->kinematics));
+        u32(static_cast<uint32_t>(B));
+        for (int32_t bd = 0; bd < B; ++bd) {
+            v3(b->robot.bodies[bd].he);
+            const Tf& l = b->robot.bodies[bd].local;
+            for (double r : l.r) f64(r);
+            v3(l.t);
+        }
+        u32(static_cast<uint32_t>(b->robot.axis.size()));
+        for (size_t j = 0; j < b->robot.axis.size(); ++j) v3(b->robot.axis[j]), v3(b->robot.offset[j]);
+        // the sphere sets (default_body_spheres), the resolution and the segment cap
+        u32(static_cast<uint32_t>(B));
+        for (int32_t bd = 0; bd < B; ++bd) {
+            const auto& sp = b->robot.bodies[bd].spheres;
+            u32(static_cast<uint32_t>(sp.size()));
+            for (const Sph& s : sp) v3(s.c), f64(s.r);
+        }
+        f64(b->eps);
+        u32(static_cast<uint32_t>(b->K));
+        // the roadmap
+        const uint32_t n_nodes = static_cast<uint32_t>(b->nodes.size() / std::max(1, b->dof));
+        u32(n_nodes);
+        u32(static_cast<uint32_t>(b->dof));
+        for (double v : b->nodes) f64(v);
+        u32(static_cast<uint32_t>(b->edges.size() / 2));
+        for (int32_t v : b->edges) u32(static_cast<uint32_t>(v));
+        // per component: the body OBBs, then per body its splines
+        u32(static_cast<uint32_t>(b->comps.size()));
+        for (const Comp& c : b->comps) {
+            u32(static_cast<uint32_t>(c.over.size()));
+            for (const Box& o : c.over) {
+                v3(o.c);
+                for (int q = 0; q < 3; ++q) v3(o.ax[q]);
+                v3(o.he);
+            }
+            for (const auto& body : c.under) {
+                u32(static_cast<uint32_t>(body.size()));
+                for (const Spline& s : body) {
+                    f64(s.radius);
+                    u32(static_cast<uint32_t>(s.sphere));
+                    u32(static_cast<uint32_t>(s.pts.size()));
+                    for (const V3& q : s.pts) v3(q);
+                }
+            }
+        }
+        u32(crc32_of(w.data(), w.size()));
+        std::FILE* f = std::fopen(path, "wb");
+        if (!f) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
+        const bool ok = std::fwrite(w.data(), 1, w.size(), f) == w.size();
+        if (std::fclose(f) != 0 || !ok) throw std::runtime_error(std::string("short write to ") + path);
         return 0;
     } catch (const std::exception& ex) {
         g_err = ex.what();

@@ -36,6 +36,7 @@ def library():
         L.rgg_built_poses.argtypes = [vp, vp, vp, vp]
         L.rgg_built_counts.argtypes = [vp, vp]
         L.rgg_built_export.argtypes = [vp] * 7
+        L.rgg_built_save_roadmap.argtypes = [vp, C.c_char_p]
         L.rgg_built_free.argtypes = [vp]
         L.rgg_built_free.restype = None
         L.rgg_build_last_error.restype = C.c_char_p
@@ -93,7 +94,7 @@ def build_layout(robot_he, nodes, edges, eps=0.25, max_segments=16, threads=0, w
 
 
 def build_layout_robot(robot: dict, nodes, edges, eps=0.25, max_segments=16, threads=0, with_obbs=False,
-                       with_poses=False, gpu_fit=None, gpu_inner=False):
+                       with_poses=False, gpu_fit=None, gpu_inner=False, save_roadmap=None):
     """build_components (proj/src/roadmap.cpp:104-127) + BatchLayout::serialize for any
     robot: ``robot`` = {"kinematics": FREE_FLYING | SERIAL_CHAIN, "he" (B, 3), optional
     "local" (B, 12), and for chains "axis" / "offset" (B, 3)}; nodes (n, dof).
@@ -101,7 +102,8 @@ def build_layout_robot(robot: dict, nodes, edges, eps=0.25, max_segments=16, thr
     forward kinematics of every discretized configuration (GPU exact resolve).
     gpu_fit: the swept-volume box fit (obb_from_points, geometry.cpp:134-195) of every
     (component, body) on the GPU, bit-identical to the host fit (tests/test_gpu_producer.py);
-    None (the default) = when a GPU is present."""
+    None (the default) = when a GPU is present.  save_roadmap: also write the build as the
+    reference's binary roadmap file (save_roadmap, proj/src/roadmap_io.cpp:150-203) to this path."""
     L = library()
     if gpu_fit is None:
         gpu_fit = gpu_available()
@@ -120,11 +122,13 @@ def build_layout_robot(robot: dict, nodes, edges, eps=0.25, max_segments=16, thr
     h = C.c_void_p()
     rc = L.rgg_build_layout_robot(C.byref(view), len(nodes), nodes.ctypes.data, len(edges), edges.ctypes.data,
                                   float(eps), int(max_segments), int(threads),
-                                  (1 if with_poses else 0) | (2 if gpu_fit else 0) | (4 if gpu_inner else 0),
-                                  C.byref(h))
+                                  (1 if with_poses else 0) | (2 if gpu_fit else 0) | (4 if gpu_inner else 0)
+                                  | (8 if save_roadmap else 0), C.byref(h))
     if rc != 0:
         raise RuntimeError(L.rgg_build_last_error().decode())
     try:
+        if save_roadmap and L.rgg_built_save_roadmap(h, str(save_roadmap).encode()) != 0:
+            raise RuntimeError(L.rgg_build_last_error().decode())
         cnt = np.zeros(4, np.int64)
         L.rgg_built_counts(h, cnt.ctypes.data)
         N, B, S, T = (int(x) for x in cnt)

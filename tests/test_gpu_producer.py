@@ -128,3 +128,15 @@ def test_engine_from_roadmap_file_matches_reference(scn, tmp_path):
     assert np.array_equal(eng.obstacle_bits().reshape(-1), re.bits().reshape(-1))
     assert eng.resolve_all_unknown() == re.resolve_all_unknown()
     assert np.array_equal(eng.states(), re.states())
+
+
+def test_gpu_fit_saves_the_reference_roadmap_file(tmp_path):
+    """The producer with the GPU box fit writes the reference's save_roadmap file byte for byte."""
+    w = _manipulator()
+    r = w.robot()
+    nodes, edges = w.roadmap()
+    ours, theirs = tmp_path / "ours.rgg", tmp_path / "ref.rgg"
+    producer.build_layout_robot(r, nodes, edges, r["eps"], r["max_segments"], threads=4, gpu_fit=True,
+                                save_roadmap=ours)
+    w.save(str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()

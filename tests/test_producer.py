@@ -199,3 +199,29 @@ def test_roadmap_file_errors(tmp_path):
     assert kind(body + struct.pack("<I", zlib.crc32(body))) == "bad_version"
     cut = raw[:-40]  # a consistent checksum over a truncated body
     assert kind(cut + struct.pack("<I", zlib.crc32(cut))) == "truncated"
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+def test_producer_saves_the_reference_roadmap_file(tmp_path):
+    """rgg_built_save_roadmap writes save_roadmap's format (roadmap_io.cpp:150-203): for the
+    manipulator's chain and a free-flying 3-D roadmap the file equals the reference's own,
+    byte for byte (so its load_roadmap reads it), and rgg_roadmap_load reads it back."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2603_28674_b200 import synth
+
+    w = ref.World.from_scn(open(os.path.join(GOLDEN, "scenarios", "table5_manipulator_100.scn")).read())
+    r = w.robot()
+    nodes, edges = w.roadmap()
+    ours = tmp_path / "ours.rgg"
+    producer.build_layout_robot(r, nodes, edges, r["eps"], r["max_segments"], threads=4, gpu_fit=False,
+                                save_roadmap=ours)
+    assert ours.read_bytes() == _saved(w, tmp_path, "ref.rgg").read_bytes()
+    rm = synth.make_roadmap("3d", 60, 6, 4.0, 5)
+    w2 = ref.World.from_roadmap(rm.robot_he, rm.env, rm.nodes, rm.edges)
+    producer.build_layout_robot(producer.free_flying(rm.robot_he), rm.nodes, rm.edges, 0.25, 16, threads=2,
+                                gpu_fit=False, save_roadmap=ours)
+    assert ours.read_bytes() == _saved(w2, tmp_path, "ref2.rgg").read_bytes()
+    rf = producer.load_roadmap(ours)
+    assert rf["N"] == len(rm.nodes) + len(rm.edges)
