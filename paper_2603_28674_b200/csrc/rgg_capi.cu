@@ -894,8 +894,8 @@ static int update_eager(rgg_gpu* h, const int32_t* ids, const double* rt12, int3
             CK(cudaHostAlloc(reinterpret_cast<void**>(&h->h_eg_rep), static_cast<size_t>(cap) * 8 * sizeof(int32_t), 0));
             h->eager_cap = cap;
         }
-        std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
-        std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 96);
+        if (ids != h->h_ids) std::memcpy(h->h_ids, ids, k * sizeof(int32_t));  // moves staged by the caller stay
+        if (rt12 != h->h_rt) std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 96);
         CK(cudaMemsetAsync(h->d_ctr + 18, 0, sizeof(int32_t), h->stream));  // the batch's sticky status
         CK(cudaMemcpyAsync(h->d_eg_ids, h->h_ids, k * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
         CK(cudaMemcpyAsync(h->d_eg_rt, h->h_rt, static_cast<size_t>(k) * 96, cudaMemcpyHostToDevice, h->stream));
@@ -959,8 +959,9 @@ static int update_core(rgg_gpu* h, const int32_t* ids, const double* rt12, int32
         if (rc) return rc;
         rc = grow_pinned(h, k);
         if (rc) return rc;
-        std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
-        std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 12 * sizeof(double));
+        // moves the caller wrote into the staging buffers (rgg_gpu_stage) are already in place
+        if (ids != h->h_ids) std::memcpy(h->h_ids, ids, k * sizeof(int32_t));
+        if (rt12 != h->h_rt) std::memcpy(h->h_rt, rt12, static_cast<size_t>(k) * 12 * sizeof(double));
         // synchronous update with matching staging layouts: the copies are graph nodes
         const bool hostio = !(flags & RGG_ASYNC) && !bad && h->pin_off == h->in_off && graphs_enabled(h);
         if (hostio) {
@@ -1167,6 +1168,19 @@ int rgg_gpu_gray_device(rgg_gpu* h, int32_t* d_count, int32_t* d_ids, int32_t ca
     const int32_t n = std::min(cap, h->s.N);
     if (n > 0) CK(cudaMemcpyAsync(d_ids, h->d_gray, static_cast<size_t>(n) * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                   h->stream));
+    return RGG_OK;
+}
+
+int rgg_gpu_stage(rgg_gpu* h, int32_t n, int32_t** ids, double** rt12) {
+    if (!h || n < 0 || !ids || !rt12) return RGG_EINVAL;
+    if (n >= kMaxBatch) return fail(h, RGG_EINVAL, "at most 2^26 - 1 moves per batch (split it)");
+    CK(cudaSetDevice(h->device));
+    int rc = grow_batch(h, std::max(n, 1));  // device and staging capacities grow together
+    if (rc) return rc;
+    rc = grow_pinned(h, std::max(n, 1));
+    if (rc) return rc;
+    *ids = h->h_ids;
+    *rt12 = h->h_rt;
     return RGG_OK;
 }
 

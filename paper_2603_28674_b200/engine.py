@@ -108,6 +108,7 @@ def library() -> C.CDLL:
         L.rgg_gpu_last_error.argtypes = [vp]
         L.rgg_gpu_last_error.restype = C.c_char_p
         L.rgg_gpu_update.argtypes = [vp, vp, vp, i32, i32, vp]
+        L.rgg_gpu_stage.argtypes = [vp, i32, C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_double))]
         L.rgg_gpu_update_device.argtypes = [vp, vp, vp, i32, i32]
         L.rgg_gpu_sync.argtypes = [vp]
         L.rgg_gpu_count.argtypes = [vp, ip, ip, ip]
@@ -170,7 +171,8 @@ EXPORTED = ["rgg_gpu_create", "rgg_gpu_create_from_components", "rgg_gpu_destroy
             "rgg_gpu_last_stats", "rgg_gpu_census", "rgg_gpu_stream", "rgg_gpu_fp64_peak",
             "rgg_gpu_copy_counters", "rgg_gpu_set_phase_timing", "rgg_gpu_set_resolver", "rgg_gpu_resolve_all",
             "rgg_gpu_exact_check", "rgg_gpu_filter_stats", "rgg_gpu_set_active_obstacles",
-            "rgg_exact_valid_sets", "rgg_gpu_gray_device", "rgg_gpu_fp32_peak", "rgg_gpu_owned", "rgg_gpu_gray_view"]
+            "rgg_exact_valid_sets", "rgg_gpu_gray_device", "rgg_gpu_fp32_peak", "rgg_gpu_owned", "rgg_gpu_gray_view",
+            "rgg_gpu_stage"]
 
 
 @dataclass
@@ -468,6 +470,16 @@ class GpuEngine:
         out = np.empty(len(ids), np.uint8)
         self._check(library().rgg_gpu_exact_check(self._h, ids.ctypes.data, len(ids), out.ctypes.data))
         return out
+
+    def staging(self, n: int):
+        """(ids int32[n], rts float64[n, 12]) views of the engine's pinned staging buffers
+        (rgg_gpu_stage): moves written there go to the device without a host copy when passed
+        to batch_update.  Valid until a larger batch grows the buffers."""
+        pi, pr = C.POINTER(C.c_int32)(), C.POINTER(C.c_double)()
+        self._check(library().rgg_gpu_stage(self._h, int(n), C.byref(pi), C.byref(pr)))
+        ids = np.ctypeslib.as_array(pi, shape=(int(n),))
+        rts = np.ctypeslib.as_array(pr, shape=(int(n), 12))
+        return ids, rts
 
     def update_async(self, ids, rts):
         """Enqueue a lazy batch without waiting (timed device path)."""

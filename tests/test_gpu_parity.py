@@ -343,3 +343,23 @@ def test_gray_list_written_inside_the_host_update(eng_mod, name):
     if len(gray):
         eng.write_states(gray[:1], np.zeros(1, np.uint8))
         assert np.array_equal(eng.gray_ids_view(), gray[1:])
+
+
+@pytest.mark.gpu
+def test_staged_moves_equal_host_moves(eng_mod):
+    """Moves written into the engine's pinned staging buffers (rgg_gpu_stage) give the same
+    reports, labels and bits as the same moves passed from ordinary host arrays."""
+    g = load_golden("scn_table4_obstacles_1000_5x")
+    a = eng_mod.GpuEngine(_layout(g))
+    b = eng_mod.GpuEngine(_layout(g))
+    ids, rts = np.asarray(g["ids"], np.int32), np.asarray(g["rts"], np.float64).reshape(-1, 12)
+    sid, srt = b.staging(len(ids))
+    for a0 in range(0, len(ids), 9):
+        n = min(9, len(ids) - a0)
+        ra = a.batch_update((ids[a0:a0 + n], rts[a0:a0 + n]), gray_list=True).counts()
+        sid[:n], srt[:n] = ids[a0:a0 + n], rts[a0:a0 + n]
+        rb = b.batch_update((sid[:n], srt[:n]), gray_list=True).counts()
+        assert np.array_equal(ra, rb), a0
+        assert np.array_equal(a.gray_ids_view(), b.gray_ids_view()), a0
+    assert np.array_equal(a.states(), b.states())
+    assert np.array_equal(a.obstacle_bits(), b.obstacle_bits())
