@@ -1,17 +1,27 @@
-// rgg_kernels.cu — the SerRGG update pipeline for sm_100a.
+// rgg_kernels.cu — the SerRGG update pipeline for sm_100a (DESIGN.md §4).
 //
-//   pose      one thread per move: BatchLayout::update_transforms
-//             (proj/src/batch_layout.cpp:148-172) on device, fp64-exact.
-//   bin       one warp per cell: closed AABB test of every event's new and old
-//             box against the cell's box, ordered warp-ballot compaction into a
-//             fixed-capacity cell list + overflow pool, dirty-cell list.
-//             Replaces SpatialGrid::candidates (proj/src/spatial_grid.cpp:114-135).
-//   classify  one CTA per dirty cell, one thread per component: the cell's event
-//             list staged in shared memory, each event applied in move order with
-//             the reference's per-move state transition (engine_batch.cpp:114-188):
-//             15-axis SAT (over) and segment-sphere (under) narrow tests.
-//   commit    one thread per move: the moved obstacles' resident operands.
-//   compact   ordered ballot/prefix compaction of the GRAY component ids.
+// One update = one CUDA graph of programmatically dependent launches:
+//   pose          one warp per move: BatchLayout::update_transforms
+//                 (proj/src/batch_layout.cpp:148-172) on the device, fp64-exact; the
+//                 event boxes (widened by 2^-40), SAT operands, Box32 filter line and the
+//                 fp32 sphere operands of every move.
+//   bin           bin_scatter_kernel (a CTA per event over a uniform grid of the cell
+//                 boxes, event bitmask per cell) + bin_cells_kernel (a warp per cell:
+//                 ordered lists by popcount / prefix scan, fixed capacity + overflow
+//                 pool, work units), or bin_small_kernel for <= 64 moves.  Replaces
+//                 SpatialGrid::build / candidates (proj/src/spatial_grid.cpp:50-135).
+//   touch         touch_cta_kernel: a CTA per cell chunk, a warp per 32-component slice:
+//                 the closed AABB tests that decide which (component, event) pairs need
+//                 the narrow tests, queued as over / under items.
+//   narrow        narrow_over_kernel (the 15-axis SAT, kernels_scalar.cpp:37-69) and
+//                 narrow_under_kernel (segment-sphere, :81-96): fp32 filters with
+//                 rigorous bounds, the reference's fp64 sequence for undecided pairs.
+//   apply         apply_warp_kernel: a warp per slice, the reference's per-move
+//                 transitions in move order (engine_batch.cpp:114-188), per-move
+//                 report counters, the moved obstacles' operands committed.
+//   compact       gray_count / gray_write: ordered compaction of the GRAY ids.
+// Single moves (update_obstacle, eager updates) run single_cells_kernel after pose
+// instead of bin .. apply.
 #include <cstdio>
 #include <cstdlib>
 
