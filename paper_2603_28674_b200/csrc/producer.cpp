@@ -1151,7 +1151,11 @@ int rgg_roadmap_load(const char* path, rgg_roadmap_file** out) {
         for (double& v : F->nodes) v = rd.f64();
         F->n_edges = static_cast<int32_t>(rd.count(1u << 26, "edges"));
         F->edges.resize(2 * static_cast<size_t>(F->n_edges));
-        for (int32_t& v : F->edges) v = static_cast<int32_t>(rd.u32());
+        for (int32_t& v : F->edges) {
+            const uint32_t e = rd.u32();
+            if (e >= static_cast<uint32_t>(F->n_nodes)) throw std::invalid_argument("edge endpoint out of range");
+            v = static_cast<int32_t>(e);
+        }
         const uint32_t ng = rd.count(1u << 26, "geometry");
         if (ng != static_cast<uint32_t>(F->n_nodes) + static_cast<uint32_t>(F->n_edges))
             throw FileError(RGG_ROADMAP_TRUNCATED, "geometry count mismatch");
