@@ -180,6 +180,8 @@ __device__ __forceinline__ void box_of(const double* rt, const double* he, int c
     }
 }
 
+constexpr int kBinSmallMax = 64;  // bin_small_kernel takes batches up to this many moves
+
 __global__ void pose_kernel(Store s, Batch b) {
     const unsigned long long t0 = tl_start(b.tl);
     pdl_trigger();  // the bin kernel's CTAs may land now; they wait for these events in pdl_wait()
@@ -203,13 +205,22 @@ __global__ void pose_kernel(Store s, Batch b) {
     // prev / last links: the same obstacle moved earlier / later in this batch
     int p = -1;
     bool is_last = true;
-    for (int base = 0; base < b.n; base += 32) {
-        const int j = base + lane;
-        const bool same = j < b.n && mids[j] == o;
-        const unsigned before = __ballot_sync(0xffffffffu, same && j < i);
-        const unsigned after = __ballot_sync(0xffffffffu, same && j > i);
-        if (before) p = base + 31 - __clz(before);
-        if (after) is_last = false;
+    for (int base = 0; base < b.n; base += 256) {  // eight ids per lane in flight, then the ballots
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = base + 32 * u + lane;
+            v[u] = j < b.n ? mids[j] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = base + 32 * u + lane;
+            const bool same = v[u] == o;
+            const unsigned before = __ballot_sync(0xffffffffu, same && j < i);
+            const unsigned after = __ballot_sync(0xffffffffu, same && j > i);
+            if (before) p = base + 32 * u + 31 - __clz(before);
+            if (after) is_last = false;
+        }
     }
     const double he[3] = {s.ohe[3 * o], s.ohe[3 * o + 1], s.ohe[3 * o + 2]};
     const double cu = lane < 6 ? s.cur_union[6 * o + lane] : 0.0;  // the old union box when p < 0
@@ -307,7 +318,9 @@ __global__ void pose_kernel(Store s, Batch b) {
         b.evbox[12 * static_cast<size_t>(i) + lane] = nu6;  // compact copy for the binning
         b.evbox[12 * static_cast<size_t>(i) + 6 + lane] = ol6;
     }
-    if (b.evready) {  // release: the warp's stores (evbox, and the counter resets of warp 0), then the count
+    // release: the warp's stores (evbox, and the counter resets of warp 0), then the count; only
+    // bin_small_kernel and the touch on published units poll it (bin_scatter takes the PDL wait)
+    if (b.evready && (b.n <= kBinSmallMax || b.unit_ready)) {
         __syncwarp();
         if (lane == 0) {
             __threadfence();
@@ -704,7 +717,6 @@ __global__ void __launch_bounds__(32 * kCellWarps) bin_cells_kernel(Store s, Bat
 // tests events l and l + 32 (exact fp64 closed-box tests of the new and old
 // boxes), two ordered ballots build the list.  Small warps-per-CTA so every cell's
 // warp is resident in one wave even for a million components (c4: 8400 cells).
-constexpr int kBinSmallMax = 64;
 constexpr int kBinSmallWarps = 8;
 
 __global__ void __launch_bounds__(32 * kBinSmallWarps) bin_small_kernel(Store s, Batch b) {
