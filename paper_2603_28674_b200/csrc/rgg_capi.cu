@@ -109,6 +109,8 @@ struct rgg_gpu {
     int4* d_items_over = nullptr;
     int4* d_items_under = nullptr;
     int32_t items_cap = 0;
+    int4* d_items_recheck = nullptr;  // Batch::items_recheck (rggk::kRecheckCap entries)
+    int32_t recheck_cap = 0;
     // pinned staging
     int32_t cap_pin = 0;
     int32_t* h_ids = nullptr;
@@ -297,6 +299,8 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.items_over = h->d_items_over;
     b.items_under = h->d_items_under;
     b.items_cap = h->items_cap;
+    b.items_recheck = h->d_items_recheck;
+    b.recheck_cap = h->recheck_cap;
     static const bool timeline = std::getenv("RGG_DEBUG_TIMELINE") != nullptr;
     if (timeline && !h->d_tl) cudaMalloc(reinterpret_cast<void**>(&h->d_tl), 128 * 8);
     b.tl = h->d_tl;
@@ -723,6 +727,10 @@ int create_impl(rgg_gpu* h, const rgg_layout_view* v, const rgg_gpu_options* opt
         h->items_cap = std::max(16, std::atoi(e));
     CK(dalloc(&h->d_items_over, h->items_cap));
     CK(dalloc(&h->d_items_under, h->items_cap));
+    CK(dalloc(&h->d_items_recheck, rggk::kRecheckCap));
+    h->recheck_cap = rggk::kRecheckCap;
+    if (const char* e = std::getenv("RGG_RECHECK_CAP"))  // tests: a tiny queue takes the re-run-every-item path
+        h->recheck_cap = std::min(rggk::kRecheckCap, std::max(0, std::atoi(e)));
     CK(dalloc(&h->d_gray, N));
     CK(dalloc(&h->d_tiles, N / 4096 + 2));
     CK(dalloc(&h->d_hits, N));
@@ -821,7 +829,7 @@ void rgg_gpu_destroy(rgg_gpu* h) {
     void* dev[] = {h->d_aabb, h->d_sat, h->d_sat32, h->grid.off, h->grid.cells, h->d_cmask, h->d_evbox, h->d_evt, h->d_evs, h->d_units, h->d_unit_ready, h->d_row, h->d_seg, h->d_seg32, h->d_spline, h->d_orig, h->d_rank, h->d_cell_aabb, h->d_slice_aabb,
                    h->d_ohe, h->d_osl, h->d_osr, h->d_osn, h->d_state, h->d_state_c, h->d_cnt, h->d_over, h->d_under, h->d_cur,
                    h->d_cur_union, h->d_ctr, h->d_census, h->d_gray, h->d_tiles, h->d_hits, h->d_cell_count,
-                   h->d_cell_list, h->d_cell_ovf, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_mpool, h->d_ev,
+                   h->d_cell_list, h->d_cell_ovf, h->d_ids, h->d_last, h->d_mtop, h->d_crec, h->d_items_over, h->d_items_under, h->d_items_recheck, h->d_mpool, h->d_ev,
                    h->d_mv, h->d_pool, h->d_tl, h->d_hits_prev, h->d_evready,
                    h->d_res_he, h->d_res_off, h->d_res_pose, h->d_opoly, h->d_res_spose, h->d_res_sact, h->d_res_ids, h->d_res_cnt, h->d_res_out,
                    h->d_eg_ids, h->d_eg_rt, h->d_eg_rep};

@@ -15,7 +15,8 @@
 //                 the narrow tests, queued as over / under items.
 //   narrow        narrow_over_kernel (the 15-axis SAT, kernels_scalar.cpp:37-69) and
 //                 narrow_under_kernel (segment-sphere, :81-96): fp32 filters with
-//                 rigorous bounds, the reference's fp64 sequence for undecided pairs.
+//                 rigorous bounds, the reference's fp64 sequence for undecided pairs
+//                 (undecided SAT pairs queued, then a warp each in narrow_under's tail).
 //   apply         apply_warp_kernel: a warp per slice, the reference's per-move
 //                 transitions in move order (engine_batch.cpp:114-188), per-move
 //                 report counters, the moved obstacles' operands committed.
@@ -821,6 +822,21 @@ __device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev
     return hit;
 }
 
+// The fp32 filter alone: 1 some body surely intersects, 0 every body surely separates,
+// 2 undecided (queued: narrow_under_kernel's tail runs the exact fp64 test; keeping that
+// path out of narrow_over_kernel leaves it 71 registers instead of 122, 7 CTAs per SM, not 4)
+__device__ __forceinline__ int over_filter(const Store& s, int c, const Event& ev) {
+    int r = 0;
+    const rggd::Box32G o32 = rggd::load_box32g(&ev.b32);
+    for (int b = 0; b < s.B; ++b) {
+        const rggd::Box32G a32 = rggd::load_box32g(s.sat32 + static_cast<size_t>(c) * s.B + b);
+        const int f = rggd::sat_filter32g(a32, o32.c, o32);
+        if (f == 1) return 1;
+        if (f == 2) r = 2;
+    }
+    return r;
+}
+
 // batch_under for one pair (engine_batch.cpp:76-112): any real segment of any
 // (body, slot) row within o_minus_r + spline_radius of any obstacle sphere.
 template <bool COUNT>
@@ -987,7 +1003,9 @@ __global__ void __launch_bounds__(128) narrow_census_kernel(Store s, Batch b) {
 // right away; narrow_under_kernel's CTAs therefore start only after every over CTA is
 // past its wait (touch complete, its items visible), run without a wait of their own,
 // and wait for narrow_over_kernel before they exit, so the apply kernel's wait on
-// narrow_under_kernel covers both.
+// narrow_under_kernel covers both.  The over pairs the fp32 filter leaves undecided are
+// queued (Batch::items_recheck) and decided in fp64 by narrow_under_kernel after that wait
+// (narrow_recheck), so narrow_over_kernel carries only the filter's registers.
 __global__ void __launch_bounds__(128) narrow_over_kernel(Store s, Batch b) {
     pdl_wait();
     pdl_trigger();
@@ -1003,14 +1021,55 @@ __global__ void __launch_bounds__(128) narrow_over_kernel(Store s, Batch b) {
             prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
             prefetch_l1(&b.ev[nx.y].b32);
         }
-        if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+        const int f = over_filter(s, it.x, b.ev[it.y]);
+        if (f == 1) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+        if (f == 2) {
+            const int q = atomicAdd(&b.ctr[12], 1);
+            if (q < b.recheck_cap) b.items_recheck[q] = it;
+        }
         it = nx;
         nx = nn;
         i = inext;
     }
 }
 
-__global__ void __launch_bounds__(128) narrow_under_kernel(Store s, Batch b) {
+// over_test<false> for one pair by a whole warp: the filter per body, and for an undecided
+// body the exact fp64 test with its 15 axes split over lanes (rggd::sat_separated_part:
+// the pair is separated iff some lane finds a separating tested axis, so the verdict is
+// sat_boxes' whatever the order)
+__device__ __forceinline__ bool over_test_warp(const Store& s, int c, const Event& ev, int lane) {
+    const rggd::Box32G o32 = rggd::load_box32g(&ev.b32);
+    for (int b = 0; b < s.B; ++b) {
+        const size_t i = static_cast<size_t>(c) * s.B + b;
+        const int f = rggd::sat_filter32g(rggd::load_box32g(s.sat32 + i), o32.c, o32);
+        if (f == 1) return true;
+        if (f == 2) {
+            if (lane == 0) atomicAdd(&g_filter_stats[1], 1ull);
+            const bool sep = lane < 15 && rggd::sat_separated_part(s.sat + i * 22, ev.sat, lane, 15);
+            if (!__any_sync(0xffffffffu, sep)) return true;
+        }
+    }
+    return false;
+}
+
+// The over items narrow_over_kernel's filter left undecided (Batch::items_recheck, count
+// ctr[12]), a warp per item, by narrow_under_kernel once narrow_over_kernel is complete;
+// past recheck_cap queued items every over item is re-run.
+__device__ __forceinline__ void narrow_recheck(const Store& s, const Batch& b) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int n = b.ctr[12];
+    const bool all = n > b.recheck_cap;
+    const int total = all ? min(b.ctr[8], b.items_cap) : n;
+    const int4* items = all ? b.items_over : b.items_recheck;
+    for (int i = gw; i < total; i += nwarps) {
+        const int4 it = items[i];
+        if (over_test_warp(s, it.x, b.ev[it.y], lane) && lane == 0)
+            atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+    }
+}
+
+__global__ void __launch_bounds__(128, 9) narrow_under_kernel(Store s, Batch b) {
     pdl_trigger();
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
     const int total = min(b.ctr[9], b.items_cap);
@@ -1031,6 +1090,7 @@ __global__ void __launch_bounds__(128) narrow_under_kernel(Store s, Batch b) {
         i = inext;
     }
     pdl_wait();  // narrow_over_kernel is complete before this grid is
+    narrow_recheck(s, b);
 }
 
 // ------------------------------------------------- warp-slice touch / GPU-wide narrow / warp-slice apply

@@ -13,6 +13,7 @@ constexpr int kMaxSpheres = 16;  // obstacle inner spheres per event (C)
 constexpr int kEvS = kMaxSpheres + 1;  // float4 records per event in Batch::evs
 constexpr int kEvChunk = 32;     // events staged in shared memory per pass (one bit each)
 constexpr int kMaxCell = 128;
+constexpr int kRecheckCap = 1 << 16;  // Batch::items_recheck entries (beyond: every over item is re-run)
 
 // One obstacle move after re-posing (BatchLayout::update_transforms,
 // proj/src/batch_layout.cpp:148-172), plus the obstacle's previous union box.
@@ -102,6 +103,8 @@ struct Batch {
     int4* items_over;            // {component, event, result word, bit}: pairs needing a SAT
     int4* items_under;           // same for the segment-sphere test
     int32_t items_cap;
+    int4* items_recheck;         // over items the fp32 filter left undecided (count ctr[12])
+    int32_t recheck_cap;
     int32_t census_on;           // touch accumulates the byte census
     int32_t* unknown;      // running GRAY count, persistent across batches
     unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null

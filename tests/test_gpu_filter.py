@@ -160,12 +160,10 @@ def test_seg_filter_adversarial_update_path(centre, o_r):
     assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} segment-sphere verdicts differ"
 
 
-@pytest.mark.parametrize("origin", [(0.4, -0.3, 0.2), (70.7, -69.2, 0.2), (-2.5e3, 4.0e3, 15.0)])
-def test_sat_filter_adversarial_update_path(origin):
-    """The narrow kernel's over filter on the 64-byte heads with an fp32 centre
-    (rggd::sat_filter32h): near-contact boxes around an obstacle far from the origin too,
-    through a real update; GRAY iff the reference's sat_boxes intersects."""
-    from paper_2603_28674_b200.engine import GpuEngine, LayoutView
+def _near_contact_sat_layout(origin):
+    """150 near-contact box families around one obstacle posed at `origin`: the box at the
+    bisected contact distance, offsets around it and the neighbouring doubles."""
+    from paper_2603_28674_b200.engine import LayoutView
 
     rng = np.random.default_rng(int(abs(origin[0])) + 17)
     he_o = np.array([1.3, 0.7, 0.9])
@@ -198,12 +196,44 @@ def test_sat_filter_adversarial_update_path(origin):
                     row_off=np.zeros(N + 1, np.int32), segs=np.zeros((0, 7)), spline_r=np.zeros(1),
                     obst_he=he_o[None, :], obst_sph_local=np.zeros((1, 1, 3)), obst_sph_r=np.array([0.1]),
                     obst_sph_n=np.ones(1, np.int32))
+    exp = oracle.sat_batch(boxes, np.arange(N, dtype=np.int32), osat).astype(bool)
+    return lv, pose, exp
+
+
+@pytest.mark.parametrize("origin", [(0.4, -0.3, 0.2), (70.7, -69.2, 0.2), (-2.5e3, 4.0e3, 15.0)])
+def test_sat_filter_adversarial_update_path(origin):
+    """The over filter on the 64-byte heads with an fp32 centre (rggd::sat_filter32h):
+    near-contact boxes around an obstacle far from the origin too, through a real update
+    (the single-move kernel); GRAY iff the reference's sat_boxes intersects."""
+    from paper_2603_28674_b200.engine import GpuEngine
+
+    lv, pose, exp = _near_contact_sat_layout(origin)
     eng = GpuEngine(lv)
     eng.update_obstacle(0, pose)
     got = eng.states() == 2
-    exp = oracle.sat_batch(boxes, np.arange(N, dtype=np.int32), osat).astype(bool)
-    assert 0 < exp.sum() < N
+    assert 0 < exp.sum() < len(exp)
     assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
+
+
+@pytest.mark.parametrize("cap", [None, "0", "5"])
+def test_sat_filter_adversarial_batched(cap, monkeypatch):
+    """The same near-contact boxes through the batched pipeline (two moves of the
+    obstacle, the second onto the contact pose): narrow_over_kernel queues the pairs its
+    fp32 filter leaves undecided, narrow_recheck_kernel decides them in fp64; with a queue
+    smaller than the undecided pairs (cap 0, 5) the recheck kernel re-runs every over item."""
+    from paper_2603_28674_b200.engine import GpuEngine
+
+    if cap is not None:
+        monkeypatch.setenv("RGG_RECHECK_CAP", cap)
+    lv, pose, exp = _near_contact_sat_layout((70.7, -69.2, 0.2))
+    eng = GpuEngine(lv)
+    far = pose.copy()
+    far[9:] += 1e4
+    eng.filter_stats(reset=True)
+    eng.batch_update((np.zeros(2, np.int32), np.stack([far, pose])))
+    got = eng.states() == 2
+    assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
+    assert eng.filter_stats()["sat_rechecks"] > 5, "the near-contact pairs must reach the fp64 recheck"
 
 
 def _aabb_of(cs):

@@ -208,6 +208,24 @@ def test_item_queue_overflow_replays(eng_mod, name, monkeypatch):
     assert np.array_equal(bits, g["snap_bits"][-1].reshape(bits.shape))
 
 
+@pytest.mark.parametrize("cap", ["0", "1"])
+@pytest.mark.parametrize("name", ["scn_table4_obstacles_1000_5x", "syn_se2_m80", "scn_table5_manipulator_100", "syn_3d_m20"])
+def test_recheck_queue_overflow(eng_mod, name, cap, monkeypatch):
+    """The over items the fp32 filter leaves undecided go through a bounded queue to
+    narrow_recheck_kernel (the fp64 recheck); past the queue's capacity that kernel re-runs
+    every over item instead.  Both ways the labels, bits and reports equal the reference's."""
+    g = load_golden(name)
+    monkeypatch.setenv("RGG_RECHECK_CAP", cap)
+    eng = eng_mod.GpuEngine(_layout(g))
+    reps = eng.batch_update((g["ids"], g["rts"]))
+    if int(g["groups"]) == 1:
+        got = np.array([[r.new_green, r.new_red, r.new_gray, r.unknown_after_heuristic] for r in reps])
+        assert np.array_equal(got, g["reports"][:, :4])
+    assert np.array_equal(eng.states(), g["snap_states"][-1])
+    bits = _bits2d(eng.obstacle_bits(), eng.words)
+    assert np.array_equal(bits, g["snap_bits"][-1].reshape(bits.shape))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}, {"RGG_NO_SMALL_BIN": "1"},
                                  {"RGG_NO_SINGLE": "1"}, {"RGG_WARP_TOUCH": "1"}, {"RGG_NO_PDL": "1"}])
