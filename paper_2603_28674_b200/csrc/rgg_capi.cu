@@ -111,6 +111,7 @@ struct rgg_gpu {
     int32_t items_cap = 0;
     int4* d_items_recheck = nullptr;  // Batch::items_recheck (rggk::kRecheckCap entries)
     int32_t recheck_cap = 0;
+    int32_t recheck_min_moves = 0;  // batches of at least this many moves queue the undecided SAT pairs
     // pinned staging
     int32_t cap_pin = 0;
     int32_t* h_ids = nullptr;
@@ -301,6 +302,7 @@ Batch batch_of(rgg_gpu* h, int32_t n) {
     b.items_cap = h->items_cap;
     b.items_recheck = h->d_items_recheck;
     b.recheck_cap = h->recheck_cap;
+    b.recheck_queue = n >= h->recheck_min_moves;
     static const bool timeline = std::getenv("RGG_DEBUG_TIMELINE") != nullptr;
     if (timeline && !h->d_tl) cudaMalloc(reinterpret_cast<void**>(&h->d_tl), 128 * 8);
     b.tl = h->d_tl;
@@ -731,6 +733,11 @@ int create_impl(rgg_gpu* h, const rgg_layout_view* v, const rgg_gpu_options* opt
     h->recheck_cap = rggk::kRecheckCap;
     if (const char* e = std::getenv("RGG_RECHECK_CAP"))  // tests: a tiny queue takes the re-run-every-item path
         h->recheck_cap = std::min(rggk::kRecheckCap, std::max(0, std::atoi(e)));
+    // small batches decide the undecided SAT pairs inline: their narrow phase is short, so the
+    // queued pairs' fp64 chain after the over grid costs more than the occupancy saves
+    h->recheck_min_moves = 128;
+    if (const char* e = std::getenv("RGG_RECHECK_MIN_MOVES"))  // tests: the queue for every batch size
+        h->recheck_min_moves = std::max(0, std::atoi(e));
     CK(dalloc(&h->d_gray, N));
     CK(dalloc(&h->d_tiles, N / 4096 + 2));
     CK(dalloc(&h->d_hits, N));

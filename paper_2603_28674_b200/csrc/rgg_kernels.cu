@@ -824,7 +824,8 @@ __device__ __forceinline__ bool over_test(const Store& s, int c, const Event& ev
 
 // The fp32 filter alone: 1 some body surely intersects, 0 every body surely separates,
 // 2 undecided (queued: narrow_under_kernel's tail runs the exact fp64 test; keeping that
-// path out of narrow_over_kernel leaves it 71 registers instead of 122, 7 CTAs per SM, not 4)
+// path out of narrow_over_kernel<true> leaves it 71 registers instead of 122, 7 CTAs per SM,
+// not 4; batches under Batch::recheck_queue's threshold run narrow_over_kernel<false>)
 __device__ __forceinline__ int over_filter(const Store& s, int c, const Event& ev) {
     int r = 0;
     const rggd::Box32G o32 = rggd::load_box32g(&ev.b32);
@@ -1006,6 +1007,7 @@ __global__ void __launch_bounds__(128) narrow_census_kernel(Store s, Batch b) {
 // narrow_under_kernel covers both.  The over pairs the fp32 filter leaves undecided are
 // queued (Batch::items_recheck) and decided in fp64 by narrow_under_kernel after that wait
 // (narrow_recheck), so narrow_over_kernel carries only the filter's registers.
+template <bool QUEUE>
 __global__ void __launch_bounds__(128) narrow_over_kernel(Store s, Batch b) {
     pdl_wait();
     pdl_trigger();
@@ -1021,11 +1023,15 @@ __global__ void __launch_bounds__(128) narrow_over_kernel(Store s, Batch b) {
             prefetch_l1(s.sat32 + static_cast<size_t>(nx.x) * s.B);
             prefetch_l1(&b.ev[nx.y].b32);
         }
-        const int f = over_filter(s, it.x, b.ev[it.y]);
-        if (f == 1) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
-        if (f == 2) {
-            const int q = atomicAdd(&b.ctr[12], 1);
-            if (q < b.recheck_cap) b.items_recheck[q] = it;
+        if (QUEUE) {
+            const int f = over_filter(s, it.x, b.ev[it.y]);
+            if (f == 1) atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
+            if (f == 2) {
+                const int q = atomicAdd(&b.ctr[12], 1);
+                if (q < b.recheck_cap) b.items_recheck[q] = it;
+            }
+        } else if (over_test<false>(s, it.x, b.ev[it.y], nullptr)) {  // small batches: the fp64 path inline
+            atomicOr(&b.mpool[it.z], static_cast<uint32_t>(it.w));
         }
         it = nx;
         nx = nn;
@@ -2176,17 +2182,21 @@ cudaError_t launch_classify(const Store& s, const Batch& b, int flags, int grid,
                                      dim3(grid_slices(s, reinterpret_cast<const void*>(touch_warp_kernel<false>))),
                                      dim3(32 * kWarpsPerCta), st, s, b);
     {
-        static int g_over = 0, g_under = 0;
+        static int g_over = 0, g_over_inline = 0, g_under = 0;
         if (!g_over) {
             int sms = 148, dev = 0, n = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_over_kernel, 128, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_over_kernel<true>, 128, 0);
             g_over = sms * std::max(1, n);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_over_kernel<false>, 128, 0);
+            g_over_inline = sms * std::max(1, n);
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, narrow_under_kernel, 128, 0);
             g_under = sms * std::max(1, n);
         }
-        if (e == cudaSuccess) e = launch_pdl(narrow_over_kernel, dim3(g_over), dim3(128), st, s, b);
+        if (e == cudaSuccess)
+            e = b.recheck_queue ? launch_pdl(narrow_over_kernel<true>, dim3(g_over), dim3(128), st, s, b)
+                                : launch_pdl(narrow_over_kernel<false>, dim3(g_over_inline), dim3(128), st, s, b);
         if (e == cudaSuccess) e = launch_pdl(narrow_under_kernel, dim3(g_under), dim3(128), st, s, b);
     }
     if (e != cudaSuccess) return e;

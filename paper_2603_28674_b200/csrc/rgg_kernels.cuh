@@ -105,6 +105,7 @@ struct Batch {
     int32_t items_cap;
     int4* items_recheck;         // over items the fp32 filter left undecided (count ctr[12])
     int32_t recheck_cap;
+    int32_t recheck_queue;       // narrow_over queues its undecided pairs (else decides them inline)
     int32_t census_on;           // touch accumulates the byte census
     int32_t* unknown;      // running GRAY count, persistent across batches
     unsigned long long* tl;      // optional per-kernel timeline (RGG_DEBUG_TIMELINE), else null

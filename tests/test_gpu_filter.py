@@ -215,15 +215,18 @@ def test_sat_filter_adversarial_update_path(origin):
     assert np.array_equal(got, exp), f"{int(np.sum(got != exp))} SAT verdicts differ"
 
 
-@pytest.mark.parametrize("cap", [None, "0", "5"])
+@pytest.mark.parametrize("cap", ["inline", None, "0", "5"])
 def test_sat_filter_adversarial_batched(cap, monkeypatch):
     """The same near-contact boxes through the batched pipeline (two moves of the
-    obstacle, the second onto the contact pose): narrow_over_kernel queues the pairs its
-    fp32 filter leaves undecided, narrow_recheck_kernel decides them in fp64; with a queue
-    smaller than the undecided pairs (cap 0, 5) the recheck kernel re-runs every over item."""
+    obstacle, the second onto the contact pose).  A batch this small decides the pairs the
+    fp32 filter leaves undecided inline ("inline"); with RGG_RECHECK_MIN_MOVES=0
+    narrow_over_kernel queues them and narrow_under_kernel's tail decides them in fp64, and
+    with a queue smaller than the undecided pairs (cap 0, 5) that tail re-runs every over item."""
     from paper_2603_28674_b200.engine import GpuEngine
 
-    if cap is not None:
+    if cap != "inline":
+        monkeypatch.setenv("RGG_RECHECK_MIN_MOVES", "0")
+    if cap not in (None, "inline"):
         monkeypatch.setenv("RGG_RECHECK_CAP", cap)
     lv, pose, exp = _near_contact_sat_layout((70.7, -69.2, 0.2))
     eng = GpuEngine(lv)

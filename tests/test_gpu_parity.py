@@ -213,9 +213,11 @@ def test_item_queue_overflow_replays(eng_mod, name, monkeypatch):
 def test_recheck_queue_overflow(eng_mod, name, cap, monkeypatch):
     """The over items the fp32 filter leaves undecided go through a bounded queue to
     narrow_recheck_kernel (the fp64 recheck); past the queue's capacity that kernel re-runs
-    every over item instead.  Both ways the labels, bits and reports equal the reference's."""
+    every over item instead.  Both ways the labels, bits and reports equal the reference's.
+    (RGG_RECHECK_MIN_MOVES=0: the queue for these small batches too.)"""
     g = load_golden(name)
     monkeypatch.setenv("RGG_RECHECK_CAP", cap)
+    monkeypatch.setenv("RGG_RECHECK_MIN_MOVES", "0")
     eng = eng_mod.GpuEngine(_layout(g))
     reps = eng.batch_update((g["ids"], g["rts"]))
     if int(g["groups"]) == 1:
