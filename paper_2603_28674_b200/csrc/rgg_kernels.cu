@@ -415,6 +415,119 @@ __global__ void pose_kernel(Store s, Batch b) {
     tl_stop(b.tl, 0, t0);
 }
 
+// The binning boxes of move i (Batch::evbox: the new box U spheres, then the old), by one
+// warp with pose_kernel's exact operations, so bin_scatter_kernel starts without waiting for
+// the pose kernel (lanes < 6 store out[lane] and out[6 + lane]).
+__device__ __forceinline__ void binning_boxes_warp(const Store& s, const Batch& b, int i, int lane, double* out) {
+    const int32_t* mids = b.src_ids ? b.src_ids : b.ids;
+    const double* mrt = b.src_ids ? b.src_rt : b.rt;
+    const double* rt_new = mrt + 12 * static_cast<size_t>(i);
+    double rtl[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) rtl[k] = rt_new[k];
+    const int o = mids[i];
+    int p = -1;
+    for (int base = 0; base < b.n; base += 256) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = base + 32 * u + lane;
+            v[u] = j < b.n ? mids[j] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int j = base + 32 * u + lane;
+            const unsigned before = __ballot_sync(0xffffffffu, v[u] == o && j < i);
+            if (before) p = base + 32 * u + 31 - __clz(before);
+        }
+    }
+    const double he[3] = {s.ohe[3 * o], s.ohe[3 * o + 1], s.ohe[3 * o + 2]};
+    const double cu = lane < 6 ? s.cur_union[6 * o + lane] : 0.0;
+    const double* rt_old = p >= 0 ? mrt + 12 * static_cast<size_t>(p) : rt_new;
+    if (p >= 0 && lane >= 8 && lane < 16)
+#pragma unroll
+        for (int k = 0; k < 12; ++k) rtl[k] = rt_old[k];
+    const int nsph = s.osn[o];
+    const double r = s.osr[o];
+    double lo[3], hi[3], pt[3] = {0, 0, 0};
+    if (lane < 16) {
+        box_of(rtl, he, lane & 7, pt);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) lo[k] = hi[k] = pt[k];
+    } else {
+        const int sp = lane - 16;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = __longlong_as_double(0x7ff0000000000000ll);
+            hi[k] = __longlong_as_double(0xfff0000000000000ll);
+        }
+        if (sp < nsph) {
+            const double* l = s.osl + (static_cast<size_t>(o) * s.C + sp) * 3;
+            rggd::tf_apply(rtl, l[0], l[1], l[2], pt);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = sub(pt[k], r);
+                hi[k] = add(pt[k], r);
+            }
+        }
+    }
+    const int width = lane < 16 ? 8 : 16;
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double a = __shfl_xor_sync(0xffffffffu, lo[k], off);
+            const double c = __shfl_xor_sync(0xffffffffu, hi[k], off);
+            if (off < width) {
+                lo[k] = fmin(lo[k], a);
+                hi[k] = fmax(hi[k], c);
+            }
+        }
+    }
+    double bn[6], bo[6], bs[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        bn[k] = widen_lo(shfl(lo[k], 0)), bn[3 + k] = widen_hi(shfl(hi[k], 0));
+        bo[k] = widen_lo(shfl(lo[k], 8)), bo[3 + k] = widen_hi(shfl(hi[k], 8));
+        bs[k] = widen_lo(shfl(lo[k], 16)), bs[3 + k] = widen_hi(shfl(hi[k], 16));
+    }
+    double os[6];
+    if (p >= 0) {
+        double olo[3], ohi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            olo[k] = __longlong_as_double(0x7ff0000000000000ll);
+            ohi[k] = __longlong_as_double(0xfff0000000000000ll);
+        }
+        if (lane >= 16 && lane - 16 < nsph) {
+            const double* l = s.osl + (static_cast<size_t>(o) * s.C + (lane - 16)) * 3;
+            double q[3];
+            rggd::tf_apply(rt_old, l[0], l[1], l[2], q);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                olo[k] = sub(q[k], r);
+                ohi[k] = add(q[k], r);
+            }
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                olo[k] = fmin(olo[k], __shfl_xor_sync(0xffffffffu, olo[k], off));
+                ohi[k] = fmax(ohi[k], __shfl_xor_sync(0xffffffffu, ohi[k], off));
+            }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            os[k] = fmin(bo[k], widen_lo(olo[k]));
+            os[3 + k] = fmax(bo[3 + k], widen_hi(ohi[k]));
+        }
+    }
+    if (lane < 6) {
+        out[lane] = lane < 3 ? fmin(bn[lane], bs[lane]) : fmax(bn[lane], bs[lane]);
+        out[6 + lane] = p >= 0 ? os[lane] : cu;
+    }
+}
+
 // Identity pose for every obstacle: serialize() poses obstacles at their
 // canonical pose (batch_layout.cpp:117-136); they stay inactive (empty union).
 __global__ void init_obstacles_kernel(Store s) {
@@ -560,23 +673,35 @@ __device__ __forceinline__ void wait_event_boxes(const Batch& b) {
 // intersection of the cell's and the box's bin ranges (the cell's low bin rides in
 // its grid entry).
 constexpr int kScatterThreads = 256;
+constexpr int kScatterSelfBox = 512;  // batches below this many moves: bin_scatter_kernel<true>
 
+template <bool SELF_BOX>
 __global__ void __launch_bounds__(kScatterThreads) bin_scatter_kernel(Store s, Batch b) {
     // a plain PDL wait for the pose kernel: a thousand CTAs polling the pose warps' count
     // (Batch::evready) slowed those warps' own release atomics more than it saved
-    const unsigned long long tw = tl_start(b.tl);
-    pdl_wait();
+    // SELF_BOX (batches under kScatterSelfBox moves): no wait for the pose kernel; warp 0
+    // derives this event's binning boxes itself with the pose kernel's operations
+    // (binning_boxes_warp), and the grid waits for the pose kernel only before it exits, so
+    // the next kernels' waits still cover the pose kernel's outputs.  Larger batches wait
+    // and read the pose kernel's boxes (a thousand CTAs redoing the pose work cost more
+    // than the overlap saves).
+    if (!SELF_BOX) pdl_wait();
     pdl_trigger();
-    tl_stop(b.tl, 5, tw);
     const unsigned long long t0 = tl_start(b.tl);
     __shared__ int s_pre[kScatterThreads + 1];
     __shared__ int s_tot;
+    __shared__ double s_bx[12];
     const int tid = threadIdx.x;
     const int e = blockIdx.x;
-    const double* evb = b.evbox + 12 * static_cast<size_t>(e);
+    if (SELF_BOX) {
+        if (tid < 32) binning_boxes_warp(s, b, e, tid, s_bx);
+    } else if (tid < 12) {
+        s_bx[tid] = b.evbox[12 * static_cast<size_t>(e) + tid];
+    }
+    __syncthreads();
     double bx[12];
 #pragma unroll
-    for (int k = 0; k < 12; ++k) bx[k] = evb[k];
+    for (int k = 0; k < 12; ++k) bx[k] = s_bx[k];
     uint32_t* col = b.cmask + (e >> 5);
     const uint32_t bit = 1u << (e & 31);
     for (int h = 0; h < 2; ++h) {
@@ -650,6 +775,7 @@ __global__ void __launch_bounds__(kScatterThreads) bin_scatter_kernel(Store s, B
         }
     }
     tl_stop(b.tl, 9, t0);
+    if (SELF_BOX) pdl_wait();  // the pose kernel is complete before this grid is
 }
 
 constexpr int kCellWarps = 32;
@@ -2068,7 +2194,13 @@ cudaError_t launch_bin(const Store& s, const Batch& b, cudaStream_t st) {
     if (b.n <= kBinSmallMax && !no_small)
         return launch_pdl(bin_small_kernel, dim3((s.ncells + kBinSmallWarps - 1) / kBinSmallWarps),
                           dim3(32 * kBinSmallWarps), st, s, b);
-    cudaError_t e = launch_pdl(bin_scatter_kernel, dim3(b.n), dim3(kScatterThreads), st, s, b);  // a CTA per event
+    static const int self_box = [] {  // tests: RGG_SELF_BOX_MAX=0 takes the waiting variant at every size
+        const char* v = std::getenv("RGG_SELF_BOX_MAX");
+        return v ? std::atoi(v) : kScatterSelfBox;
+    }();
+    cudaError_t e = b.n < self_box  // a CTA per event
+                        ? launch_pdl(bin_scatter_kernel<true>, dim3(b.n), dim3(kScatterThreads), st, s, b)
+                        : launch_pdl(bin_scatter_kernel<false>, dim3(b.n), dim3(kScatterThreads), st, s, b);
     if (e != cudaSuccess) return e;
     return launch_pdl(bin_cells_kernel, dim3((s.ncells + kCellWarps - 1) / kCellWarps), dim3(32 * kCellWarps), st, s, b);
 }

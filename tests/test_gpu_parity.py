@@ -230,13 +230,16 @@ def test_recheck_queue_overflow(eng_mod, name, cap, monkeypatch):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", [{"RGG_EARLY_TOUCH_MIN": "1"}, {"RGG_NO_EARLY_BIN": "1"}, {"RGG_NO_SMALL_BIN": "1"},
-                                 {"RGG_NO_SINGLE": "1"}, {"RGG_WARP_TOUCH": "1"}, {"RGG_NO_PDL": "1"}])
+                                 {"RGG_NO_SINGLE": "1"}, {"RGG_WARP_TOUCH": "1"}, {"RGG_NO_PDL": "1"},
+                                 {"RGG_NO_SMALL_BIN": "1", "RGG_SELF_BOX_MAX": "0"}])
 def test_kernel_handoffs(env):
     """The split pipeline's in-kernel handoffs, forced on or off for every batch size
     (rgg_kernels.cu: bin on the pose warps' published boxes, touch on bin's published
     units; by default touch waits for the whole bin kernel below 256 moves; single moves
     through the batched pipeline instead of the single-move kernel; touch one warp per slice
-    instead of one CTA per cell chunk; plain stream order instead of programmatic launches)."""
+    instead of one CTA per cell chunk; plain stream order instead of programmatic launches;
+    the scatter binning at every batch size, waiting for the pose kernel's boxes instead of
+    deriving them itself as it does below 512 moves)."""
     import os
     import subprocess
     import sys
