@@ -6,7 +6,8 @@
 //                 event boxes (widened by 2^-40), SAT operands, Box32 filter line and the
 //                 fp32 sphere operands of every move.
 //   bin           bin_scatter_kernel (a CTA per event over a uniform grid of the cell
-//                 boxes, event bitmask per cell) + bin_cells_kernel (a warp per cell:
+//                 boxes, event bitmask per cell; below 512 moves it derives the event's
+//                 boxes itself, overlapping the pose kernel) + bin_cells_kernel (a warp per cell:
 //                 ordered lists by popcount / prefix scan, fixed capacity + overflow
 //                 pool, work units), or bin_small_kernel for <= 64 moves.  Replaces
 //                 SpatialGrid::build / candidates (proj/src/spatial_grid.cpp:50-135).
